@@ -1,0 +1,190 @@
+"""ctypes front-end of the fp64 CPU oracle (oracle/sta_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and the
+cpu_baseline / --impl reference legs of bench.py -- never by the product
+package.  Shares no code with paper_2511_11660_b200/.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "sta_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (-O2, strict IEEE: no -ffast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
+            os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "sta_oracle.h"))):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fno-fast-math",
+                               "-ffp-contract=off", "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+class _Design(C.Structure):
+    _fields_ = [
+        ("num_pins", C.c_uint32), ("pin_cap", C.c_void_p), ("pin_role", C.c_void_p),
+        ("num_nets", C.c_uint32), ("net_ptr", C.c_void_p), ("net_pins", C.c_void_p),
+        ("num_arcs", C.c_uint32), ("arc_from", C.c_void_p), ("arc_to", C.c_void_p),
+        ("arc_sense", C.c_void_p), ("arc_tab", C.c_void_p),
+        ("num_checks", C.c_uint32), ("chk_d", C.c_void_p), ("chk_ck", C.c_void_p),
+        ("chk_tab", C.c_void_p),
+        ("num_tables", C.c_uint32), ("tab_n1", C.c_void_p), ("tab_n2", C.c_void_p),
+        ("tab_off", C.c_void_p), ("tab_data", C.c_void_p),
+        ("rc_ptr", C.c_void_p), ("rc_parent", C.c_void_p), ("rc_node_pin", C.c_void_p),
+        ("rc_res", C.c_void_p), ("rc_cap", C.c_void_p),
+        ("period", C.c_double), ("clock_slew", C.c_double),
+        ("n_pi", C.c_uint32), ("pi_pin", C.c_void_p), ("pi_at", C.c_void_p),
+        ("pi_slew", C.c_void_p),
+        ("n_po", C.c_uint32), ("po_pin", C.c_void_p), ("po_out_max", C.c_void_p),
+        ("po_out_min", C.c_void_p), ("po_load", C.c_void_p),
+    ]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        _lib = C.CDLL(_LIB)
+        _lib.orc_lut.restype = C.c_double
+        _lib.orc_lut.argtypes = [C.c_uint32, C.c_uint32, C.c_void_p, C.c_double, C.c_double]
+        _lib.orc_levelize.restype = C.c_int
+        _lib.orc_levelize.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        _lib.orc_rc.restype = None
+        _lib.orc_rc.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        _lib.orc_update.restype = C.c_int
+        _lib.orc_update.argtypes = [C.c_void_p] * 5 + [C.c_void_p] * 4
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data if a is not None and a.size else None
+
+
+class _Marshal:
+    """Holds contiguous copies alive while the C call runs."""
+
+    def __init__(self, d, corner: int = 0):
+        keep = []
+
+        def arr(x, dt):
+            a = np.ascontiguousarray(np.asarray(x, dtype=dt))
+            keep.append(a)
+            return a
+
+        lib_c = d.libs[corner]
+        rc = d.rc[corner]
+        cons = d.cons
+        s = _Design()
+        s.num_pins = d.num_pins
+        s.pin_cap = _p(arr(d.pin_cap, np.float32))
+        s.pin_role = _p(arr(d.pin_role, np.uint8))
+        s.num_nets = d.num_nets
+        s.net_ptr = _p(arr(d.net_ptr, np.uint32))
+        s.net_pins = _p(arr(d.net_pins, np.uint32))
+        s.num_arcs = d.num_arcs
+        s.arc_from = _p(arr(d.arc_from, np.uint32))
+        s.arc_to = _p(arr(d.arc_to, np.uint32))
+        s.arc_sense = _p(arr(d.arc_sense, np.uint8))
+        s.arc_tab = _p(arr(d.arc_tab, np.uint32))
+        s.num_checks = d.num_checks
+        s.chk_d = _p(arr(d.chk_d, np.uint32))
+        s.chk_ck = _p(arr(d.chk_ck, np.uint32))
+        s.chk_tab = _p(arr(d.chk_tab, np.uint32))
+        s.num_tables = lib_c.num_tables
+        s.tab_n1 = _p(arr(lib_c.n1, np.uint8))
+        s.tab_n2 = _p(arr(lib_c.n2, np.uint8))
+        s.tab_off = _p(arr(lib_c.off, np.uint32))
+        s.tab_data = _p(arr(lib_c.data, np.float32))
+        s.rc_ptr = _p(arr(rc.rc_ptr, np.uint32))
+        s.rc_parent = _p(arr(rc.parent, np.int32))
+        s.rc_node_pin = _p(arr(rc.node_pin, np.uint32))
+        s.rc_res = _p(arr(rc.res, np.float32))
+        s.rc_cap = _p(arr(rc.cap, np.float32))
+        s.period = float(cons.period)
+        s.clock_slew = float(cons.clock_slew)
+        s.n_pi = int(cons.pi_pin.shape[0])
+        s.pi_pin = _p(arr(cons.pi_pin, np.uint32))
+        s.pi_at = _p(arr(cons.pi_at, np.float32))
+        s.pi_slew = _p(arr(cons.pi_slew, np.float32))
+        s.n_po = int(cons.po_pin.shape[0])
+        s.po_pin = _p(arr(cons.po_pin, np.uint32))
+        s.po_out_max = _p(arr(cons.po_out_max, np.float32))
+        s.po_out_min = _p(arr(cons.po_out_min, np.float32))
+        s.po_load = _p(arr(cons.po_load, np.float32))
+        self.s = s
+        self.keep = keep
+
+    @property
+    def ptr(self):
+        return C.addressof(self.s)
+
+
+def lut(n1, n2, tab, s, c) -> float:
+    t = np.ascontiguousarray(np.asarray(tab, np.float32))
+    return lib().orc_lut(int(n1), int(n2), t.ctypes.data, float(s), float(c))
+
+
+def levelize(d):
+    """-> (level[P] u32, perm[P] u32, num_levels) or raises on a cycle."""
+    m = _Marshal(d)
+    level = np.zeros(d.num_pins, np.uint32)
+    perm = np.zeros(d.num_pins, np.uint32)
+    nl = np.zeros(1, np.uint32)
+    st = lib().orc_levelize(m.ptr, _p(level), _p(perm), nl.ctypes.data)
+    if st == 1:
+        raise ValueError("combinational cycle")
+    if st:
+        raise MemoryError("oracle allocation failed")
+    return level, perm, int(nl[0])
+
+
+def rc(d, corner: int = 0):
+    """-> (load[N] f64, elm[P] f64)."""
+    m = _Marshal(d, corner)
+    load = np.zeros(max(d.num_nets, 1), np.float64)
+    elm = np.zeros(max(d.num_pins, 1), np.float64)
+    lib().orc_rc(m.ptr, _p(load), _p(elm))
+    return load[:d.num_nets], elm[:d.num_pins]
+
+
+def update(d, corner: int = 0, want_all: bool = True):
+    """Full update for one corner -> dict(at, slew, rat, slack [P,4] f64,
+    res[4] = (WNS_setup, TNS_setup, WNS_hold, TNS_hold), ep_pin, ep_ws)."""
+    m = _Marshal(d, corner)
+    P = d.num_pins
+    at = np.zeros((max(P, 1), 4))
+    slew = np.zeros((max(P, 1), 4)) if want_all else None
+    rat = np.zeros((max(P, 1), 4)) if want_all else None
+    slack = np.zeros((max(P, 1), 4)) if want_all else None
+    res = np.zeros(4)
+    n_ep_max = int(d.cons.po_pin.shape[0]) + d.num_checks + 1
+    ep_pin = np.zeros(n_ep_max, np.uint32)
+    ep_ws = np.zeros((n_ep_max, 2))
+    n_ep = np.zeros(1, np.uint32)
+    st = lib().orc_update(m.ptr, _p(at), _p(slew) if want_all else None,
+                          _p(rat) if want_all else None, _p(slack) if want_all else None,
+                          res.ctypes.data, _p(ep_pin), _p(ep_ws), n_ep.ctypes.data)
+    if st == 1:
+        raise ValueError("combinational cycle")
+    if st:
+        raise MemoryError("oracle allocation failed")
+    ne = int(n_ep[0])
+    out = dict(at=at[:P], res=res, ep_pin=ep_pin[:ne], ep_ws=ep_ws[:ne])
+    if want_all:
+        out.update(slew=slew[:P], rat=rat[:P], slack=slack[:P])
+    return out
+
+
+def update_all_corners(d):
+    """O9: per-corner results plus global WNS = min, TNS = sum over corners."""
+    per = [update(d, c) for c in range(d.num_corners)]
+    r = np.array([p["res"] for p in per])
+    glob = np.array([r[:, 0].min(), r[:, 1].sum(), r[:, 2].min(), r[:, 3].sum()])
+    return per, glob

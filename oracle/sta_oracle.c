@@ -1,0 +1,404 @@
+/*
+ * sta_oracle.c -- the CPU oracle (TEST INFRASTRUCTURE ONLY; see sta_oracle.h).
+ *
+ * Plain single-thread C, fp64 arithmetic, written step by step after
+ * SURVEY.md §8(c) O1-O9 with the conventions of SPEC.md:371-532.  No blocking,
+ * no fusion, no reordering: each step is a loop a reader can check against the
+ * cited passage.  Pinned by tests/test_oracle_*.py (hand examples, closed
+ * forms, brute force); see DESIGN.md §4 for the pin list.
+ */
+#include "sta_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define INF HUGE_VAL
+/* quantity index q = el*2 + rf with el: 0 early, 1 late; rf: 0 rise, 1 fall */
+#define Q(el, rf) ((el) * 2 + (rf))
+
+/* ---------------------------------------------------------------- O6: LUT */
+/* bilinear inside the grid, linear extrapolation from the
+ * boundary cell outside (tx, ty not clamped); 1-D tables interpolate on their
+ * single axis; a 1x1 table is a constant.  Segment: i = clamp(ub(x,s)-1, 0,
+ * n-2) (SURVEY.md §8(c) reading #4). */
+static uint32_t seg(const float* x, uint32_t n, double s) {
+  uint32_t ub = 0;                       /* upper_bound: first x[k] > s */
+  while (ub < n && (double)x[ub] <= s) ub++;
+  long i = (long)ub - 1;
+  if (i < 0) i = 0;
+  if (i > (long)n - 2) i = (long)n - 2;
+  return (uint32_t)i;
+}
+
+double orc_lut(uint32_t n1, uint32_t n2, const float* tab, double s, double c) {
+  const float* x = tab;
+  const float* y = tab + n1;
+  const float* v = tab + n1 + n2;       /* v[i*n2 + j] */
+  if (n1 == 1 && n2 == 1) return v[0];
+  if (n1 == 1) {
+    uint32_t j = seg(y, n2, c);
+    double ty = (c - y[j]) / ((double)y[j + 1] - y[j]);
+    return (1 - ty) * v[j] + ty * v[j + 1];
+  }
+  if (n2 == 1) {
+    uint32_t i = seg(x, n1, s);
+    double tx = (s - x[i]) / ((double)x[i + 1] - x[i]);
+    return (1 - tx) * v[i] + tx * v[i + 1];
+  }
+  uint32_t i = seg(x, n1, s), j = seg(y, n2, c);
+  double tx = (s - x[i]) / ((double)x[i + 1] - x[i]);
+  double ty = (c - y[j]) / ((double)y[j + 1] - y[j]);
+  double v00 = v[i * n2 + j], v10 = v[(i + 1) * n2 + j];
+  double v01 = v[i * n2 + j + 1], v11 = v[(i + 1) * n2 + j + 1];
+  return (1 - tx) * (1 - ty) * v00 + tx * (1 - ty) * v10 + (1 - tx) * ty * v01 + tx * ty * v11;
+}
+
+static double lut_id(const orc_design* d, uint32_t t, double s, double c) {
+  return orc_lut(d->tab_n1[t], d->tab_n2[t], d->tab_data + d->tab_off[t], s, c);
+}
+
+/* ---------------------------------------------------------------- O1: arcs */
+/* Net arcs: driver -> each sink, nets in order, sinks in order; then cell
+ * arcs in input order.  Check arcs are not edges
+ * (SPEC.md:223). */
+typedef struct {
+  uint32_t E, En;        /* total arcs, net arcs */
+  uint32_t* from;
+  uint32_t* to;
+  uint32_t* cell;        /* cell arc index for id >= En */
+  uint32_t *fi_ptr, *fi; /* fan-in CSR of arc ids (canonical order) */
+  uint32_t *fo_ptr, *fo; /* fan-out CSR */
+} arcs_t;
+
+static void free_arcs(arcs_t* g) {
+  free(g->from); free(g->to); free(g->cell);
+  free(g->fi_ptr); free(g->fi); free(g->fo_ptr); free(g->fo);
+}
+
+static int build_arcs(const orc_design* d, arcs_t* g) {
+  uint32_t P = d->num_pins;
+  uint32_t En = d->net_ptr[d->num_nets] - d->num_nets;
+  uint32_t E = En + d->num_arcs;
+  g->E = E; g->En = En;
+  g->from = malloc(sizeof(uint32_t) * (E + 1));
+  g->to = malloc(sizeof(uint32_t) * (E + 1));
+  g->cell = malloc(sizeof(uint32_t) * (E + 1));
+  g->fi_ptr = calloc(P + 1, sizeof(uint32_t));
+  g->fo_ptr = calloc(P + 1, sizeof(uint32_t));
+  g->fi = malloc(sizeof(uint32_t) * (E + 1));
+  g->fo = malloc(sizeof(uint32_t) * (E + 1));
+  if (!g->from || !g->to || !g->cell || !g->fi_ptr || !g->fo_ptr || !g->fi || !g->fo) return 2;
+  uint32_t k = 0;
+  for (uint32_t n = 0; n < d->num_nets; n++) {
+    uint32_t drv = d->net_pins[d->net_ptr[n]];
+    for (uint32_t j = d->net_ptr[n] + 1; j < d->net_ptr[n + 1]; j++) {
+      g->from[k] = drv; g->to[k] = d->net_pins[j]; g->cell[k] = 0; k++;
+    }
+  }
+  for (uint32_t a = 0; a < d->num_arcs; a++) {
+    g->from[k] = d->arc_from[a]; g->to[k] = d->arc_to[a]; g->cell[k] = a; k++;
+  }
+  for (uint32_t e = 0; e < E; e++) { g->fi_ptr[g->to[e] + 1]++; g->fo_ptr[g->from[e] + 1]++; }
+  for (uint32_t p = 0; p < P; p++) { g->fi_ptr[p + 1] += g->fi_ptr[p]; g->fo_ptr[p + 1] += g->fo_ptr[p]; }
+  uint32_t* fi_fill = malloc(sizeof(uint32_t) * (P + 1));
+  uint32_t* fo_fill = malloc(sizeof(uint32_t) * (P + 1));
+  if (!fi_fill || !fo_fill) { free(fi_fill); free(fo_fill); return 2; }
+  memcpy(fi_fill, g->fi_ptr, sizeof(uint32_t) * (P + 1));
+  memcpy(fo_fill, g->fo_ptr, sizeof(uint32_t) * (P + 1));
+  for (uint32_t e = 0; e < E; e++) {
+    g->fi[fi_fill[g->to[e]]++] = e;
+    g->fo[fo_fill[g->from[e]]++] = e;
+  }
+  free(fi_fill); free(fo_fill);
+  return 0;
+}
+
+/* ---------------------------------------------------------- O2: levelize */
+/* Kahn with a FIFO seeded by in-degree-0 pins in increasing id;
+ * level(v) = 0 without fan-in, else 1 + max level over fan-in.  `order`
+ * receives the pop order, itself a topological order. */
+static int kahn(const orc_design* d, const arcs_t* g, uint32_t* level, uint32_t* order) {
+  uint32_t P = d->num_pins;
+  uint32_t* indeg = malloc(sizeof(uint32_t) * (P + 1));
+  if (!indeg) return 2;
+  uint32_t head = 0, tail = 0;
+  for (uint32_t p = 0; p < P; p++) {
+    indeg[p] = g->fi_ptr[p + 1] - g->fi_ptr[p];
+    level[p] = 0;
+    if (indeg[p] == 0) order[tail++] = p;
+  }
+  while (head < tail) {
+    uint32_t u = order[head++];
+    for (uint32_t k = g->fo_ptr[u]; k < g->fo_ptr[u + 1]; k++) {
+      uint32_t v = g->to[g->fo[k]];
+      if (level[u] + 1 > level[v]) level[v] = level[u] + 1;
+      if (--indeg[v] == 0) order[tail++] = v;
+    }
+  }
+  free(indeg);
+  return tail == P ? 0 : 1;
+}
+
+int orc_levelize(const orc_design* d, uint32_t* level, uint32_t* perm, uint32_t* num_levels) {
+  arcs_t g; memset(&g, 0, sizeof g);
+  int st = build_arcs(d, &g);
+  uint32_t P = d->num_pins;
+  uint32_t* order = malloc(sizeof(uint32_t) * (P + 1));
+  if (st || !order) { free_arcs(&g); free(order); return 2; }
+  st = kahn(d, &g, level, order);
+  free(order);
+  free_arcs(&g);
+  if (st) return st;
+  uint32_t L = 0;
+  for (uint32_t p = 0; p < P; p++) if (level[p] + 1 > L) L = level[p] + 1;
+  *num_levels = L;
+  if (perm) { /* stable counting sort by level: pins of one level in id order */
+    uint32_t* start = calloc(L + 1, sizeof(uint32_t));
+    if (!start) return 2;
+    for (uint32_t p = 0; p < P; p++) start[level[p] + 1]++;
+    for (uint32_t l = 0; l < L; l++) start[l + 1] += start[l];
+    for (uint32_t p = 0; p < P; p++) perm[start[level[p]]++] = p;
+    free(start);
+  }
+  return 0;
+}
+
+/* --------------------------------------------------------------- O3: RC */
+/* Per net with RC nodes: node cap C_i = Cw_i + pin cap of
+ * the pin at node i (+ its PO load, reading R10); Cdown bottom-up
+ * (parent[i] < i); load = Cdown_0; elm_i = elm_parent + R_i * Cdown_i.
+ * Nets without RC nodes are lumped: load = sum of the net's pin caps (+ PO
+ * loads), every net-arc delay 0. */
+void orc_rc(const orc_design* d, double* load, double* elm) {
+  uint32_t P = d->num_pins;
+  double* po_ld = calloc(P + 1, sizeof(double));
+  for (uint32_t k = 0; k < d->n_po; k++) po_ld[d->po_pin[k]] += d->po_load[k];
+  for (uint32_t p = 0; p < P; p++) elm[p] = 0.0;
+  uint32_t maxn = 1;
+  for (uint32_t n = 0; n < d->num_nets; n++) {
+    uint32_t m = d->rc_ptr[n + 1] - d->rc_ptr[n];
+    if (m > maxn) maxn = m;
+  }
+  double* cd = malloc(sizeof(double) * maxn);
+  double* el = malloc(sizeof(double) * maxn);
+  for (uint32_t n = 0; n < d->num_nets; n++) {
+    uint32_t b = d->rc_ptr[n], m = d->rc_ptr[n + 1] - b;
+    if (m == 0) {
+      double c = 0;
+      for (uint32_t j = d->net_ptr[n]; j < d->net_ptr[n + 1]; j++) {
+        uint32_t p = d->net_pins[j];
+        c += d->pin_cap[p] + po_ld[p];
+      }
+      load[n] = c;
+      continue;
+    }
+    for (uint32_t i = 0; i < m; i++) {
+      uint32_t p = d->rc_node_pin[b + i];
+      cd[i] = d->rc_cap[b + i] + (p != ORC_NO_PIN ? d->pin_cap[p] + po_ld[p] : 0.0);
+    }
+    for (uint32_t i = m - 1; i >= 1; i--) cd[d->rc_parent[b + i]] += cd[i];
+    load[n] = cd[0];
+    el[0] = 0.0;
+    for (uint32_t i = 1; i < m; i++) el[i] = el[d->rc_parent[b + i]] + (double)d->rc_res[b + i] * cd[i];
+    for (uint32_t i = 1; i < m; i++) {
+      uint32_t p = d->rc_node_pin[b + i];
+      if (p != ORC_NO_PIN) elm[p] = el[i];
+    }
+  }
+  free(cd); free(el); free(po_ld);
+}
+
+/* ------------------------------------------------------- sense pairs (O5) */
+/* SPEC.md:383 and SURVEY.md §8(c) O5: which (input edge -> output edge) pairs
+ * an arc of a given sense propagates. */
+static int sense_allows(uint8_t sense, int irf, int orf) {
+  switch (sense) {
+    case ORC_POS: return irf == orf;
+    case ORC_NEG: return irf != orf;
+    case ORC_NON: return 1;
+    case ORC_RISE_EDGE: return irf == 0;
+    case ORC_FALL_EDGE: return irf == 1;
+  }
+  return 0;
+}
+
+/* --------------------------------------------------------- O4-O8: update */
+int orc_update(const orc_design* d, double* at, double* slew, double* rat, double* slack,
+               double res[4], uint32_t* ep_pin, double* ep_ws, uint32_t* n_ep_out) {
+  const uint32_t P = d->num_pins;
+  const double LN9 = log(9.0);
+  arcs_t g; memset(&g, 0, sizeof g);
+  if (build_arcs(d, &g)) { free_arcs(&g); return 2; }
+  uint32_t* level = malloc(sizeof(uint32_t) * (P + 1));
+  uint32_t* order = malloc(sizeof(uint32_t) * (P + 1));
+  double* load = malloc(sizeof(double) * (d->num_nets + 1));
+  double* elm = malloc(sizeof(double) * (P + 1));
+  double* drv_load = calloc(P + 1, sizeof(double));  /* load seen by a net's driver pin */
+  double* dly = malloc(sizeof(double) * (8 * (size_t)d->num_arcs + 1)); /* d_el(a, irf->orf) */
+  double* own_slew = slew ? NULL : malloc(sizeof(double) * 4 * (size_t)(P + 1));
+  double* own_rat = rat ? NULL : malloc(sizeof(double) * 4 * (size_t)(P + 1));
+  double* own_slack = slack ? NULL : malloc(sizeof(double) * 4 * (size_t)(P + 1));
+  uint8_t* is_ep = calloc(P + 1, 1);
+  int st = 0;
+  if (!slew) slew = own_slew;
+  if (!rat) rat = own_rat;
+  if (!slack) slack = own_slack;
+  if (!level || !order || !load || !elm || !drv_load || !dly || !slew || !rat || !slack || !is_ep) {
+    st = 2; goto done;
+  }
+  if (kahn(d, &g, level, order)) { st = 1; goto done; }
+
+  /* O3 */
+  orc_rc(d, load, elm);
+  for (uint32_t n = 0; n < d->num_nets; n++) drv_load[d->net_pins[d->net_ptr[n]]] = load[n];
+
+  /* O4 seeds: everything undefined, then PIs and ideal-clock CK pins. */
+  for (uint32_t p = 0; p < P; p++) {
+    for (int rf = 0; rf < 2; rf++) {
+      at[4 * p + Q(0, rf)] = INF;   slew[4 * p + Q(0, rf)] = INF;
+      at[4 * p + Q(1, rf)] = -INF;  slew[4 * p + Q(1, rf)] = -INF;
+    }
+  }
+  for (uint32_t k = 0; k < d->n_pi; k++) {
+    uint32_t p = d->pi_pin[k];
+    if (g.fi_ptr[p + 1] != g.fi_ptr[p]) continue;
+    for (int q = 0; q < 4; q++) { at[4 * p + q] = d->pi_at[4 * k + q]; slew[4 * p + q] = d->pi_slew[4 * k + q]; }
+  }
+  for (uint32_t p = 0; p < P; p++) {
+    if (d->pin_role[p] != ORC_FF_CK || g.fi_ptr[p + 1] != g.fi_ptr[p]) continue;
+    /* ideal clock, rising edge at 0, waveform (0, T/2) */
+    at[4 * p + Q(0, 0)] = 0.0; at[4 * p + Q(0, 1)] = d->period / 2;
+    at[4 * p + Q(1, 0)] = 0.0; at[4 * p + Q(1, 1)] = d->period / 2;
+    for (int q = 0; q < 4; q++) slew[4 * p + q] = d->clock_slew;
+  }
+
+  /* O5 forward in topological order. */
+  for (uint32_t k = 0; k < P; k++) {
+    uint32_t v = order[k];
+    if (g.fi_ptr[v + 1] == g.fi_ptr[v]) continue;
+    for (uint32_t x = g.fi_ptr[v]; x < g.fi_ptr[v + 1]; x++) {
+      uint32_t e = g.fi[x], u = g.from[e];
+      for (int el = 0; el < 2; el++) {
+        for (int irf = 0; irf < 2; irf++) {
+          double a_in = at[4 * u + Q(el, irf)];
+          if (!isfinite(a_in)) continue;
+          double s_in = slew[4 * u + Q(el, irf)];
+          for (int orf = 0; orf < 2; orf++) {
+            double ca, cs;
+            if (e < g.En) {                /* net arc: positive unate, Elmore */
+              if (irf != orf) continue;
+              double imp = LN9 * elm[v];   /* SPEC.md:418 PERI */
+              ca = a_in + elm[v];
+              cs = sqrt(s_in * s_in + imp * imp);
+            } else {                       /* cell arc: NLDM */
+              uint32_t a = g.cell[e];
+              if (!sense_allows(d->arc_sense[a], irf, orf)) continue;
+              uint32_t tb = d->arc_tab[a];
+              double ld = drv_load[v];
+              double dd = lut_id(d, tb + (uint32_t)orf, s_in, ld);        /* cell_rise/fall */
+              double ss = lut_id(d, tb + 2 + (uint32_t)orf, s_in, ld);    /* rise/fall_tr */
+              if (dd < 0) dd = 0;
+              if (ss < 0) ss = 0;
+              dly[8 * (size_t)a + 4 * el + 2 * irf + orf] = dd;
+              ca = a_in + dd;
+              cs = ss;
+            }
+            /* merge: early takes min, late takes max, AT and slew independently */
+            double* pa = &at[4 * v + Q(el, orf)];
+            double* ps = &slew[4 * v + Q(el, orf)];
+            if (el == 0) { if (ca < *pa) *pa = ca; if (cs < *ps) *ps = cs; }
+            else         { if (ca > *pa) *pa = ca; if (cs > *ps) *ps = cs; }
+          }
+        }
+      }
+    }
+  }
+
+  /* O7 endpoint seeds then backward in reverse order. */
+  for (uint32_t p = 0; p < P; p++) {
+    for (int rf = 0; rf < 2; rf++) { rat[4 * p + Q(0, rf)] = -INF; rat[4 * p + Q(1, rf)] = INF; }
+  }
+  for (uint32_t k = 0; k < d->n_po; k++) {
+    uint32_t p = d->po_pin[k];
+    is_ep[p] = 1;
+    for (int rf = 0; rf < 2; rf++) {
+      double rl = d->period - d->po_out_max[2 * k + rf];
+      double re = -(double)d->po_out_min[2 * k + rf];
+      if (rl < rat[4 * p + Q(1, rf)]) rat[4 * p + Q(1, rf)] = rl;
+      if (re > rat[4 * p + Q(0, rf)]) rat[4 * p + Q(0, rf)] = re;
+    }
+  }
+  for (uint32_t c = 0; c < d->num_checks; c++) {
+    uint32_t p = d->chk_d[c], tb = d->chk_tab[c];
+    is_ep[p] = 1;
+    for (int rf = 0; rf < 2; rf++) {
+      if (isfinite(at[4 * p + Q(1, rf)])) {   /* setup: index_1 data slew, index_2 clock slew */
+        double rl = d->period - lut_id(d, tb + (uint32_t)rf, slew[4 * p + Q(1, rf)], d->clock_slew);
+        if (rl < rat[4 * p + Q(1, rf)]) rat[4 * p + Q(1, rf)] = rl;
+      }
+      if (isfinite(at[4 * p + Q(0, rf)])) {   /* hold */
+        double re = lut_id(d, tb + 2 + (uint32_t)rf, slew[4 * p + Q(0, rf)], d->clock_slew);
+        if (re > rat[4 * p + Q(0, rf)]) rat[4 * p + Q(0, rf)] = re;
+      }
+    }
+  }
+  for (uint32_t k = P; k-- > 0;) {
+    uint32_t u = order[k];
+    for (uint32_t x = g.fo_ptr[u]; x < g.fo_ptr[u + 1]; x++) {
+      uint32_t e = g.fo[x], v = g.to[e];
+      for (int el = 0; el < 2; el++) {
+        for (int irf = 0; irf < 2; irf++) {
+          if (!isfinite(at[4 * u + Q(el, irf)])) continue;   /* only arcs O5 used */
+          for (int orf = 0; orf < 2; orf++) {
+            double dd;
+            if (e < g.En) { if (irf != orf) continue; dd = elm[v]; }
+            else {
+              uint32_t a = g.cell[e];
+              if (!sense_allows(d->arc_sense[a], irf, orf)) continue;
+              dd = dly[8 * (size_t)a + 4 * el + 2 * irf + orf];
+            }
+            double cand = rat[4 * v + Q(el, orf)] - dd;
+            double* pr = &rat[4 * u + Q(el, irf)];
+            if (el == 1) { if (cand < *pr) *pr = cand; }   /* late: min */
+            else         { if (cand > *pr) *pr = cand; }   /* early: max */
+          }
+        }
+      }
+    }
+  }
+
+  /* O8 slack, WNS, TNS */
+  for (uint32_t p = 0; p < P; p++) {
+    for (int rf = 0; rf < 2; rf++) {
+      double al = at[4 * p + Q(1, rf)], rl = rat[4 * p + Q(1, rf)];
+      double ae = at[4 * p + Q(0, rf)], re = rat[4 * p + Q(0, rf)];
+      slack[4 * p + Q(1, rf)] = (isfinite(al) && isfinite(rl)) ? rl - al : INF;
+      slack[4 * p + Q(0, rf)] = (isfinite(ae) && isfinite(re)) ? ae - re : INF;
+    }
+  }
+  {
+    double wns_s = INF, tns_s = 0.0, wns_h = INF, tns_h = 0.0;
+    uint32_t ne = 0;
+    for (uint32_t p = 0; p < P; p++) {
+      if (!is_ep[p]) continue;
+      double ws = slack[4 * p + Q(1, 0)] < slack[4 * p + Q(1, 1)] ? slack[4 * p + Q(1, 0)] : slack[4 * p + Q(1, 1)];
+      double wh = slack[4 * p + Q(0, 0)] < slack[4 * p + Q(0, 1)] ? slack[4 * p + Q(0, 0)] : slack[4 * p + Q(0, 1)];
+      if (ws < wns_s) wns_s = ws;
+      if (wh < wns_h) wns_h = wh;
+      if (ws < 0) tns_s += ws;
+      if (wh < 0) tns_h += wh;
+      if (ep_pin) ep_pin[ne] = p;
+      if (ep_ws) { ep_ws[2 * ne] = ws; ep_ws[2 * ne + 1] = wh; }
+      ne++;
+    }
+    res[0] = wns_s; res[1] = tns_s; res[2] = wns_h; res[3] = tns_h;
+    if (n_ep_out) *n_ep_out = ne;
+  }
+
+done:
+  free_arcs(&g);
+  free(level); free(order); free(load); free(elm); free(drv_load); free(dly);
+  free(own_slew); free(own_rat); free(own_slack); free(is_ep);
+  return st;
+}

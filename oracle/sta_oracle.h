@@ -1,0 +1,97 @@
+/*
+ * sta_oracle.h -- plain, slow, single-thread fp64 CPU oracle of one full
+ * graph-based STA timing update (HeteroSTA, arxiv 2511.11660).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * It shares no code, header, table or helper with the CUDA path
+ * (paper_2511_11660_b200/csrc, include/sta.h).
+ *
+ * What it computes follows SURVEY.md §8(c) steps O1-O9 (textbook max/min-plus
+ * STA; the paper names the reports -- "WNS/TNS, pin slacks", PAPER.md:187 --
+ * but not the formulas, which come from SPEC.md:371-532).  Every readings the
+ * paper leaves open is listed in DESIGN.md §2.
+ *
+ * Layout of per-pin quantities: double[P][4] in (early_rise, early_fall,
+ * late_rise, late_fall) order, indexed by the caller's pin id.
+ */
+#ifndef STA_ORACLE_H
+#define STA_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { ORC_POS = 0, ORC_NEG = 1, ORC_NON = 2, ORC_RISE_EDGE = 3, ORC_FALL_EDGE = 4 };
+enum { ORC_INTERNAL = 0, ORC_PI = 1, ORC_PO = 2, ORC_FF_CK = 3, ORC_FF_D = 4 };
+#define ORC_NO_PIN 0xFFFFFFFFu
+
+typedef struct {
+  /* netlist */
+  uint32_t num_pins;
+  const float* pin_cap;      /* [P] fF */
+  const uint8_t* pin_role;   /* [P] */
+  uint32_t num_nets;
+  const uint32_t* net_ptr;   /* [N+1] */
+  const uint32_t* net_pins;  /* driver first */
+  uint32_t num_arcs;
+  const uint32_t* arc_from;
+  const uint32_t* arc_to;
+  const uint8_t* arc_sense;
+  const uint32_t* arc_tab;   /* base of cell_rise, cell_fall, rise_tr, fall_tr */
+  uint32_t num_checks;
+  const uint32_t* chk_d;
+  const uint32_t* chk_ck;
+  const uint32_t* chk_tab;   /* base of setup_r, setup_f, hold_r, hold_f */
+  /* one corner's NLDM table pool */
+  uint32_t num_tables;
+  const uint8_t* tab_n1;
+  const uint8_t* tab_n2;
+  const uint32_t* tab_off;
+  const float* tab_data;
+  /* one corner's RC trees */
+  const uint32_t* rc_ptr;    /* [N+1] */
+  const int32_t* rc_parent;  /* local parent, -1 at node 0 */
+  const uint32_t* rc_node_pin;
+  const float* rc_res;       /* kOhm, edge parent->i */
+  const float* rc_cap;       /* fF, wire cap at node i */
+  /* constraints: one ideal clock */
+  double period;
+  double clock_slew;
+  uint32_t n_pi;
+  const uint32_t* pi_pin;
+  const float* pi_at;        /* [n_pi][4] */
+  const float* pi_slew;      /* [n_pi][4] */
+  uint32_t n_po;
+  const uint32_t* po_pin;
+  const float* po_out_max;   /* [n_po][2] rise, fall */
+  const float* po_out_min;   /* [n_po][2] */
+  const float* po_load;      /* [n_po] fF */
+} orc_design;
+
+/* O6: NLDM bilinear lookup, fp64.  `tab` points at
+ * index_1[n1], index_2[n2], values[n1][n2]. */
+double orc_lut(uint32_t n1, uint32_t n2, const float* tab, double s, double c);
+
+/* O2: Kahn levelization over net + cell arcs.
+ * level[P], perm[P] (stable sort by (level, pin id)).  Returns 0, or 1 on a
+ * combinational cycle. */
+int orc_levelize(const orc_design* d, uint32_t* level, uint32_t* perm, uint32_t* num_levels);
+
+/* O3: per-net Elmore.  load[N] = total net cap (fF),
+ * elm[P] = Elmore delay of the net arc into each sink pin (0 for non-sinks). */
+void orc_rc(const orc_design* d, double* load, double* elm);
+
+/* O1-O8: full update.  at/slew/rat/slack: double[P][4] (may be NULL except
+ * at); res[4] = {WNS_setup, TNS_setup, WNS_hold, TNS_hold};
+ * ep_pin/ep_ws (optional, [n_ep] and [n_ep][2]) receive the endpoints in
+ * increasing pin id with their worst setup/hold slack.  Returns 0, 1 on a
+ * cycle, 2 on allocation failure.  *n_ep receives the endpoint count. */
+int orc_update(const orc_design* d, double* at, double* slew, double* rat, double* slack,
+               double res[4], uint32_t* ep_pin, double* ep_ws, uint32_t* n_ep);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,33 @@
+#!/usr/bin/env bash
+# Plausible-mistake check of the oracle's pins: apply one
+# mutation at a time to oracle/sta_oracle.c and require the CPU suite to fail.
+set -u
+cd "$(dirname "$0")/.."
+cp oracle/sta_oracle.c /tmp/orc_backup.c
+trap 'cp /tmp/orc_backup.c oracle/sta_oracle.c; rm -f oracle/liboracle.so' EXIT
+mut() {
+  python - "$1" "$2" <<'PY'
+import sys
+s = open('/tmp/orc_backup.c').read(); a, b = sys.argv[1], sys.argv[2]
+assert a in s, a
+open('oracle/sta_oracle.c', 'w').write(s.replace(a, b, 1))
+PY
+  rm -f oracle/liboracle.so
+  if timeout 600 python -m pytest tests/test_oracle_lut_rc.py tests/test_oracle_propagation.py -q -x >/dev/null 2>&1; then
+    echo "NOT CAUGHT: $1"; return 1
+  else echo "caught: $1"; fi
+}
+mut 'case ORC_NEG: return irf != orf;' 'case ORC_NEG: return irf == orf;'
+mut 'cs = sqrt(s_in * s_in + imp * imp);' 'cs = sqrt(s_in * s_in + elm[v] * elm[v]);'
+mut 'el[i] = el[d->rc_parent[b + i]] + (double)d->rc_res[b + i] * cd[i];' 'el[i] = el[d->rc_parent[b + i]] + (double)d->rc_res[b + i] * d->rc_cap[b+i];'
+mut 'case ORC_FALL_EDGE: return irf == 1;' 'case ORC_FALL_EDGE: return irf == 0;'
+mut 'double rl = d->period - lut_id(d, tb + (uint32_t)rf,' 'double rl = d->period - lut_id(d, tb + 2 + (uint32_t)rf,'
+mut 'double re = -(double)d->po_out_min[2 * k + rf];' 'double re = (double)d->po_out_min[2 * k + rf];'
+mut 'double dd = lut_id(d, tb + (uint32_t)orf, s_in, ld);' 'double dd = lut_id(d, tb + (uint32_t)orf, ld, s_in);'
+mut 'return (1 - tx) * (1 - ty) * v00 + tx * (1 - ty) * v10' 'return (1 - tx) * (1 - ty) * v00 + tx * (1 - ty) * v01'
+mut 'if (ws < 0) tns_s += ws;' 'if (ws < 0) tns_s += wh;'
+mut 'at[4 * p + Q(0, 1)] = d->period / 2;' 'at[4 * p + Q(0, 1)] = d->period;'
+mut 'if (!isfinite(at[4 * u + Q(el, irf)])) continue;   /* only arcs O5 used */' ''
+mut 'if (level[u] + 1 > level[v]) level[v] = level[u] + 1;' 'if (level[u] > level[v]) level[v] = level[u] + 1;'
+mut 'if (dd < 0) dd = 0;' ''
+mut 'if (ss < 0) ss = 0;' ''

@@ -1,0 +1,236 @@
+"""Independent brute-force references used to PIN the oracle (tests only).
+
+Nothing here calls oracle/ or the CUDA path.  Each routine computes a
+quantity from its plain definition by exhaustive enumeration on tiny inputs:
+
+* elmore_bruteforce: SPEC.md:434 -- Elmore(sink) = sum_k C_k * R(path(root,k)
+  intersect path(root,sink)), the shared-path double loop.
+* longest_path_levels: SPEC.md:257/267 -- level = length of the longest path
+  from any source, by enumerating every path.
+* path_enumeration_timing: SPEC.md:539/688 -- with frozen (slew-independent)
+  delays, AT_L = max and AT_E = min over enumerated source->v paths with
+  rise/fall tracking; RAT by enumerating v->endpoint paths.
+"""
+from __future__ import annotations
+
+import math
+from collections import defaultdict
+
+import numpy as np
+
+from synth.design import (NO_PIN, ROLE_FF_CK, SENSE_POS, SENSE_NEG, SENSE_NON,
+                          SENSE_RISE_EDGE, SENSE_FALL_EDGE, Library)
+
+INF = math.inf
+
+
+def elmore_bruteforce(parent, R, C):
+    """parent[i] (local, -1 root), R[i] edge parent->i, C[i] node cap (total)."""
+    n = len(parent)
+
+    def path_edges(i):
+        e = set()
+        while i > 0:
+            e.add(i)
+            i = parent[i]
+        return e
+
+    paths = [path_edges(i) for i in range(n)]
+    out = []
+    for s in range(n):
+        tot = 0.0
+        for k in range(n):
+            shared = paths[s] & paths[k]
+            tot += C[k] * sum(R[j] for j in shared)
+        out.append(tot)
+    return out
+
+
+def _fanin_lists(d):
+    """Explicit arc list: (u, v, kind, sense, tab) with kind 'net'/'cell'."""
+    arcs = []
+    for n in range(d.num_nets):
+        b, e = int(d.net_ptr[n]), int(d.net_ptr[n + 1])
+        drv = int(d.net_pins[b])
+        for j in range(b + 1, e):
+            arcs.append((drv, int(d.net_pins[j]), "net", SENSE_POS, None))
+    for a in range(d.num_arcs):
+        arcs.append((int(d.arc_from[a]), int(d.arc_to[a]), "cell", int(d.arc_sense[a]),
+                     int(d.arc_tab[a])))
+    return arcs
+
+
+def longest_path_levels(d):
+    arcs = _fanin_lists(d)
+    succ = defaultdict(list)
+    indeg = np.zeros(d.num_pins, int)
+    for u, v, *_ in arcs:
+        succ[u].append(v)
+        indeg[v] += 1
+    level = np.zeros(d.num_pins, int)
+
+    def walk(u, length):      # enumerate every path
+        if length > level[u]:
+            level[u] = length
+        for v in succ[u]:
+            walk(v, length + 1)
+
+    for s in range(d.num_pins):
+        if indeg[s] == 0:
+            walk(s, 0)
+    return level
+
+
+def _pairs(sense):
+    return {SENSE_POS: [(0, 0), (1, 1)], SENSE_NEG: [(0, 1), (1, 0)],
+            SENSE_NON: [(0, 0), (0, 1), (1, 0), (1, 1)],
+            SENSE_RISE_EDGE: [(0, 0), (0, 1)], SENSE_FALL_EDGE: [(1, 0), (1, 1)]}[sense]
+
+
+def const_value(lib: Library, t: int) -> float:
+    _, _, v = lib.table(t)
+    assert v.size == 1
+    return float(v.reshape(-1)[0])
+
+
+def path_enumeration_timing(d, elm_of_pin):
+    """Frozen-delay brute force.  The library must hold 1x1 (constant) tables so
+    that every arc delay is independent of slew and load.  elm_of_pin[p] is the
+    net-arc delay into sink p (from elmore_bruteforce).  Returns at, rat,
+    slack [P][4] (E_r, E_f, L_r, L_f) and res (WNS_s, TNS_s, WNS_h, TNS_h)."""
+    lib = d.libs[0]
+    cons = d.cons
+    T = float(cons.period)
+    arcs = _fanin_lists(d)
+    P = d.num_pins
+    succ = defaultdict(list)
+    indeg = np.zeros(P, int)
+    for (u, v, kind, sense, tab) in arcs:
+        if kind == "net":
+            dl = {(0, 0): elm_of_pin[v], (1, 1): elm_of_pin[v]}
+        else:
+            dl = {(i, o): max(0.0, const_value(lib, tab + o)) for (i, o) in _pairs(sense)}
+        succ[u].append((v, dl))
+        indeg[v] += 1
+
+    # source arrival seeds
+    seed_at = {}
+    for k in range(cons.pi_pin.size):
+        p = int(cons.pi_pin[k])
+        if indeg[p] == 0:
+            seed_at[p] = [float(x) for x in cons.pi_at[k]]
+    for p in range(P):
+        if int(d.pin_role[p]) == ROLE_FF_CK and indeg[p] == 0:
+            seed_at[p] = [0.0, T / 2, 0.0, T / 2]
+
+    at = np.empty((P, 4))
+    at[:, 0:2] = INF
+    at[:, 2:4] = -INF
+
+    def fwd(v, orf, acc_e, acc_l):
+        at[v, orf] = min(at[v, orf], acc_e)
+        at[v, 2 + orf] = max(at[v, 2 + orf], acc_l)
+        for (w, dl) in succ[v]:
+            for (i, o), x in dl.items():
+                if i == orf:
+                    fwd(w, o, acc_e + x, acc_l + x)
+
+    for s, a in seed_at.items():
+        for rf in (0, 1):
+            # early and late walk the same paths with the same frozen delays
+            fwd(s, rf, a[rf], a[2 + rf])
+
+    # endpoint seeds
+    seed_l = defaultdict(lambda: [INF, INF])
+    seed_e = defaultdict(lambda: [-INF, -INF])
+    for k in range(cons.po_pin.size):
+        p = int(cons.po_pin[k])
+        for rf in (0, 1):
+            seed_l[p][rf] = min(seed_l[p][rf], T - float(cons.po_out_max[k, rf]))
+            seed_e[p][rf] = max(seed_e[p][rf], -float(cons.po_out_min[k, rf]))
+    for c in range(d.num_checks):
+        p, tb = int(d.chk_d[c]), int(d.chk_tab[c])
+        for rf in (0, 1):
+            if math.isfinite(at[p, 2 + rf]):
+                seed_l[p][rf] = min(seed_l[p][rf], T - const_value(lib, tb + rf))
+            if math.isfinite(at[p, rf]):
+                seed_e[p][rf] = max(seed_e[p][rf], const_value(lib, tb + 2 + rf))
+    endpoints = sorted(set(seed_l) | set(seed_e))
+
+    rat = np.empty((P, 4))
+    rat[:, 0:2] = -INF
+    rat[:, 2:4] = INF
+
+    def bwd(u, irf):
+        """all (sum of delays, endpoint, orf) reachable from (u, irf)."""
+        out = []
+
+        def walk(v, rf, acc):
+            if v in seed_l or v in seed_e:
+                out.append((acc, v, rf))
+            for (w, dl) in succ[v]:
+                for (i, o), x in dl.items():
+                    if i == rf:
+                        walk(w, o, acc + x)
+        walk(u, irf, 0.0)
+        return out
+
+    def bwd_strict(u, irf):
+        """(sum, endpoint, orf) over paths with at least one arc."""
+        out = []
+        for (w, dl) in succ[u]:
+            for (i, o), x in dl.items():
+                if i == irf:
+                    out.extend((acc + x, e, rf) for acc, e, rf in bwd(w, o))
+        return out
+
+    for u in range(P):
+        for irf in (0, 1):
+            # the pin's own seed (PO seeds are unconditional; D-pin seeds were
+            # only created where the data arrival is defined) ...
+            if u in seed_l:
+                rat[u, 2 + irf] = seed_l[u][irf]
+            if u in seed_e:
+                rat[u, irf] = seed_e[u][irf]
+            # ... and every path of length >= 1 to an endpoint, counted only
+            # when the pin's arrival of that edge is defined
+            reach = bwd_strict(u, irf)
+            if math.isfinite(at[u, 2 + irf]):
+                for acc, e, orf in reach:
+                    rat[u, 2 + irf] = min(rat[u, 2 + irf], seed_l[e][orf] - acc)
+            if math.isfinite(at[u, irf]):
+                for acc, e, orf in reach:
+                    rat[u, irf] = max(rat[u, irf], seed_e[e][orf] - acc)
+
+    slack = np.full((P, 4), INF)
+    for p in range(P):
+        for rf in (0, 1):
+            if math.isfinite(at[p, 2 + rf]) and math.isfinite(rat[p, 2 + rf]):
+                slack[p, 2 + rf] = rat[p, 2 + rf] - at[p, 2 + rf]
+            if math.isfinite(at[p, rf]) and math.isfinite(rat[p, rf]):
+                slack[p, rf] = at[p, rf] - rat[p, rf]
+    ws = [min(slack[e, 2], slack[e, 3]) for e in endpoints]
+    wh = [min(slack[e, 0], slack[e, 1]) for e in endpoints]
+    res = (min(ws, default=INF), sum(min(0.0, x) for x in ws),
+           min(wh, default=INF), sum(min(0.0, x) for x in wh))
+    return at, rat, slack, res
+
+
+def constant_library_like(lib: Library, rng, lo=1.0, hi=10.0, chk=None) -> Library:
+    """Replace every table of `lib` by a random 1x1 constant table."""
+    tables = []
+    for t in range(lib.num_tables):
+        tables.append(([0.0], [0.0], [[float(np.round(rng.uniform(lo, hi), 3))]]))
+    return Library.from_tables(tables)
+
+
+def design_node_caps(d, corner=0):
+    """Total node capacitance (wire + pin + PO load) per RC node, float64."""
+    rc = d.rc[corner]
+    po_ld = np.zeros(d.num_pins)
+    for k in range(d.cons.po_pin.size):
+        po_ld[int(d.cons.po_pin[k])] += float(d.cons.po_load[k])
+    caps = rc.cap.astype(np.float64).copy()
+    has = rc.node_pin != NO_PIN
+    caps[has] += d.pin_cap[rc.node_pin[has]].astype(np.float64) + po_ld[rc.node_pin[has]]
+    return caps
