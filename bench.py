@@ -1,0 +1,325 @@
+#!/usr/bin/env python
+"""Benchmark of one full graph-based STA timing update on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Workload (BASELINE.json configs[2], the config its metric is quoted on):
+superblue-shaped synthetic netlist, ~10.4M pins, 151 pin levels, 32
+high-fan-out nets, NLDM LIB-SYN tables, random RC trees.  One
+step = one full update a1-a5 (Elmore RC + loads, forward AT/slew, endpoint
+seeds, backward RAT, per-pin slack, WNS/TNS) of one corner per GPU; with N
+GPUs (torchrun) every rank times its own corner and the per-corner WNS/TNS
+rows are combined with one NCCL all_reduce per step (weak scaling).
+
+`--impl reference` times the fp64 CPU oracle (the reference arm of this
+tier) on a bounded sample of the same recipe, on rank 0's host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "pins/s and ms per full STA update (10M-pin DAG), % HBM peak; 1/2/4/8-GPU corners"
+CONFIG = "c3_superblue"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=CONFIG)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="skip e2e/profile/cpu legs (ncu runs)")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def corner_design(name, corner):
+    """The config's design with corner `corner` of the nominal corner recipe."""
+    import synth
+    d = synth.config_design(name, corners=1)
+    if corner:
+        ls, rs, cs = synth.corner_scales(corner, "nominal")
+        d.libs = [d.libs[0].scaled(ls)]
+        d.rc = [d.rc[0].scaled(rs, cs)]
+    return d
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def algorithmic_bytes(d, info):
+    """Unique bytes each phase must touch per update: fp32/u32
+    elements counted once per pass."""
+    P, NP, NS = info["num_pins"], info["num_pull_pins"], info["num_sink_pins"]
+    E = info["num_cell_arcs"]
+    N = info["num_nets"]
+    n_rc = int(d.rc[0].parent.shape[0])
+    n_ep = info["num_endpoints"]
+    rc = 20 * n_rc + 16 * N + 4 * NS            # parent,sink,scap,R,Cw; net tables; elm
+    fwd = (4 * NP + 12 * E + 4 * NS               # fan-in CSR + sink->driver
+           + 32 * NP                              # source records (drivers / pull sources)
+           + 4 * NS + 4 * NP                      # elm, load
+           + 32 * P)                              # write AT + slew
+    bwd = (8 * NP + 4 * P + 4 * NS + 8 * E        # sink ranges, endpoint map, fan-out CSR
+           + 32 * P + 16 * NP + 4 * NP + 4 * NS   # records, rat of fan-out pins, load, elm
+           + 16 * P + 16 * P + 8 * n_ep)          # write rat, slack, endpoint worst
+    red = 8 * n_ep
+    return dict(rc=rc, forward=fwd, backward=bwd, reduce=red)
+
+
+class Clocks:
+    """nvidia-smi sampling of SM clocks / throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if not self.p:
+            return None
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+            out, _ = self.p.communicate()
+        rows = [r.split(",") for r in out.strip().splitlines() if r.count(",") >= 8]
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows]
+        mx = float(rows[0][2])
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.strip() == "Active"})
+        busy = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def run_reference(args, world, rank):
+    """Reference arm: the fp64 oracle, as it stands, on the host cores."""
+    if rank != 0:
+        return
+    import oracle
+    import synth
+    oracle.build()
+    cfg = dict(synth.CONFIGS[args.config])
+    scale = 10                                   # bounded sample: 1/10 of the cells
+    cfg["n_cells"] //= scale
+    d = synth.generate(name=args.config, **cfg)
+    d.cons.period = synth.recipe.lookup_period(args.config) or d.cons.period
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.update(d, 0, want_all=False)
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            times.append(t1 - t0)
+    ms = 1e3 * sum(times) / len(times)
+    v = d.num_pins / (ms / 1e3)
+    sample = (f"same recipe at 1/{scale} size: {d.num_pins} pins, one full oracle update per step, "
+              "single thread fp64")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "pins/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} (sample)", "pins": d.num_pins},
+            "cpu_baseline": {"value": v, "unit": "pins/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "pins/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2511_11660_b200 as pkg
+    from paper_2511_11660_b200 import build as pbuild
+    pbuild.build()
+
+    stream = torch.cuda.current_stream()
+    t0 = time.perf_counter()
+    d = corner_design(args.config, rank)
+    gen_s = time.perf_counter() - t0
+    ctx = pkg.Context(local, 1, stream=stream.cuda_stream)
+    t0 = time.perf_counter()
+    pkg.load_design(ctx, d)
+    torch.cuda.synchronize()
+    load_s = time.perf_counter() - t0
+    # inputs resident in HBM for the device-timed value: borrowed RC tensors
+    res_d = torch.from_numpy(d.rc[0].res).cuda()
+    cap_d = torch.from_numpy(d.rc[0].cap).cuda()
+    ctx.set_rc_values(0, res_d, cap_d)
+    rows = torch.zeros((world, 4), dtype=torch.float64, device="cuda")
+
+    def step():
+        ctx.update_timing()
+        if world > 1:
+            rows.zero_()
+            ctx.report_wns_tns_device(0, rows[rank])
+            dist.all_reduce(rows)          # one NCCL allreduce of the per-corner rows
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3) if args.warmup else 0):
+        step()
+    barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    info = ctx.info()
+    P = info["num_pins"]
+    value = world * P / (ms / 1e3)
+    res_global = None
+    res_own, _ = ctx.report_slack(0)
+    if world > 1:
+        r = rows.cpu().numpy()
+        res_global = [float(r[:, 0].min()), float(r[:, 1].sum()), float(r[:, 2].min()), float(r[:, 3].sum())]
+
+    line = {"metric": METRIC, "value": value, "unit": "pins/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.config}: BASELINE.json configs[2] superblue-shaped synthetic "
+                                   f"netlist, one corner per GPU",
+                       "pins_per_gpu": P, "pin_levels": info["num_levels"], "gate_stages": info["num_stages"],
+                       "cell_arcs": info["num_cell_arcs"], "net_arcs": info["num_net_arcs"],
+                       "endpoints": info["num_endpoints"], "heavy_drivers": info["num_heavy_drivers"],
+                       "corners_per_gpu": 1, "parallelism": f"corners x{world}",
+                       "l2": "no flush: per-update working set > 1.5 GB >> 126 MB L2",
+                       "gen_s": round(gen_s, 1), "load_graph_s": round(load_s, 2)},
+            "gpu_launches": info["kernels_per_update"] * args.steps,
+            "clocks": clk, "wns_tns": [float(x) for x in res_own]}
+    if res_global:
+        line["wns_tns_global"] = res_global
+
+    if not args.quick:
+        # roofline: per-phase device time with CUDA events on the ctx stream
+        ctx.profile_enable(True)
+        for _ in range(min(args.steps, 10)):
+            ctx.update_timing()
+        prof = ctx.profile_read()
+        ctx.profile_enable(False)
+        nu = max(prof["updates"], 1)
+        ph_ms = {k: v / nu for k, v in prof["ms"].items()}
+        ab = algorithmic_bytes(d, info)
+        peak, peak_src = measured_peaks()
+        dom = max(("forward", "backward"), key=lambda k: ph_ms[k])
+        ach = ab[dom] / (ph_ms[dom] / 1e3) / 1e9
+        line["roofline"] = {"bound": "hbm", "kernel": f"{dom} stage kernels (phase)", "achieved": ach,
+                            "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                            "peak_source": peak_src, "algorithmic_bytes": ab[dom]}
+        line["phases_ms"] = ph_ms
+        line["phases_gbs"] = {k: ab[k] / (ph_ms[k] / 1e3) / 1e9 for k in ab if ph_ms.get(k, 0) > 0}
+        whole = sum(ab.values())
+        line["update_model_bytes"] = whole
+        line["update_frac_hbm"] = whole / (ms / 1e3) / 1e9 / peak
+
+        # e2e: public API with host buffers; per step H2D of the RC values
+        # (the per-iteration inputs of an optimization loop) from pinned memory,
+        # update, D2H of WNS/TNS
+        res_h = torch.from_numpy(d.rc[0].res).pin_memory()
+        cap_h = torch.from_numpy(d.rc[0].cap).pin_memory()
+        res_s = torch.empty_like(res_d)
+        cap_s = torch.empty_like(cap_d)
+
+        def e2e_step():
+            res_s.copy_(res_h, non_blocking=True)
+            cap_s.copy_(cap_h, non_blocking=True)
+            ctx.set_rc_values(0, res_s, cap_s)
+            ctx.update_timing()
+            return ctx.report_slack(0)[0]          # D2H of the step's result, synchronizes
+
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        barrier()
+        ms_e2e = e0.elapsed_time(e1) / args.steps
+        if world > 1:
+            t = torch.tensor([ms_e2e], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e2e = float(t.item())
+        line["e2e"] = {"value": world * P / (ms_e2e / 1e3), "unit": "pins/s",
+                       "h2d_bytes_per_step": int(res_h.numel() * 4 + cap_h.numel() * 4),
+                       "d2h_bytes_per_step": 32, "ms_per_step": ms_e2e}
+        ctx.set_rc_values(0, res_d, cap_d)
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.quick:
+        import oracle
+        oracle.build()
+        t0 = time.perf_counter()
+        ref = oracle.update(d, 0, want_all=False)
+        cpu_s = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": P / cpu_s, "unit": "pins/s", "cores": 1, "kind": "oracle",
+                                "sample": f"one full update of the same {P}-pin design, fp64, single thread "
+                                          f"({cpu_s:.1f} s)"}
+        r = ref["res"]
+        line["parity_wns_tns"] = {"oracle": [float(x) for x in r],
+                                  "abs_err": [float(abs(a - b)) for a, b in zip(res_own, r)]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,289 @@
+/*
+ * sta.h -- C ABI of the B200-native graph-based STA hot path
+ *          (HeteroSTA, arxiv 2511.11660, re-designed for sm_100a).
+ *
+ * The paper's boundary is a "zero-overhead flattened heterogeneous API"
+ * (PAPER.md:39, 131-134): the netlist arrives as CSR arrays (PAPER.md:166-171,
+ * "accepts external net and cell CSR arrays directly ... eliminates the need to
+ * ... maintain pin indices mappings"), parasitics as a flattened RC structure
+ * "on either CPU or GPU", reports are "WNS/TNS, pin slacks"
+ * and "all output arrays can be on CPU or GPU at user's option"
+ * (PAPER.md:191); the deliverable is a ".so" plus "C header files"
+ * (PAPER.md:198).  Every entry point below is one of those calls.
+ *
+ * Units: ps, fF, kOhm (kOhm * fF = ps).  Ids are the caller's 0-based ids and
+ * are never re-indexed: every per-pin input and output is indexed by the
+ * caller's pin id.  Per-pin timing quantities are float[4] in the order
+ * (early_rise, early_fall, late_rise, late_fall).
+ *
+ * Memory: each pointer argument is tagged by an sta_mem flag.  STA_MEM_HOST
+ * pointers are read (or written) before the call returns; the caller may free
+ * them afterwards.  STA_MEM_DEVICE pointers are CUDA device pointers on the
+ * ctx's device; inputs are copied device-to-device in stream order, except
+ * sta_set_rc_values which BORROWS them (zero copy, see there).  The library
+ * never hands out memory; outputs go to caller buffers.
+ *
+ * Errors: every call returns an sta_status; nothing throws across the ABI.
+ * sta_last_error(ctx) names the offending index ("net 17: offsets not
+ * monotone").  A CUDA failure poisons the ctx: every later call except
+ * sta_destroy / sta_last_error returns STA_ERR_CUDA.
+ *
+ * Async: sta_update_timing only enqueues work on the ctx stream.  Calls that
+ * write HOST buffers synchronize the stream; calls that write DEVICE buffers
+ * are stream ordered.
+ *
+ * Threading: a ctx is used by one host thread at a time; there is no global
+ * state, so independent ctxs may run concurrently.
+ */
+#ifndef STA_H
+#define STA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define STA_API __attribute__((visibility("default")))
+#else
+#define STA_API
+#endif
+
+typedef struct sta_ctx_s* sta_ctx;
+
+typedef enum {
+  STA_OK = 0,
+  STA_ERR_ARG = 1,         /* NULL pointer, bad count, enum or corner index, role mismatch */
+  STA_ERR_CSR = 2,         /* CSR offsets not starting at 0, not monotone, empty net */
+  STA_ERR_ID = 3,          /* pin / table id out of range */
+  STA_ERR_MULTIDRIVER = 4, /* pin in two nets, or driven by a net and a cell arc */
+  STA_ERR_CYCLE = 5,       /* combinational cycle through net + cell arcs */
+  STA_ERR_LUT = 6,         /* table size outside 1..8, axes not strictly ascending, non-finite */
+  STA_ERR_RC = 7,          /* RC tree malformed, or R/C negative or non-finite */
+  STA_ERR_ORDER = 8,       /* call order violated (see sta_update_timing) */
+  STA_ERR_CUDA = 9,        /* CUDA runtime failure; ctx poisoned */
+  STA_ERR_OOM = 10         /* device or host allocation failed */
+} sta_status;
+
+typedef enum { STA_MEM_HOST = 0, STA_MEM_DEVICE = 1 } sta_mem;
+
+/* Timing sense of a cell arc. */
+typedef enum {
+  STA_POS_UNATE = 0,   /* r->r, f->f */
+  STA_NEG_UNATE = 1,   /* r->f, f->r */
+  STA_NON_UNATE = 2,   /* all four (late: worst, early: best) */
+  STA_RISE_EDGE = 3,   /* clock-to-Q of a rising-edge register: r->r, r->f */
+  STA_FALL_EDGE = 4    /* f->r, f->f */
+} sta_sense;
+
+/* Pin roles.  PI and FF_CK pins must have no fan-in.  FF_CK pins are ideal
+ * clock sources: arrival (0, T/2) for (rise, fall), slew = clock_slew
+ * (SPEC.md:542).  FF_D pins are the data pins of check arcs. */
+typedef enum {
+  STA_PIN_INTERNAL = 0, STA_PIN_PI = 1, STA_PIN_PO = 2, STA_PIN_FF_CK = 3, STA_PIN_FF_D = 4
+} sta_pin_role;
+
+#define STA_NO_PIN 0xFFFFFFFFu
+
+/* ------------------------------------------------------------- lifecycle */
+
+/* Create a context on `cuda_device` for `num_corners` >= 1 analysis corners.
+ * `cuda_stream` is a cudaStream_t to enqueue on, or NULL for a stream the ctx
+ * creates and owns.  *out receives the handle. */
+STA_API sta_status sta_create(int cuda_device, uint32_t num_corners, void* cuda_stream, sta_ctx* out);
+
+/* Synchronize and release every resource of ctx.  NULL is a no-op. */
+STA_API sta_status sta_destroy(sta_ctx ctx);
+
+/* Message of the last failed call on ctx (valid until the next call). */
+STA_API const char* sta_last_error(sta_ctx ctx);
+
+/* Static name of a status code. */
+STA_API const char* sta_status_string(sta_status st);
+
+/* ---------------------------------------------------------------- inputs */
+
+/* Flattened netlist.
+ *  - num_pins P, pin_cap[P] (fF, input pin capacitance), pin_role[P].
+ *  - nets: net_ptr[N+1] offsets into net_pins; net n = net_pins[net_ptr[n] ..
+ *    net_ptr[n+1]); its FIRST entry is the driver, the rest are sinks.  Every
+ *    net has a driver; a pin belongs to at most one net.  Each sink gets one
+ *    net arc (driver -> sink), positive unate.
+ *  - cell arcs a < num_arcs: arc_from[a] -> arc_to[a] with arc_sense[a] and
+ *    arc_tab[a] = id of the first of 4 consecutive tables (cell_rise,
+ *    cell_fall, rise_transition, fall_transition).  A cell-arc target must not
+ *    also be a net sink.
+ *  - checks c < num_checks: data pin chk_d[c] (role FF_D), clock pin
+ *    chk_ck[c] (role FF_CK), chk_tab[c] = first of 4 tables (setup_rise,
+ *    setup_fall, hold_rise, hold_fall), indexed by (data slew, clock slew).
+ *    Checks create endpoints, not graph edges.
+ *  - num_tables: size of every corner's table pool; every table id used above
+ *    (+3) must be < num_tables.
+ * Arrays are all HOST or all DEVICE (`mem`); arrays of a zero count may be NULL. */
+typedef struct {
+  sta_mem mem;
+  uint32_t num_pins;
+  const float* pin_cap;
+  const uint8_t* pin_role;
+  uint32_t num_nets;
+  const uint32_t* net_ptr;
+  const uint32_t* net_pins;
+  uint32_t num_arcs;
+  const uint32_t* arc_from;
+  const uint32_t* arc_to;
+  const uint8_t* arc_sense;
+  const uint32_t* arc_tab;
+  uint32_t num_checks;
+  const uint32_t* chk_d;
+  const uint32_t* chk_ck;
+  const uint32_t* chk_tab;
+  uint32_t num_tables;
+} sta_graph_desc;
+
+/* Validate the netlist, levelize it (longest-path pin levels over net + cell
+ * arcs) and build the device-resident timing graph.  Runs
+ * once per design; resets every library / RC / constraint input.
+ * Errors: STA_ERR_ARG, STA_ERR_CSR, STA_ERR_ID, STA_ERR_MULTIDRIVER,
+ * STA_ERR_CYCLE, STA_ERR_OOM, STA_ERR_CUDA. */
+STA_API sta_status sta_load_graph(sta_ctx ctx, const sta_graph_desc* desc);
+
+/* NLDM table pool of one corner (SPEC.md:30-45 Lut2D).
+ * Table t: n1[t], n2[t] in 1..8, data[off[t] ...] = index_1[n1] (input slew
+ * ps; data slew for constraint tables), index_2[n2] (load fF; clock slew for
+ * constraint tables), values[n1][n2] row-major (ps).  Axes strictly
+ * ascending.  Copied (small).  Errors: STA_ERR_ARG, STA_ERR_LUT. */
+STA_API sta_status sta_set_library(sta_ctx ctx, uint32_t corner, sta_mem mem, uint32_t num_tables,
+                           const uint8_t* n1, const uint8_t* n2, const uint32_t* off,
+                           const float* data, uint32_t data_len);
+
+/* RC tree topology, shared by all corners ("a set of predefined
+ * CSR structures").  Net n owns nodes
+ * [rc_ptr[n], rc_ptr[n+1]) (rc_ptr[N] = num_nodes).  Within a net, node 0 is
+ * the driver (parent -1), parent[i] is a LOCAL index < i, node_pin[i] is a
+ * pin of that net or STA_NO_PIN (Steiner/wire node).  If a net has nodes,
+ * each of its sinks maps to exactly one node and node 0 maps to the driver or
+ * STA_NO_PIN.  A net without nodes is lumped (load = its pin caps + PO
+ * loads, zero wire delay).  Copied.  Errors: STA_ERR_ORDER (no graph),
+ * STA_ERR_ARG, STA_ERR_CSR, STA_ERR_RC. */
+STA_API sta_status sta_set_rc_tree(sta_ctx ctx, sta_mem mem, const uint32_t* rc_ptr, uint32_t num_nodes,
+                           const int32_t* parent, const uint32_t* node_pin);
+
+/* Per-corner RC values: res[i] = resistance of the edge parent -> i (kOhm,
+ * ignored at node 0), cap[i] = wire capacitance to ground at node i (fF);
+ * both num_nodes long, >= 0 and finite.  HOST: copied (validated).  DEVICE:
+ * BORROWED, zero copy -- the caller keeps both arrays alive and unmodified
+ * until the next sta_update_timing has completed on the ctx stream; a bad
+ * value is detected on the device and reported as STA_ERR_RC by the next
+ * synchronizing call.  This is the per-iteration call of an optimization
+ * loop. */
+STA_API sta_status sta_set_rc_values(sta_ctx ctx, uint32_t corner, sta_mem mem, const float* res,
+                             const float* cap);
+
+/* One ideal clock plus port constraints.
+ *  - period_ps > 0 (setup capture edge), clock_slew_ps >= 0.
+ *  - PIs: pi_pin[k] (role PI), pi_at[k][4], pi_slew[k][4] (finite).  A PI pin
+ *    not listed is an undefined source (no arrival).
+ *  - POs: po_pin[k] (role PO), po_out_max[k][2], po_out_min[k][2]
+ *    (rise, fall output delays), po_load_ff[k] added to the PO pin's node cap.
+ * All arrays HOST or DEVICE per `mem`; copied.  Errors: STA_ERR_ORDER,
+ * STA_ERR_ARG, STA_ERR_ID. */
+typedef struct {
+  sta_mem mem;
+  float period_ps;
+  float clock_slew_ps;
+  uint32_t n_pi;
+  const uint32_t* pi_pin;
+  const float* pi_at;
+  const float* pi_slew;
+  uint32_t n_po;
+  const uint32_t* po_pin;
+  const float* po_out_max;
+  const float* po_out_min;
+  const float* po_load_ff;
+} sta_constraints;
+STA_API sta_status sta_set_constraints(sta_ctx ctx, const sta_constraints* cons);
+
+/* --------------------------------------------------------------- update */
+
+/* One full timing update for every corner of ctx, enqueued on the ctx
+ * stream: Elmore RC and loads, forward AT/slew with NLDM cell delays, endpoint
+ * required-time seeds, backward RAT, per-pin slack, WNS/TNS (SURVEY.md §8(a)
+ * a1-a5).  Requires sta_load_graph, sta_set_rc_tree, sta_set_constraints and,
+ * for every corner, sta_set_library and sta_set_rc_values (else
+ * STA_ERR_ORDER).  Asynchronous: errors of the kernels surface at the next
+ * synchronizing call. */
+STA_API sta_status sta_update_timing(sta_ctx ctx);
+
+/* ------------------------------------------------------------- reports */
+
+/* Results of `corner` after the last update.
+ *  - res4 (may be NULL): double[4] {WNS_setup, TNS_setup, WNS_hold, TNS_hold}
+ *    in ps, in `mem` memory.  WNS = min over endpoints (PO pins and check data
+ *    pins) of the worst (over rise/fall) slack, +inf if none is constrained;
+ *    TNS = sum over endpoints of min(0, worst slack), accumulated in fp64
+ *    (SPEC.md:515-523, 547).  HOST: synchronizes and reports deferred errors;
+ *    DEVICE: stream ordered (for a device-side allreduce across ranks).
+ *  - pin_slack (may be NULL): float[P][4] per pin (hold rise, hold fall, setup
+ *    rise, setup fall) = (AT_E - RAT_E, AT_E - RAT_E, RAT_L - AT_L, RAT_L -
+ *    AT_L), +inf where either side is undefined, in `mem` memory. */
+STA_API sta_status sta_report_slack(sta_ctx ctx, uint32_t corner, double* res4, float* pin_slack,
+                            sta_mem mem);
+
+/* Full per-pin state of `corner` (any pointer may be NULL): at, slew, rat as
+ * float[P][4].  Undefined components are +inf (early) / -inf (late) for at
+ * and slew and -inf (early) / +inf (late) for rat. */
+STA_API sta_status sta_get_timing(sta_ctx ctx, uint32_t corner, float* at, float* slew, float* rat,
+                          sta_mem mem);
+
+/* Delay-calculation results of `corner` (either pointer may be NULL):
+ * net_load[N] (fF, the NLDM load of each net's driver) and pin_elm[P] (the
+ * Elmore delay of the net arc into each sink pin, 0 for non-sinks). */
+STA_API sta_status sta_get_rc(sta_ctx ctx, uint32_t corner, float* net_load, float* pin_elm,
+                      sta_mem mem);
+
+/* Levelization of the loaded graph: level[P] = longest-path depth of each
+ * pin (0 without fan-in), perm[P] = pins stably sorted by (level, pin id),
+ * *num_levels = max level + 1 (HOST).  level/perm may be NULL. */
+STA_API sta_status sta_get_levels(sta_ctx ctx, uint32_t* level, uint32_t* perm, uint32_t* num_levels,
+                          sta_mem mem);
+
+/* Counters describing the loaded graph and the last update. */
+typedef struct {
+  uint32_t num_pins, num_nets, num_net_arcs, num_cell_arcs, num_checks, num_endpoints;
+  uint32_t num_levels;       /* pin levels */
+  uint32_t num_stages;       /* gate stages the kernels step through */
+  uint32_t num_pull_pins;    /* pins evaluated over cell arcs (stage pins) */
+  uint32_t num_sink_pins;    /* net sinks */
+  uint32_t num_heavy_drivers;
+  uint32_t kernels_per_update; /* kernel launches of one sta_update_timing */
+  uint64_t device_bytes;     /* device memory held by ctx */
+} sta_info;
+STA_API sta_status sta_get_info(sta_ctx ctx, sta_info* out);
+
+/* Block until all work enqueued on the ctx stream is done; returns any
+ * deferred kernel error (STA_ERR_CUDA, STA_ERR_RC). */
+STA_API sta_status sta_synchronize(sta_ctx ctx);
+
+/* ------------------------------------------------------------ profiling */
+
+/* Per-phase device time of sta_update_timing, measured with CUDA events on the
+ * ctx stream around each phase's kernels (used by bench.py's roofline).
+ * Phases: 0 = RC/Elmore (a1), 1 = forward AT/slew (a2), 2 = backward RAT +
+ * slack (a3-a5 per pin), 3 = WNS/TNS reduction (a5), 4 = whole update. */
+#define STA_NUM_PHASES 5
+typedef struct {
+  double ms[STA_NUM_PHASES];        /* accumulated milliseconds */
+  uint32_t launches[STA_NUM_PHASES];/* accumulated kernel launches */
+  uint32_t updates;                 /* updates accumulated */
+} sta_profile;
+
+/* enable != 0: start (and zero) accumulation; 0: stop. */
+STA_API sta_status sta_profile_enable(sta_ctx ctx, int enable);
+/* Synchronizes, then copies the accumulated profile. */
+STA_API sta_status sta_profile_read(sta_ctx ctx, sta_profile* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STA_H */

@@ -176,7 +176,7 @@ def update(d, corner: int = 0, want_all: bool = True):
     if st:
         raise MemoryError("oracle allocation failed")
     ne = int(n_ep[0])
-    out = dict(at=at[:P], res=res, ep_pin=ep_pin[:ne], ep_ws=ep_ws[:ne])
+    out = dict(at=at[:P], res=res, ep_pin=ep_pin[:ne], ep_ws=ep_ws[:ne], period=float(d.cons.period))
     if want_all:
         out.update(slew=slew[:P], rat=rat[:P], slack=slack[:P])
     return out

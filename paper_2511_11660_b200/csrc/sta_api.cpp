@@ -1,0 +1,1102 @@
+// sta_api.cpp -- the C ABI of include/sta.h: validation, the host-side
+// plan of the timing graph (levels, gate stages, internal numbering, CSR
+// arrays, RC schedules), device memory and the update launcher.
+//
+// Every arithmetic step of the timing update runs in sta_kernels.cu; this file
+// only arranges data (integer bookkeeping) and enqueues kernels.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/sta.h"
+#include "sta_internal.h"
+
+using sta::kNone;
+using u32 = uint32_t;
+
+namespace {
+
+struct StaError {
+  sta_status st;
+  std::string msg;
+};
+
+[[noreturn]] void fail(sta_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  throw StaError{st, buf};
+}
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    if (e == cudaErrorMemoryAllocation) fail(STA_ERR_OOM, "%s: %s", what, cudaGetErrorString(e));
+    fail(STA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  }
+}
+
+// device allocations grouped by lifetime scope
+struct Arena {
+  std::vector<void*> ptrs;
+  uint64_t bytes = 0;
+  template <class T>
+  T* alloc(size_t n) {
+    if (n == 0) n = 1;
+    void* p = nullptr;
+    ck(cudaMalloc(&p, n * sizeof(T)), "cudaMalloc");
+    ptrs.push_back(p);
+    bytes += n * sizeof(T);
+    return static_cast<T*>(p);
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v, cudaStream_t s) {
+    T* p = alloc<T>(v.size());
+    if (!v.empty()) ck(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
+    return p;
+  }
+  void release() {
+    for (void* p : ptrs) cudaFree(p);
+    ptrs.clear();
+    bytes = 0;
+  }
+};
+
+// copy caller input (HOST or DEVICE) into a host vector
+template <class T>
+std::vector<T> fetch(const T* p, size_t n, sta_mem mem, const char* name) {
+  std::vector<T> v(n);
+  if (n == 0) return v;
+  if (!p) fail(STA_ERR_ARG, "%s: NULL pointer for %zu elements", name, n);
+  if (mem == STA_MEM_HOST) {
+    std::memcpy(v.data(), p, n * sizeof(T));
+  } else if (mem == STA_MEM_DEVICE) {
+    ck(cudaMemcpy(v.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost), name);
+  } else {
+    fail(STA_ERR_ARG, "%s: bad sta_mem %d", name, (int)mem);
+  }
+  return v;
+}
+
+struct CornerState {
+  bool lib = false, rcv = false;
+  u32 n_tables = 0;
+  Arena lib_arena, rc_arena, state_arena;
+  const float* rc_res = nullptr;
+  const float* rc_cap = nullptr;
+  sta::CornerDev dev{};
+};
+
+}  // namespace
+
+struct sta_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  u32 K = 1;
+  std::string err;
+  bool poisoned = false;
+  bool has_graph = false, has_tree = false, has_cons = false, prepared = false;
+
+  // ---- host copy of the netlist (validated)
+  u32 P = 0, N = 0, A = 0, C = 0, T = 0;
+  std::vector<float> pin_cap;
+  std::vector<uint8_t> pin_role;
+  std::vector<u32> net_ptr, net_pins, arc_from, arc_to, arc_tab, chk_d, chk_ck, chk_tab;
+  std::vector<uint8_t> arc_sense;
+  std::vector<u32> pin_net;       // net of each pin or kNone
+  std::vector<uint8_t> is_sink;   // pin is a net sink (not driver)
+  std::vector<u32> chk_of_pin;    // check index of a data pin or kNone
+
+  // ---- plan
+  std::vector<u32> level, perm;
+  u32 num_levels = 0;
+  std::vector<u32> stage, int_of_user, user_of_int;
+  u32 NP = 0, NS = 0, S = 0, n0 = 0;
+  std::vector<u32> pull_stage_ptr, sink_stage_ptr, heavy_stage_ptr, sink_ptr, heavy;
+  std::vector<u32> drv_of_net;    // user net -> internal driver id
+  u32 n_heavy = 0;
+
+  // ---- RC tree (host)
+  std::vector<u32> rc_ptr, rc_node_pin;
+  std::vector<int32_t> rc_parent;
+  u32 n_rc = 0;
+  u32 big_total = 0;
+
+  // ---- constraints (host)
+  float period = 0, clock_slew = 0;
+  std::vector<u32> pi_pin, po_pin;
+  std::vector<float> pi_at, pi_slew, po_out_max, po_out_min, po_load;
+  u32 n_ep = 0;
+
+  // ---- device
+  Arena graph_arena, tree_arena, cons_arena, tmp_arena;
+  sta::Topo topo{};
+  std::vector<CornerState> corners;
+
+  // ---- profiling
+  bool prof = false;
+  sta_profile profile{};
+  cudaEvent_t ev[STA_NUM_PHASES * 2] = {};
+  u32 launches_per_update = 0;
+};
+
+namespace {
+
+void prof_mark(sta_ctx c, int idx) {
+  if (c->prof) ck(cudaEventRecord(c->ev[idx], c->stream), "cudaEventRecord");
+}
+
+// ------------------------------------------------------------ validation
+void validate_graph(sta_ctx c) {
+  const u32 P = c->P;
+  for (u32 p = 0; p < P; ++p) {
+    if (c->pin_role[p] > STA_PIN_FF_D) fail(STA_ERR_ARG, "pin %u: bad role %u", p, c->pin_role[p]);
+    if (!std::isfinite(c->pin_cap[p]) || c->pin_cap[p] < 0) fail(STA_ERR_ARG, "pin %u: bad pin_cap", p);
+  }
+  if (c->N) {
+    if (c->net_ptr[0] != 0) fail(STA_ERR_CSR, "net_ptr[0] = %u, expected 0", c->net_ptr[0]);
+    for (u32 n = 0; n < c->N; ++n)
+      if (c->net_ptr[n + 1] <= c->net_ptr[n])
+        fail(STA_ERR_CSR, "net %u: offsets not monotone or empty net (no driver)", n);
+  }
+  c->pin_net.assign(P, kNone);
+  c->is_sink.assign(P, 0);
+  for (u32 n = 0; n < c->N; ++n) {
+    for (u32 k = c->net_ptr[n]; k < c->net_ptr[n + 1]; ++k) {
+      const u32 p = c->net_pins[k];
+      if (p >= P) fail(STA_ERR_ID, "net %u: pin id %u out of range", n, p);
+      if (c->pin_net[p] != kNone) fail(STA_ERR_MULTIDRIVER, "pin %u: in nets %u and %u", p, c->pin_net[p], n);
+      c->pin_net[p] = n;
+      c->is_sink[p] = k != c->net_ptr[n];
+    }
+  }
+  for (u32 a = 0; a < c->A; ++a) {
+    const u32 f = c->arc_from[a], t = c->arc_to[a];
+    if (f >= P || t >= P) fail(STA_ERR_ID, "arc %u: pin id out of range", a);
+    if (c->arc_sense[a] > STA_FALL_EDGE) fail(STA_ERR_ARG, "arc %u: bad sense %u", a, c->arc_sense[a]);
+    if ((uint64_t)c->arc_tab[a] + 3 >= c->T) fail(STA_ERR_ID, "arc %u: table id %u out of range", a, c->arc_tab[a]);
+    if (c->is_sink[t]) fail(STA_ERR_MULTIDRIVER, "pin %u: driven by net %u and by cell arc %u", t, c->pin_net[t], a);
+    if (f == t) fail(STA_ERR_CYCLE, "cycle through pin %u (self arc %u)", f, a);
+  }
+  c->chk_of_pin.assign(P, kNone);
+  for (u32 k = 0; k < c->C; ++k) {
+    const u32 d = c->chk_d[k], ckp = c->chk_ck[k];
+    if (d >= P || ckp >= P) fail(STA_ERR_ID, "check %u: pin id out of range", k);
+    if (c->pin_role[d] != STA_PIN_FF_D) fail(STA_ERR_ARG, "check %u: data pin %u does not have role FF_D", k, d);
+    if (c->pin_role[ckp] != STA_PIN_FF_CK) fail(STA_ERR_ARG, "check %u: clock pin %u does not have role FF_CK", k, ckp);
+    if ((uint64_t)c->chk_tab[k] + 3 >= c->T) fail(STA_ERR_ID, "check %u: table id %u out of range", k, c->chk_tab[k]);
+    if (c->chk_of_pin[d] != kNone) fail(STA_ERR_ARG, "pin %u: two checks (%u, %u)", d, c->chk_of_pin[d], k);
+    c->chk_of_pin[d] = k;
+  }
+  for (u32 p = 0; p < P; ++p)
+    if ((c->pin_role[p] == STA_PIN_PI || c->pin_role[p] == STA_PIN_FF_CK) && c->is_sink[p])
+      fail(STA_ERR_ARG, "pin %u: role %s must not have fan-in", p, c->pin_role[p] == STA_PIN_PI ? "PI" : "FF_CK");
+}
+
+// CSR of arcs grouped by key (stable in arc id order)
+void group_arcs(const std::vector<u32>& key, u32 P, std::vector<u32>& ptr, std::vector<u32>& ids) {
+  ptr.assign(P + 1, 0);
+  for (u32 k : key) ptr[k + 1]++;
+  for (u32 p = 0; p < P; ++p) ptr[p + 1] += ptr[p];
+  ids.resize(key.size());
+  std::vector<u32> fill(ptr.begin(), ptr.end() - 1);
+  for (u32 a = 0; a < key.size(); ++a) ids[fill[key[a]]++] = a;
+}
+
+// ------------------------------------------------------------------ plan
+void build_plan(sta_ctx c) {
+  const u32 P = c->P;
+  std::vector<u32> fi_ptr, fi_ids, fo_ptr, fo_ids;
+  group_arcs(c->arc_to, P, fi_ptr, fi_ids);
+  group_arcs(c->arc_from, P, fo_ptr, fo_ids);
+  for (u32 p = 0; p < P; ++p)
+    if (c->pin_role[p] == STA_PIN_PI || c->pin_role[p] == STA_PIN_FF_CK)
+      if (fi_ptr[p + 1] != fi_ptr[p])
+        fail(STA_ERR_ARG, "pin %u: role %s must not have fan-in", p, c->pin_role[p] == STA_PIN_PI ? "PI" : "FF_CK");
+  auto driver_of = [&](u32 p) { return c->net_pins[c->net_ptr[c->pin_net[p]]]; };
+
+  // Kahn levelization over net + cell arcs, FIFO seeded in id order
+  // (SPEC.md:257).  level = longest path depth.
+  std::vector<u32> indeg(P), order;
+  order.reserve(P);
+  c->level.assign(P, 0);
+  for (u32 p = 0; p < P; ++p) {
+    indeg[p] = (c->is_sink[p] ? 1u : 0u) + (fi_ptr[p + 1] - fi_ptr[p]);
+    if (!indeg[p]) order.push_back(p);
+  }
+  for (size_t h = 0; h < order.size(); ++h) {
+    const u32 u = order[h];
+    auto relax = [&](u32 v) {
+      if (c->level[u] + 1 > c->level[v]) c->level[v] = c->level[u] + 1;
+      if (--indeg[v] == 0) order.push_back(v);
+    };
+    const u32 n = c->pin_net[u];
+    if (n != kNone && !c->is_sink[u])
+      for (u32 k = c->net_ptr[n] + 1; k < c->net_ptr[n + 1]; ++k) relax(c->net_pins[k]);
+    for (u32 x = fo_ptr[u]; x < fo_ptr[u + 1]; ++x) relax(c->arc_to[fo_ids[x]]);
+  }
+  if (order.size() != P) {
+    for (u32 p = 0; p < P; ++p)
+      if (indeg[p]) fail(STA_ERR_CYCLE, "combinational cycle through pin %u", p);
+  }
+  c->num_levels = 0;
+  for (u32 p = 0; p < P; ++p) c->num_levels = std::max(c->num_levels, c->level[p] + 1);
+  {
+    std::vector<u32> start(c->num_levels + 1, 0);
+    for (u32 p = 0; p < P; ++p) start[c->level[p] + 1]++;
+    for (u32 l = 0; l < c->num_levels; ++l) start[l + 1] += start[l];
+    c->perm.resize(P);
+    for (u32 p = 0; p < P; ++p) c->perm[start[c->level[p]]++] = p;
+  }
+
+  // gate stages in pin-level order
+  c->stage.assign(P, 0);
+  for (u32 p : c->perm) {
+    if (c->is_sink[p]) {
+      c->stage[p] = c->stage[driver_of(p)];
+    } else if (fi_ptr[p + 1] != fi_ptr[p]) {
+      u32 s = 0;
+      for (u32 x = fi_ptr[p]; x < fi_ptr[p + 1]; ++x) s = std::max(s, c->stage[c->arc_from[fi_ids[x]]] + 1);
+      c->stage[p] = s;
+    }
+  }
+
+  // internal numbering: pull pins by (stage, id); sinks grouped by driver
+  u32 NP = 0, S = 0;
+  for (u32 p = 0; p < P; ++p)
+    if (!c->is_sink[p]) { ++NP; S = std::max(S, c->stage[p] + 1); }
+  c->NP = NP;
+  c->NS = P - NP;
+  c->S = S;
+  c->pull_stage_ptr.assign(S + 1, 0);
+  for (u32 p = 0; p < P; ++p)
+    if (!c->is_sink[p]) c->pull_stage_ptr[c->stage[p] + 1]++;
+  for (u32 s = 0; s < S; ++s) c->pull_stage_ptr[s + 1] += c->pull_stage_ptr[s];
+  c->n0 = S ? c->pull_stage_ptr[1] : 0;
+  c->int_of_user.assign(P, kNone);
+  c->user_of_int.assign(P, kNone);
+  {
+    std::vector<u32> fill(c->pull_stage_ptr.begin(), c->pull_stage_ptr.end());
+    for (u32 p = 0; p < P; ++p)
+      if (!c->is_sink[p]) {
+        const u32 i = fill[c->stage[p]]++;
+        c->int_of_user[p] = i;
+        c->user_of_int[i] = p;
+      }
+  }
+  c->sink_ptr.assign(NP + 1, 0);
+  c->drv_of_net.assign(c->N, kNone);
+  u32 k = 0;
+  for (u32 i = 0; i < NP; ++i) {
+    const u32 p = c->user_of_int[i];
+    c->sink_ptr[i] = k;
+    const u32 n = c->pin_net[p];
+    if (n != kNone) {   // p is the driver of n
+      c->drv_of_net[n] = i;
+      for (u32 x = c->net_ptr[n] + 1; x < c->net_ptr[n + 1]; ++x) {
+        const u32 s = c->net_pins[x];
+        c->int_of_user[s] = NP + k;
+        c->user_of_int[NP + k] = s;
+        ++k;
+      }
+    }
+  }
+  c->sink_ptr[NP] = k;
+  c->sink_stage_ptr.assign(S + 1, 0);
+  for (u32 s = 0; s <= S; ++s) c->sink_stage_ptr[s] = c->sink_ptr[c->pull_stage_ptr[s]];
+
+  // forward fan-in terms of pull pins (cell arcs, arc id order)
+  std::vector<u32> fi_p(NP + 1, 0), fi_src, fi_hop, fi_info;
+  fi_src.reserve(c->A);
+  fi_hop.reserve(c->A);
+  fi_info.reserve(c->A);
+  for (u32 i = 0; i < NP; ++i) {
+    const u32 p = c->user_of_int[i];
+    fi_p[i] = (u32)fi_src.size();
+    for (u32 x = fi_ptr[p]; x < fi_ptr[p + 1]; ++x) {
+      const u32 a = fi_ids[x], u = c->arc_from[a];
+      if (c->is_sink[u]) {
+        fi_src.push_back(c->int_of_user[driver_of(u)]);
+        fi_hop.push_back(c->int_of_user[u] - NP);
+      } else {
+        fi_src.push_back(c->int_of_user[u]);
+        fi_hop.push_back(kNone);
+      }
+      fi_info.push_back(sta::pack_info(c->arc_sense[a], c->arc_tab[a]));
+    }
+  }
+  fi_p[NP] = (u32)fi_src.size();
+
+  // backward: cell fan-out of sinks and of pull pins
+  std::vector<u32> sfo_p(c->NS + 1, 0), sfo_dst, sfo_info, pfo_p(NP + 1, 0), pfo_dst, pfo_info;
+  for (u32 kk = 0; kk < c->NS; ++kk) {
+    const u32 u = c->user_of_int[NP + kk];
+    sfo_p[kk] = (u32)sfo_dst.size();
+    for (u32 x = fo_ptr[u]; x < fo_ptr[u + 1]; ++x) {
+      const u32 a = fo_ids[x];
+      sfo_dst.push_back(c->int_of_user[c->arc_to[a]]);
+      sfo_info.push_back(sta::pack_info(c->arc_sense[a], c->arc_tab[a]));
+    }
+  }
+  sfo_p[c->NS] = (u32)sfo_dst.size();
+  for (u32 i = 0; i < NP; ++i) {
+    const u32 u = c->user_of_int[i];
+    pfo_p[i] = (u32)pfo_dst.size();
+    for (u32 x = fo_ptr[u]; x < fo_ptr[u + 1]; ++x) {
+      const u32 a = fo_ids[x];
+      pfo_dst.push_back(c->int_of_user[c->arc_to[a]]);
+      pfo_info.push_back(sta::pack_info(c->arc_sense[a], c->arc_tab[a]));
+    }
+  }
+  pfo_p[NP] = (u32)pfo_dst.size();
+
+  // heavy drivers per stage
+  c->heavy.clear();
+  c->heavy_stage_ptr.assign(S + 1, 0);
+  for (u32 s = 0; s < S; ++s) {
+    c->heavy_stage_ptr[s] = (u32)c->heavy.size();
+    for (u32 i = c->pull_stage_ptr[s]; i < c->pull_stage_ptr[s + 1]; ++i)
+      if (c->sink_ptr[i + 1] - c->sink_ptr[i] > (u32)sta::kHeavyFanout) c->heavy.push_back(i);
+  }
+  c->heavy_stage_ptr[S] = (u32)c->heavy.size();
+  c->n_heavy = (u32)c->heavy.size();
+
+  std::vector<u32> sink_drv(c->NS);
+  for (u32 i = 0; i < NP; ++i)
+    for (u32 x = c->sink_ptr[i]; x < c->sink_ptr[i + 1]; ++x) sink_drv[x] = i;
+
+  // upload
+  cudaStream_t s = c->stream;
+  Arena& g = c->graph_arena;
+  sta::Topo& t = c->topo;
+  t = sta::Topo{};
+  t.P = P; t.NP = NP; t.NS = c->NS; t.S = S; t.N = c->N;
+  t.fi_ptr = g.upload(fi_p, s);
+  t.fi_src = g.upload(fi_src, s);
+  t.fi_hop = g.upload(fi_hop, s);
+  t.fi_info = g.upload(fi_info, s);
+  t.sink_ptr = g.upload(c->sink_ptr, s);
+  t.sink_drv = g.upload(sink_drv, s);
+  t.sfo_ptr = g.upload(sfo_p, s);
+  t.sfo_dst = g.upload(sfo_dst, s);
+  t.sfo_info = g.upload(sfo_info, s);
+  t.pfo_ptr = g.upload(pfo_p, s);
+  t.pfo_dst = g.upload(pfo_dst, s);
+  t.pfo_info = g.upload(pfo_info, s);
+  t.heavy = g.upload(c->heavy, s);
+  t.int_of_user = g.upload(c->int_of_user, s);
+  ck(cudaStreamSynchronize(s), "plan upload");
+}
+
+// RC tree topology: validation and per-net schedules (tree scope)
+void build_rc(sta_ctx c) {
+  const u32 N = c->N;
+  // validation
+  if (c->rc_ptr.size() != N + 1) fail(STA_ERR_ARG, "rc_ptr must have num_nets + 1 entries");
+  if (N && c->rc_ptr[0] != 0) fail(STA_ERR_CSR, "rc_ptr[0] = %u, expected 0", c->rc_ptr[0]);
+  for (u32 n = 0; n < N; ++n)
+    if (c->rc_ptr[n + 1] < c->rc_ptr[n]) fail(STA_ERR_CSR, "rc net %u: offsets not monotone", n);
+  if (N && c->rc_ptr[N] != c->n_rc) fail(STA_ERR_CSR, "rc_ptr[N] = %u != num_nodes %u", c->rc_ptr[N], c->n_rc);
+  std::vector<u32> seen(c->P, 0);
+  for (u32 n = 0; n < N; ++n) {
+    const u32 b = c->rc_ptr[n], m = c->rc_ptr[n + 1] - b;
+    if (!m) continue;
+    const u32 drv = c->net_pins[c->net_ptr[n]];
+    if (c->rc_parent[b] != -1) fail(STA_ERR_RC, "rc net %u: node 0 must have parent -1", n);
+    if (c->rc_node_pin[b] != kNone && c->rc_node_pin[b] != drv)
+      fail(STA_ERR_RC, "rc net %u: node 0 maps pin %u, not the driver %u", n, c->rc_node_pin[b], drv);
+    for (u32 i = 1; i < m; ++i) {
+      const int32_t pa = c->rc_parent[b + i];
+      if (pa < 0 || (u32)pa >= i) fail(STA_ERR_RC, "rc net %u node %u: parent %d not in [0, %u)", n, i, pa, i);
+      const u32 pin = c->rc_node_pin[b + i];
+      if (pin == kNone) continue;
+      if (pin >= c->P || c->pin_net[pin] != n || !c->is_sink[pin])
+        fail(STA_ERR_RC, "rc net %u node %u: pin %u is not a sink of the net", n, i, pin);
+      if (seen[pin]++) fail(STA_ERR_RC, "rc net %u: sink pin %u mapped to two nodes", n, pin);
+    }
+    for (u32 x = c->net_ptr[n] + 1; x < c->net_ptr[n + 1]; ++x)
+      if (!seen[c->net_pins[x]]) fail(STA_ERR_RC, "rc net %u: sink pin %u has no RC node", n, c->net_pins[x]);
+  }
+
+  // nets in driver order j
+  std::vector<u32> net_drv, net_rc, net_rcn, net_of_j;
+  net_drv.reserve(N);
+  for (u32 i = 0; i < c->NP; ++i) {
+    const u32 p = c->user_of_int[i];
+    const u32 n = c->pin_net[p];
+    if (n == kNone) continue;
+    net_of_j.push_back(n);
+    net_drv.push_back(i);
+    net_rc.push_back(c->rc_ptr[n]);
+    net_rcn.push_back(c->rc_ptr[n + 1] - c->rc_ptr[n]);
+  }
+  net_rc.push_back(c->n_rc);
+  std::vector<u32> rc_sink(c->n_rc, kNone);
+  for (u32 i = 0; i < c->n_rc; ++i) {
+    const u32 pin = c->rc_node_pin[i];
+    if (pin != kNone && c->is_sink[pin]) rc_sink[i] = c->int_of_user[pin] - c->NP;
+  }
+  // big-net schedules
+  std::vector<u32> big_net, big_scr{0}, hoff{0}, hptr, hnode, doff{0}, dptr, dnode, cptr, child;
+  for (u32 j = 0; j < (u32)net_of_j.size(); ++j) {
+    const u32 m = net_rcn[j];
+    if (m <= (u32)sta::kSmallNet) continue;
+    const u32 b = net_rc[j];
+    big_net.push_back(j);
+    big_scr.push_back(big_scr.back() + m);
+    std::vector<u32> h(m, 0), dep(m, 0), cnt(m + 1, 0);
+    for (u32 i = m - 1; i >= 1; --i) {
+      const u32 pa = (u32)c->rc_parent[b + i];
+      h[pa] = std::max(h[pa], h[i] + 1);
+      cnt[pa + 1]++;
+    }
+    for (u32 i = 1; i < m; ++i) dep[i] = dep[(u32)c->rc_parent[b + i]] + 1;
+    // children CSR, decreasing child index within a parent
+    const size_t cbase = child.size();
+    for (u32 i = 0; i < m; ++i) cnt[i + 1] += cnt[i];
+    for (u32 i = 0; i <= m; ++i) cptr.push_back((u32)cbase + cnt[i]);
+    child.resize(cbase + (m - 1));
+    {
+      std::vector<u32> fill(cnt.begin(), cnt.end() - 1);
+      for (u32 i = m - 1; i >= 1; --i) child[cbase + fill[(u32)c->rc_parent[b + i]]++] = i;
+    }
+    // nodes grouped by height
+    const u32 H = *std::max_element(h.begin(), h.end());
+    std::vector<u32> hs(H + 2, 0);
+    for (u32 i = 0; i < m; ++i) hs[h[i] + 1]++;
+    for (u32 x = 0; x <= H; ++x) hs[x + 1] += hs[x];
+    const size_t hbase = hnode.size();
+    hnode.resize(hbase + m);
+    {
+      std::vector<u32> fill(hs.begin(), hs.end() - 1);
+      for (u32 i = 0; i < m; ++i) hnode[hbase + fill[h[i]]++] = i;
+    }
+    for (u32 x = 0; x <= H + 1; ++x) hptr.push_back((u32)hbase + hs[x]);
+    hoff.push_back((u32)hptr.size());
+    // nodes grouped by depth (depth >= 1)
+    const u32 Dm = *std::max_element(dep.begin(), dep.end());
+    std::vector<u32> ds(Dm + 2, 0);
+    for (u32 i = 1; i < m; ++i) ds[dep[i] + 1]++;
+    for (u32 x = 0; x <= Dm; ++x) ds[x + 1] += ds[x];
+    const size_t dbase = dnode.size();
+    dnode.resize(dbase + (m - 1));
+    {
+      std::vector<u32> fill(ds.begin(), ds.end() - 1);
+      for (u32 i = 1; i < m; ++i) dnode[dbase + fill[dep[i]]++] = i;
+    }
+    for (u32 x = 1; x <= Dm + 1; ++x) dptr.push_back((u32)dbase + ds[x]);
+    doff.push_back((u32)dptr.size());
+  }
+  // hoff/doff were pushed after each net: turn them into [n_big+1] ranges
+  // (hoff[b]..hoff[b+1]) -- they already are, since they started at 0.
+  c->big_total = big_scr.back();
+
+  cudaStream_t s = c->stream;
+  c->tree_arena.release();
+  Arena& g = c->tree_arena;
+  sta::Topo& t = c->topo;
+  t.net_drv = g.upload(net_drv, s);
+  t.net_rc = g.upload(net_rc, s);
+  t.net_rcn = g.upload(net_rcn, s);
+  t.rc_parent = g.upload(c->rc_parent, s);
+  t.rc_sink = g.upload(rc_sink, s);
+  t.n_big = (u32)big_net.size();
+  t.big_net = g.upload(big_net, s);
+  t.big_scr = g.upload(big_scr, s);
+  t.big_hptr_off = g.upload(hoff, s);
+  t.big_hptr = g.upload(hptr, s);
+  t.big_hnode = g.upload(hnode, s);
+  t.big_dptr_off = g.upload(doff, s);
+  t.big_dptr = g.upload(dptr, s);
+  t.big_dnode = g.upload(dnode, s);
+  t.big_cptr = g.upload(cptr, s);
+  t.big_child = g.upload(child, s);
+  ck(cudaStreamSynchronize(s), "rc upload");
+}
+
+// constraints + tree dependent arrays (endpoints, seeds, static node caps)
+void prepare(sta_ctx c) {
+  if (c->prepared) return;
+  const u32 P = c->P;
+  std::vector<u32> pi_idx(P, kNone), po_idx(P, kNone);
+  for (u32 k = 0; k < c->pi_pin.size(); ++k) pi_idx[c->pi_pin[k]] = k;
+  for (u32 k = 0; k < c->po_pin.size(); ++k) po_idx[c->po_pin[k]] = k;
+  std::vector<float> po_ld(P, 0.f);
+  for (u32 k = 0; k < c->po_pin.size(); ++k) po_ld[c->po_pin[k]] += c->po_load[k];
+
+  // endpoints in increasing user pin id
+  std::vector<u32> pin_ep(P, kNone);
+  std::vector<sta::EpRec> ep;
+  for (u32 p = 0; p < P; ++p) {
+    if (po_idx[p] == kNone && c->chk_of_pin[p] == kNone) continue;
+    sta::EpRec r;
+    r.po = po_idx[p];
+    r.chk_tab = c->chk_of_pin[p] == kNone ? kNone : c->chk_tab[c->chk_of_pin[p]];
+    pin_ep[c->int_of_user[p]] = (u32)ep.size();
+    ep.push_back(r);
+  }
+  c->n_ep = (u32)ep.size();
+  // stage-0 seeds
+  std::vector<u32> seed(c->n0, kNone);
+  for (u32 i = 0; i < c->n0; ++i) {
+    const u32 p = c->user_of_int[i];
+    if (c->pin_role[p] == STA_PIN_FF_CK) seed[i] = sta::kSeedClock;
+    else if (pi_idx[p] != kNone) seed[i] = pi_idx[p];
+  }
+  // static node caps (pin cap + PO load) and lumped net loads, in fp64 then
+  // rounded once
+  std::vector<float> scap(c->n_rc, 0.f);
+  for (u32 i = 0; i < c->n_rc; ++i) {
+    const u32 pin = c->rc_node_pin[i];
+    if (pin != kNone) scap[i] = (float)((double)c->pin_cap[pin] + (double)po_ld[pin]);
+  }
+  std::vector<float> lumped;
+  for (u32 i = 0; i < c->NP; ++i) {
+    const u32 n = c->pin_net[c->user_of_int[i]];
+    if (n == kNone) continue;
+    double sum = 0;
+    for (u32 x = c->net_ptr[n]; x < c->net_ptr[n + 1]; ++x) {
+      const u32 pin = c->net_pins[x];
+      sum += (double)c->pin_cap[pin] + (double)po_ld[pin];
+    }
+    lumped.push_back((float)sum);
+  }
+
+  cudaStream_t s = c->stream;
+  c->cons_arena.release();
+  Arena& g = c->cons_arena;
+  sta::Topo& t = c->topo;
+  t.n_ep = c->n_ep;
+  t.n_pi = (u32)c->pi_pin.size();
+  t.n_po = (u32)c->po_pin.size();
+  t.pin_ep = g.upload(pin_ep, s);
+  t.ep = g.upload(ep, s);
+  t.seed = g.upload(seed, s);
+  t.pi_at = reinterpret_cast<const float4*>(g.upload(c->pi_at, s));
+  t.pi_slew = reinterpret_cast<const float4*>(g.upload(c->pi_slew, s));
+  t.po_out_max = reinterpret_cast<const float2*>(g.upload(c->po_out_max, s));
+  t.po_out_min = reinterpret_cast<const float2*>(g.upload(c->po_out_min, s));
+  t.period = c->period;
+  t.clock_slew = c->clock_slew;
+  t.rc_scap = g.upload(scap, s);
+  t.net_lumped = g.upload(lumped, s);
+
+  // per-corner state buffers
+  for (CornerState& cs : c->corners) {
+    cs.state_arena.release();
+    Arena& a = cs.state_arena;
+    sta::CornerDev& d = cs.dev;
+    d.rec = a.alloc<float4>(2 * (size_t)P);
+    d.rat = a.alloc<float4>(P);
+    d.slack = a.alloc<float4>(P);
+    d.elm = a.alloc<float>(c->NS);
+    d.load = a.alloc<float>(c->NP);
+    d.ep_ws = a.alloc<float2>(c->n_ep);
+    d.res = a.alloc<double>(4);
+    d.scratch = a.alloc<double>(2 * (size_t)c->big_total);
+    d.err_flag = a.alloc<u32>(1);
+    ck(cudaMemsetAsync(d.load, 0, sizeof(float) * std::max<u32>(c->NP, 1), s), "memset");
+    ck(cudaMemsetAsync(d.err_flag, 0, sizeof(u32), s), "memset");
+  }
+  ck(cudaStreamSynchronize(s), "prepare upload");
+  c->prepared = true;
+}
+
+void enqueue_update(sta_ctx c) {
+  const sta::Topo& t = c->topo;
+  cudaStream_t s = c->stream;
+  u32 launches = 0;
+  prof_mark(c, 8);
+  for (CornerState& cs : c->corners) {
+    sta::CornerDev d = cs.dev;
+    d.rc_res = cs.rc_res;
+    d.rc_cap = cs.rc_cap;
+    prof_mark(c, 0);
+    ck(sta::launch_rc(t, d, 0, s), "rc kernel");
+    launches += (t.N ? 1 : 0) + (t.n_big ? 1 : 0);
+    prof_mark(c, 1);
+    prof_mark(c, 2);
+    ck(sta::launch_seed(t, d, c->n0, s), "seed kernel");
+    launches += c->n0 ? 1 : 0;
+    for (u32 st = 1; st <= c->S; ++st) {
+      // sinks of stage st-1 drivers, then pull pins of stage st (none for st == S)
+      const u32 a0 = c->sink_stage_ptr[st - 1], a1 = c->sink_stage_ptr[st];
+      const u32 b0 = st < c->S ? c->pull_stage_ptr[st] : 0;
+      const u32 b1 = st < c->S ? c->pull_stage_ptr[st + 1] : 0;
+      ck(sta::launch_fwd_stage(t, d, a0, a1 - a0, b0, b1 - b0, s), "forward kernel");
+      launches += (a1 - a0 + b1 - b0) ? 1 : 0;
+    }
+    prof_mark(c, 3);
+    prof_mark(c, 4);
+    for (u32 st = c->S; st-- > 0;) {
+      const u32 p0 = c->pull_stage_ptr[st], p1 = c->pull_stage_ptr[st + 1];
+      const u32 h0 = c->heavy_stage_ptr[st], h1 = c->heavy_stage_ptr[st + 1];
+      ck(sta::launch_bwd_stage(t, d, p0, p1 - p0, h0, h1 - h0, s), "backward kernel");
+      launches += (p1 - p0) ? 1 : 0;
+    }
+    prof_mark(c, 5);
+    prof_mark(c, 6);
+    ck(sta::launch_reduce(t, d, s), "reduce kernel");
+    launches += 1;
+    prof_mark(c, 7);
+    if (c->prof) {
+      // accumulate per phase (synchronous read of the event pairs)
+      ck(cudaEventSynchronize(c->ev[7]), "event sync");
+      for (int ph = 0; ph < 4; ++ph) {
+        float ms = 0;
+        ck(cudaEventElapsedTime(&ms, c->ev[2 * ph], c->ev[2 * ph + 1]), "elapsed");
+        c->profile.ms[ph] += ms;
+      }
+      c->profile.launches[0] += (t.N ? 1 : 0) + (t.n_big ? 1 : 0);
+      c->profile.launches[1] += c->S + (c->n0 ? 1 : 0);
+      c->profile.launches[2] += c->S;
+      c->profile.launches[3] += 1;
+    }
+  }
+  if (c->prof) {
+    ck(cudaEventRecord(c->ev[9], s), "cudaEventRecord");
+    ck(cudaEventSynchronize(c->ev[9]), "event sync");
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, c->ev[8], c->ev[9]), "elapsed");
+    c->profile.ms[4] += ms;
+    c->profile.launches[4] += launches;
+    c->profile.updates += 1;
+  }
+  c->launches_per_update = launches;
+}
+
+// device error flag check after a sync
+void check_flags(sta_ctx c) {
+  for (size_t k = 0; k < c->corners.size(); ++k) {
+    CornerState& cs = c->corners[k];
+    if (!cs.dev.err_flag) continue;
+    u32 f = 0;
+    ck(cudaMemcpy(&f, cs.dev.err_flag, sizeof f, cudaMemcpyDeviceToHost), "flag D2H");
+    if (f) {
+      ck(cudaMemset(cs.dev.err_flag, 0, sizeof f), "memset");
+      fail(STA_ERR_RC, "corner %zu: negative or non-finite RC value in the borrowed arrays", k);
+    }
+  }
+}
+
+template <class F>
+sta_status guard(sta_ctx c, F&& f) {
+  if (!c) return STA_ERR_ARG;
+  if (c->poisoned) {
+    return STA_ERR_CUDA;
+  }
+  try {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != c->device) ck(cudaSetDevice(c->device), "cudaSetDevice");
+    f();
+    c->err.clear();
+    return STA_OK;
+  } catch (const StaError& e) {
+    c->err = e.msg;
+    if (e.st == STA_ERR_CUDA) c->poisoned = true;
+    return e.st;
+  } catch (const std::bad_alloc&) {
+    c->err = "host allocation failed";
+    return STA_ERR_OOM;
+  }
+}
+
+CornerState& corner_of(sta_ctx c, u32 corner) {
+  if (corner >= c->K) fail(STA_ERR_ARG, "corner %u out of range (ctx has %u)", corner, c->K);
+  return c->corners[corner];
+}
+
+void require_updated(sta_ctx c) {
+  if (!c->prepared) fail(STA_ERR_ORDER, "no timing update has been run");
+}
+
+// copy a device buffer of n elements to the caller (host or device)
+template <class T>
+void deliver(sta_ctx c, T* dst, const T* dev_src, size_t n, sta_mem mem) {
+  if (!n) return;
+  if (mem == STA_MEM_DEVICE) {
+    ck(cudaMemcpyAsync(dst, dev_src, n * sizeof(T), cudaMemcpyDeviceToDevice, c->stream), "D2D");
+  } else if (mem == STA_MEM_HOST) {
+    ck(cudaMemcpyAsync(dst, dev_src, n * sizeof(T), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  } else {
+    fail(STA_ERR_ARG, "bad sta_mem %d", (int)mem);
+  }
+}
+
+// gather float4 per user pin into the caller buffer
+void deliver_pins(sta_ctx c, float* dst, const float4* src, u32 stride, sta_mem mem) {
+  if (!dst || !c->P) return;
+  const u32 P = c->P;
+  float4* out;
+  if (mem == STA_MEM_DEVICE) {
+    out = reinterpret_cast<float4*>(dst);
+  } else {
+    c->tmp_arena.release();
+    out = c->tmp_arena.alloc<float4>(P);
+  }
+  ck(sta::launch_gather4(src, c->topo.int_of_user, out, P, stride, c->stream), "gather kernel");
+  if (mem != STA_MEM_DEVICE) deliver(c, reinterpret_cast<float4*>(dst), out, P, STA_MEM_HOST);
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+const char* sta_status_string(sta_status st) {
+  switch (st) {
+    case STA_OK: return "STA_OK";
+    case STA_ERR_ARG: return "STA_ERR_ARG";
+    case STA_ERR_CSR: return "STA_ERR_CSR";
+    case STA_ERR_ID: return "STA_ERR_ID";
+    case STA_ERR_MULTIDRIVER: return "STA_ERR_MULTIDRIVER";
+    case STA_ERR_CYCLE: return "STA_ERR_CYCLE";
+    case STA_ERR_LUT: return "STA_ERR_LUT";
+    case STA_ERR_RC: return "STA_ERR_RC";
+    case STA_ERR_ORDER: return "STA_ERR_ORDER";
+    case STA_ERR_CUDA: return "STA_ERR_CUDA";
+    case STA_ERR_OOM: return "STA_ERR_OOM";
+  }
+  return "STA_ERR_UNKNOWN";
+}
+
+sta_status sta_create(int cuda_device, uint32_t num_corners, void* cuda_stream, sta_ctx* out) {
+  if (!out || num_corners == 0) return STA_ERR_ARG;
+  *out = nullptr;
+  sta_ctx c = new (std::nothrow) sta_ctx_s;
+  if (!c) return STA_ERR_OOM;
+  c->device = cuda_device;
+  c->K = num_corners;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev) {
+    delete c;
+    return ndev == 0 ? STA_ERR_CUDA : STA_ERR_ARG;
+  }
+  if (cudaSetDevice(cuda_device) != cudaSuccess) { delete c; return STA_ERR_CUDA; }
+  if (cuda_stream) {
+    c->stream = static_cast<cudaStream_t>(cuda_stream);
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) { delete c; return STA_ERR_CUDA; }
+    c->own_stream = true;
+  }
+  for (auto& e : c->ev)
+    if (cudaEventCreate(&e) != cudaSuccess) { delete c; return STA_ERR_CUDA; }
+  c->corners.resize(num_corners);
+  *out = c;
+  return STA_OK;
+}
+
+sta_status sta_destroy(sta_ctx c) {
+  if (!c) return STA_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  c->graph_arena.release();
+  c->tree_arena.release();
+  c->cons_arena.release();
+  c->tmp_arena.release();
+  for (CornerState& cs : c->corners) {
+    cs.lib_arena.release();
+    cs.rc_arena.release();
+    cs.state_arena.release();
+  }
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return STA_OK;
+}
+
+const char* sta_last_error(sta_ctx c) { return c ? c->err.c_str() : "null ctx"; }
+
+sta_status sta_load_graph(sta_ctx c, const sta_graph_desc* d) {
+  return guard(c, [&] {
+    if (!d) fail(STA_ERR_ARG, "desc is NULL");
+    c->has_graph = c->has_tree = c->has_cons = c->prepared = false;
+    for (CornerState& cs : c->corners) { cs.lib = false; cs.rcv = false; }
+    c->graph_arena.release();
+    c->tree_arena.release();
+    c->cons_arena.release();
+    c->P = d->num_pins; c->N = d->num_nets; c->A = d->num_arcs; c->C = d->num_checks; c->T = d->num_tables;
+    c->pin_cap = fetch(d->pin_cap, c->P, d->mem, "pin_cap");
+    c->pin_role = fetch(d->pin_role, c->P, d->mem, "pin_role");
+    c->net_ptr = fetch(d->net_ptr, c->N ? c->N + 1 : 0, d->mem, "net_ptr");
+    const u32 nnp = c->N ? c->net_ptr[c->N] : 0;
+    c->net_pins = fetch(d->net_pins, nnp, d->mem, "net_pins");
+    c->arc_from = fetch(d->arc_from, c->A, d->mem, "arc_from");
+    c->arc_to = fetch(d->arc_to, c->A, d->mem, "arc_to");
+    c->arc_sense = fetch(d->arc_sense, c->A, d->mem, "arc_sense");
+    c->arc_tab = fetch(d->arc_tab, c->A, d->mem, "arc_tab");
+    c->chk_d = fetch(d->chk_d, c->C, d->mem, "chk_d");
+    c->chk_ck = fetch(d->chk_ck, c->C, d->mem, "chk_ck");
+    c->chk_tab = fetch(d->chk_tab, c->C, d->mem, "chk_tab");
+    validate_graph(c);
+    build_plan(c);
+    c->has_graph = true;
+  });
+}
+
+sta_status sta_set_library(sta_ctx c, uint32_t corner, sta_mem mem, uint32_t num_tables, const uint8_t* n1,
+                           const uint8_t* n2, const uint32_t* off, const float* data, uint32_t data_len) {
+  return guard(c, [&] {
+    CornerState& cs = corner_of(c, corner);
+    if (!c->has_graph) fail(STA_ERR_ORDER, "sta_set_library before sta_load_graph");
+    if (num_tables != c->T) fail(STA_ERR_ARG, "library has %u tables, graph expects %u", num_tables, c->T);
+    auto h1 = fetch(n1, num_tables, mem, "n1");
+    auto h2 = fetch(n2, num_tables, mem, "n2");
+    auto ho = fetch(off, num_tables, mem, "off");
+    auto hd = fetch(data, data_len, mem, "data");
+    if (data_len >= (1u << 26)) fail(STA_ERR_LUT, "table pool too large (%u floats)", data_len);
+    std::vector<u32> tdesc(num_tables);
+    for (u32 t = 0; t < num_tables; ++t) {
+      const u32 a = h1[t], b = h2[t];
+      if (a < 1 || a > 8 || b < 1 || b > 8) fail(STA_ERR_LUT, "table %u: size %ux%u outside 1..8", t, a, b);
+      if ((uint64_t)ho[t] + a + b + (uint64_t)a * b > data_len) fail(STA_ERR_LUT, "table %u: data out of range", t);
+      const float* x = hd.data() + ho[t];
+      for (u32 k = 0; k < a + b + a * b; ++k)
+        if (!std::isfinite(x[k])) fail(STA_ERR_LUT, "table %u: non-finite entry %u", t, k);
+      for (u32 k = 1; k < a; ++k)
+        if (!(x[k] > x[k - 1])) fail(STA_ERR_LUT, "table %u: index_1 not strictly ascending", t);
+      for (u32 k = 1; k < b; ++k)
+        if (!(x[a + k] > x[a + k - 1])) fail(STA_ERR_LUT, "table %u: index_2 not strictly ascending", t);
+      tdesc[t] = sta::pack_tdesc(ho[t], a, b);
+    }
+    cs.lib_arena.release();
+    cs.dev.lut = cs.lib_arena.upload(hd, c->stream);
+    cs.dev.tdesc = cs.lib_arena.upload(tdesc, c->stream);
+    ck(cudaStreamSynchronize(c->stream), "library upload");
+    cs.n_tables = num_tables;
+    cs.lib = true;
+  });
+}
+
+sta_status sta_set_rc_tree(sta_ctx c, sta_mem mem, const uint32_t* rc_ptr, uint32_t num_nodes,
+                           const int32_t* parent, const uint32_t* node_pin) {
+  return guard(c, [&] {
+    if (!c->has_graph) fail(STA_ERR_ORDER, "sta_set_rc_tree before sta_load_graph");
+    c->has_tree = false;
+    c->prepared = false;
+    for (CornerState& cs : c->corners) cs.rcv = false;
+    c->n_rc = num_nodes;
+    c->rc_ptr = fetch(rc_ptr, c->N + 1, mem, "rc_ptr");
+    c->rc_parent = fetch(parent, num_nodes, mem, "parent");
+    c->rc_node_pin = fetch(node_pin, num_nodes, mem, "node_pin");
+    build_rc(c);
+    c->has_tree = true;
+  });
+}
+
+sta_status sta_set_rc_values(sta_ctx c, uint32_t corner, sta_mem mem, const float* res, const float* cap) {
+  return guard(c, [&] {
+    CornerState& cs = corner_of(c, corner);
+    if (!c->has_tree) fail(STA_ERR_ORDER, "sta_set_rc_values before sta_set_rc_tree");
+    if (c->n_rc && (!res || !cap)) fail(STA_ERR_ARG, "res/cap NULL");
+    if (mem == STA_MEM_DEVICE) {
+      cs.rc_arena.release();
+      cs.rc_res = res;
+      cs.rc_cap = cap;
+    } else if (mem == STA_MEM_HOST) {
+      for (u32 i = 0; i < c->n_rc; ++i) {
+        if (!(res[i] >= 0.f) || !std::isfinite(res[i])) fail(STA_ERR_RC, "node %u: bad resistance", i);
+        if (!(cap[i] >= 0.f) || !std::isfinite(cap[i])) fail(STA_ERR_RC, "node %u: bad capacitance", i);
+      }
+      if (!cs.rc_arena.ptrs.empty() && cs.rc_res && cs.rc_arena.bytes >= 2ull * c->n_rc * sizeof(float)) {
+        // reuse owned buffers
+      } else {
+        cs.rc_arena.release();
+        float* r = cs.rc_arena.alloc<float>(c->n_rc);
+        float* k = cs.rc_arena.alloc<float>(c->n_rc);
+        cs.rc_res = r;
+        cs.rc_cap = k;
+      }
+      if (c->n_rc) {
+        ck(cudaMemcpyAsync(const_cast<float*>(cs.rc_res), res, sizeof(float) * c->n_rc, cudaMemcpyHostToDevice,
+                           c->stream), "H2D");
+        ck(cudaMemcpyAsync(const_cast<float*>(cs.rc_cap), cap, sizeof(float) * c->n_rc, cudaMemcpyHostToDevice,
+                           c->stream), "H2D");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+      }
+    } else {
+      fail(STA_ERR_ARG, "bad sta_mem %d", (int)mem);
+    }
+    cs.rcv = true;
+  });
+}
+
+sta_status sta_set_constraints(sta_ctx c, const sta_constraints* k) {
+  return guard(c, [&] {
+    if (!k) fail(STA_ERR_ARG, "constraints NULL");
+    if (!c->has_graph) fail(STA_ERR_ORDER, "sta_set_constraints before sta_load_graph");
+    if (!(k->period_ps > 0.f) || !std::isfinite(k->period_ps)) fail(STA_ERR_ARG, "period must be > 0");
+    if (!(k->clock_slew_ps >= 0.f) || !std::isfinite(k->clock_slew_ps)) fail(STA_ERR_ARG, "clock slew must be >= 0");
+    auto pi_pin = fetch(k->pi_pin, k->n_pi, k->mem, "pi_pin");
+    auto pi_at = fetch(k->pi_at, 4ull * k->n_pi, k->mem, "pi_at");
+    auto pi_slew = fetch(k->pi_slew, 4ull * k->n_pi, k->mem, "pi_slew");
+    auto po_pin = fetch(k->po_pin, k->n_po, k->mem, "po_pin");
+    auto po_max = fetch(k->po_out_max, 2ull * k->n_po, k->mem, "po_out_max");
+    auto po_min = fetch(k->po_out_min, 2ull * k->n_po, k->mem, "po_out_min");
+    auto po_ld = fetch(k->po_load_ff, k->n_po, k->mem, "po_load_ff");
+    std::vector<uint8_t> seen(c->P, 0);
+    for (u32 i = 0; i < k->n_pi; ++i) {
+      const u32 p = pi_pin[i];
+      if (p >= c->P) fail(STA_ERR_ID, "pi %u: pin id %u out of range", i, p);
+      if (c->pin_role[p] != STA_PIN_PI) fail(STA_ERR_ARG, "pi %u: pin %u does not have role PI", i, p);
+      if (seen[p]++) fail(STA_ERR_ARG, "pi %u: pin %u listed twice", i, p);
+      for (int q = 0; q < 4; ++q)
+        if (!std::isfinite(pi_at[4 * i + q]) || !std::isfinite(pi_slew[4 * i + q]) || pi_slew[4 * i + q] < 0)
+          fail(STA_ERR_ARG, "pi %u: non-finite arrival or bad slew", i);
+    }
+    std::fill(seen.begin(), seen.end(), 0);
+    for (u32 i = 0; i < k->n_po; ++i) {
+      const u32 p = po_pin[i];
+      if (p >= c->P) fail(STA_ERR_ID, "po %u: pin id %u out of range", i, p);
+      if (c->pin_role[p] != STA_PIN_PO) fail(STA_ERR_ARG, "po %u: pin %u does not have role PO", i, p);
+      if (seen[p]++) fail(STA_ERR_ARG, "po %u: pin %u listed twice", i, p);
+      if (!std::isfinite(po_max[2 * i]) || !std::isfinite(po_max[2 * i + 1]) || !std::isfinite(po_min[2 * i]) ||
+          !std::isfinite(po_min[2 * i + 1]) || !(po_ld[i] >= 0.f) || !std::isfinite(po_ld[i]))
+        fail(STA_ERR_ARG, "po %u: non-finite output delay or bad load", i);
+    }
+    c->period = k->period_ps;
+    c->clock_slew = k->clock_slew_ps;
+    c->pi_pin = std::move(pi_pin);
+    c->pi_at = std::move(pi_at);
+    c->pi_slew = std::move(pi_slew);
+    c->po_pin = std::move(po_pin);
+    c->po_out_max = std::move(po_max);
+    c->po_out_min = std::move(po_min);
+    c->po_load = std::move(po_ld);
+    c->has_cons = true;
+    c->prepared = false;
+  });
+}
+
+sta_status sta_update_timing(sta_ctx c) {
+  return guard(c, [&] {
+    if (!c->has_graph) fail(STA_ERR_ORDER, "sta_update_timing before sta_load_graph");
+    if (!c->has_tree) fail(STA_ERR_ORDER, "sta_update_timing before sta_set_rc_tree");
+    if (!c->has_cons) fail(STA_ERR_ORDER, "sta_update_timing before sta_set_constraints");
+    for (u32 k = 0; k < c->K; ++k) {
+      if (!c->corners[k].lib) fail(STA_ERR_ORDER, "corner %u: no library", k);
+      if (!c->corners[k].rcv) fail(STA_ERR_ORDER, "corner %u: no RC values", k);
+    }
+    prepare(c);
+    enqueue_update(c);
+  });
+}
+
+sta_status sta_synchronize(sta_ctx c) {
+  return guard(c, [&] {
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    check_flags(c);
+  });
+}
+
+sta_status sta_report_slack(sta_ctx c, uint32_t corner, double* res4, float* pin_slack, sta_mem mem) {
+  return guard(c, [&] {
+    CornerState& cs = corner_of(c, corner);
+    require_updated(c);
+    if (res4) {
+      deliver(c, res4, cs.dev.res, 4, mem);
+      if (mem == STA_MEM_HOST) check_flags(c);
+    }
+    deliver_pins(c, pin_slack, cs.dev.slack, 1, mem);
+  });
+}
+
+sta_status sta_get_timing(sta_ctx c, uint32_t corner, float* at, float* slew, float* rat, sta_mem mem) {
+  return guard(c, [&] {
+    CornerState& cs = corner_of(c, corner);
+    require_updated(c);
+    deliver_pins(c, at, cs.dev.rec, 2, mem);
+    deliver_pins(c, slew, cs.dev.rec + 1, 2, mem);
+    deliver_pins(c, rat, cs.dev.rat, 1, mem);
+  });
+}
+
+sta_status sta_get_rc(sta_ctx c, uint32_t corner, float* net_load, float* pin_elm, sta_mem mem) {
+  return guard(c, [&] {
+    CornerState& cs = corner_of(c, corner);
+    require_updated(c);
+    float* nl = net_load;
+    float* pe = pin_elm;
+    if (mem == STA_MEM_HOST) {
+      c->tmp_arena.release();
+      nl = net_load ? c->tmp_arena.alloc<float>(c->N) : nullptr;
+      pe = pin_elm ? c->tmp_arena.alloc<float>(c->P) : nullptr;
+    } else if (mem != STA_MEM_DEVICE) {
+      fail(STA_ERR_ARG, "bad sta_mem %d", (int)mem);
+    }
+    Arena tmp;
+    const u32* dn = tmp.upload(c->drv_of_net, c->stream);
+    ck(sta::launch_gather_rc(c->topo, cs.dev, nl, pe, dn, nullptr, c->stream), "gather rc");
+    if (mem == STA_MEM_HOST) {
+      if (net_load) deliver(c, net_load, nl, c->N, STA_MEM_HOST);
+      if (pin_elm) deliver(c, pin_elm, pe, c->P, STA_MEM_HOST);
+    }
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    tmp.release();
+  });
+}
+
+sta_status sta_get_levels(sta_ctx c, uint32_t* level, uint32_t* perm, uint32_t* num_levels, sta_mem mem) {
+  return guard(c, [&] {
+    if (!c->has_graph) fail(STA_ERR_ORDER, "sta_get_levels before sta_load_graph");
+    if (num_levels) *num_levels = c->num_levels;
+    auto put = [&](uint32_t* dst, const std::vector<u32>& v) {
+      if (!dst || v.empty()) return;
+      if (mem == STA_MEM_HOST) std::memcpy(dst, v.data(), v.size() * sizeof(u32));
+      else ck(cudaMemcpy(dst, v.data(), v.size() * sizeof(u32), cudaMemcpyHostToDevice), "H2D");
+    };
+    put(level, c->level);
+    put(perm, c->perm);
+  });
+}
+
+sta_status sta_get_info(sta_ctx c, sta_info* o) {
+  return guard(c, [&] {
+    if (!o) fail(STA_ERR_ARG, "out NULL");
+    std::memset(o, 0, sizeof *o);
+    o->num_pins = c->P;
+    o->num_nets = c->N;
+    o->num_net_arcs = c->N ? c->net_ptr[c->N] - c->N : 0;
+    o->num_cell_arcs = c->A;
+    o->num_checks = c->C;
+    o->num_endpoints = c->n_ep;
+    o->num_levels = c->num_levels;
+    o->num_stages = c->S;
+    o->num_pull_pins = c->NP;
+    o->num_sink_pins = c->NS;
+    o->num_heavy_drivers = c->n_heavy;
+    o->kernels_per_update = c->launches_per_update;
+    uint64_t b = c->graph_arena.bytes + c->tree_arena.bytes + c->cons_arena.bytes;
+    for (auto& cs : c->corners) b += cs.lib_arena.bytes + cs.rc_arena.bytes + cs.state_arena.bytes;
+    o->device_bytes = b;
+  });
+}
+
+sta_status sta_profile_enable(sta_ctx c, int enable) {
+  return guard(c, [&] {
+    c->prof = enable != 0;
+    if (c->prof) std::memset(&c->profile, 0, sizeof c->profile);
+  });
+}
+
+sta_status sta_profile_read(sta_ctx c, sta_profile* out) {
+  return guard(c, [&] {
+    if (!out) fail(STA_ERR_ARG, "out NULL");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    *out = c->profile;
+  });
+}
+
+}  // extern "C"

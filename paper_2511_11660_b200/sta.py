@@ -1,0 +1,336 @@
+"""Thin ctypes binding of include/sta.h (argument marshalling only).
+
+Every function here forwards to the same-named C entry point of libsta.so;
+no step of the timing update runs in Python.  Arrays may be numpy (host) or
+torch CUDA tensors (device, zero-copy: their data_ptr() is passed with
+STA_MEM_DEVICE).  There is no CPU fallback: if libsta.so is missing or no
+CUDA device is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libsta.so")
+
+STA_MEM_HOST, STA_MEM_DEVICE = 0, 1
+STATUS = ["STA_OK", "STA_ERR_ARG", "STA_ERR_CSR", "STA_ERR_ID", "STA_ERR_MULTIDRIVER",
+          "STA_ERR_CYCLE", "STA_ERR_LUT", "STA_ERR_RC", "STA_ERR_ORDER", "STA_ERR_CUDA",
+          "STA_ERR_OOM"]
+NUM_PHASES = 5
+PHASES = ["rc", "forward", "backward", "reduce", "update"]
+
+EXPORTS = ["sta_create", "sta_destroy", "sta_last_error", "sta_status_string", "sta_load_graph",
+           "sta_set_library", "sta_set_rc_tree", "sta_set_rc_values", "sta_set_constraints",
+           "sta_update_timing", "sta_report_slack", "sta_get_timing", "sta_get_rc",
+           "sta_get_levels", "sta_get_info", "sta_synchronize", "sta_profile_enable",
+           "sta_profile_read"]
+
+
+class StaError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        self.name = STATUS[status] if 0 <= status < len(STATUS) else f"status {status}"
+        super().__init__(f"{self.name}: {msg}")
+
+
+class GraphDesc(C.Structure):
+    _fields_ = [("mem", C.c_int), ("num_pins", C.c_uint32), ("pin_cap", C.c_void_p),
+                ("pin_role", C.c_void_p), ("num_nets", C.c_uint32), ("net_ptr", C.c_void_p),
+                ("net_pins", C.c_void_p), ("num_arcs", C.c_uint32), ("arc_from", C.c_void_p),
+                ("arc_to", C.c_void_p), ("arc_sense", C.c_void_p), ("arc_tab", C.c_void_p),
+                ("num_checks", C.c_uint32), ("chk_d", C.c_void_p), ("chk_ck", C.c_void_p),
+                ("chk_tab", C.c_void_p), ("num_tables", C.c_uint32)]
+
+
+class ConstraintsDesc(C.Structure):
+    _fields_ = [("mem", C.c_int), ("period_ps", C.c_float), ("clock_slew_ps", C.c_float),
+                ("n_pi", C.c_uint32), ("pi_pin", C.c_void_p), ("pi_at", C.c_void_p),
+                ("pi_slew", C.c_void_p), ("n_po", C.c_uint32), ("po_pin", C.c_void_p),
+                ("po_out_max", C.c_void_p), ("po_out_min", C.c_void_p),
+                ("po_load_ff", C.c_void_p)]
+
+
+class Info(C.Structure):
+    _fields_ = [(n, C.c_uint32) for n in (
+        "num_pins", "num_nets", "num_net_arcs", "num_cell_arcs", "num_checks", "num_endpoints",
+        "num_levels", "num_stages", "num_pull_pins", "num_sink_pins", "num_heavy_drivers",
+        "kernels_per_update")] + [("device_bytes", C.c_uint64)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+class Profile(C.Structure):
+    _fields_ = [("ms", C.c_double * NUM_PHASES), ("launches", C.c_uint32 * NUM_PHASES),
+                ("updates", C.c_uint32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libsta.so (built by paper_2511_11660_b200.build / __graft_entry__.build)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, u32, i32 = C.c_void_p, C.c_uint32, C.c_int
+        sig = {
+            "sta_create": (i32, [i32, u32, vp, C.POINTER(vp)]),
+            "sta_destroy": (i32, [vp]),
+            "sta_last_error": (C.c_char_p, [vp]),
+            "sta_status_string": (C.c_char_p, [i32]),
+            "sta_load_graph": (i32, [vp, C.POINTER(GraphDesc)]),
+            "sta_set_library": (i32, [vp, u32, i32, u32, vp, vp, vp, vp, u32]),
+            "sta_set_rc_tree": (i32, [vp, i32, vp, u32, vp, vp]),
+            "sta_set_rc_values": (i32, [vp, u32, i32, vp, vp]),
+            "sta_set_constraints": (i32, [vp, C.POINTER(ConstraintsDesc)]),
+            "sta_update_timing": (i32, [vp]),
+            "sta_report_slack": (i32, [vp, u32, vp, vp, i32]),
+            "sta_get_timing": (i32, [vp, u32, vp, vp, vp, i32]),
+            "sta_get_rc": (i32, [vp, u32, vp, vp, i32]),
+            "sta_get_levels": (i32, [vp, vp, vp, vp, i32]),
+            "sta_get_info": (i32, [vp, C.POINTER(Info)]),
+            "sta_synchronize": (i32, [vp]),
+            "sta_profile_enable": (i32, [vp, i32]),
+            "sta_profile_read": (i32, [vp, C.POINTER(Profile)]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _is_torch_cuda(x) -> bool:
+    return hasattr(x, "is_cuda") and hasattr(x, "data_ptr") and bool(x.is_cuda)
+
+
+class _Args:
+    """Marshals a group of arrays that must share one memory kind."""
+
+    def __init__(self):
+        self.keep = []
+        self.mem = None
+
+    def ptr(self, x, dtype):
+        if x is None:
+            return None
+        if _is_torch_cuda(x):
+            self._kind(STA_MEM_DEVICE)
+            x = x.contiguous()
+            self.keep.append(x)
+            return x.data_ptr() if x.numel() else None
+        self._kind(STA_MEM_HOST)
+        a = np.ascontiguousarray(np.asarray(x, dtype=dtype))
+        self.keep.append(a)
+        return a.ctypes.data if a.size else None
+
+    def _kind(self, k):
+        if self.mem is None:
+            self.mem = k
+        elif self.mem != k:
+            raise ValueError("mixing host and device arrays in one call")
+
+    @property
+    def kind(self):
+        return STA_MEM_HOST if self.mem is None else self.mem
+
+
+class Context:
+    """One sta_ctx: a design loaded on one GPU for `num_corners` corners."""
+
+    def __init__(self, device: int = 0, num_corners: int = 1, stream: Optional[int] = None):
+        self._L = lib()
+        h = C.c_void_p()
+        st = self._L.sta_create(int(device), int(num_corners), stream, C.byref(h))
+        if st:
+            raise StaError(st, "sta_create failed (no CUDA device?)")
+        self.h = h
+        self.num_corners = num_corners
+        self.num_pins = 0
+        self.num_nets = 0
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._L.sta_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _check(self, st):
+        if st:
+            raise StaError(st, self._L.sta_last_error(self.h).decode())
+
+    # ------------------------------------------------------------ inputs
+    def load_graph(self, pin_cap, pin_role, net_ptr, net_pins, arc_from, arc_to, arc_sense,
+                   arc_tab, chk_d, chk_ck, chk_tab, num_tables: int):
+        a = _Args()
+        d = GraphDesc()
+        d.num_pins = len(pin_cap)
+        d.pin_cap = a.ptr(pin_cap, np.float32)
+        d.pin_role = a.ptr(pin_role, np.uint8)
+        d.num_nets = max(len(net_ptr) - 1, 0)
+        d.net_ptr = a.ptr(net_ptr, np.uint32)
+        d.net_pins = a.ptr(net_pins, np.uint32)
+        d.num_arcs = len(arc_from)
+        d.arc_from = a.ptr(arc_from, np.uint32)
+        d.arc_to = a.ptr(arc_to, np.uint32)
+        d.arc_sense = a.ptr(arc_sense, np.uint8)
+        d.arc_tab = a.ptr(arc_tab, np.uint32)
+        d.num_checks = len(chk_d)
+        d.chk_d = a.ptr(chk_d, np.uint32)
+        d.chk_ck = a.ptr(chk_ck, np.uint32)
+        d.chk_tab = a.ptr(chk_tab, np.uint32)
+        d.num_tables = int(num_tables)
+        d.mem = a.kind
+        self._check(self._L.sta_load_graph(self.h, C.byref(d)))
+        self.num_pins, self.num_nets = d.num_pins, d.num_nets
+
+    def set_library(self, corner: int, n1, n2, off, data):
+        a = _Args()
+        p = [a.ptr(n1, np.uint8), a.ptr(n2, np.uint8), a.ptr(off, np.uint32), a.ptr(data, np.float32)]
+        self._check(self._L.sta_set_library(self.h, int(corner), a.kind, len(n1), *p, len(data)))
+
+    def set_rc_tree(self, rc_ptr, parent, node_pin):
+        a = _Args()
+        p = [a.ptr(rc_ptr, np.uint32), None, a.ptr(parent, np.int32), a.ptr(node_pin, np.uint32)]
+        self._check(self._L.sta_set_rc_tree(self.h, a.kind, p[0], len(parent), p[2], p[3]))
+
+    def set_rc_values(self, corner: int, res, cap):
+        """Device tensors are BORROWED until the next update completes."""
+        a = _Args()
+        pr, pc = a.ptr(res, np.float32), a.ptr(cap, np.float32)
+        self._borrowed = getattr(self, "_borrowed", {})
+        self._borrowed[corner] = a.keep       # keep torch tensors alive
+        self._check(self._L.sta_set_rc_values(self.h, int(corner), a.kind, pr, pc))
+
+    def set_constraints(self, period, clock_slew, pi_pin, pi_at, pi_slew, po_pin, po_out_max,
+                        po_out_min, po_load):
+        a = _Args()
+        k = ConstraintsDesc()
+        k.period_ps = float(period)
+        k.clock_slew_ps = float(clock_slew)
+        k.n_pi = len(pi_pin)
+        k.pi_pin = a.ptr(pi_pin, np.uint32)
+        k.pi_at = a.ptr(pi_at, np.float32)
+        k.pi_slew = a.ptr(pi_slew, np.float32)
+        k.n_po = len(po_pin)
+        k.po_pin = a.ptr(po_pin, np.uint32)
+        k.po_out_max = a.ptr(po_out_max, np.float32)
+        k.po_out_min = a.ptr(po_out_min, np.float32)
+        k.po_load_ff = a.ptr(po_load, np.float32)
+        k.mem = a.kind
+        self._check(self._L.sta_set_constraints(self.h, C.byref(k)))
+
+    # ------------------------------------------------------------ update
+    def update_timing(self):
+        self._check(self._L.sta_update_timing(self.h))
+
+    def synchronize(self):
+        self._check(self._L.sta_synchronize(self.h))
+
+    # ----------------------------------------------------------- reports
+    def report_slack(self, corner: int = 0, pin_slack=None, want_pins: bool = False):
+        """-> (res4 numpy f64 [WNS_s, TNS_s, WNS_h, TNS_h], pin slack or None).
+        pin_slack: optional torch CUDA tensor [P,4] f32 to fill (device);
+        want_pins: return a host numpy [P,4] array instead."""
+        if pin_slack is not None:
+            # device outputs: res4 is returned as a torch float64 CUDA tensor
+            import torch
+            res_d = torch.empty(4, dtype=torch.float64, device=pin_slack.device)
+            self._check(self._L.sta_report_slack(self.h, corner, res_d.data_ptr(),
+                                                 pin_slack.data_ptr(), STA_MEM_DEVICE))
+            return res_d, pin_slack
+        res = np.zeros(4, np.float64)
+        out = np.zeros((self.num_pins, 4), np.float32) if want_pins else None
+        self._check(self._L.sta_report_slack(self.h, corner, res.ctypes.data,
+                                             out.ctypes.data if want_pins and out.size else None,
+                                             STA_MEM_HOST))
+        return res, out
+
+    def report_wns_tns_device(self, corner: int, out):
+        """Stream-ordered copy of {WNS_s, TNS_s, WNS_h, TNS_h} into a float64 CUDA tensor view."""
+        self._check(self._L.sta_report_slack(self.h, corner, out.data_ptr(), None, STA_MEM_DEVICE))
+
+    def get_timing(self, corner: int = 0):
+        P = self.num_pins
+        at, slew, rat = (np.zeros((P, 4), np.float32) for _ in range(3))
+        if P:
+            self._check(self._L.sta_get_timing(self.h, corner, at.ctypes.data, slew.ctypes.data,
+                                               rat.ctypes.data, STA_MEM_HOST))
+        return at, slew, rat
+
+    def get_rc(self, corner: int = 0):
+        load = np.zeros(self.num_nets, np.float32)
+        elm = np.zeros(self.num_pins, np.float32)
+        self._check(self._L.sta_get_rc(self.h, corner, load.ctypes.data if load.size else None,
+                                       elm.ctypes.data if elm.size else None, STA_MEM_HOST))
+        return load, elm
+
+    def get_levels(self):
+        P = self.num_pins
+        level = np.zeros(P, np.uint32)
+        perm = np.zeros(P, np.uint32)
+        nl = C.c_uint32()
+        self._check(self._L.sta_get_levels(self.h, level.ctypes.data if P else None,
+                                           perm.ctypes.data if P else None, C.byref(nl),
+                                           STA_MEM_HOST))
+        return level, perm, nl.value
+
+    def info(self) -> dict:
+        i = Info()
+        self._check(self._L.sta_get_info(self.h, C.byref(i)))
+        return i.as_dict()
+
+    def profile_enable(self, on: bool = True):
+        self._check(self._L.sta_profile_enable(self.h, 1 if on else 0))
+
+    def profile_read(self) -> dict:
+        p = Profile()
+        self._check(self._L.sta_profile_read(self.h, C.byref(p)))
+        return dict(ms={PHASES[i]: p.ms[i] for i in range(NUM_PHASES)},
+                    launches={PHASES[i]: p.launches[i] for i in range(NUM_PHASES)},
+                    updates=p.updates)
+
+
+# ---------------------------------------------------------------- helpers
+def load_design(ctx: Context, d, corners=None, device_rc: bool = False):
+    """Load a synth.Design (netlist, libraries, RC, constraints) into ctx.
+    corners: which design corners map to ctx corners 0..K-1 (default all)."""
+    ctx.load_graph(d.pin_cap, d.pin_role, d.net_ptr, d.net_pins, d.arc_from, d.arc_to,
+                   d.arc_sense, d.arc_tab, d.chk_d, d.chk_ck, d.chk_tab, d.libs[0].num_tables)
+    corners = list(range(ctx.num_corners)) if corners is None else list(corners)
+    for k, c in enumerate(corners):
+        L = d.libs[c]
+        ctx.set_library(k, L.n1, L.n2, L.off, L.data)
+    rc0 = d.rc[corners[0]]
+    ctx.set_rc_tree(rc0.rc_ptr, rc0.parent, rc0.node_pin)
+    for k, c in enumerate(corners):
+        rc = d.rc[c]
+        if device_rc:
+            import torch
+            ctx.set_rc_values(k, torch.from_numpy(rc.res).cuda(), torch.from_numpy(rc.cap).cuda())
+        else:
+            ctx.set_rc_values(k, rc.res, rc.cap)
+    k = d.cons
+    ctx.set_constraints(k.period, k.clock_slew, k.pi_pin, k.pi_at, k.pi_slew, k.po_pin,
+                        k.po_out_max, k.po_out_min, k.po_load)

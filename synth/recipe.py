@@ -14,7 +14,8 @@ Recipe, all vectorised numpy, deterministic for a seed:
   every depth populated; input 0 of a depth-d cell is driven from depth d-1
   (so pin levels ~ 2D+2), other inputs from any depth < d; endpoints (D pins,
   POs) absorb any leftover driver slots.
-* Optional high-fan-out nets (superblue-like): PIs with log-uniform fan-out.
+* Optional high-fan-out nets (superblue-like): PIs with log-uniform fan-out,
+  wire R scaled by 0.1 (thick upper-layer routing).
 * RC: random recursive tree per net, driver = node 0, one node per sink plus
   floor(k/2) Steiner nodes, R U[0.02,0.2] kOhm, Cw U[0.1,1.0] fF.
 * Constraints: PI AT U[0,50] ps, slew U[5,40] ps, output delays U[0,50],
@@ -324,6 +325,11 @@ def generate(n_cells: int, levels: int, seed: int, n_hfn: int = 0,
     res = rng.uniform(0.02, 0.2, n_rc).astype(np.float32)
     res[local == 0] = 0.0
     cap = rng.uniform(0.1, 1.0, n_rc).astype(np.float32)
+    if n_hfn > 0:
+        # high-fan-out nets are routed on thick upper layers: 10x lower unit R
+        hfn_net = np.nonzero(net_drv < n_hfn)[0]       # PI pins 0..n_hfn-1 drive them
+        node_net = np.repeat(np.arange(N), n_nodes)
+        res[np.isin(node_net, hfn_net)] *= np.float32(0.1)
 
     # ---- constraints ----
     pi_L = rng.uniform(0, 50, (n_pi, 2))
