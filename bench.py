@@ -177,7 +177,10 @@ def main():
     from paper_2511_11660_b200 import build as pbuild
     pbuild.build()
 
-    stream = torch.cuda.current_stream()
+    # one dedicated stream carries the STA kernels, the NCCL allreduce and the
+    # timing events (the legacy default stream cannot be shared by handle)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     t0 = time.perf_counter()
     d = corner_design(args.config, rank)
     gen_s = time.perf_counter() - t0

@@ -9,6 +9,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
+#include <limits>
 #include <new>
 #include <string>
 #include <vector>
@@ -88,10 +90,11 @@ std::vector<T> fetch(const T* p, size_t n, sta_mem mem, const char* name) {
 
 struct CornerState {
   bool lib = false, rcv = false;
-  u32 n_tables = 0;
-  Arena lib_arena, rc_arena, state_arena;
-  const float* rc_res = nullptr;
+  Arena lib_arena, rc_arena, state_arena, ptr_arena;
+  const float* rc_res = nullptr;   // active R / Cw arrays (owned or borrowed)
   const float* rc_cap = nullptr;
+  const float** rc_ptr_host = nullptr;   // pinned staging of {res, cap}
+  size_t lut_bytes = 0;                  // device table pool size
   sta::CornerDev dev{};
 };
 
@@ -120,16 +123,18 @@ struct sta_ctx_s {
   std::vector<u32> level, perm;
   u32 num_levels = 0;
   std::vector<u32> stage, int_of_user, user_of_int;
-  u32 NP = 0, NS = 0, S = 0, n0 = 0;
-  std::vector<u32> pull_stage_ptr, sink_stage_ptr, heavy_stage_ptr, sink_ptr, heavy;
+  u32 NP = 0, NS = 0, S = 0, n0 = 0, Pi = 0;   // NP includes stage padding; Pi = NP + NS
+  std::vector<u32> pull_stage_ptr, sink_stage_ptr, tile_stage_ptr, nosink_stage_ptr, sink_ptr;
   std::vector<u32> drv_of_net;    // user net -> internal driver id
-  u32 n_heavy = 0;
+  u32 n_heavy = 0, n_units = 0;
 
   // ---- RC tree (host)
   std::vector<u32> rc_ptr, rc_node_pin;
   std::vector<int32_t> rc_parent;
   u32 n_rc = 0;
-  u32 big_total = 0;
+  u32 big_total = 0;              // tier-C nodes
+  std::vector<u32> node_user;     // internal RC node -> caller node id
+  std::vector<u32> rc_net_j;      // net j (driver order) -> internal driver id
 
   // ---- constraints (host)
   float period = 0, clock_slew = 0;
@@ -147,9 +152,26 @@ struct sta_ctx_s {
   sta_profile profile{};
   cudaEvent_t ev[STA_NUM_PHASES * 2] = {};
   u32 launches_per_update = 0;
+  u32 lut_f4 = 0;                 // table pool staged in shared memory (float4s)
+  // the update as one CUDA graph (captured lazily, invalidated by any input
+  // change except sta_set_rc_values, which only rewrites a device-side
+  // pointer pair)
+  cudaGraphExec_t gexec = nullptr;
+  bool use_graph = true;
+  // forward / backward as persistent cooperative dataflow kernels (default)
+  // or one launch per gate stage (STA_STAGE_KERNELS=1, or no cooperative launch)
+  bool use_persistent = true;
+  std::string trace_path;         // STA_TRACE (debug)
+  std::vector<u32> unit_stage;    // stage of each backward unit (trace labels)
+  u32 pgrid = 0;
 };
 
 namespace {
+
+void invalidate_graph(sta_ctx c) {
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  c->gexec = nullptr;
+}
 
 void prof_mark(sta_ctx c, int idx) {
   if (c->prof) ck(cudaEventRecord(c->ev[idx], c->stream), "cudaEventRecord");
@@ -272,18 +294,27 @@ void build_plan(sta_ctx c) {
 
   // internal numbering: pull pins by (stage, id); sinks grouped by driver
   u32 NP = 0, S = 0;
-  for (u32 p = 0; p < P; ++p)
-    if (!c->is_sink[p]) { ++NP; S = std::max(S, c->stage[p] + 1); }
-  c->NP = NP;
-  c->NS = P - NP;
+  u32 NS = 0;
+  for (u32 p = 0; p < P; ++p) {
+    if (!c->is_sink[p]) S = std::max(S, c->stage[p] + 1);
+    else ++NS;
+  }
   c->S = S;
-  c->pull_stage_ptr.assign(S + 1, 0);
+  // each stage's pull pins start on a kChunk boundary (padding ids are inert
+  // dummies), so the chunk of a pin is id / kChunk for the persistent kernels
+  std::vector<u32> stage_cnt(S, 0);
   for (u32 p = 0; p < P; ++p)
-    if (!c->is_sink[p]) c->pull_stage_ptr[c->stage[p] + 1]++;
-  for (u32 s = 0; s < S; ++s) c->pull_stage_ptr[s + 1] += c->pull_stage_ptr[s];
+    if (!c->is_sink[p]) stage_cnt[c->stage[p]]++;
+  c->pull_stage_ptr.assign(S + 1, 0);
+  for (u32 s = 0; s < S; ++s)
+    c->pull_stage_ptr[s + 1] = c->pull_stage_ptr[s] + (stage_cnt[s] + sta::kChunk - 1) / sta::kChunk * sta::kChunk;
+  NP = c->pull_stage_ptr[S];
+  c->NP = NP;
+  c->NS = NS;
+  c->Pi = NP + NS;
   c->n0 = S ? c->pull_stage_ptr[1] : 0;
   c->int_of_user.assign(P, kNone);
-  c->user_of_int.assign(P, kNone);
+  c->user_of_int.assign(c->Pi, kNone);
   {
     std::vector<u32> fill(c->pull_stage_ptr.begin(), c->pull_stage_ptr.end());
     for (u32 p = 0; p < P; ++p)
@@ -299,6 +330,7 @@ void build_plan(sta_ctx c) {
   for (u32 i = 0; i < NP; ++i) {
     const u32 p = c->user_of_int[i];
     c->sink_ptr[i] = k;
+    if (p == kNone) continue;                 // padding
     const u32 n = c->pin_net[p];
     if (n != kNone) {   // p is the driver of n
       c->drv_of_net[n] = i;
@@ -322,6 +354,7 @@ void build_plan(sta_ctx c) {
   for (u32 i = 0; i < NP; ++i) {
     const u32 p = c->user_of_int[i];
     fi_p[i] = (u32)fi_src.size();
+    if (p == kNone) continue;
     for (u32 x = fi_ptr[p]; x < fi_ptr[p + 1]; ++x) {
       const u32 a = fi_ids[x], u = c->arc_from[a];
       if (c->is_sink[u]) {
@@ -351,6 +384,7 @@ void build_plan(sta_ctx c) {
   for (u32 i = 0; i < NP; ++i) {
     const u32 u = c->user_of_int[i];
     pfo_p[i] = (u32)pfo_dst.size();
+    if (u == kNone) continue;
     for (u32 x = fo_ptr[u]; x < fo_ptr[u + 1]; ++x) {
       const u32 a = fo_ids[x];
       pfo_dst.push_back(c->int_of_user[c->arc_to[a]]);
@@ -359,16 +393,68 @@ void build_plan(sta_ctx c) {
   }
   pfo_p[NP] = (u32)pfo_dst.size();
 
-  // heavy drivers per stage
-  c->heavy.clear();
-  c->heavy_stage_ptr.assign(S + 1, 0);
+  // backward warp tiles per stage: runs of <= 32 consecutive sinks that never
+  // split a driver with <= 32 sinks; a driver with more sinks gets its own
+  // tiles (heavy slot: atomics + last-tile finish).  Stage pins without sinks
+  // are listed separately.
+  std::vector<uint2> tiles;
+  std::vector<u32> nosink, heavy_nchunk;
+  c->tile_stage_ptr.assign(S + 1, 0);
+  c->nosink_stage_ptr.assign(S + 1, 0);
   for (u32 s = 0; s < S; ++s) {
-    c->heavy_stage_ptr[s] = (u32)c->heavy.size();
-    for (u32 i = c->pull_stage_ptr[s]; i < c->pull_stage_ptr[s + 1]; ++i)
-      if (c->sink_ptr[i + 1] - c->sink_ptr[i] > (u32)sta::kHeavyFanout) c->heavy.push_back(i);
+    c->tile_stage_ptr[s] = (u32)tiles.size();
+    c->nosink_stage_ptr[s] = (u32)nosink.size();
+    u32 cur = kNone, fill = 0;   // open light tile: first sink, lanes used
+    for (u32 i = c->pull_stage_ptr[s]; i < c->pull_stage_ptr[s + 1]; ++i) {
+      const u32 b = c->sink_ptr[i], n = c->sink_ptr[i + 1] - b;
+      if (n == 0) {
+        if (c->user_of_int[i] != kNone) nosink.push_back(i);   // padding has no work
+        continue;
+      }
+      if (n > (u32)sta::kTile) {
+        cur = kNone;
+        const u32 slot = (u32)heavy_nchunk.size();
+        const u32 nch = (n + sta::kTile - 1) / sta::kTile;
+        heavy_nchunk.push_back(nch);
+        for (u32 q = 0; q < nch; ++q) tiles.push_back(make_uint2(b + q * sta::kTile, slot));
+        continue;
+      }
+      if (cur == kNone || fill + n > (u32)sta::kTile) {
+        cur = b;
+        fill = 0;
+        tiles.push_back(make_uint2(b, kNone));
+      }
+      fill += n;
+    }
   }
-  c->heavy_stage_ptr[S] = (u32)c->heavy.size();
-  c->n_heavy = (u32)c->heavy.size();
+  c->tile_stage_ptr[S] = (u32)tiles.size();
+  c->nosink_stage_ptr[S] = (u32)nosink.size();
+  c->n_heavy = (u32)heavy_nchunk.size();
+
+  // persistent-kernel work lists: forward chunks are kChunk consecutive pull
+  // pins of one stage; backward units (one block iteration each) are up to 8
+  // tiles or up to kChunk sink-less pins of one stage, in descending stage order
+  std::vector<u32> chunk_stage(NP / sta::kChunk), stage_units(S, 0), stage_sink_end(S), stage_tile_end(S);
+  for (u32 s = 0; s < S; ++s) {
+    for (u32 x = c->pull_stage_ptr[s] / sta::kChunk; x < c->pull_stage_ptr[s + 1] / sta::kChunk; ++x)
+      chunk_stage[x] = s;
+    stage_sink_end[s] = c->sink_ptr[c->pull_stage_ptr[s + 1]];
+    stage_tile_end[s] = c->tile_stage_ptr[s + 1];
+  }
+  std::vector<uint4> units;
+  for (u32 s = S; s-- > 0;) {
+    for (u32 x = c->tile_stage_ptr[s]; x < c->tile_stage_ptr[s + 1]; x += 8) {
+      units.push_back(make_uint4(s, 0, x, std::min<u32>(8, c->tile_stage_ptr[s + 1] - x)));
+      stage_units[s]++;
+    }
+    for (u32 x = c->nosink_stage_ptr[s]; x < c->nosink_stage_ptr[s + 1]; x += sta::kChunk) {
+      units.push_back(make_uint4(s, 1, x, std::min<u32>(sta::kChunk, c->nosink_stage_ptr[s + 1] - x)));
+      stage_units[s]++;
+    }
+  }
+  c->n_units = (u32)units.size();
+  c->unit_stage.resize(units.size());
+  for (size_t u = 0; u < units.size(); ++u) c->unit_stage[u] = units[u].x;
 
   std::vector<u32> sink_drv(c->NS);
   for (u32 i = 0; i < NP; ++i)
@@ -379,7 +465,7 @@ void build_plan(sta_ctx c) {
   Arena& g = c->graph_arena;
   sta::Topo& t = c->topo;
   t = sta::Topo{};
-  t.P = P; t.NP = NP; t.NS = c->NS; t.S = S; t.N = c->N;
+  t.P = P; t.NP = NP; t.NS = c->NS; t.S = S; t.N = c->N; t.n0 = c->n0;
   t.fi_ptr = g.upload(fi_p, s);
   t.fi_src = g.upload(fi_src, s);
   t.fi_hop = g.upload(fi_hop, s);
@@ -392,8 +478,20 @@ void build_plan(sta_ctx c) {
   t.pfo_ptr = g.upload(pfo_p, s);
   t.pfo_dst = g.upload(pfo_dst, s);
   t.pfo_info = g.upload(pfo_info, s);
-  t.heavy = g.upload(c->heavy, s);
+  t.tiles = g.upload(tiles, s);
+  t.chunk_stage = g.upload(chunk_stage, s);
+  t.stage_units = g.upload(stage_units, s);
+  std::vector<u32> stage_chunks(S);
+  for (u32 q = 0; q < S; ++q) stage_chunks[q] = (c->pull_stage_ptr[q + 1] - c->pull_stage_ptr[q]) / sta::kChunk;
+  t.stage_chunks = g.upload(stage_chunks, s);
+  t.stage_sink_end = g.upload(stage_sink_end, s);
+  t.stage_tile_end = g.upload(stage_tile_end, s);
+  t.units = g.upload(units, s);
+  t.n_units = c->n_units;
+  t.nosink = g.upload(nosink, s);
+  t.heavy_nchunk = g.upload(heavy_nchunk, s);
   t.int_of_user = g.upload(c->int_of_user, s);
+  t.drv_of_net = g.upload(c->drv_of_net, s);
   ck(cudaStreamSynchronize(s), "plan upload");
 }
 
@@ -427,105 +525,181 @@ void build_rc(sta_ctx c) {
       if (!seen[c->net_pins[x]]) fail(STA_ERR_RC, "rc net %u: sink pin %u has no RC node", n, c->net_pins[x]);
   }
 
-  // nets in driver order j
-  std::vector<u32> net_drv, net_rc, net_rcn, net_of_j;
+  // nets in driver order j; RC nodes renumbered net by net in that order
+  // ("internal nodes") so the kernels read topology contiguously.  R and Cw
+  // stay in the caller's node order (borrowed zero-copy), addressed by
+  // net_user[j] + local index.
+  std::vector<u32> net_drv, net_node{0}, net_user, node_user;
   net_drv.reserve(N);
+  node_user.reserve(c->n_rc);
   for (u32 i = 0; i < c->NP; ++i) {
-    const u32 p = c->user_of_int[i];
-    const u32 n = c->pin_net[p];
+    if (c->user_of_int[i] == kNone) continue;
+    const u32 n = c->pin_net[c->user_of_int[i]];
     if (n == kNone) continue;
-    net_of_j.push_back(n);
+    const u32 b = c->rc_ptr[n], m = c->rc_ptr[n + 1] - b;
     net_drv.push_back(i);
-    net_rc.push_back(c->rc_ptr[n]);
-    net_rcn.push_back(c->rc_ptr[n + 1] - c->rc_ptr[n]);
+    net_user.push_back(b);
+    for (u32 q = 0; q < m; ++q) node_user.push_back(b + q);
+    net_node.push_back((u32)node_user.size());
   }
-  net_rc.push_back(c->n_rc);
+  const u32 NJ = (u32)net_drv.size();
+  std::vector<int32_t> rc_parent(c->n_rc);
   std::vector<u32> rc_sink(c->n_rc, kNone);
-  for (u32 i = 0; i < c->n_rc; ++i) {
-    const u32 pin = c->rc_node_pin[i];
-    if (pin != kNone && c->is_sink[pin]) rc_sink[i] = c->int_of_user[pin] - c->NP;
+  for (u32 x = 0; x < c->n_rc; ++x) {
+    const u32 un = node_user[x];
+    rc_parent[x] = c->rc_parent[un];
+    const u32 pin = c->rc_node_pin[un];
+    if (pin != kNone && c->is_sink[pin]) rc_sink[x] = c->int_of_user[pin] - c->NP;
   }
-  // big-net schedules
-  std::vector<u32> big_net, big_scr{0}, hoff{0}, hptr, hnode, doff{0}, dptr, dnode, cptr, child;
-  for (u32 j = 0; j < (u32)net_of_j.size(); ++j) {
-    const u32 m = net_rcn[j];
-    if (m <= (u32)sta::kSmallNet) continue;
-    const u32 b = net_rc[j];
-    big_net.push_back(j);
-    big_scr.push_back(big_scr.back() + m);
+  c->node_user = std::move(node_user);
+
+  // tiers: A (<= 8 nodes, lumped included), B (<= 256), C (larger)
+  std::vector<u32> tierA, tierB, tierC;
+  for (u32 j = 0; j < NJ; ++j) {
+    const u32 m = net_node[j + 1] - net_node[j];
+    (m <= (u32)sta::kTierA ? tierA : m <= (u32)sta::kTierB ? tierB : tierC).push_back(j);
+  }
+  // level schedules of tier B then tier C nets
+  std::vector<u32> sched_off{0}, sched_h, sched_hn, sched_doff{0}, sched_d, sched_dn, child_off{0}, child_ptr,
+      child;
+  auto schedule = [&](u32 j) {
+    const u32 b = net_node[j], m = net_node[j + 1] - b;
     std::vector<u32> h(m, 0), dep(m, 0), cnt(m + 1, 0);
     for (u32 i = m - 1; i >= 1; --i) {
-      const u32 pa = (u32)c->rc_parent[b + i];
+      const u32 pa = (u32)rc_parent[b + i];
       h[pa] = std::max(h[pa], h[i] + 1);
       cnt[pa + 1]++;
     }
-    for (u32 i = 1; i < m; ++i) dep[i] = dep[(u32)c->rc_parent[b + i]] + 1;
-    // children CSR, decreasing child index within a parent
-    const size_t cbase = child.size();
+    for (u32 i = 1; i < m; ++i) dep[i] = dep[(u32)rc_parent[b + i]] + 1;
+    // children CSR (absolute into child[]), decreasing child index per parent
+    const u32 cbase = (u32)child.size();
     for (u32 i = 0; i < m; ++i) cnt[i + 1] += cnt[i];
-    for (u32 i = 0; i <= m; ++i) cptr.push_back((u32)cbase + cnt[i]);
+    for (u32 i = 0; i <= m; ++i) child_ptr.push_back(cbase + cnt[i]);
     child.resize(cbase + (m - 1));
     {
       std::vector<u32> fill(cnt.begin(), cnt.end() - 1);
-      for (u32 i = m - 1; i >= 1; --i) child[cbase + fill[(u32)c->rc_parent[b + i]]++] = i;
+      for (u32 i = m - 1; i >= 1; --i) child[cbase + fill[(u32)rc_parent[b + i]]++] = i;
     }
-    // nodes grouped by height
+    child_off.push_back((u32)child_ptr.size());
+    // nodes by height: [H+2 bounds relative to the node list] [m nodes]
     const u32 H = *std::max_element(h.begin(), h.end());
     std::vector<u32> hs(H + 2, 0);
     for (u32 i = 0; i < m; ++i) hs[h[i] + 1]++;
-    for (u32 x = 0; x <= H; ++x) hs[x + 1] += hs[x];
-    const size_t hbase = hnode.size();
-    hnode.resize(hbase + m);
+    for (u32 q = 0; q <= H; ++q) hs[q + 1] += hs[q];
+    for (u32 q = 0; q <= H + 1; ++q) sched_h.push_back(hs[q]);
+    const size_t hb = sched_h.size();
+    sched_h.resize(hb + m);
     {
       std::vector<u32> fill(hs.begin(), hs.end() - 1);
-      for (u32 i = 0; i < m; ++i) hnode[hbase + fill[h[i]]++] = i;
+      for (u32 i = 0; i < m; ++i) sched_h[hb + fill[h[i]]++] = i;
     }
-    for (u32 x = 0; x <= H + 1; ++x) hptr.push_back((u32)hbase + hs[x]);
-    hoff.push_back((u32)hptr.size());
-    // nodes grouped by depth (depth >= 1)
+    sched_hn.push_back(H + 1);
+    sched_off.push_back((u32)sched_h.size());
+    // nodes by depth >= 1: [Dm+1 bounds] [m-1 nodes]
     const u32 Dm = *std::max_element(dep.begin(), dep.end());
-    std::vector<u32> ds(Dm + 2, 0);
-    for (u32 i = 1; i < m; ++i) ds[dep[i] + 1]++;
-    for (u32 x = 0; x <= Dm; ++x) ds[x + 1] += ds[x];
-    const size_t dbase = dnode.size();
-    dnode.resize(dbase + (m - 1));
+    std::vector<u32> ds(Dm + 1, 0);
+    for (u32 i = 1; i < m; ++i) ds[dep[i]]++;      // ds[d-1 + 1] counts depth d
+    std::vector<u32> bnd(Dm + 1, 0);
+    for (u32 q = 1; q <= Dm; ++q) bnd[q] = bnd[q - 1] + ds[q];
+    for (u32 q = 0; q <= Dm; ++q) sched_d.push_back(bnd[q]);
+    const size_t db = sched_d.size();
+    sched_d.resize(db + (m - 1));
     {
-      std::vector<u32> fill(ds.begin(), ds.end() - 1);
-      for (u32 i = 1; i < m; ++i) dnode[dbase + fill[dep[i]]++] = i;
+      std::vector<u32> fill(bnd.begin(), bnd.end());
+      for (u32 i = 1; i < m; ++i) sched_d[db + fill[dep[i] - 1]++] = i;
     }
-    for (u32 x = 1; x <= Dm + 1; ++x) dptr.push_back((u32)dbase + ds[x]);
-    doff.push_back((u32)dptr.size());
+    sched_dn.push_back(Dm);
+    sched_doff.push_back((u32)sched_d.size());
+  };
+  for (u32 j : tierB) schedule(j);
+  // tier C: one global array of all tier-C nodes, each net in DFS preorder
+  // (children in increasing index order), with subtree ends and, for each
+  // position, the positions whose subtree ends there
+  std::vector<u32> tc_user, tc_int, tc_end, tc_start, tc_eptr{0}, tc_ends, tc_root, tc_drv;
+  for (u32 j : tierC) {
+    const u32 b = net_node[j], m = net_node[j + 1] - b;
+    const u32 g0 = (u32)tc_user.size();
+    std::vector<u32> cnt(m + 1, 0), ch(m), pos(m), endp(m), pre;
+    pre.reserve(m);
+    for (u32 i = 1; i < m; ++i) cnt[(u32)rc_parent[b + i] + 1]++;
+    for (u32 i = 0; i < m; ++i) cnt[i + 1] += cnt[i];
+    {
+      std::vector<u32> fill(cnt.begin(), cnt.end() - 1);
+      for (u32 i = 1; i < m; ++i) ch[fill[(u32)rc_parent[b + i]]++] = i;
+    }
+    std::vector<std::pair<u32, u32>> stack{{0u, 0u}};   // (node, next child slot)
+    pos[0] = 0;
+    pre.push_back(0);
+    while (!stack.empty()) {
+      const u32 nd = stack.back().first;
+      if (cnt[nd] + stack.back().second < cnt[nd + 1]) {
+        const u32 cld = ch[cnt[nd] + stack.back().second++];
+        pos[cld] = (u32)pre.size();
+        pre.push_back(cld);
+        stack.push_back({cld, 0u});
+      } else {
+        endp[pos[nd]] = (u32)pre.size();
+        stack.pop_back();
+      }
+    }
+    std::vector<std::vector<u32>> ends_at(m);
+    for (u32 a = 1; a < m; ++a)
+      if (endp[a] < m) ends_at[endp[a]].push_back(a);
+    for (u32 q = 0; q < m; ++q) {
+      tc_user.push_back(net_user[j] + pre[q]);
+      tc_int.push_back(b + pre[q]);
+      tc_end.push_back(g0 + endp[q]);
+      tc_start.push_back(g0);
+      for (u32 a : ends_at[q]) tc_ends.push_back(g0 + a);
+      tc_eptr.push_back((u32)tc_ends.size());
+    }
+    tc_root.push_back(g0);
+    tc_drv.push_back(net_drv[j]);
   }
-  // hoff/doff were pushed after each net: turn them into [n_big+1] ranges
-  // (hoff[b]..hoff[b+1]) -- they already are, since they started at 0.
-  c->big_total = big_scr.back();
+  c->big_total = (u32)tc_user.size();
 
   cudaStream_t s = c->stream;
   c->tree_arena.release();
   Arena& g = c->tree_arena;
   sta::Topo& t = c->topo;
   t.net_drv = g.upload(net_drv, s);
-  t.net_rc = g.upload(net_rc, s);
-  t.net_rcn = g.upload(net_rcn, s);
-  t.rc_parent = g.upload(c->rc_parent, s);
+  t.net_node = g.upload(net_node, s);
+  t.net_user = g.upload(net_user, s);
+  t.rc_parent = g.upload(rc_parent, s);
   t.rc_sink = g.upload(rc_sink, s);
-  t.n_big = (u32)big_net.size();
-  t.big_net = g.upload(big_net, s);
-  t.big_scr = g.upload(big_scr, s);
-  t.big_hptr_off = g.upload(hoff, s);
-  t.big_hptr = g.upload(hptr, s);
-  t.big_hnode = g.upload(hnode, s);
-  t.big_dptr_off = g.upload(doff, s);
-  t.big_dptr = g.upload(dptr, s);
-  t.big_dnode = g.upload(dnode, s);
-  t.big_cptr = g.upload(cptr, s);
-  t.big_child = g.upload(child, s);
+  t.nA = (u32)tierA.size();
+  t.nB = (u32)tierB.size();
+  t.nC = (u32)tierC.size();
+  t.tierA = g.upload(tierA, s);
+  t.tierB = g.upload(tierB, s);
+  t.tierC = g.upload(tierC, s);
+  t.sched_off = g.upload(sched_off, s);
+  t.sched_h = g.upload(sched_h, s);
+  t.sched_hn = g.upload(sched_hn, s);
+  t.sched_doff = g.upload(sched_doff, s);
+  t.sched_d = g.upload(sched_d, s);
+  t.sched_dn = g.upload(sched_dn, s);
+  t.child_off = g.upload(child_off, s);
+  t.child_ptr = g.upload(child_ptr, s);
+  t.child = g.upload(child, s);
+  t.nCn = c->big_total;
+  t.tc_user = g.upload(tc_user, s);
+  t.tc_int = g.upload(tc_int, s);
+  t.tc_end = g.upload(tc_end, s);
+  t.tc_start = g.upload(tc_start, s);
+  t.tc_eptr = g.upload(tc_eptr, s);
+  t.tc_ends = g.upload(tc_ends, s);
+  t.tc_root = g.upload(tc_root, s);
+  t.tc_drv = g.upload(tc_drv, s);
+  c->rc_net_j = std::move(net_drv);
   ck(cudaStreamSynchronize(s), "rc upload");
 }
 
 // constraints + tree dependent arrays (endpoints, seeds, static node caps)
 void prepare(sta_ctx c) {
   if (c->prepared) return;
+  invalidate_graph(c);
+  c->pgrid = c->use_persistent ? sta::persistent_grid(c->lut_f4) : 0;
   const u32 P = c->P;
   std::vector<u32> pi_idx(P, kNone), po_idx(P, kNone);
   for (u32 k = 0; k < c->pi_pin.size(); ++k) pi_idx[c->pi_pin[k]] = k;
@@ -534,7 +708,7 @@ void prepare(sta_ctx c) {
   for (u32 k = 0; k < c->po_pin.size(); ++k) po_ld[c->po_pin[k]] += c->po_load[k];
 
   // endpoints in increasing user pin id
-  std::vector<u32> pin_ep(P, kNone);
+  std::vector<u32> pin_ep(c->Pi, kNone);
   std::vector<sta::EpRec> ep;
   for (u32 p = 0; p < P; ++p) {
     if (po_idx[p] == kNone && c->chk_of_pin[p] == kNone) continue;
@@ -549,20 +723,21 @@ void prepare(sta_ctx c) {
   std::vector<u32> seed(c->n0, kNone);
   for (u32 i = 0; i < c->n0; ++i) {
     const u32 p = c->user_of_int[i];
+    if (p == kNone) continue;
     if (c->pin_role[p] == STA_PIN_FF_CK) seed[i] = sta::kSeedClock;
     else if (pi_idx[p] != kNone) seed[i] = pi_idx[p];
   }
-  // static node caps (pin cap + PO load) and lumped net loads, in fp64 then
-  // rounded once
+  // static node caps (pin cap + PO load, internal node order) and lumped net
+  // loads (nets in driver order), in fp64 then rounded once
   std::vector<float> scap(c->n_rc, 0.f);
-  for (u32 i = 0; i < c->n_rc; ++i) {
-    const u32 pin = c->rc_node_pin[i];
-    if (pin != kNone) scap[i] = (float)((double)c->pin_cap[pin] + (double)po_ld[pin]);
+  for (u32 x = 0; x < c->n_rc; ++x) {
+    const u32 pin = c->rc_node_pin[c->node_user[x]];
+    if (pin != kNone) scap[x] = (float)((double)c->pin_cap[pin] + (double)po_ld[pin]);
   }
   std::vector<float> lumped;
-  for (u32 i = 0; i < c->NP; ++i) {
+  lumped.reserve(c->rc_net_j.size());
+  for (u32 i : c->rc_net_j) {
     const u32 n = c->pin_net[c->user_of_int[i]];
-    if (n == kNone) continue;
     double sum = 0;
     for (u32 x = c->net_ptr[n]; x < c->net_ptr[n + 1]; ++x) {
       const u32 pin = c->net_pins[x];
@@ -595,59 +770,138 @@ void prepare(sta_ctx c) {
     cs.state_arena.release();
     Arena& a = cs.state_arena;
     sta::CornerDev& d = cs.dev;
-    d.rec = a.alloc<float4>(2 * (size_t)P);
-    d.rat = a.alloc<float4>(P);
-    d.slack = a.alloc<float4>(P);
+    d.rec = a.alloc<float4>(2 * (size_t)c->NP);
+    d.rat = a.alloc<float4>(c->Pi);
+    d.slack = a.alloc<float4>(c->Pi);
     d.elm = a.alloc<float>(c->NS);
     d.load = a.alloc<float>(c->NP);
     d.ep_ws = a.alloc<float2>(c->n_ep);
     d.res = a.alloc<double>(4);
-    d.scratch = a.alloc<double>(2 * (size_t)c->big_total);
+    d.red_part = a.alloc<double>(4 * sta::kRedBlocks);
+    d.red_cnt = a.alloc<u32>(1);
+    d.heavy_key = a.alloc<int4>(c->n_heavy);
+    d.heavy_cnt = a.alloc<u32>(c->n_heavy);
+    d.scratch = a.alloc<double>(sta::tierC_scratch(c->big_total));
     d.err_flag = a.alloc<u32>(1);
+    d.fwd_done = a.alloc<u32>(std::max<u32>(c->S, 1));
+    d.bwd_done = a.alloc<u32>(std::max<u32>(c->S, 1));
+    ck(cudaMemsetAsync(d.fwd_done, 0, sizeof(u32) * std::max<u32>(c->S, 1), s), "memset");
+    ck(cudaMemsetAsync(d.bwd_done, 0, sizeof(u32) * std::max<u32>(c->S, 1), s), "memset");
+    d.trace = nullptr;
+    if (!c->trace_path.empty()) {   // debug: per-chunk / per-unit timestamps
+      const size_t n = 3 * ((size_t)c->NP / sta::kChunk + c->n_units);
+      d.trace = a.alloc<unsigned long long>(n);
+      ck(cudaMemsetAsync(d.trace, 0, n * sizeof(unsigned long long), s), "memset");
+    }
     ck(cudaMemsetAsync(d.load, 0, sizeof(float) * std::max<u32>(c->NP, 1), s), "memset");
-    ck(cudaMemsetAsync(d.err_flag, 0, sizeof(u32), s), "memset");
+    ck(sta::launch_init_corner(t, d, c->n_heavy, s), "init kernel");
   }
   ck(cudaStreamSynchronize(s), "prepare upload");
   c->prepared = true;
 }
 
-void enqueue_update(sta_ctx c) {
+// Kernel sequence of one update of one corner (see sta_kernels.cu).
+u32 enqueue_corner(sta_ctx c, const sta::CornerDev& d) {
   const sta::Topo& t = c->topo;
   cudaStream_t s = c->stream;
   u32 launches = 0;
-  prof_mark(c, 8);
-  for (CornerState& cs : c->corners) {
-    sta::CornerDev d = cs.dev;
-    d.rc_res = cs.rc_res;
-    d.rc_cap = cs.rc_cap;
-    prof_mark(c, 0);
-    ck(sta::launch_rc(t, d, 0, s), "rc kernel");
-    launches += (t.N ? 1 : 0) + (t.n_big ? 1 : 0);
-    prof_mark(c, 1);
+  prof_mark(c, 0);
+  ck(sta::launch_rc(t, d, s), "rc kernel");
+  launches += (t.nA ? 1 : 0) + (t.nB ? 1 : 0) + (t.nC ? 10 : 0);
+  prof_mark(c, 1);
+  if (c->use_persistent && c->pgrid) {
     prof_mark(c, 2);
-    ck(sta::launch_seed(t, d, c->n0, s), "seed kernel");
-    launches += c->n0 ? 1 : 0;
-    for (u32 st = 1; st <= c->S; ++st) {
-      // sinks of stage st-1 drivers, then pull pins of stage st (none for st == S)
-      const u32 a0 = c->sink_stage_ptr[st - 1], a1 = c->sink_stage_ptr[st];
-      const u32 b0 = st < c->S ? c->pull_stage_ptr[st] : 0;
-      const u32 b1 = st < c->S ? c->pull_stage_ptr[st + 1] : 0;
-      ck(sta::launch_fwd_stage(t, d, a0, a1 - a0, b0, b1 - b0, s), "forward kernel");
-      launches += (a1 - a0 + b1 - b0) ? 1 : 0;
-    }
+    ck(sta::launch_fwd_persistent(t, d, c->pgrid, c->lut_f4, s), "forward persistent kernel");
     prof_mark(c, 3);
     prof_mark(c, 4);
-    for (u32 st = c->S; st-- > 0;) {
-      const u32 p0 = c->pull_stage_ptr[st], p1 = c->pull_stage_ptr[st + 1];
-      const u32 h0 = c->heavy_stage_ptr[st], h1 = c->heavy_stage_ptr[st + 1];
-      ck(sta::launch_bwd_stage(t, d, p0, p1 - p0, h0, h1 - h0, s), "backward kernel");
-      launches += (p1 - p0) ? 1 : 0;
-    }
+    ck(sta::launch_bwd_persistent(t, d, c->pgrid, c->lut_f4, s), "backward persistent kernel");
     prof_mark(c, 5);
     prof_mark(c, 6);
     ck(sta::launch_reduce(t, d, s), "reduce kernel");
-    launches += 1;
     prof_mark(c, 7);
+    return launches + 3;
+  }
+  prof_mark(c, 2);
+  ck(sta::launch_seed(t, d, c->n0, s), "seed kernel");
+  launches += c->n0 ? 1 : 0;
+  for (u32 st = 1; st < c->S; ++st) {
+    const u32 b0 = c->pull_stage_ptr[st], b1 = c->pull_stage_ptr[st + 1];
+    ck(sta::launch_fwd_stage(t, d, b0, b1 - b0, c->lut_f4, s), "forward kernel");
+    launches += (b1 - b0) ? 1 : 0;
+  }
+  prof_mark(c, 3);
+  prof_mark(c, 4);
+  for (u32 st = c->S; st-- > 0;) {
+    const u32 t0 = c->tile_stage_ptr[st], t1 = c->tile_stage_ptr[st + 1];
+    const u32 n0 = c->nosink_stage_ptr[st], n1 = c->nosink_stage_ptr[st + 1];
+    const u32 sink_end = c->sink_ptr[c->pull_stage_ptr[st + 1]];
+    ck(sta::launch_bwd_stage(t, d, t0, t1 - t0, sink_end, n0, n1 - n0, c->lut_f4, s), "backward kernel");
+    launches += (t1 - t0 + n1 - n0) ? 1 : 0;
+  }
+  prof_mark(c, 5);
+  prof_mark(c, 6);
+  ck(sta::launch_reduce(t, d, s), "reduce kernel");
+  launches += 1;
+  prof_mark(c, 7);
+  return launches;
+}
+
+// STA_TRACE=<path>: after an update, write the persistent kernels' per-chunk
+// and per-unit {start, ready, end} timestamps of corner 0 and the stage of
+// every chunk / unit (debug tooling: scripts/trace_report.py)
+void dump_trace(sta_ctx c) {
+  const sta::CornerDev& d = c->corners[0].dev;
+  if (!d.trace) return;
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  const size_t nch = c->NP / sta::kChunk, n = 3 * (nch + c->n_units);
+  std::vector<unsigned long long> h(n);
+  ck(cudaMemcpy(h.data(), d.trace, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "D2H trace");
+  FILE* f = std::fopen(c->trace_path.c_str(), "w");
+  if (!f) return;
+  std::fprintf(f, "kind,index,stage,start,ready,end\n");
+  for (size_t x = 0; x < nch; ++x) {
+    u32 st = 0;
+    while (st + 1 < c->S && c->pull_stage_ptr[st + 1] <= x * sta::kChunk) ++st;
+    std::fprintf(f, "fwd,%zu,%u,%llu,%llu,%llu\n", x, st, h[3 * x], h[3 * x + 1], h[3 * x + 2]);
+  }
+  for (size_t u = 0; u < c->n_units; ++u)
+    std::fprintf(f, "bwd,%zu,%u,%llu,%llu,%llu\n", u, c->unit_stage[u], h[3 * (nch + u)], h[3 * (nch + u) + 1],
+                 h[3 * (nch + u) + 2]);
+  std::fclose(f);
+}
+
+void enqueue_update(sta_ctx c) {
+  cudaStream_t s = c->stream;
+  if (!c->trace_path.empty()) {
+    for (CornerState& cs : c->corners) c->launches_per_update = enqueue_corner(c, cs.dev);
+    dump_trace(c);
+    return;
+  }
+  if (!c->prof && c->use_graph) {
+    if (!c->gexec) {
+      cudaGraph_t g = nullptr;
+      ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
+      u32 launches = 0;
+      try {
+        for (CornerState& cs : c->corners) launches += enqueue_corner(c, cs.dev);
+      } catch (...) {
+        cudaStreamEndCapture(s, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      ck(cudaStreamEndCapture(s, &g), "end capture");
+      cudaError_t e = cudaGraphInstantiate(&c->gexec, g, 0);
+      cudaGraphDestroy(g);
+      ck(e, "graph instantiate");
+      c->launches_per_update = launches;
+    }
+    ck(cudaGraphLaunch(c->gexec, s), "graph launch");
+    return;
+  }
+  u32 launches = 0;
+  prof_mark(c, 8);
+  for (CornerState& cs : c->corners) {
+    launches += enqueue_corner(c, cs.dev);
     if (c->prof) {
       // accumulate per phase (synchronous read of the event pairs)
       ck(cudaEventSynchronize(c->ev[7]), "event sync");
@@ -656,10 +910,6 @@ void enqueue_update(sta_ctx c) {
         ck(cudaEventElapsedTime(&ms, c->ev[2 * ph], c->ev[2 * ph + 1]), "elapsed");
         c->profile.ms[ph] += ms;
       }
-      c->profile.launches[0] += (t.N ? 1 : 0) + (t.n_big ? 1 : 0);
-      c->profile.launches[1] += c->S + (c->n0 ? 1 : 0);
-      c->profile.launches[2] += c->S;
-      c->profile.launches[3] += 1;
     }
   }
   if (c->prof) {
@@ -734,19 +984,38 @@ void deliver(sta_ctx c, T* dst, const T* dev_src, size_t n, sta_mem mem) {
   }
 }
 
-// gather float4 per user pin into the caller buffer
-void deliver_pins(sta_ctx c, float* dst, const float4* src, u32 stride, sta_mem mem) {
+// gather a float4 per user pin (what: 0 at, 1 slew, 2 rat, 3 slack) into the
+// caller buffer
+void deliver_pins(sta_ctx c, float* dst, const sta::CornerDev& d, int what, sta_mem mem) {
   if (!dst || !c->P) return;
   const u32 P = c->P;
   float4* out;
   if (mem == STA_MEM_DEVICE) {
     out = reinterpret_cast<float4*>(dst);
-  } else {
+  } else if (mem == STA_MEM_HOST) {
     c->tmp_arena.release();
     out = c->tmp_arena.alloc<float4>(P);
+  } else {
+    fail(STA_ERR_ARG, "bad sta_mem %d", (int)mem);
   }
-  ck(sta::launch_gather4(src, c->topo.int_of_user, out, P, stride, c->stream), "gather kernel");
+  ck(sta::launch_gather_pins(c->topo, d, what, out, c->stream), "gather kernel");
   if (mem != STA_MEM_DEVICE) deliver(c, reinterpret_cast<float4*>(dst), out, P, STA_MEM_HOST);
+}
+
+// per-corner {res, cap} device pointer pair, updated in stream order so a
+// captured update graph stays valid when borrowed arrays change
+void publish_rc_pointers(sta_ctx c, CornerState& cs) {
+  if (!cs.rc_ptr_host) {
+    void* h = nullptr;
+    ck(cudaHostAlloc(&h, 2 * sizeof(float*), cudaHostAllocDefault), "cudaHostAlloc");
+    cs.rc_ptr_host = static_cast<const float**>(h);
+    cs.dev.rc_vals = cs.ptr_arena.alloc<const float*>(2);
+  }
+  ck(cudaStreamSynchronize(c->stream), "sync");   // staging buffer reuse
+  cs.rc_ptr_host[0] = cs.rc_res;
+  cs.rc_ptr_host[1] = cs.rc_cap;
+  ck(cudaMemcpyAsync(const_cast<const float**>(cs.dev.rc_vals), cs.rc_ptr_host, 2 * sizeof(float*),
+                     cudaMemcpyHostToDevice, c->stream), "H2D rc pointers");
 }
 
 }  // namespace
@@ -793,6 +1062,9 @@ sta_status sta_create(int cuda_device, uint32_t num_corners, void* cuda_stream, 
   for (auto& e : c->ev)
     if (cudaEventCreate(&e) != cudaSuccess) { delete c; return STA_ERR_CUDA; }
   c->corners.resize(num_corners);
+  if (const char* g = std::getenv("STA_NO_GRAPH")) c->use_graph = g[0] == '0';
+  if (const char* g = std::getenv("STA_STAGE_KERNELS")) c->use_persistent = g[0] == '0';
+  if (const char* g = std::getenv("STA_TRACE")) c->trace_path = g;
   *out = c;
   return STA_OK;
 }
@@ -809,7 +1081,10 @@ sta_status sta_destroy(sta_ctx c) {
     cs.lib_arena.release();
     cs.rc_arena.release();
     cs.state_arena.release();
+    cs.ptr_arena.release();
+    if (cs.rc_ptr_host) cudaFreeHost(cs.rc_ptr_host);
   }
+  invalidate_graph(c);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -856,8 +1131,12 @@ sta_status sta_set_library(sta_ctx c, uint32_t corner, sta_mem mem, uint32_t num
     auto h2 = fetch(n2, num_tables, mem, "n2");
     auto ho = fetch(off, num_tables, mem, "off");
     auto hd = fetch(data, data_len, mem, "data");
-    if (data_len >= (1u << 26)) fail(STA_ERR_LUT, "table pool too large (%u floats)", data_len);
-    std::vector<u32> tdesc(num_tables);
+    // device pool (sta_internal.h): table blocks of kTabStride floats, then
+    // deduplicated 16-byte aligned axis templates of kTmplStride floats
+    const size_t tmpl0 = ((size_t)num_tables * sta::kTabStride + 3) / 4 * 4;
+    std::vector<float> rec(tmpl0, 0.f);
+    std::vector<std::vector<float>> tmpls;
+    const float inf = std::numeric_limits<float>::infinity();
     for (u32 t = 0; t < num_tables; ++t) {
       const u32 a = h1[t], b = h2[t];
       if (a < 1 || a > 8 || b < 1 || b > 8) fail(STA_ERR_LUT, "table %u: size %ux%u outside 1..8", t, a, b);
@@ -869,13 +1148,43 @@ sta_status sta_set_library(sta_ctx c, uint32_t corner, sta_mem mem, uint32_t num
         if (!(x[k] > x[k - 1])) fail(STA_ERR_LUT, "table %u: index_1 not strictly ascending", t);
       for (u32 k = 1; k < b; ++k)
         if (!(x[a + k] > x[a + k - 1])) fail(STA_ERR_LUT, "table %u: index_2 not strictly ascending", t);
-      tdesc[t] = sta::pack_tdesc(ho[t], a, b);
+      std::vector<float> tm(sta::kTmplStride);
+      auto axis = [&](const float* ax, u32 n, float* sx, float* xx, float* rx) {
+        for (u32 k = 0; k < 8; ++k) {
+          sx[k] = (k >= 1 && k + 2 <= n) ? ax[k] : inf;
+          xx[k] = ax[std::min(k, n - 1)];
+          if (k + 1 < n) {
+            volatile float w = ax[k + 1] - ax[k];     // fp32 width, IEEE
+            rx[k] = 1.0f / w;
+          } else {
+            rx[k] = 0.f;
+          }
+        }
+      };
+      axis(x, a, tm.data() + 0, tm.data() + 8, tm.data() + 16);
+      axis(x + a, b, tm.data() + 24, tm.data() + 32, tm.data() + 40);
+      size_t id = 0;
+      while (id < tmpls.size() && std::memcmp(tmpls[id].data(), tm.data(), tm.size() * sizeof(float))) ++id;
+      if (id == tmpls.size()) tmpls.push_back(tm);
+      float* r = rec.data() + (size_t)t * sta::kTabStride;
+      const int32_t toff = (int32_t)(tmpl0 + id * sta::kTmplStride);
+      std::memcpy(r, &toff, sizeof toff);
+      const float* v = x + a + b;
+      for (u32 i = 0; i < 8; ++i)
+        for (u32 j = 0; j < 8; ++j) r[1 + i * 8 + j] = v[std::min(i, a - 1) * b + std::min(j, b - 1)];
     }
+    for (const auto& tm : tmpls) rec.insert(rec.end(), tm.begin(), tm.end());
+    invalidate_graph(c);
+    ck(cudaStreamSynchronize(c->stream), "sync");
     cs.lib_arena.release();
-    cs.dev.lut = cs.lib_arena.upload(hd, c->stream);
-    cs.dev.tdesc = cs.lib_arena.upload(tdesc, c->stream);
+    cs.dev.lut = cs.lib_arena.upload(rec, c->stream);
+    cs.lut_bytes = rec.size() * sizeof(float);
+    size_t bytes = 0;                          // the staged pool must fit every corner's
+    for (const CornerState& o : c->corners) bytes = std::max(bytes, o.lut_bytes);
+    c->lut_f4 = bytes <= sta::kLutSmemMax ? (u32)(bytes / 16) : 0;
+    if (c->lut_f4 && bytes > 48 * 1024) ck(sta::set_lut_smem_limit(bytes), "smem attribute");
+    c->pgrid = c->use_persistent ? sta::persistent_grid(c->lut_f4) : 0;
     ck(cudaStreamSynchronize(c->stream), "library upload");
-    cs.n_tables = num_tables;
     cs.lib = true;
   });
 }
@@ -902,6 +1211,7 @@ sta_status sta_set_rc_values(sta_ctx c, uint32_t corner, sta_mem mem, const floa
     if (!c->has_tree) fail(STA_ERR_ORDER, "sta_set_rc_values before sta_set_rc_tree");
     if (c->n_rc && (!res || !cap)) fail(STA_ERR_ARG, "res/cap NULL");
     if (mem == STA_MEM_DEVICE) {
+      ck(cudaStreamSynchronize(c->stream), "sync");   // owned buffers may be in use
       cs.rc_arena.release();
       cs.rc_res = res;
       cs.rc_cap = cap;
@@ -929,6 +1239,7 @@ sta_status sta_set_rc_values(sta_ctx c, uint32_t corner, sta_mem mem, const floa
     } else {
       fail(STA_ERR_ARG, "bad sta_mem %d", (int)mem);
     }
+    publish_rc_pointers(c, cs);
     cs.rcv = true;
   });
 }
@@ -1009,7 +1320,7 @@ sta_status sta_report_slack(sta_ctx c, uint32_t corner, double* res4, float* pin
       deliver(c, res4, cs.dev.res, 4, mem);
       if (mem == STA_MEM_HOST) check_flags(c);
     }
-    deliver_pins(c, pin_slack, cs.dev.slack, 1, mem);
+    deliver_pins(c, pin_slack, cs.dev, 3, mem);
   });
 }
 
@@ -1017,9 +1328,9 @@ sta_status sta_get_timing(sta_ctx c, uint32_t corner, float* at, float* slew, fl
   return guard(c, [&] {
     CornerState& cs = corner_of(c, corner);
     require_updated(c);
-    deliver_pins(c, at, cs.dev.rec, 2, mem);
-    deliver_pins(c, slew, cs.dev.rec + 1, 2, mem);
-    deliver_pins(c, rat, cs.dev.rat, 1, mem);
+    deliver_pins(c, at, cs.dev, 0, mem);
+    deliver_pins(c, slew, cs.dev, 1, mem);
+    deliver_pins(c, rat, cs.dev, 2, mem);
   });
 }
 
@@ -1036,15 +1347,12 @@ sta_status sta_get_rc(sta_ctx c, uint32_t corner, float* net_load, float* pin_el
     } else if (mem != STA_MEM_DEVICE) {
       fail(STA_ERR_ARG, "bad sta_mem %d", (int)mem);
     }
-    Arena tmp;
-    const u32* dn = tmp.upload(c->drv_of_net, c->stream);
-    ck(sta::launch_gather_rc(c->topo, cs.dev, nl, pe, dn, nullptr, c->stream), "gather rc");
+    ck(sta::launch_gather_rc(c->topo, cs.dev, nl, pe, c->stream), "gather rc");
     if (mem == STA_MEM_HOST) {
       if (net_load) deliver(c, net_load, nl, c->N, STA_MEM_HOST);
       if (pin_elm) deliver(c, pin_elm, pe, c->P, STA_MEM_HOST);
     }
     ck(cudaStreamSynchronize(c->stream), "sync");
-    tmp.release();
   });
 }
 

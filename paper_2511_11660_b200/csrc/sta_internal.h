@@ -7,9 +7,9 @@
 //     evaluated by pulling over its cell-arc fan-in.
 //   * "sinks" -- net sinks (exactly one fan-in: the net arc): internal ids
 //     [NP, P), grouped by driver in driver order, in net order.  A sink is a
-//     pure function of its driver (AT + Elmore, PERI slew), so it needs no
-//     step of its own: the forward kernel of the stage after its driver's
-//     materializes it, and consumers recompute it inline (pull-through).
+//     pure function of its driver (AT + Elmore, PERI slew): its arrival and
+//     slew are never stored, every consumer recomputes them from the driver's
+//     record with the same instructions (pull-through).
 //   Gate stage: 0 for pins without fan-in, else 1 + max over cell fan-in
 //   (u -> v) of stage(driver(u)) (stage(u) if u is itself a pull pin).
 #pragma once
@@ -20,16 +20,27 @@ namespace sta {
 
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kSeedClock = 0xFFFFFFFEu;   // stage-0 seed: ideal clock pin
-constexpr int kSmallNet = 48;                  // RC nodes handled by one thread
-constexpr int kHeavyFanout = 32;               // backward: sinks above -> block per driver
+constexpr int kTierA = 8;                      // RC nodes handled by one thread in registers
+constexpr int kTierB = 256;                    // RC nodes handled by one warp (above: one block)
+constexpr int kTile = 32;                      // backward: sinks per warp tile
+constexpr uint32_t kChunk = 256;               // persistent kernels: pins per chunk (= block size)
 
-// fan-in / fan-out arc info word: sense (3 bits) | first table id << 3
+// Device NLDM table pool (built by sta_set_library), shared-memory friendly:
+//   * table t: a block of kTabStride = 65 floats at t * 65: word 0 = offset
+//     (as int) of its axis template, words 1..64 = values v[8][8] row-major,
+//     rows >= n1 / columns >= n2 replicating the last row / column (so a
+//     1-wide axis interpolates by 0).  The odd stride spreads lanes that read
+//     the same entry of different tables over different shared-memory banks.
+//   * axis templates (deduplicated, 16-byte aligned), 48 floats: for index_1
+//     then index_2: sx[8] search thresholds (sx[k] = x[k] for 1 <= k <= n-2,
+//     +inf otherwise -> segment i = #{k : sx[k] <= s}), x[8] (padded with the
+//     last value), rx[8] = 1 / (x[k+1] - x[k]) (0 past the end), fp32.
+//     Tables of one library template share one record (warp broadcast).
+constexpr int kTabStride = 65;
+constexpr int kTmplStride = 48;
+
+// arc info word: sense (3 bits) | first table id << 3
 __host__ __device__ inline uint32_t pack_info(uint32_t sense, uint32_t tab) { return sense | (tab << 3); }
-
-// table descriptor: data offset (26 bits) | (n1-1) << 26 | (n2-1) << 29
-__host__ __device__ inline uint32_t pack_tdesc(uint32_t off, uint32_t n1, uint32_t n2) {
-  return off | ((n1 - 1u) << 26) | ((n2 - 1u) << 29);
-}
 
 struct EpRec {          // one timing endpoint
   uint32_t po;          // index into the PO constraint arrays or kNone
@@ -38,8 +49,8 @@ struct EpRec {          // one timing endpoint
 
 // Topology shared by all corners (device pointers).
 struct Topo {
-  uint32_t P, NP, NS, S, N, n_ep, n_pi, n_po;
-  // forward
+  uint32_t P, NP, NS, S, N, n_ep, n_pi, n_po, n0;   // P: caller pins; NP: pull ids incl. padding
+  // forward: fan-in terms of pull pins
   const uint32_t* fi_ptr;    // [NP+1]
   const uint32_t* fi_src;    // record to read (driver of u, or u if u is a pull pin)
   const uint32_t* fi_hop;    // sink index of u (net hop to apply) or kNone
@@ -56,73 +67,112 @@ struct Topo {
   const uint32_t* pfo_info;
   const uint32_t* pin_ep;    // [P] internal id -> endpoint index or kNone
   const EpRec* ep;           // [n_ep]
-  const uint32_t* heavy;     // heavy drivers, grouped by stage
+  const uint2* tiles;        // backward warp tiles: {first sink, heavy slot or kNone}, by stage
+  const uint32_t* nosink;    // pull pins without sinks, by stage
+  const uint32_t* heavy_nchunk; // [n_heavy] tiles of each heavy driver
+  // persistent kernels
+  const uint32_t* chunk_stage;   // [NP / kChunk] stage of each forward chunk
+  const uint32_t* stage_units;   // [S] backward units per stage
+  const uint32_t* stage_chunks;  // [S] forward chunks per stage
+  const uint32_t* stage_sink_end;// [S] end of the sink range of each stage's drivers
+  const uint32_t* stage_tile_end;// [S] end of each stage's tiles
+  const uint4* units;            // backward units {stage, kind 0 tiles / 1 sink-less, first, count}
+  uint32_t n_units;
   // constraints
   const float4* pi_at;       // [n_pi]
   const float4* pi_slew;
   const float2* po_out_max;  // [n_po]
   const float2* po_out_min;
   float period, clock_slew;
-  // RC (nets in driver order j = 0..N-1)
+  // RC: nets in driver order j; node arrays in driver order ("internal nodes")
   const uint32_t* net_drv;   // [N] internal pull id of the driver
-  const uint32_t* net_rc;    // [N+1] user RC node offsets in driver order (begin)
-  const uint32_t* net_rcn;   // [N] node count
+  const uint32_t* net_node;  // [N+1] internal node offsets
+  const uint32_t* net_user;  // [N] user node offset (R / Cw arrays are in user order)
   const float* net_lumped;   // [N] lumped load (nets without RC nodes)
-  const int32_t* rc_parent;  // [n_rc] user node order, local parent
+  const int32_t* rc_parent;  // [n_rc] internal node order, local parent
   const uint32_t* rc_sink;   // [n_rc] sink index of the node's pin or kNone
   const float* rc_scap;      // [n_rc] pin cap + PO load at the node
-  // big-net schedule (block per net)
-  uint32_t n_big;
-  const uint32_t* big_net;     // [n_big] net index j (driver order)
-  const uint32_t* big_scr;     // [n_big+1] prefix of node counts: scratch offset of net b
-  const uint32_t* big_hptr_off;// [n_big+1] range of net b in big_hptr
-  const uint32_t* big_hptr;    // height-level boundaries, absolute into big_hnode
-  const uint32_t* big_hnode;   // local node ids grouped by height (leaves first)
-  const uint32_t* big_dptr_off;// [n_big+1] range of net b in big_dptr
-  const uint32_t* big_dptr;    // depth-level boundaries, absolute into big_dnode
-  const uint32_t* big_dnode;   // local node ids grouped by depth (depth >= 1)
-  const uint32_t* big_cptr;    // children CSR: net b node i at big_scr[b] + b + i, absolute
-  const uint32_t* big_child;   // child local ids, decreasing within a parent
+  uint32_t nA, nB, nC;       // nets per tier
+  const uint32_t* tierA;     // net ids j with <= kTierA nodes (lumped included)
+  const uint32_t* tierB;     // warp-per-net tier
+  const uint32_t* tierC;     // block-per-net tier
+  const uint32_t* sched_off; // [nB+nC+1] schedule offset of each tier-B/C net (B first)
+  const uint32_t* sched_h;   // per net: height-level boundaries (relative), then nodes by height
+  const uint32_t* sched_hn;  // [nB+nC] number of height levels
+  const uint32_t* sched_d;   // depth-level boundaries / nodes by depth (depth >= 1)
+  const uint32_t* sched_doff;// [nB+nC+1]
+  const uint32_t* sched_dn;  // [nB+nC] number of depth levels
+  const uint32_t* child_off; // [nB+nC+1] offsets into child arrays
+  const uint32_t* child_ptr; // per net: [m+1] relative children CSR
+  const uint32_t* child;     // child local ids, decreasing within a parent
+  // tier C (nets > kTierB nodes), Euler-tour form over ONE global preorder
+  // array of all tier-C nodes (each net contiguous, DFS preorder inside):
+  // Cdown(g) = S[end(g)] - S[g] with S the global exclusive prefix sum of the
+  // node caps, and elm(g) = G[g] - G[start(g) - 1] with G the global inclusive
+  // prefix sum of (+w(g), -w(a) for each a whose subtree ends at g), w = R Cdown.
+  uint32_t nCn;               // tier-C nodes
+  const uint32_t* tc_user;    // [nCn] caller node id (R / Cw index)
+  const uint32_t* tc_int;     // [nCn] internal node id (scap / sink index)
+  const uint32_t* tc_end;     // [nCn] global position one past the subtree
+  const uint32_t* tc_start;   // [nCn] global position of the net's root
+  const uint32_t* tc_eptr;    // [nCn+1] CSR into tc_ends
+  const uint32_t* tc_ends;    // positions a with end(a) == g
+  const uint32_t* tc_root;    // [nC] root position of each tier-C net
+  const uint32_t* tc_drv;     // [nC] its driver (internal pull id)
   // outputs to user order
   const uint32_t* int_of_user; // [P]
+  const uint32_t* drv_of_net;  // [N] user net -> internal driver
 };
 
 // Per-corner device state.
 struct CornerDev {
-  float4* rec;        // [2P]: at, slew per pin (internal order)
+  float4* rec;        // [2 NP]: at, slew of pull pins (internal order)
   float4* rat;        // [P]
   float4* slack;      // [P]
   float* elm;         // [NS] Elmore delay of each sink's net arc
   float* load;        // [NP] NLDM load seen by each pull pin (0 if no net)
   float2* ep_ws;      // [n_ep] worst setup / hold slack per endpoint
   double* res;        // [4]
-  const float* lut;   // table pool
-  const uint32_t* tdesc;
-  const float* rc_res;  // [n_rc] user node order (owned or borrowed)
-  const float* rc_cap;
-  double* scratch;    // big-net scratch: cd then elm
+  double* red_part;   // [kRedBlocks * 4] reduction partials
+  uint32_t* red_cnt;  // [1] last-block counter (self-resetting)
+  int4* heavy_key;    // [n_heavy] ordered-int RAT accumulators (self-resetting)
+  uint32_t* heavy_cnt;// [n_heavy] finished tiles (self-resetting)
+  const float* lut;   // table records (kTabStride floats each)
+  const float* const* rc_vals;  // device {res, cap} pointer pair (user node order)
+  double* scratch;    // tier-C scratch: 3 * (nCn + 1) doubles + scan tiles
   uint32_t* err_flag; // nonzero: bad RC value seen
+  uint32_t* fwd_done; // [S] completed forward chunks per stage (reset by reduce_kernel)
+  uint32_t* bwd_done; // [S] completed backward units per stage (reset by reduce_kernel)
+  unsigned long long* trace;  // optional (STA_TRACE): per chunk / unit {start, ready, end} ns
 };
 
-// ---- launchers (sta_kernels.cu); all enqueue on `s`, return cudaGetLastError()
-struct StagePlan {
-  // host-side per-stage ranges
-  const uint32_t* pull_stage_ptr;  // [S+1] (host)
-  const uint32_t* sink_stage_ptr;  // [S+1] sink ranges of the drivers of each stage (host)
-  const uint32_t* heavy_stage_ptr; // [S+1] (host)
-};
+constexpr int kRedBlocks = 148;
 
-cudaError_t launch_rc(const Topo& t, const CornerDev& c, uint32_t n_small_blocks, cudaStream_t s);
+// ---- launchers (sta_kernels.cu); all enqueue on `s` with programmatic
+// dependent launch, return cudaGetLastError()
+cudaError_t launch_rc(const Topo& t, const CornerDev& c, cudaStream_t s);
+constexpr uint32_t kScanTile = 4096;          // elements per tier-C scan tile
+inline size_t tierC_scratch(uint32_t nCn) {   // doubles
+  const size_t tiles = (nCn + kScanTile - 1) / kScanTile;
+  return 3 * ((size_t)nCn + 1) + 2 * (tiles + 1);
+}
 cudaError_t launch_seed(const Topo& t, const CornerDev& c, uint32_t n0, cudaStream_t s);
-cudaError_t launch_fwd_stage(const Topo& t, const CornerDev& c, uint32_t sinkA0, uint32_t nA,
-                             uint32_t pullB0, uint32_t nB, cudaStream_t s);
-cudaError_t launch_bwd_stage(const Topo& t, const CornerDev& c, uint32_t pull0, uint32_t nPull,
-                             uint32_t heavy0, uint32_t nHeavy, cudaStream_t s);
+// lut_f4: float4 count of the table pool staged in shared memory per block
+// (0: the pool is too large, lookups read global memory)
+cudaError_t launch_fwd_stage(const Topo& t, const CornerDev& c, uint32_t pull0, uint32_t n, uint32_t lut_f4,
+                             cudaStream_t s);
+cudaError_t launch_bwd_stage(const Topo& t, const CornerDev& c, uint32_t tile0, uint32_t nTiles, uint32_t sinkEnd,
+                             uint32_t nos0, uint32_t nNos, uint32_t lut_f4, cudaStream_t s);
+cudaError_t set_lut_smem_limit(size_t bytes);
+// persistent (cooperative, sync-free dataflow) forward / backward passes;
+// grid = co-resident blocks.  persistent_grid returns 0 if unsupported.
+uint32_t persistent_grid(uint32_t lut_f4);
+cudaError_t launch_fwd_persistent(const Topo& t, const CornerDev& c, uint32_t grid, uint32_t lut_f4, cudaStream_t s);
+cudaError_t launch_bwd_persistent(const Topo& t, const CornerDev& c, uint32_t grid, uint32_t lut_f4, cudaStream_t s);
+constexpr size_t kLutSmemMax = 160 * 1024;   // larger pools stay in global memory
 cudaError_t launch_reduce(const Topo& t, const CornerDev& c, cudaStream_t s);
-cudaError_t launch_gather4(const float4* src, const uint32_t* idx, float4* dst, uint32_t n,
-                           uint32_t stride_f4, cudaStream_t s);
-cudaError_t launch_gather_rc(const Topo& t, const CornerDev& c, float* net_load, float* pin_elm,
-                             const uint32_t* net_of_j, const uint32_t* user_of_int, cudaStream_t s);
-cudaError_t launch_check_rc_values(const CornerDev& c, uint32_t n_rc, cudaStream_t s);
+cudaError_t launch_gather_pins(const Topo& t, const CornerDev& c, int what, float4* dst, cudaStream_t s);
+cudaError_t launch_gather_rc(const Topo& t, const CornerDev& c, float* net_load, float* pin_elm, cudaStream_t s);
+cudaError_t launch_init_corner(const Topo& t, const CornerDev& c, uint32_t n_heavy, cudaStream_t s);
 
 }  // namespace sta

@@ -1,24 +1,34 @@
 // sta_kernels.cu -- sm_100a kernels of one graph-based STA timing update.
 //
 // Hot path:
-//   a1  rc_small_kernel / rc_big_kernel  Elmore RC per net: Cdown bottom-up,
-//       load = Cdown[root], elm top-down
+//   a1  rc_tierA/B/C_kernel   Elmore RC per net: Cdown bottom-up, load =
+//       Cdown[root], elm top-down, in fp64;
+//       one thread (<= 8 nodes, registers), one warp (<= 256 nodes, shared
+//       memory) or one block (larger) per net.
 //   a2  seed_kernel + fwd_stage_kernel   arrival/slew, one launch per gate
-//       stage; NLDM bilinear lookup for cell arcs,
-//       Elmore + PERI slew for net arcs, early min / late
-//       max merge
-//   a3-a5 bwd_stage_kernel               endpoint seeds,
-//       required times over fan-out (min late / max early), per-pin slack and
-//       per-endpoint worst slack, one launch per gate stage in reverse
-//   a5  reduce_kernel                    WNS / TNS (TNS in fp64), fixed order
+//       stage, one thread per stage pin; NLDM bilinear lookup for cell arcs
+//       (SPEC.md:371-388), Elmore + PERI slew for net arcs
+//       (SPEC.md:416-418), early-min / late-max merge.
+//   a3-a5 bwd_stage_kernel   endpoint seeds, required
+//       times over the fan-out (late min / early max), per-pin slack and
+//       per-endpoint worst slack; one launch per gate stage in reverse; one
+//       warp per tile of <= 32 consecutive sinks, segmented shuffle reduction
+//       into their drivers, ordered-int atomics only for drivers with more
+//       than 32 sinks.
+//   a5  reduce_kernel   WNS / TNS (TNS in fp64), fixed-order two-level tree.
+//
+// All stage kernels are launched with programmatic dependent launch: the
+// static topology of a stage is read before griddepcontrol.wait, so it
+// overlaps the tail of the previous stage.
 //
 // Numerics: fp32 state, no fast-math.  Every floating-point operation whose
 // result is reused by another kernel (net hop, LUT lookup) is written with
 // explicit round-to-nearest intrinsics so that no FMA-contraction choice of
-// the compiler can make the forward and the backward recomputation of an arc
-// delay differ by one ulp.  RC is accumulated in fp64.
+// the compiler can make two recomputations of the same quantity differ.
 #include <cuda_runtime.h>
 #include <math_constants.h>
+
+#include <algorithm>
 
 #include "sta_internal.h"
 
@@ -28,6 +38,9 @@ namespace {
 
 constexpr float kLn9 = 2.19722457733621956f;   // ln 9: PERI impulse factor
 constexpr int kThreads = 256;
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 struct Q4 {
   float v[4];   // (early_rise, early_fall, late_rise, late_fall)
@@ -42,52 +55,68 @@ __device__ __forceinline__ Q4 undef_at() { return Q4{{CUDART_INF_F, CUDART_INF_F
 // undefined required time: early -inf, late +inf (O7)
 __device__ __forceinline__ Q4 undef_rat() { return Q4{{-CUDART_INF_F, -CUDART_INF_F, CUDART_INF_F, CUDART_INF_F}}; }
 
-__device__ __forceinline__ bool sense_allows(uint32_t sense, int irf, int orf) {
-  switch (sense) {
-    case 0: return irf == orf;          // positive unate
-    case 1: return irf != orf;          // negative unate
-    case 2: return true;                // non-unate
-    case 3: return irf == 0;            // rising edge (clock-to-Q)
-    default: return irf == 1;           // falling edge
-  }
+// NLDM bilinear lookup with boundary-cell extrapolation on the
+// device table pool (layout in sta_internal.h), split into the two axis
+// searches and the interpolation so callers can reuse a search:
+// segment i = clamp(upper_bound(x, s) - 1, 0, n - 2) = #{k : sx[k] <= s}.
+// L points at the pool in shared memory (staged once per block by
+// stage_lut) or, for pools too large for shared memory, in global memory.
+struct Seg {
+  int i;     // segment index
+  float t;   // (s - x_i) / (x_{i+1} - x_i), not clamped (extrapolation)
+};
+
+struct Tab {
+  const float* ax;   // axis template: index_1 at ax, index_2 at ax + 24
+  const float* v;    // values v[8][8]
+};
+
+__device__ __forceinline__ Tab tab_rec(const float* __restrict__ L, uint32_t tab) {
+  const float* b = L + (size_t)tab * kTabStride;
+  return Tab{L + __float_as_int(b[0]), b + 1};
 }
 
-// NLDM bilinear lookup with boundary-cell extrapolation.
-// Segment i = clamp(upper_bound(x, s) - 1, 0, n - 2) = #{k in 1..n-2 : x[k] <= s}.
-__device__ __forceinline__ float lut_eval(const float* __restrict__ pool, uint32_t desc, float s, float c) {
-  const uint32_t off = desc & 0x03FFFFFFu;
-  const int n1 = int((desc >> 26) & 7u) + 1;
-  const int n2 = int((desc >> 29) & 7u) + 1;
-  const float* x = pool + off;
-  const float* y = x + n1;
-  const float* v = y + n2;
-  int i = 0, j = 0;
-#pragma unroll
-  for (int k = 1; k < 7; ++k) {
-    if (k <= n1 - 2 && __ldg(x + k) <= s) ++i;
-    if (k <= n2 - 2 && __ldg(y + k) <= c) ++j;
-  }
-  float tx = 0.f, ty = 0.f;
-  int si = 0, sj = 0;
-  if (n1 > 1) {
-    const float x0 = __ldg(x + i), x1 = __ldg(x + i + 1);
-    tx = __fdiv_rn(__fsub_rn(s, x0), __fsub_rn(x1, x0));
-    si = n2;
-  }
-  if (n2 > 1) {
-    const float y0 = __ldg(y + j), y1 = __ldg(y + j + 1);
-    ty = __fdiv_rn(__fsub_rn(c, y0), __fsub_rn(y1, y0));
-    sj = 1;
-  }
-  const float* p = v + i * n2 + j;
-  const float v00 = __ldg(p), v10 = __ldg(p + si), v01 = __ldg(p + sj), v11 = __ldg(p + si + sj);
-  const float a = __fmaf_rn(tx, __fsub_rn(v10, v00), v00);
-  const float b = __fmaf_rn(tx, __fsub_rn(v11, v01), v01);
-  return __fmaf_rn(ty, __fsub_rn(b, a), a);
+// axis (sx[8], x[8], rx[8])
+__device__ __forceinline__ Seg seg(const float* a, float s) {
+  const float4 sa = *reinterpret_cast<const float4*>(a);
+  const float4 sb = *reinterpret_cast<const float4*>(a + 4);
+  const int i = (sa.y <= s) + (sa.z <= s) + (sa.w <= s) + (sb.x <= s) + (sb.y <= s) + (sb.z <= s);
+  return Seg{i, __fmul_rn(__fsub_rn(s, a[8 + i]), a[16 + i])};
 }
 
-__device__ __forceinline__ float lut_id(const CornerDev& c, uint32_t tab, float s, float ld) {
-  return lut_eval(c.lut, __ldg(c.tdesc + tab), s, ld);
+__device__ __forceinline__ float interp(const Tab& r, Seg si, Seg sj) {
+  const float* v = r.v + si.i * 8 + sj.i;
+  const float v00 = v[0], v01 = v[1], v10 = v[8], v11 = v[9];
+  const float a = __fmaf_rn(si.t, __fsub_rn(v10, v00), v00);
+  const float b = __fmaf_rn(si.t, __fsub_rn(v11, v01), v01);
+  return __fmaf_rn(sj.t, __fsub_rn(b, a), a);
+}
+
+__device__ __forceinline__ float lut(const float* __restrict__ L, uint32_t tab, float s, float c) {
+  const Tab r = tab_rec(L, tab);
+  return interp(r, seg(r.ax, s), seg(r.ax + 24, c));
+}
+
+// Input edge of the (first) candidate pair producing output edge orf
+// (SPEC.md:383): positive unate / non-unate r->r f->f, negative unate
+// crosses, rising edge from r, falling edge from f.  Only non-unate arcs have
+// a second candidate (irf = 1 - primary).
+__device__ __forceinline__ int primary_irf(uint32_t sense, int orf) {
+  return sense == 1 ? 1 - orf : sense == 3 ? 0 : sense == 4 ? 1 : orf;
+}
+
+// Copy the table records into shared memory (static data: may run before
+// griddepcontrol.wait).  Returns the pointer lookups should use.  SMEM is a
+// compile-time choice so that lookups compile to LDS (a pointer that may be
+// shared or global compiles to slow generic loads).
+extern __shared__ float4 s_dyn[];
+template <bool SMEM>
+__device__ __forceinline__ const float* stage_lut(const CornerDev& c, uint32_t n_f4) {
+  if (!SMEM) return c.lut;                   // pool too large: global / L1
+  const float4* g = reinterpret_cast<const float4*>(c.lut);
+  for (uint32_t x = threadIdx.x; x < n_f4; x += blockDim.x) s_dyn[x] = __ldg(g + x);
+  __syncthreads();
+  return reinterpret_cast<const float*>(s_dyn);
 }
 
 // Net arc driver -> sink: AT + elm, slew = sqrt(slew^2 + (ln9 elm)^2) (PERI,
@@ -97,32 +126,41 @@ __device__ __forceinline__ void net_hop(Q4& at, Q4& sl, float e) {
   const float imp2 = __fmul_rn(imp, imp);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    if (fin(at.v[q])) {
-      at.v[q] = __fadd_rn(at.v[q], e);
-      sl.v[q] = __fsqrt_rn(__fmaf_rn(sl.v[q], sl.v[q], imp2));
-    } else {
-      sl.v[q] = q < 2 ? CUDART_INF_F : -CUDART_INF_F;
-    }
+    const bool ok = fin(at.v[q]);
+    at.v[q] = ok ? __fadd_rn(at.v[q], e) : at.v[q];
+    sl.v[q] = ok ? __fsqrt_rn(__fmaf_rn(sl.v[q], sl.v[q], imp2)) : (q < 2 ? CUDART_INF_F : -CUDART_INF_F);
   }
 }
 
-// Cell arc u -> v (forward): merge candidates of every (el, irf -> orf) pair
-// the sense allows into acc_at / acc_sl (early min, late max).
-__device__ __forceinline__ void cell_fwd(const CornerDev& c, const Q4& at, const Q4& sl, uint32_t info,
+// Cell arc u -> v (forward): merge the candidates of every (el, irf -> orf)
+// pair the sense allows into acc_at / acc_sl (early min, late max).  The load
+// axis search of each of the 4 tables is done once per arc.
+__device__ __forceinline__ void cell_fwd(const float* __restrict__ L, const Q4& at, const Q4& sl, uint32_t info,
                                          float ld, Q4& acc_at, Q4& acc_sl) {
   const uint32_t sense = info & 7u, tab = info >> 3;
+  const Tab rd0 = tab_rec(L, tab);            // cell_rise
+  const Tab rd1 = tab_rec(L, tab + 1);        // cell_fall
+  const Tab rs0 = tab_rec(L, tab + 2);        // rise_transition
+  const Tab rs1 = tab_rec(L, tab + 3);        // fall_transition
+  const Seg cd0 = seg(rd0.ax + 24, ld), cd1 = seg(rd1.ax + 24, ld);
+  const Seg cs0 = seg(rs0.ax + 24, ld), cs1 = seg(rs1.ax + 24, ld);
 #pragma unroll
-  for (int el = 0; el < 2; ++el) {
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1 && sense != 2) break;        // second candidate: non-unate only
 #pragma unroll
-    for (int irf = 0; irf < 2; ++irf) {
-      const float a_in = at.v[el * 2 + irf];
-      if (!fin(a_in)) continue;
-      const float s_in = sl.v[el * 2 + irf];
+    for (int orf = 0; orf < 2; ++orf) {
+      const int irf = pass ? 1 - primary_irf(sense, orf) : primary_irf(sense, orf);
+      const Tab rd = orf ? rd1 : rd0;
+      const Tab rs = orf ? rs1 : rs0;
+      const Seg cd = orf ? cd1 : cd0;
+      const Seg cs = orf ? cs1 : cs0;
 #pragma unroll
-      for (int orf = 0; orf < 2; ++orf) {
-        if (!sense_allows(sense, irf, orf)) continue;
-        const float d = fmaxf(0.f, lut_id(c, tab + orf, s_in, ld));
-        const float so = fmaxf(0.f, lut_id(c, tab + 2 + orf, s_in, ld));
+      for (int el = 0; el < 2; ++el) {
+        const float a_in = irf ? at.v[el * 2 + 1] : at.v[el * 2];
+        const float s_in = irf ? sl.v[el * 2 + 1] : sl.v[el * 2];
+        if (!fin(a_in)) continue;
+        const float d = fmaxf(0.f, interp(rd, seg(rd.ax, s_in), cd));
+        const float so = fmaxf(0.f, interp(rs, seg(rs.ax, s_in), cs));
         const float ca = __fadd_rn(a_in, d);
         const int q = el * 2 + orf;
         if (el == 0) { acc_at.v[q] = fminf(acc_at.v[q], ca); acc_sl.v[q] = fminf(acc_sl.v[q], so); }
@@ -134,23 +172,30 @@ __device__ __forceinline__ void cell_fwd(const CornerDev& c, const Q4& at, const
 
 // Cell arc u -> w (backward): RAT_L(u,irf) = min(RAT_L(w,orf) - d), RAT_E =
 // max(RAT_E(w,orf) - d) over exactly the pairs the forward pass used, with d
-// recomputed bit-identically from slew(u) and load(w).
-__device__ __forceinline__ void cell_bwd(const CornerDev& c, const Q4& at_u, const Q4& sl_u, uint32_t info,
-                                         float ld, const Q4& rat_w, Q4& acc) {
+// recomputed bit-identically (same seg / interp calls) from slew(u), load(w).
+__device__ __forceinline__ void cell_bwd(const float* __restrict__ L, const Q4& at_u, const Q4& sl_u,
+                                         uint32_t info, float ld, const Q4& rat_w, Q4& acc) {
   const uint32_t sense = info & 7u, tab = info >> 3;
+  const Tab rd0 = tab_rec(L, tab);
+  const Tab rd1 = tab_rec(L, tab + 1);
+  const Seg cd0 = seg(rd0.ax + 24, ld), cd1 = seg(rd1.ax + 24, ld);
 #pragma unroll
-  for (int el = 0; el < 2; ++el) {
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1 && sense != 2) break;
 #pragma unroll
-    for (int irf = 0; irf < 2; ++irf) {
-      if (!fin(at_u.v[el * 2 + irf])) continue;
-      const float s_in = sl_u.v[el * 2 + irf];
+    for (int orf = 0; orf < 2; ++orf) {
+      const int irf = pass ? 1 - primary_irf(sense, orf) : primary_irf(sense, orf);
+      const Tab rd = orf ? rd1 : rd0;
+      const Seg cd = orf ? cd1 : cd0;
 #pragma unroll
-      for (int orf = 0; orf < 2; ++orf) {
-        if (!sense_allows(sense, irf, orf)) continue;
-        const float d = fmaxf(0.f, lut_id(c, tab + orf, s_in, ld));
+      for (int el = 0; el < 2; ++el) {
+        const float a_in = irf ? at_u.v[el * 2 + 1] : at_u.v[el * 2];
+        const float s_in = irf ? sl_u.v[el * 2 + 1] : sl_u.v[el * 2];
+        if (!fin(a_in)) continue;
+        const float d = fmaxf(0.f, interp(rd, seg(rd.ax, s_in), cd));
         const float cand = __fsub_rn(rat_w.v[el * 2 + orf], d);
-        const int q = el * 2 + irf;
-        acc.v[q] = el == 0 ? fmaxf(acc.v[q], cand) : fminf(acc.v[q], cand);
+        if (irf) acc.v[el * 2 + 1] = el == 0 ? fmaxf(acc.v[1], cand) : fminf(acc.v[3], cand);
+        else     acc.v[el * 2] = el == 0 ? fmaxf(acc.v[0], cand) : fminf(acc.v[2], cand);
       }
     }
   }
@@ -159,8 +204,8 @@ __device__ __forceinline__ void cell_bwd(const CornerDev& c, const Q4& at_u, con
 // Endpoint required-time seeds: PO: RAT_L = T - out_max,
 // RAT_E = -out_min; check: RAT_L = T - setup(slew_L(D), clock slew),
 // RAT_E = hold(slew_E(D), clock slew), only where the data arrival exists.
-__device__ __forceinline__ void apply_seed(const Topo& t, const CornerDev& c, uint32_t e, const Q4& at,
-                                           const Q4& sl, Q4& r) {
+__device__ __forceinline__ void apply_seed(const Topo& t, const CornerDev& c, const float* L, uint32_t e,
+                                           const Q4& at, const Q4& sl, Q4& r) {
   const EpRec ep = t.ep[e];
   if (ep.po != kNone) {
     const float2 omax = t.po_out_max[ep.po], omin = t.po_out_min[ep.po];
@@ -173,9 +218,9 @@ __device__ __forceinline__ void apply_seed(const Topo& t, const CornerDev& c, ui
 #pragma unroll
     for (int rf = 0; rf < 2; ++rf) {
       if (fin(at.v[2 + rf]))
-        r.v[2 + rf] = fminf(r.v[2 + rf], __fsub_rn(t.period, lut_id(c, ep.chk_tab + rf, sl.v[2 + rf], t.clock_slew)));
+        r.v[2 + rf] = fminf(r.v[2 + rf], __fsub_rn(t.period, lut(L, ep.chk_tab + rf, sl.v[2 + rf], t.clock_slew)));
       if (fin(at.v[rf]))
-        r.v[rf] = fmaxf(r.v[rf], lut_id(c, ep.chk_tab + 2 + rf, sl.v[rf], t.clock_slew));
+        r.v[rf] = fmaxf(r.v[rf], lut(L, ep.chk_tab + 2 + rf, sl.v[rf], t.clock_slew));
     }
   }
 }
@@ -195,98 +240,291 @@ __device__ __forceinline__ void write_ep(const CornerDev& c, uint32_t e, const Q
   c.ep_ws[e] = make_float2(fminf(s.v[2], s.v[3]), fminf(s.v[0], s.v[1]));
 }
 
+// records written by earlier kernels of this update: L2 loads (keep L1 for LUTs)
 __device__ __forceinline__ void load_rec(const CornerDev& c, uint32_t i, Q4& at, Q4& sl) {
-  at = to_q(__ldg(c.rec + 2 * (size_t)i));
-  sl = to_q(__ldg(c.rec + 2 * (size_t)i + 1));
+  at = to_q(__ldcg(c.rec + 2 * (size_t)i));
+  sl = to_q(__ldcg(c.rec + 2 * (size_t)i + 1));
 }
+
+// ordered-int image of a float: monotone for signed-int comparison
+__device__ __forceinline__ int f2o(float f) {
+  const int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float o2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
 
 // ------------------------------------------------------------------ a1: RC
 __device__ __forceinline__ bool bad_rc(float r, float cw) {
   return !(r >= 0.f) || !(cw >= 0.f) || !(r < CUDART_INF_F) || !(cw < CUDART_INF_F);
 }
 
-// One thread per net with <= kSmallNet RC nodes (and lumped nets): the
-// textbook O(n) two-pass recursion, in fp64.
-__global__ void __launch_bounds__(kThreads) rc_small_kernel(Topo t, CornerDev c) {
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= t.N) return;
+// Tier A: one thread per net with <= kTierA nodes (lumped nets included);
+// the textbook two-pass recursion in registers, fp64.  Children are added to
+// a parent in decreasing index order, the order the warp / block tiers use.
+__global__ void __launch_bounds__(kThreads) rc_tierA_kernel(Topo t, CornerDev c) {
+  pdl_wait();
+  pdl_launch();
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= t.nA) return;
+  const uint32_t j = t.tierA[x];
   const uint32_t drv = t.net_drv[j];
-  const uint32_t m = t.net_rcn[j];
-  const uint32_t sb = t.sink_ptr[drv], se = t.sink_ptr[drv + 1];
+  const uint32_t b = t.net_node[j];
+  const uint32_t m = t.net_node[j + 1] - b;
   if (m == 0) {                            // lumped net
     c.load[drv] = t.net_lumped[j];
-    for (uint32_t k = sb; k < se; ++k) c.elm[k] = 0.f;
+    for (uint32_t k = t.sink_ptr[drv]; k < t.sink_ptr[drv + 1]; ++k) c.elm[k] = 0.f;
     return;
   }
-  if (m > (uint32_t)kSmallNet) return;
-  const uint32_t b = t.net_rc[j];
-  double cd[kSmallNet];
+  const float* R = c.rc_vals[0] + t.net_user[j];
+  const float* Cw = c.rc_vals[1] + t.net_user[j];
+  double cd[kTierA], el[kTierA];
+  int par[kTierA];
+  float r[kTierA];
   bool bad = false;
-  for (uint32_t i = 0; i < m; ++i) {
-    const float cw = c.rc_cap[b + i];
-    const float r = c.rc_res[b + i];
-    bad |= bad_rc(i ? r : 0.f, cw);
-    cd[i] = (double)cw + (double)t.rc_scap[b + i];
+#pragma unroll
+  for (int i = 0; i < kTierA; ++i) {
+    if (i < (int)m) {
+      par[i] = t.rc_parent[b + i];
+      r[i] = i ? R[i] : 0.f;
+      const float cw = Cw[i];
+      bad |= bad_rc(r[i], cw);
+      cd[i] = (double)cw + (double)t.rc_scap[b + i];
+    } else {
+      par[i] = 0; r[i] = 0.f; cd[i] = 0.0;
+    }
   }
-  for (uint32_t i = m - 1; i >= 1; --i) cd[t.rc_parent[b + i]] += cd[i];
+#pragma unroll
+  for (int i = kTierA - 1; i >= 1; --i) {
+    if (i < (int)m) {
+#pragma unroll
+      for (int k = 0; k < i; ++k)
+        if (k == par[i]) cd[k] += cd[i];
+    }
+  }
   c.load[drv] = (float)cd[0];
-  double el[kSmallNet];
   el[0] = 0.0;
-  for (uint32_t i = 1; i < m; ++i) {
-    el[i] = __fma_rn((double)c.rc_res[b + i], cd[i], el[t.rc_parent[b + i]]);
-    const uint32_t k = t.rc_sink[b + i];
-    if (k != kNone) c.elm[k] = (float)el[i];
+#pragma unroll
+  for (int i = 1; i < kTierA; ++i) {
+    double ep = 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k)
+      if (k == par[i]) ep = el[k];
+    el[i] = __fma_rn((double)r[i], cd[i], ep);
+    if (i < (int)m) {
+      const uint32_t k = t.rc_sink[b + i];
+      if (k != kNone) c.elm[k] = (float)el[i];
+    }
   }
   if (bad) atomicOr(c.err_flag, 1u);
 }
 
-// One block per big net: Cdown by height level (children summed in
-// decreasing index order -- the same rounding order as the sequential
-// recursion), then Elmore by depth level.
-__global__ void __launch_bounds__(kThreads) rc_big_kernel(Topo t, CornerDev c) {
-  const uint32_t bi = blockIdx.x;
-  const uint32_t j = t.big_net[bi];
+// Tier B: one warp per net (<= kTierB nodes), height-level Cdown and
+// depth-level Elmore in shared memory.
+constexpr int kWarpsB = 4;
+__global__ void __launch_bounds__(32 * kWarpsB) rc_tierB_kernel(Topo t, CornerDev c) {
+  __shared__ double s_cd[kWarpsB][kTierB];
+  __shared__ double s_el[kWarpsB][kTierB];
+  pdl_wait();
+  pdl_launch();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t x = blockIdx.x * kWarpsB + w;
+  if (x >= t.nB) return;
+  const uint32_t j = t.tierB[x];
   const uint32_t drv = t.net_drv[j];
-  const uint32_t b = t.net_rc[j];
-  double* cd = c.scratch + t.big_scr[bi];
-  double* el = c.scratch + t.big_scr[t.n_big] + t.big_scr[bi];
-  const uint32_t* cptr = t.big_cptr + t.big_scr[bi] + bi;
+  const uint32_t b = t.net_node[j];
+  const uint32_t m = t.net_node[j + 1] - b;
+  const float* R = c.rc_vals[0] + t.net_user[j];
+  const float* Cw = c.rc_vals[1] + t.net_user[j];
+  double* cd = s_cd[w];
+  double* el = s_el[w];
   bool bad = false;
-  for (uint32_t h = t.big_hptr_off[bi]; h + 1 < t.big_hptr_off[bi + 1]; ++h) {
-    for (uint32_t x = t.big_hptr[h] + threadIdx.x; x < t.big_hptr[h + 1]; x += blockDim.x) {
-      const uint32_t p = t.big_hnode[x];
-      const float cw = c.rc_cap[b + p];
-      bad |= bad_rc(p ? c.rc_res[b + p] : 0.f, cw);
-      double v = (double)cw + (double)t.rc_scap[b + p];
-      for (uint32_t k = cptr[p]; k < cptr[p + 1]; ++k) v += cd[t.big_child[k]];
+  for (uint32_t i = lane; i < m; i += 32) {
+    const float cw = Cw[i];
+    bad |= bad_rc(i ? R[i] : 0.f, cw);
+    cd[i] = (double)cw + (double)t.rc_scap[b + i];
+  }
+  __syncwarp();
+  const uint32_t* sh = t.sched_h + t.sched_off[x];
+  const uint32_t hn = t.sched_hn[x];
+  const uint32_t* nodes = sh + hn + 1;
+  const uint32_t* cp = t.child_ptr + t.child_off[x];
+  for (uint32_t h = 0; h < hn; ++h) {
+    for (uint32_t y = sh[h] + lane; y < sh[h + 1]; y += 32) {
+      const uint32_t p = nodes[y];
+      double v = cd[p];
+      for (uint32_t q = cp[p]; q < cp[p + 1]; ++q) v += cd[t.child[q]];
       cd[p] = v;
     }
-    __syncthreads();
+    __syncwarp();
   }
-  if (threadIdx.x == 0) {
+  if (lane == 0) {
     c.load[drv] = (float)cd[0];
     el[0] = 0.0;
   }
-  __syncthreads();
-  for (uint32_t h = t.big_dptr_off[bi]; h + 1 < t.big_dptr_off[bi + 1]; ++h) {
-    for (uint32_t x = t.big_dptr[h] + threadIdx.x; x < t.big_dptr[h + 1]; x += blockDim.x) {
-      const uint32_t i = t.big_dnode[x];
-      const double e = __fma_rn((double)c.rc_res[b + i], cd[i], el[t.rc_parent[b + i]]);
+  __syncwarp();
+  const uint32_t* sd = t.sched_d + t.sched_doff[x];
+  const uint32_t dn = t.sched_dn[x];
+  const uint32_t* dnodes = sd + dn + 1;
+  for (uint32_t h = 0; h < dn; ++h) {
+    for (uint32_t y = sd[h] + lane; y < sd[h + 1]; y += 32) {
+      const uint32_t i = dnodes[y];
+      const double e = __fma_rn((double)R[i], cd[i], el[t.rc_parent[b + i]]);
       el[i] = e;
       const uint32_t k = t.rc_sink[b + i];
       if (k != kNone) c.elm[k] = (float)e;
     }
-    __syncthreads();
+    __syncwarp();
   }
-  if (bad) atomicOr(c.err_flag, 1u);
+  if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(c.err_flag, 1u);
+}
+
+// ---- tier C: Euler-tour RC over one global preorder array (sta_internal.h)
+// Device-wide fp64 prefix sums by reduce-then-scan with a fixed tiling
+// (bitwise reproducible): tile sums, one-block scan of the tile sums, then
+// per-tile scan plus offset.
+constexpr int kScanThreads = 1024;
+constexpr int kScanPer = kScanTile / kScanThreads;   // 4 elements per thread
+
+__device__ __forceinline__ double block_excl_scan(double v, double* s_warp, double* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_warp[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    double x = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0.0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+      if (lane >= o) x += y;
+    }
+    s_warp[lane] = x;                             // inclusive over warps
+  }
+  __syncthreads();
+  double excl = __shfl_up_sync(0xFFFFFFFFu, inc, 1);
+  if (lane == 0) excl = 0.0;
+  if (total) *total = s_warp[(blockDim.x >> 5) - 1];
+  const double r = (w ? s_warp[w - 1] : 0.0) + excl;
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_tiles_kernel(const double* __restrict__ x, uint32_t n,
+                                                                  double* __restrict__ tsum) {
+  __shared__ double s_warp[32];
+  pdl_wait();
+  pdl_launch();
+  const uint32_t base = blockIdx.x * kScanTile + threadIdx.x * kScanPer;
+  double v = 0.0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k)
+    if (base + k < n) v += x[base + k];
+  double tot;
+  block_excl_scan(v, s_warp, &tot);
+  if (threadIdx.x == 0) tsum[blockIdx.x] = tot;
+}
+
+// one block: exclusive scan of the tile sums; x[n] receives the grand total
+__global__ void __launch_bounds__(kScanThreads) scan_offsets_kernel(const double* __restrict__ tsum, uint32_t ntiles,
+                                                                    double* __restrict__ toff, double* x, uint32_t n) {
+  __shared__ double s_warp[32];
+  pdl_wait();
+  pdl_launch();
+  double carry = 0.0;
+  for (uint32_t b0 = 0; b0 < ntiles; b0 += blockDim.x) {
+    const uint32_t i = b0 + threadIdx.x;
+    const double v = i < ntiles ? tsum[i] : 0.0;
+    double tot;
+    const double e = block_excl_scan(v, s_warp, &tot);
+    if (i < ntiles) toff[i] = carry + e;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) x[n] = carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(double* x, uint32_t n,
+                                                                  const double* __restrict__ toff, int inclusive) {
+  __shared__ double s_warp[32];
+  pdl_wait();
+  pdl_launch();
+  const uint32_t base = blockIdx.x * kScanTile + threadIdx.x * kScanPer;
+  double v[kScanPer];
+  double sum = 0.0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    v[k] = base + k < n ? x[base + k] : 0.0;
+    sum += v[k];
+  }
+  double run = toff[blockIdx.x] + block_excl_scan(sum, s_warp, nullptr);
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    if (inclusive) run += v[k];
+    if (base + k < n) x[base + k] = run;
+    if (!inclusive) run += v[k];
+  }
+}
+
+// node caps in preorder
+__global__ void __launch_bounds__(kThreads) tc_cap_kernel(Topo t, CornerDev c, double* A) {
+  pdl_wait();
+  pdl_launch();
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= t.nCn) return;
+  const uint32_t u = t.tc_user[g];
+  const float cw = c.rc_vals[1][u];
+  const float r = g == t.tc_start[g] ? 0.f : c.rc_vals[0][u];
+  if (bad_rc(r, cw)) atomicOr(c.err_flag, 1u);
+  A[g] = (double)cw + (double)t.rc_scap[t.tc_int[g]];
+}
+
+// Cdown = S[end] - S[g]; w = R Cdown on the edge into the node; net loads
+__global__ void __launch_bounds__(kThreads) tc_w_kernel(Topo t, CornerDev c, const double* S, double* W) {
+  pdl_wait();
+  pdl_launch();
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < t.nC) {
+    const uint32_t r = t.tc_root[g];
+    c.load[t.tc_drv[g]] = (float)(S[t.tc_end[r]] - S[r]);
+  }
+  if (g >= t.nCn) return;
+  const double cd = S[t.tc_end[g]] - S[g];
+  W[g] = g == t.tc_start[g] ? 0.0 : (double)c.rc_vals[0][t.tc_user[g]] * cd;
+}
+
+// D[g] = w(g) - sum of w(a) over subtrees a ending at g
+__global__ void __launch_bounds__(kThreads) tc_d_kernel(Topo t, const double* W, double* D) {
+  pdl_wait();
+  pdl_launch();
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= t.nCn) return;
+  double v = W[g];
+  for (uint32_t q = t.tc_eptr[g]; q < t.tc_eptr[g + 1]; ++q) v -= W[t.tc_ends[q]];
+  D[g] = v;
+}
+
+// elm(g) = G[g] - G[start - 1]
+__global__ void __launch_bounds__(kThreads) tc_elm_kernel(Topo t, CornerDev c, const double* G) {
+  pdl_wait();
+  pdl_launch();
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= t.nCn) return;
+  const uint32_t st = t.tc_start[g];
+  const uint32_t k = t.rc_sink[t.tc_int[g]];
+  if (k != kNone) c.elm[k] = (float)(G[g] - (st ? G[st - 1] : 0.0));
 }
 
 // ------------------------------------------------------------ a2: forward
 // Stage-0 pull pins (no fan-in): PI arrivals, ideal clock, or undefined.
 __global__ void __launch_bounds__(kThreads) seed_kernel(Topo t, CornerDev c, uint32_t n0) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t s = i < n0 ? t.seed[i] : kNone;
+  pdl_wait();
+  pdl_launch();
   if (i >= n0) return;
-  const uint32_t s = t.seed[i];
   float4 at, sl;
   if (s == kNone) {
     at = to_f4(undef_at());
@@ -303,79 +541,79 @@ __global__ void __launch_bounds__(kThreads) seed_kernel(Topo t, CornerDev c, uin
   c.rec[2 * (size_t)i + 1] = sl;
 }
 
-// One launch per gate stage s >= 1.  Items [0, nA): materialize the sinks of
-// the stage s-1 drivers.  Items [nA, nA+nB): pull pins of stage s, each
-// merging its cell fan-in; a fan-in pin that is a net sink is recomputed
-// inline from its driver (pull-through), so sinks never cost a stage.
-__global__ void __launch_bounds__(kThreads) fwd_stage_kernel(Topo t, CornerDev c, uint32_t sinkA0, uint32_t nA,
-                                                             uint32_t pullB0, uint32_t nB) {
-  const uint32_t item = blockIdx.x * blockDim.x + threadIdx.x;
-  if (item < nA) {
-    const uint32_t k = sinkA0 + item;
-    Q4 at, sl;
-    load_rec(c, t.sink_drv[k], at, sl);
-    net_hop(at, sl, c.elm[k]);
-    const size_t u = (size_t)t.NP + k;
-    c.rec[2 * u] = to_f4(at);
-    c.rec[2 * u + 1] = to_f4(sl);
-    return;
+// One launch per gate stage s >= 1: each thread merges the cell fan-in of
+// one stage pin.  A fan-in pin that is a net sink is recomputed inline from
+// its driver's record (pull-through), so sinks never cost a stage.
+template <bool SMEM_LUT>
+__global__ void __launch_bounds__(kThreads) fwd_stage_kernel(Topo t, CornerDev c, uint32_t pull0, uint32_t n,
+                                                             uint32_t lut_f4) {
+  const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t v = pull0 + i;
+  uint32_t e0 = 0, e1 = 0, src0 = 0, hop0 = kNone, info0 = 0;
+  if (i < n) {                               // static topology: before the wait
+    e0 = t.fi_ptr[v];
+    e1 = t.fi_ptr[v + 1];
+    if (e1 > e0) { src0 = t.fi_src[e0]; hop0 = t.fi_hop[e0]; info0 = t.fi_info[e0]; }
   }
-  if (item >= nA + nB) return;
-  const uint32_t v = pullB0 + (item - nA);
-  const float ld = c.load[v];
+  pdl_wait();
+  pdl_launch();
+  if (i >= n) return;
+  const float ld = __ldcg(c.load + v);
   Q4 acc_at = undef_at(), acc_sl = undef_at();
-  const uint32_t e0 = t.fi_ptr[v], e1 = t.fi_ptr[v + 1];
   for (uint32_t e = e0; e < e1; ++e) {
-    const uint32_t src = t.fi_src[e], hop = t.fi_hop[e], info = t.fi_info[e];
+    uint32_t src = src0, hop = hop0, info = info0;
+    if (e != e0) { src = t.fi_src[e]; hop = t.fi_hop[e]; info = t.fi_info[e]; }
     Q4 at, sl;
     load_rec(c, src, at, sl);
-    if (hop != kNone) net_hop(at, sl, c.elm[hop]);
-    cell_fwd(c, at, sl, info, ld, acc_at, acc_sl);
+    if (hop != kNone) net_hop(at, sl, __ldcg(c.elm + hop));
+    cell_fwd(L, at, sl, info, ld, acc_at, acc_sl);
   }
   c.rec[2 * (size_t)v] = to_f4(acc_at);
   c.rec[2 * (size_t)v + 1] = to_f4(acc_sl);
 }
 
+// ---------------------------------------------- inter-block dataflow flags
+// Persistent kernels publish completed work with a release store / atomic
+// after a block barrier and a gpu-scope fence.  Consumers poll the flag with
+// relaxed gpu-scope loads and, once it is set, read the produced records with
+// L2-only loads (ld.global.cg): the records reached L2 before the flag
+// (producer fence), the consumer's record loads are issued only after the
+// flag value returned (control dependency), and no L1 copy can be stale.  An
+// ld.acquire.gpu here would compile to CCTL.IVALL (whole-L1 invalidate),
+// which profiling showed to cost half of the kernel time.
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// wait until *f >= target (wrap-around safe)
+__device__ __forceinline__ void wait_ge(const uint32_t* f, uint32_t target) {
+  if ((int)(ld_acquire(f) - target) >= 0) return;
+  while ((int)(ld_acquire(f) - target) < 0) __nanosleep(64);
+}
+// backward: every unit of the stage of pull pin w is complete
+template <bool WAIT>
+__device__ __forceinline__ void wait_pull(const Topo& t, const CornerDev& c, uint32_t w) {
+  if (!WAIT) return;
+  const uint32_t s = __ldg(t.chunk_stage + w / kChunk);
+  wait_ge(c.bwd_done + s, __ldg(t.stage_units + s));
+}
+
 // ------------------------------------------------------ a3-a5: backward
-// Required time of sink k (internal id NP + k): its endpoint seed combined
-// with its cell fan-out.  Writes rat / slack / endpoint worst slack of the sink.
-__device__ __forceinline__ Q4 sink_rat(const Topo& t, const CornerDev& c, uint32_t k) {
-  const uint32_t u = t.NP + k;
-  Q4 at, sl;
-  load_rec(c, u, at, sl);
-  Q4 r = undef_rat();
-  const uint32_t e = t.pin_ep[u];
-  if (e != kNone) apply_seed(t, c, e, at, sl, r);
-  for (uint32_t x = t.sfo_ptr[k]; x < t.sfo_ptr[k + 1]; ++x) {
-    const uint32_t w = t.sfo_dst[x];
-    const Q4 rw = to_q(__ldg(c.rat + w));
-    cell_bwd(c, at, sl, t.sfo_info[x], c.load[w], rw, r);
-  }
-  c.rat[u] = to_f4(r);
-  const Q4 s = slack_of(at, r);
-  c.slack[u] = to_f4(s);
-  if (e != kNone) write_ep(c, e, s);
-  return r;
-}
-
-// Candidate of a driver from one of its sinks through the net arc.
-__device__ __forceinline__ void net_bwd(const Q4& at_v, const Q4& r_u, float e, Q4& acc) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    if (!fin(at_v.v[q])) continue;
-    const float cand = __fsub_rn(r_u.v[q], e);
-    acc.v[q] = q < 2 ? fmaxf(acc.v[q], cand) : fminf(acc.v[q], cand);
-  }
-}
-
 // Finish a pull pin: own seed, direct cell fan-out, then rat / slack.
-__device__ __forceinline__ void finish_pull(const Topo& t, const CornerDev& c, uint32_t v, const Q4& at,
-                                            const Q4& sl, Q4 acc) {
+template <bool WAIT>
+__device__ __forceinline__ void finish_pull(const Topo& t, const CornerDev& c, const float* L, uint32_t v,
+                                            const Q4& at, const Q4& sl, Q4 acc) {
   const uint32_t e = t.pin_ep[v];
-  if (e != kNone) apply_seed(t, c, e, at, sl, acc);
+  if (e != kNone) apply_seed(t, c, L, e, at, sl, acc);
   for (uint32_t x = t.pfo_ptr[v]; x < t.pfo_ptr[v + 1]; ++x) {
     const uint32_t w = t.pfo_dst[x];
-    cell_bwd(c, at, sl, t.pfo_info[x], c.load[w], to_q(__ldg(c.rat + w)), acc);
+    wait_pull<WAIT>(t, c, w);
+    cell_bwd(L, at, sl, t.pfo_info[x], __ldcg(c.load + w), to_q(__ldcg(c.rat + w)), acc);
   }
   c.rat[v] = to_f4(acc);
   const Q4 s = slack_of(at, acc);
@@ -383,158 +621,561 @@ __device__ __forceinline__ void finish_pull(const Topo& t, const CornerDev& c, u
   if (e != kNone) write_ep(c, e, s);
 }
 
-// One launch per gate stage s (descending).  Blocks [0, nLightBlocks): one
-// thread per pull pin of the stage with <= kHeavyFanout sinks, which also
-// owns its sinks.  Remaining blocks: one block per heavy driver.
-__global__ void __launch_bounds__(kThreads) bwd_stage_kernel(Topo t, CornerDev c, uint32_t pull0, uint32_t nPull,
-                                                             uint32_t heavy0, uint32_t nLightBlocks) {
-  if (blockIdx.x < nLightBlocks) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nPull) return;
-    const uint32_t v = pull0 + i;
-    const uint32_t sb = t.sink_ptr[v], se = t.sink_ptr[v + 1];
-    if (se - sb > (uint32_t)kHeavyFanout) return;
-    Q4 at, sl;
-    load_rec(c, v, at, sl);
-    Q4 acc = undef_rat();
-    for (uint32_t k = sb; k < se; ++k) {
-      const Q4 r = sink_rat(t, c, k);
-      net_bwd(at, r, c.elm[k], acc);
+__device__ __forceinline__ void combine(Q4& a, const Q4& b) {
+  a.v[0] = fmaxf(a.v[0], b.v[0]);
+  a.v[1] = fmaxf(a.v[1], b.v[1]);
+  a.v[2] = fminf(a.v[2], b.v[2]);
+  a.v[3] = fminf(a.v[3], b.v[3]);
+}
+
+// Static part of a backward tile lane (readable before the previous stage ends).
+struct TileLane {
+  uint2 td;
+  uint32_t k, v, e, f0, f1;
+  bool active;
+};
+
+__device__ __forceinline__ TileLane tile_lane(const Topo& t, uint32_t tile, uint32_t k1) {
+  TileLane x;
+  x.td = t.tiles[tile];
+  x.k = x.td.x + (threadIdx.x & 31);
+  x.active = x.k < k1;
+  x.v = kNone; x.e = kNone; x.f0 = 0; x.f1 = 0;
+  if (x.active) {
+    x.v = t.sink_drv[x.k];
+    x.e = t.pin_ep[t.NP + x.k];
+    x.f0 = t.sfo_ptr[x.k];
+    x.f1 = t.sfo_ptr[x.k + 1];
+  }
+  return x;
+}
+
+// One warp, one tile of <= 32 consecutive sinks of one stage's drivers: each
+// lane owns one sink (required time from its endpoint seed and its cell
+// fan-out, then rat / slack), and a segmented shuffle reduction by driver
+// produces the drivers' required times.  Drivers with more than 32 sinks
+// (heavy slot) combine their tiles with ordered-int atomics; the last tile
+// finishes them.
+template <bool WAIT>
+__device__ __forceinline__ void process_tile(const Topo& t, const CornerDev& c, const float* L, const TileLane& x) {
+  const int lane = threadIdx.x & 31;
+  Q4 at_v = undef_at(), sl_v = undef_at(), acc = undef_rat();
+  if (x.active) {
+    load_rec(c, x.v, at_v, sl_v);
+    const float el = __ldcg(c.elm + x.k);
+    Q4 at = at_v, sl = sl_v;
+    net_hop(at, sl, el);                    // the sink's own arrival / slew
+    Q4 r = undef_rat();
+    if (x.e != kNone) apply_seed(t, c, L, x.e, at, sl, r);
+    for (uint32_t f = x.f0; f < x.f1; ++f) {
+      const uint32_t w = t.sfo_dst[f];
+      wait_pull<WAIT>(t, c, w);
+      cell_bwd(L, at, sl, t.sfo_info[f], __ldcg(c.load + w), to_q(__ldcg(c.rat + w)), r);
     }
-    finish_pull(t, c, v, at, sl, acc);
+    const size_t u = (size_t)t.NP + x.k;
+    c.rat[u] = to_f4(r);
+    const Q4 s = slack_of(at, r);
+    c.slack[u] = to_f4(s);
+    if (x.e != kNone) write_ep(c, x.e, s);
+    // candidate of the driver through the net arc (only edges the forward used)
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (fin(at_v.v[q])) acc.v[q] = __fsub_rn(r.v[q], el);
+  }
+  // segmented inclusive scan by driver (drivers are contiguous in the tile)
+  const uint32_t v = x.v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t vo = __shfl_up_sync(0xFFFFFFFFu, v, o);
+    Q4 b;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) b.v[q] = __shfl_up_sync(0xFFFFFFFFu, acc.v[q], o);
+    if (lane >= o && vo == v) combine(acc, b);
+  }
+  const uint32_t vn = __shfl_down_sync(0xFFFFFFFFu, v, 1);
+  const bool tail = x.active && (lane == 31 || vn != v);
+  if (!tail) return;
+  if (x.td.y == kNone) {                    // light driver: complete in this tile
+    finish_pull<WAIT>(t, c, L, v, at_v, sl_v, acc);
     return;
   }
-  // heavy driver: block-strided sinks, block min/max reduction
-  const uint32_t v = t.heavy[heavy0 + (blockIdx.x - nLightBlocks)];
-  const uint32_t sb = t.sink_ptr[v], se = t.sink_ptr[v + 1];
-  Q4 at, sl;
-  load_rec(c, v, at, sl);
-  Q4 acc = undef_rat();
-  for (uint32_t k = sb + threadIdx.x; k < se; k += blockDim.x) {
-    const Q4 r = sink_rat(t, c, k);
-    net_bwd(at, r, c.elm[k], acc);
+  const uint32_t slot = x.td.y;
+  int* key = reinterpret_cast<int*>(c.heavy_key + slot);
+  atomicMax(key + 0, f2o(acc.v[0]));
+  atomicMax(key + 1, f2o(acc.v[1]));
+  atomicMin(key + 2, f2o(acc.v[2]));
+  atomicMin(key + 3, f2o(acc.v[3]));
+  __threadfence();
+  const uint32_t done = atomicAdd(c.heavy_cnt + slot, 1u);
+  if (done + 1 != t.heavy_nchunk[slot]) return;
+  __threadfence();
+  Q4 a;
+  a.v[0] = o2f(atomicExch(key + 0, f2o(-CUDART_INF_F)));
+  a.v[1] = o2f(atomicExch(key + 1, f2o(-CUDART_INF_F)));
+  a.v[2] = o2f(atomicExch(key + 2, f2o(CUDART_INF_F)));
+  a.v[3] = o2f(atomicExch(key + 3, f2o(CUDART_INF_F)));
+  c.heavy_cnt[slot] = 0;                    // self-reset for the next update
+  finish_pull<WAIT>(t, c, L, v, at_v, sl_v, a);
+}
+
+// One launch per gate stage (descending).  Blocks [0, nTileBlocks): one warp
+// per tile.  Remaining blocks: stage pins without sinks, one thread each.
+template <bool SMEM_LUT>
+__global__ void __launch_bounds__(kThreads) bwd_stage_kernel(Topo t, CornerDev c, uint32_t tile0, uint32_t nTiles,
+                                                             uint32_t sinkEnd, uint32_t nos0, uint32_t nNos,
+                                                             uint32_t nTileBlocks, uint32_t lut_f4) {
+  const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
+  if (blockIdx.x >= nTileBlocks) {
+    const uint32_t i = (blockIdx.x - nTileBlocks) * blockDim.x + threadIdx.x;
+    const uint32_t v = i < nNos ? t.nosink[nos0 + i] : 0;
+    pdl_wait();
+    pdl_launch();
+    if (i >= nNos) return;
+    Q4 at, sl;
+    load_rec(c, v, at, sl);
+    finish_pull<false>(t, c, L, v, at, sl, undef_rat());
+    return;
   }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float x = __shfl_xor_sync(0xFFFFFFFFu, acc.v[q], o);
-      acc.v[q] = q < 2 ? fmaxf(acc.v[q], x) : fminf(acc.v[q], x);
-    }
-  }
-  __shared__ float4 part[kThreads / 32];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) part[w] = to_f4(acc);
+  const uint32_t tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  TileLane x{};
+  if (tile < nTiles) x = tile_lane(t, tile0 + tile, tile + 1 < nTiles ? t.tiles[tile0 + tile + 1].x : sinkEnd);
+  pdl_wait();
+  pdl_launch();
+  if (tile >= nTiles) return;
+  process_tile<false>(t, c, L, x);
+}
+
+// ---------------------------------------------- persistent dataflow passes
+// Grid = co-resident blocks (cooperative launch).  Work items are processed in
+// dependency order (block b takes items b, b + G, ...), every item depends
+// only on items with a smaller index, and all blocks are resident, so the
+// smallest unfinished item can always proceed: no deadlock, no grid barrier.
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// producer side of a chunk: every thread's stores -> barrier -> one gpu-scope
+// fence -> flag store
+__device__ __forceinline__ void publish(uint32_t* flag, uint32_t v) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    Q4 a = undef_rat();
-    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
-      const Q4 p = to_q(part[k]);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) a.v[q] = q < 2 ? fmaxf(a.v[q], p.v[q]) : fminf(a.v[q], p.v[q]);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+  }
+}
+
+constexpr int kPrefetch = 4;   // fan-in terms whose topology is loaded up front
+
+// Block-level readiness: one thread per block polls the per-stage completion
+// counters and the whole block waits at a barrier, so at most one poller per
+// block touches L2 (per-thread polling by ~150K threads slowed the producers).
+// *wm caches, per block, the stages already known complete.
+__device__ __forceinline__ void fwd_wait_stages(const Topo& t, const CornerDev& c, uint32_t stage, uint32_t* wm) {
+  if (threadIdx.x == 0) {
+    uint32_t w = *wm;
+    while (w < stage) {                    // every stage < stage must be complete
+      wait_ge(c.fwd_done + w, __ldg(t.stage_chunks + w));
+      ++w;
     }
-    finish_pull(t, c, v, at, sl, a);
+    *wm = w;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void bwd_wait_stages(const Topo& t, const CornerDev& c, uint32_t stage, uint32_t* wm) {
+  if (threadIdx.x == 0) {
+    uint32_t w = *wm;
+    while (w > stage + 1) {                // every stage > stage must be complete
+      wait_ge(c.bwd_done + w - 1, __ldg(t.stage_units + w - 1));
+      --w;
+    }
+    *wm = w;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void count_done(uint32_t* ctr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    atomicAdd(ctr, 1u);
+  }
+}
+
+template <bool SMEM_LUT>
+__global__ void __launch_bounds__(kThreads) fwd_persistent_kernel(Topo t, CornerDev c, uint32_t lut_f4) {
+  __shared__ uint32_t s_wm;
+  const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
+  if (threadIdx.x == 0) s_wm = 0;
+  const uint32_t nch = t.NP / kChunk, c0 = t.n0 / kChunk;
+  for (uint32_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+    unsigned long long t_start = 0, t_ready = 0;
+    if (c.trace && threadIdx.x == 0) t_start = gtimer();
+    const uint32_t v = ch * kChunk + threadIdx.x;
+    const uint32_t stage = __ldg(t.chunk_stage + ch);
+    Q4 acc_at = undef_at(), acc_sl = undef_at();
+    if (ch < c0) {                          // stage 0: seeds
+      const uint32_t s = t.seed[v];
+      if (s == kSeedClock) {
+        const float h = 0.5f * t.period;
+        acc_at = Q4{{0.f, h, 0.f, h}};
+        acc_sl = Q4{{t.clock_slew, t.clock_slew, t.clock_slew, t.clock_slew}};
+      } else if (s != kNone) {
+        acc_at = to_q(t.pi_at[s]);
+        acc_sl = to_q(t.pi_slew[s]);
+      }
+    } else {
+      // static topology and RC results of the first kPrefetch terms are
+      // loaded before waiting; only the record loads depend on the producers
+      const uint32_t e0 = t.fi_ptr[v], e1 = t.fi_ptr[v + 1];
+      const float ld = __ldcg(c.load + v);
+      uint32_t src[kPrefetch], info[kPrefetch];
+      float elm[kPrefetch];
+      bool hop[kPrefetch];
+#pragma unroll
+      for (int k = 0; k < kPrefetch; ++k) {
+        const uint32_t e = e0 + k;
+        src[k] = 0; info[k] = 0; elm[k] = 0.f; hop[k] = false;
+        if (e < e1) {
+          src[k] = t.fi_src[e];
+          info[k] = t.fi_info[e];
+          const uint32_t h = t.fi_hop[e];
+          hop[k] = h != kNone;
+          if (hop[k]) elm[k] = __ldcg(c.elm + h);
+        }
+      }
+      fwd_wait_stages(t, c, stage, &s_wm);
+      if (c.trace && threadIdx.x == 0) t_ready = gtimer();
+#pragma unroll
+      for (int k = 0; k < kPrefetch; ++k) {
+        if (e0 + k >= e1) break;
+        Q4 at, sl;
+        load_rec(c, src[k], at, sl);
+        if (hop[k]) net_hop(at, sl, elm[k]);
+        cell_fwd(L, at, sl, info[k], ld, acc_at, acc_sl);
+      }
+      for (uint32_t e = e0 + kPrefetch; e < e1; ++e) {
+        const uint32_t h = t.fi_hop[e];
+        Q4 at, sl;
+        load_rec(c, t.fi_src[e], at, sl);
+        if (h != kNone) net_hop(at, sl, __ldcg(c.elm + h));
+        cell_fwd(L, at, sl, t.fi_info[e], ld, acc_at, acc_sl);
+      }
+    }
+    c.rec[2 * (size_t)v] = to_f4(acc_at);
+    c.rec[2 * (size_t)v + 1] = to_f4(acc_sl);
+    if (c.trace) {                          // debug: time when the whole block computed
+      __syncthreads();
+      if (threadIdx.x == 0) t_start = gtimer();
+    }
+    count_done(c.fwd_done + stage);
+    if (c.trace && threadIdx.x == 0) {
+      c.trace[3 * (size_t)ch] = t_start;
+      c.trace[3 * (size_t)ch + 1] = t_ready;
+      c.trace[3 * (size_t)ch + 2] = gtimer();
+    }
+  }
+}
+
+template <bool SMEM_LUT>
+__global__ void __launch_bounds__(kThreads) bwd_persistent_kernel(Topo t, CornerDev c, uint32_t lut_f4) {
+  __shared__ uint32_t s_wm;
+  const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
+  if (threadIdx.x == 0) s_wm = t.S;
+  for (uint32_t u = blockIdx.x; u < t.n_units; u += gridDim.x) {
+    unsigned long long t_start = 0, t_ready = 0;
+    if (c.trace && threadIdx.x == 0) t_start = gtimer();
+    const uint4 ud = t.units[u];             // {stage, kind, first, count}
+    const uint32_t w = threadIdx.x >> 5;
+    TileLane x{};
+    uint32_t v = 0;
+    if (ud.y == 0) {                         // static part before waiting
+      if (w < ud.w) {
+        const uint32_t tile = ud.z + w;
+        const uint32_t k1 = tile + 1 < t.stage_tile_end[ud.x] ? t.tiles[tile + 1].x : t.stage_sink_end[ud.x];
+        x = tile_lane(t, tile, k1);
+      }
+    } else if (threadIdx.x < ud.w) {
+      v = t.nosink[ud.z + threadIdx.x];
+    }
+    bwd_wait_stages(t, c, ud.x, &s_wm);
+    if (c.trace && threadIdx.x == 0) t_ready = gtimer();
+    if (ud.y == 0) {
+      if (w < ud.w) process_tile<false>(t, c, L, x);
+    } else if (threadIdx.x < ud.w) {
+      Q4 at, sl;
+      load_rec(c, v, at, sl);
+      finish_pull<false>(t, c, L, v, at, sl, undef_rat());
+    }
+    count_done(c.bwd_done + ud.x);
+    if (c.trace && threadIdx.x == 0) {
+      const size_t q = 3 * ((size_t)t.NP / kChunk + u);
+      c.trace[q] = t_start;
+      c.trace[q + 1] = t_ready;
+      c.trace[q + 2] = gtimer();
+    }
   }
 }
 
 // ------------------------------------------------------- a5: WNS / TNS
-// Single block, fixed element-to-thread assignment and fixed tree: the
-// result is bitwise reproducible (SURVEY.md §8(c) reading #16).
-__global__ void __launch_bounds__(1024) reduce_kernel(Topo t, CornerDev c) {
-  __shared__ double s_tns[1024], h_tns[1024];
-  __shared__ float s_wns[1024], h_wns[1024];
+// kRedBlocks blocks with a fixed endpoint range each, fixed-shape trees and a
+// fixed-order final combine by the last block: bitwise reproducible.
+__global__ void __launch_bounds__(kThreads) reduce_kernel(Topo t, CornerDev c) {
+  __shared__ double s_t[2][kThreads];
+  __shared__ float s_w[2][kThreads];
+  __shared__ bool last;
+  pdl_wait();
+  pdl_launch();
+  const uint32_t n = t.n_ep;
+  const uint32_t lo = (uint32_t)((uint64_t)n * blockIdx.x / gridDim.x);
+  const uint32_t hi = (uint32_t)((uint64_t)n * (blockIdx.x + 1) / gridDim.x);
   float ws = CUDART_INF_F, wh = CUDART_INF_F;
   double ts = 0.0, th = 0.0;
-  for (uint32_t e = threadIdx.x; e < t.n_ep; e += blockDim.x) {
-    const float2 x = c.ep_ws[e];
+  for (uint32_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+    const float2 x = __ldcg(c.ep_ws + e);
     ws = fminf(ws, x.x);
     wh = fminf(wh, x.y);
     if (x.x < 0.f) ts += (double)x.x;
     if (x.y < 0.f) th += (double)x.y;
   }
-  s_wns[threadIdx.x] = ws; h_wns[threadIdx.x] = wh;
-  s_tns[threadIdx.x] = ts; h_tns[threadIdx.x] = th;
+  s_w[0][threadIdx.x] = ws; s_w[1][threadIdx.x] = wh;
+  s_t[0][threadIdx.x] = ts; s_t[1][threadIdx.x] = th;
   __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+  for (int o = kThreads / 2; o > 0; o >>= 1) {
     if ((int)threadIdx.x < o) {
-      s_wns[threadIdx.x] = fminf(s_wns[threadIdx.x], s_wns[threadIdx.x + o]);
-      h_wns[threadIdx.x] = fminf(h_wns[threadIdx.x], h_wns[threadIdx.x + o]);
-      s_tns[threadIdx.x] += s_tns[threadIdx.x + o];
-      h_tns[threadIdx.x] += h_tns[threadIdx.x + o];
+      s_w[0][threadIdx.x] = fminf(s_w[0][threadIdx.x], s_w[0][threadIdx.x + o]);
+      s_w[1][threadIdx.x] = fminf(s_w[1][threadIdx.x], s_w[1][threadIdx.x + o]);
+      s_t[0][threadIdx.x] += s_t[0][threadIdx.x + o];
+      s_t[1][threadIdx.x] += s_t[1][threadIdx.x + o];
     }
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    c.res[0] = (double)s_wns[0];
-    c.res[1] = s_tns[0];
-    c.res[2] = (double)h_wns[0];
-    c.res[3] = h_tns[0];
+    double* p = c.red_part + 4 * blockIdx.x;
+    p[0] = s_w[0][0]; p[1] = s_t[0][0]; p[2] = s_w[1][0]; p[3] = s_t[1][0];
+    __threadfence();
+    last = atomicAdd(c.red_cnt, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  double r0 = CUDART_INF, r1 = 0.0, r2 = CUDART_INF, r3 = 0.0;
+  for (uint32_t b = 0; b < gridDim.x; ++b) {
+    const double* p = c.red_part + 4 * b;
+    r0 = fmin(r0, __ldcg(p + 0)); r1 += __ldcg(p + 1);
+    r2 = fmin(r2, __ldcg(p + 2)); r3 += __ldcg(p + 3);
+  }
+  c.res[0] = r0; c.res[1] = r1; c.res[2] = r2; c.res[3] = r3;
+  *c.red_cnt = 0;                           // self-reset for the next update
+  for (uint32_t x = 0; x < t.S; ++x) {        // stage counters: ready for the next update
+    c.bwd_done[x] = 0;
+    c.fwd_done[x] = 0;
   }
 }
 
-// ----------------------------------------------------- output gathers
-__global__ void gather4_kernel(const float4* __restrict__ src, const uint32_t* __restrict__ idx,
-                               float4* __restrict__ dst, uint32_t n, uint32_t stride) {
+// ----------------------------------------------------- outputs / setup
+// what: 0 at, 1 slew, 2 rat, 3 slack, in user pin order; sink arrivals and
+// slews are recomputed from their drivers exactly as the kernels do.
+__global__ void gather_pins_kernel(Topo t, CornerDev c, int what, float4* __restrict__ dst) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < n) dst[p] = src[(size_t)idx[p] * stride];
+  if (p >= t.P) return;
+  const uint32_t i = t.int_of_user[p];
+  if (what >= 2) {
+    dst[p] = what == 2 ? c.rat[i] : c.slack[i];
+    return;
+  }
+  if (i < t.NP) {
+    dst[p] = c.rec[2 * (size_t)i + what];
+    return;
+  }
+  const uint32_t k = i - t.NP;
+  Q4 at, sl;
+  load_rec(c, t.sink_drv[k], at, sl);
+  net_hop(at, sl, c.elm[k]);
+  dst[p] = to_f4(what == 0 ? at : sl);
 }
 
-__global__ void gather_rc_kernel(Topo t, CornerDev c, float* net_load, float* pin_elm,
-                                 const uint32_t* drv_of_net) {
+__global__ void gather_rc_kernel(Topo t, CornerDev c, float* net_load, float* pin_elm) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (net_load && p < t.N) net_load[p] = c.load[drv_of_net[p]];
+  if (net_load && p < t.N) net_load[p] = c.load[t.drv_of_net[p]];
   if (pin_elm && p < t.P) {
     const uint32_t i = t.int_of_user[p];
     pin_elm[p] = i >= t.NP ? c.elm[i - t.NP] : 0.f;
   }
 }
 
+__global__ void init_corner_kernel(CornerDev c, uint32_t n_heavy) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n_heavy) {
+    c.heavy_key[i] = make_int4(f2o(-CUDART_INF_F), f2o(-CUDART_INF_F), f2o(CUDART_INF_F), f2o(CUDART_INF_F));
+    c.heavy_cnt[i] = 0;
+  }
+  if (i == 0) {
+    *c.red_cnt = 0;
+    *c.err_flag = 0;
+  }
+}
+
 inline uint32_t blocks(uint64_t n, uint32_t th = kThreads) { return (uint32_t)((n + th - 1) / th); }
+
+// launch with programmatic dependent launch enabled
+template <class K, class... A>
+cudaError_t pdl_launch_smem(K kernel, uint32_t grid, uint32_t block, size_t smem, cudaStream_t s, A... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+template <class K, class... A>
+cudaError_t pdl_launch_kernel(K kernel, uint32_t grid, uint32_t block, cudaStream_t s, A... args) {
+  return pdl_launch_smem(kernel, grid, block, 0, s, args...);
+}
 
 }  // namespace
 
-cudaError_t launch_rc(const Topo& t, const CornerDev& c, uint32_t, cudaStream_t s) {
-  if (t.N) rc_small_kernel<<<blocks(t.N), kThreads, 0, s>>>(t, c);
-  if (t.n_big) rc_big_kernel<<<t.n_big, kThreads, 0, s>>>(t, c);
-  return cudaGetLastError();
+cudaError_t launch_scan(double* x, uint32_t n, double* tsum, double* toff, bool inclusive, cudaStream_t s) {
+  const uint32_t tiles = (n + kScanTile - 1) / kScanTile;
+  cudaError_t e = pdl_launch_kernel(scan_tiles_kernel, tiles, kScanThreads, s, (const double*)x, n, tsum);
+  if (e == cudaSuccess)
+    e = pdl_launch_kernel(scan_offsets_kernel, 1u, kScanThreads, s, (const double*)tsum, tiles, toff, x, n);
+  if (e == cudaSuccess)
+    e = pdl_launch_kernel(scan_apply_kernel, tiles, kScanThreads, s, x, n, (const double*)toff, inclusive ? 1 : 0);
+  return e;
+}
+
+cudaError_t launch_rc(const Topo& t, const CornerDev& c, cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
+  if (t.nA && e == cudaSuccess) e = pdl_launch_kernel(rc_tierA_kernel, blocks(t.nA), kThreads, s, t, c);
+  if (t.nB && e == cudaSuccess) e = pdl_launch_kernel(rc_tierB_kernel, blocks(t.nB, kWarpsB), 32 * kWarpsB, s, t, c);
+  if (t.nC && e == cudaSuccess) {
+    const uint32_t n = t.nCn;
+    const size_t tiles = (n + kScanTile - 1) / kScanTile;
+    double* A = c.scratch;
+    double* W = A + n + 1;
+    double* G = W + n + 1;
+    double* tsum = G + n + 1;
+    double* toff = tsum + tiles + 1;
+    const uint32_t nb = blocks(n > t.nC ? n : t.nC);
+    e = pdl_launch_kernel(tc_cap_kernel, blocks(n), kThreads, s, t, c, A);
+    if (e == cudaSuccess) e = launch_scan(A, n, tsum, toff, false, s);
+    if (e == cudaSuccess) e = pdl_launch_kernel(tc_w_kernel, nb, kThreads, s, t, c, (const double*)A, W);
+    if (e == cudaSuccess) e = pdl_launch_kernel(tc_d_kernel, blocks(n), kThreads, s, t, (const double*)W, G);
+    if (e == cudaSuccess) e = launch_scan(G, n, tsum, toff, true, s);
+    if (e == cudaSuccess) e = pdl_launch_kernel(tc_elm_kernel, blocks(n), kThreads, s, t, c, (const double*)G);
+  }
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_seed(const Topo& t, const CornerDev& c, uint32_t n0, cudaStream_t s) {
-  if (n0) seed_kernel<<<blocks(n0), kThreads, 0, s>>>(t, c, n0);
-  return cudaGetLastError();
+  if (!n0) return cudaSuccess;
+  return pdl_launch_kernel(seed_kernel, blocks(n0), kThreads, s, t, c, n0);
 }
 
-cudaError_t launch_fwd_stage(const Topo& t, const CornerDev& c, uint32_t sinkA0, uint32_t nA, uint32_t pullB0,
-                             uint32_t nB, cudaStream_t s) {
-  if (nA + nB) fwd_stage_kernel<<<blocks((uint64_t)nA + nB), kThreads, 0, s>>>(t, c, sinkA0, nA, pullB0, nB);
-  return cudaGetLastError();
+cudaError_t launch_fwd_stage(const Topo& t, const CornerDev& c, uint32_t pull0, uint32_t n, uint32_t lut_f4,
+                             cudaStream_t s) {
+  if (!n) return cudaSuccess;
+  if (lut_f4) return pdl_launch_smem(fwd_stage_kernel<true>, blocks(n), kThreads, 16ull * lut_f4, s, t, c, pull0, n, lut_f4);
+  return pdl_launch_smem(fwd_stage_kernel<false>, blocks(n), kThreads, 0, s, t, c, pull0, n, lut_f4);
 }
 
-cudaError_t launch_bwd_stage(const Topo& t, const CornerDev& c, uint32_t pull0, uint32_t nPull, uint32_t heavy0,
-                             uint32_t nHeavy, cudaStream_t s) {
-  const uint32_t nl = blocks(nPull);
-  if (nl + nHeavy) bwd_stage_kernel<<<nl + nHeavy, kThreads, 0, s>>>(t, c, pull0, nPull, heavy0, nl);
-  return cudaGetLastError();
+cudaError_t launch_bwd_stage(const Topo& t, const CornerDev& c, uint32_t tile0, uint32_t nTiles, uint32_t sinkEnd,
+                             uint32_t nos0, uint32_t nNos, uint32_t lut_f4, cudaStream_t s) {
+  const uint32_t tb = blocks((uint64_t)nTiles * 32);
+  const uint32_t nb = blocks(nNos);
+  if (!(tb + nb)) return cudaSuccess;
+  if (lut_f4)
+    return pdl_launch_smem(bwd_stage_kernel<true>, tb + nb, kThreads, 16ull * lut_f4, s, t, c, tile0, nTiles, sinkEnd,
+                           nos0, nNos, tb, lut_f4);
+  return pdl_launch_smem(bwd_stage_kernel<false>, tb + nb, kThreads, 0, s, t, c, tile0, nTiles, sinkEnd, nos0, nNos, tb,
+                         lut_f4);
 }
 
 cudaError_t launch_reduce(const Topo& t, const CornerDev& c, cudaStream_t s) {
-  reduce_kernel<<<1, 1024, 0, s>>>(t, c);
+  return pdl_launch_kernel(reduce_kernel, (uint32_t)kRedBlocks, kThreads, s, t, c);
+}
+
+cudaError_t launch_gather_pins(const Topo& t, const CornerDev& c, int what, float4* dst, cudaStream_t s) {
+  if (t.P) gather_pins_kernel<<<blocks(t.P), kThreads, 0, s>>>(t, c, what, dst);
   return cudaGetLastError();
 }
 
-cudaError_t launch_gather4(const float4* src, const uint32_t* idx, float4* dst, uint32_t n, uint32_t stride,
-                           cudaStream_t s) {
-  if (n) gather4_kernel<<<blocks(n), kThreads, 0, s>>>(src, idx, dst, n, stride);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_gather_rc(const Topo& t, const CornerDev& c, float* net_load, float* pin_elm,
-                             const uint32_t* drv_of_net, const uint32_t*, cudaStream_t s) {
+cudaError_t launch_gather_rc(const Topo& t, const CornerDev& c, float* net_load, float* pin_elm, cudaStream_t s) {
   const uint32_t n = t.N > t.P ? t.N : t.P;
-  if (n) gather_rc_kernel<<<blocks(n), kThreads, 0, s>>>(t, c, net_load, pin_elm, drv_of_net);
+  if (n) gather_rc_kernel<<<blocks(n), kThreads, 0, s>>>(t, c, net_load, pin_elm);
   return cudaGetLastError();
 }
 
-cudaError_t launch_check_rc_values(const CornerDev&, uint32_t, cudaStream_t) { return cudaSuccess; }
+uint32_t persistent_grid(uint32_t lut_f4) {
+  int dev = 0, sms = 0, nb = 0, coop = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  if (!coop) return 0;
+  const size_t smem = 16ull * lut_f4;
+  int nb2 = 0;
+  if (lut_f4) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fwd_persistent_kernel<true>, kThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, bwd_persistent_kernel<true>, kThreads, smem);
+  } else {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fwd_persistent_kernel<false>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, bwd_persistent_kernel<false>, kThreads, 0);
+  }
+  cudaGetLastError();
+  return (uint32_t)(std::min(nb, nb2) * sms);
+}
+
+template <class K>
+cudaError_t coop_launch(K kernel, uint32_t grid, size_t smem, cudaStream_t s, const Topo& t, const CornerDev& c,
+                        uint32_t lut_f4) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, t, c, lut_f4);
+}
+
+cudaError_t launch_fwd_persistent(const Topo& t, const CornerDev& c, uint32_t grid, uint32_t lut_f4, cudaStream_t s) {
+  if (!t.NP) return cudaSuccess;
+  return lut_f4 ? coop_launch(fwd_persistent_kernel<true>, grid, 16ull * lut_f4, s, t, c, lut_f4)
+                : coop_launch(fwd_persistent_kernel<false>, grid, 0, s, t, c, lut_f4);
+}
+
+cudaError_t launch_bwd_persistent(const Topo& t, const CornerDev& c, uint32_t grid, uint32_t lut_f4, cudaStream_t s) {
+  if (!t.n_units) return cudaSuccess;
+  return lut_f4 ? coop_launch(bwd_persistent_kernel<true>, grid, 16ull * lut_f4, s, t, c, lut_f4)
+                : coop_launch(bwd_persistent_kernel<false>, grid, 0, s, t, c, lut_f4);
+}
+
+cudaError_t set_lut_smem_limit(size_t bytes) {
+  cudaError_t e = cudaFuncSetAttribute(fwd_stage_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(bwd_stage_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(fwd_persistent_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(bwd_persistent_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  return e;
+}
+
+cudaError_t launch_init_corner(const Topo&, const CornerDev& c, uint32_t n_heavy, cudaStream_t s) {
+  init_corner_kernel<<<blocks(n_heavy + 1), kThreads, 0, s>>>(c, n_heavy);
+  return cudaGetLastError();
+}
 
 }  // namespace sta

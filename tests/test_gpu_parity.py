@@ -186,3 +186,22 @@ def test_c3_superblue_full(sta):
     compare_update(ctx, oracle.update(d), report=rep)
     check_levels(ctx, d)
     print(json.dumps(rep))
+
+
+def test_stage_kernels_equal_persistent_kernels(sta):
+    """The two launch strategies of the forward / backward passes (one launch
+    per gate stage with PDL vs. persistent dataflow kernels) give identical bits."""
+    d = synth.generate(30000, 60, seed=31, n_hfn=3, hfn_range=(100, 2000), period=500.0)
+    out = []
+    for mode in ("1", "0"):
+        os.environ["STA_STAGE_KERNELS"] = mode
+        try:
+            ctx = run(sta, d)
+        finally:
+            os.environ.pop("STA_STAGE_KERNELS", None)
+        out.append((ctx.get_timing(0), ctx.report_slack(0, want_pins=True)))
+        ctx.close()
+    (a, ra), (b, rb) = out
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    assert np.array_equal(ra[0], rb[0]) and np.array_equal(ra[1], rb[1])
