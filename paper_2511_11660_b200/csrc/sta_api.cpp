@@ -126,7 +126,7 @@ struct sta_ctx_s {
   u32 NP = 0, NS = 0, S = 0, n0 = 0, Pi = 0;   // NP includes stage padding; Pi = NP + NS
   std::vector<u32> pull_stage_ptr, sink_stage_ptr, tile_stage_ptr, nosink_stage_ptr, sink_ptr;
   std::vector<u32> drv_of_net;    // user net -> internal driver id
-  u32 n_heavy = 0, n_units = 0;
+  u32 n_heavy = 0, n_units = 0, n_fchunks = 0;
 
   // ---- RC tree (host)
   std::vector<u32> rc_ptr, rc_node_pin;
@@ -162,8 +162,10 @@ struct sta_ctx_s {
   // or one launch per gate stage (STA_STAGE_KERNELS=1, or no cooperative launch)
   bool use_persistent = true;
   std::string trace_path;         // STA_TRACE (debug)
+  bool rc_tierB = false;          // STA_RC_TIERB=1: warp-per-net RC tier for 9..256 nodes
   std::vector<u32> unit_stage;    // stage of each backward unit (trace labels)
-  u32 pgrid = 0;
+  std::vector<u32> fchunk_stage_h; // stage of each forward chunk (trace labels)
+  u32 pgrid = 0, pgrid_b = 0;     // co-resident grids (forward, backward)
 };
 
 namespace {
@@ -346,6 +348,17 @@ void build_plan(sta_ctx c) {
   c->sink_stage_ptr.assign(S + 1, 0);
   for (u32 s = 0; s <= S; ++s) c->sink_stage_ptr[s] = c->sink_ptr[c->pull_stage_ptr[s]];
 
+  // A non-unate arc's (irf -> orf) pairs are the union of the positive- and
+  // negative-unate pairs, so it becomes two terms with the same
+  // tables; every kernel item then evaluates exactly one pair per output edge
+  // (no divergent second pass).  Min / max merges are order-free, so results
+  // are unchanged.
+  auto n_terms = [&](u32 a) { return c->arc_sense[a] == STA_NON_UNATE ? 2u : 1u; };
+  auto term_info = [&](u32 a, u32 q) {
+    const u32 sense = c->arc_sense[a] == STA_NON_UNATE ? (q ? STA_NEG_UNATE : STA_POS_UNATE) : c->arc_sense[a];
+    return sta::pack_info(sense, c->arc_tab[a]);
+  };
+
   // forward fan-in terms of pull pins (cell arcs, arc id order)
   std::vector<u32> fi_p(NP + 1, 0), fi_src, fi_hop, fi_info;
   fi_src.reserve(c->A);
@@ -357,14 +370,16 @@ void build_plan(sta_ctx c) {
     if (p == kNone) continue;
     for (u32 x = fi_ptr[p]; x < fi_ptr[p + 1]; ++x) {
       const u32 a = fi_ids[x], u = c->arc_from[a];
-      if (c->is_sink[u]) {
-        fi_src.push_back(c->int_of_user[driver_of(u)]);
-        fi_hop.push_back(c->int_of_user[u] - NP);
-      } else {
-        fi_src.push_back(c->int_of_user[u]);
-        fi_hop.push_back(kNone);
+      for (u32 q = 0; q < n_terms(a); ++q) {
+        if (c->is_sink[u]) {
+          fi_src.push_back(c->int_of_user[driver_of(u)]);
+          fi_hop.push_back(c->int_of_user[u] - NP);
+        } else {
+          fi_src.push_back(c->int_of_user[u]);
+          fi_hop.push_back(kNone);
+        }
+        fi_info.push_back(term_info(a, q));
       }
-      fi_info.push_back(sta::pack_info(c->arc_sense[a], c->arc_tab[a]));
     }
   }
   fi_p[NP] = (u32)fi_src.size();
@@ -376,8 +391,10 @@ void build_plan(sta_ctx c) {
     sfo_p[kk] = (u32)sfo_dst.size();
     for (u32 x = fo_ptr[u]; x < fo_ptr[u + 1]; ++x) {
       const u32 a = fo_ids[x];
-      sfo_dst.push_back(c->int_of_user[c->arc_to[a]]);
-      sfo_info.push_back(sta::pack_info(c->arc_sense[a], c->arc_tab[a]));
+      for (u32 q = 0; q < n_terms(a); ++q) {
+        sfo_dst.push_back(c->int_of_user[c->arc_to[a]]);
+        sfo_info.push_back(term_info(a, q));
+      }
     }
   }
   sfo_p[c->NS] = (u32)sfo_dst.size();
@@ -387,8 +404,10 @@ void build_plan(sta_ctx c) {
     if (u == kNone) continue;
     for (u32 x = fo_ptr[u]; x < fo_ptr[u + 1]; ++x) {
       const u32 a = fo_ids[x];
-      pfo_dst.push_back(c->int_of_user[c->arc_to[a]]);
-      pfo_info.push_back(sta::pack_info(c->arc_sense[a], c->arc_tab[a]));
+      for (u32 q = 0; q < n_terms(a); ++q) {
+        pfo_dst.push_back(c->int_of_user[c->arc_to[a]]);
+        pfo_info.push_back(term_info(a, q));
+      }
     }
   }
   pfo_p[NP] = (u32)pfo_dst.size();
@@ -441,6 +460,42 @@ void build_plan(sta_ctx c) {
     stage_sink_end[s] = c->sink_ptr[c->pull_stage_ptr[s + 1]];
     stage_tile_end[s] = c->tile_stage_ptr[s + 1];
   }
+  // forward chunks: stage 0 = 256 seed pins; later stages = consecutive pins
+  // of one stage whose fan-in terms fit one 256-thread block (a pin with more
+  // terms gets a chunk of its own and is looped over)
+  std::vector<uint4> fchunks;              // {pin0, npins, item0, nitems}
+  std::vector<u32> fchunk_stage, stage_fchunks(S, 0), fi_pin(fi_src.size());
+  for (u32 i = 0; i < NP; ++i)
+    for (u32 e = fi_p[i]; e < fi_p[i + 1]; ++e) fi_pin[e] = i;
+  for (u32 s = 0; s < S; ++s) {
+    const u32 p0 = c->pull_stage_ptr[s], p1 = c->pull_stage_ptr[s + 1];
+    if (s == 0) {
+      for (u32 p = p0; p < p1; p += sta::kChunk) {
+        fchunks.push_back(make_uint4(p, std::min<u32>(sta::kChunk, p1 - p), 0, 0));
+        fchunk_stage.push_back(s);
+        stage_fchunks[s]++;
+      }
+      continue;
+    }
+    u32 p = p0;
+    while (p < p1) {
+      while (p < p1 && fi_p[p + 1] == fi_p[p]) ++p;   // stage padding: no work
+      if (p == p1) break;
+      const u32 q0 = p;
+      u32 items = 0;
+      while (p < p1) {
+        const u32 n = fi_p[p + 1] - fi_p[p];
+        if (n == 0 || (items && items + n > sta::kChunk) || p - q0 >= sta::kChunk) break;
+        items += n;
+        ++p;
+      }
+      fchunks.push_back(make_uint4(q0, p - q0, fi_p[q0], items));
+      fchunk_stage.push_back(s);
+      stage_fchunks[s]++;
+    }
+  }
+  c->n_fchunks = (u32)fchunks.size();
+  c->fchunk_stage_h = fchunk_stage;
   std::vector<uint4> units;
   for (u32 s = S; s-- > 0;) {
     for (u32 x = c->tile_stage_ptr[s]; x < c->tile_stage_ptr[s + 1]; x += 8) {
@@ -481,9 +536,11 @@ void build_plan(sta_ctx c) {
   t.tiles = g.upload(tiles, s);
   t.chunk_stage = g.upload(chunk_stage, s);
   t.stage_units = g.upload(stage_units, s);
-  std::vector<u32> stage_chunks(S);
-  for (u32 q = 0; q < S; ++q) stage_chunks[q] = (c->pull_stage_ptr[q + 1] - c->pull_stage_ptr[q]) / sta::kChunk;
-  t.stage_chunks = g.upload(stage_chunks, s);
+  t.stage_chunks = g.upload(stage_fchunks, s);
+  t.fchunks = g.upload(fchunks, s);
+  t.fchunk_stage = g.upload(fchunk_stage, s);
+  t.fi_pin = g.upload(fi_pin, s);
+  t.n_fchunks = c->n_fchunks;
   t.stage_sink_end = g.upload(stage_sink_end, s);
   t.stage_tile_end = g.upload(stage_tile_end, s);
   t.units = g.upload(units, s);
@@ -557,7 +614,11 @@ void build_rc(sta_ctx c) {
   std::vector<u32> tierA, tierB, tierC;
   for (u32 j = 0; j < NJ; ++j) {
     const u32 m = net_node[j + 1] - net_node[j];
-    (m <= (u32)sta::kTierA ? tierA : m <= (u32)sta::kTierB ? tierB : tierC).push_back(j);
+    // tier B (warp per net, level schedule) is kept for STA_RC_TIERB=1; by
+    // default every net above kTierA nodes takes the Euler-tour scan path,
+    // which measured ~6x faster on C3 (no per-level barriers)
+    const bool tb = c->rc_tierB && m <= (u32)sta::kTierB;
+    (m <= (u32)sta::kTierA ? tierA : tb ? tierB : tierC).push_back(j);
   }
   // level schedules of tier B then tier C nets
   std::vector<u32> sched_off{0}, sched_h, sched_hn, sched_doff{0}, sched_d, sched_dn, child_off{0}, child_ptr,
@@ -699,7 +760,8 @@ void build_rc(sta_ctx c) {
 void prepare(sta_ctx c) {
   if (c->prepared) return;
   invalidate_graph(c);
-  c->pgrid = c->use_persistent ? sta::persistent_grid(c->lut_f4) : 0;
+  c->pgrid = c->use_persistent ? sta::persistent_grid(c->lut_f4, 0) : 0;
+  c->pgrid_b = c->use_persistent ? sta::persistent_grid(c->lut_f4, 1) : 0;
   const u32 P = c->P;
   std::vector<u32> pi_idx(P, kNone), po_idx(P, kNone);
   for (u32 k = 0; k < c->pi_pin.size(); ++k) pi_idx[c->pi_pin[k]] = k;
@@ -789,7 +851,7 @@ void prepare(sta_ctx c) {
     ck(cudaMemsetAsync(d.bwd_done, 0, sizeof(u32) * std::max<u32>(c->S, 1), s), "memset");
     d.trace = nullptr;
     if (!c->trace_path.empty()) {   // debug: per-chunk / per-unit timestamps
-      const size_t n = 3 * ((size_t)c->NP / sta::kChunk + c->n_units);
+      const size_t n = 3 * ((size_t)c->n_fchunks + c->n_units);
       d.trace = a.alloc<unsigned long long>(n);
       ck(cudaMemsetAsync(d.trace, 0, n * sizeof(unsigned long long), s), "memset");
     }
@@ -809,12 +871,12 @@ u32 enqueue_corner(sta_ctx c, const sta::CornerDev& d) {
   ck(sta::launch_rc(t, d, s), "rc kernel");
   launches += (t.nA ? 1 : 0) + (t.nB ? 1 : 0) + (t.nC ? 10 : 0);
   prof_mark(c, 1);
-  if (c->use_persistent && c->pgrid) {
+  if (c->use_persistent && c->pgrid && c->pgrid_b) {
     prof_mark(c, 2);
     ck(sta::launch_fwd_persistent(t, d, c->pgrid, c->lut_f4, s), "forward persistent kernel");
     prof_mark(c, 3);
     prof_mark(c, 4);
-    ck(sta::launch_bwd_persistent(t, d, c->pgrid, c->lut_f4, s), "backward persistent kernel");
+    ck(sta::launch_bwd_persistent(t, d, c->pgrid_b, c->lut_f4, s), "backward persistent kernel");
     prof_mark(c, 5);
     prof_mark(c, 6);
     ck(sta::launch_reduce(t, d, s), "reduce kernel");
@@ -853,17 +915,14 @@ void dump_trace(sta_ctx c) {
   const sta::CornerDev& d = c->corners[0].dev;
   if (!d.trace) return;
   ck(cudaStreamSynchronize(c->stream), "sync");
-  const size_t nch = c->NP / sta::kChunk, n = 3 * (nch + c->n_units);
+  const size_t nch = c->n_fchunks, n = 3 * (nch + c->n_units);
   std::vector<unsigned long long> h(n);
   ck(cudaMemcpy(h.data(), d.trace, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "D2H trace");
   FILE* f = std::fopen(c->trace_path.c_str(), "w");
   if (!f) return;
   std::fprintf(f, "kind,index,stage,start,ready,end\n");
-  for (size_t x = 0; x < nch; ++x) {
-    u32 st = 0;
-    while (st + 1 < c->S && c->pull_stage_ptr[st + 1] <= x * sta::kChunk) ++st;
-    std::fprintf(f, "fwd,%zu,%u,%llu,%llu,%llu\n", x, st, h[3 * x], h[3 * x + 1], h[3 * x + 2]);
-  }
+  for (size_t x = 0; x < nch; ++x)
+    std::fprintf(f, "fwd,%zu,%u,%llu,%llu,%llu\n", x, c->fchunk_stage_h[x], h[3 * x], h[3 * x + 1], h[3 * x + 2]);
   for (size_t u = 0; u < c->n_units; ++u)
     std::fprintf(f, "bwd,%zu,%u,%llu,%llu,%llu\n", u, c->unit_stage[u], h[3 * (nch + u)], h[3 * (nch + u) + 1],
                  h[3 * (nch + u) + 2]);
@@ -1065,6 +1124,7 @@ sta_status sta_create(int cuda_device, uint32_t num_corners, void* cuda_stream, 
   if (const char* g = std::getenv("STA_NO_GRAPH")) c->use_graph = g[0] == '0';
   if (const char* g = std::getenv("STA_STAGE_KERNELS")) c->use_persistent = g[0] == '0';
   if (const char* g = std::getenv("STA_TRACE")) c->trace_path = g;
+  if (const char* g = std::getenv("STA_RC_TIERB")) c->rc_tierB = g[0] == '1';
   *out = c;
   return STA_OK;
 }
@@ -1183,7 +1243,8 @@ sta_status sta_set_library(sta_ctx c, uint32_t corner, sta_mem mem, uint32_t num
     for (const CornerState& o : c->corners) bytes = std::max(bytes, o.lut_bytes);
     c->lut_f4 = bytes <= sta::kLutSmemMax ? (u32)(bytes / 16) : 0;
     if (c->lut_f4 && bytes > 48 * 1024) ck(sta::set_lut_smem_limit(bytes), "smem attribute");
-    c->pgrid = c->use_persistent ? sta::persistent_grid(c->lut_f4) : 0;
+    c->pgrid = c->use_persistent ? sta::persistent_grid(c->lut_f4, 0) : 0;
+  c->pgrid_b = c->use_persistent ? sta::persistent_grid(c->lut_f4, 1) : 0;
     ck(cudaStreamSynchronize(c->stream), "library upload");
     cs.lib = true;
   });

@@ -23,7 +23,7 @@ constexpr uint32_t kSeedClock = 0xFFFFFFFEu;   // stage-0 seed: ideal clock pin
 constexpr int kTierA = 8;                      // RC nodes handled by one thread in registers
 constexpr int kTierB = 256;                    // RC nodes handled by one warp (above: one block)
 constexpr int kTile = 32;                      // backward: sinks per warp tile
-constexpr uint32_t kChunk = 256;               // persistent kernels: pins per chunk (= block size)
+constexpr uint32_t kChunk = 256;               // persistent kernels: work per block unit; stage id padding
 
 // Device NLDM table pool (built by sta_set_library), shared-memory friendly:
 //   * table t: a block of kTabStride = 65 floats at t * 65: word 0 = offset
@@ -74,9 +74,13 @@ struct Topo {
   const uint32_t* chunk_stage;   // [NP / kChunk] stage of each forward chunk
   const uint32_t* stage_units;   // [S] backward units per stage
   const uint32_t* stage_chunks;  // [S] forward chunks per stage
+  const uint4* fchunks;          // forward chunks {pin0, npins, term0, nterms}
+  const uint32_t* fchunk_stage;  // stage of each forward chunk
+  const uint32_t* fi_pin;        // owner pull pin of each fan-in term
+  uint32_t n_fchunks;
   const uint32_t* stage_sink_end;// [S] end of the sink range of each stage's drivers
   const uint32_t* stage_tile_end;// [S] end of each stage's tiles
-  const uint4* units;            // backward units {stage, kind 0 tiles / 1 sink-less, first, count}
+  const uint4* units;            // backward units {stage, kind 0 tiles / 1 sink-less pins, first, count}
   uint32_t n_units;
   // constraints
   const float4* pi_at;       // [n_pi]
@@ -166,7 +170,7 @@ cudaError_t launch_bwd_stage(const Topo& t, const CornerDev& c, uint32_t tile0, 
 cudaError_t set_lut_smem_limit(size_t bytes);
 // persistent (cooperative, sync-free dataflow) forward / backward passes;
 // grid = co-resident blocks.  persistent_grid returns 0 if unsupported.
-uint32_t persistent_grid(uint32_t lut_f4);
+uint32_t persistent_grid(uint32_t lut_f4, int which);
 cudaError_t launch_fwd_persistent(const Topo& t, const CornerDev& c, uint32_t grid, uint32_t lut_f4, cudaStream_t s);
 cudaError_t launch_bwd_persistent(const Topo& t, const CornerDev& c, uint32_t grid, uint32_t lut_f4, cudaStream_t s);
 constexpr size_t kLutSmemMax = 160 * 1024;   // larger pools stay in global memory
