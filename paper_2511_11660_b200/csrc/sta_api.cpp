@@ -162,7 +162,6 @@ struct sta_ctx_s {
   // or one launch per gate stage (STA_STAGE_KERNELS=1, or no cooperative launch)
   bool use_persistent = true;
   std::string trace_path;         // STA_TRACE (debug)
-  bool rc_tierB = false;          // STA_RC_TIERB=1: warp-per-net RC tier for 9..256 nodes
   std::vector<u32> unit_stage;    // stage of each backward unit (trace labels)
   std::vector<u32> fchunk_stage_h; // stage of each forward chunk (trace labels)
   u32 pgrid = 0, pgrid_b = 0;     // co-resident grids (forward, backward)
@@ -582,113 +581,47 @@ void build_rc(sta_ctx c) {
       if (!seen[c->net_pins[x]]) fail(STA_ERR_RC, "rc net %u: sink pin %u has no RC node", n, c->net_pins[x]);
   }
 
-  // nets in driver order j; RC nodes renumbered net by net in that order
-  // ("internal nodes") so the kernels read topology contiguously.  R and Cw
-  // stay in the caller's node order (borrowed zero-copy), addressed by
-  // net_user[j] + local index.
-  std::vector<u32> net_drv, net_node{0}, net_user, node_user;
+  // nets in driver order j; each net's RC nodes renumbered in DFS preorder
+  // (children in increasing index order) into "internal nodes", so that a
+  // subtree is a contiguous range [pos, end) and the kernels read topology
+  // contiguously.  R and Cw stay in the caller's node order (borrowed
+  // zero-copy), addressed through node_user.
+  std::vector<u32> net_drv, net_node{0}, node_user, node_meta, node_tag;
   net_drv.reserve(N);
   node_user.reserve(c->n_rc);
+  node_meta.reserve(c->n_rc);
+  node_tag.reserve(c->n_rc);
+  std::vector<u32> cnt, ch, pos, endp, pre;
+  std::vector<std::pair<u32, u32>> stack;
+  std::vector<uint2> wtiles;                // warp tiles of nets with 1..32 nodes
+  std::vector<u32> lumped_j, tierC;
+  std::vector<u32> tc_user, tc_int, tc_end, tc_start, tc_eptr{0}, tc_ends, tc_root, tc_drv;
+  u32 wt_fill = 0;
   for (u32 i = 0; i < c->NP; ++i) {
     if (c->user_of_int[i] == kNone) continue;
     const u32 n = c->pin_net[c->user_of_int[i]];
     if (n == kNone) continue;
-    const u32 b = c->rc_ptr[n], m = c->rc_ptr[n + 1] - b;
+    const u32 j = (u32)net_drv.size();
+    const u32 ub = c->rc_ptr[n], m = c->rc_ptr[n + 1] - ub;
+    const u32 x0 = (u32)node_user.size();
     net_drv.push_back(i);
-    net_user.push_back(b);
-    for (u32 q = 0; q < m; ++q) node_user.push_back(b + q);
-    net_node.push_back((u32)node_user.size());
-  }
-  const u32 NJ = (u32)net_drv.size();
-  std::vector<int32_t> rc_parent(c->n_rc);
-  std::vector<u32> rc_sink(c->n_rc, kNone);
-  for (u32 x = 0; x < c->n_rc; ++x) {
-    const u32 un = node_user[x];
-    rc_parent[x] = c->rc_parent[un];
-    const u32 pin = c->rc_node_pin[un];
-    if (pin != kNone && c->is_sink[pin]) rc_sink[x] = c->int_of_user[pin] - c->NP;
-  }
-  c->node_user = std::move(node_user);
-
-  // tiers: A (<= 8 nodes, lumped included), B (<= 256), C (larger)
-  std::vector<u32> tierA, tierB, tierC;
-  for (u32 j = 0; j < NJ; ++j) {
-    const u32 m = net_node[j + 1] - net_node[j];
-    // tier B (warp per net, level schedule) is kept for STA_RC_TIERB=1; by
-    // default every net above kTierA nodes takes the Euler-tour scan path,
-    // which measured ~6x faster on C3 (no per-level barriers)
-    const bool tb = c->rc_tierB && m <= (u32)sta::kTierB;
-    (m <= (u32)sta::kTierA ? tierA : tb ? tierB : tierC).push_back(j);
-  }
-  // level schedules of tier B then tier C nets
-  std::vector<u32> sched_off{0}, sched_h, sched_hn, sched_doff{0}, sched_d, sched_dn, child_off{0}, child_ptr,
-      child;
-  auto schedule = [&](u32 j) {
-    const u32 b = net_node[j], m = net_node[j + 1] - b;
-    std::vector<u32> h(m, 0), dep(m, 0), cnt(m + 1, 0);
-    for (u32 i = m - 1; i >= 1; --i) {
-      const u32 pa = (u32)rc_parent[b + i];
-      h[pa] = std::max(h[pa], h[i] + 1);
-      cnt[pa + 1]++;
+    if (m == 0) {
+      lumped_j.push_back(j);
+      net_node.push_back(x0);
+      continue;
     }
-    for (u32 i = 1; i < m; ++i) dep[i] = dep[(u32)rc_parent[b + i]] + 1;
-    // children CSR (absolute into child[]), decreasing child index per parent
-    const u32 cbase = (u32)child.size();
-    for (u32 i = 0; i < m; ++i) cnt[i + 1] += cnt[i];
-    for (u32 i = 0; i <= m; ++i) child_ptr.push_back(cbase + cnt[i]);
-    child.resize(cbase + (m - 1));
+    cnt.assign(m + 1, 0);
+    ch.resize(m);
+    pos.resize(m);
+    endp.resize(m);
+    pre.clear();
+    for (u32 q = 1; q < m; ++q) cnt[(u32)c->rc_parent[ub + q] + 1]++;
+    for (u32 q = 0; q < m; ++q) cnt[q + 1] += cnt[q];
     {
       std::vector<u32> fill(cnt.begin(), cnt.end() - 1);
-      for (u32 i = m - 1; i >= 1; --i) child[cbase + fill[(u32)rc_parent[b + i]]++] = i;
+      for (u32 q = 1; q < m; ++q) ch[fill[(u32)c->rc_parent[ub + q]]++] = q;
     }
-    child_off.push_back((u32)child_ptr.size());
-    // nodes by height: [H+2 bounds relative to the node list] [m nodes]
-    const u32 H = *std::max_element(h.begin(), h.end());
-    std::vector<u32> hs(H + 2, 0);
-    for (u32 i = 0; i < m; ++i) hs[h[i] + 1]++;
-    for (u32 q = 0; q <= H; ++q) hs[q + 1] += hs[q];
-    for (u32 q = 0; q <= H + 1; ++q) sched_h.push_back(hs[q]);
-    const size_t hb = sched_h.size();
-    sched_h.resize(hb + m);
-    {
-      std::vector<u32> fill(hs.begin(), hs.end() - 1);
-      for (u32 i = 0; i < m; ++i) sched_h[hb + fill[h[i]]++] = i;
-    }
-    sched_hn.push_back(H + 1);
-    sched_off.push_back((u32)sched_h.size());
-    // nodes by depth >= 1: [Dm+1 bounds] [m-1 nodes]
-    const u32 Dm = *std::max_element(dep.begin(), dep.end());
-    std::vector<u32> ds(Dm + 1, 0);
-    for (u32 i = 1; i < m; ++i) ds[dep[i]]++;      // ds[d-1 + 1] counts depth d
-    std::vector<u32> bnd(Dm + 1, 0);
-    for (u32 q = 1; q <= Dm; ++q) bnd[q] = bnd[q - 1] + ds[q];
-    for (u32 q = 0; q <= Dm; ++q) sched_d.push_back(bnd[q]);
-    const size_t db = sched_d.size();
-    sched_d.resize(db + (m - 1));
-    {
-      std::vector<u32> fill(bnd.begin(), bnd.end());
-      for (u32 i = 1; i < m; ++i) sched_d[db + fill[dep[i] - 1]++] = i;
-    }
-    sched_dn.push_back(Dm);
-    sched_doff.push_back((u32)sched_d.size());
-  };
-  for (u32 j : tierB) schedule(j);
-  // tier C: one global array of all tier-C nodes, each net in DFS preorder
-  // (children in increasing index order), with subtree ends and, for each
-  // position, the positions whose subtree ends there
-  std::vector<u32> tc_user, tc_int, tc_end, tc_start, tc_eptr{0}, tc_ends, tc_root, tc_drv;
-  for (u32 j : tierC) {
-    const u32 b = net_node[j], m = net_node[j + 1] - b;
-    const u32 g0 = (u32)tc_user.size();
-    std::vector<u32> cnt(m + 1, 0), ch(m), pos(m), endp(m), pre;
-    pre.reserve(m);
-    for (u32 i = 1; i < m; ++i) cnt[(u32)rc_parent[b + i] + 1]++;
-    for (u32 i = 0; i < m; ++i) cnt[i + 1] += cnt[i];
-    {
-      std::vector<u32> fill(cnt.begin(), cnt.end() - 1);
-      for (u32 i = 1; i < m; ++i) ch[fill[(u32)rc_parent[b + i]]++] = i;
-    }
-    std::vector<std::pair<u32, u32>> stack{{0u, 0u}};   // (node, next child slot)
+    stack.assign(1, {0u, 0u});
     pos[0] = 0;
     pre.push_back(0);
     while (!stack.empty()) {
@@ -703,20 +636,52 @@ void build_rc(sta_ctx c) {
         stack.pop_back();
       }
     }
-    std::vector<std::vector<u32>> ends_at(m);
-    for (u32 a = 1; a < m; ++a)
-      if (endp[a] < m) ends_at[endp[a]].push_back(a);
-    for (u32 q = 0; q < m; ++q) {
-      tc_user.push_back(net_user[j] + pre[q]);
-      tc_int.push_back(b + pre[q]);
-      tc_end.push_back(g0 + endp[q]);
-      tc_start.push_back(g0);
-      for (u32 a : ends_at[q]) tc_ends.push_back(g0 + a);
-      tc_eptr.push_back((u32)tc_ends.size());
+    for (u32 t2 = 0; t2 < m; ++t2) {
+      const u32 q = pre[t2];
+      const u32 un = ub + q;
+      node_user.push_back(un);
+      const u32 ppos = q ? pos[(u32)c->rc_parent[un]] : 0xFFu;
+      node_meta.push_back(std::min<u32>(t2, 255) | (std::min<u32>(ppos, 255) << 8) |
+                          (std::min<u32>(endp[t2], 255) << 16));
+      const u32 pin = c->rc_node_pin[un];
+      u32 tag = kNone;
+      if (t2 == 0) tag = i | 0x80000000u;                      // root: the driver
+      else if (pin != kNone && c->is_sink[pin]) tag = c->int_of_user[pin] - c->NP;
+      node_tag.push_back(tag);
     }
-    tc_root.push_back(g0);
-    tc_drv.push_back(net_drv[j]);
+    net_node.push_back((u32)node_user.size());
+    if (m <= 32) {
+      if (wtiles.empty() || wt_fill + m > 32) {
+        wtiles.push_back(make_uint2(x0, 0));
+        wt_fill = 0;
+      }
+      wtiles.back().y += m;
+      wt_fill += m;
+    } else {
+      // tier C (> 32 nodes): one global array of their nodes (each net in
+      // preorder, as internally), subtree ends, and for each position the
+      // positions whose subtree ends there
+      tierC.push_back(j);
+      wt_fill = 33;                         // a warp tile covers a contiguous node range
+      const u32 g0 = (u32)tc_user.size();
+      std::vector<std::vector<u32>> ends_at(m);
+      for (u32 a2 = 1; a2 < m; ++a2)
+        if (endp[a2] < m) ends_at[endp[a2]].push_back(a2);
+      for (u32 t2 = 0; t2 < m; ++t2) {
+        tc_user.push_back(ub + pre[t2]);
+        tc_int.push_back(x0 + t2);
+        tc_end.push_back(g0 + endp[t2]);
+        tc_start.push_back(g0);
+        for (u32 a2 : ends_at[t2]) tc_ends.push_back(g0 + a2);
+        tc_eptr.push_back((u32)tc_ends.size());
+      }
+      tc_root.push_back(g0);
+      tc_drv.push_back(i);
+    }
   }
+  if (node_user.size() != c->n_rc)   // nets without a driver-order entry cannot exist
+    fail(STA_ERR_RC, "internal error: %zu of %u RC nodes placed", node_user.size(), c->n_rc);
+
   c->big_total = (u32)tc_user.size();
 
   cudaStream_t s = c->stream;
@@ -725,24 +690,14 @@ void build_rc(sta_ctx c) {
   sta::Topo& t = c->topo;
   t.net_drv = g.upload(net_drv, s);
   t.net_node = g.upload(net_node, s);
-  t.net_user = g.upload(net_user, s);
-  t.rc_parent = g.upload(rc_parent, s);
-  t.rc_sink = g.upload(rc_sink, s);
-  t.nA = (u32)tierA.size();
-  t.nB = (u32)tierB.size();
+  t.node_user = g.upload(node_user, s);
+  t.node_meta = g.upload(node_meta, s);
+  t.node_tag = g.upload(node_tag, s);
+  t.n_wtiles = (u32)wtiles.size();
+  t.wtiles = g.upload(wtiles, s);
+  t.n_lumped = (u32)lumped_j.size();
+  t.lumped_j = g.upload(lumped_j, s);
   t.nC = (u32)tierC.size();
-  t.tierA = g.upload(tierA, s);
-  t.tierB = g.upload(tierB, s);
-  t.tierC = g.upload(tierC, s);
-  t.sched_off = g.upload(sched_off, s);
-  t.sched_h = g.upload(sched_h, s);
-  t.sched_hn = g.upload(sched_hn, s);
-  t.sched_doff = g.upload(sched_doff, s);
-  t.sched_d = g.upload(sched_d, s);
-  t.sched_dn = g.upload(sched_dn, s);
-  t.child_off = g.upload(child_off, s);
-  t.child_ptr = g.upload(child_ptr, s);
-  t.child = g.upload(child, s);
   t.nCn = c->big_total;
   t.tc_user = g.upload(tc_user, s);
   t.tc_int = g.upload(tc_int, s);
@@ -752,6 +707,7 @@ void build_rc(sta_ctx c) {
   t.tc_ends = g.upload(tc_ends, s);
   t.tc_root = g.upload(tc_root, s);
   t.tc_drv = g.upload(tc_drv, s);
+  c->node_user = std::move(node_user);
   c->rc_net_j = std::move(net_drv);
   ck(cudaStreamSynchronize(s), "rc upload");
 }
@@ -869,7 +825,7 @@ u32 enqueue_corner(sta_ctx c, const sta::CornerDev& d) {
   u32 launches = 0;
   prof_mark(c, 0);
   ck(sta::launch_rc(t, d, s), "rc kernel");
-  launches += (t.nA ? 1 : 0) + (t.nB ? 1 : 0) + (t.nC ? 10 : 0);
+  launches += (t.n_wtiles ? 1 : 0) + (t.n_lumped ? 1 : 0) + (t.nC ? 10 : 0);
   prof_mark(c, 1);
   if (c->use_persistent && c->pgrid && c->pgrid_b) {
     prof_mark(c, 2);
@@ -1124,7 +1080,6 @@ sta_status sta_create(int cuda_device, uint32_t num_corners, void* cuda_stream, 
   if (const char* g = std::getenv("STA_NO_GRAPH")) c->use_graph = g[0] == '0';
   if (const char* g = std::getenv("STA_STAGE_KERNELS")) c->use_persistent = g[0] == '0';
   if (const char* g = std::getenv("STA_TRACE")) c->trace_path = g;
-  if (const char* g = std::getenv("STA_RC_TIERB")) c->rc_tierB = g[0] == '1';
   *out = c;
   return STA_OK;
 }

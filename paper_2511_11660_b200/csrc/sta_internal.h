@@ -20,8 +20,6 @@ namespace sta {
 
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kSeedClock = 0xFFFFFFFEu;   // stage-0 seed: ideal clock pin
-constexpr int kTierA = 8;                      // RC nodes handled by one thread in registers
-constexpr int kTierB = 256;                    // RC nodes handled by one warp (above: one block)
 constexpr int kTile = 32;                      // backward: sinks per warp tile
 constexpr uint32_t kChunk = 256;               // persistent kernels: work per block unit; stage id padding
 
@@ -88,28 +86,21 @@ struct Topo {
   const float2* po_out_max;  // [n_po]
   const float2* po_out_min;
   float period, clock_slew;
-  // RC: nets in driver order j; node arrays in driver order ("internal nodes")
+  // RC: nets in driver order j; each net's nodes in DFS preorder ("internal
+  // nodes", subtree of position p = [p, end(p))).
   const uint32_t* net_drv;   // [N] internal pull id of the driver
   const uint32_t* net_node;  // [N+1] internal node offsets
-  const uint32_t* net_user;  // [N] user node offset (R / Cw arrays are in user order)
   const float* net_lumped;   // [N] lumped load (nets without RC nodes)
-  const int32_t* rc_parent;  // [n_rc] internal node order, local parent
-  const uint32_t* rc_sink;   // [n_rc] sink index of the node's pin or kNone
+  const uint32_t* node_user; // [n_rc] caller node id (R / Cw are in caller order)
+  const uint32_t* node_meta; // [n_rc] pos | parent pos << 8 (0xFF: root) | end << 16 (nets <= 32 nodes)
+  const uint32_t* node_tag;  // [n_rc] sink index, driver | 0x80000000 at the root, or kNone
   const float* rc_scap;      // [n_rc] pin cap + PO load at the node
-  uint32_t nA, nB, nC;       // nets per tier
-  const uint32_t* tierA;     // net ids j with <= kTierA nodes (lumped included)
-  const uint32_t* tierB;     // warp-per-net tier
-  const uint32_t* tierC;     // block-per-net tier
-  const uint32_t* sched_off; // [nB+nC+1] schedule offset of each tier-B/C net (B first)
-  const uint32_t* sched_h;   // per net: height-level boundaries (relative), then nodes by height
-  const uint32_t* sched_hn;  // [nB+nC] number of height levels
-  const uint32_t* sched_d;   // depth-level boundaries / nodes by depth (depth >= 1)
-  const uint32_t* sched_doff;// [nB+nC+1]
-  const uint32_t* sched_dn;  // [nB+nC] number of depth levels
-  const uint32_t* child_off; // [nB+nC+1] offsets into child arrays
-  const uint32_t* child_ptr; // per net: [m+1] relative children CSR
-  const uint32_t* child;     // child local ids, decreasing within a parent
-  // tier C (nets > kTierB nodes), Euler-tour form over ONE global preorder
+  uint32_t n_wtiles;         // warp tiles of nets with 1..32 nodes (no net straddles a tile)
+  const uint2* wtiles;       // {first internal node, node count}
+  uint32_t n_lumped;
+  const uint32_t* lumped_j;  // nets without RC nodes
+  uint32_t nC;               // nets with > 32 nodes
+  // tier C (nets > 32 nodes), Euler-tour form over ONE global preorder
   // array of all tier-C nodes (each net contiguous, DFS preorder inside):
   // Cdown(g) = S[end(g)] - S[g] with S the global exclusive prefix sum of the
   // node caps, and elm(g) = G[g] - G[start(g) - 1] with G the global inclusive

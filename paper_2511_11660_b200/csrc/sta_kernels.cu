@@ -1,10 +1,11 @@
 // sta_kernels.cu -- sm_100a kernels of one graph-based STA timing update.
 //
 // Hot path:
-//   a1  rc_tierA/B/C_kernel   Elmore RC per net: Cdown bottom-up, load =
-//       Cdown[root], elm top-down, in fp64;
-//       one thread (<= 8 nodes, registers), one warp (<= 256 nodes, shared
-//       memory) or one block (larger) per net.
+//   a1  rc_warp_kernel / tc_* + scan_*   Elmore RC per net in fp64: Cdown
+//       (subtree caps), load = Cdown[root], Elmore = sum of R Cdown over the
+//       root path, from each net's DFS
+//       preorder: warp shuffle scans for nets <= 32 nodes, device-wide prefix
+//       sums (Euler tour) for larger nets.
 //   a2  seed_kernel + fwd_stage_kernel   arrival/slew, one launch per gate
 //       stage, one thread per stage pin; NLDM bilinear lookup for cell arcs
 //       (SPEC.md:371-388), Elmore + PERI slew for net arcs
@@ -264,121 +265,76 @@ __device__ __forceinline__ bool bad_rc(float r, float cw) {
   return !(r >= 0.f) || !(cw >= 0.f) || !(r < CUDART_INF_F) || !(cw < CUDART_INF_F);
 }
 
-// Tier A: one thread per net with <= kTierA nodes (lumped nets included);
-// the textbook two-pass recursion in fp64 with the per-node accumulators in
-// shared memory, node-major ([node][thread]: conflict-free for any parent
-// index), so no local-memory stack.  All global loads are issued first.
-__global__ void __launch_bounds__(kThreads) rc_tierA_kernel(Topo t, CornerDev c) {
-  __shared__ double s_cd[kTierA][kThreads];
-  __shared__ double s_el[kTierA][kThreads];
+// Nets with 1..32 RC nodes: one warp tile holds whole nets, one lane per
+// node in DFS preorder.  Cdown(p) = S[end(p)] - S[p] with S the segmented
+// exclusive prefix sum of node caps (shuffle scan), Elmore(p) = sum of
+// R * Cdown over the root path by pointer jumping over parent lanes (5
+// rounds), all in fp64; every node is read once, coalesced.
+__global__ void __launch_bounds__(kThreads) rc_warp_kernel(Topo t, CornerDev c) {
+  pdl_wait();
+  pdl_launch();
+  const int lane = threadIdx.x & 31;
+  const uint32_t wt = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (wt >= t.n_wtiles) return;
+  const uint2 tile = t.wtiles[wt];
+  const bool act = lane < (int)tile.y;
+  const uint32_t x = tile.x + lane;
+  uint32_t meta = 0, tag = kNone;
+  double C = 0.0;
+  float r = 0.f;
+  bool bad = false;
+  if (act) {
+    meta = t.node_meta[x];
+    tag = t.node_tag[x];
+    const uint32_t u = t.node_user[x];
+    const float cw = c.rc_vals[1][u];
+    const bool root = ((meta >> 8) & 0xFFu) == 0xFFu;
+    r = root ? 0.f : c.rc_vals[0][u];
+    bad = bad_rc(r, cw);
+    C = (double)cw + (double)t.rc_scap[x];
+  }
+  const int pos = (int)(meta & 0xFFu), ppos = (int)((meta >> 8) & 0xFFu), epos = (int)((meta >> 16) & 0xFFu);
+  // segmented inclusive scan of C (a net's lanes are contiguous; pos resets)
+  double inc = C;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+    if (pos >= o) inc += y;
+  }
+  double exc = __shfl_up_sync(0xFFFFFFFFu, inc, 1);
+  if (pos == 0) exc = 0.0;
+  const int seg0 = lane - pos;
+  const double s_end = __shfl_sync(0xFFFFFFFFu, inc, act ? seg0 + epos - 1 : lane);
+  const double cd = s_end - exc;            // subtree cap of this node
+  // root path sums of w = R * Cdown by pointer jumping
+  double val = (act && ppos != 0xFF) ? (double)r * cd : 0.0;
+  int pl = (act && ppos != 0xFF) ? seg0 + ppos : -1;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const double pv = __shfl_sync(0xFFFFFFFFu, val, pl >= 0 ? pl : lane);
+    const int pp = __shfl_sync(0xFFFFFFFFu, pl, pl >= 0 ? pl : lane);
+    if (pl >= 0) {
+      val += pv;
+      pl = pp;
+    }
+  }
+  if (act && tag != kNone) {
+    if (tag & 0x80000000u) c.load[tag & 0x7FFFFFFFu] = (float)cd;   // root: net load
+    else c.elm[tag] = (float)val;
+  }
+  if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(c.err_flag, 1u);
+}
+
+// nets without RC nodes: load = their pins' caps, no wire delay
+__global__ void __launch_bounds__(kThreads) rc_lumped_kernel(Topo t, CornerDev c) {
   pdl_wait();
   pdl_launch();
   const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= t.nA) return;
-  const int tid = threadIdx.x;
-  const uint32_t j = t.tierA[x];
+  if (x >= t.n_lumped) return;
+  const uint32_t j = t.lumped_j[x];
   const uint32_t drv = t.net_drv[j];
-  const uint32_t b = t.net_node[j];
-  const uint32_t m = t.net_node[j + 1] - b;
-  if (m == 0) {                            // lumped net
-    c.load[drv] = t.net_lumped[j];
-    for (uint32_t k = t.sink_ptr[drv]; k < t.sink_ptr[drv + 1]; ++k) c.elm[k] = 0.f;
-    return;
-  }
-  const float* R = c.rc_vals[0] + t.net_user[j];
-  const float* Cw = c.rc_vals[1] + t.net_user[j];
-  int par[kTierA];
-  float r[kTierA], cw[kTierA], sc[kTierA];
-  uint32_t snk[kTierA];
-#pragma unroll
-  for (int i = 0; i < kTierA; ++i) {
-    const bool in = i < (int)m;
-    par[i] = in ? t.rc_parent[b + i] : 0;
-    r[i] = (in && i) ? R[i] : 0.f;
-    cw[i] = in ? Cw[i] : 0.f;
-    sc[i] = in ? t.rc_scap[b + i] : 0.f;
-    snk[i] = (in && i) ? t.rc_sink[b + i] : kNone;
-  }
-  bool bad = false;
-#pragma unroll
-  for (int i = 0; i < kTierA; ++i) {
-    bad |= bad_rc(r[i], cw[i]);
-    s_cd[i][tid] = (double)cw[i] + (double)sc[i];
-  }
-  // Cdown bottom-up: children added to their parent in decreasing index order
-#pragma unroll
-  for (int i = kTierA - 1; i >= 1; --i)
-    if (i < (int)m) s_cd[par[i]][tid] += s_cd[i][tid];
-  c.load[drv] = (float)s_cd[0][tid];
-  s_el[0][tid] = 0.0;
-#pragma unroll
-  for (int i = 1; i < kTierA; ++i) {
-    if (i >= (int)m) break;
-    const double e = __fma_rn((double)r[i], s_cd[i][tid], s_el[par[i]][tid]);
-    s_el[i][tid] = e;
-    if (snk[i] != kNone) c.elm[snk[i]] = (float)e;
-  }
-  if (bad) atomicOr(c.err_flag, 1u);
-}
-
-// Tier B: one warp per net (<= kTierB nodes), height-level Cdown and
-// depth-level Elmore in shared memory.
-constexpr int kWarpsB = 4;
-__global__ void __launch_bounds__(32 * kWarpsB) rc_tierB_kernel(Topo t, CornerDev c) {
-  __shared__ double s_cd[kWarpsB][kTierB];
-  __shared__ double s_el[kWarpsB][kTierB];
-  pdl_wait();
-  pdl_launch();
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t x = blockIdx.x * kWarpsB + w;
-  if (x >= t.nB) return;
-  const uint32_t j = t.tierB[x];
-  const uint32_t drv = t.net_drv[j];
-  const uint32_t b = t.net_node[j];
-  const uint32_t m = t.net_node[j + 1] - b;
-  const float* R = c.rc_vals[0] + t.net_user[j];
-  const float* Cw = c.rc_vals[1] + t.net_user[j];
-  double* cd = s_cd[w];
-  double* el = s_el[w];
-  bool bad = false;
-  for (uint32_t i = lane; i < m; i += 32) {
-    const float cw = Cw[i];
-    bad |= bad_rc(i ? R[i] : 0.f, cw);
-    cd[i] = (double)cw + (double)t.rc_scap[b + i];
-  }
-  __syncwarp();
-  const uint32_t* sh = t.sched_h + t.sched_off[x];
-  const uint32_t hn = t.sched_hn[x];
-  const uint32_t* nodes = sh + hn + 1;
-  const uint32_t* cp = t.child_ptr + t.child_off[x];
-  for (uint32_t h = 0; h < hn; ++h) {
-    for (uint32_t y = sh[h] + lane; y < sh[h + 1]; y += 32) {
-      const uint32_t p = nodes[y];
-      double v = cd[p];
-      for (uint32_t q = cp[p]; q < cp[p + 1]; ++q) v += cd[t.child[q]];
-      cd[p] = v;
-    }
-    __syncwarp();
-  }
-  if (lane == 0) {
-    c.load[drv] = (float)cd[0];
-    el[0] = 0.0;
-  }
-  __syncwarp();
-  const uint32_t* sd = t.sched_d + t.sched_doff[x];
-  const uint32_t dn = t.sched_dn[x];
-  const uint32_t* dnodes = sd + dn + 1;
-  for (uint32_t h = 0; h < dn; ++h) {
-    for (uint32_t y = sd[h] + lane; y < sd[h + 1]; y += 32) {
-      const uint32_t i = dnodes[y];
-      const double e = __fma_rn((double)R[i], cd[i], el[t.rc_parent[b + i]]);
-      el[i] = e;
-      const uint32_t k = t.rc_sink[b + i];
-      if (k != kNone) c.elm[k] = (float)e;
-    }
-    __syncwarp();
-  }
-  if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(c.err_flag, 1u);
+  c.load[drv] = t.net_lumped[j];
+  for (uint32_t k = t.sink_ptr[drv]; k < t.sink_ptr[drv + 1]; ++k) c.elm[k] = 0.f;
 }
 
 // ---- tier C: Euler-tour RC over one global preorder array (sta_internal.h)
@@ -516,8 +472,8 @@ __global__ void __launch_bounds__(kThreads) tc_elm_kernel(Topo t, CornerDev c, c
   const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= t.nCn) return;
   const uint32_t st = t.tc_start[g];
-  const uint32_t k = t.rc_sink[t.tc_int[g]];
-  if (k != kNone) c.elm[k] = (float)(G[g] - (st ? G[st - 1] : 0.0));
+  const uint32_t k = t.node_tag[t.tc_int[g]];
+  if (k != kNone && !(k & 0x80000000u)) c.elm[k] = (float)(G[g] - (st ? G[st - 1] : 0.0));
 }
 
 // ------------------------------------------------------------ a2: forward
@@ -1199,8 +1155,8 @@ cudaError_t launch_scan(double* x, uint32_t n, double* tsum, double* toff, bool 
 
 cudaError_t launch_rc(const Topo& t, const CornerDev& c, cudaStream_t s) {
   cudaError_t e = cudaSuccess;
-  if (t.nA && e == cudaSuccess) e = pdl_launch_kernel(rc_tierA_kernel, blocks(t.nA), kThreads, s, t, c);
-  if (t.nB && e == cudaSuccess) e = pdl_launch_kernel(rc_tierB_kernel, blocks(t.nB, kWarpsB), 32 * kWarpsB, s, t, c);
+  if (t.n_wtiles && e == cudaSuccess) e = pdl_launch_kernel(rc_warp_kernel, blocks(32ull * t.n_wtiles), kThreads, s, t, c);
+  if (t.n_lumped && e == cudaSuccess) e = pdl_launch_kernel(rc_lumped_kernel, blocks(t.n_lumped), kThreads, s, t, c);
   if (t.nC && e == cudaSuccess) {
     const uint32_t n = t.nCn;
     const size_t tiles = (n + kScanTile - 1) / kScanTile;
