@@ -211,25 +211,45 @@ __device__ __forceinline__ void cell_bwd(const float* __restrict__ L, const Q4& 
 // Endpoint required-time seeds: PO: RAT_L = T - out_max,
 // RAT_E = -out_min; check: RAT_L = T - setup(slew_L(D), clock slew),
 // RAT_E = hold(slew_E(D), clock slew), only where the data arrival exists.
-__device__ __forceinline__ void apply_seed(const Topo& t, const CornerDev& c, const float* L, uint32_t e,
-                                           const Q4& at, const Q4& sl, Q4& r) {
+// The static part (endpoint record, PO seeds) is loaded before the stage
+// wait; the check-table lookups need the data slew and run after it.
+struct SeedPre {
+  Q4 po;              // PO seeds, or the undefined required time
+  uint32_t chk;       // first check table or kNone
+};
+
+__device__ __forceinline__ SeedPre load_seed(const Topo& t, uint32_t e) {
+  SeedPre p{undef_rat(), kNone};
+  if (e == kNone) return p;
   const EpRec ep = t.ep[e];
+  p.chk = ep.chk_tab;
   if (ep.po != kNone) {
     const float2 omax = t.po_out_max[ep.po], omin = t.po_out_min[ep.po];
-    r.v[2] = fminf(r.v[2], __fsub_rn(t.period, omax.x));
-    r.v[3] = fminf(r.v[3], __fsub_rn(t.period, omax.y));
-    r.v[0] = fmaxf(r.v[0], -omin.x);
-    r.v[1] = fmaxf(r.v[1], -omin.y);
+    p.po = Q4{{-omin.x, -omin.y, __fsub_rn(t.period, omax.x), __fsub_rn(t.period, omax.y)}};
   }
-  if (ep.chk_tab != kNone) {
+  return p;
+}
+
+__device__ __forceinline__ void apply_seed_pre(const Topo& t, const float* L, const SeedPre& p, const Q4& at,
+                                               const Q4& sl, Q4& r) {
+  r.v[0] = fmaxf(r.v[0], p.po.v[0]);
+  r.v[1] = fmaxf(r.v[1], p.po.v[1]);
+  r.v[2] = fminf(r.v[2], p.po.v[2]);
+  r.v[3] = fminf(r.v[3], p.po.v[3]);
+  if (p.chk != kNone) {
 #pragma unroll
     for (int rf = 0; rf < 2; ++rf) {
       if (fin(at.v[2 + rf]))
-        r.v[2 + rf] = fminf(r.v[2 + rf], __fsub_rn(t.period, lut(L, ep.chk_tab + rf, sl.v[2 + rf], t.clock_slew)));
+        r.v[2 + rf] = fminf(r.v[2 + rf], __fsub_rn(t.period, lut(L, p.chk + rf, sl.v[2 + rf], t.clock_slew)));
       if (fin(at.v[rf]))
-        r.v[rf] = fmaxf(r.v[rf], lut(L, ep.chk_tab + 2 + rf, sl.v[rf], t.clock_slew));
+        r.v[rf] = fmaxf(r.v[rf], lut(L, p.chk + 2 + rf, sl.v[rf], t.clock_slew));
     }
   }
+}
+
+__device__ __forceinline__ void apply_seed(const Topo& t, const CornerDev&, const float* L, uint32_t e,
+                                           const Q4& at, const Q4& sl, Q4& r) {
+  apply_seed_pre(t, L, load_seed(t, e), at, sl, r);
 }
 
 // slack_L = RAT_L - AT_L, slack_E = AT_E - RAT_E, +inf if either is undefined.
@@ -609,6 +629,7 @@ struct TileLane {
   uint32_t k, v, e, f0, f1, w0, info0, pe, p0, p1;
   float el, ld0;
   bool active;
+  SeedPre seed;       // the sink's endpoint seed (static part)
 };
 
 __device__ __forceinline__ TileLane tile_lane(const Topo& t, uint32_t tile, uint32_t k1) {
@@ -618,6 +639,7 @@ __device__ __forceinline__ TileLane tile_lane(const Topo& t, uint32_t tile, uint
   x.active = x.k < k1;
   x.v = kNone; x.e = kNone; x.f0 = 0; x.f1 = 0; x.w0 = 0; x.info0 = 0; x.pe = kNone; x.p0 = 0; x.p1 = 0;
   x.el = 0.f; x.ld0 = 0.f;
+  x.seed = SeedPre{undef_rat(), kNone};
   if (x.active) {
     x.v = t.sink_drv[x.k];
     x.e = t.pin_ep[t.NP + x.k];
@@ -626,6 +648,7 @@ __device__ __forceinline__ TileLane tile_lane(const Topo& t, uint32_t tile, uint
     x.pe = t.pin_ep[x.v];
     x.p0 = t.pfo_ptr[x.v];
     x.p1 = t.pfo_ptr[x.v + 1];
+    x.seed = load_seed(t, x.e);
     if (x.f1 > x.f0) {
       x.w0 = t.sfo_dst[x.f0];
       x.info0 = t.sfo_info[x.f0];
@@ -661,7 +684,7 @@ __device__ __forceinline__ void process_tile(const Topo& t, const CornerDev& c, 
     Q4 at = at_v, sl = sl_v;
     net_hop(at, sl, x.el);                  // the sink's own arrival / slew
     Q4 r = undef_rat();
-    if (x.e != kNone) apply_seed(t, c, L, x.e, at, sl, r);
+    if (x.e != kNone) apply_seed_pre(t, L, x.seed, at, sl, r);
     if (x.f1 > x.f0) cell_bwd(L, at, sl, x.info0, x.ld0, rw0, r);
     for (uint32_t f = x.f0 + 1; f < x.f1; ++f) {
       const uint32_t w = t.sfo_dst[f];
@@ -701,10 +724,12 @@ __device__ __forceinline__ void process_tile(const Topo& t, const CornerDev& c, 
   atomicMax(key + 1, f2o(acc.v[1]));
   atomicMin(key + 2, f2o(acc.v[2]));
   atomicMin(key + 3, f2o(acc.v[3]));
-  __threadfence();
-  const uint32_t done = atomicAdd(c.heavy_cnt + slot, 1u);
+  // release counter: orders this tile's key updates before it; only the last
+  // tile pays the acquire fence before reading everyone's keys
+  uint32_t done;
+  asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(done) : "l"(c.heavy_cnt + slot) : "memory");
   if (done + 1 != t.heavy_nchunk[slot]) return;
-  __threadfence();
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
   Q4 a;
   a.v[0] = o2f(atomicExch(key + 0, f2o(-CUDART_INF_F)));
   a.v[1] = o2f(atomicExch(key + 1, f2o(-CUDART_INF_F)));
@@ -989,7 +1014,7 @@ __global__ void __launch_bounds__(kThreads, 4) bwd_persistent_kernel(Topo t, Cor
     const uint4 ud = t.units[u];             // {stage, kind, first, count}
     const uint32_t w = threadIdx.x >> 5;
     TileLane x{};
-    uint32_t v = 0;
+    uint32_t v = 0, pe = kNone, p0 = 0, p1 = 0;
     if (ud.y == 0) {                         // static part before waiting
       if (w < ud.w) {
         const uint32_t tile = ud.z + w;
@@ -999,6 +1024,9 @@ __global__ void __launch_bounds__(kThreads, 4) bwd_persistent_kernel(Topo t, Cor
       }
     } else if (threadIdx.x < ud.w) {
       v = t.nosink[ud.z + threadIdx.x];
+      pe = t.pin_ep[v];
+      p0 = t.pfo_ptr[v];
+      p1 = t.pfo_ptr[v + 1];
     }
     block_wait_bwd(t, c, ud.x, &s_wm);
     if (c.trace && threadIdx.x == 0) t_ready = gtimer();
@@ -1007,7 +1035,7 @@ __global__ void __launch_bounds__(kThreads, 4) bwd_persistent_kernel(Topo t, Cor
     } else if (threadIdx.x < ud.w) {
       Q4 at, sl;
       load_rec(c, v, at, sl);
-      finish_pull<false>(t, c, L, v, at, sl, undef_rat());
+      finish_pull_pre<false>(t, c, L, v, pe, p0, p1, at, sl, undef_rat());
     }
     block_publish(c.bwd_done + ud.x);
     if (c.trace && threadIdx.x == 0) {
