@@ -104,6 +104,8 @@ struct sta_ctx_s {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t side = nullptr;    // tier-C RC branch (forked from / joined to `stream`)
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   u32 K = 1;
   std::string err;
   bool poisoned = false;
@@ -584,18 +586,21 @@ void build_rc(sta_ctx c) {
   // nets in driver order j; each net's RC nodes renumbered in DFS preorder
   // (children in increasing index order) into "internal nodes", so that a
   // subtree is a contiguous range [pos, end) and the kernels read topology
-  // contiguously.  R and Cw stay in the caller's node order (borrowed
-  // zero-copy), addressed through node_user.
-  std::vector<u32> net_drv, net_node{0}, node_user, node_meta, node_tag;
+  // contiguously.  Internal nodes are grouped by tier: nets of 1..32 nodes
+  // (warp tiles), then 33..kBNet (block tiles, packed densely), then larger
+  // (tier C), each group in driver order.  R and Cw stay in the caller's
+  // node order (borrowed zero-copy), addressed through node_user.
+  struct Group {
+    std::vector<u32> user, meta, tag;
+  } grp[3];
+  std::vector<u32> net_drv;
   net_drv.reserve(N);
-  node_user.reserve(c->n_rc);
-  node_meta.reserve(c->n_rc);
-  node_tag.reserve(c->n_rc);
   std::vector<u32> cnt, ch, pos, endp, pre;
   std::vector<std::pair<u32, u32>> stack;
   std::vector<uint2> wtiles;                // warp tiles of nets with 1..32 nodes
+  std::vector<uint2> btiles;                // block tiles of nets with 33..kBNet nodes (group-1 offsets)
   std::vector<u32> lumped_j, tierC;
-  std::vector<u32> tc_user, tc_int, tc_end, tc_start, tc_eptr{0}, tc_ends, tc_root, tc_drv;
+  std::vector<u32> tc_user, tc_int, tc_end, tc_start, tc_enter, tc_ev, tc_root, tc_drv;
   u32 wt_fill = 0;
   for (u32 i = 0; i < c->NP; ++i) {
     if (c->user_of_int[i] == kNone) continue;
@@ -603,13 +608,14 @@ void build_rc(sta_ctx c) {
     if (n == kNone) continue;
     const u32 j = (u32)net_drv.size();
     const u32 ub = c->rc_ptr[n], m = c->rc_ptr[n + 1] - ub;
-    const u32 x0 = (u32)node_user.size();
     net_drv.push_back(i);
     if (m == 0) {
       lumped_j.push_back(j);
-      net_node.push_back(x0);
       continue;
     }
+    const int tier = m <= 32 ? 0 : m <= sta::kBNet ? 1 : 2;
+    Group& G = grp[tier];
+    const u32 x0 = (u32)G.user.size();
     cnt.assign(m + 1, 0);
     ch.resize(m);
     pos.resize(m);
@@ -639,45 +645,70 @@ void build_rc(sta_ctx c) {
     for (u32 t2 = 0; t2 < m; ++t2) {
       const u32 q = pre[t2];
       const u32 un = ub + q;
-      node_user.push_back(un);
-      const u32 ppos = q ? pos[(u32)c->rc_parent[un]] : 0xFFu;
-      node_meta.push_back(std::min<u32>(t2, 255) | (std::min<u32>(ppos, 255) << 8) |
-                          (std::min<u32>(endp[t2], 255) << 16));
+      G.user.push_back(un);
+      if (tier == 0) {
+        const u32 ppos = q ? pos[(u32)c->rc_parent[un]] : 0xFFu;
+        G.meta.push_back(t2 | (ppos << 8) | (endp[t2] << 16));
+      } else if (tier == 1) {
+        const u32 ppos = q ? pos[(u32)c->rc_parent[un]] : 0x7FFu;
+        G.meta.push_back(t2 | (ppos << 10) | (endp[t2] << 21));
+      } else {
+        G.meta.push_back(0);                // tier C: tc_* arrays
+      }
       const u32 pin = c->rc_node_pin[un];
       u32 tag = kNone;
       if (t2 == 0) tag = i | 0x80000000u;                      // root: the driver
       else if (pin != kNone && c->is_sink[pin]) tag = c->int_of_user[pin] - c->NP;
-      node_tag.push_back(tag);
+      G.tag.push_back(tag);
     }
-    net_node.push_back((u32)node_user.size());
-    if (m <= 32) {
+    if (tier == 0) {
       if (wtiles.empty() || wt_fill + m > 32) {
         wtiles.push_back(make_uint2(x0, 0));
         wt_fill = 0;
       }
       wtiles.back().y += m;
       wt_fill += m;
+    } else if (tier == 1) {
+      if (btiles.empty() || btiles.back().y + m > sta::kBNet) btiles.push_back(make_uint2(x0, 0));
+      btiles.back().y += m;
     } else {
-      // tier C (> 32 nodes): one global array of their nodes (each net in
-      // preorder, as internally), subtree ends, and for each position the
-      // positions whose subtree ends there
+      // tier C (> kBNet nodes): one global array of their nodes (each net in
+      // preorder, as internally), subtree ends, and the Euler event sequence
+      // (before entering position t2: exit every node whose subtree ends
+      // there, deepest first; after the last node: exit the rest)
       tierC.push_back(j);
-      wt_fill = 33;                         // a warp tile covers a contiguous node range
-      const u32 g0 = (u32)tc_user.size();
-      std::vector<std::vector<u32>> ends_at(m);
-      for (u32 a2 = 1; a2 < m; ++a2)
-        if (endp[a2] < m) ends_at[endp[a2]].push_back(a2);
-      for (u32 t2 = 0; t2 < m; ++t2) {
+      const u32 g0 = (u32)tc_user.size();   // == x0: tier-C positions are group-2 internal offsets
+      std::vector<std::vector<u32>> ends_at(m + 1);
+      for (u32 a2 = 0; a2 < m; ++a2) ends_at[endp[a2]].push_back(a2);
+      tc_enter.resize(g0 + m);
+      for (u32 t2 = 0; t2 <= m; ++t2) {
+        for (auto it = ends_at[t2].rbegin(); it != ends_at[t2].rend(); ++it) tc_ev.push_back((g0 + *it) | 0x80000000u);
+        if (t2 == m) break;
+        tc_enter[g0 + t2] = (u32)tc_ev.size();
+        tc_ev.push_back(g0 + t2);
         tc_user.push_back(ub + pre[t2]);
-        tc_int.push_back(x0 + t2);
+        tc_int.push_back((x0 + t2) | (t2 == 0 ? 0x80000000u : 0u));
         tc_end.push_back(g0 + endp[t2]);
         tc_start.push_back(g0);
-        for (u32 a2 : ends_at[t2]) tc_ends.push_back(g0 + a2);
-        tc_eptr.push_back((u32)tc_ends.size());
       }
+      if (tc_ev.size() != 2 * (size_t)(g0 + m)) fail(STA_ERR_RC, "internal error: Euler tour of net %u", n);
       tc_root.push_back(g0);
       tc_drv.push_back(i);
     }
+  }
+  // concatenate the groups; rebase block tiles and tier-C internal ids
+  const u32 nA = (u32)grp[0].user.size(), nB = (u32)grp[1].user.size();
+  for (uint2& b : btiles) b.x += nA;
+  for (u32& x : tc_int) x += nA + nB;       // root bit (bit 31) unaffected: ids < 2^31
+  std::vector<u32> node_user, node_meta, node_tag;
+  node_user.reserve(c->n_rc);
+  node_meta.reserve(c->n_rc);
+  node_tag.reserve(c->n_rc);
+  for (Group& G : grp) {
+    node_user.insert(node_user.end(), G.user.begin(), G.user.end());
+    node_meta.insert(node_meta.end(), G.meta.begin(), G.meta.end());
+    node_tag.insert(node_tag.end(), G.tag.begin(), G.tag.end());
+    G = Group{};
   }
   if (node_user.size() != c->n_rc)   // nets without a driver-order entry cannot exist
     fail(STA_ERR_RC, "internal error: %zu of %u RC nodes placed", node_user.size(), c->n_rc);
@@ -689,12 +720,13 @@ void build_rc(sta_ctx c) {
   Arena& g = c->tree_arena;
   sta::Topo& t = c->topo;
   t.net_drv = g.upload(net_drv, s);
-  t.net_node = g.upload(net_node, s);
   t.node_user = g.upload(node_user, s);
   t.node_meta = g.upload(node_meta, s);
   t.node_tag = g.upload(node_tag, s);
   t.n_wtiles = (u32)wtiles.size();
   t.wtiles = g.upload(wtiles, s);
+  t.n_btiles = (u32)btiles.size();
+  t.btiles = g.upload(btiles, s);
   t.n_lumped = (u32)lumped_j.size();
   t.lumped_j = g.upload(lumped_j, s);
   t.nC = (u32)tierC.size();
@@ -703,8 +735,8 @@ void build_rc(sta_ctx c) {
   t.tc_int = g.upload(tc_int, s);
   t.tc_end = g.upload(tc_end, s);
   t.tc_start = g.upload(tc_start, s);
-  t.tc_eptr = g.upload(tc_eptr, s);
-  t.tc_ends = g.upload(tc_ends, s);
+  t.tc_enter = g.upload(tc_enter, s);
+  t.tc_ev = g.upload(tc_ev, s);
   t.tc_root = g.upload(tc_root, s);
   t.tc_drv = g.upload(tc_drv, s);
   c->node_user = std::move(node_user);
@@ -800,6 +832,7 @@ void prepare(sta_ctx c) {
     d.heavy_key = a.alloc<int4>(c->n_heavy);
     d.heavy_cnt = a.alloc<u32>(c->n_heavy);
     d.scratch = a.alloc<double>(sta::tierC_scratch(c->big_total));
+    ck(cudaMemsetAsync(d.scratch, 0, sizeof(double) * sta::tierC_scratch(c->big_total), s), "memset");
     d.err_flag = a.alloc<u32>(1);
     d.fwd_done = a.alloc<u32>(std::max<u32>(c->S, 1));
     d.bwd_done = a.alloc<u32>(std::max<u32>(c->S, 1));
@@ -824,8 +857,17 @@ u32 enqueue_corner(sta_ctx c, const sta::CornerDev& d) {
   cudaStream_t s = c->stream;
   u32 launches = 0;
   prof_mark(c, 0);
+  if (t.nC && std::getenv("STA_RC_SERIAL")) {
+    ck(sta::launch_rc_tierC(t, d, s), "rc tier-C kernels");
+  } else if (t.nC) {                         // tier C concurrently with the small nets
+    ck(cudaEventRecord(c->fork_ev, s), "fork");
+    ck(cudaStreamWaitEvent(c->side, c->fork_ev, 0), "fork wait");
+    ck(sta::launch_rc_tierC(t, d, c->side), "rc tier-C kernels");
+    ck(cudaEventRecord(c->join_ev, c->side), "join");
+  }
   ck(sta::launch_rc(t, d, s), "rc kernel");
-  launches += (t.n_wtiles ? 1 : 0) + (t.n_lumped ? 1 : 0) + (t.nC ? 10 : 0);
+  if (t.nC && !std::getenv("STA_RC_SERIAL")) ck(cudaStreamWaitEvent(s, c->join_ev, 0), "join wait");
+  launches += (t.n_wtiles ? 1 : 0) + (t.n_btiles ? 1 : 0) + (t.n_lumped ? 1 : 0) + (t.nC ? 1 : 0);
   prof_mark(c, 1);
   if (c->use_persistent && c->pgrid && c->pgrid_b) {
     prof_mark(c, 2);
@@ -905,7 +947,7 @@ void enqueue_update(sta_ctx c) {
         throw;
       }
       ck(cudaStreamEndCapture(s, &g), "end capture");
-      cudaError_t e = cudaGraphInstantiate(&c->gexec, g, 0);
+      cudaError_t e = cudaGraphInstantiate(&c->gexec, g, cudaGraphInstantiateFlagUseNodePriority);
       cudaGraphDestroy(g);
       ck(e, "graph instantiate");
       c->launches_per_update = launches;
@@ -1076,6 +1118,14 @@ sta_status sta_create(int cuda_device, uint32_t num_corners, void* cuda_stream, 
   }
   for (auto& e : c->ev)
     if (cudaEventCreate(&e) != cudaSuccess) { delete c; return STA_ERR_CUDA; }
+  int prio_lo = 0, prio_hi = 0;
+  if (cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming) != cudaSuccess) {
+    delete c;
+    return STA_ERR_CUDA;
+  }
   c->corners.resize(num_corners);
   if (const char* g = std::getenv("STA_NO_GRAPH")) c->use_graph = g[0] == '0';
   if (const char* g = std::getenv("STA_STAGE_KERNELS")) c->use_persistent = g[0] == '0';
@@ -1102,6 +1152,9 @@ sta_status sta_destroy(sta_ctx c) {
   invalidate_graph(c);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+  if (c->join_ev) cudaEventDestroy(c->join_ev);
+  if (c->side) cudaStreamDestroy(c->side);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return STA_OK;

@@ -21,6 +21,7 @@ namespace sta {
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kSeedClock = 0xFFFFFFFEu;   // stage-0 seed: ideal clock pin
 constexpr int kTile = 32;                      // backward: sinks per warp tile
+constexpr uint32_t kBNet = 1024;               // RC tier B: nets of 33..1024 nodes, one block tile
 constexpr uint32_t kChunk = 256;               // persistent kernels: work per block unit; stage id padding
 
 // Device NLDM table pool (built by sta_set_library), shared-memory friendly:
@@ -87,9 +88,9 @@ struct Topo {
   const float2* po_out_min;
   float period, clock_slew;
   // RC: nets in driver order j; each net's nodes in DFS preorder ("internal
-  // nodes", subtree of position p = [p, end(p))).
+  // nodes", subtree of position p = [p, end(p))), grouped by tier (A: 1..32
+  // nodes, B: 33..kBNet, C: larger), each group in driver order.
   const uint32_t* net_drv;   // [N] internal pull id of the driver
-  const uint32_t* net_node;  // [N+1] internal node offsets
   const float* net_lumped;   // [N] lumped load (nets without RC nodes)
   const uint32_t* node_user; // [n_rc] caller node id (R / Cw are in caller order)
   const uint32_t* node_meta; // [n_rc] pos | parent pos << 8 (0xFF: root) | end << 16 (nets <= 32 nodes)
@@ -97,21 +98,29 @@ struct Topo {
   const float* rc_scap;      // [n_rc] pin cap + PO load at the node
   uint32_t n_wtiles;         // warp tiles of nets with 1..32 nodes (no net straddles a tile)
   const uint2* wtiles;       // {first internal node, node count}
+  // tier B: nets with 33..kBNet nodes, whole nets in block tiles of <= kBNet
+  // contiguous nodes; their node_meta is pos | parent pos << 10 (0x7FF: root) | end << 21
+  uint32_t n_btiles;
+  const uint2* btiles;       // {first internal node, node count}
   uint32_t n_lumped;
   const uint32_t* lumped_j;  // nets without RC nodes
   uint32_t nC;               // nets with > 32 nodes
-  // tier C (nets > 32 nodes), Euler-tour form over ONE global preorder
-  // array of all tier-C nodes (each net contiguous, DFS preorder inside):
+  // tier C (nets > kBNet nodes), Euler-tour form over ONE global preorder
+  // array of all tier-C nodes (each net contiguous, DFS preorder inside) and
+  // its Euler event sequence (enter / exit of every node, 2 per node; a net
+  // whose root sits at position g0 owns events [2 g0, 2 g0 + 2 m)):
   // Cdown(g) = S[end(g)] - S[g] with S the global exclusive prefix sum of the
-  // node caps, and elm(g) = G[g] - G[start(g) - 1] with G the global inclusive
-  // prefix sum of (+w(g), -w(a) for each a whose subtree ends at g), w = R Cdown.
+  // node caps in preorder; with w = R Cdown, event values +w(a) at enter(a)
+  // and -w(a) at exit(a), and H their inclusive prefix sum,
+  // elm(g) = H[enter(g)] - H[2 g0 - 1] (the ancestors-or-self of g are exactly
+  // the nodes entered and not yet exited at enter(g)).
   uint32_t nCn;               // tier-C nodes
   const uint32_t* tc_user;    // [nCn] caller node id (R / Cw index)
-  const uint32_t* tc_int;     // [nCn] internal node id (scap / sink index)
+  const uint32_t* tc_int;     // [nCn] internal node id (scap / tag index) | 0x80000000 at a net root
   const uint32_t* tc_end;     // [nCn] global position one past the subtree
   const uint32_t* tc_start;   // [nCn] global position of the net's root
-  const uint32_t* tc_eptr;    // [nCn+1] CSR into tc_ends
-  const uint32_t* tc_ends;    // positions a with end(a) == g
+  const uint32_t* tc_enter;   // [nCn] event position of enter(g)
+  const uint32_t* tc_ev;      // [2 nCn] node position of each event | 0x80000000 for an exit
   const uint32_t* tc_root;    // [nC] root position of each tier-C net
   const uint32_t* tc_drv;     // [nC] its driver (internal pull id)
   // outputs to user order
@@ -134,23 +143,25 @@ struct CornerDev {
   uint32_t* heavy_cnt;// [n_heavy] finished tiles (self-resetting)
   const float* lut;   // table records (kTabStride floats each)
   const float* const* rc_vals;  // device {res, cap} pointer pair (user node order)
-  double* scratch;    // tier-C scratch: 3 * (nCn + 1) doubles + scan tiles
+  double* scratch;    // tier-C scratch (tierC_scratch; tickets / flags zero between updates)
   uint32_t* err_flag; // nonzero: bad RC value seen
   uint32_t* fwd_done; // [S] completed forward chunks per stage (reset by reduce_kernel)
   uint32_t* bwd_done; // [S] completed backward units per stage (reset by reduce_kernel)
   unsigned long long* trace;  // optional (STA_TRACE): per chunk / unit {start, ready, end} ns
 };
 
-constexpr int kRedBlocks = 148;
+constexpr int kRedBlocks = 4 * 148;
 
 // ---- launchers (sta_kernels.cu); all enqueue on `s` with programmatic
 // dependent launch, return cudaGetLastError()
+// RC of nets with <= kBNet nodes and lumped nets; tier C (nets > kBNet nodes) is
+// independent of it and is enqueued on a second stream (1 cooperative launch)
 cudaError_t launch_rc(const Topo& t, const CornerDev& c, cudaStream_t s);
-constexpr uint32_t kScanTile = 4096;          // elements per tier-C scan tile
-inline size_t tierC_scratch(uint32_t nCn) {   // doubles
-  const size_t tiles = (nCn + kScanTile - 1) / kScanTile;
-  return 3 * ((size_t)nCn + 1) + 2 * (tiles + 1);
-}
+cudaError_t launch_rc_tierC(const Topo& t, const CornerDev& c, cudaStream_t s);
+// tier-C scratch, doubles: S[n+1], H[2n], W[n], block sums[kTcMaxGrid], then
+// the grid barrier {count, generation} (u32, zero-initialised, self-resetting)
+constexpr uint32_t kTcMaxGrid = 1024;
+inline size_t tierC_scratch(uint32_t nCn) { return 4 * (size_t)nCn + 1 + kTcMaxGrid + 1; }
 cudaError_t launch_seed(const Topo& t, const CornerDev& c, uint32_t n0, cudaStream_t s);
 // lut_f4: float4 count of the table pool staged in shared memory per block
 // (0: the pool is too large, lookups read global memory)

@@ -345,25 +345,6 @@ __global__ void __launch_bounds__(kThreads) rc_warp_kernel(Topo t, CornerDev c) 
   if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(c.err_flag, 1u);
 }
 
-// nets without RC nodes (SPEC.md:307): load = their pins' caps, no wire delay
-__global__ void __launch_bounds__(kThreads) rc_lumped_kernel(Topo t, CornerDev c) {
-  pdl_wait();
-  pdl_launch();
-  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= t.n_lumped) return;
-  const uint32_t j = t.lumped_j[x];
-  const uint32_t drv = t.net_drv[j];
-  c.load[drv] = t.net_lumped[j];
-  for (uint32_t k = t.sink_ptr[drv]; k < t.sink_ptr[drv + 1]; ++k) c.elm[k] = 0.f;
-}
-
-// ---- tier C: Euler-tour RC over one global preorder array (sta_internal.h)
-// Device-wide fp64 prefix sums by reduce-then-scan with a fixed tiling
-// (bitwise reproducible): tile sums, one-block scan of the tile sums, then
-// per-tile scan plus offset.
-constexpr int kScanThreads = 1024;
-constexpr int kScanPer = kScanTile / kScanThreads;   // 4 elements per thread
-
 __device__ __forceinline__ double block_excl_scan(double v, double* s_warp, double* total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double inc = v;
@@ -392,108 +373,314 @@ __device__ __forceinline__ double block_excl_scan(double v, double* s_warp, doub
   return r;
 }
 
-__global__ void __launch_bounds__(kScanThreads) scan_tiles_kernel(const double* __restrict__ x, uint32_t n,
-                                                                  double* __restrict__ tsum) {
+// Tier B, nets with 33..kBNet nodes: one block per tile of whole nets, four
+// consecutive nodes per thread in shared memory.  Same arithmetic as the warp
+// kernel: Cdown from a block-wide exclusive scan of the node caps (a net's
+// subtree ranges never leave the net), Elmore by pointer jumping over parent
+// slots until every node reaches its root, fp64 throughout.
+constexpr uint32_t kBPer = kBNet / kThreads;
+
+__global__ void __launch_bounds__(kThreads) rc_block_kernel(Topo t, CornerDev c) {
+  __shared__ double s_S[kBNet + 1], s_v[kBNet];
+  __shared__ int16_t s_p[kBNet];
   __shared__ double s_warp[32];
   pdl_wait();
   pdl_launch();
-  const uint32_t base = blockIdx.x * kScanTile + threadIdx.x * kScanPer;
-  double v = 0.0;
+  const uint2 tile = t.btiles[blockIdx.x];
+  const uint32_t i0 = threadIdx.x * kBPer;
+  uint32_t meta[kBPer], tag[kBPer];
+  double C[kBPer];
+  float r[kBPer];
+  bool bad = false;
 #pragma unroll
-  for (int k = 0; k < kScanPer; ++k)
-    if (base + k < n) v += x[base + k];
-  double tot;
-  block_excl_scan(v, s_warp, &tot);
-  if (threadIdx.x == 0) tsum[blockIdx.x] = tot;
-}
-
-// one block: exclusive scan of the tile sums; x[n] receives the grand total
-__global__ void __launch_bounds__(kScanThreads) scan_offsets_kernel(const double* __restrict__ tsum, uint32_t ntiles,
-                                                                    double* __restrict__ toff, double* x, uint32_t n) {
-  __shared__ double s_warp[32];
-  pdl_wait();
-  pdl_launch();
-  double carry = 0.0;
-  for (uint32_t b0 = 0; b0 < ntiles; b0 += blockDim.x) {
-    const uint32_t i = b0 + threadIdx.x;
-    const double v = i < ntiles ? tsum[i] : 0.0;
-    double tot;
-    const double e = block_excl_scan(v, s_warp, &tot);
-    if (i < ntiles) toff[i] = carry + e;
-    carry += tot;
+  for (int k = 0; k < (int)kBPer; ++k) {
+    const uint32_t i = i0 + k;
+    meta[k] = 0; tag[k] = kNone; C[k] = 0.0; r[k] = 0.f;
+    if (i < tile.y) {
+      const uint32_t x = tile.x + i;
+      meta[k] = t.node_meta[x];
+      tag[k] = t.node_tag[x];
+      const uint32_t u = t.node_user[x];
+      const float cw = c.rc_vals[1][u];
+      r[k] = ((meta[k] >> 10) & 0x7FFu) == 0x7FFu ? 0.f : c.rc_vals[0][u];
+      bad |= bad_rc(r[k], cw);
+      C[k] = (double)cw + (double)t.rc_scap[x];
+    }
   }
-  if (threadIdx.x == 0) x[n] = carry;
-}
-
-__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(double* x, uint32_t n,
-                                                                  const double* __restrict__ toff, int inclusive) {
-  __shared__ double s_warp[32];
-  pdl_wait();
-  pdl_launch();
-  const uint32_t base = blockIdx.x * kScanTile + threadIdx.x * kScanPer;
-  double v[kScanPer];
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(c.err_flag, 1u);
   double sum = 0.0;
 #pragma unroll
-  for (int k = 0; k < kScanPer; ++k) {
-    v[k] = base + k < n ? x[base + k] : 0.0;
-    sum += v[k];
-  }
-  double run = toff[blockIdx.x] + block_excl_scan(sum, s_warp, nullptr);
+  for (int k = 0; k < (int)kBPer; ++k) sum += C[k];
+  double tot;
+  double run = block_excl_scan(sum, s_warp, &tot);
 #pragma unroll
-  for (int k = 0; k < kScanPer; ++k) {
-    if (inclusive) run += v[k];
-    if (base + k < n) x[base + k] = run;
-    if (!inclusive) run += v[k];
+  for (int k = 0; k < (int)kBPer; ++k) {
+    s_S[i0 + k] = run;
+    run += C[k];
+  }
+  if (threadIdx.x == 0) s_S[kBNet] = tot;
+  __syncthreads();
+  double val[kBPer];
+  int pl[kBPer];
+#pragma unroll
+  for (int k = 0; k < (int)kBPer; ++k) {
+    const uint32_t i = i0 + k;
+    const int pos = (int)(meta[k] & 0x3FFu), ppos = (int)((meta[k] >> 10) & 0x7FFu), epos = (int)(meta[k] >> 21);
+    const int seg0 = (int)i - pos;
+    const bool act = i < tile.y;
+    const double cd = act ? (epos + seg0 == (int)tile.y ? s_S[kBNet] : s_S[seg0 + epos]) - s_S[i] : 0.0;
+    C[k] = cd;
+    const bool child = act && ppos != 0x7FF;
+    val[k] = child ? (double)r[k] * cd : 0.0;
+    pl[k] = child ? seg0 + ppos : -1;
+  }
+  // pointer jumping: val(i) += val(p(i)), p(i) = p(p(i)), synchronously
+  for (;;) {
+#pragma unroll
+    for (int k = 0; k < (int)kBPer; ++k) {
+      s_v[i0 + k] = val[k];
+      s_p[i0 + k] = (int16_t)pl[k];
+    }
+    __syncthreads();
+    bool more = false;
+#pragma unroll
+    for (int k = 0; k < (int)kBPer; ++k) {
+      if (pl[k] >= 0) {
+        val[k] += s_v[pl[k]];
+        pl[k] = s_p[pl[k]];
+        more |= pl[k] >= 0;
+      }
+    }
+    if (!__syncthreads_or(more)) break;
+  }
+#pragma unroll
+  for (int k = 0; k < (int)kBPer; ++k) {
+    if (i0 + k < tile.y && tag[k] != kNone) {
+      if (tag[k] & 0x80000000u) c.load[tag[k] & 0x7FFFFFFFu] = (float)C[k];   // root: net load
+      else c.elm[tag[k]] = (float)val[k];
+    }
   }
 }
 
-// node caps in preorder
-__global__ void __launch_bounds__(kThreads) tc_cap_kernel(Topo t, CornerDev c, double* A) {
+// nets without RC nodes (SPEC.md:307): load = their pins' caps, no wire delay
+__global__ void __launch_bounds__(kThreads) rc_lumped_kernel(Topo t, CornerDev c) {
   pdl_wait();
   pdl_launch();
-  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= t.nCn) return;
-  const uint32_t u = t.tc_user[g];
-  const float cw = c.rc_vals[1][u];
-  const float r = g == t.tc_start[g] ? 0.f : c.rc_vals[0][u];
-  if (bad_rc(r, cw)) atomicOr(c.err_flag, 1u);
-  A[g] = (double)cw + (double)t.rc_scap[t.tc_int[g]];
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= t.n_lumped) return;
+  const uint32_t j = t.lumped_j[x];
+  const uint32_t drv = t.net_drv[j];
+  c.load[drv] = t.net_lumped[j];
+  for (uint32_t k = t.sink_ptr[drv]; k < t.sink_ptr[drv + 1]; ++k) c.elm[k] = 0.f;
 }
 
-// Cdown = S[end] - S[g]; w = R Cdown on the edge into the node; net loads
-__global__ void __launch_bounds__(kThreads) tc_w_kernel(Topo t, CornerDev c, const double* S, double* W) {
-  pdl_wait();
-  pdl_launch();
-  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g < t.nC) {
-    const uint32_t r = t.tc_root[g];
-    c.load[t.tc_drv[g]] = (float)(S[t.tc_end[r]] - S[r]);
+// L2-only loads (ld.global.cg): the records reached L2 before the flag
+// (producer fence), the consumer's record loads are issued only after the
+// flag value returned (control dependency), and no L1 copy can be stale.  An
+// ld.acquire.gpu here would compile to CCTL.IVALL (whole-L1 invalidate),
+// which profiling showed to cost half of the kernel time.
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// ---- tier C: Euler-tour RC over one global preorder array (sta_internal.h)
+// One persistent cooperative kernel, two blocks per SM (a small footprint
+// next to the concurrently running small-net RC kernel), four phases
+// separated by grid barriers:
+//   1. S = exclusive prefix sum of the node caps (block ranges: local scan,
+//      block sums, barrier, offsets), S[n] = total;
+//   2. w(g) = R(g) (S[end(g)] - S[g]) in node order (0 at a net root), net loads;
+//   3. H = inclusive prefix sum of the Euler event values +-w;
+//   4. elm(g) = H[enter(g)] - H[2 g0 - 1].
+// Offsets are fixed-shape sums of the block sums: bitwise reproducible.
+constexpr int kTcThreads = 512;
+constexpr int kTcBatch = 4;                  // elements in flight per thread
+
+__device__ __forceinline__ void tc_grid_barrier(uint32_t* bar, uint32_t nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t gen = ld_acquire(bar + 1);
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      uint32_t ns = 32;
+      while (ld_acquire(bar + 1) == gen) {
+        __nanosleep(ns);
+        ns = ns < 256 ? 2 * ns : ns;
+      }
+    }
+    __threadfence();
   }
-  if (g >= t.nCn) return;
-  const double cd = S[t.tc_end[g]] - S[g];
-  W[g] = g == t.tc_start[g] ? 0.0 : (double)c.rc_vals[0][t.tc_user[g]] * cd;
+  __syncthreads();
 }
 
-// D[g] = w(g) - sum of w(a) over subtrees a ending at g
-__global__ void __launch_bounds__(kThreads) tc_d_kernel(Topo t, const double* W, double* D) {
-  pdl_wait();
-  pdl_launch();
-  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= t.nCn) return;
-  double v = W[g];
-  for (uint32_t q = t.tc_eptr[g]; q < t.tc_eptr[g + 1]; ++q) v -= W[t.tc_ends[q]];
-  D[g] = v;
+// fixed-tree sum of sums[0 .. b) (the offset of block b)
+__device__ __forceinline__ double tc_block_offset(const double* sums, uint32_t b, double* s_red) {
+  double v = 0.0;
+  for (uint32_t q = threadIdx.x; q < b; q += blockDim.x) v += __ldcg(sums + q);
+  s_red[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = kTcThreads / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) s_red[threadIdx.x] += s_red[threadIdx.x + o];
+    __syncthreads();
+  }
+  const double off = s_red[0];
+  __syncthreads();
+  return off;
 }
 
-// elm(g) = G[g] - G[start - 1]
-__global__ void __launch_bounds__(kThreads) tc_elm_kernel(Topo t, CornerDev c, const double* G) {
+// Device-wide prefix scan of x, whose block range [lo, hi) the block wrote
+// with the strided mapping i = lo + threadIdx.x + k blockDim.x, each thread
+// also accumulating `part` (its values in that order).  Block sums, grid
+// barrier, offsets, then one block-wide scan per row of blockDim.x values.
+// Returns the inclusive prefix at hi.
+template <bool INCLUSIVE>
+__device__ __forceinline__ double tc_scan_range(double* x, size_t lo, size_t hi, double part, double* sums,
+                                                uint32_t* bar, double* s_warp, double* s_red) {
+  s_red[threadIdx.x] = part;
+  __syncthreads();
+  for (int o = kTcThreads / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) s_red[threadIdx.x] += s_red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sums[blockIdx.x] = s_red[0];
+  tc_grid_barrier(bar, gridDim.x);
+  double carry = tc_block_offset(sums, blockIdx.x, s_red);
+  for (size_t r0 = lo; r0 < hi; r0 += blockDim.x) {
+    const size_t i = r0 + threadIdx.x;
+    const double v = i < hi ? x[i] : 0.0;      // own write (same mapping)
+    double tot;
+    const double e = block_excl_scan(v, s_warp, &tot);
+    if (i < hi) x[i] = carry + (INCLUSIVE ? e + v : e);
+    carry += tot;
+  }
+  return carry;
+}
+
+__global__ void __launch_bounds__(kTcThreads, 2) tc_persistent_kernel(Topo t, CornerDev c) {
+  __shared__ double s_warp[32], s_red[kTcThreads];
   pdl_wait();
   pdl_launch();
-  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= t.nCn) return;
-  const uint32_t st = t.tc_start[g];
-  const uint32_t k = t.node_tag[t.tc_int[g]];
-  if (k != kNone && !(k & 0x80000000u)) c.elm[k] = (float)(G[g] - (st ? G[st - 1] : 0.0));
+  const uint32_t n = t.nCn, G = gridDim.x, B = blockIdx.x, BD = blockDim.x;
+  const size_t m = 2 * (size_t)n;
+  double* S = c.scratch;                     // [n + 1]
+  double* H = S + n + 1;                     // [2n]
+  double* W = H + m;                         // [n]
+  double* sums = W + n;                      // [kTcMaxGrid]
+  uint32_t* bar = reinterpret_cast<uint32_t*>(sums + kTcMaxGrid);
+  const float* R = c.rc_vals[0];
+  const float* Cw = c.rc_vals[1];
+  const size_t lo = (size_t)n * B / G, hi = (size_t)n * (B + 1) / G;
+  const size_t elo = m * B / G, ehi = m * (B + 1) / G;
+  const size_t step = (size_t)BD * kTcBatch;
+
+  // 1. node caps -> S (exclusive)
+  bool bad = false;
+  double part = 0.0;
+  for (size_t i0 = lo + threadIdx.x; i0 < hi; i0 += step) {
+    float cw[kTcBatch], sc[kTcBatch];
+#pragma unroll
+    for (int k = 0; k < kTcBatch; ++k) {
+      const size_t i = i0 + (size_t)k * BD;
+      const bool in = i < hi;
+      const uint32_t u = in ? t.tc_user[i] : 0u, ti = in ? t.tc_int[i] : 0u;
+      cw[k] = in ? Cw[u] : 0.f;
+      sc[k] = in ? t.rc_scap[ti & 0x7FFFFFFFu] : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < kTcBatch; ++k) {
+      const size_t i = i0 + (size_t)k * BD;
+      if (i < hi) {
+        bad |= bad_rc(0.f, cw[k]);
+        const double v = (double)cw[k] + (double)sc[k];
+        S[i] = v;
+        part += v;
+      }
+    }
+  }
+  const double total = tc_scan_range<false>(S, lo, hi, part, sums, bar, s_warp, s_red);
+  if (B == G - 1 && threadIdx.x == 0) S[n] = total;
+  tc_grid_barrier(bar, G);
+
+  // 2. w in node order; net loads
+  for (size_t i0 = lo + threadIdx.x; i0 < hi; i0 += step) {
+    double w[kTcBatch];
+#pragma unroll
+    for (int k = 0; k < kTcBatch; ++k) {
+      const size_t i = i0 + (size_t)k * BD;
+      w[k] = 0.0;
+      if (i < hi && !(t.tc_int[i] & 0x80000000u)) {
+        const float r = R[t.tc_user[i]];
+        bad |= bad_rc(r, 0.f);
+        w[k] = (double)r * (__ldcg(S + t.tc_end[i]) - __ldcg(S + i));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kTcBatch; ++k) {
+      const size_t i = i0 + (size_t)k * BD;
+      if (i < hi) W[i] = w[k];
+    }
+  }
+  for (uint32_t j = B * BD + threadIdx.x; j < t.nC; j += G * BD) {
+    const uint32_t r = t.tc_root[j];
+    c.load[t.tc_drv[j]] = (float)(__ldcg(S + t.tc_end[r]) - __ldcg(S + r));
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(c.err_flag, 1u);
+  tc_grid_barrier(bar, G);
+
+  // 3. Euler event values -> H (inclusive)
+  part = 0.0;
+  for (size_t e0 = elo + threadIdx.x; e0 < ehi; e0 += step) {
+    double x[kTcBatch];
+#pragma unroll
+    for (int k = 0; k < kTcBatch; ++k) {
+      const size_t e = e0 + (size_t)k * BD;
+      x[k] = 0.0;
+      if (e < ehi) {
+        const uint32_t ev = t.tc_ev[e];
+        const double w = __ldcg(W + (ev & 0x7FFFFFFFu));
+        x[k] = (ev & 0x80000000u) ? -w : w;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kTcBatch; ++k) {
+      const size_t e = e0 + (size_t)k * BD;
+      if (e < ehi) {
+        H[e] = x[k];
+        part += x[k];
+      }
+    }
+  }
+  tc_scan_range<true>(H, elo, ehi, part, sums, bar, s_warp, s_red);
+  tc_grid_barrier(bar, G);
+
+  // 4. elm of the sink nodes
+  for (size_t i0 = lo + threadIdx.x; i0 < hi; i0 += step) {
+    uint32_t k2[kTcBatch];
+    float v[kTcBatch];
+#pragma unroll
+    for (int k = 0; k < kTcBatch; ++k) {
+      const size_t i = i0 + (size_t)k * BD;
+      k2[k] = kNone;
+      v[k] = 0.f;
+      if (i < hi) {
+        k2[k] = t.node_tag[t.tc_int[i] & 0x7FFFFFFFu];
+        const uint32_t g0 = t.tc_start[i];
+        v[k] = (float)(__ldcg(H + t.tc_enter[i]) - (g0 ? __ldcg(H + 2 * (size_t)g0 - 1) : 0.0));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kTcBatch; ++k)
+      if (k2[k] != kNone && !(k2[k] & 0x80000000u)) c.elm[k2[k]] = v[k];
+  }
 }
 
 // ------------------------------------------------------------ a2: forward
@@ -556,19 +743,6 @@ __global__ void __launch_bounds__(kThreads) fwd_stage_kernel(Topo t, CornerDev c
 // Persistent kernels publish completed work with a release store / atomic
 // after a block barrier and a gpu-scope fence.  Consumers poll the flag with
 // relaxed gpu-scope loads and, once it is set, read the produced records with
-// L2-only loads (ld.global.cg): the records reached L2 before the flag
-// (producer fence), the consumer's record loads are issued only after the
-// flag value returned (control dependency), and no L1 copy can be stale.  An
-// ld.acquire.gpu here would compile to CCTL.IVALL (whole-L1 invalidate),
-// which profiling showed to cost half of the kernel time.
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 // wait until *f >= target (wrap-around safe)
 // Exponential backoff (32 ns .. 1 us): a poller competes for issue slots with
 // the working warps of its SM; without backoff polling was 15% of the
@@ -778,7 +952,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-constexpr int kPrefetch = 4;   // fan-in terms whose topology is loaded up front
 
 // Block-level readiness.  Each block is a worker; its warp 0 checks the
 // per-stage completion counters of the stages a unit depends on, 32 stages
@@ -1049,27 +1222,9 @@ __global__ void __launch_bounds__(kThreads, 4) bwd_persistent_kernel(Topo t, Cor
 
 // ------------------------------------------------------- a5: WNS / TNS
 // kRedBlocks blocks with a fixed endpoint range each, fixed-shape trees and a
-// fixed-order final combine by the last block: bitwise reproducible.
-__global__ void __launch_bounds__(kThreads) reduce_kernel(Topo t, CornerDev c) {
-  __shared__ double s_t[2][kThreads];
-  __shared__ float s_w[2][kThreads];
-  __shared__ bool last;
-  pdl_wait();
-  pdl_launch();
-  const uint32_t n = t.n_ep;
-  const uint32_t lo = (uint32_t)((uint64_t)n * blockIdx.x / gridDim.x);
-  const uint32_t hi = (uint32_t)((uint64_t)n * (blockIdx.x + 1) / gridDim.x);
-  float ws = CUDART_INF_F, wh = CUDART_INF_F;
-  double ts = 0.0, th = 0.0;
-  for (uint32_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
-    const float2 x = __ldcg(c.ep_ws + e);
-    ws = fminf(ws, x.x);
-    wh = fminf(wh, x.y);
-    if (x.x < 0.f) ts += (double)x.x;
-    if (x.y < 0.f) th += (double)x.y;
-  }
-  s_w[0][threadIdx.x] = ws; s_w[1][threadIdx.x] = wh;
-  s_t[0][threadIdx.x] = ts; s_t[1][threadIdx.x] = th;
+// fixed-shape final combine by the last block: bitwise reproducible.
+// Fixed-shape block tree: min of the two w lanes, sum of the two t lanes.
+__device__ __forceinline__ void block_tree(float (*s_w)[kThreads], double (*s_t)[kThreads]) {
   __syncthreads();
   for (int o = kThreads / 2; o > 0; o >>= 1) {
     if ((int)threadIdx.x < o) {
@@ -1080,6 +1235,38 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(Topo t, CornerDev c) {
     }
     __syncthreads();
   }
+}
+
+__global__ void __launch_bounds__(kThreads) reduce_kernel(Topo t, CornerDev c) {
+  constexpr int kU = 4;                      // loads in flight per thread
+  __shared__ double s_t[2][kThreads];
+  __shared__ float s_w[2][kThreads];
+  __shared__ bool last;
+  pdl_wait();
+  pdl_launch();
+  const uint32_t n = t.n_ep;
+  const uint32_t lo = (uint32_t)((uint64_t)n * blockIdx.x / gridDim.x);
+  const uint32_t hi = (uint32_t)((uint64_t)n * (blockIdx.x + 1) / gridDim.x);
+  float ws = CUDART_INF_F, wh = CUDART_INF_F;
+  double ts = 0.0, th = 0.0;
+  for (uint32_t e0 = lo + threadIdx.x; e0 < hi; e0 += kU * blockDim.x) {
+    float2 x[kU];
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const uint32_t e = e0 + q * blockDim.x;
+      x[q] = e < hi ? __ldcg(c.ep_ws + e) : make_float2(CUDART_INF_F, CUDART_INF_F);
+    }
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      ws = fminf(ws, x[q].x);
+      wh = fminf(wh, x[q].y);
+      if (x[q].x < 0.f) ts += (double)x[q].x;
+      if (x[q].y < 0.f) th += (double)x[q].y;
+    }
+  }
+  s_w[0][threadIdx.x] = ws; s_w[1][threadIdx.x] = wh;
+  s_t[0][threadIdx.x] = ts; s_t[1][threadIdx.x] = th;
+  block_tree(s_w, s_t);
   if (threadIdx.x == 0) {
     double* p = c.red_part + 4 * blockIdx.x;
     p[0] = s_w[0][0]; p[1] = s_t[0][0]; p[2] = s_w[1][0]; p[3] = s_t[1][0];
@@ -1087,17 +1274,24 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(Topo t, CornerDev c) {
     last = atomicAdd(c.red_cnt, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
+  if (!last) return;
   __threadfence();
-  double r0 = CUDART_INF, r1 = 0.0, r2 = CUDART_INF, r3 = 0.0;
-  for (uint32_t b = 0; b < gridDim.x; ++b) {
-    const double* p = c.red_part + 4 * b;
-    r0 = fmin(r0, __ldcg(p + 0)); r1 += __ldcg(p + 1);
-    r2 = fmin(r2, __ldcg(p + 2)); r3 += __ldcg(p + 3);
+  // final combine of the block partials: fixed lanes, fixed tree
+  ws = CUDART_INF_F; wh = CUDART_INF_F; ts = 0.0; th = 0.0;
+  for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+    const double2 p = __ldcg(reinterpret_cast<const double2*>(c.red_part) + 2 * b);
+    const double2 q = __ldcg(reinterpret_cast<const double2*>(c.red_part) + 2 * b + 1);
+    ws = fminf(ws, (float)p.x); ts += p.y;
+    wh = fminf(wh, (float)q.x); th += q.y;
   }
-  c.res[0] = r0; c.res[1] = r1; c.res[2] = r2; c.res[3] = r3;
-  *c.red_cnt = 0;                           // self-reset for the next update
-  for (uint32_t x = 0; x < t.S; ++x) {        // stage counters: ready for the next update
+  s_w[0][threadIdx.x] = ws; s_w[1][threadIdx.x] = wh;
+  s_t[0][threadIdx.x] = ts; s_t[1][threadIdx.x] = th;
+  block_tree(s_w, s_t);
+  if (threadIdx.x == 0) {
+    c.res[0] = s_w[0][0]; c.res[1] = s_t[0][0]; c.res[2] = s_w[1][0]; c.res[3] = s_t[1][0];
+    *c.red_cnt = 0;                         // self-reset for the next update
+  }
+  for (uint32_t x = threadIdx.x; x < t.S; x += blockDim.x) {   // stage counters: ready for the next update
     c.bwd_done[x] = 0;
     c.fwd_done[x] = 0;
   }
@@ -1156,11 +1350,17 @@ cudaError_t pdl_launch_smem(K kernel, uint32_t grid, uint32_t block, size_t smem
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  // the stream's priority as an explicit launch attribute, so that it
+  // survives graph capture (tier-C RC runs beside the small-net RC kernel)
+  int prio = 0;
+  cudaStreamGetPriority(s, &prio);
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributePriority;
+  attr[1].val.priority = prio;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
@@ -1171,36 +1371,39 @@ cudaError_t pdl_launch_kernel(K kernel, uint32_t grid, uint32_t block, cudaStrea
 
 }  // namespace
 
-cudaError_t launch_scan(double* x, uint32_t n, double* tsum, double* toff, bool inclusive, cudaStream_t s) {
-  const uint32_t tiles = (n + kScanTile - 1) / kScanTile;
-  cudaError_t e = pdl_launch_kernel(scan_tiles_kernel, tiles, kScanThreads, s, (const double*)x, n, tsum);
-  if (e == cudaSuccess)
-    e = pdl_launch_kernel(scan_offsets_kernel, 1u, kScanThreads, s, (const double*)tsum, tiles, toff, x, n);
-  if (e == cudaSuccess)
-    e = pdl_launch_kernel(scan_apply_kernel, tiles, kScanThreads, s, x, n, (const double*)toff, inclusive ? 1 : 0);
-  return e;
-}
-
 cudaError_t launch_rc(const Topo& t, const CornerDev& c, cudaStream_t s) {
   cudaError_t e = cudaSuccess;
   if (t.n_wtiles && e == cudaSuccess) e = pdl_launch_kernel(rc_warp_kernel, blocks(32ull * t.n_wtiles), kThreads, s, t, c);
+  if (t.n_btiles && e == cudaSuccess) e = pdl_launch_kernel(rc_block_kernel, t.n_btiles, kThreads, s, t, c);
   if (t.n_lumped && e == cudaSuccess) e = pdl_launch_kernel(rc_lumped_kernel, blocks(t.n_lumped), kThreads, s, t, c);
-  if (t.nC && e == cudaSuccess) {
-    const uint32_t n = t.nCn;
-    const size_t tiles = (n + kScanTile - 1) / kScanTile;
-    double* A = c.scratch;
-    double* W = A + n + 1;
-    double* G = W + n + 1;
-    double* tsum = G + n + 1;
-    double* toff = tsum + tiles + 1;
-    const uint32_t nb = blocks(n > t.nC ? n : t.nC);
-    e = pdl_launch_kernel(tc_cap_kernel, blocks(n), kThreads, s, t, c, A);
-    if (e == cudaSuccess) e = launch_scan(A, n, tsum, toff, false, s);
-    if (e == cudaSuccess) e = pdl_launch_kernel(tc_w_kernel, nb, kThreads, s, t, c, (const double*)A, W);
-    if (e == cudaSuccess) e = pdl_launch_kernel(tc_d_kernel, blocks(n), kThreads, s, t, (const double*)W, G);
-    if (e == cudaSuccess) e = launch_scan(G, n, tsum, toff, true, s);
-    if (e == cudaSuccess) e = pdl_launch_kernel(tc_elm_kernel, blocks(n), kThreads, s, t, c, (const double*)G);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_rc_tierC(const Topo& t, const CornerDev& c, cudaStream_t s) {
+  if (!t.nC) return cudaSuccess;
+  static uint32_t grid = 0;
+  if (!grid) {
+    int dev = 0, sms = 0, nb = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tc_persistent_kernel, kTcThreads, 0);
+    grid = (uint32_t)std::min<int>(std::max(nb, 0) * sms, (int)kTcMaxGrid);
+    if (!grid) return cudaErrorCooperativeLaunchTooLarge;
   }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.stream = s;
+  int prio = 0;
+  cudaStreamGetPriority(s, &prio);
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributePriority;
+  attr[1].val.priority = prio;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_persistent_kernel, t, c);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
