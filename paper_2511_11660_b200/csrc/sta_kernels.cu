@@ -747,12 +747,15 @@ __global__ void __launch_bounds__(kThreads) fwd_stage_kernel(Topo t, CornerDev c
 // Exponential backoff (32 ns .. 1 us): a poller competes for issue slots with
 // the working warps of its SM; without backoff polling was 15% of the
 // forward kernel's instructions.
+// polling backoff cap: a waiter notices a completed stage at most this late
+constexpr uint32_t kMaxSleepNs = 128;
+
 __device__ __forceinline__ void wait_ge(const uint32_t* f, uint32_t target) {
   if ((int)(ld_acquire(f) - target) >= 0) return;
   uint32_t ns = 32;
   while ((int)(ld_acquire(f) - target) < 0) {
     __nanosleep(ns);
-    ns = ns < 1024 ? 2 * ns : ns;
+    ns = ns < kMaxSleepNs ? 2 * ns : ns;
   }
 }
 // backward: every unit of the stage of pull pin w is complete
@@ -974,7 +977,7 @@ __device__ __forceinline__ void block_wait_fwd(const Topo& t, const CornerDev& c
       } else {
         wm += __ffs(miss) - 1;
         __nanosleep(ns);
-        ns = ns < 1024 ? 2 * ns : ns;
+        ns = ns < kMaxSleepNs ? 2 * ns : ns;
       }
     }
     if (lane == 0) *s_wm = wm;
@@ -995,7 +998,7 @@ __device__ __forceinline__ void block_wait_bwd(const Topo& t, const CornerDev& c
       } else {
         wm -= __ffs(miss) - 1;
         __nanosleep(ns);
-        ns = ns < 1024 ? 2 * ns : ns;
+        ns = ns < kMaxSleepNs ? 2 * ns : ns;
       }
     }
     if (lane == 0) *s_wm = wm;
