@@ -56,6 +56,13 @@ __device__ __forceinline__ Q4 undef_at() { return Q4{{CUDART_INF_F, CUDART_INF_F
 // undefined required time: early -inf, late +inf (O7)
 __device__ __forceinline__ Q4 undef_rat() { return Q4{{-CUDART_INF_F, -CUDART_INF_F, CUDART_INF_F, CUDART_INF_F}}; }
 
+// %globaltimer (ns, 32 ns resolution): STA_TRACE timestamps
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // NLDM bilinear lookup with boundary-cell extrapolation on the
 // device table pool (layout in sta_internal.h), split into the two axis
 // searches and the interpolation so callers can reuse a search:
@@ -949,11 +956,6 @@ __global__ void __launch_bounds__(kThreads) bwd_stage_kernel(Topo t, CornerDev c
 // dependency order (block b takes items b, b + G, ...), every item depends
 // only on items with a smaller index, and all blocks are resident, so the
 // smallest unfinished item can always proceed: no deadlock, no grid barrier.
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 
 // Block-level readiness.  Each block is a worker; its warp 0 checks the
