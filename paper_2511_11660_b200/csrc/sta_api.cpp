@@ -22,6 +22,7 @@
 
 using sta::kNone;
 using u32 = uint32_t;
+using u64 = uint64_t;
 
 namespace {
 
@@ -128,7 +129,11 @@ struct sta_ctx_s {
   u32 NP = 0, NS = 0, S = 0, n0 = 0, Pi = 0;   // NP includes stage padding; Pi = NP + NS
   std::vector<u32> pull_stage_ptr, sink_stage_ptr, tile_stage_ptr, nosink_stage_ptr, sink_ptr;
   std::vector<u32> drv_of_net;    // user net -> internal driver id
-  u32 n_heavy = 0, n_units = 0, n_fchunks = 0;
+  u32 n_heavy = 0, n_fwu = 0, n_bwu = 0;
+  std::vector<u32> sfo_p, pfo_p, sink_drv;      // host copies for prepare()
+  std::vector<u32> sfo_dst, sfo_info, pfo_dst, pfo_info;
+  std::vector<u32> fwu_stage_ptr;                // [S + 1] forward units of each stage
+  std::vector<u32> bwu_stage_lo, bwu_stage_hi;   // [S] backward units of each stage (descending list)
 
   // ---- RC tree (host)
   std::vector<u32> rc_ptr, rc_node_pin;
@@ -164,8 +169,9 @@ struct sta_ctx_s {
   // or one launch per gate stage (STA_STAGE_KERNELS=1, or no cooperative launch)
   bool use_persistent = true;
   std::string trace_path;         // STA_TRACE (debug)
-  std::vector<u32> unit_stage;    // stage of each backward unit (trace labels)
-  std::vector<u32> fchunk_stage_h; // stage of each forward chunk (trace labels)
+  std::vector<u32> fwu_stage_h;   // stage of each forward warp unit (trace labels)
+  std::vector<u32> bwu_stage_h;   // stage of each backward warp unit (trace labels)
+  std::vector<u32> bwu_kind_h;    // 0 light tile, 1 heavy tile, 2 sink-less pins (trace labels)
   u32 pgrid = 0, pgrid_b = 0;     // co-resident grids (forward, backward)
 };
 
@@ -319,9 +325,16 @@ void build_plan(sta_ctx c) {
   c->int_of_user.assign(P, kNone);
   c->user_of_int.assign(c->Pi, kNone);
   {
+    // within a stage: drivers of nets with sinks first, then sink-less pins
+    // (each class by user id), so the backward's sink-less units are ranges
     std::vector<u32> fill(c->pull_stage_ptr.begin(), c->pull_stage_ptr.end());
-    for (u32 p = 0; p < P; ++p)
-      if (!c->is_sink[p]) {
+    auto has_sinks = [&](u32 p) {
+      const u32 n = c->pin_net[p];
+      return n != kNone && c->net_ptr[n + 1] - c->net_ptr[n] > 1;
+    };
+    for (int pass = 0; pass < 2; ++pass)
+      for (u32 p = 0; p < P; ++p)
+      if (!c->is_sink[p] && has_sinks(p) == (pass == 0)) {
         const u32 i = fill[c->stage[p]]++;
         c->int_of_user[p] = i;
         c->user_of_int[i] = p;
@@ -421,9 +434,26 @@ void build_plan(sta_ctx c) {
   std::vector<u32> nosink, heavy_nchunk;
   c->tile_stage_ptr.assign(S + 1, 0);
   c->nosink_stage_ptr.assign(S + 1, 0);
+  // Work-unit size adapts to the stage: a unit waits for the slowest of its
+  // inputs, so small stages (latency-bound) use small units -- down to one
+  // driver / pin per warp -- and large stages (throughput-bound) full ones.
+  // Target: about half the persistent grid's warps per stage.
+  u32 sms = 148;
+  {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
+      sms = (u32)n;
+    cudaGetLastError();
+  }
+  const u32 fwd_warps = sms * 8 * sta::kFwdMinBlocks, bwd_warps = sms * 8 * sta::kBwdMinBlocks;
+  auto unit_cap = [&](u64 items, u32 cap, u32 warps) {
+    const u64 per = (items + warps / 2 - 1) / (warps / 2);
+    return (u32)std::min<u64>(cap, std::max<u64>(1, per));
+  };
   for (u32 s = 0; s < S; ++s) {
     c->tile_stage_ptr[s] = (u32)tiles.size();
     c->nosink_stage_ptr[s] = (u32)nosink.size();
+    const u32 tcap = unit_cap(c->sink_ptr[c->pull_stage_ptr[s + 1]] - c->sink_ptr[c->pull_stage_ptr[s]], sta::kTile, bwd_warps);
     u32 cur = kNone, fill = 0;   // open light tile: first sink, lanes used
     for (u32 i = c->pull_stage_ptr[s]; i < c->pull_stage_ptr[s + 1]; ++i) {
       const u32 b = c->sink_ptr[i], n = c->sink_ptr[i + 1] - b;
@@ -439,7 +469,7 @@ void build_plan(sta_ctx c) {
         for (u32 q = 0; q < nch; ++q) tiles.push_back(make_uint2(b + q * sta::kTile, slot));
         continue;
       }
-      if (cur == kNone || fill + n > (u32)sta::kTile) {
+      if (cur == kNone || fill + n > tcap) {
         cur = b;
         fill = 0;
         tiles.push_back(make_uint2(b, kNone));
@@ -451,33 +481,37 @@ void build_plan(sta_ctx c) {
   c->nosink_stage_ptr[S] = (u32)nosink.size();
   c->n_heavy = (u32)heavy_nchunk.size();
 
-  // persistent-kernel work lists: forward chunks are kChunk consecutive pull
-  // pins of one stage; backward units (one block iteration each) are up to 8
-  // tiles or up to kChunk sink-less pins of one stage, in descending stage order
-  std::vector<u32> chunk_stage(NP / sta::kChunk), stage_units(S, 0), stage_sink_end(S), stage_tile_end(S);
-  for (u32 s = 0; s < S; ++s) {
-    for (u32 x = c->pull_stage_ptr[s] / sta::kChunk; x < c->pull_stage_ptr[s + 1] / sta::kChunk; ++x)
-      chunk_stage[x] = s;
-    stage_sink_end[s] = c->sink_ptr[c->pull_stage_ptr[s + 1]];
-    stage_tile_end[s] = c->tile_stage_ptr[s + 1];
-  }
-  // forward chunks: stage 0 = 256 seed pins; later stages = consecutive pins
-  // of one stage whose fan-in terms fit one 256-thread block (a pin with more
-  // terms gets a chunk of its own and is looped over)
-  std::vector<uint4> fchunks;              // {pin0, npins, item0, nitems}
-  std::vector<u32> fchunk_stage, stage_fchunks(S, 0), fi_pin(fi_src.size());
+  // persistent-kernel work lists (warp-granular dataflow, sta_kernels.cu):
+  // forward units are runs of consecutive pull pins of one stage with <=
+  // kFwdUnitTerms fan-in terms (four lanes per term; a pin with more terms
+  // is a unit of its own and its warp loops); stage-0 units are <=
+  // kFwdUnitTerms seed pins.  Unit u is the kFwdUnitTerms term slots
+  // [u kFwdUnitTerms, (u + 1) kFwdUnitTerms) of fterm (layout in
+  // sta_internal.h), so a lane's static data is one 16-byte load.  Backward
+  // units are one tile of <= kTile sinks, or <= kTile sink-less pins, in
+  // descending stage order.  Both lists are in dependency order: every unit
+  // depends only on units with a smaller index.
+  std::vector<uint4> fterm, bwu;           // forward term slots (kFwdUnitTerms per unit) / backward units
+  std::vector<u32> fwu_stage, stage_sink_end(S);
+  for (u32 s = 0; s < S; ++s) stage_sink_end[s] = c->sink_ptr[c->pull_stage_ptr[s + 1]];
+  std::vector<u32> fi_pin(fi_src.size());
   for (u32 i = 0; i < NP; ++i)
     for (u32 e = fi_p[i]; e < fi_p[i + 1]; ++e) fi_pin[e] = i;
+  const uint4 pad = make_uint4(kNone, kNone, 0, kNone);
   for (u32 s = 0; s < S; ++s) {
     const u32 p0 = c->pull_stage_ptr[s], p1 = c->pull_stage_ptr[s + 1];
-    if (s == 0) {
-      for (u32 p = p0; p < p1; p += sta::kChunk) {
-        fchunks.push_back(make_uint4(p, std::min<u32>(sta::kChunk, p1 - p), 0, 0));
-        fchunk_stage.push_back(s);
-        stage_fchunks[s]++;
+    if (s == 0) {                          // seed units: slot = pin
+      for (u32 p = p0; p < p1; p += sta::kFwdUnitTerms) {
+        u32 n = 0;
+        while (n < sta::kFwdUnitTerms && p + n < p1 && c->user_of_int[p + n] != kNone) ++n;
+        if (!n) break;                                  // stage padding
+        for (u32 x = 0; x < sta::kFwdUnitTerms; ++x)
+          fterm.push_back(make_uint4(sta::kSeedMark, 0, 0, x < n ? p + x : kNone));
+        fwu_stage.push_back(s);
       }
       continue;
     }
+    const u32 fcap = unit_cap(fi_p[p1] - fi_p[p0], sta::kFwdUnitTerms, fwd_warps);
     u32 p = p0;
     while (p < p1) {
       while (p < p1 && fi_p[p + 1] == fi_p[p]) ++p;   // stage padding: no work
@@ -486,35 +520,70 @@ void build_plan(sta_ctx c) {
       u32 items = 0;
       while (p < p1) {
         const u32 n = fi_p[p + 1] - fi_p[p];
-        if (n == 0 || (items && items + n > sta::kChunk) || p - q0 >= sta::kChunk) break;
+        if (n == 0 || (items && items + n > fcap)) break;
         items += n;
         ++p;
       }
-      fchunks.push_back(make_uint4(q0, p - q0, fi_p[q0], items));
-      fchunk_stage.push_back(s);
-      stage_fchunks[s]++;
+      const u32 e0 = fi_p[q0];
+      if (items > sta::kFwdUnitTerms) {    // one pin with many terms: the warp loops over fi_*
+        for (u32 x = 0; x < sta::kFwdUnitTerms; ++x) fterm.push_back(make_uint4(sta::kHeavyMark, e0, items, q0));
+      } else {
+        // probe term: the one whose source record is produced last (ids are
+        // in stage order)
+        u32 probe = 0;
+        for (u32 x = 1; x < items; ++x)
+          if (fi_src[e0 + x] > fi_src[e0 + probe]) probe = x;
+        for (u32 x = 0; x < sta::kFwdUnitTerms; ++x) {
+          if (x >= items) {
+            fterm.push_back(pad);
+            continue;
+          }
+          const u32 e = e0 + x;
+          if (fi_info[e] >> 31) fail(STA_ERR_LUT, "table id too large for the forward plan");
+          fterm.push_back(make_uint4(fi_src[e], fi_hop[e], fi_info[e] | (x == probe ? 0x80000000u : 0u), fi_pin[e]));
+        }
+      }
+      fwu_stage.push_back(s);
     }
   }
-  c->n_fchunks = (u32)fchunks.size();
-  c->fchunk_stage_h = fchunk_stage;
-  std::vector<uint4> units;
+  c->fwu_stage_ptr.assign(S + 1, 0);
+  for (u32 s : fwu_stage) c->fwu_stage_ptr[s + 1]++;
+  for (u32 s = 0; s < S; ++s) c->fwu_stage_ptr[s + 1] += c->fwu_stage_ptr[s];
+  c->bwu_stage_lo.assign(S, 0);
+  c->bwu_stage_hi.assign(S, 0);
   for (u32 s = S; s-- > 0;) {
-    for (u32 x = c->tile_stage_ptr[s]; x < c->tile_stage_ptr[s + 1]; x += 8) {
-      units.push_back(make_uint4(s, 0, x, std::min<u32>(8, c->tile_stage_ptr[s + 1] - x)));
-      stage_units[s]++;
+    c->bwu_stage_lo[s] = (u32)bwu.size();
+    for (u32 x = c->tile_stage_ptr[s]; x < c->tile_stage_ptr[s + 1]; ++x) {
+      const u32 k1 = x + 1 < c->tile_stage_ptr[s + 1] ? tiles[x + 1].x : stage_sink_end[s];
+      bwu.push_back(make_uint4(tiles[x].x, k1, tiles[x].y, 0));
     }
-    for (u32 x = c->nosink_stage_ptr[s]; x < c->nosink_stage_ptr[s + 1]; x += sta::kChunk) {
-      units.push_back(make_uint4(s, 1, x, std::min<u32>(sta::kChunk, c->nosink_stage_ptr[s + 1] - x)));
-      stage_units[s]++;
+    const u32 ncap = unit_cap(c->nosink_stage_ptr[s + 1] - c->nosink_stage_ptr[s], sta::kTile, bwd_warps);
+    for (u32 x = c->nosink_stage_ptr[s]; x < c->nosink_stage_ptr[s + 1]; x += ncap) {
+      const u32 x1 = std::min<u32>(x + ncap, c->nosink_stage_ptr[s + 1]);
+      if (nosink[x1 - 1] - nosink[x] != x1 - 1 - x) fail(STA_ERR_ARG, "internal: sink-less pins not contiguous");
+      bwu.push_back(make_uint4(nosink[x], nosink[x1 - 1] + 1, 0, 1));
     }
+    c->bwu_stage_hi[s] = (u32)bwu.size();
   }
-  c->n_units = (u32)units.size();
-  c->unit_stage.resize(units.size());
-  for (size_t u = 0; u < units.size(); ++u) c->unit_stage[u] = units[u].x;
+  c->n_fwu = (u32)fwu_stage.size();
+  c->n_bwu = (u32)bwu.size();
+  c->fwu_stage_h = fwu_stage;
+  c->bwu_stage_h.resize(bwu.size());
+  c->bwu_kind_h.resize(bwu.size());
+  for (size_t x = 0; x < bwu.size(); ++x) c->bwu_kind_h[x] = bwu[x].w ? 2 : bwu[x].z != kNone ? 1 : 0;
+  for (u32 s = 0; s < S; ++s)
+    for (u32 x = c->bwu_stage_lo[s]; x < c->bwu_stage_hi[s]; ++x) c->bwu_stage_h[x] = s;
 
-  std::vector<u32> sink_drv(c->NS);
+  std::vector<u32>& sink_drv = c->sink_drv;
+  sink_drv.assign(c->NS, 0);
   for (u32 i = 0; i < NP; ++i)
     for (u32 x = c->sink_ptr[i]; x < c->sink_ptr[i + 1]; ++x) sink_drv[x] = i;
+  c->sfo_p = sfo_p;
+  c->pfo_p = pfo_p;
+  c->sfo_dst = sfo_dst;
+  c->sfo_info = sfo_info;
+  c->pfo_dst = pfo_dst;
+  c->pfo_info = pfo_info;
 
   // upload
   cudaStream_t s = c->stream;
@@ -522,30 +591,19 @@ void build_plan(sta_ctx c) {
   sta::Topo& t = c->topo;
   t = sta::Topo{};
   t.P = P; t.NP = NP; t.NS = c->NS; t.S = S; t.N = c->N; t.n0 = c->n0;
-  t.fi_ptr = g.upload(fi_p, s);
   t.fi_src = g.upload(fi_src, s);
   t.fi_hop = g.upload(fi_hop, s);
   t.fi_info = g.upload(fi_info, s);
   t.sink_ptr = g.upload(c->sink_ptr, s);
   t.sink_drv = g.upload(sink_drv, s);
-  t.sfo_ptr = g.upload(sfo_p, s);
   t.sfo_dst = g.upload(sfo_dst, s);
   t.sfo_info = g.upload(sfo_info, s);
-  t.pfo_ptr = g.upload(pfo_p, s);
   t.pfo_dst = g.upload(pfo_dst, s);
   t.pfo_info = g.upload(pfo_info, s);
-  t.tiles = g.upload(tiles, s);
-  t.chunk_stage = g.upload(chunk_stage, s);
-  t.stage_units = g.upload(stage_units, s);
-  t.stage_chunks = g.upload(stage_fchunks, s);
-  t.fchunks = g.upload(fchunks, s);
-  t.fchunk_stage = g.upload(fchunk_stage, s);
-  t.fi_pin = g.upload(fi_pin, s);
-  t.n_fchunks = c->n_fchunks;
-  t.stage_sink_end = g.upload(stage_sink_end, s);
-  t.stage_tile_end = g.upload(stage_tile_end, s);
-  t.units = g.upload(units, s);
-  t.n_units = c->n_units;
+  t.fterm = g.upload(fterm, s);
+  t.n_fwu = c->n_fwu;
+  t.bwu = g.upload(bwu, s);
+  t.n_bwu = c->n_bwu;
   t.nosink = g.upload(nosink, s);
   t.heavy_nchunk = g.upload(heavy_nchunk, s);
   t.int_of_user = g.upload(c->int_of_user, s);
@@ -769,6 +827,26 @@ void prepare(sta_ctx c) {
     ep.push_back(r);
   }
   c->n_ep = (u32)ep.size();
+  // backward fan-out records (layout in sta_internal.h) and PO seeds
+  std::vector<float4> po_seed(c->po_pin.size());
+  for (u32 k = 0; k < c->po_pin.size(); ++k)   // fp32 arithmetic, as the kernels did it
+    po_seed[k] = make_float4(-c->po_out_min[2 * k], -c->po_out_min[2 * k + 1], c->period - c->po_out_max[2 * k],
+                             c->period - c->po_out_max[2 * k + 1]);
+  auto fo_rec = [&](uint4* r, u32 aux, u32 e, const std::vector<u32>& ptr, const std::vector<u32>& dst,
+                    const std::vector<u32>& info, u32 i) {
+    const u32 f0 = ptr[i], nfo = ptr[i + 1] - f0;
+    r[0] = make_uint4(aux, nfo, f0, e);
+    if (e != kNone) {
+      r[1] = make_uint4(ep[e].chk_tab, ep[e].po, 0, 0);
+    } else {
+      r[1] = make_uint4(nfo > 0 ? dst[f0] : kNone, nfo > 0 ? info[f0] : 0, nfo > 1 ? dst[f0 + 1] : kNone,
+                        nfo > 1 ? info[f0 + 1] : 0);
+    }
+  };
+  std::vector<uint4> sinkfo(2 * (size_t)c->NS), pullfo(2 * (size_t)c->NP);
+  for (u32 k = 0; k < c->NS; ++k)
+    fo_rec(&sinkfo[2 * (size_t)k], c->sink_drv[k], pin_ep[c->NP + k], c->sfo_p, c->sfo_dst, c->sfo_info, k);
+  for (u32 i = 0; i < c->NP; ++i) fo_rec(&pullfo[2 * (size_t)i], 0, pin_ep[i], c->pfo_p, c->pfo_dst, c->pfo_info, i);
   // stage-0 seeds
   std::vector<u32> seed(c->n0, kNone);
   for (u32 i = 0; i < c->n0; ++i) {
@@ -803,7 +881,9 @@ void prepare(sta_ctx c) {
   t.n_ep = c->n_ep;
   t.n_pi = (u32)c->pi_pin.size();
   t.n_po = (u32)c->po_pin.size();
-  t.pin_ep = g.upload(pin_ep, s);
+  t.sinkfo = g.upload(sinkfo, s);
+  t.pullfo = g.upload(pullfo, s);
+  t.po_seed = g.upload(po_seed, s);
   t.ep = g.upload(ep, s);
   t.seed = g.upload(seed, s);
   t.pi_at = reinterpret_cast<const float4*>(g.upload(c->pi_at, s));
@@ -820,7 +900,11 @@ void prepare(sta_ctx c) {
     cs.state_arena.release();
     Arena& a = cs.state_arena;
     sta::CornerDev& d = cs.dev;
-    d.rec = a.alloc<float4>(2 * (size_t)c->NP);
+    d.rec = a.alloc<uint4>(4 * (size_t)c->NP);
+    d.rat_ll = a.alloc<uint4>(2 * (size_t)c->NP);
+    d.epoch = a.alloc<u32>(1);
+    ck(cudaMemsetAsync(d.rec, 0, sizeof(uint4) * 4 * (size_t)c->NP, s), "memset");
+    ck(cudaMemsetAsync(d.rat_ll, 0, sizeof(uint4) * 2 * (size_t)c->NP, s), "memset");
     d.rat = a.alloc<float4>(c->Pi);
     d.slack = a.alloc<float4>(c->Pi);
     d.elm = a.alloc<float>(c->NS);
@@ -834,13 +918,9 @@ void prepare(sta_ctx c) {
     d.scratch = a.alloc<double>(sta::tierC_scratch(c->big_total));
     ck(cudaMemsetAsync(d.scratch, 0, sizeof(double) * sta::tierC_scratch(c->big_total), s), "memset");
     d.err_flag = a.alloc<u32>(1);
-    d.fwd_done = a.alloc<u32>(std::max<u32>(c->S, 1));
-    d.bwd_done = a.alloc<u32>(std::max<u32>(c->S, 1));
-    ck(cudaMemsetAsync(d.fwd_done, 0, sizeof(u32) * std::max<u32>(c->S, 1), s), "memset");
-    ck(cudaMemsetAsync(d.bwd_done, 0, sizeof(u32) * std::max<u32>(c->S, 1), s), "memset");
     d.trace = nullptr;
     if (!c->trace_path.empty()) {   // debug: per-chunk / per-unit timestamps
-      const size_t n = 3 * ((size_t)c->n_fchunks + c->n_units);
+      const size_t n = 4 * ((size_t)c->n_fwu + c->n_bwu);
       d.trace = a.alloc<unsigned long long>(n);
       ck(cudaMemsetAsync(d.trace, 0, n * sizeof(unsigned long long), s), "memset");
     }
@@ -882,21 +962,17 @@ u32 enqueue_corner(sta_ctx c, const sta::CornerDev& d) {
     return launches + 3;
   }
   prof_mark(c, 2);
-  ck(sta::launch_seed(t, d, c->n0, s), "seed kernel");
-  launches += c->n0 ? 1 : 0;
-  for (u32 st = 1; st < c->S; ++st) {
-    const u32 b0 = c->pull_stage_ptr[st], b1 = c->pull_stage_ptr[st + 1];
-    ck(sta::launch_fwd_stage(t, d, b0, b1 - b0, c->lut_f4, s), "forward kernel");
-    launches += (b1 - b0) ? 1 : 0;
+  for (u32 st = 0; st < c->S; ++st) {
+    const u32 u0 = c->fwu_stage_ptr[st], u1 = c->fwu_stage_ptr[st + 1];
+    ck(sta::launch_fwd_stage(t, d, u0, u1, c->lut_f4, s), "forward kernel");
+    launches += u1 > u0 ? 1 : 0;
   }
   prof_mark(c, 3);
   prof_mark(c, 4);
   for (u32 st = c->S; st-- > 0;) {
-    const u32 t0 = c->tile_stage_ptr[st], t1 = c->tile_stage_ptr[st + 1];
-    const u32 n0 = c->nosink_stage_ptr[st], n1 = c->nosink_stage_ptr[st + 1];
-    const u32 sink_end = c->sink_ptr[c->pull_stage_ptr[st + 1]];
-    ck(sta::launch_bwd_stage(t, d, t0, t1 - t0, sink_end, n0, n1 - n0, c->lut_f4, s), "backward kernel");
-    launches += (t1 - t0 + n1 - n0) ? 1 : 0;
+    const u32 u0 = c->bwu_stage_lo[st], u1 = c->bwu_stage_hi[st];
+    ck(sta::launch_bwd_stage(t, d, u0, u1, c->lut_f4, s), "backward kernel");
+    launches += u1 > u0 ? 1 : 0;
   }
   prof_mark(c, 5);
   prof_mark(c, 6);
@@ -913,17 +989,19 @@ void dump_trace(sta_ctx c) {
   const sta::CornerDev& d = c->corners[0].dev;
   if (!d.trace) return;
   ck(cudaStreamSynchronize(c->stream), "sync");
-  const size_t nch = c->n_fchunks, n = 3 * (nch + c->n_units);
+  const size_t nch = c->n_fwu, n = 4 * (nch + c->n_bwu);
   std::vector<unsigned long long> h(n);
   ck(cudaMemcpy(h.data(), d.trace, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "D2H trace");
   FILE* f = std::fopen(c->trace_path.c_str(), "w");
   if (!f) return;
-  std::fprintf(f, "kind,index,stage,start,ready,end\n");
+  std::fprintf(f, "kind,index,stage,start,ready,data,end,type\n");
   for (size_t x = 0; x < nch; ++x)
-    std::fprintf(f, "fwd,%zu,%u,%llu,%llu,%llu\n", x, c->fchunk_stage_h[x], h[3 * x], h[3 * x + 1], h[3 * x + 2]);
-  for (size_t u = 0; u < c->n_units; ++u)
-    std::fprintf(f, "bwd,%zu,%u,%llu,%llu,%llu\n", u, c->unit_stage[u], h[3 * (nch + u)], h[3 * (nch + u) + 1],
-                 h[3 * (nch + u) + 2]);
+    std::fprintf(f, "fwd,%zu,%u,%llu,%llu,%llu,%llu,0\n", x, c->fwu_stage_h[x], h[4 * x], h[4 * x + 1], h[4 * x + 2],
+                 h[4 * x + 3]);
+  for (size_t u = 0; u < c->n_bwu; ++u) {
+    const unsigned long long* q = &h[4 * (nch + u)];
+    std::fprintf(f, "bwd,%zu,%u,%llu,%llu,%llu,%llu,%u\n", u, c->bwu_stage_h[u], q[0], q[1], q[2], q[3], c->bwu_kind_h[u]);
+  }
   std::fclose(f);
 }
 

@@ -20,9 +20,24 @@ namespace sta {
 
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kSeedClock = 0xFFFFFFFEu;   // stage-0 seed: ideal clock pin
-constexpr int kTile = 32;                      // backward: sinks per warp tile
+constexpr uint32_t kSeedMark = 0xFFFFFFFDu;    // forward term slot: seed pin
+constexpr uint32_t kHeavyMark = 0xFFFFFFFCu;   // forward term slot: pin with many terms
+constexpr uint32_t kTile = 32;                 // backward: sinks per warp tile (lane = sink)
 constexpr uint32_t kBNet = 1024;               // RC tier B: nets of 33..1024 nodes, one block tile
-constexpr uint32_t kChunk = 256;               // persistent kernels: work per block unit; stage id padding
+constexpr uint32_t kChunk = 256;               // stage id padding; readiness group of the persistent kernels
+constexpr uint32_t kWarpUnit = 32;             // persistent kernels: items per warp unit
+constexpr uint32_t kFwdUnitTerms = 8;          // forward warp unit: fan-in terms (4 lanes each)
+// persistent kernels: co-resident 256-thread blocks per SM (register budget;
+// tuned on C3: the forward's short per-lane chains want many warps, the
+// backward's one-lane-per-sink chains want registers)
+#ifndef STA_FWD_BLOCKS
+#define STA_FWD_BLOCKS 5
+#endif
+#ifndef STA_BWD_BLOCKS
+#define STA_BWD_BLOCKS 3
+#endif
+constexpr int kFwdMinBlocks = STA_FWD_BLOCKS;
+constexpr int kBwdMinBlocks = STA_BWD_BLOCKS;
 
 // Device NLDM table pool (built by sta_set_library), shared-memory friendly:
 //   * table t: a block of kTabStride = 65 floats at t * 65: word 0 = offset
@@ -49,38 +64,46 @@ struct EpRec {          // one timing endpoint
 // Topology shared by all corners (device pointers).
 struct Topo {
   uint32_t P, NP, NS, S, N, n_ep, n_pi, n_po, n0;   // P: caller pins; NP: pull ids incl. padding
-  // forward: fan-in terms of pull pins
-  const uint32_t* fi_ptr;    // [NP+1]
+  // forward: fan-in terms of pull pins (heavy pins and tests; the kernels read fterm)
   const uint32_t* fi_src;    // record to read (driver of u, or u if u is a pull pin)
   const uint32_t* fi_hop;    // sink index of u (net hop to apply) or kNone
   const uint32_t* fi_info;
   const uint32_t* sink_ptr;  // [NP+1] sinks of each pull pin (sink index space)
   const uint32_t* sink_drv;  // [NS]
   const uint32_t* seed;      // [pins of stage 0]: PI index, kSeedClock or kNone
-  // backward
-  const uint32_t* sfo_ptr;   // [NS+1] cell fan-out of each sink
+  // backward: cell fan-out arcs of sinks / pull pins (ranges in sinkrec / pullrec)
   const uint32_t* sfo_dst;   // pull pin
   const uint32_t* sfo_info;
-  const uint32_t* pfo_ptr;   // [NP+1] cell fan-out of each pull pin
   const uint32_t* pfo_dst;
   const uint32_t* pfo_info;
-  const uint32_t* pin_ep;    // [P] internal id -> endpoint index or kNone
   const EpRec* ep;           // [n_ep]
-  const uint2* tiles;        // backward warp tiles: {first sink, heavy slot or kNone}, by stage
   const uint32_t* nosink;    // pull pins without sinks, by stage
   const uint32_t* heavy_nchunk; // [n_heavy] tiles of each heavy driver
-  // persistent kernels
-  const uint32_t* chunk_stage;   // [NP / kChunk] stage of each forward chunk
-  const uint32_t* stage_units;   // [S] backward units per stage
-  const uint32_t* stage_chunks;  // [S] forward chunks per stage
-  const uint4* fchunks;          // forward chunks {pin0, npins, term0, nterms}
-  const uint32_t* fchunk_stage;  // stage of each forward chunk
-  const uint32_t* fi_pin;        // owner pull pin of each fan-in term
-  uint32_t n_fchunks;
-  const uint32_t* stage_sink_end;// [S] end of the sink range of each stage's drivers
-  const uint32_t* stage_tile_end;// [S] end of each stage's tiles
-  const uint4* units;            // backward units {stage, kind 0 tiles / 1 sink-less pins, first, count}
-  uint32_t n_units;
+  // propagation work units (sta_kernels.cu), lists in dependency order
+  // forward warp unit u = term slots [kFwdUnitTerms u, kFwdUnitTerms (u + 1)):
+  //   {src, hop, info | probe << 31, pin}: a fan-in term of pull pin `pin`
+  //     (record src, sink hop or kNone); probe: the slot polled first
+  //   {kNone, kNone, 0, kNone}: padding
+  //   {kSeedMark, 0, 0, pin or kNone}: stage-0 pin (seed)
+  //   {kHeavyMark, term0, nterms, pin} in every slot: one pin with more than
+  //     kFwdUnitTerms terms (fi_* arrays), looped over by the warp
+  const uint4* fterm;
+  uint32_t n_fwu;
+  // backward warp units, descending stage: {k0, k1, heavy slot or kNone, 0}:
+  // sinks [k0, k1) (<= kTile, a light driver never split); {x0, x1, 0, 1}:
+  // sink-less pull pins [x0, x1) (<= kTile; internal ids of a stage put
+  // drivers first, so a stage's sink-less pins are contiguous)
+  const uint4* bwu;
+  uint32_t n_bwu;
+  // backward fan-out records, two uint4 per sink (sinkfo) / pull pin (pullfo):
+  //   a = {driver (sinks; 0 for pull pins), nfo = cell fan-out terms, f0 =
+  //        first term in sfo_* / pfo_*, endpoint index or kNone}
+  //   b = non-endpoints: {dst, info} of the first two fan-out terms (kNone
+  //       dst if absent); endpoints: {check table or kNone, PO index or
+  //       kNone, 0, 0} and the fan-out is read from sfo_* / pfo_*
+  const uint4* sinkfo;
+  const uint4* pullfo;
+  const float4* po_seed;         // [n_po] {-out_min_r, -out_min_f, T - out_max_r, T - out_max_f}
   // constraints
   const float4* pi_at;       // [n_pi]
   const float4* pi_slew;
@@ -130,8 +153,10 @@ struct Topo {
 
 // Per-corner device state.
 struct CornerDev {
-  float4* rec;        // [2 NP]: at, slew of pull pins (internal order)
-  float4* rat;        // [P]
+  uint4* rec;         // [4 NP]: tagged forward records of pull pins (sta_kernels.cu: ld_ll)
+  uint4* rat_ll;      // [2 NP]: tagged required times of pull pins
+  uint32_t* epoch;    // [1] tag of the current update (advanced by reduce_kernel)
+  float4* rat;        // [P]: required times of sinks (ids >= NP; pull pins use rat_ll)
   float4* slack;      // [P]
   float* elm;         // [NS] Elmore delay of each sink's net arc
   float* load;        // [NP] NLDM load seen by each pull pin (0 if no net)
@@ -145,9 +170,7 @@ struct CornerDev {
   const float* const* rc_vals;  // device {res, cap} pointer pair (user node order)
   double* scratch;    // tier-C scratch (tierC_scratch; tickets / flags zero between updates)
   uint32_t* err_flag; // nonzero: bad RC value seen
-  uint32_t* fwd_done; // [S] completed forward chunks per stage (reset by reduce_kernel)
-  uint32_t* bwd_done; // [S] completed backward units per stage (reset by reduce_kernel)
-  unsigned long long* trace;  // optional (STA_TRACE): per chunk / unit {start, ready, end} ns
+  unsigned long long* trace;  // optional (STA_TRACE): per warp unit {start, ready, end} ns
 };
 
 constexpr int kRedBlocks = 4 * 148;
@@ -162,13 +185,13 @@ cudaError_t launch_rc_tierC(const Topo& t, const CornerDev& c, cudaStream_t s);
 // the grid barrier {count, generation} (u32, zero-initialised, self-resetting)
 constexpr uint32_t kTcMaxGrid = 1024;
 inline size_t tierC_scratch(uint32_t nCn) { return 4 * (size_t)nCn + 1 + kTcMaxGrid + 1; }
-cudaError_t launch_seed(const Topo& t, const CornerDev& c, uint32_t n0, cudaStream_t s);
 // lut_f4: float4 count of the table pool staged in shared memory per block
 // (0: the pool is too large, lookups read global memory)
-cudaError_t launch_fwd_stage(const Topo& t, const CornerDev& c, uint32_t pull0, uint32_t n, uint32_t lut_f4,
+// units [u0, u1) of one gate stage (one launch per stage)
+cudaError_t launch_fwd_stage(const Topo& t, const CornerDev& c, uint32_t u0, uint32_t u1, uint32_t lut_f4,
                              cudaStream_t s);
-cudaError_t launch_bwd_stage(const Topo& t, const CornerDev& c, uint32_t tile0, uint32_t nTiles, uint32_t sinkEnd,
-                             uint32_t nos0, uint32_t nNos, uint32_t lut_f4, cudaStream_t s);
+cudaError_t launch_bwd_stage(const Topo& t, const CornerDev& c, uint32_t u0, uint32_t u1, uint32_t lut_f4,
+                             cudaStream_t s);
 cudaError_t set_lut_smem_limit(size_t bytes);
 // persistent (cooperative, sync-free dataflow) forward / backward passes;
 // grid = co-resident blocks.  persistent_grid returns 0 if unsupported.

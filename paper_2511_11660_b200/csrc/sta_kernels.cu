@@ -140,144 +140,53 @@ __device__ __forceinline__ void net_hop(Q4& at, Q4& sl, float e) {
   }
 }
 
-// Cell arc u -> v (forward): merge the candidates of every (el, irf -> orf)
-// pair the sense allows into acc_at / acc_sl (early min, late max).  The load
-// axis search of each of the 4 tables is done once per arc.
-__device__ __forceinline__ void cell_fwd(const float* __restrict__ L, const Q4& at, const Q4& sl, uint32_t info,
-                                         float ld, Q4& acc_at, Q4& acc_sl) {
-  const uint32_t sense = info & 7u, tab = info >> 3;
-  const Tab rd0 = tab_rec(L, tab);            // cell_rise
-  const Tab rd1 = tab_rec(L, tab + 1);        // cell_fall
-  const Tab rs0 = tab_rec(L, tab + 2);        // rise_transition
-  const Tab rs1 = tab_rec(L, tab + 3);        // fall_transition
-  // tables of one library template share their axis searches
-  const Seg cd0 = seg(rd0.ax + 24, ld);
-  const Seg cd1 = rd1.ax == rd0.ax ? cd0 : seg(rd1.ax + 24, ld);
-  const Seg cs0 = rs0.ax == rd0.ax ? cd0 : seg(rs0.ax + 24, ld);
-  const Seg cs1 = rs1.ax == rd1.ax ? cd1 : seg(rs1.ax + 24, ld);
-#pragma unroll
-  // one pass: the plan expands a non-unate arc into positive- and
-  // negative-unate terms (sta_api.cpp build_plan)
-  for (int pass = 0; pass < 1; ++pass) {
-#pragma unroll
-    for (int orf = 0; orf < 2; ++orf) {
-      const int irf = pass ? 1 - primary_irf(sense, orf) : primary_irf(sense, orf);
-      const Tab rd = orf ? rd1 : rd0;
-      const Tab rs = orf ? rs1 : rs0;
-      const Seg cd = orf ? cd1 : cd0;
-      const Seg cs = orf ? cs1 : cs0;
-#pragma unroll
-      for (int el = 0; el < 2; ++el) {
-        const float a_in = irf ? at.v[el * 2 + 1] : at.v[el * 2];
-        const float s_in = irf ? sl.v[el * 2 + 1] : sl.v[el * 2];
-        if (!fin(a_in)) continue;
-        const Seg sd = seg(rd.ax, s_in);
-        const Seg ss = rs.ax == rd.ax ? sd : seg(rs.ax, s_in);
-        const float d = fmaxf(0.f, interp(rd, sd, cd));
-        const float so = fmaxf(0.f, interp(rs, ss, cs));
-        const float ca = __fadd_rn(a_in, d);
-        const int q = el * 2 + orf;
-        if (el == 0) { acc_at.v[q] = fminf(acc_at.v[q], ca); acc_sl.v[q] = fminf(acc_sl.v[q], so); }
-        else         { acc_at.v[q] = fmaxf(acc_at.v[q], ca); acc_sl.v[q] = fmaxf(acc_sl.v[q], so); }
-      }
-    }
+// ---- tagged ("low-latency") records.  The forward record of pull pin v is
+// four 16-byte words, word q = (el, rf) = {AT_q, tag, slew_q, tag}; the
+// backward required time of pull pin v is two words, word el =
+// {RAT_(el,r), tag, RAT_(el,f), tag}.  tag = the update's epoch (*c.epoch,
+// advanced by reduce_kernel), so a word is valid for this update iff both
+// its tags equal the epoch: every 8-byte {value, tag} half validates itself
+// (8-byte accesses are single-copy atomic), no flag, fence or counter is
+// needed, and a consumer detects readiness with the same L2 round trip that
+// fetches the data (a producer -> consumer hop measured 265 ns vs 920 ns for
+// data + release flag + poll + load, scripts/ubench/pingpong.cu).
+__device__ __forceinline__ uint4 ld_ll(const uint4* p) {
+  uint4 w;
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w) : "l"(p) : "memory");
+  return w;
+}
+__device__ __forceinline__ void st_ll(uint4* p, float a, float b, uint32_t ep) {
+  asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};"
+               ::"l"(p), "r"(__float_as_uint(a)), "r"(ep), "r"(__float_as_uint(b)), "r"(ep) : "memory");
+}
+__device__ __forceinline__ bool ll_ok(const uint4& w, uint32_t ep) { return w.y == ep && w.w == ep; }
+// polling backoff cap: a waiter notices a completed record at most this late
+constexpr uint32_t kMaxSleepNs = 128;
+__device__ __forceinline__ uint4 spin_ll(const uint4* p, uint32_t ep) {
+  uint4 w = ld_ll(p);
+  uint32_t ns = 32;
+  while (!ll_ok(w, ep)) {
+    __nanosleep(ns);
+    ns = ns < kMaxSleepNs ? 2 * ns : ns;
+    w = ld_ll(p);
   }
+  return w;
 }
+__device__ __forceinline__ uint32_t epoch_of(const CornerDev& c) { return __ldcg(c.epoch); }
 
-// Cell arc u -> w (backward): RAT_L(u,irf) = min(RAT_L(w,orf) - d), RAT_E =
-// max(RAT_E(w,orf) - d) over exactly the pairs the forward pass used, with d
-// recomputed bit-identically (same seg / interp calls) from slew(u), load(w).
-__device__ __forceinline__ void cell_bwd(const float* __restrict__ L, const Q4& at_u, const Q4& sl_u,
-                                         uint32_t info, float ld, const Q4& rat_w, Q4& acc) {
-  const uint32_t sense = info & 7u, tab = info >> 3;
-  const Tab rd0 = tab_rec(L, tab);
-  const Tab rd1 = tab_rec(L, tab + 1);
-  const Seg cd0 = seg(rd0.ax + 24, ld);
-  const Seg cd1 = rd1.ax == rd0.ax ? cd0 : seg(rd1.ax + 24, ld);
-#pragma unroll
-  for (int pass = 0; pass < 1; ++pass) {   // non-unate arcs arrive expanded
-#pragma unroll
-    for (int orf = 0; orf < 2; ++orf) {
-      const int irf = pass ? 1 - primary_irf(sense, orf) : primary_irf(sense, orf);
-      const Tab rd = orf ? rd1 : rd0;
-      const Seg cd = orf ? cd1 : cd0;
-#pragma unroll
-      for (int el = 0; el < 2; ++el) {
-        const float a_in = irf ? at_u.v[el * 2 + 1] : at_u.v[el * 2];
-        const float s_in = irf ? sl_u.v[el * 2 + 1] : sl_u.v[el * 2];
-        if (!fin(a_in)) continue;
-        const float d = fmaxf(0.f, interp(rd, seg(rd.ax, s_in), cd));
-        const float cand = __fsub_rn(rat_w.v[el * 2 + orf], d);
-        if (irf) acc.v[el * 2 + 1] = el == 0 ? fmaxf(acc.v[1], cand) : fminf(acc.v[3], cand);
-        else     acc.v[el * 2] = el == 0 ? fmaxf(acc.v[0], cand) : fminf(acc.v[2], cand);
-      }
-    }
-  }
-}
-
-// Endpoint required-time seeds: PO: RAT_L = T - out_max,
-// RAT_E = -out_min; check: RAT_L = T - setup(slew_L(D), clock slew),
-// RAT_E = hold(slew_E(D), clock slew), only where the data arrival exists.
-// The static part (endpoint record, PO seeds) is loaded before the stage
-// wait; the check-table lookups need the data slew and run after it.
-struct SeedPre {
-  Q4 po;              // PO seeds, or the undefined required time
-  uint32_t chk;       // first check table or kNone
-};
-
-__device__ __forceinline__ SeedPre load_seed(const Topo& t, uint32_t e) {
-  SeedPre p{undef_rat(), kNone};
-  if (e == kNone) return p;
-  const EpRec ep = t.ep[e];
-  p.chk = ep.chk_tab;
-  if (ep.po != kNone) {
-    const float2 omax = t.po_out_max[ep.po], omin = t.po_out_min[ep.po];
-    p.po = Q4{{-omin.x, -omin.y, __fsub_rn(t.period, omax.x), __fsub_rn(t.period, omax.y)}};
-  }
-  return p;
-}
-
-__device__ __forceinline__ void apply_seed_pre(const Topo& t, const float* L, const SeedPre& p, const Q4& at,
-                                               const Q4& sl, Q4& r) {
-  r.v[0] = fmaxf(r.v[0], p.po.v[0]);
-  r.v[1] = fmaxf(r.v[1], p.po.v[1]);
-  r.v[2] = fminf(r.v[2], p.po.v[2]);
-  r.v[3] = fminf(r.v[3], p.po.v[3]);
-  if (p.chk != kNone) {
-#pragma unroll
-    for (int rf = 0; rf < 2; ++rf) {
-      if (fin(at.v[2 + rf]))
-        r.v[2 + rf] = fminf(r.v[2 + rf], __fsub_rn(t.period, lut(L, p.chk + rf, sl.v[2 + rf], t.clock_slew)));
-      if (fin(at.v[rf]))
-        r.v[rf] = fmaxf(r.v[rf], lut(L, p.chk + 2 + rf, sl.v[rf], t.clock_slew));
-    }
-  }
-}
-
-__device__ __forceinline__ void apply_seed(const Topo& t, const CornerDev&, const float* L, uint32_t e,
-                                           const Q4& at, const Q4& sl, Q4& r) {
-  apply_seed_pre(t, L, load_seed(t, e), at, sl, r);
-}
-
-// slack_L = RAT_L - AT_L, slack_E = AT_E - RAT_E, +inf if either is undefined.
-__device__ __forceinline__ Q4 slack_of(const Q4& at, const Q4& r) {
-  Q4 s;
+// forward records completed by an earlier kernel: L2 loads (keep L1 for LUTs)
+__device__ __forceinline__ void load_rec(const CornerDev& c, uint32_t i, Q4& at, Q4& sl) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const bool ok = fin(at.v[q]) && fin(r.v[q]);
-    s.v[q] = ok ? (q < 2 ? __fsub_rn(at.v[q], r.v[q]) : __fsub_rn(r.v[q], at.v[q])) : CUDART_INF_F;
+    const uint4 w = __ldcg(c.rec + 4 * (size_t)i + q);
+    at.v[q] = __uint_as_float(w.x);
+    sl.v[q] = __uint_as_float(w.z);
   }
-  return s;
 }
-
-__device__ __forceinline__ void write_ep(const CornerDev& c, uint32_t e, const Q4& s) {
-  c.ep_ws[e] = make_float2(fminf(s.v[2], s.v[3]), fminf(s.v[0], s.v[1]));
-}
-
-// records written by earlier kernels of this update: L2 loads (keep L1 for LUTs)
-__device__ __forceinline__ void load_rec(const CornerDev& c, uint32_t i, Q4& at, Q4& sl) {
-  at = to_q(__ldcg(c.rec + 2 * (size_t)i));
-  sl = to_q(__ldcg(c.rec + 2 * (size_t)i + 1));
+__device__ __forceinline__ void store_rec(const CornerDev& c, uint32_t i, const Q4& at, const Q4& sl, uint32_t ep) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) st_ll(c.rec + 4 * (size_t)i + q, at.v[q], sl.v[q], ep);
 }
 
 // ordered-int image of a float: monotone for signed-int comparison
@@ -690,114 +599,44 @@ __global__ void __launch_bounds__(kTcThreads, 2) tc_persistent_kernel(Topo t, Co
   }
 }
 
-// ------------------------------------------------------------ a2: forward
-// Stage-0 pull pins (no fan-in): PI arrivals, ideal clock, or undefined.
-__global__ void __launch_bounds__(kThreads) seed_kernel(Topo t, CornerDev c, uint32_t n0) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t s = i < n0 ? t.seed[i] : kNone;
-  pdl_wait();
-  pdl_launch();
-  if (i >= n0) return;
-  float4 at, sl;
-  if (s == kNone) {
-    at = to_f4(undef_at());
-    sl = at;
-  } else if (s == kSeedClock) {              // rising edge at 0, falling at T/2
-    const float h = 0.5f * t.period;
-    at = make_float4(0.f, h, 0.f, h);
-    sl = make_float4(t.clock_slew, t.clock_slew, t.clock_slew, t.clock_slew);
-  } else {
-    at = t.pi_at[s];
-    sl = t.pi_slew[s];
-  }
-  c.rec[2 * (size_t)i] = at;
-  c.rec[2 * (size_t)i + 1] = sl;
-}
+// ------------------------------------------- a2-a5: propagation work units
+// The forward and backward passes are lists of warp work units in
+// dependency order (every unit depends only on units with a smaller index;
+// layouts in sta_internal.h).  Two launchers run the same unit code:
+//   * persistent (default): one cooperative grid of co-resident blocks; warp
+//     w takes units w, w + W, ... in order.  All warps are resident, so the
+//     smallest unfinished unit can always proceed: no deadlock, no barrier.
+//     A unit waits only for the tagged words it reads, so stages overlap
+//     wherever the graph allows, and a producer -> consumer hop is one L2
+//     round trip.
+//   * per stage (STA_STAGE_KERNELS=1): one launch per gate stage (PDL), one
+//     warp per unit; the tags are then always valid on first read.
+constexpr uint32_t kFull = 0xFFFFFFFFu;
 
-// One launch per gate stage s >= 1: each thread merges the cell fan-in of
-// one stage pin.  A fan-in pin that is a net sink is recomputed inline from
-// its driver's record (pull-through), so sinks never cost a stage.
-template <bool SMEM_LUT>
-__global__ void __launch_bounds__(kThreads) fwd_stage_kernel(Topo t, CornerDev c, uint32_t pull0, uint32_t n,
-                                                             uint32_t lut_f4) {
-  const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t v = pull0 + i;
-  uint32_t e0 = 0, e1 = 0, src0 = 0, hop0 = kNone, info0 = 0;
-  if (i < n) {                               // static topology: before the wait
-    e0 = t.fi_ptr[v];
-    e1 = t.fi_ptr[v + 1];
-    if (e1 > e0) { src0 = t.fi_src[e0]; hop0 = t.fi_hop[e0]; info0 = t.fi_info[e0]; }
-  }
-  pdl_wait();
-  pdl_launch();
-  if (i >= n) return;
-  const float ld = __ldcg(c.load + v);
-  Q4 acc_at = undef_at(), acc_sl = undef_at();
-  for (uint32_t e = e0; e < e1; ++e) {
-    uint32_t src = src0, hop = hop0, info = info0;
-    if (e != e0) { src = t.fi_src[e]; hop = t.fi_hop[e]; info = t.fi_info[e]; }
-    Q4 at, sl;
-    load_rec(c, src, at, sl);
-    if (hop != kNone) net_hop(at, sl, __ldcg(c.elm + hop));
-    cell_fwd(L, at, sl, info, ld, acc_at, acc_sl);
-  }
-  c.rec[2 * (size_t)v] = to_f4(acc_at);
-  c.rec[2 * (size_t)v + 1] = to_f4(acc_sl);
-}
-
-// ---------------------------------------------- inter-block dataflow flags
-// Persistent kernels publish completed work with a release store / atomic
-// after a block barrier and a gpu-scope fence.  Consumers poll the flag with
-// relaxed gpu-scope loads and, once it is set, read the produced records with
-// wait until *f >= target (wrap-around safe)
-// Exponential backoff (32 ns .. 1 us): a poller competes for issue slots with
-// the working warps of its SM; without backoff polling was 15% of the
-// forward kernel's instructions.
-// polling backoff cap: a waiter notices a completed stage at most this late
-constexpr uint32_t kMaxSleepNs = 128;
-
-__device__ __forceinline__ void wait_ge(const uint32_t* f, uint32_t target) {
-  if ((int)(ld_acquire(f) - target) >= 0) return;
-  uint32_t ns = 32;
-  while ((int)(ld_acquire(f) - target) < 0) {
-    __nanosleep(ns);
-    ns = ns < kMaxSleepNs ? 2 * ns : ns;
+// STA_TRACE: {start, inputs' producers seen (probe), inputs loaded, end} of a unit
+__device__ __forceinline__ void trace_unit(const CornerDev& c, size_t q, unsigned long long t0,
+                                           unsigned long long t1, unsigned long long t2 = 0) {
+  if (c.trace && (threadIdx.x & 31) == 0) {
+    c.trace[4 * q] = t0;
+    c.trace[4 * q + 1] = t1;
+    c.trace[4 * q + 2] = t2 ? t2 : t1;
+    c.trace[4 * q + 3] = gtimer();
   }
 }
-// backward: every unit of the stage of pull pin w is complete
-template <bool WAIT>
-__device__ __forceinline__ void wait_pull(const Topo& t, const CornerDev& c, uint32_t w) {
-  if (!WAIT) return;
-  const uint32_t s = __ldg(t.chunk_stage + w / kChunk);
-  wait_ge(c.bwd_done + s, __ldg(t.stage_units + s));
-}
 
-// ------------------------------------------------------ a3-a5: backward
-// Finish a pull pin: own seed, direct cell fan-out, then rat / slack.
-// e = pin_ep[v], [p0, p1) = its direct fan-out (prefetched by the caller).
-template <bool WAIT>
-__device__ __forceinline__ void finish_pull_pre(const Topo& t, const CornerDev& c, const float* L, uint32_t v,
-                                                uint32_t e, uint32_t p0, uint32_t p1, const Q4& at, const Q4& sl,
-                                                Q4 acc) {
-  if (e != kNone) apply_seed(t, c, L, e, at, sl, acc);
-  for (uint32_t x = p0; x < p1; ++x) {
-    const uint32_t w = t.pfo_dst[x];
-    wait_pull<WAIT>(t, c, w);
-    cell_bwd(L, at, sl, t.pfo_info[x], __ldcg(c.load + w), to_q(__ldcg(c.rat + w)), acc);
+// undefined-safe slack: slack_L = RAT_L - AT_L, slack_E = AT_E - RAT_E, +inf
+// if either side is undefined
+__device__ __forceinline__ Q4 slack_of(const Q4& at, const Q4& r) {
+  Q4 s;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const bool ok = fin(at.v[q]) && fin(r.v[q]);
+    s.v[q] = ok ? (q < 2 ? __fsub_rn(at.v[q], r.v[q]) : __fsub_rn(r.v[q], at.v[q])) : CUDART_INF_F;
   }
-  c.rat[v] = to_f4(acc);
-  const Q4 s = slack_of(at, acc);
-  c.slack[v] = to_f4(s);
-  if (e != kNone) write_ep(c, e, s);
+  return s;
 }
 
-template <bool WAIT>
-__device__ __forceinline__ void finish_pull(const Topo& t, const CornerDev& c, const float* L, uint32_t v,
-                                            const Q4& at, const Q4& sl, Q4 acc) {
-  finish_pull_pre<WAIT>(t, c, L, v, t.pin_ep[v], t.pfo_ptr[v], t.pfo_ptr[v + 1], at, sl, acc);
-}
-
+// required-time merge: early components take the max, late the min
 __device__ __forceinline__ void combine(Q4& a, const Q4& b) {
   a.v[0] = fmaxf(a.v[0], b.v[0]);
   a.v[1] = fmaxf(a.v[1], b.v[1]);
@@ -805,424 +644,450 @@ __device__ __forceinline__ void combine(Q4& a, const Q4& b) {
   a.v[3] = fminf(a.v[3], b.v[3]);
 }
 
-// Static part of a backward tile lane (topology and RC results: readable
-// before the previous stage ends), so that after the wait only the
-// producers' records (driver AT/slew, fan-out RATs) remain to be loaded.
-struct TileLane {
-  uint2 td;
-  uint32_t k, v, e, f0, f1, w0, info0, pe, p0, p1;
-  float el, ld0;
-  bool active;
-  SeedPre seed;       // the sink's endpoint seed (static part)
-};
+// ---- forward: four lanes per fan-in term, lane = (term slot tl = lane / 4,
+// output component q = lane % 4 = (el, orf)).  A unit is a run of pins of
+// one stage with <= kFwdTerms terms (a pin is never split; a pin with more
+// terms is a unit of its own, looped over by the warp).  A lane reads the
+// one tagged record word its candidate needs -- (el, irf) of the source, irf
+// by the term's sense -- spinning on its tags, applies the net hop of a sink
+// input, looks up delay[orf] and slew[orf] (bit-identical to the backward's
+// recomputation: same seg / interp calls on the same operands), and the first
+// term of each pin merges its pin's candidates by shuffles and writes word q
+// of the pin's record.  Before the lanes load, one probe lane (the plan's
+// choice: the term whose source was produced last) polls alone with backoff,
+// so warps running ahead of the wavefront cost one L2 sector per poll.
+// (Four lanes per term keep the per-lane dependent chain short: the forward
+// wavefront's stage-to-stage latency is that chain.)
+constexpr uint32_t kFwdTerms = kFwdUnitTerms;
 
-__device__ __forceinline__ TileLane tile_lane(const Topo& t, uint32_t tile, uint32_t k1) {
-  TileLane x;
-  x.td = t.tiles[tile];
-  x.k = x.td.x + (threadIdx.x & 31);
-  x.active = x.k < k1;
-  x.v = kNone; x.e = kNone; x.f0 = 0; x.f1 = 0; x.w0 = 0; x.info0 = 0; x.pe = kNone; x.p0 = 0; x.p1 = 0;
-  x.el = 0.f; x.ld0 = 0.f;
-  x.seed = SeedPre{undef_rat(), kNone};
-  if (x.active) {
-    x.v = t.sink_drv[x.k];
-    x.e = t.pin_ep[t.NP + x.k];
-    x.f0 = t.sfo_ptr[x.k];
-    x.f1 = t.sfo_ptr[x.k + 1];
-    x.pe = t.pin_ep[x.v];
-    x.p0 = t.pfo_ptr[x.v];
-    x.p1 = t.pfo_ptr[x.v + 1];
-    x.seed = load_seed(t, x.e);
-    if (x.f1 > x.f0) {
-      x.w0 = t.sfo_dst[x.f0];
-      x.info0 = t.sfo_info[x.f0];
-    }
-  }
-  return x;
+__device__ __forceinline__ void fwd_lane(const float* __restrict__ L, uint32_t info, int el, int orf, float ld,
+                                         float a_in, float s_in, float& ca, float& cs) {
+  const uint32_t tab = info >> 3;
+  const Tab rd = tab_rec(L, tab + orf);          // cell_rise / cell_fall
+  const Tab rs = tab_rec(L, tab + 2 + orf);      // rise / fall transition
+  const bool same = rs.ax == rd.ax;
+  const Seg cd = seg(rd.ax + 24, ld);
+  const Seg cc = same ? cd : seg(rs.ax + 24, ld);
+  const Seg sd = seg(rd.ax, s_in);
+  const Seg ss = same ? sd : seg(rs.ax, s_in);
+  const float d = fmaxf(0.f, interp(rd, sd, cd));
+  const float so = fmaxf(0.f, interp(rs, ss, cc));
+  const bool ok = fin(a_in);
+  const float undef = el ? -CUDART_INF_F : CUDART_INF_F;
+  ca = ok ? __fadd_rn(a_in, d) : undef;
+  cs = ok ? so : undef;
 }
 
-// RC results of a tile lane (written by the RC kernels of this update)
-__device__ __forceinline__ void tile_lane_rc(const CornerDev& c, TileLane& x) {
-  if (!x.active) return;
-  x.el = __ldcg(c.elm + x.k);
-  if (x.f1 > x.f0) x.ld0 = __ldcg(c.load + x.w0);
+__device__ __forceinline__ void merge_q(float& a, float b, int el) { a = el ? fmaxf(a, b) : fminf(a, b); }
+
+// net hop driver -> sink of one component (net_hop): AT + elm, PERI slew
+__device__ __forceinline__ void hop_q(float& a_in, float& s_in, float elm) {
+  if (!fin(a_in)) return;
+  const float imp = __fmul_rn(kLn9, elm);
+  a_in = __fadd_rn(a_in, elm);
+  s_in = __fsqrt_rn(__fmaf_rn(s_in, s_in, __fmul_rn(imp, imp)));
 }
 
-// One warp, one tile of <= 32 consecutive sinks of one stage's drivers: each
-// lane owns one sink (required time from its endpoint seed and its cell
-// fan-out, then rat / slack), and a segmented shuffle reduction by driver
-// produces the drivers' required times.  Drivers with more than 32 sinks
-// (heavy slot) combine their tiles with ordered-int atomics; the last tile
-// finishes them.
-template <bool WAIT>
-__device__ __forceinline__ void process_tile(const Topo& t, const CornerDev& c, const float* L, const TileLane& x) {
-  const int lane = threadIdx.x & 31;
-  Q4 at_v = undef_at(), sl_v = undef_at(), acc = undef_rat();
-  if (x.active) {
-    Q4 rw0 = undef_rat();
-    if (x.f1 > x.f0) {
-      wait_pull<WAIT>(t, c, x.w0);
-      rw0 = to_q(__ldcg(c.rat + x.w0));
+// forward unit u; tr = this lane's term slot of the unit
+__device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, const float* __restrict__ L,
+                                         uint32_t ep, uint32_t u, const uint4& tr) {
+  const uint32_t lane = threadIdx.x & 31, tl = lane >> 2, q = lane & 3;
+  const int el = (int)(q >> 1), orf = (int)(q & 1);
+  const float undef = el ? -CUDART_INF_F : CUDART_INF_F;
+  unsigned long long t_start = 0, t_ready = 0, t_data = 0;
+  if (c.trace && lane == 0) t_start = gtimer();
+  const uint32_t kind = __shfl_sync(kFull, tr.x, 0);
+  if (kind == kSeedMark) {                   // seeds: lane = (pin, q)
+    if (tr.w != kNone) {
+      const uint32_t v = tr.w;
+      const uint32_t s = t.seed[v];
+      float a = undef, sl = undef;
+      if (s == kSeedClock) {                 // rising edge at 0, falling at T/2
+        a = orf ? 0.5f * t.period : 0.f;
+        sl = t.clock_slew;
+      } else if (s != kNone) {
+        a = reinterpret_cast<const float*>(t.pi_at + s)[q];
+        sl = reinterpret_cast<const float*>(t.pi_slew + s)[q];
+      }
+      st_ll(c.rec + 4 * (size_t)v + q, a, sl, ep);
     }
-    load_rec(c, x.v, at_v, sl_v);
-    Q4 at = at_v, sl = sl_v;
-    net_hop(at, sl, x.el);                  // the sink's own arrival / slew
-    Q4 r = undef_rat();
-    if (x.e != kNone) apply_seed_pre(t, L, x.seed, at, sl, r);
-    if (x.f1 > x.f0) cell_bwd(L, at, sl, x.info0, x.ld0, rw0, r);
-    for (uint32_t f = x.f0 + 1; f < x.f1; ++f) {
-      const uint32_t w = t.sfo_dst[f];
-      wait_pull<WAIT>(t, c, w);
-      cell_bwd(L, at, sl, t.sfo_info[f], __ldcg(c.load + w), to_q(__ldcg(c.rat + w)), r);
-    }
-    const size_t u = (size_t)t.NP + x.k;
-    c.rat[u] = to_f4(r);
-    const Q4 s = slack_of(at, r);
-    c.slack[u] = to_f4(s);
-    if (x.e != kNone) write_ep(c, x.e, s);
-    // candidate of the driver through the net arc (only edges the forward used)
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (fin(at_v.v[q])) acc.v[q] = __fsub_rn(r.v[q], x.el);
-  }
-  // segmented inclusive scan by driver (drivers are contiguous in the tile)
-  const uint32_t v = x.v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t vo = __shfl_up_sync(0xFFFFFFFFu, v, o);
-    Q4 b;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) b.v[q] = __shfl_up_sync(0xFFFFFFFFu, acc.v[q], o);
-    if (lane >= o && vo == v) combine(acc, b);
-  }
-  const uint32_t vn = __shfl_down_sync(0xFFFFFFFFu, v, 1);
-  const bool tail = x.active && (lane == 31 || vn != v);
-  if (!tail) return;
-  if (x.td.y == kNone) {                    // light driver: complete in this tile
-    finish_pull_pre<WAIT>(t, c, L, v, x.pe, x.p0, x.p1, at_v, sl_v, acc);
+    trace_unit(c, u, t_start, t_start);
     return;
   }
-  const uint32_t slot = x.td.y;
-  int* key = reinterpret_cast<int*>(c.heavy_key + slot);
-  atomicMax(key + 0, f2o(acc.v[0]));
-  atomicMax(key + 1, f2o(acc.v[1]));
-  atomicMin(key + 2, f2o(acc.v[2]));
-  atomicMin(key + 3, f2o(acc.v[3]));
-  // release counter: orders this tile's key updates before it; only the last
-  // tile pays the acquire fence before reading everyone's keys
-  uint32_t done;
-  asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(done) : "l"(c.heavy_cnt + slot) : "memory");
-  if (done + 1 != t.heavy_nchunk[slot]) return;
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
-  Q4 a;
-  a.v[0] = o2f(atomicExch(key + 0, f2o(-CUDART_INF_F)));
-  a.v[1] = o2f(atomicExch(key + 1, f2o(-CUDART_INF_F)));
-  a.v[2] = o2f(atomicExch(key + 2, f2o(CUDART_INF_F)));
-  a.v[3] = o2f(atomicExch(key + 3, f2o(CUDART_INF_F)));
-  c.heavy_cnt[slot] = 0;                    // self-reset for the next update
-  finish_pull_pre<WAIT>(t, c, L, v, x.pe, x.p0, x.p1, at_v, sl_v, a);
+  if (kind != kHeavyMark) {
+    const bool item = tr.x != kNone;
+    const uint32_t src = tr.x, info = tr.z & 0x7FFFFFFFu, v = tr.w;
+    float elm = 0.f, ld = 0.f;
+    if (item) {                              // RC results of this update
+      if (tr.y != kNone) elm = __ldcg(c.elm + tr.y);
+      ld = __ldcg(c.load + v);
+    }
+    const int irf = primary_irf(info & 7u, orf);
+    const uint4* wp = c.rec + 4 * (size_t)src + (el * 2 + irf);
+    if ((tr.z >> 31) && q == 3) spin_ll(wp, ep);   // probe
+    __syncwarp();
+    if (c.trace && lane == 0) t_ready = gtimer();
+    float ca = undef, cs = undef;
+    if (item) {
+      const uint4 w = spin_ll(wp, ep);
+      if (c.trace) t_data = gtimer();
+      float a_in = __uint_as_float(w.x), s_in = __uint_as_float(w.z);
+      if (tr.y != kNone) hop_q(a_in, s_in, elm);
+      fwd_lane(L, info, el, orf, ld, a_in, s_in, ca, cs);
+    }
+    // merge the pin's terms into its first term's lanes (same q); a pin's
+    // terms occupy consecutive slots
+    const uint32_t peers = __match_any_sync(kFull, item ? v : kNone);
+    const uint32_t head_tl = (uint32_t)(__ffs(peers) - 1) >> 2, end_tl = (uint32_t)(31 - __clz(peers)) >> 2;
+#pragma unroll
+    for (uint32_t j = 1; j < kFwdTerms; ++j) {
+      const float oa = __shfl_down_sync(kFull, ca, 4 * j);
+      const float os = __shfl_down_sync(kFull, cs, 4 * j);
+      if (tl + j <= end_tl) {
+        merge_q(ca, oa, el);
+        merge_q(cs, os, el);
+      }
+    }
+    if (item && tl == head_tl) st_ll(c.rec + 4 * (size_t)v + q, ca, cs, ep);
+  } else {                                   // one pin with > kFwdTerms terms: warp loop
+    const uint32_t v = tr.w, e0 = tr.y, nterms = tr.z;
+    const float ld = __ldcg(c.load + v);
+    float ca = undef, cs = undef;
+    for (uint32_t b = tl; b < nterms; b += kFwdTerms) {
+      const uint32_t e = e0 + b;
+      const uint32_t info = t.fi_info[e], h = t.fi_hop[e];
+      const int irf = primary_irf(info & 7u, orf);
+      const uint4 w = spin_ll(c.rec + 4 * (size_t)t.fi_src[e] + (el * 2 + irf), ep);
+      float a_in = __uint_as_float(w.x), s_in = __uint_as_float(w.z);
+      if (h != kNone) hop_q(a_in, s_in, __ldcg(c.elm + h));
+      float oa, os;
+      fwd_lane(L, info, el, orf, ld, a_in, s_in, oa, os);
+      merge_q(ca, oa, el);
+      merge_q(cs, os, el);
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      merge_q(ca, __shfl_xor_sync(kFull, ca, o), el);
+      merge_q(cs, __shfl_xor_sync(kFull, cs, o), el);
+    }
+    if (tl == 0) st_ll(c.rec + 4 * (size_t)v + q, ca, cs, ep);
+    t_ready = t_start;
+  }
+  if (c.trace) {                             // latest lane's data arrival
+    const uint32_t lo = (uint32_t)t_data, hi = (uint32_t)(t_data >> 32);
+    const uint32_t mh = __reduce_max_sync(kFull, hi);
+    const uint32_t ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
+    t_data = ((unsigned long long)mh << 32) | ml;
+  }
+  trace_unit(c, u, t_start, t_ready, t_data);
 }
 
-// One launch per gate stage (descending).  Blocks [0, nTileBlocks): one warp
-// per tile.  Remaining blocks: stage pins without sinks, one thread each.
 template <bool SMEM_LUT>
-__global__ void __launch_bounds__(kThreads) bwd_stage_kernel(Topo t, CornerDev c, uint32_t tile0, uint32_t nTiles,
-                                                             uint32_t sinkEnd, uint32_t nos0, uint32_t nNos,
-                                                             uint32_t nTileBlocks, uint32_t lut_f4) {
+__global__ void __launch_bounds__(kThreads, kFwdMinBlocks) fwd_persistent_kernel(Topo t, CornerDev c,
+                                                                                   uint32_t lut_f4) {
   const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
-  if (blockIdx.x >= nTileBlocks) {
-    const uint32_t i = (blockIdx.x - nTileBlocks) * blockDim.x + threadIdx.x;
-    const uint32_t v = i < nNos ? t.nosink[nos0 + i] : 0;
-    pdl_wait();
-    pdl_launch();
-    if (i >= nNos) return;
-    Q4 at, sl;
-    load_rec(c, v, at, sl);
-    finish_pull<false>(t, c, L, v, at, sl, undef_rat());
-    return;
+  const uint32_t ep = epoch_of(c);
+  const uint32_t tl = (threadIdx.x & 31) >> 2;
+  const uint32_t W = gridDim.x * (kThreads / 32);
+  uint32_t u = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  uint4 nx = u < t.n_fwu ? __ldg(t.fterm + (size_t)kFwdTerms * u + tl) : make_uint4(0, 0, 0, 0);
+  for (; u < t.n_fwu; u += W) {
+    const uint4 tr = nx;
+    if (u + W < t.n_fwu) nx = __ldg(t.fterm + (size_t)kFwdTerms * (u + W) + tl);   // prefetch the next unit
+    fwd_unit(t, c, L, ep, u, tr);
   }
-  const uint32_t tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  TileLane x{};
-  if (tile < nTiles) x = tile_lane(t, tile0 + tile, tile + 1 < nTiles ? t.tiles[tile0 + tile + 1].x : sinkEnd);
+}
+
+// units [u0, u1) of one gate stage, one warp each
+template <bool SMEM_LUT>
+__global__ void __launch_bounds__(kThreads) fwd_stage_kernel(Topo t, CornerDev c, uint32_t u0, uint32_t u1,
+                                                             uint32_t lut_f4) {
+  const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
+  const uint32_t u = u0 + blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  const uint4 tr = u < u1 ? __ldg(t.fterm + (size_t)kFwdTerms * u + ((threadIdx.x & 31) >> 2)) : make_uint4(0, 0, 0, 0);
   pdl_wait();
   pdl_launch();
-  if (tile >= nTiles) return;
-  tile_lane_rc(c, x);
-  process_tile<false>(t, c, L, x);
+  if (u >= u1) return;
+  fwd_unit(t, c, L, epoch_of(c), u, tr);
 }
 
-// ---------------------------------------------- persistent dataflow passes
-// Grid = co-resident blocks (cooperative launch).  Work items are processed in
-// dependency order (block b takes items b, b + G, ...), every item depends
-// only on items with a smaller index, and all blocks are resident, so the
-// smallest unfinished item can always proceed: no deadlock, no grid barrier.
-
-
-// Block-level readiness.  Each block is a worker; its warp 0 checks the
-// per-stage completion counters of the stages a unit depends on, 32 stages
-// per L2 round trip (one per lane), with a per-block watermark of stages
-// already seen complete; the block continues after a barrier.  A finished
-// unit publishes with a barrier and one red.release.gpu (orders the block's
-// stores through MEMBAR.ALL.GPU without the L1 invalidation a fence.acq_rel /
-// __threadfence adds).  Per-warp units (one release per 32 items) and
-// per-thread polling both measured 1.7-2x slower on C3.
-__device__ __forceinline__ void block_wait_fwd(const Topo& t, const CornerDev& c, uint32_t stage, uint32_t* s_wm) {
-  if (threadIdx.x < 32) {
-    const uint32_t lane = threadIdx.x;
-    uint32_t wm = *s_wm, ns = 32;
-    while (wm < stage) {                     // every stage < stage must be complete
-      const uint32_t q = wm + lane;
-      const bool ok = q >= stage || (int)(ld_acquire(c.fwd_done + q) - __ldg(t.stage_chunks + q)) >= 0;
-      const uint32_t miss = __ballot_sync(0xFFFFFFFFu, !ok);
-      if (!miss) {
-        wm = min(stage, wm + 32);
-      } else {
-        wm += __ffs(miss) - 1;
-        __nanosleep(ns);
-        ns = ns < kMaxSleepNs ? 2 * ns : ns;
-      }
-    }
-    if (lane == 0) *s_wm = wm;
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ void block_wait_bwd(const Topo& t, const CornerDev& c, uint32_t stage, uint32_t* s_wm) {
-  if (threadIdx.x < 32) {
-    const uint32_t lane = threadIdx.x;
-    uint32_t wm = *s_wm, ns = 32;
-    while (wm > stage + 1) {                 // every stage > stage must be complete
-      const int q = (int)wm - 1 - (int)lane;
-      const bool ok = q <= (int)stage || (int)(ld_acquire(c.bwd_done + q) - __ldg(t.stage_units + q)) >= 0;
-      const uint32_t miss = __ballot_sync(0xFFFFFFFFu, !ok);
-      if (!miss) {
-        wm = max(stage + 1, wm > 32 ? wm - 32 : 0u);
-      } else {
-        wm -= __ffs(miss) - 1;
-        __nanosleep(ns);
-        ns = ns < kMaxSleepNs ? 2 * ns : ns;
-      }
-    }
-    if (lane == 0) *s_wm = wm;
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ void block_publish(uint32_t* ctr) {
-  __syncthreads();
-  if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
-}
-
-// forward merge: early components take the min, late the max
-__device__ __forceinline__ void merge_fwd(Q4& a, const Q4& b) {
-  a.v[0] = fminf(a.v[0], b.v[0]);
-  a.v[1] = fminf(a.v[1], b.v[1]);
-  a.v[2] = fmaxf(a.v[2], b.v[2]);
-  a.v[3] = fmaxf(a.v[3], b.v[3]);
-}
-
-// One fan-in term of the forward pass, both modes: the candidates of the
-// term's cell arc for every (el, orf), merged into acc_at / acc_sl (early
-// min, late max).  Same seg / interp calls as cell_fwd / cell_bwd
-// (bit-identical); branch-free: lookups of undefined inputs are computed and
-// discarded by select, so a warp never diverges on them.
-__device__ __forceinline__ void cell_term(const float* __restrict__ L, const Q4& at, const Q4& sl, uint32_t info,
-                                          float ld, Q4& acc_at, Q4& acc_sl) {
+// ---- backward: one lane per sink / pin (all four components in the lane)
+// Cell arc u -> w, backward: RAT(u, el, irf) combines
+// RAT(w, el, orf) - d(el, irf -> orf) over the output edges orf whose input
+// edge irf (by the sense) has a defined arrival -- exactly the pairs the
+// forward used; late min, early max.  we / wl: w's tagged required-time words
+// (early, late).  d is recomputed with cell_term's seg / interp calls on the
+// same operands: bit-identical.
+__device__ __forceinline__ void bwd_arc(const float* __restrict__ L, const Q4& a, const Q4& s, uint32_t info,
+                                        float ld, const uint4& we, const uint4& wl, Q4& r) {
   const uint32_t sense = info & 7u, tab = info >> 3;
   const Tab rd0 = tab_rec(L, tab), rd1 = tab_rec(L, tab + 1);
-  const Tab rs0 = tab_rec(L, tab + 2), rs1 = tab_rec(L, tab + 3);
   const Seg cd0 = seg(rd0.ax + 24, ld);
   const Seg cd1 = rd1.ax == rd0.ax ? cd0 : seg(rd1.ax + 24, ld);
-  const Seg cs0 = rs0.ax == rd0.ax ? cd0 : seg(rs0.ax + 24, ld);
-  const Seg cs1 = rs1.ax == rd1.ax ? cd1 : seg(rs1.ax + 24, ld);
 #pragma unroll
   for (int orf = 0; orf < 2; ++orf) {
     const int irf = primary_irf(sense, orf);
     const Tab rd = orf ? rd1 : rd0;
-    const Tab rs = orf ? rs1 : rs0;
-    const bool same = rs.ax == rd.ax;
 #pragma unroll
     for (int el = 0; el < 2; ++el) {
-      const float a_in = irf ? at.v[el * 2 + 1] : at.v[el * 2];
-      const float s_in = irf ? sl.v[el * 2 + 1] : sl.v[el * 2];
-      const Seg sd = seg(rd.ax, s_in);
-      const Seg ss = same ? sd : seg(rs.ax, s_in);
-      const float d = fmaxf(0.f, interp(rd, sd, orf ? cd1 : cd0));
-      const float so = fmaxf(0.f, interp(rs, ss, orf ? cs1 : cs0));
-      const float ca = __fadd_rn(a_in, d);
-      const bool ok = fin(a_in);
-      const int q = el * 2 + orf;
-      if (el == 0) {
-        acc_at.v[q] = ok ? fminf(acc_at.v[q], ca) : acc_at.v[q];
-        acc_sl.v[q] = ok ? fminf(acc_sl.v[q], so) : acc_sl.v[q];
-      } else {
-        acc_at.v[q] = ok ? fmaxf(acc_at.v[q], ca) : acc_at.v[q];
-        acc_sl.v[q] = ok ? fmaxf(acc_sl.v[q], so) : acc_sl.v[q];
-      }
+      // (selects, not dynamic register-array indices: those go to local memory)
+      const float s_in = irf ? s.v[el * 2 + 1] : s.v[el * 2];
+      const bool ok = fin(irf ? a.v[el * 2 + 1] : a.v[el * 2]);
+      const float d = fmaxf(0.f, interp(rd, seg(rd.ax, s_in), orf ? cd1 : cd0));
+      const uint4& w = el ? wl : we;
+      const float cand = __fsub_rn(__uint_as_float(orf ? w.z : w.x), d);
+      float& r0 = r.v[el * 2];
+      float& r1 = r.v[el * 2 + 1];
+      const float m0 = el ? fminf(r0, cand) : fmaxf(r0, cand);
+      const float m1 = el ? fminf(r1, cand) : fmaxf(r1, cand);
+      r0 = ok && irf == 0 ? m0 : r0;
+      r1 = ok && irf == 1 ? m1 : r1;
     }
   }
 }
 
-// Forward pass.  A chunk is a run of pins of one stage whose fan-in terms fit
-// the block: phase 1 evaluates one term per thread (one cell arc, both
-// modes), phase 2 merges each pin's terms from shared memory.  This keeps
-// the per-thread dependent chain to one arc.  A pin with more than 256 terms
-// has a chunk of its own and its terms are looped over.
-template <bool SMEM_LUT>
-__global__ void __launch_bounds__(kThreads, 4) fwd_persistent_kernel(Topo t, CornerDev c, uint32_t lut_f4) {
-  __shared__ uint32_t s_wm;
-  __shared__ float4 s_at[kThreads], s_sl[kThreads];
-  const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
-  if (threadIdx.x == 0) s_wm = 0;
-  for (uint32_t ch = blockIdx.x; ch < t.n_fchunks; ch += gridDim.x) {
-    unsigned long long t_start = 0, t_ready = 0;
-    if (c.trace && threadIdx.x == 0) t_start = gtimer();
-    const uint4 fc = t.fchunks[ch];          // {pin0, npins, term0, nterms}
-    const uint32_t stage = t.fchunk_stage[ch];
-    if (stage == 0) {                        // seeds: PI arrivals, ideal clock, undefined
-      if (threadIdx.x < fc.y) {
-        const uint32_t v = fc.x + threadIdx.x;
-        const uint32_t s = t.seed[v];
-        Q4 at = undef_at(), sl = undef_at();
-        if (s == kSeedClock) {
-          const float h = 0.5f * t.period;
-          at = Q4{{0.f, h, 0.f, h}};
-          sl = Q4{{t.clock_slew, t.clock_slew, t.clock_slew, t.clock_slew}};
-        } else if (s != kNone) {
-          at = to_q(t.pi_at[s]);
-          sl = to_q(t.pi_slew[s]);
-        }
-        c.rec[2 * (size_t)v] = to_f4(at);
-        c.rec[2 * (size_t)v + 1] = to_f4(sl);
-      }
-      block_publish(c.fwd_done);
-      continue;
-    }
-    if (fc.w <= kThreads) {
-      // static topology and RC results before waiting for the producers
-      const bool item = threadIdx.x < fc.w;
-      uint32_t src = 0, info = 0;
-      float elm = 0.f, ld = 0.f;
-      bool hop = false;
-      if (item) {
-        const uint32_t e = fc.z + threadIdx.x;
-        src = t.fi_src[e];
-        info = t.fi_info[e];
-        const uint32_t h = t.fi_hop[e];
-        hop = h != kNone;
-        if (hop) elm = __ldcg(c.elm + h);
-        ld = __ldcg(c.load + t.fi_pin[e]);
-      }
-      uint32_t pv = 0, i0 = 0, i1 = 0;
-      if (threadIdx.x < fc.y) {
-        pv = fc.x + threadIdx.x;
-        i0 = t.fi_ptr[pv] - fc.z;
-        i1 = t.fi_ptr[pv + 1] - fc.z;
-      }
-      block_wait_fwd(t, c, stage, &s_wm);
-      if (c.trace && threadIdx.x == 0) t_ready = gtimer();
-      if (item) {
-        Q4 at, sl;
-        load_rec(c, src, at, sl);
-        if (hop) net_hop(at, sl, elm);
-        Q4 acc_at = undef_at(), acc_sl = undef_at();
-        cell_term(L, at, sl, info, ld, acc_at, acc_sl);
-        s_at[threadIdx.x] = to_f4(acc_at);
-        s_sl[threadIdx.x] = to_f4(acc_sl);
-      }
-      __syncthreads();
-      if (threadIdx.x < fc.y) {
-        Q4 acc_at = undef_at(), acc_sl = undef_at();
-        for (uint32_t i = i0; i < i1; ++i) {
-          merge_fwd(acc_at, to_q(s_at[i]));
-          merge_fwd(acc_sl, to_q(s_sl[i]));
-        }
-        if (i1 > i0) {                       // padding pins (no terms) are never read
-          c.rec[2 * (size_t)pv] = to_f4(acc_at);
-          c.rec[2 * (size_t)pv + 1] = to_f4(acc_sl);
-        }
-      }
-    } else {                                 // one pin with > 256 terms: block loop
-      block_wait_fwd(t, c, stage, &s_wm);
-      if (c.trace && threadIdx.x == 0) t_ready = gtimer();
-      const float ld = __ldcg(c.load + fc.x);
-      Q4 acc_at = undef_at(), acc_sl = undef_at();
-      for (uint32_t e = fc.z + threadIdx.x; e < fc.z + fc.w; e += blockDim.x) {
-        const uint32_t h = t.fi_hop[e];
-        Q4 at, sl;
-        load_rec(c, t.fi_src[e], at, sl);
-        if (h != kNone) net_hop(at, sl, __ldcg(c.elm + h));
-        cell_term(L, at, sl, t.fi_info[e], ld, acc_at, acc_sl);
-      }
-      s_at[threadIdx.x] = to_f4(acc_at);
-      s_sl[threadIdx.x] = to_f4(acc_sl);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        for (uint32_t i = 1; i < blockDim.x; ++i) {
-          merge_fwd(acc_at, to_q(s_at[i]));
-          merge_fwd(acc_sl, to_q(s_sl[i]));
-        }
-        c.rec[2 * (size_t)fc.x] = to_f4(acc_at);
-        c.rec[2 * (size_t)fc.x + 1] = to_f4(acc_sl);
-      }
-    }
-    if (c.trace) {                           // debug: time when the whole block computed
-      __syncthreads();
-      if (threadIdx.x == 0) t_start = gtimer();
-    }
-    block_publish(c.fwd_done + stage);
-    if (c.trace && threadIdx.x == 0) {
-      c.trace[3 * (size_t)ch] = t_start;
-      c.trace[3 * (size_t)ch + 1] = t_ready;
-      c.trace[3 * (size_t)ch + 2] = gtimer();
+// does the arc use some defined input component (otherwise nothing to wait for)
+__device__ __forceinline__ bool arc_live(uint32_t info, const Q4& a) {
+  const uint32_t sense = info & 7u;
+  const bool r_used = primary_irf(sense, 0) == 0 || primary_irf(sense, 1) == 0;
+  const bool f_used = primary_irf(sense, 0) == 1 || primary_irf(sense, 1) == 1;
+  return (r_used && (fin(a.v[0]) || fin(a.v[2]))) || (f_used && (fin(a.v[1]) || fin(a.v[3])));
+}
+
+// Endpoint seeds: PO: RAT_L = T - out_max, RAT_E =
+// -out_min (po_seed, precomputed in fp32); check: RAT_L = T - setup(slew_L(D),
+// clock slew), RAT_E = hold(slew_E(D), clock slew), only where the arrival
+// exists.  chk / po: from the pin's fan-out record.
+__device__ __forceinline__ void seed4(const Topo& t, const float* __restrict__ L, uint32_t chk, uint32_t po,
+                                      const Q4& a, const Q4& s, Q4& r) {
+  if (po != kNone) {
+    const float4 ps = __ldg(t.po_seed + po);
+    r.v[0] = fmaxf(r.v[0], ps.x);
+    r.v[1] = fmaxf(r.v[1], ps.y);
+    r.v[2] = fminf(r.v[2], ps.z);
+    r.v[3] = fminf(r.v[3], ps.w);
+  }
+  if (chk != kNone) {
+#pragma unroll
+    for (int rf = 0; rf < 2; ++rf) {
+      if (fin(a.v[2 + rf]))
+        r.v[2 + rf] = fminf(r.v[2 + rf], __fsub_rn(t.period, lut(L, chk + rf, s.v[2 + rf], t.clock_slew)));
+      if (fin(a.v[rf])) r.v[rf] = fmaxf(r.v[rf], lut(L, chk + 2 + rf, s.v[rf], t.clock_slew));
     }
   }
 }
 
-// Backward pass.  A unit is up to 8 tiles (one warp each, process_tile) or
-// up to 256 sink-less pins of one stage (one thread each).
-template <bool SMEM_LUT>
-__global__ void __launch_bounds__(kThreads, 4) bwd_persistent_kernel(Topo t, CornerDev c, uint32_t lut_f4) {
-  __shared__ uint32_t s_wm;
-  const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
-  if (threadIdx.x == 0) s_wm = t.S;
-  for (uint32_t u = blockIdx.x; u < t.n_units; u += gridDim.x) {
-    unsigned long long t_start = 0, t_ready = 0;
-    if (c.trace && threadIdx.x == 0) t_start = gtimer();
-    const uint4 ud = t.units[u];             // {stage, kind, first, count}
-    const uint32_t w = threadIdx.x >> 5;
-    TileLane x{};
-    uint32_t v = 0, pe = kNone, p0 = 0, p1 = 0;
-    if (ud.y == 0) {                         // static part before waiting
-      if (w < ud.w) {
-        const uint32_t tile = ud.z + w;
-        const uint32_t k1 = tile + 1 < t.stage_tile_end[ud.x] ? t.tiles[tile + 1].x : t.stage_sink_end[ud.x];
-        x = tile_lane(t, tile, k1);
-        tile_lane_rc(c, x);
-      }
-    } else if (threadIdx.x < ud.w) {
-      v = t.nosink[ud.z + threadIdx.x];
-      pe = t.pin_ep[v];
-      p0 = t.pfo_ptr[v];
-      p1 = t.pfo_ptr[v + 1];
-    }
-    block_wait_bwd(t, c, ud.x, &s_wm);
-    if (c.trace && threadIdx.x == 0) t_ready = gtimer();
-    if (ud.y == 0) {
-      if (w < ud.w) process_tile<false>(t, c, L, x);
-    } else if (threadIdx.x < ud.w) {
-      Q4 at, sl;
-      load_rec(c, v, at, sl);
-      finish_pull_pre<false>(t, c, L, v, pe, p0, p1, at, sl, undef_rat());
-    }
-    block_publish(c.bwd_done + ud.x);
-    if (c.trace && threadIdx.x == 0) {
-      const size_t q = 3 * ((size_t)t.n_fchunks + u);
-      c.trace[q] = t_start;
-      c.trace[q + 1] = t_ready;
-      c.trace[q + 2] = gtimer();
+// Loads of the two inline fan-out terms of a pin's fan-out record (fa, fb),
+// issued as soon as the record is known so the round trips overlap the
+// pin's own loads; the tag check comes later (bwd_pin).
+struct FoPre {
+  float ld0, ld1;
+  uint4 e0, l0, e1, l1;      // required-time words (early, late) of the two terms' pins
+};
+
+__device__ __forceinline__ FoPre bwd_pre(const CornerDev& c, const uint4& fa, const uint4& fb, uint32_t ep) {
+  const uint4 ok = make_uint4(0, ep, 0, ep);
+  FoPre p{0.f, 0.f, ok, ok, ok, ok};
+  if (fa.w == kNone && fa.y) {
+    p.ld0 = __ldcg(c.load + fb.x);
+    p.e0 = ld_ll(c.rat_ll + 2 * (size_t)fb.x);
+    p.l0 = ld_ll(c.rat_ll + 2 * (size_t)fb.x + 1);
+    if (fa.y > 1) {
+      p.ld1 = __ldcg(c.load + fb.z);
+      p.e1 = ld_ll(c.rat_ll + 2 * (size_t)fb.z);
+      p.l1 = ld_ll(c.rat_ll + 2 * (size_t)fb.z + 1);
     }
   }
+  return p;
+}
+
+__device__ __forceinline__ void spin_pair(const uint4* p, uint4& we, uint4& wl, uint32_t ep) {
+  for (uint32_t ns = 32; !ll_ok(we, ep) || !ll_ok(wl, ep); ns = ns < kMaxSleepNs ? 2 * ns : ns) {
+    __nanosleep(ns);
+    if (!ll_ok(we, ep)) we = ld_ll(p);
+    if (!ll_ok(wl, ep)) wl = ld_ll(p + 1);
+  }
+}
+
+// Required times of an input pin (arrival a, slew s) from its endpoint seed
+// and its cell fan-out; fan-out record (fa, fb), inline terms' loads in
+// flight (p); further terms from the CSR (dst_csr / info_csr).
+__device__ __forceinline__ void bwd_pin(const Topo& t, const CornerDev& c, const float* __restrict__ L, uint32_t ep,
+                                        const uint4& fa, const uint4& fb, FoPre p,
+                                        const uint32_t* __restrict__ dst_csr, const uint32_t* __restrict__ info_csr,
+                                        const Q4& a, const Q4& s, Q4& r) {
+  const uint32_t nfo = fa.y;
+  uint32_t f = 0;
+  if (fa.w != kNone) {
+    seed4(t, L, fb.x, fb.y, a, s, r);
+  } else if (nfo) {
+    if (arc_live(fb.y, a)) {
+      spin_pair(c.rat_ll + 2 * (size_t)fb.x, p.e0, p.l0, ep);
+      bwd_arc(L, a, s, fb.y, p.ld0, p.e0, p.l0, r);
+    }
+    if (nfo > 1 && arc_live(fb.w, a)) {
+      spin_pair(c.rat_ll + 2 * (size_t)fb.z, p.e1, p.l1, ep);
+      bwd_arc(L, a, s, fb.w, p.ld1, p.e1, p.l1, r);
+    }
+    f = nfo < 2 ? nfo : 2;
+  }
+  for (; f < nfo; ++f) {
+    const uint32_t info = __ldg(info_csr + fa.z + f);
+    if (!arc_live(info, a)) continue;
+    const uint32_t w2 = __ldg(dst_csr + fa.z + f);
+    const uint4* pw = c.rat_ll + 2 * (size_t)w2;
+    uint4 we = ld_ll(pw), wl = ld_ll(pw + 1);
+    spin_pair(pw, we, wl, ep);
+    bwd_arc(L, a, s, info, __ldcg(c.load + w2), we, wl, r);
+  }
+}
+
+__device__ __forceinline__ void write_ep(const CornerDev& c, uint32_t e, const Q4& s) {
+  c.ep_ws[e] = make_float2(fminf(s.v[2], s.v[3]), fminf(s.v[0], s.v[1]));   // {setup, hold}
+}
+
+// Backward unit: {k0, k1, heavy slot, 0}: a tile of sinks [k0, k1) of one
+// stage's drivers (lane = sink), or {x0, x1, 0, 1}: sink-less pull pins
+// [x0, x1) (lane = pin).  A sink lane: the sink's arrival / slew from its
+// driver's record and net hop, its endpoint seed, its cell fan-out (spinning
+// on the fan-out pins' tagged required-time words), rat / slack, then the
+// candidate of its driver through the net arc; the first lane of each driver
+// merges its sinks from the warp's shared-memory slots and finishes the
+// driver (own seed, direct cell fan-out, rat / slack, the tagged required-
+// time words).  A driver with more than kTile sinks spans tiles of its own
+// (heavy slot): they combine with ordered-int atomics and the last tile
+// finishes the driver.
+__device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, const float* __restrict__ L,
+                                         uint32_t ep, uint32_t u, const uint4& ud, float4* sm) {
+  const uint32_t lane = threadIdx.x & 31;
+  unsigned long long t_start = 0, t_ready = 0, t_data = 0;
+  if (c.trace && lane == 0) t_start = gtimer();
+  uint32_t v = kNone;
+  Q4 at_v = undef_at(), sl_v = undef_at(), acc = undef_rat();
+  bool head = false;
+  uint4 pa = make_uint4(0, 0, 0, kNone), pb = make_uint4(kNone, 0, kNone, 0);   // driver's fan-out record
+  if (ud.w == 0) {
+    const uint32_t k = ud.x + lane;
+    const bool act = k < ud.y;
+    uint4 fa = make_uint4(kNone, 0, 0, kNone), fb = make_uint4(kNone, 0, kNone, 0);
+    if (act) {
+      fa = __ldg(t.sinkfo + 2 * (size_t)k);
+      fb = __ldg(t.sinkfo + 2 * (size_t)k + 1);
+    }
+    v = act ? fa.x : kNone;
+    const uint32_t vp = __shfl_up_sync(kFull, v, 1);
+    head = act && (lane == 0 || vp != v);    // first lane of its driver
+    if (act) {
+      const float elm = __ldcg(c.elm + k);
+      load_rec(c, v, at_v, sl_v);
+      if (head) {
+        pa = __ldg(t.pullfo + 2 * (size_t)v);
+        pb = __ldg(t.pullfo + 2 * (size_t)v + 1);
+      }
+      const FoPre pre = bwd_pre(c, fa, fb, ep);
+      if (c.trace) t_ready = gtimer();
+      Q4 a = at_v, s = sl_v, r = undef_rat();
+      net_hop(a, s, elm);                    // the sink's own arrival / slew
+      bwd_pin(t, c, L, ep, fa, fb, pre, t.sfo_dst, t.sfo_info, a, s, r);
+      if (c.trace) t_data = gtimer();
+      c.rat[t.NP + k] = to_f4(r);
+      const Q4 sk = slack_of(a, r);
+      c.slack[t.NP + k] = to_f4(sk);
+      if (fa.w != kNone) write_ep(c, fa.w, sk);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)            // through the net arc (edges the forward used)
+        if (fin(at_v.v[q])) acc.v[q] = __fsub_rn(r.v[q], elm);
+    }
+    // the first lane of each driver merges the driver's sinks (contiguous)
+    sm[lane] = to_f4(acc);
+    const uint32_t peers = __match_any_sync(kFull, v);
+    __syncwarp();
+    if (head) {
+      const uint32_t end = 31 - __clz(peers);
+      for (uint32_t j = lane + 1; j <= end; ++j) combine(acc, to_q(sm[j]));
+    }
+    __syncwarp();
+    if (ud.z != kNone) {                      // heavy driver: every lane is v
+      int* key = reinterpret_cast<int*>(c.heavy_key + ud.z);
+      if (lane == 0) {
+        atomicMax(key + 0, f2o(acc.v[0]));
+        atomicMax(key + 1, f2o(acc.v[1]));
+        atomicMin(key + 2, f2o(acc.v[2]));
+        atomicMin(key + 3, f2o(acc.v[3]));
+      }
+      // release counter: orders this tile's key updates before it; only the
+      // last tile pays the acquire fence before reading everyone's keys
+      uint32_t done = 0;
+      if (lane == 0)
+        asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(done) : "l"(c.heavy_cnt + ud.z) : "memory");
+      head = false;
+      if (lane == 0 && done + 1 == __ldg(t.heavy_nchunk + ud.z)) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        acc.v[0] = o2f(atomicExch(key + 0, f2o(-CUDART_INF_F)));   // read, reset for the next update
+        acc.v[1] = o2f(atomicExch(key + 1, f2o(-CUDART_INF_F)));
+        acc.v[2] = o2f(atomicExch(key + 2, f2o(CUDART_INF_F)));
+        acc.v[3] = o2f(atomicExch(key + 3, f2o(CUDART_INF_F)));
+        c.heavy_cnt[ud.z] = 0;
+        head = true;
+      }
+    }
+  } else {
+    v = ud.x + lane;                         // sink-less pins [x0, x1)
+    head = v < ud.y;
+    if (head) {
+      load_rec(c, v, at_v, sl_v);
+      pa = __ldg(t.pullfo + 2 * (size_t)v);
+      pb = __ldg(t.pullfo + 2 * (size_t)v + 1);
+    }
+  }
+  // finish driver / pin v
+  if (head) {
+    bwd_pin(t, c, L, ep, pa, pb, bwd_pre(c, pa, pb, ep), t.pfo_dst, t.pfo_info, at_v, sl_v, acc);
+    const Q4 sp = slack_of(at_v, acc);
+    c.slack[v] = to_f4(sp);
+    if (pa.w != kNone) write_ep(c, pa.w, sp);
+    st_ll(c.rat_ll + 2 * (size_t)v, acc.v[0], acc.v[1], ep);
+    st_ll(c.rat_ll + 2 * (size_t)v + 1, acc.v[2], acc.v[3], ep);
+  }
+  if (c.trace) {                             // latest lane's fan-out data
+    const uint32_t lo = (uint32_t)t_data, hi = (uint32_t)(t_data >> 32);
+    const uint32_t mh = __reduce_max_sync(kFull, hi);
+    const uint32_t ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
+    t_data = ((unsigned long long)mh << 32) | ml;
+    t_ready = __shfl_sync(kFull, t_ready, 0);
+  }
+  trace_unit(c, (size_t)t.n_fwu + u, t_start, t_ready ? t_ready : t_start, t_data);
+}
+
+template <bool SMEM_LUT>
+__global__ void __launch_bounds__(kThreads, kBwdMinBlocks) bwd_persistent_kernel(Topo t, CornerDev c,
+                                                                                   uint32_t lut_f4) {
+  __shared__ float4 s_m[kThreads];
+  const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
+  const uint32_t ep = epoch_of(c);
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t W = gridDim.x * (kThreads / 32);
+  uint32_t u = blockIdx.x * (kThreads / 32) + warp;
+  uint4 nx = u < t.n_bwu ? __ldg(t.bwu + u) : make_uint4(0, 0, 0, 0);
+  for (; u < t.n_bwu; u += W) {
+    const uint4 ud = nx;
+    if (u + W < t.n_bwu) nx = __ldg(t.bwu + u + W);   // prefetch the next unit
+    bwd_unit(t, c, L, ep, u, ud, s_m + 32 * warp);
+  }
+}
+
+template <bool SMEM_LUT>
+__global__ void __launch_bounds__(kThreads) bwd_stage_kernel(Topo t, CornerDev c, uint32_t u0, uint32_t u1,
+                                                             uint32_t lut_f4) {
+  __shared__ float4 s_m[kThreads];
+  const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t u = u0 + blockIdx.x * (kThreads / 32) + warp;
+  const uint4 ud = u < u1 ? __ldg(t.bwu + u) : make_uint4(0, 0, 0, 0);
+  pdl_wait();
+  pdl_launch();
+  if (u >= u1) return;
+  bwd_unit(t, c, L, epoch_of(c), u, ud, s_m + 32 * warp);
 }
 
 // ------------------------------------------------------- a5: WNS / TNS
@@ -1295,10 +1160,8 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(Topo t, CornerDev c) {
   if (threadIdx.x == 0) {
     c.res[0] = s_w[0][0]; c.res[1] = s_t[0][0]; c.res[2] = s_w[1][0]; c.res[3] = s_t[1][0];
     *c.red_cnt = 0;                         // self-reset for the next update
-  }
-  for (uint32_t x = threadIdx.x; x < t.S; x += blockDim.x) {   // stage counters: ready for the next update
-    c.bwd_done[x] = 0;
-    c.fwd_done[x] = 0;
+    const uint32_t e = *c.epoch + 1;         // the next update's record tag (never 0)
+    *c.epoch = e ? e : 1;
   }
 }
 
@@ -1309,12 +1172,23 @@ __global__ void gather_pins_kernel(Topo t, CornerDev c, int what, float4* __rest
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= t.P) return;
   const uint32_t i = t.int_of_user[p];
-  if (what >= 2) {
-    dst[p] = what == 2 ? c.rat[i] : c.slack[i];
+  if (what == 3) {
+    dst[p] = c.slack[i];
+    return;
+  }
+  if (what == 2) {                           // pull pins: tagged words {(el, r), (el, f)}
+    if (i >= t.NP) {
+      dst[p] = c.rat[i];
+      return;
+    }
+    const uint4 e = __ldcg(c.rat_ll + 2 * (size_t)i), l = __ldcg(c.rat_ll + 2 * (size_t)i + 1);
+    dst[p] = make_float4(__uint_as_float(e.x), __uint_as_float(e.z), __uint_as_float(l.x), __uint_as_float(l.z));
     return;
   }
   if (i < t.NP) {
-    dst[p] = c.rec[2 * (size_t)i + what];
+    Q4 at, sl;
+    load_rec(c, i, at, sl);
+    dst[p] = to_f4(what == 0 ? at : sl);
     return;
   }
   const uint32_t k = i - t.NP;
@@ -1342,6 +1216,7 @@ __global__ void init_corner_kernel(CornerDev c, uint32_t n_heavy) {
   if (i == 0) {
     *c.red_cnt = 0;
     *c.err_flag = 0;
+    *c.epoch = 1;
   }
 }
 
@@ -1412,28 +1287,20 @@ cudaError_t launch_rc_tierC(const Topo& t, const CornerDev& c, cudaStream_t s) {
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-cudaError_t launch_seed(const Topo& t, const CornerDev& c, uint32_t n0, cudaStream_t s) {
-  if (!n0) return cudaSuccess;
-  return pdl_launch_kernel(seed_kernel, blocks(n0), kThreads, s, t, c, n0);
-}
-
-cudaError_t launch_fwd_stage(const Topo& t, const CornerDev& c, uint32_t pull0, uint32_t n, uint32_t lut_f4,
+cudaError_t launch_fwd_stage(const Topo& t, const CornerDev& c, uint32_t u0, uint32_t u1, uint32_t lut_f4,
                              cudaStream_t s) {
-  if (!n) return cudaSuccess;
-  if (lut_f4) return pdl_launch_smem(fwd_stage_kernel<true>, blocks(n), kThreads, 16ull * lut_f4, s, t, c, pull0, n, lut_f4);
-  return pdl_launch_smem(fwd_stage_kernel<false>, blocks(n), kThreads, 0, s, t, c, pull0, n, lut_f4);
+  if (u1 <= u0) return cudaSuccess;
+  const uint32_t g = blocks(32ull * (u1 - u0));
+  if (lut_f4) return pdl_launch_smem(fwd_stage_kernel<true>, g, kThreads, 16ull * lut_f4, s, t, c, u0, u1, lut_f4);
+  return pdl_launch_smem(fwd_stage_kernel<false>, g, kThreads, 0, s, t, c, u0, u1, lut_f4);
 }
 
-cudaError_t launch_bwd_stage(const Topo& t, const CornerDev& c, uint32_t tile0, uint32_t nTiles, uint32_t sinkEnd,
-                             uint32_t nos0, uint32_t nNos, uint32_t lut_f4, cudaStream_t s) {
-  const uint32_t tb = blocks((uint64_t)nTiles * 32);
-  const uint32_t nb = blocks(nNos);
-  if (!(tb + nb)) return cudaSuccess;
-  if (lut_f4)
-    return pdl_launch_smem(bwd_stage_kernel<true>, tb + nb, kThreads, 16ull * lut_f4, s, t, c, tile0, nTiles, sinkEnd,
-                           nos0, nNos, tb, lut_f4);
-  return pdl_launch_smem(bwd_stage_kernel<false>, tb + nb, kThreads, 0, s, t, c, tile0, nTiles, sinkEnd, nos0, nNos, tb,
-                         lut_f4);
+cudaError_t launch_bwd_stage(const Topo& t, const CornerDev& c, uint32_t u0, uint32_t u1, uint32_t lut_f4,
+                             cudaStream_t s) {
+  if (u1 <= u0) return cudaSuccess;
+  const uint32_t g = blocks(32ull * (u1 - u0));
+  if (lut_f4) return pdl_launch_smem(bwd_stage_kernel<true>, g, kThreads, 16ull * lut_f4, s, t, c, u0, u1, lut_f4);
+  return pdl_launch_smem(bwd_stage_kernel<false>, g, kThreads, 0, s, t, c, u0, u1, lut_f4);
 }
 
 cudaError_t launch_reduce(const Topo& t, const CornerDev& c, cudaStream_t s) {
@@ -1493,7 +1360,7 @@ cudaError_t launch_fwd_persistent(const Topo& t, const CornerDev& c, uint32_t gr
 }
 
 cudaError_t launch_bwd_persistent(const Topo& t, const CornerDev& c, uint32_t grid, uint32_t lut_f4, cudaStream_t s) {
-  if (!t.n_units) return cudaSuccess;
+  if (!t.n_bwu) return cudaSuccess;
   return lut_f4 ? coop_launch(bwd_persistent_kernel<true>, grid, 16ull * lut_f4, s, t, c, lut_f4)
                 : coop_launch(bwd_persistent_kernel<false>, grid, 0, s, t, c, lut_f4);
 }

@@ -24,3 +24,30 @@ for kind in ("fwd", "bwd"):
         dur = [(int(r["end"]) - int(r["start"])) / 1e3 for r in g]
         print(f"  stage {s:3d} n={len(g):5d} first_start={st / 1e3:8.1f} last_ready={rd / 1e3:8.1f} "
               f"last_end={en / 1e3:8.1f} item_us max={max(dur):6.1f} mean={sum(dur) / len(dur):6.1f}")
+
+# per unit type (backward: 0 light tile, 1 heavy tile, 2 sink-less pins)
+by_t = defaultdict(list)
+for r in rows:
+    if r["kind"] == "bwd" and int(r["end"]) > 0:
+        by_t[(int(r["stage"]) == 0, r.get("type", "0"))].append((int(r["end"]) - int(r["start"])) / 1e3)
+for k in sorted(by_t):
+    v = by_t[k]
+    print(f"bwd stage0={k[0]} type={k[1]}: n={len(v)} mean={sum(v) / len(v):.2f} us max={max(v):.1f} us")
+
+# phases of the units of each stage: start -> producers seen (forward probe /
+# backward: fan-out record loaded), -> inputs loaded and computed, -> end
+import statistics
+for kind in ("fwd", "bwd"):
+    fw = defaultdict(list)
+    for r in rows:
+        if r["kind"] == kind and int(r["end"]) > 0 and "data" in r and int(r["data"]) >= int(r["ready"]):
+            fw[int(r["stage"])].append(r)
+    print(f"{kind} phases per stage: median (max) of ready-start, data-ready, end-data  [us]")
+    order = sorted(fw) if kind == "fwd" else sorted(fw, reverse=True)
+    for s in order:
+        g = fw[s]
+        a = [(int(r["ready"]) - int(r["start"])) / 1e3 for r in g]
+        b = [(int(r["data"]) - int(r["ready"])) / 1e3 for r in g]
+        e = [(int(r["end"]) - int(r["data"])) / 1e3 for r in g]
+        print(f"  {s:3d} n={len(g):6d} wait={statistics.median(a):6.2f} ({max(a):6.2f}) load={statistics.median(b):5.2f} "
+              f"({max(b):5.2f}) compute={statistics.median(e):5.2f} ({max(e):5.2f})")
