@@ -129,7 +129,7 @@ struct sta_ctx_s {
   u32 NP = 0, NS = 0, S = 0, n0 = 0, Pi = 0;   // NP includes stage padding; Pi = NP + NS
   std::vector<u32> pull_stage_ptr, sink_stage_ptr, tile_stage_ptr, nosink_stage_ptr, sink_ptr;
   std::vector<u32> drv_of_net;    // user net -> internal driver id
-  u32 n_heavy = 0, n_fwu = 0, n_bwu = 0;
+  u32 n_heavy = 0, n_heavy_parts = 0, n_fwu = 0, n_bwu = 0, n_dslots = 0;
   std::vector<u32> sfo_p, pfo_p, sink_drv;      // host copies for prepare()
   std::vector<u32> sfo_dst, sfo_info, pfo_dst, pfo_info;
   std::vector<u32> fwu_stage_ptr;                // [S + 1] forward units of each stage
@@ -374,7 +374,7 @@ void build_plan(sta_ctx c) {
   };
 
   // forward fan-in terms of pull pins (cell arcs, arc id order)
-  std::vector<u32> fi_p(NP + 1, 0), fi_src, fi_hop, fi_info;
+  std::vector<u32> fi_p(NP + 1, 0), fi_src, fi_hop, fi_info, arc_term(c->A, kNone);
   fi_src.reserve(c->A);
   fi_hop.reserve(c->A);
   fi_info.reserve(c->A);
@@ -384,6 +384,7 @@ void build_plan(sta_ctx c) {
     if (p == kNone) continue;
     for (u32 x = fi_ptr[p]; x < fi_ptr[p + 1]; ++x) {
       const u32 a = fi_ids[x], u = c->arc_from[a];
+      arc_term[a] = (u32)fi_src.size();
       for (u32 q = 0; q < n_terms(a); ++q) {
         if (c->is_sink[u]) {
           fi_src.push_back(c->int_of_user[driver_of(u)]);
@@ -407,7 +408,7 @@ void build_plan(sta_ctx c) {
       const u32 a = fo_ids[x];
       for (u32 q = 0; q < n_terms(a); ++q) {
         sfo_dst.push_back(c->int_of_user[c->arc_to[a]]);
-        sfo_info.push_back(term_info(a, q));
+        sfo_info.push_back(arc_term[a] + q);   // term index; becomes sense | delay slot << 3 below
       }
     }
   }
@@ -420,7 +421,7 @@ void build_plan(sta_ctx c) {
       const u32 a = fo_ids[x];
       for (u32 q = 0; q < n_terms(a); ++q) {
         pfo_dst.push_back(c->int_of_user[c->arc_to[a]]);
-        pfo_info.push_back(term_info(a, q));
+        pfo_info.push_back(arc_term[a] + q);
       }
     }
   }
@@ -431,7 +432,8 @@ void build_plan(sta_ctx c) {
   // tiles (heavy slot: atomics + last-tile finish).  Stage pins without sinks
   // are listed separately.
   std::vector<uint2> tiles;
-  std::vector<u32> nosink, heavy_nchunk;
+  std::vector<u32> nosink, heavy_nchunk, heavy_base, tile_part;   // tile_part: partial slot of a heavy tile
+  u32 n_parts = 0;
   c->tile_stage_ptr.assign(S + 1, 0);
   c->nosink_stage_ptr.assign(S + 1, 0);
   // Work-unit size adapts to the stage: a unit waits for the slowest of its
@@ -465,14 +467,19 @@ void build_plan(sta_ctx c) {
         cur = kNone;
         const u32 slot = (u32)heavy_nchunk.size();
         const u32 nch = (n + sta::kTile - 1) / sta::kTile;
+        heavy_base.push_back(n_parts);
         heavy_nchunk.push_back(nch);
-        for (u32 q = 0; q < nch; ++q) tiles.push_back(make_uint2(b + q * sta::kTile, slot));
+        for (u32 q = 0; q < nch; ++q) {
+          tiles.push_back(make_uint2(b + q * sta::kTile, slot));
+          tile_part.push_back(n_parts++);
+        }
         continue;
       }
       if (cur == kNone || fill + n > tcap) {
         cur = b;
         fill = 0;
         tiles.push_back(make_uint2(b, kNone));
+        tile_part.push_back(kNone);
       }
       fill += n;
     }
@@ -480,6 +487,7 @@ void build_plan(sta_ctx c) {
   c->tile_stage_ptr[S] = (u32)tiles.size();
   c->nosink_stage_ptr[S] = (u32)nosink.size();
   c->n_heavy = (u32)heavy_nchunk.size();
+  c->n_heavy_parts = n_parts;
 
   // persistent-kernel work lists (warp-granular dataflow, sta_kernels.cu):
   // forward units are runs of consecutive pull pins of one stage with <=
@@ -492,6 +500,10 @@ void build_plan(sta_ctx c) {
   // descending stage order.  Both lists are in dependency order: every unit
   // depends only on units with a smaller index.
   std::vector<uint4> fterm, bwu;           // forward term slots (kFwdUnitTerms per unit) / backward units
+  // delay slot of each fan-in term: its unit slot, or past the unit slots for
+  // the terms of heavy pins (the forward stores the term's four delays there,
+  // the backward reads them)
+  std::vector<u32> term_slot(fi_src.size(), kNone), heavy_units;
   std::vector<u32> fwu_stage, stage_sink_end(S);
   for (u32 s = 0; s < S; ++s) stage_sink_end[s] = c->sink_ptr[c->pull_stage_ptr[s + 1]];
   std::vector<u32> fi_pin(fi_src.size());
@@ -526,7 +538,12 @@ void build_plan(sta_ctx c) {
       }
       const u32 e0 = fi_p[q0];
       if (items > sta::kFwdUnitTerms) {    // one pin with many terms: the warp loops over fi_*
-        for (u32 x = 0; x < sta::kFwdUnitTerms; ++x) fterm.push_back(make_uint4(sta::kHeavyMark, e0, items, q0));
+        // slot 0: {mark, first term, terms, pin}; slot 1: {mark, first delay slot}
+        // (the delays of these terms live past the unit slots)
+        heavy_units.push_back((u32)fterm.size());
+        fterm.push_back(make_uint4(sta::kHeavyMark, e0, items, q0));
+        fterm.push_back(make_uint4(sta::kHeavyMark, 0, 0, 0));
+        for (u32 x = 2; x < sta::kFwdUnitTerms; ++x) fterm.push_back(make_uint4(sta::kHeavyMark, e0, items, q0));
       } else {
         // probe term: the one whose source record is produced last (ids are
         // in stage order)
@@ -540,11 +557,23 @@ void build_plan(sta_ctx c) {
           }
           const u32 e = e0 + x;
           if (fi_info[e] >> 31) fail(STA_ERR_LUT, "table id too large for the forward plan");
+          term_slot[e] = (u32)fterm.size();
           fterm.push_back(make_uint4(fi_src[e], fi_hop[e], fi_info[e] | (x == probe ? 0x80000000u : 0u), fi_pin[e]));
         }
       }
       fwu_stage.push_back(s);
     }
+  }
+  {
+    u32 next = (u32)fterm.size();
+    for (u32 h : heavy_units) {
+      fterm[h + 1].y = next;
+      for (u32 x = 0; x < fterm[h].z; ++x) term_slot[fterm[h].y + x] = next++;
+    }
+    c->n_dslots = next;
+    if (next >= (1u << 29)) fail(STA_ERR_ARG, "forward plan too large (%u term slots)", next);
+    for (u32& x : sfo_info) x = (fi_info[x] & 7u) | term_slot[x] << 3;
+    for (u32& x : pfo_info) x = (fi_info[x] & 7u) | term_slot[x] << 3;
   }
   c->fwu_stage_ptr.assign(S + 1, 0);
   for (u32 s : fwu_stage) c->fwu_stage_ptr[s + 1]++;
@@ -555,7 +584,7 @@ void build_plan(sta_ctx c) {
     c->bwu_stage_lo[s] = (u32)bwu.size();
     for (u32 x = c->tile_stage_ptr[s]; x < c->tile_stage_ptr[s + 1]; ++x) {
       const u32 k1 = x + 1 < c->tile_stage_ptr[s + 1] ? tiles[x + 1].x : stage_sink_end[s];
-      bwu.push_back(make_uint4(tiles[x].x, k1, tiles[x].y, 0));
+      bwu.push_back(make_uint4(tiles[x].x, k1, tiles[x].y, tile_part[x] == kNone ? 0 : 2 + tile_part[x]));
     }
     const u32 ncap = unit_cap(c->nosink_stage_ptr[s + 1] - c->nosink_stage_ptr[s], sta::kTile, bwd_warps);
     for (u32 x = c->nosink_stage_ptr[s]; x < c->nosink_stage_ptr[s + 1]; x += ncap) {
@@ -570,7 +599,7 @@ void build_plan(sta_ctx c) {
   c->fwu_stage_h = fwu_stage;
   c->bwu_stage_h.resize(bwu.size());
   c->bwu_kind_h.resize(bwu.size());
-  for (size_t x = 0; x < bwu.size(); ++x) c->bwu_kind_h[x] = bwu[x].w ? 2 : bwu[x].z != kNone ? 1 : 0;
+  for (size_t x = 0; x < bwu.size(); ++x) c->bwu_kind_h[x] = bwu[x].w == 1 ? 2 : bwu[x].z != kNone ? 1 : 0;
   for (u32 s = 0; s < S; ++s)
     for (u32 x = c->bwu_stage_lo[s]; x < c->bwu_stage_hi[s]; ++x) c->bwu_stage_h[x] = s;
 
@@ -604,8 +633,10 @@ void build_plan(sta_ctx c) {
   t.n_fwu = c->n_fwu;
   t.bwu = g.upload(bwu, s);
   t.n_bwu = c->n_bwu;
+  t.n_bwu_static = S ? c->bwu_stage_lo[0] : 0;
   t.nosink = g.upload(nosink, s);
   t.heavy_nchunk = g.upload(heavy_nchunk, s);
+  t.heavy_base = g.upload(heavy_base, s);
   t.int_of_user = g.upload(c->int_of_user, s);
   t.drv_of_net = g.upload(c->drv_of_net, s);
   ck(cudaStreamSynchronize(s), "plan upload");
@@ -902,6 +933,7 @@ void prepare(sta_ctx c) {
     sta::CornerDev& d = cs.dev;
     d.rec = a.alloc<uint4>(4 * (size_t)c->NP);
     d.rat_ll = a.alloc<uint4>(2 * (size_t)c->NP);
+    d.tdel = a.alloc<float4>(std::max<u32>(c->n_dslots, 1));
     d.epoch = a.alloc<u32>(1);
     ck(cudaMemsetAsync(d.rec, 0, sizeof(uint4) * 4 * (size_t)c->NP, s), "memset");
     ck(cudaMemsetAsync(d.rat_ll, 0, sizeof(uint4) * 2 * (size_t)c->NP, s), "memset");
@@ -912,8 +944,9 @@ void prepare(sta_ctx c) {
     d.ep_ws = a.alloc<float2>(c->n_ep);
     d.res = a.alloc<double>(4);
     d.red_part = a.alloc<double>(4 * sta::kRedBlocks);
-    d.red_cnt = a.alloc<u32>(1);
-    d.heavy_key = a.alloc<int4>(c->n_heavy);
+    d.red_cnt = a.alloc<u32>(2);
+    ck(cudaMemsetAsync(d.red_cnt, 0, 2 * sizeof(u32), s), "memset");
+    d.heavy_part = a.alloc<float4>(c->n_heavy_parts);
     d.heavy_cnt = a.alloc<u32>(c->n_heavy);
     d.scratch = a.alloc<double>(sta::tierC_scratch(c->big_total));
     ck(cudaMemsetAsync(d.scratch, 0, sizeof(double) * sta::tierC_scratch(c->big_total), s), "memset");

@@ -34,7 +34,7 @@ constexpr uint32_t kFwdUnitTerms = 8;          // forward warp unit: fan-in term
 #define STA_FWD_BLOCKS 5
 #endif
 #ifndef STA_BWD_BLOCKS
-#define STA_BWD_BLOCKS 3
+#define STA_BWD_BLOCKS 2
 #endif
 constexpr int kFwdMinBlocks = STA_FWD_BLOCKS;
 constexpr int kBwdMinBlocks = STA_BWD_BLOCKS;
@@ -79,26 +79,32 @@ struct Topo {
   const EpRec* ep;           // [n_ep]
   const uint32_t* nosink;    // pull pins without sinks, by stage
   const uint32_t* heavy_nchunk; // [n_heavy] tiles of each heavy driver
+  const uint32_t* heavy_base;   // [n_heavy] first partial slot of each heavy driver
   // propagation work units (sta_kernels.cu), lists in dependency order
   // forward warp unit u = term slots [kFwdUnitTerms u, kFwdUnitTerms (u + 1)):
   //   {src, hop, info | probe << 31, pin}: a fan-in term of pull pin `pin`
   //     (record src, sink hop or kNone); probe: the slot polled first
   //   {kNone, kNone, 0, kNone}: padding
   //   {kSeedMark, 0, 0, pin or kNone}: stage-0 pin (seed)
-  //   {kHeavyMark, term0, nterms, pin} in every slot: one pin with more than
-  //     kFwdUnitTerms terms (fi_* arrays), looped over by the warp
+  //   {kHeavyMark, term0, nterms, pin} in every slot but slot 1 = {kHeavyMark,
+  //     first delay slot, 0, 0}: one pin with more than kFwdUnitTerms terms
+  //     (fi_* arrays), looped over by the warp
+  // the delay slot of a term is its unit slot (heavy pins: past the units)
   const uint4* fterm;
   uint32_t n_fwu;
-  // backward warp units, descending stage: {k0, k1, heavy slot or kNone, 0}:
-  // sinks [k0, k1) (<= kTile, a light driver never split); {x0, x1, 0, 1}:
+  // backward warp units, descending stage: {k0, k1, kNone, 0}: sinks [k0, k1)
+  // (<= kTile, a light driver never split); {k0, k1, heavy slot, 2 + partial
+  // slot}: one tile of a driver with more than kTile sinks; {x0, x1, 0, 1}:
   // sink-less pull pins [x0, x1) (<= kTile; internal ids of a stage put
   // drivers first, so a stage's sink-less pins are contiguous)
   const uint4* bwu;
   uint32_t n_bwu;
+  uint32_t n_bwu_static;         // units [0, n_bwu_static) statically assigned; the rest (stage 0,
+                                 // no dependencies among them) handed out by a ticket counter
   // backward fan-out records, two uint4 per sink (sinkfo) / pull pin (pullfo):
   //   a = {driver (sinks; 0 for pull pins), nfo = cell fan-out terms, f0 =
   //        first term in sfo_* / pfo_*, endpoint index or kNone}
-  //   b = non-endpoints: {dst, info} of the first two fan-out terms (kNone
+  //   b = non-endpoints: {dst, sense | delay slot << 3} of the first two fan-out terms (kNone
   //       dst if absent); endpoints: {check table or kNone, PO index or
   //       kNone, 0, 0} and the fan-out is read from sfo_* / pfo_*
   const uint4* sinkfo;
@@ -156,6 +162,8 @@ struct CornerDev {
   uint4* rec;         // [4 NP]: tagged forward records of pull pins (sta_kernels.cu: ld_ll)
   uint4* rat_ll;      // [2 NP]: tagged required times of pull pins
   uint32_t* epoch;    // [1] tag of the current update (advanced by reduce_kernel)
+  float4* tdel;       // [delay slots] cell-arc delays of each fan-in term, (el, orf) order,
+                      // written by the forward, read by the backward
   float4* rat;        // [P]: required times of sinks (ids >= NP; pull pins use rat_ll)
   float4* slack;      // [P]
   float* elm;         // [NS] Elmore delay of each sink's net arc
@@ -163,8 +171,8 @@ struct CornerDev {
   float2* ep_ws;      // [n_ep] worst setup / hold slack per endpoint
   double* res;        // [4]
   double* red_part;   // [kRedBlocks * 4] reduction partials
-  uint32_t* red_cnt;  // [1] last-block counter (self-resetting)
-  int4* heavy_key;    // [n_heavy] ordered-int RAT accumulators (self-resetting)
+  uint32_t* red_cnt;  // [2] last-block counter, backward tail ticket (reset by reduce_kernel)
+  float4* heavy_part; // [heavy tiles] partial required time of each heavy-driver tile
   uint32_t* heavy_cnt;// [n_heavy] finished tiles (self-resetting)
   const float* lut;   // table records (kTabStride floats each)
   const float* const* rc_vals;  // device {res, cap} pointer pair (user node order)

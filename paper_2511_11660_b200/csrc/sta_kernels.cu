@@ -162,7 +162,10 @@ __device__ __forceinline__ void st_ll(uint4* p, float a, float b, uint32_t ep) {
 }
 __device__ __forceinline__ bool ll_ok(const uint4& w, uint32_t ep) { return w.y == ep && w.w == ep; }
 // polling backoff cap: a waiter notices a completed record at most this late
-constexpr uint32_t kMaxSleepNs = 128;
+#ifndef STA_MAX_SLEEP_NS
+#define STA_MAX_SLEEP_NS 128
+#endif
+constexpr uint32_t kMaxSleepNs = STA_MAX_SLEEP_NS;
 __device__ __forceinline__ uint4 spin_ll(const uint4* p, uint32_t ep) {
   uint4 w = ld_ll(p);
   uint32_t ns = 32;
@@ -661,7 +664,7 @@ __device__ __forceinline__ void combine(Q4& a, const Q4& b) {
 constexpr uint32_t kFwdTerms = kFwdUnitTerms;
 
 __device__ __forceinline__ void fwd_lane(const float* __restrict__ L, uint32_t info, int el, int orf, float ld,
-                                         float a_in, float s_in, float& ca, float& cs) {
+                                         float a_in, float s_in, float& ca, float& cs, float& dl) {
   const uint32_t tab = info >> 3;
   const Tab rd = tab_rec(L, tab + orf);          // cell_rise / cell_fall
   const Tab rs = tab_rec(L, tab + 2 + orf);      // rise / fall transition
@@ -676,6 +679,7 @@ __device__ __forceinline__ void fwd_lane(const float* __restrict__ L, uint32_t i
   const float undef = el ? -CUDART_INF_F : CUDART_INF_F;
   ca = ok ? __fadd_rn(a_in, d) : undef;
   cs = ok ? so : undef;
+  dl = d;                                    // the backward's delay of this (el, irf -> orf)
 }
 
 __device__ __forceinline__ void merge_q(float& a, float b, int el) { a = el ? fmaxf(a, b) : fminf(a, b); }
@@ -688,9 +692,23 @@ __device__ __forceinline__ void hop_q(float& a_in, float& s_in, float elm) {
   s_in = __fsqrt_rn(__fmaf_rn(s_in, s_in, __fmul_rn(imp, imp)));
 }
 
-// forward unit u; tr = this lane's term slot of the unit
+// RC results a term slot needs: {Elmore delay of its sink input, load of its pin}
+struct FwdRc {
+  float elm, ld;
+};
+__device__ __forceinline__ FwdRc fwd_rc(const CornerDev& c, const uint4& tr) {
+  FwdRc r{0.f, 0.f};
+  if (tr.x < kHeavyMark) {                   // a term (not padding / seed / heavy marker)
+    if (tr.y != kNone) r.elm = __ldcg(c.elm + tr.y);
+    r.ld = __ldcg(c.load + tr.w);
+  }
+  return r;
+}
+
+// forward unit u; tr = this lane's term slot of the unit, rc its RC results
+// (loaded by the caller, software-pipelined one unit ahead)
 __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, const float* __restrict__ L,
-                                         uint32_t ep, uint32_t u, const uint4& tr) {
+                                         uint32_t ep, uint32_t u, const uint4& tr, FwdRc rc) {
   const uint32_t lane = threadIdx.x & 31, tl = lane >> 2, q = lane & 3;
   const int el = (int)(q >> 1), orf = (int)(q & 1);
   const float undef = el ? -CUDART_INF_F : CUDART_INF_F;
@@ -717,11 +735,7 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
   if (kind != kHeavyMark) {
     const bool item = tr.x != kNone;
     const uint32_t src = tr.x, info = tr.z & 0x7FFFFFFFu, v = tr.w;
-    float elm = 0.f, ld = 0.f;
-    if (item) {                              // RC results of this update
-      if (tr.y != kNone) elm = __ldcg(c.elm + tr.y);
-      ld = __ldcg(c.load + v);
-    }
+    const float elm = rc.elm, ld = rc.ld;
     const int irf = primary_irf(info & 7u, orf);
     const uint4* wp = c.rec + 4 * (size_t)src + (el * 2 + irf);
     if ((tr.z >> 31) && q == 3) spin_ll(wp, ep);   // probe
@@ -733,7 +747,9 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
       if (c.trace) t_data = gtimer();
       float a_in = __uint_as_float(w.x), s_in = __uint_as_float(w.z);
       if (tr.y != kNone) hop_q(a_in, s_in, elm);
-      fwd_lane(L, info, el, orf, ld, a_in, s_in, ca, cs);
+      float dl;
+      fwd_lane(L, info, el, orf, ld, a_in, s_in, ca, cs, dl);
+      reinterpret_cast<float*>(c.tdel + (size_t)kFwdTerms * u + tl)[q] = dl;
     }
     // merge the pin's terms into its first term's lanes (same q); a pin's
     // terms occupy consecutive slots
@@ -750,7 +766,8 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
     }
     if (item && tl == head_tl) st_ll(c.rec + 4 * (size_t)v + q, ca, cs, ep);
   } else {                                   // one pin with > kFwdTerms terms: warp loop
-    const uint32_t v = tr.w, e0 = tr.y, nterms = tr.z;
+    const uint32_t v = __shfl_sync(kFull, tr.w, 0), e0 = __shfl_sync(kFull, tr.y, 0), nterms = __shfl_sync(kFull, tr.z, 0);
+    const uint32_t dbase = __shfl_sync(kFull, tr.y, 4);   // slot 1: first delay slot
     const float ld = __ldcg(c.load + v);
     float ca = undef, cs = undef;
     for (uint32_t b = tl; b < nterms; b += kFwdTerms) {
@@ -760,8 +777,9 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
       const uint4 w = spin_ll(c.rec + 4 * (size_t)t.fi_src[e] + (el * 2 + irf), ep);
       float a_in = __uint_as_float(w.x), s_in = __uint_as_float(w.z);
       if (h != kNone) hop_q(a_in, s_in, __ldcg(c.elm + h));
-      float oa, os;
-      fwd_lane(L, info, el, orf, ld, a_in, s_in, oa, os);
+      float oa, os, dl;
+      fwd_lane(L, info, el, orf, ld, a_in, s_in, oa, os, dl);
+      reinterpret_cast<float*>(c.tdel + dbase + b)[q] = dl;
       merge_q(ca, oa, el);
       merge_q(cs, os, el);
     }
@@ -790,11 +808,14 @@ __global__ void __launch_bounds__(kThreads, kFwdMinBlocks) fwd_persistent_kernel
   const uint32_t tl = (threadIdx.x & 31) >> 2;
   const uint32_t W = gridDim.x * (kThreads / 32);
   uint32_t u = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  // software pipeline: the next unit's term slot is in flight while a unit
+  // waits for its producers (the RC results are loaded by the unit itself: prefetching them too
+  // measured slower on C3)
   uint4 nx = u < t.n_fwu ? __ldg(t.fterm + (size_t)kFwdTerms * u + tl) : make_uint4(0, 0, 0, 0);
   for (; u < t.n_fwu; u += W) {
     const uint4 tr = nx;
     if (u + W < t.n_fwu) nx = __ldg(t.fterm + (size_t)kFwdTerms * (u + W) + tl);   // prefetch the next unit
-    fwd_unit(t, c, L, ep, u, tr);
+    fwd_unit(t, c, L, ep, u, tr, fwd_rc(c, tr));
   }
 }
 
@@ -808,7 +829,7 @@ __global__ void __launch_bounds__(kThreads) fwd_stage_kernel(Topo t, CornerDev c
   pdl_wait();
   pdl_launch();
   if (u >= u1) return;
-  fwd_unit(t, c, L, epoch_of(c), u, tr);
+  fwd_unit(t, c, L, epoch_of(c), u, tr, fwd_rc(c, tr));
 }
 
 // ---- backward: one lane per sink / pin (all four components in the lane)
@@ -816,26 +837,21 @@ __global__ void __launch_bounds__(kThreads) fwd_stage_kernel(Topo t, CornerDev c
 // RAT(w, el, orf) - d(el, irf -> orf) over the output edges orf whose input
 // edge irf (by the sense) has a defined arrival -- exactly the pairs the
 // forward used; late min, early max.  we / wl: w's tagged required-time words
-// (early, late).  d is recomputed with cell_term's seg / interp calls on the
-// same operands: bit-identical.
-__device__ __forceinline__ void bwd_arc(const float* __restrict__ L, const Q4& a, const Q4& s, uint32_t info,
-                                        float ld, const uint4& we, const uint4& wl, Q4& r) {
-  const uint32_t sense = info & 7u, tab = info >> 3;
-  const Tab rd0 = tab_rec(L, tab), rd1 = tab_rec(L, tab + 1);
-  const Seg cd0 = seg(rd0.ax + 24, ld);
-  const Seg cd1 = rd1.ax == rd0.ax ? cd0 : seg(rd1.ax + 24, ld);
+// (early, late); d: the term's delays stored by the forward, (el, orf) order
+// (the very values the forward added: no recomputation).
+__device__ __forceinline__ void bwd_arc(const Q4& a, uint32_t info, const float4& d4, const uint4& we,
+                                        const uint4& wl, Q4& r) {
+  const uint32_t sense = info & 7u;
+  const float d[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
   for (int orf = 0; orf < 2; ++orf) {
     const int irf = primary_irf(sense, orf);
-    const Tab rd = orf ? rd1 : rd0;
 #pragma unroll
     for (int el = 0; el < 2; ++el) {
       // (selects, not dynamic register-array indices: those go to local memory)
-      const float s_in = irf ? s.v[el * 2 + 1] : s.v[el * 2];
       const bool ok = fin(irf ? a.v[el * 2 + 1] : a.v[el * 2]);
-      const float d = fmaxf(0.f, interp(rd, seg(rd.ax, s_in), orf ? cd1 : cd0));
       const uint4& w = el ? wl : we;
-      const float cand = __fsub_rn(__uint_as_float(orf ? w.z : w.x), d);
+      const float cand = __fsub_rn(__uint_as_float(orf ? w.z : w.x), d[el * 2 + orf]);
       float& r0 = r.v[el * 2];
       float& r1 = r.v[el * 2 + 1];
       const float m0 = el ? fminf(r0, cand) : fmaxf(r0, cand);
@@ -881,19 +897,20 @@ __device__ __forceinline__ void seed4(const Topo& t, const float* __restrict__ L
 // issued as soon as the record is known so the round trips overlap the
 // pin's own loads; the tag check comes later (bwd_pin).
 struct FoPre {
-  float ld0, ld1;
-  uint4 e0, l0, e1, l1;      // required-time words (early, late) of the two terms' pins
+  float4 d0, d1;             // the terms' delays
+  uint4 e0, l0, e1, l1;      // required-time words (early, late) of the terms' pins
 };
 
 __device__ __forceinline__ FoPre bwd_pre(const CornerDev& c, const uint4& fa, const uint4& fb, uint32_t ep) {
   const uint4 ok = make_uint4(0, ep, 0, ep);
-  FoPre p{0.f, 0.f, ok, ok, ok, ok};
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  FoPre p{z, z, ok, ok, ok, ok};
   if (fa.w == kNone && fa.y) {
-    p.ld0 = __ldcg(c.load + fb.x);
+    p.d0 = __ldcg(c.tdel + (fb.y >> 3));
     p.e0 = ld_ll(c.rat_ll + 2 * (size_t)fb.x);
     p.l0 = ld_ll(c.rat_ll + 2 * (size_t)fb.x + 1);
     if (fa.y > 1) {
-      p.ld1 = __ldcg(c.load + fb.z);
+      p.d1 = __ldcg(c.tdel + (fb.w >> 3));
       p.e1 = ld_ll(c.rat_ll + 2 * (size_t)fb.z);
       p.l1 = ld_ll(c.rat_ll + 2 * (size_t)fb.z + 1);
     }
@@ -923,11 +940,11 @@ __device__ __forceinline__ void bwd_pin(const Topo& t, const CornerDev& c, const
   } else if (nfo) {
     if (arc_live(fb.y, a)) {
       spin_pair(c.rat_ll + 2 * (size_t)fb.x, p.e0, p.l0, ep);
-      bwd_arc(L, a, s, fb.y, p.ld0, p.e0, p.l0, r);
+      bwd_arc(a, fb.y, p.d0, p.e0, p.l0, r);
     }
     if (nfo > 1 && arc_live(fb.w, a)) {
       spin_pair(c.rat_ll + 2 * (size_t)fb.z, p.e1, p.l1, ep);
-      bwd_arc(L, a, s, fb.w, p.ld1, p.e1, p.l1, r);
+      bwd_arc(a, fb.w, p.d1, p.e1, p.l1, r);
     }
     f = nfo < 2 ? nfo : 2;
   }
@@ -937,8 +954,9 @@ __device__ __forceinline__ void bwd_pin(const Topo& t, const CornerDev& c, const
     const uint32_t w2 = __ldg(dst_csr + fa.z + f);
     const uint4* pw = c.rat_ll + 2 * (size_t)w2;
     uint4 we = ld_ll(pw), wl = ld_ll(pw + 1);
+    const float4 d4 = __ldcg(c.tdel + (info >> 3));
     spin_pair(pw, we, wl, ep);
-    bwd_arc(L, a, s, info, __ldcg(c.load + w2), we, wl, r);
+    bwd_arc(a, info, d4, we, wl, r);
   }
 }
 
@@ -957,8 +975,23 @@ __device__ __forceinline__ void write_ep(const CornerDev& c, uint32_t e, const Q
 // time words).  A driver with more than kTile sinks spans tiles of its own
 // (heavy slot): they combine with ordered-int atomics and the last tile
 // finishes the driver.
+// fan-out record of the lane's sink in tile unit ud (the caller loads it one
+// unit ahead)
+struct SinkFo {
+  uint4 a, b;
+};
+__device__ __forceinline__ SinkFo bwd_fo(const Topo& t, const uint4& ud) {
+  SinkFo f{make_uint4(kNone, 0, 0, kNone), make_uint4(kNone, 0, kNone, 0)};
+  const uint32_t k = ud.x + (threadIdx.x & 31);
+  if (ud.w != 1 && k < ud.y) {
+    f.a = __ldg(t.sinkfo + 2 * (size_t)k);
+    f.b = __ldg(t.sinkfo + 2 * (size_t)k + 1);
+  }
+  return f;
+}
+
 __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, const float* __restrict__ L,
-                                         uint32_t ep, uint32_t u, const uint4& ud, float4* sm) {
+                                         uint32_t ep, uint32_t u, const uint4& ud, const SinkFo& fo, float4* sm) {
   const uint32_t lane = threadIdx.x & 31;
   unsigned long long t_start = 0, t_ready = 0, t_data = 0;
   if (c.trace && lane == 0) t_start = gtimer();
@@ -966,14 +999,10 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
   Q4 at_v = undef_at(), sl_v = undef_at(), acc = undef_rat();
   bool head = false;
   uint4 pa = make_uint4(0, 0, 0, kNone), pb = make_uint4(kNone, 0, kNone, 0);   // driver's fan-out record
-  if (ud.w == 0) {
+  if (ud.w != 1) {                           // tile of sinks (light or heavy)
     const uint32_t k = ud.x + lane;
     const bool act = k < ud.y;
-    uint4 fa = make_uint4(kNone, 0, 0, kNone), fb = make_uint4(kNone, 0, kNone, 0);
-    if (act) {
-      fa = __ldg(t.sinkfo + 2 * (size_t)k);
-      fb = __ldg(t.sinkfo + 2 * (size_t)k + 1);
-    }
+    const uint4 fa = fo.a, fb = fo.b;
     v = act ? fa.x : kNone;
     const uint32_t vp = __shfl_up_sync(kFull, v, 1);
     head = act && (lane == 0 || vp != v);    // first lane of its driver
@@ -1008,27 +1037,30 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
     }
     __syncwarp();
     if (ud.z != kNone) {                      // heavy driver: every lane is v
-      int* key = reinterpret_cast<int*>(c.heavy_key + ud.z);
-      if (lane == 0) {
-        atomicMax(key + 0, f2o(acc.v[0]));
-        atomicMax(key + 1, f2o(acc.v[1]));
-        atomicMin(key + 2, f2o(acc.v[2]));
-        atomicMin(key + 3, f2o(acc.v[3]));
-      }
-      // release counter: orders this tile's key updates before it; only the
-      // last tile pays the acquire fence before reading everyone's keys
+      // partial of this tile, then a release increment of the driver's tile
+      // counter (one atomic per tile); the last tile combines all partials
+      if (lane == 0) c.heavy_part[ud.w - 2] = to_f4(acc);
+      __syncwarp();
       uint32_t done = 0;
       if (lane == 0)
         asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(done) : "l"(c.heavy_cnt + ud.z) : "memory");
+      const uint32_t nch = __ldg(t.heavy_nchunk + ud.z);
       head = false;
-      if (lane == 0 && done + 1 == __ldg(t.heavy_nchunk + ud.z)) {
+      if (__shfl_sync(kFull, done, 0) + 1 == nch) {
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        acc.v[0] = o2f(atomicExch(key + 0, f2o(-CUDART_INF_F)));   // read, reset for the next update
-        acc.v[1] = o2f(atomicExch(key + 1, f2o(-CUDART_INF_F)));
-        acc.v[2] = o2f(atomicExch(key + 2, f2o(CUDART_INF_F)));
-        acc.v[3] = o2f(atomicExch(key + 3, f2o(CUDART_INF_F)));
-        c.heavy_cnt[ud.z] = 0;
-        head = true;
+        const uint32_t b0 = __ldg(t.heavy_base + ud.z);
+        acc = undef_rat();
+#pragma unroll 4
+        for (uint32_t x = lane; x < nch; x += 32) combine(acc, to_q(__ldcg(c.heavy_part + b0 + x)));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          Q4 b;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) b.v[q] = __shfl_xor_sync(kFull, acc.v[q], o);
+          combine(acc, b);
+        }
+        if (lane == 0) c.heavy_cnt[ud.z] = 0;   // self-reset for the next update
+        head = lane == 0;
       }
     }
   } else {
@@ -1068,11 +1100,40 @@ __global__ void __launch_bounds__(kThreads, kBwdMinBlocks) bwd_persistent_kernel
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t W = gridDim.x * (kThreads / 32);
   uint32_t u = blockIdx.x * (kThreads / 32) + warp;
-  uint4 nx = u < t.n_bwu ? __ldg(t.bwu + u) : make_uint4(0, 0, 0, 0);
-  for (; u < t.n_bwu; u += W) {
-    const uint4 ud = nx;
-    if (u + W < t.n_bwu) nx = __ldg(t.bwu + u + W);   // prefetch the next unit
-    bwd_unit(t, c, L, ep, u, ud, s_m + 32 * warp);
+  // software pipeline: the unit record two units ahead, the sinks' fan-out
+  // records one unit ahead are in flight while a unit waits for its producers
+  // (issued at the start of the previous unit, so they overlap its work)
+  const uint4 none = make_uint4(0, 0, 0, 1);
+  uint4 ud = u < t.n_bwu_static ? __ldg(t.bwu + u) : none;
+  SinkFo fo = bwd_fo(t, ud);
+  uint4 nx = u + W < t.n_bwu_static ? __ldg(t.bwu + u + W) : none;
+  // Stage-0 units (no dependencies among them, all inputs produced by the
+  // static part) go to whichever warp is free, by ticket: warps finish their
+  // static units at different times, and a static split of the tail would
+  // leave the stragglers' share waiting for them.
+  const uint32_t ns = t.n_bwu_static, lane = threadIdx.x & 31;
+  for (;;) {
+    SinkFo nfo = fo;
+    uint4 nnx = none;
+    const bool dyn = u >= ns;
+    if (dyn) {
+      uint32_t x = 0;
+      if (lane == 0) x = atomicAdd(c.red_cnt + 1, 1u);
+      u = ns + __shfl_sync(kFull, x, 0);
+      if (u >= t.n_bwu) break;
+      ud = __ldg(t.bwu + u);
+      fo = bwd_fo(t, ud);
+    } else {
+      nfo = bwd_fo(t, nx);                   // next unit's fan-out records (its record arrived)
+      if (u + 2 * W < ns) nnx = __ldg(t.bwu + u + 2 * W);
+    }
+    bwd_unit(t, c, L, ep, u, ud, fo, s_m + 32 * warp);
+    if (!dyn) {
+      u += W;
+      ud = nx;
+      fo = nfo;
+      nx = nnx;
+    }
   }
 }
 
@@ -1084,10 +1145,11 @@ __global__ void __launch_bounds__(kThreads) bwd_stage_kernel(Topo t, CornerDev c
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t u = u0 + blockIdx.x * (kThreads / 32) + warp;
   const uint4 ud = u < u1 ? __ldg(t.bwu + u) : make_uint4(0, 0, 0, 0);
+  const SinkFo fo = bwd_fo(t, ud);
   pdl_wait();
   pdl_launch();
   if (u >= u1) return;
-  bwd_unit(t, c, L, epoch_of(c), u, ud, s_m + 32 * warp);
+  bwd_unit(t, c, L, epoch_of(c), u, ud, fo, s_m + 32 * warp);
 }
 
 // ------------------------------------------------------- a5: WNS / TNS
@@ -1159,7 +1221,8 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(Topo t, CornerDev c) {
   block_tree(s_w, s_t);
   if (threadIdx.x == 0) {
     c.res[0] = s_w[0][0]; c.res[1] = s_t[0][0]; c.res[2] = s_w[1][0]; c.res[3] = s_t[1][0];
-    *c.red_cnt = 0;                         // self-reset for the next update
+    c.red_cnt[0] = 0;                        // self-reset for the next update
+    c.red_cnt[1] = 0;                        // backward tail ticket
     const uint32_t e = *c.epoch + 1;         // the next update's record tag (never 0)
     *c.epoch = e ? e : 1;
   }
@@ -1209,12 +1272,10 @@ __global__ void gather_rc_kernel(Topo t, CornerDev c, float* net_load, float* pi
 
 __global__ void init_corner_kernel(CornerDev c, uint32_t n_heavy) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n_heavy) {
-    c.heavy_key[i] = make_int4(f2o(-CUDART_INF_F), f2o(-CUDART_INF_F), f2o(CUDART_INF_F), f2o(CUDART_INF_F));
-    c.heavy_cnt[i] = 0;
-  }
+  if (i < n_heavy) c.heavy_cnt[i] = 0;
   if (i == 0) {
-    *c.red_cnt = 0;
+    c.red_cnt[0] = 0;
+    c.red_cnt[1] = 0;
     *c.err_flag = 0;
     *c.epoch = 1;
   }

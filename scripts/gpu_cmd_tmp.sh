@@ -10,5 +10,5 @@ for nb in ${NBS:-4}; do
   timeout 300 python bench.py --steps 20 --no-cpu-baseline > gpurun_out/bench_${T}_$(echo $nb | tr -dc "0-9_").json 2> gpurun_out/bench_${T}_$(echo $nb | tr -dc "0-9_").err
 done
 python -m paper_2511_11660_b200.build --force > /dev/null 2>&1
-timeout 300 python scripts/trace_run.py c3_superblue /tmp/trace_$T.csv > gpurun_out/trace_$T.txt 2>&1
+STA_TRACE_W=${TW:-5920,3552} timeout 300 python scripts/trace_run.py c3_superblue /tmp/trace_$T.csv > gpurun_out/trace_$T.txt 2>&1
 du -sh gpurun_out/* | sort -h | tail -3

@@ -51,3 +51,21 @@ for kind in ("fwd", "bwd"):
         e = [(int(r["end"]) - int(r["data"])) / 1e3 for r in g]
         print(f"  {s:3d} n={len(g):6d} wait={statistics.median(a):6.2f} ({max(a):6.2f}) load={statistics.median(b):5.2f} "
               f"({max(b):5.2f}) compute={statistics.median(e):5.2f} ({max(e):5.2f})")
+
+# gaps between consecutive units of one warp (warp w runs units w, w + W, ...)
+# STA_TRACE_W = "fwd_warps,bwd_warps" (grid blocks x 8)
+import os
+if os.environ.get("STA_TRACE_W"):
+    wf, wb = (int(x) for x in os.environ["STA_TRACE_W"].split(","))
+    for kind, W in (("fwd", wf), ("bwd", wb)):
+        rs = [r for r in rows if r["kind"] == kind]
+        idx = {int(r["index"]): r for r in rs}
+        gaps = defaultdict(list)
+        for u, r in idx.items():
+            nx = idx.get(u + W)
+            if nx and int(nx["start"]) > 0 and int(r["end"]) > 0:
+                gaps[int(nx["stage"])].append((int(nx["start"]) - int(r["end"])) / 1e3)
+        print(f"{kind} gap before a unit (us), by the unit's stage: median / p90 / max")
+        for s in sorted(gaps)[:: 5 if kind == "fwd" else 1][:40]:
+            g = sorted(gaps[s])
+            print(f"  {s:3d} n={len(g):6d} {g[len(g) // 2]:6.2f} {g[int(len(g) * 0.9)]:6.2f} {g[-1]:7.2f}")
