@@ -72,8 +72,9 @@ def measured_peaks():
 
 
 def algorithmic_bytes(d, info):
-    """Unique bytes each phase must touch per update (DESIGN.md §7): fp32/u32
-    elements counted once per pass."""
+    """Unique bytes each phase must touch per update (DESIGN.md §5): fp32/u32
+    elements counted once per pass, independent of the kernels' layout (the
+    tags, padding and term records the kernels add are not counted)."""
     P, NP, NS = info["num_pins"], info["num_pull_pins"], info["num_sink_pins"]
     E = info["num_cell_arcs"]
     N = info["num_nets"]
@@ -91,6 +92,20 @@ def algorithmic_bytes(d, info):
     return dict(rc=rc, forward=fwd, backward=bwd, reduce=red)
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes (read + write) of one launch of `kernel` from the committed
+    `ncu --set full` summary of the current kernels (profiles/ncu_latest.json,
+    written by scripts/ncu_summary.py), or None."""
+    try:
+        j = json.load(open(os.path.join(ROOT, "profiles", "ncu_latest.json")))
+    except (OSError, ValueError):
+        return None, None
+    for name, k in j.get("kernels", {}).items():
+        if name.startswith(kernel):
+            return k["dram_bytes"], f"profiles/ncu_{j.get('tag')}.json"
+    return None, None
+
+
 class Clocks:
     """nvidia-smi sampling of SM clocks / throttle reasons during the timed region."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -104,7 +119,7 @@ class Clocks:
     def start(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "20"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.p = None
@@ -263,9 +278,12 @@ def main():
         peak, peak_src = measured_peaks()
         dom = max(("forward", "backward"), key=lambda k: ph_ms[k])
         ach = ab[dom] / (ph_ms[dom] / 1e3) / 1e9
-        line["roofline"] = {"bound": "hbm", "kernel": f"{dom} stage kernels (phase)", "achieved": ach,
-                            "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
-                            "peak_source": peak_src, "algorithmic_bytes": ab[dom]}
+        kern = {"forward": "fwd_persistent_kernel", "backward": "bwd_persistent_kernel"}[dom]
+        traffic, tsrc = ncu_traffic(kern)
+        line["roofline"] = {"bound": "hbm", "kernel": kern, "achieved": ach,
+                            "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
+                            "traffic_source": tsrc, "peak_source": peak_src, "algorithmic_bytes": ab[dom],
+                            "kernel_ms": ph_ms[dom]}
         line["phases_ms"] = ph_ms
         line["phases_gbs"] = {k: ab[k] / (ph_ms[k] / 1e3) / 1e9 for k in ab if ph_ms.get(k, 0) > 0}
         whole = sum(ab.values())

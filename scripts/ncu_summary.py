@@ -42,7 +42,8 @@ def num(x):
 
 
 def main():
-    tag, lcsv, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
+    args = [a for a in sys.argv[1:] if a != "--latest"]
+    tag, lcsv, reps = args[0], args[1], args[2:]
     md = [f"# ncu summary {tag}", ""]
     js = {"tag": tag, "kernels": {}}
     if lcsv and os.path.exists(lcsv):
@@ -85,6 +86,8 @@ def main():
     os.makedirs("profiles", exist_ok=True)
     open(f"profiles/ncu_{tag}.md", "w").write("\n".join(md) + "\n")
     json.dump(js, open(f"profiles/ncu_{tag}.json", "w"), indent=1)
+    if "--latest" in sys.argv:
+        json.dump(js, open("profiles/ncu_latest.json", "w"), indent=1)
     print("\n".join(md))
 
 
