@@ -510,6 +510,7 @@ void build_plan(sta_ctx c) {
   for (u32 i = 0; i < NP; ++i)
     for (u32 e = fi_p[i]; e < fi_p[i + 1]; ++e) fi_pin[e] = i;
   const uint4 pad = make_uint4(kNone, kNone, 0, kNone);
+  std::vector<u32> fwu_of_pin(NP, 0);     // forward unit writing each pull pin
   for (u32 s = 0; s < S; ++s) {
     const u32 p0 = c->pull_stage_ptr[s], p1 = c->pull_stage_ptr[s + 1];
     if (s == 0) {                          // seed units: slot = pin
@@ -517,13 +518,21 @@ void build_plan(sta_ctx c) {
         u32 n = 0;
         while (n < sta::kFwdUnitTerms && p + n < p1 && c->user_of_int[p + n] != kNone) ++n;
         if (!n) break;                                  // stage padding
-        for (u32 x = 0; x < sta::kFwdUnitTerms; ++x)
+        for (u32 x = 0; x < sta::kFwdUnitTerms; ++x) {
           fterm.push_back(make_uint4(sta::kSeedMark, 0, 0, x < n ? p + x : kNone));
+          if (x < n) fwu_of_pin[p + x] = (u32)fwu_stage.size();
+        }
         fwu_stage.push_back(s);
       }
       continue;
     }
     const u32 fcap = unit_cap(fi_p[p1] - fi_p[p0], sta::kFwdUnitTerms, fwd_warps);
+    // the stage's units {first pin, first term, terms}, then ordered by the
+    // position of their latest-produced input (units of one stage are
+    // independent): warps take units in list order, so a unit's inputs are
+    // then most likely complete when its warp reaches it
+    std::vector<uint3> su;
+    std::vector<u64> key;
     u32 p = p0;
     while (p < p1) {
       while (p < p1 && fi_p[p + 1] == fi_p[p]) ++p;   // stage padding: no work
@@ -536,7 +545,17 @@ void build_plan(sta_ctx c) {
         items += n;
         ++p;
       }
-      const u32 e0 = fi_p[q0];
+      u32 kmax = 0;
+      for (u32 e = fi_p[q0]; e < fi_p[q0] + items; ++e) kmax = std::max(kmax, fwu_of_pin[fi_src[e]]);
+      key.push_back((u64)kmax << 32 | su.size());
+      su.push_back(make_uint3(q0, fi_p[q0], items));
+    }
+    std::sort(key.begin(), key.end());
+    for (u64 kk : key) {
+      const uint3 un = su[(u32)kk];
+      const u32 q0 = un.x, e0 = un.y, items = un.z;
+      const u32 upos = (u32)fwu_stage.size();
+      for (u32 e = e0; e < e0 + items; ++e) fwu_of_pin[fi_pin[e]] = upos;
       if (items > sta::kFwdUnitTerms) {    // one pin with many terms: the warp loops over fi_*
         // slot 0: {mark, first term, terms, pin}; slot 1: {mark, first delay slot}
         // (the delays of these terms live past the unit slots)
@@ -545,11 +564,10 @@ void build_plan(sta_ctx c) {
         fterm.push_back(make_uint4(sta::kHeavyMark, 0, 0, 0));
         for (u32 x = 2; x < sta::kFwdUnitTerms; ++x) fterm.push_back(make_uint4(sta::kHeavyMark, e0, items, q0));
       } else {
-        // probe term: the one whose source record is produced last (ids are
-        // in stage order)
+        // probe term: the one whose source is produced by the latest unit
         u32 probe = 0;
         for (u32 x = 1; x < items; ++x)
-          if (fi_src[e0 + x] > fi_src[e0 + probe]) probe = x;
+          if (fwu_of_pin[fi_src[e0 + x]] > fwu_of_pin[fi_src[e0 + probe]]) probe = x;
         for (u32 x = 0; x < sta::kFwdUnitTerms; ++x) {
           if (x >= items) {
             fterm.push_back(pad);
@@ -578,19 +596,51 @@ void build_plan(sta_ctx c) {
   c->fwu_stage_ptr.assign(S + 1, 0);
   for (u32 s : fwu_stage) c->fwu_stage_ptr[s + 1]++;
   for (u32 s = 0; s < S; ++s) c->fwu_stage_ptr[s + 1] += c->fwu_stage_ptr[s];
+  // backward units per stage (descending), ordered within a stage by the
+  // position of the latest unit producing a required time they read (units
+  // of one stage are independent), like the forward's
+  std::vector<u32> drv_of_sink(c->NS);
+  for (u32 i = 0; i < NP; ++i)
+    for (u32 x = c->sink_ptr[i]; x < c->sink_ptr[i + 1]; ++x) drv_of_sink[x] = i;
+  std::vector<u32> bwu_of_pin(NP, 0);     // backward unit finishing each pull pin
   c->bwu_stage_lo.assign(S, 0);
   c->bwu_stage_hi.assign(S, 0);
   for (u32 s = S; s-- > 0;) {
     c->bwu_stage_lo[s] = (u32)bwu.size();
+    std::vector<uint4> su;
+    std::vector<u64> key;
+    auto reads_pin = [&](u32 i, u32& kmax) {   // pull pin i's direct fan-out
+      for (u32 f = pfo_p[i]; f < pfo_p[i + 1]; ++f) kmax = std::max(kmax, bwu_of_pin[pfo_dst[f]]);
+    };
     for (u32 x = c->tile_stage_ptr[s]; x < c->tile_stage_ptr[s + 1]; ++x) {
       const u32 k1 = x + 1 < c->tile_stage_ptr[s + 1] ? tiles[x + 1].x : stage_sink_end[s];
-      bwu.push_back(make_uint4(tiles[x].x, k1, tiles[x].y, tile_part[x] == kNone ? 0 : 2 + tile_part[x]));
+      u32 kmax = 0;
+      for (u32 k = tiles[x].x; k < k1; ++k) {
+        for (u32 f = sfo_p[k]; f < sfo_p[k + 1]; ++f) kmax = std::max(kmax, bwu_of_pin[sfo_dst[f]]);
+        if (k == tiles[x].x || drv_of_sink[k] != drv_of_sink[k - 1]) reads_pin(drv_of_sink[k], kmax);
+      }
+      key.push_back((u64)kmax << 32 | su.size());
+      su.push_back(make_uint4(tiles[x].x, k1, tiles[x].y, tile_part[x] == kNone ? 0 : 2 + tile_part[x]));
     }
     const u32 ncap = unit_cap(c->nosink_stage_ptr[s + 1] - c->nosink_stage_ptr[s], sta::kTile, bwd_warps);
     for (u32 x = c->nosink_stage_ptr[s]; x < c->nosink_stage_ptr[s + 1]; x += ncap) {
       const u32 x1 = std::min<u32>(x + ncap, c->nosink_stage_ptr[s + 1]);
       if (nosink[x1 - 1] - nosink[x] != x1 - 1 - x) fail(STA_ERR_ARG, "internal: sink-less pins not contiguous");
-      bwu.push_back(make_uint4(nosink[x], nosink[x1 - 1] + 1, 0, 1));
+      u32 kmax = 0;
+      for (u32 i = nosink[x]; i <= nosink[x1 - 1]; ++i) reads_pin(i, kmax);
+      key.push_back((u64)kmax << 32 | su.size());
+      su.push_back(make_uint4(nosink[x], nosink[x1 - 1] + 1, 0, 1));
+    }
+    std::sort(key.begin(), key.end());
+    for (u64 kk : key) {
+      const uint4 un = su[(u32)kk];
+      const u32 upos = (u32)bwu.size();
+      if (un.w == 1) {
+        for (u32 i = un.x; i < un.y; ++i) bwu_of_pin[i] = upos;
+      } else {
+        for (u32 k = un.x; k < un.y; ++k) bwu_of_pin[drv_of_sink[k]] = std::max(bwu_of_pin[drv_of_sink[k]], upos);
+      }
+      bwu.push_back(un);
     }
     c->bwu_stage_hi[s] = (u32)bwu.size();
   }
