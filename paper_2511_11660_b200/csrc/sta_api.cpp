@@ -564,10 +564,6 @@ void build_plan(sta_ctx c) {
         fterm.push_back(make_uint4(sta::kHeavyMark, 0, 0, 0));
         for (u32 x = 2; x < sta::kFwdUnitTerms; ++x) fterm.push_back(make_uint4(sta::kHeavyMark, e0, items, q0));
       } else {
-        // probe term: the one whose source is produced by the latest unit
-        u32 probe = 0;
-        for (u32 x = 1; x < items; ++x)
-          if (fwu_of_pin[fi_src[e0 + x]] > fwu_of_pin[fi_src[e0 + probe]]) probe = x;
         for (u32 x = 0; x < sta::kFwdUnitTerms; ++x) {
           if (x >= items) {
             fterm.push_back(pad);
@@ -576,7 +572,7 @@ void build_plan(sta_ctx c) {
           const u32 e = e0 + x;
           if (fi_info[e] >> 31) fail(STA_ERR_LUT, "table id too large for the forward plan");
           term_slot[e] = (u32)fterm.size();
-          fterm.push_back(make_uint4(fi_src[e], fi_hop[e], fi_info[e] | (x == probe ? 0x80000000u : 0u), fi_pin[e]));
+          fterm.push_back(make_uint4(fi_src[e], fi_hop[e], fi_info[e], fi_pin[e]));
         }
       }
       fwu_stage.push_back(s);

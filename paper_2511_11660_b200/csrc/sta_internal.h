@@ -82,8 +82,8 @@ struct Topo {
   const uint32_t* heavy_base;   // [n_heavy] first partial slot of each heavy driver
   // propagation work units (sta_kernels.cu), lists in dependency order
   // forward warp unit u = term slots [kFwdUnitTerms u, kFwdUnitTerms (u + 1)):
-  //   {src, hop, info | probe << 31, pin}: a fan-in term of pull pin `pin`
-  //     (record src, sink hop or kNone); probe: the slot polled first
+  //   {src, hop, info, pin}: a fan-in term of pull pin `pin` (record src,
+  //     sink hop or kNone, sense | table << 3)
   //   {kNone, kNone, 0, kNone}: padding
   //   {kSeedMark, 0, 0, pin or kNone}: stage-0 pin (seed)
   //   {kHeavyMark, term0, nterms, pin} in every slot but slot 1 = {kHeavyMark,

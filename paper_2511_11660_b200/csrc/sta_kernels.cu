@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) tc_persistent_kernel(Topo t, Co
 //     warp per unit; the tags are then always valid on first read.
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 
-// STA_TRACE: {start, inputs' producers seen (probe), inputs loaded, end} of a unit
+// STA_TRACE: {start, ready (forward: before the inputs are polled), inputs loaded, end} of a unit
 __device__ __forceinline__ void trace_unit(const CornerDev& c, size_t q, unsigned long long t0,
                                            unsigned long long t1, unsigned long long t2 = 0) {
   if (c.trace && (threadIdx.x & 31) == 0) {
@@ -656,9 +656,9 @@ __device__ __forceinline__ void combine(Q4& a, const Q4& b) {
 // input, looks up delay[orf] and slew[orf] (bit-identical to the backward's
 // recomputation: same seg / interp calls on the same operands), and the first
 // term of each pin merges its pin's candidates by shuffles and writes word q
-// of the pin's record.  Before the lanes load, one probe lane (the plan's
-// choice: the term whose source was produced last) polls alone with backoff,
-// so warps running ahead of the wavefront cost one L2 sector per poll.
+// of the pin's record.  (A single "probe" lane polling first, to spare L2
+// sectors while a warp runs ahead of the wavefront, measured slower once the
+// units of a stage are ordered by readiness.)
 // (Four lanes per term keep the per-lane dependent chain short: the forward
 // wavefront's stage-to-stage latency is that chain.)
 constexpr uint32_t kFwdTerms = kFwdUnitTerms;
@@ -734,12 +734,10 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
   }
   if (kind != kHeavyMark) {
     const bool item = tr.x != kNone;
-    const uint32_t src = tr.x, info = tr.z & 0x7FFFFFFFu, v = tr.w;
+    const uint32_t src = tr.x, info = tr.z, v = tr.w;
     const float elm = rc.elm, ld = rc.ld;
     const int irf = primary_irf(info & 7u, orf);
     const uint4* wp = c.rec + 4 * (size_t)src + (el * 2 + irf);
-    if ((tr.z >> 31) && q == 3) spin_ll(wp, ep);   // probe
-    __syncwarp();
     if (c.trace && lane == 0) t_ready = gtimer();
     float ca = undef, cs = undef;
     if (item) {
