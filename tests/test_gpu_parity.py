@@ -205,3 +205,89 @@ def test_stage_kernels_equal_persistent_kernels(sta):
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
     assert np.array_equal(ra[0], rb[0]) and np.array_equal(ra[1], rb[1])
+
+
+def _wide_multi_output_design(width=12, depth=3, seed=3):
+    """Cells the synthetic recipe never makes: a `width`-input gate (one pin
+    with more fan-in terms than a forward warp unit holds -> the warp-loop
+    path) and two-output full adders (an input pin with three fan-out terms
+    -> the backward's CSR path beyond the two inline terms), chained `depth`
+    times, with PIs driving several sinks."""
+    import copy
+    from synth.design import (ROLE_PI, ROLE_PO, SENSE_NEG, SENSE_NON, SENSE_POS, affine_table)
+    from synth.hand import AFFINE_LOAD, AFFINE_SLEW, Builder, _cons
+    rng = np.random.default_rng(seed)
+    b = Builder()
+
+    def tabs():
+        return b.tables4([affine_table(AFFINE_SLEW, AFFINE_LOAD, *rng.uniform([4, 0.05, 0.5], [15, 0.3, 3]))
+                          for _ in range(4)])
+    pis = [f"i{k}" for k in range(width)]
+    for n in pis:
+        b.pin(n, 0.0, ROLE_PI)
+    sinks_of = {n: [] for n in pis}
+    prev = list(pis)
+    for lvl in range(depth):
+        W = f"W{lvl}"
+        for k in range(width):
+            b.pin(f"{W}/a{k}", float(rng.uniform(0.5, 2)))
+        b.pin(f"{W}/y")
+        for k in range(width):
+            b.arc(f"{W}/a{k}", f"{W}/y", [SENSE_NEG, SENSE_NON, SENSE_POS][k % 3], tabs())
+            sinks_of.setdefault(prev[k % len(prev)], []).append(f"{W}/a{k}")
+        F = f"F{lvl}"
+        for p in ("a", "b", "c"):
+            b.pin(f"{F}/{p}", float(rng.uniform(0.5, 2)))
+        b.pin(f"{F}/s")
+        b.pin(f"{F}/co")
+        for p in ("a", "b", "c"):
+            b.arc(f"{F}/{p}", f"{F}/s", SENSE_NON, tabs())
+            b.arc(f"{F}/{p}", f"{F}/co", SENSE_POS, tabs())
+        sinks_of.setdefault(f"{W}/y", []).append(f"{F}/a")
+        sinks_of[pis[lvl % width]].append(f"{F}/b")
+        sinks_of.setdefault(prev[(lvl + 1) % len(prev)], []).append(f"{F}/c")
+        prev = [f"{W}/y", f"{F}/s", f"{F}/co"] + pis[3:]
+    pos = []
+    for k, n in enumerate(prev[:3]):
+        po = f"o{k}"
+        b.pin(po, 0.0, ROLE_PO)
+        sinks_of.setdefault(n, []).append(po)
+        pos.append((po, [float(rng.uniform(0, 20))] * 2, [0.0, 0.0], 1.5))
+    for drv, sk in sinks_of.items():
+        if sk:
+            b.net(drv, sk, b.star_rc(drv, sk, float(rng.uniform(0.05, 0.3)), float(rng.uniform(0.1, 1.0))))
+    cons = _cons(b, 400.0, 20.0, [(n, [0, 0, 0, 0], [10, 12, 10, 12]) for n in pis], pos)
+    return b.build(cons, name="wide_multi_output")
+
+
+@pytest.mark.parametrize("mode", ["0", "1"])
+def test_wide_gates_and_multi_output_cells(sta, mode):
+    """Forward warp-loop path (> 8 fan-in terms on one pin) and the backward's
+    CSR fan-out path (> 2 fan-out terms on one pin), both launchers."""
+    d = _wide_multi_output_design()
+    os.environ["STA_STAGE_KERNELS"] = mode
+    try:
+        ctx = run(sta, d)
+    finally:
+        os.environ.pop("STA_STAGE_KERNELS", None)
+    compare_update(ctx, oracle.update(d))
+    check_levels(ctx, d)
+    ctx.close()
+
+
+def test_repeated_updates_with_changing_rc(sta):
+    """An optimization loop (C4 pattern): RC values re-set between updates,
+    every update compared with the oracle -- the tagged records of one update
+    must never be taken for the next one's."""
+    d = synth.generate(8000, 40, seed=12, n_hfn=2, hfn_range=(200, 3000), period=300.0)
+    ctx = sta.Context(0, 1)
+    sta.load_design(ctx, d)
+    import copy
+    for i, (rs, cs) in enumerate([(1.0, 1.0), (1.3, 0.8), (0.7, 1.25), (1.0, 1.0)]):
+        di = copy.copy(d)
+        di.rc = [d.rc[0].scaled(rs, cs)]
+        ctx.set_rc_values(0, di.rc[0].res, di.rc[0].cap)
+        ctx.update_timing()
+        ctx.synchronize()
+        compare_update(ctx, oracle.update(di))
+    ctx.close()
