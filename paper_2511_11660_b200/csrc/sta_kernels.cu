@@ -751,10 +751,12 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
     }
     // merge the pin's terms into its first term's lanes (same q); a pin's
     // terms occupy consecutive slots
+    // (log-step doubling over term slots; min / max are idempotent, so the
+    // overlapping windows are harmless)
     const uint32_t peers = __match_any_sync(kFull, item ? v : kNone);
     const uint32_t head_tl = (uint32_t)(__ffs(peers) - 1) >> 2, end_tl = (uint32_t)(31 - __clz(peers)) >> 2;
 #pragma unroll
-    for (uint32_t j = 1; j < kFwdTerms; ++j) {
+    for (uint32_t j = 1; j < kFwdTerms; j <<= 1) {
       const float oa = __shfl_down_sync(kFull, ca, 4 * j);
       const float os = __shfl_down_sync(kFull, cs, 4 * j);
       if (tl + j <= end_tl) {
