@@ -1027,15 +1027,19 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
       for (int q = 0; q < 4; ++q)            // through the net arc (edges the forward used)
         if (fin(at_v.v[q])) acc.v[q] = __fsub_rn(r.v[q], elm);
     }
-    // the first lane of each driver merges the driver's sinks (contiguous)
-    sm[lane] = to_f4(acc);
+    // merge the sinks of each driver (contiguous lanes) into its first lane:
+    // log-step doubling (max / min are idempotent: overlapping windows are
+    // harmless); a loop over the run measured 18% of the kernel's
+    // instructions on heavy tiles
     const uint32_t peers = __match_any_sync(kFull, v);
-    __syncwarp();
-    if (head) {
-      const uint32_t end = 31 - __clz(peers);
-      for (uint32_t j = lane + 1; j <= end; ++j) combine(acc, to_q(sm[j]));
+    const uint32_t end = 31 - __clz(peers);
+#pragma unroll
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+      Q4 b;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) b.v[q] = __shfl_down_sync(kFull, acc.v[q], o);
+      if (lane + o <= end) combine(acc, b);
     }
-    __syncwarp();
     if (ud.z != kNone) {                      // heavy driver: every lane is v
       // partial of this tile, then a release increment of the driver's tile
       // counter (one atomic per tile); the last tile combines all partials
