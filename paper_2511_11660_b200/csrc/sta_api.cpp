@@ -325,16 +325,26 @@ void build_plan(sta_ctx c) {
   c->int_of_user.assign(P, kNone);
   c->user_of_int.assign(c->Pi, kNone);
   {
-    // within a stage: drivers of nets with sinks first, then sink-less pins
-    // (each class by user id), so the backward's sink-less units are ranges
+    // within a stage: drivers of nets with an endpoint sink (PO / check data
+    // pin), other drivers of nets with sinks, then sink-less pins (each
+    // class by user id): the backward's sink-less units are ranges, and its
+    // endpoint-seed lookups (divergent work) concentrate in few warps
     std::vector<u32> fill(c->pull_stage_ptr.begin(), c->pull_stage_ptr.end());
-    auto has_sinks = [&](u32 p) {
+    auto pin_class = [&](u32 p) {
       const u32 n = c->pin_net[p];
-      return n != kNone && c->net_ptr[n + 1] - c->net_ptr[n] > 1;
+      if (n == kNone || c->net_ptr[n + 1] - c->net_ptr[n] <= 1) return 2;
+      for (u32 x = c->net_ptr[n] + 1; x < c->net_ptr[n + 1]; ++x) {
+        const u32 q = c->net_pins[x];
+        if (c->pin_role[q] == STA_PIN_PO || c->pin_role[q] == STA_PIN_FF_D || c->chk_of_pin[q] != kNone) return 0;
+      }
+      return 1;
     };
-    for (int pass = 0; pass < 2; ++pass)
+    std::vector<uint8_t> cls(P, 0);
+    for (u32 p = 0; p < P; ++p)
+      if (!c->is_sink[p]) cls[p] = (uint8_t)pin_class(p);
+    for (int pass = 0; pass < 3; ++pass)
       for (u32 p = 0; p < P; ++p)
-      if (!c->is_sink[p] && has_sinks(p) == (pass == 0)) {
+      if (!c->is_sink[p] && cls[p] == pass) {
         const u32 i = fill[c->stage[p]]++;
         c->int_of_user[p] = i;
         c->user_of_int[i] = p;
