@@ -459,8 +459,10 @@ __device__ __forceinline__ double tc_block_offset(const double* sums, uint32_t b
 // Device-wide prefix scan of x, whose block range [lo, hi) the block wrote
 // with the strided mapping i = lo + threadIdx.x + k blockDim.x, each thread
 // also accumulating `part` (its values in that order).  Block sums, grid
-// barrier, offsets, then one block-wide scan per row of blockDim.x values.
-// Returns the inclusive prefix at hi.
+// barrier, offsets, then within the block: each thread sums a contiguous
+// chunk, one block-wide scan of the chunk sums, each thread rescans its chunk
+// (one block scan instead of one per row of blockDim.x values).  Fixed
+// shapes: bitwise reproducible.  Returns the inclusive prefix at hi.
 template <bool INCLUSIVE>
 __device__ __forceinline__ double tc_scan_range(double* x, size_t lo, size_t hi, double part, double* sums,
                                                 uint32_t* bar, double* s_warp, double* s_red) {
@@ -472,16 +474,24 @@ __device__ __forceinline__ double tc_scan_range(double* x, size_t lo, size_t hi,
   }
   if (threadIdx.x == 0) sums[blockIdx.x] = s_red[0];
   tc_grid_barrier(bar, gridDim.x);
-  double carry = tc_block_offset(sums, blockIdx.x, s_red);
-  for (size_t r0 = lo; r0 < hi; r0 += blockDim.x) {
-    const size_t i = r0 + threadIdx.x;
-    const double v = i < hi ? x[i] : 0.0;      // own write (same mapping)
-    double tot;
-    const double e = block_excl_scan(v, s_warp, &tot);
-    if (i < hi) x[i] = carry + (INCLUSIVE ? e + v : e);
-    carry += tot;
+  const double off = tc_block_offset(sums, blockIdx.x, s_red);
+  const size_t n = hi - lo, K = (n + blockDim.x - 1) / blockDim.x;
+  const size_t a = lo + min(n, (size_t)threadIdx.x * K), b = lo + min(n, (size_t)(threadIdx.x + 1) * K);
+  double csum = 0.0;
+  for (size_t i = a; i < b; ++i) csum += x[i];    // the block's own writes (barrier above)
+  double tot;
+  double carry = off + block_excl_scan(csum, s_warp, &tot);
+  for (size_t i = a; i < b; ++i) {
+    const double v = x[i];
+    if (INCLUSIVE) {
+      carry += v;
+      x[i] = carry;
+    } else {
+      x[i] = carry;
+      carry += v;
+    }
   }
-  return carry;
+  return off + tot;
 }
 
 __global__ void __launch_bounds__(kTcThreads, 2) tc_persistent_kernel(Topo t, CornerDev c) {
@@ -1332,7 +1342,10 @@ cudaError_t launch_rc_tierC(const Topo& t, const CornerDev& c, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tc_persistent_kernel, kTcThreads, 0);
-    grid = (uint32_t)std::min<int>(std::max(nb, 0) * sms, (int)kTcMaxGrid);
+    // one block per SM: the small-net RC kernels on the main stream need the
+    // rest of the register file to run beside it (two blocks per SM filled
+    // it and serialised the two)
+    grid = (uint32_t)std::min<int>(std::min(std::max(nb, 0), 1) * sms, (int)kTcMaxGrid);
     if (!grid) return cudaErrorCooperativeLaunchTooLarge;
   }
   cudaLaunchConfig_t cfg = {};
