@@ -210,12 +210,14 @@ def main():
     ctx.set_rc_values(0, res_d, cap_d)
     rows = torch.zeros((world, 4), dtype=torch.float64, device="cuda")
 
+    from paper_2511_11660_b200 import multicorner as mc
+
     def step():
         ctx.update_timing()
         if world > 1:
             rows.zero_()
             ctx.report_wns_tns_device(0, rows[rank])
-            dist.all_reduce(rows)          # one NCCL allreduce of the per-corner rows
+            mc.combine_rows(rows)          # one NCCL allreduce of the per-corner rows
 
     def barrier():
         torch.cuda.synchronize()
@@ -246,8 +248,7 @@ def main():
     res_global = None
     res_own, _ = ctx.report_slack(0)
     if world > 1:
-        r = rows.cpu().numpy()
-        res_global = [float(r[:, 0].min()), float(r[:, 1].sum()), float(r[:, 2].min()), float(r[:, 3].sum())]
+        res_global = [float(x) for x in mc.global_report(rows.cpu())]
 
     line = {"metric": METRIC, "value": value, "unit": "pins/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
