@@ -36,7 +36,7 @@ CONFIG = "c3_superblue"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=CONFIG)
@@ -115,8 +115,10 @@ class Clocks:
     def __init__(self, index):
         self.index = index
         self.p = None
+        self.t0 = None
 
     def start(self):
+        self.t0 = time.time()
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "20"],
@@ -124,9 +126,12 @@ class Clocks:
         except OSError:
             self.p = None
 
-    def stop(self):
+    def stop(self, since=None):
+        """Stop sampling; keep the samples taken after wall time `since` (the
+        start of the timed region), or the last one if none was."""
         if not self.p:
             return None
+        t_stop = time.time()
         self.p.terminate()
         try:
             out, _ = self.p.communicate(timeout=5)
@@ -134,6 +139,10 @@ class Clocks:
             self.p.kill()
             out, _ = self.p.communicate()
         rows = [r.split(",") for r in out.strip().splitlines() if r.count(",") >= 8]
+        if since is not None and rows and self.t0:
+            # samples are -lms 20 apart, the first at about self.t0
+            n_keep = max(1, int((t_stop - since) / 0.02) + 1)
+            rows = rows[-n_keep:]
         if not rows:
             return None
         sm = [float(r[1]) for r in rows]
@@ -225,18 +234,22 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # the clock sampler starts before the warm-up so that it is running (not
+    # still spawning) during the timed region
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
     for _ in range(max(args.warmup, 3) if args.warmup else 0):
         step()
     barrier()
-    clocks = Clocks(local)
-    clocks.start()
+    tc0 = time.time()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
         step()
     e1.record(stream)
     barrier()
-    clk = clocks.stop()
+    clk = clocks.stop(since=tc0)
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
