@@ -31,7 +31,7 @@ constexpr uint32_t kFwdUnitTerms = 8;          // forward warp unit: fan-in term
 // tuned on C3: the forward's short per-lane chains want many warps, the
 // backward's one-lane-per-sink chains want registers)
 #ifndef STA_FWD_BLOCKS
-#define STA_FWD_BLOCKS 5
+#define STA_FWD_BLOCKS 4
 #endif
 #ifndef STA_BWD_BLOCKS
 #define STA_BWD_BLOCKS 2

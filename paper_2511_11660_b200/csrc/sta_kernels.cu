@@ -673,18 +673,33 @@ __device__ __forceinline__ void combine(Q4& a, const Q4& b) {
 // wavefront's stage-to-stage latency is that chain.)
 constexpr uint32_t kFwdTerms = kFwdUnitTerms;
 
-__device__ __forceinline__ void fwd_lane(const float* __restrict__ L, uint32_t info, int el, int orf, float ld,
-                                         float a_in, float s_in, float& ca, float& cs, float& dl) {
+// The lookup of delay[orf] / slew[orf] in two halves: the part that does not
+// depend on the input arrival (table records, load-axis segments) runs before
+// the lane waits for its producer, so only the slew-axis search and the
+// interpolations remain on the critical path after the data arrives.
+struct FwdTabs {
+  Tab rd, rs;       // cell_rise / cell_fall, rise / fall transition of orf
+  Seg cd, cc;       // their load-axis segments
+  bool same;        // one axis template for both
+};
+
+__device__ __forceinline__ FwdTabs fwd_tabs(const float* __restrict__ L, uint32_t info, int orf, float ld) {
+  FwdTabs f;
   const uint32_t tab = info >> 3;
-  const Tab rd = tab_rec(L, tab + orf);          // cell_rise / cell_fall
-  const Tab rs = tab_rec(L, tab + 2 + orf);      // rise / fall transition
-  const bool same = rs.ax == rd.ax;
-  const Seg cd = seg(rd.ax + 24, ld);
-  const Seg cc = same ? cd : seg(rs.ax + 24, ld);
-  const Seg sd = seg(rd.ax, s_in);
-  const Seg ss = same ? sd : seg(rs.ax, s_in);
-  const float d = fmaxf(0.f, interp(rd, sd, cd));
-  const float so = fmaxf(0.f, interp(rs, ss, cc));
+  f.rd = tab_rec(L, tab + orf);
+  f.rs = tab_rec(L, tab + 2 + orf);
+  f.same = f.rs.ax == f.rd.ax;
+  f.cd = seg(f.rd.ax + 24, ld);
+  f.cc = f.same ? f.cd : seg(f.rs.ax + 24, ld);
+  return f;
+}
+
+__device__ __forceinline__ void fwd_lane(const FwdTabs& f, int el, float a_in, float s_in, float& ca, float& cs,
+                                         float& dl) {
+  const Seg sd = seg(f.rd.ax, s_in);
+  const Seg ss = f.same ? sd : seg(f.rs.ax, s_in);
+  const float d = fmaxf(0.f, interp(f.rd, sd, f.cd));
+  const float so = fmaxf(0.f, interp(f.rs, ss, f.cc));
   const bool ok = fin(a_in);
   const float undef = el ? -CUDART_INF_F : CUDART_INF_F;
   ca = ok ? __fadd_rn(a_in, d) : undef;
@@ -751,12 +766,13 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
     if (c.trace && lane == 0) t_ready = gtimer();
     float ca = undef, cs = undef;
     if (item) {
+      const FwdTabs f = fwd_tabs(L, info, orf, ld);   // before waiting for the producer
       const uint4 w = spin_ll(wp, ep);
       if (c.trace) t_data = gtimer();
       float a_in = __uint_as_float(w.x), s_in = __uint_as_float(w.z);
       if (tr.y != kNone) hop_q(a_in, s_in, elm);
       float dl;
-      fwd_lane(L, info, el, orf, ld, a_in, s_in, ca, cs, dl);
+      fwd_lane(f, el, a_in, s_in, ca, cs, dl);
       reinterpret_cast<float*>(c.tdel + (size_t)kFwdTerms * u + tl)[q] = dl;
     }
     // merge the pin's terms into its first term's lanes (same q); a pin's
@@ -784,11 +800,12 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
       const uint32_t e = e0 + b;
       const uint32_t info = t.fi_info[e], h = t.fi_hop[e];
       const int irf = primary_irf(info & 7u, orf);
+      const FwdTabs f = fwd_tabs(L, info, orf, ld);
       const uint4 w = spin_ll(c.rec + 4 * (size_t)t.fi_src[e] + (el * 2 + irf), ep);
       float a_in = __uint_as_float(w.x), s_in = __uint_as_float(w.z);
       if (h != kNone) hop_q(a_in, s_in, __ldcg(c.elm + h));
       float oa, os, dl;
-      fwd_lane(L, info, el, orf, ld, a_in, s_in, oa, os, dl);
+      fwd_lane(f, el, a_in, s_in, oa, os, dl);
       reinterpret_cast<float*>(c.tdel + dbase + b)[q] = dl;
       merge_q(ca, oa, el);
       merge_q(cs, os, el);
