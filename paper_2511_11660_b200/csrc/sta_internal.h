@@ -38,6 +38,9 @@ constexpr uint32_t kFwdUnitTerms = 8;          // forward warp unit: fan-in term
 #endif
 constexpr int kFwdMinBlocks = STA_FWD_BLOCKS;
 constexpr int kBwdMinBlocks = STA_BWD_BLOCKS;
+#ifndef STA_BWD_PIPE
+#define STA_BWD_PIPE 1                          // backward: prefetch the next unit's fan-out records
+#endif
 
 // Device NLDM table pool (built by sta_set_library), shared-memory friendly:
 //   * table t: a block of kTabStride = 65 floats at t * 65: word 0 = offset

@@ -1143,6 +1143,26 @@ __global__ void __launch_bounds__(kThreads, kBwdMinBlocks) bwd_persistent_kernel
   // static units at different times, and a static split of the tail would
   // leave the stragglers' share waiting for them.
   const uint32_t ns = t.n_bwu_static, lane = threadIdx.x & 31;
+#if STA_BWD_PIPE == 0
+  // (variant: no fan-out record prefetch, fewer registers)
+  for (;;) {
+    if (u >= ns) {
+      uint32_t x = 0;
+      if (lane == 0) x = atomicAdd(c.red_cnt + 1, 1u);
+      u = ns + __shfl_sync(kFull, x, 0);
+      if (u >= t.n_bwu) break;
+      ud = __ldg(t.bwu + u);
+      bwd_unit(t, c, L, ep, u, ud, bwd_fo(t, ud), s_m + 32 * warp);
+      continue;
+    }
+    const uint4 nu = u + W < ns ? __ldg(t.bwu + u + W) : none;
+    bwd_unit(t, c, L, ep, u, ud, bwd_fo(t, ud), s_m + 32 * warp);
+    u += W;
+    ud = nu;
+  }
+  (void)fo;
+  (void)nx;
+#else
   for (;;) {
     SinkFo nfo = fo;
     uint4 nnx = none;
@@ -1166,6 +1186,7 @@ __global__ void __launch_bounds__(kThreads, kBwdMinBlocks) bwd_persistent_kernel
       nx = nnx;
     }
   }
+#endif
 }
 
 template <bool SMEM_LUT>
