@@ -141,6 +141,8 @@ struct sta_ctx_s {
   u32 n_rc = 0;
   u32 big_total = 0;              // tier-C nodes
   std::vector<u32> node_user;     // internal RC node -> caller node id
+  std::vector<u32> node_meta_h, node_tag_h;   // host copies (packed node records, prepare())
+  u32 n_rc_ab = 0;                // internal RC nodes of tiers A and B (they come first)
   std::vector<u32> rc_net_j;      // net j (driver order) -> internal driver id
 
   // ---- constraints (host)
@@ -868,6 +870,9 @@ void build_rc(sta_ctx c) {
   t.node_user = g.upload(node_user, s);
   t.node_meta = g.upload(node_meta, s);
   t.node_tag = g.upload(node_tag, s);
+  c->node_meta_h = node_meta;
+  c->node_tag_h = node_tag;
+  c->n_rc_ab = nA + nB;
   t.n_wtiles = (u32)wtiles.size();
   t.wtiles = g.upload(wtiles, s);
   t.n_btiles = (u32)btiles.size();
@@ -981,6 +986,15 @@ void prepare(sta_ctx c) {
   t.clock_slew = c->clock_slew;
   t.rc_scap = g.upload(scap, s);
   t.net_lumped = g.upload(lumped, s);
+  {   // packed per-node records of the small-net RC kernels (tiers A and B)
+    std::vector<uint4> nodes(c->n_rc_ab);
+    for (u32 x = 0; x < c->n_rc_ab; ++x) {
+      u32 sc;
+      std::memcpy(&sc, &scap[x], 4);
+      nodes[x] = make_uint4(c->node_meta_h[x], c->node_tag_h[x], c->node_user[x], sc);
+    }
+    t.rc_node = g.upload(nodes, s);
+  }
 
   // per-corner state buffers
   for (CornerState& cs : c->corners) {

@@ -128,6 +128,7 @@ struct Topo {
   const uint32_t* node_meta; // [n_rc] pos | parent pos << 8 (0xFF: root) | end << 16 (nets <= 32 nodes)
   const uint32_t* node_tag;  // [n_rc] sink index, driver | 0x80000000 at the root, or kNone
   const float* rc_scap;      // [n_rc] pin cap + PO load at the node
+  const uint4* rc_node;      // [tier A + B nodes] {node_meta, node_tag, node_user, rc_scap bits} packed
   uint32_t n_wtiles;         // warp tiles of nets with 1..32 nodes (no net straddles a tile)
   const uint2* wtiles;       // {first internal node, node count}
   // tier B: nets with 33..kBNet nodes, whole nets in block tiles of <= kBNet

@@ -223,14 +223,14 @@ __global__ void __launch_bounds__(kThreads) rc_warp_kernel(Topo t, CornerDev c) 
   float r = 0.f;
   bool bad = false;
   if (act) {
-    meta = t.node_meta[x];
-    tag = t.node_tag[x];
-    const uint32_t u = t.node_user[x];
-    const float cw = c.rc_vals[1][u];
+    const uint4 nd = __ldg(t.rc_node + x);   // {meta, tag, caller node, static cap}
+    meta = nd.x;
+    tag = nd.y;
+    const float cw = c.rc_vals[1][nd.z];
     const bool root = ((meta >> 8) & 0xFFu) == 0xFFu;
-    r = root ? 0.f : c.rc_vals[0][u];
+    r = root ? 0.f : c.rc_vals[0][nd.z];
     bad = bad_rc(r, cw);
-    C = (double)cw + (double)t.rc_scap[x];
+    C = (double)cw + (double)__uint_as_float(nd.w);
   }
   const int pos = (int)(meta & 0xFFu), ppos = (int)((meta >> 8) & 0xFFu), epos = (int)((meta >> 16) & 0xFFu);
   // segmented inclusive scan of C (a net's lanes are contiguous; pos resets)
@@ -317,13 +317,13 @@ __global__ void __launch_bounds__(kThreads) rc_block_kernel(Topo t, CornerDev c)
     meta[k] = 0; tag[k] = kNone; C[k] = 0.0; r[k] = 0.f;
     if (i < tile.y) {
       const uint32_t x = tile.x + i;
-      meta[k] = t.node_meta[x];
-      tag[k] = t.node_tag[x];
-      const uint32_t u = t.node_user[x];
-      const float cw = c.rc_vals[1][u];
-      r[k] = ((meta[k] >> 10) & 0x7FFu) == 0x7FFu ? 0.f : c.rc_vals[0][u];
+      const uint4 nd = __ldg(t.rc_node + x); // {meta, tag, caller node, static cap}
+      meta[k] = nd.x;
+      tag[k] = nd.y;
+      const float cw = c.rc_vals[1][nd.z];
+      r[k] = ((meta[k] >> 10) & 0x7FFu) == 0x7FFu ? 0.f : c.rc_vals[0][nd.z];
       bad |= bad_rc(r[k], cw);
-      C[k] = (double)cw + (double)t.rc_scap[x];
+      C[k] = (double)cw + (double)__uint_as_float(nd.w);
     }
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(c.err_flag, 1u);
