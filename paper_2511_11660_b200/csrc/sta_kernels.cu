@@ -418,6 +418,9 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
 //   4. elm(g) = H[enter(g)] - H[2 g0 - 1].
 // Offsets are fixed-shape sums of the block sums: bitwise reproducible.
 constexpr int kTcThreads = 512;
+#ifndef STA_TC_BLOCKS
+#define STA_TC_BLOCKS 1                      // blocks per SM of the tier-C kernel
+#endif
 constexpr int kTcBatch = 4;                  // elements in flight per thread
 
 __device__ __forceinline__ void tc_grid_barrier(uint32_t* bar, uint32_t nblocks) {
@@ -478,9 +481,11 @@ __device__ __forceinline__ double tc_scan_range(double* x, size_t lo, size_t hi,
   const size_t n = hi - lo, K = (n + blockDim.x - 1) / blockDim.x;
   const size_t a = lo + min(n, (size_t)threadIdx.x * K), b = lo + min(n, (size_t)(threadIdx.x + 1) * K);
   double csum = 0.0;
+#pragma unroll 8
   for (size_t i = a; i < b; ++i) csum += x[i];    // the block's own writes (barrier above)
   double tot;
   double carry = off + block_excl_scan(csum, s_warp, &tot);
+#pragma unroll 8
   for (size_t i = a; i < b; ++i) {
     const double v = x[i];
     if (INCLUSIVE) {
@@ -1383,7 +1388,7 @@ cudaError_t launch_rc_tierC(const Topo& t, const CornerDev& c, cudaStream_t s) {
     // one block per SM: the small-net RC kernels on the main stream need the
     // rest of the register file to run beside it (two blocks per SM filled
     // it and serialised the two)
-    grid = (uint32_t)std::min<int>(std::min(std::max(nb, 0), 1) * sms, (int)kTcMaxGrid);
+    grid = (uint32_t)std::min<int>(std::min(std::max(nb, 0), STA_TC_BLOCKS) * sms, (int)kTcMaxGrid);
     if (!grid) return cudaErrorCooperativeLaunchTooLarge;
   }
   cudaLaunchConfig_t cfg = {};
