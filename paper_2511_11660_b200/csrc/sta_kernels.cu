@@ -1,31 +1,28 @@
 // sta_kernels.cu -- sm_100a kernels of one graph-based STA timing update.
 //
-// Hot path (SURVEY.md §8(a), DESIGN.md §5):
-//   a1  rc_warp_kernel / tc_* + scan_*   Elmore RC per net in fp64: Cdown
-//       (subtree caps), load = Cdown[root], Elmore = sum of R Cdown over the
-//       root path, from each net's DFS
-//       preorder: warp shuffle scans for nets <= 32 nodes, device-wide prefix
-//       sums (Euler tour) for larger nets.
-//   a2  seed_kernel + fwd_stage_kernel   arrival/slew, one launch per gate
-//       stage, one thread per stage pin; NLDM bilinear lookup for cell arcs
+// Hot path (SURVEY.md §8(a), DESIGN.md §4):
+//   a1  rc_warp_kernel / rc_block_kernel / rc_lumped_kernel / tc_persistent_kernel
+//       Elmore RC per net in fp64: Cdown (subtree caps), load = Cdown[root],
+//       Elmore = sum of R Cdown over the root path (
+//       SPEC.md:389-397), from each net's DFS preorder: warp shuffle scans for
+//       nets <= 32 nodes, block tiles up to 1024 nodes, device-wide Euler-tour
+//       prefix sums for larger (high-fan-out) nets.
+//   a2  fwd_persistent_kernel (or fwd_stage_kernel, one launch per stage)
+//       arrival / slew by gate stage: NLDM bilinear lookup for cell arcs
 //       (SPEC.md:371-388), Elmore + PERI slew for net arcs
-//       (SPEC.md:416-418), early-min / late-max merge.
-//   a3-a5 bwd_stage_kernel   endpoint seeds, required
-//       times over the fan-out (late min / early max), per-pin slack and
-//       per-endpoint worst slack; one launch per gate stage in reverse; one
-//       warp per tile of <= 32 consecutive sinks, segmented shuffle reduction
-//       into their drivers, ordered-int atomics only for drivers with more
-//       than 32 sinks.
+//       (SPEC.md:416-418), early-min / late-max merge;
+//       warp work units, four lanes per fan-in term, tagged records.
+//   a3-a5 bwd_persistent_kernel (or bwd_stage_kernel)   endpoint seeds
+//       (SPEC.md:509, 548), required times over the fan-out with the delays
+//       the forward stored (late min / early max), per-pin slack and
+//       per-endpoint worst slack; one lane per sink, segmented shuffle merge
+//       into the drivers, per-tile partials for drivers with > 32 sinks.
 //   a5  reduce_kernel   WNS / TNS (TNS in fp64), fixed-order two-level tree.
 //
-// All stage kernels are launched with programmatic dependent launch: the
-// static topology of a stage is read before griddepcontrol.wait, so it
-// overlaps the tail of the previous stage.
-//
 // Numerics: fp32 state, no fast-math.  Every floating-point operation whose
-// result is reused by another kernel (net hop, LUT lookup) is written with
-// explicit round-to-nearest intrinsics so that no FMA-contraction choice of
-// the compiler can make two recomputations of the same quantity differ.
+// result is recomputed elsewhere (net hop) is written with explicit
+// round-to-nearest intrinsics so that no FMA-contraction choice of the
+// compiler can make two recomputations of the same quantity differ.
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
@@ -187,17 +184,7 @@ __device__ __forceinline__ void load_rec(const CornerDev& c, uint32_t i, Q4& at,
     sl.v[q] = __uint_as_float(w.z);
   }
 }
-__device__ __forceinline__ void store_rec(const CornerDev& c, uint32_t i, const Q4& at, const Q4& sl, uint32_t ep) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) st_ll(c.rec + 4 * (size_t)i + q, at.v[q], sl.v[q], ep);
-}
 
-// ordered-int image of a float: monotone for signed-int comparison
-__device__ __forceinline__ int f2o(float f) {
-  const int i = __float_as_int(f);
-  return i >= 0 ? i : i ^ 0x7FFFFFFF;
-}
-__device__ __forceinline__ float o2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
 
 // ------------------------------------------------------------------ a1: RC
 __device__ __forceinline__ bool bad_rc(float r, float cw) {
@@ -402,9 +389,6 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
-}
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // ---- tier C: Euler-tour RC over one global preorder array (sta_internal.h)
@@ -1023,7 +1007,7 @@ __device__ __forceinline__ SinkFo bwd_fo(const Topo& t, const uint4& ud) {
 }
 
 __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, const float* __restrict__ L,
-                                         uint32_t ep, uint32_t u, const uint4& ud, const SinkFo& fo, float4* sm) {
+                                         uint32_t ep, uint32_t u, const uint4& ud, const SinkFo& fo) {
   const uint32_t lane = threadIdx.x & 31;
   unsigned long long t_start = 0, t_ready = 0, t_data = 0;
   if (c.trace && lane == 0) t_start = gtimer();
@@ -1130,7 +1114,6 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
 template <bool SMEM_LUT>
 __global__ void __launch_bounds__(kThreads, kBwdMinBlocks) bwd_persistent_kernel(Topo t, CornerDev c,
                                                                                    uint32_t lut_f4) {
-  __shared__ float4 s_m[kThreads];
   const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
   const uint32_t ep = epoch_of(c);
   const uint32_t warp = threadIdx.x >> 5;
@@ -1157,11 +1140,11 @@ __global__ void __launch_bounds__(kThreads, kBwdMinBlocks) bwd_persistent_kernel
       u = ns + __shfl_sync(kFull, x, 0);
       if (u >= t.n_bwu) break;
       ud = __ldg(t.bwu + u);
-      bwd_unit(t, c, L, ep, u, ud, bwd_fo(t, ud), s_m + 32 * warp);
+      bwd_unit(t, c, L, ep, u, ud, bwd_fo(t, ud));
       continue;
     }
     const uint4 nu = u + W < ns ? __ldg(t.bwu + u + W) : none;
-    bwd_unit(t, c, L, ep, u, ud, bwd_fo(t, ud), s_m + 32 * warp);
+    bwd_unit(t, c, L, ep, u, ud, bwd_fo(t, ud));
     u += W;
     ud = nu;
   }
@@ -1183,7 +1166,7 @@ __global__ void __launch_bounds__(kThreads, kBwdMinBlocks) bwd_persistent_kernel
       nfo = bwd_fo(t, nx);                   // next unit's fan-out records (its record arrived)
       if (u + 2 * W < ns) nnx = __ldg(t.bwu + u + 2 * W);
     }
-    bwd_unit(t, c, L, ep, u, ud, fo, s_m + 32 * warp);
+    bwd_unit(t, c, L, ep, u, ud, fo);
     if (!dyn) {
       u += W;
       ud = nx;
@@ -1197,7 +1180,6 @@ __global__ void __launch_bounds__(kThreads, kBwdMinBlocks) bwd_persistent_kernel
 template <bool SMEM_LUT>
 __global__ void __launch_bounds__(kThreads) bwd_stage_kernel(Topo t, CornerDev c, uint32_t u0, uint32_t u1,
                                                              uint32_t lut_f4) {
-  __shared__ float4 s_m[kThreads];
   const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t u = u0 + blockIdx.x * (kThreads / 32) + warp;
@@ -1206,7 +1188,7 @@ __global__ void __launch_bounds__(kThreads) bwd_stage_kernel(Topo t, CornerDev c
   pdl_wait();
   pdl_launch();
   if (u >= u1) return;
-  bwd_unit(t, c, L, epoch_of(c), u, ud, fo, s_m + 32 * warp);
+  bwd_unit(t, c, L, epoch_of(c), u, ud, fo);
 }
 
 // ------------------------------------------------------- a5: WNS / TNS
