@@ -459,7 +459,7 @@ void build_plan(sta_ctx c) {
       sms = (u32)n;
     cudaGetLastError();
   }
-  const u32 fwd_warps = sms * 8 * sta::kFwdMinBlocks, bwd_warps = sms * 8 * sta::kBwdMinBlocks;
+  const u32 fwd_warps = sms * (sta::kFwdThreads / 32) * sta::kFwdMinBlocks, bwd_warps = sms * (sta::kBwdThreads / 32) * sta::kBwdMinBlocks;
   auto unit_cap = [&](u64 items, u32 cap, u32 warps) {
     const u64 per = (items + warps / 2 - 1) / (warps / 2);
     return (u32)std::min<u64>(cap, std::max<u64>(1, per));

@@ -34,10 +34,18 @@ constexpr uint32_t kFwdUnitTerms = 8;          // forward warp unit: fan-in term
 #define STA_FWD_BLOCKS 4
 #endif
 #ifndef STA_BWD_BLOCKS
-#define STA_BWD_BLOCKS 2
+#define STA_BWD_BLOCKS 5
 #endif
 constexpr int kFwdMinBlocks = STA_FWD_BLOCKS;
+#ifndef STA_FWD_THREADS
+#define STA_FWD_THREADS 256
+#endif
+constexpr int kFwdThreads = STA_FWD_THREADS;    // forward persistent kernel block size
 constexpr int kBwdMinBlocks = STA_BWD_BLOCKS;
+#ifndef STA_BWD_THREADS
+#define STA_BWD_THREADS 128
+#endif
+constexpr int kBwdThreads = STA_BWD_THREADS;    // backward persistent kernel block size
 #ifndef STA_BWD_PIPE
 #define STA_BWD_PIPE 1                          // backward: prefetch the next unit's fan-out records
 #endif

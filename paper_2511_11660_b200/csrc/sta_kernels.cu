@@ -817,13 +817,13 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
 }
 
 template <bool SMEM_LUT>
-__global__ void __launch_bounds__(kThreads, kFwdMinBlocks) fwd_persistent_kernel(Topo t, CornerDev c,
+__global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) fwd_persistent_kernel(Topo t, CornerDev c,
                                                                                    uint32_t lut_f4) {
   const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
   const uint32_t ep = epoch_of(c);
   const uint32_t tl = (threadIdx.x & 31) >> 2;
-  const uint32_t W = gridDim.x * (kThreads / 32);
-  uint32_t u = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  const uint32_t W = gridDim.x * (kFwdThreads / 32);
+  uint32_t u = blockIdx.x * (kFwdThreads / 32) + (threadIdx.x >> 5);
   // software pipeline: the next unit's term slot is in flight while a unit
   // waits for its producers (the RC results are loaded by the unit itself: prefetching them too
   // measured slower on C3)
@@ -1112,13 +1112,13 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
 }
 
 template <bool SMEM_LUT>
-__global__ void __launch_bounds__(kThreads, kBwdMinBlocks) bwd_persistent_kernel(Topo t, CornerDev c,
+__global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_kernel(Topo t, CornerDev c,
                                                                                    uint32_t lut_f4) {
   const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
   const uint32_t ep = epoch_of(c);
   const uint32_t warp = threadIdx.x >> 5;
-  const uint32_t W = gridDim.x * (kThreads / 32);
-  uint32_t u = blockIdx.x * (kThreads / 32) + warp;
+  const uint32_t W = gridDim.x * (kBwdThreads / 32);
+  uint32_t u = blockIdx.x * (kBwdThreads / 32) + warp;
   // software pipeline: the unit record two units ahead, the sinks' fan-out
   // records one unit ahead are in flight while a unit waits for its producers
   // (issued at the start of the previous unit, so they overlap its work)
@@ -1432,20 +1432,20 @@ uint32_t persistent_grid(uint32_t lut_f4, int which) {
   const size_t smem = 16ull * lut_f4;
   if (which == 0)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &nb, lut_f4 ? fwd_persistent_kernel<true> : fwd_persistent_kernel<false>, kThreads, lut_f4 ? smem : 0);
+        &nb, lut_f4 ? fwd_persistent_kernel<true> : fwd_persistent_kernel<false>, kFwdThreads, lut_f4 ? smem : 0);
   else
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &nb, lut_f4 ? bwd_persistent_kernel<true> : bwd_persistent_kernel<false>, kThreads, lut_f4 ? smem : 0);
+        &nb, lut_f4 ? bwd_persistent_kernel<true> : bwd_persistent_kernel<false>, kBwdThreads, lut_f4 ? smem : 0);
   cudaGetLastError();
   return (uint32_t)(nb * sms);
 }
 
 template <class K>
-cudaError_t coop_launch(K kernel, uint32_t grid, size_t smem, cudaStream_t s, const Topo& t, const CornerDev& c,
-                        uint32_t lut_f4) {
+cudaError_t coop_launch(K kernel, uint32_t grid, uint32_t block, size_t smem, cudaStream_t s, const Topo& t,
+                        const CornerDev& c, uint32_t lut_f4) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -1458,14 +1458,14 @@ cudaError_t coop_launch(K kernel, uint32_t grid, size_t smem, cudaStream_t s, co
 
 cudaError_t launch_fwd_persistent(const Topo& t, const CornerDev& c, uint32_t grid, uint32_t lut_f4, cudaStream_t s) {
   if (!t.NP) return cudaSuccess;
-  return lut_f4 ? coop_launch(fwd_persistent_kernel<true>, grid, 16ull * lut_f4, s, t, c, lut_f4)
-                : coop_launch(fwd_persistent_kernel<false>, grid, 0, s, t, c, lut_f4);
+  return lut_f4 ? coop_launch(fwd_persistent_kernel<true>, grid, kFwdThreads, 16ull * lut_f4, s, t, c, lut_f4)
+                : coop_launch(fwd_persistent_kernel<false>, grid, kFwdThreads, 0, s, t, c, lut_f4);
 }
 
 cudaError_t launch_bwd_persistent(const Topo& t, const CornerDev& c, uint32_t grid, uint32_t lut_f4, cudaStream_t s) {
   if (!t.n_bwu) return cudaSuccess;
-  return lut_f4 ? coop_launch(bwd_persistent_kernel<true>, grid, 16ull * lut_f4, s, t, c, lut_f4)
-                : coop_launch(bwd_persistent_kernel<false>, grid, 0, s, t, c, lut_f4);
+  return lut_f4 ? coop_launch(bwd_persistent_kernel<true>, grid, kBwdThreads, 16ull * lut_f4, s, t, c, lut_f4)
+                : coop_launch(bwd_persistent_kernel<false>, grid, kBwdThreads, 0, s, t, c, lut_f4);
 }
 
 cudaError_t set_lut_smem_limit(size_t bytes) {
