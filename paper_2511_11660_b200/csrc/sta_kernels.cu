@@ -914,22 +914,19 @@ __device__ __forceinline__ void seed4(const Topo& t, const float* __restrict__ L
 // pin's own loads; the tag check comes later (bwd_pin).
 struct FoPre {
   float4 d0, d1;             // the terms' delays
-  uint4 e0, l0, e1, l1;      // required-time words (early, late) of the terms' pins
+  uint4 e0, l0;              // required-time words (early, late) of the first term's pin (a
+                             // non-unate arc's two terms share it; other second pins load later)
 };
 
 __device__ __forceinline__ FoPre bwd_pre(const CornerDev& c, const uint4& fa, const uint4& fb, uint32_t ep) {
   const uint4 ok = make_uint4(0, ep, 0, ep);
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-  FoPre p{z, z, ok, ok, ok, ok};
+  FoPre p{z, z, ok, ok};
   if (fa.w == kNone && fa.y) {
     p.d0 = __ldcg(c.tdel + (fb.y >> 3));
     p.e0 = ld_ll(c.rat_ll + 2 * (size_t)fb.x);
     p.l0 = ld_ll(c.rat_ll + 2 * (size_t)fb.x + 1);
-    if (fa.y > 1) {
-      p.d1 = __ldcg(c.tdel + (fb.w >> 3));
-      p.e1 = ld_ll(c.rat_ll + 2 * (size_t)fb.z);
-      p.l1 = ld_ll(c.rat_ll + 2 * (size_t)fb.z + 1);
-    }
+    if (fa.y > 1) p.d1 = __ldcg(c.tdel + (fb.w >> 3));
   }
   return p;
 }
@@ -954,13 +951,18 @@ __device__ __forceinline__ void bwd_pin(const Topo& t, const CornerDev& c, const
   if (fa.w != kNone) {
     seed4(t, L, fb.x, fb.y, a, s, r);
   } else if (nfo) {
-    if (arc_live(fb.y, a)) {
-      spin_pair(c.rat_ll + 2 * (size_t)fb.x, p.e0, p.l0, ep);
-      bwd_arc(a, fb.y, p.d0, p.e0, p.l0, r);
-    }
-    if (nfo > 1 && arc_live(fb.w, a)) {
-      spin_pair(c.rat_ll + 2 * (size_t)fb.z, p.e1, p.l1, ep);
-      bwd_arc(a, fb.w, p.d1, p.e1, p.l1, r);
+    const bool l0 = arc_live(fb.y, a), l1 = nfo > 1 && arc_live(fb.w, a), shared = fb.z == fb.x;
+    if (l0 || (l1 && shared)) spin_pair(c.rat_ll + 2 * (size_t)fb.x, p.e0, p.l0, ep);
+    if (l0) bwd_arc(a, fb.y, p.d0, p.e0, p.l0, r);
+    if (l1) {
+      if (shared) {
+        bwd_arc(a, fb.w, p.d1, p.e0, p.l0, r);
+      } else {
+        const uint4* pw = c.rat_ll + 2 * (size_t)fb.z;
+        uint4 we = ld_ll(pw), wl = ld_ll(pw + 1);
+        spin_pair(pw, we, wl, ep);
+        bwd_arc(a, fb.w, p.d1, we, wl, r);
+      }
     }
     f = nfo < 2 ? nfo : 2;
   }
