@@ -616,9 +616,10 @@ __global__ void __launch_bounds__(kTcThreads, 2) tc_persistent_kernel(Topo t, Co
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 
 // STA_TRACE: {start, ready (forward: before the inputs are polled), inputs loaded, end} of a unit
+template <bool TRACE>
 __device__ __forceinline__ void trace_unit(const CornerDev& c, size_t q, unsigned long long t0,
                                            unsigned long long t1, unsigned long long t2 = 0) {
-  if (c.trace && (threadIdx.x & 31) == 0) {
+  if (TRACE && (threadIdx.x & 31) == 0) {
     c.trace[4 * q] = t0;
     c.trace[4 * q + 1] = t1;
     c.trace[4 * q + 2] = t2 ? t2 : t1;
@@ -721,13 +722,14 @@ __device__ __forceinline__ FwdRc fwd_rc(const CornerDev& c, const uint4& tr) {
 
 // forward unit u; tr = this lane's term slot of the unit, rc its RC results
 // (loaded by the caller, software-pipelined one unit ahead)
+template <bool TRACE>
 __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, const float* __restrict__ L,
                                          uint32_t ep, uint32_t u, const uint4& tr, FwdRc rc) {
   const uint32_t lane = threadIdx.x & 31, tl = lane >> 2, q = lane & 3;
   const int el = (int)(q >> 1), orf = (int)(q & 1);
   const float undef = el ? -CUDART_INF_F : CUDART_INF_F;
   unsigned long long t_start = 0, t_ready = 0, t_data = 0;
-  if (c.trace && lane == 0) t_start = gtimer();
+  if (TRACE && lane == 0) t_start = gtimer();
   const uint32_t kind = __shfl_sync(kFull, tr.x, 0);
   if (kind == kSeedMark) {                   // seeds: lane = (pin, q)
     if (tr.w != kNone) {
@@ -743,7 +745,7 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
       }
       st_ll(c.rec + 4 * (size_t)v + q, a, sl, ep);
     }
-    trace_unit(c, u, t_start, t_start);
+    trace_unit<TRACE>(c, u, t_start, t_start);
     return;
   }
   if (kind != kHeavyMark) {
@@ -752,12 +754,12 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
     const float elm = rc.elm, ld = rc.ld;
     const int irf = primary_irf(info & 7u, orf);
     const uint4* wp = c.rec + 4 * (size_t)src + (el * 2 + irf);
-    if (c.trace && lane == 0) t_ready = gtimer();
+    if (TRACE && lane == 0) t_ready = gtimer();
     float ca = undef, cs = undef;
     if (item) {
       const FwdTabs f = fwd_tabs(L, info, orf, ld);   // before waiting for the producer
       const uint4 w = spin_ll(wp, ep);
-      if (c.trace) t_data = gtimer();
+      if (TRACE) t_data = gtimer();
       float a_in = __uint_as_float(w.x), s_in = __uint_as_float(w.z);
       if (tr.y != kNone) hop_q(a_in, s_in, elm);
       float dl;
@@ -807,16 +809,16 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
     if (tl == 0) st_ll(c.rec + 4 * (size_t)v + q, ca, cs, ep);
     t_ready = t_start;
   }
-  if (c.trace) {                             // latest lane's data arrival
+  if (TRACE) {                             // latest lane's data arrival
     const uint32_t lo = (uint32_t)t_data, hi = (uint32_t)(t_data >> 32);
     const uint32_t mh = __reduce_max_sync(kFull, hi);
     const uint32_t ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
     t_data = ((unsigned long long)mh << 32) | ml;
   }
-  trace_unit(c, u, t_start, t_ready, t_data);
+  trace_unit<TRACE>(c, u, t_start, t_ready, t_data);
 }
 
-template <bool SMEM_LUT>
+template <bool SMEM_LUT, bool TRACE>
 __global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) fwd_persistent_kernel(Topo t, CornerDev c,
                                                                                    uint32_t lut_f4) {
   const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
@@ -831,12 +833,12 @@ __global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) fwd_persistent_ker
   for (; u < t.n_fwu; u += W) {
     const uint4 tr = nx;
     if (u + W < t.n_fwu) nx = __ldg(t.fterm + (size_t)kFwdTerms * (u + W) + tl);   // prefetch the next unit
-    fwd_unit(t, c, L, ep, u, tr, fwd_rc(c, tr));
+    fwd_unit<TRACE>(t, c, L, ep, u, tr, fwd_rc(c, tr));
   }
 }
 
 // units [u0, u1) of one gate stage, one warp each
-template <bool SMEM_LUT>
+template <bool SMEM_LUT, bool TRACE>
 __global__ void __launch_bounds__(kThreads) fwd_stage_kernel(Topo t, CornerDev c, uint32_t u0, uint32_t u1,
                                                              uint32_t lut_f4) {
   const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
@@ -845,7 +847,7 @@ __global__ void __launch_bounds__(kThreads) fwd_stage_kernel(Topo t, CornerDev c
   pdl_wait();
   pdl_launch();
   if (u >= u1) return;
-  fwd_unit(t, c, L, epoch_of(c), u, tr, fwd_rc(c, tr));
+  fwd_unit<TRACE>(t, c, L, epoch_of(c), u, tr, fwd_rc(c, tr));
 }
 
 // ---- backward: one lane per sink / pin (all four components in the lane)
@@ -1008,11 +1010,12 @@ __device__ __forceinline__ SinkFo bwd_fo(const Topo& t, const uint4& ud) {
   return f;
 }
 
+template <bool TRACE>
 __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, const float* __restrict__ L,
                                          uint32_t ep, uint32_t u, const uint4& ud, const SinkFo& fo) {
   const uint32_t lane = threadIdx.x & 31;
   unsigned long long t_start = 0, t_ready = 0, t_data = 0;
-  if (c.trace && lane == 0) t_start = gtimer();
+  if (TRACE && lane == 0) t_start = gtimer();
   uint32_t v = kNone;
   Q4 at_v = undef_at(), sl_v = undef_at(), acc = undef_rat();
   bool head = false;
@@ -1032,11 +1035,11 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
         pb = __ldg(t.pullfo + 2 * (size_t)v + 1);
       }
       const FoPre pre = bwd_pre(c, fa, fb, ep);
-      if (c.trace) t_ready = gtimer();
+      if (TRACE) t_ready = gtimer();
       Q4 a = at_v, s = sl_v, r = undef_rat();
       net_hop(a, s, elm);                    // the sink's own arrival / slew
       bwd_pin(t, c, L, ep, fa, fb, pre, t.sfo_dst, t.sfo_info, a, s, r);
-      if (c.trace) t_data = gtimer();
+      if (TRACE) t_data = gtimer();
       c.rat[t.NP + k] = to_f4(r);
       const Q4 sk = slack_of(a, r);
       c.slack[t.NP + k] = to_f4(sk);
@@ -1103,17 +1106,17 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
     st_ll(c.rat_ll + 2 * (size_t)v, acc.v[0], acc.v[1], ep);
     st_ll(c.rat_ll + 2 * (size_t)v + 1, acc.v[2], acc.v[3], ep);
   }
-  if (c.trace) {                             // latest lane's fan-out data
+  if (TRACE) {                             // latest lane's fan-out data
     const uint32_t lo = (uint32_t)t_data, hi = (uint32_t)(t_data >> 32);
     const uint32_t mh = __reduce_max_sync(kFull, hi);
     const uint32_t ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
     t_data = ((unsigned long long)mh << 32) | ml;
     t_ready = __shfl_sync(kFull, t_ready, 0);
   }
-  trace_unit(c, (size_t)t.n_fwu + u, t_start, t_ready ? t_ready : t_start, t_data);
+  trace_unit<TRACE>(c, (size_t)t.n_fwu + u, t_start, t_ready ? t_ready : t_start, t_data);
 }
 
-template <bool SMEM_LUT>
+template <bool SMEM_LUT, bool TRACE>
 __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_kernel(Topo t, CornerDev c,
                                                                                    uint32_t lut_f4) {
   const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
@@ -1142,11 +1145,11 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_ker
       u = ns + __shfl_sync(kFull, x, 0);
       if (u >= t.n_bwu) break;
       ud = __ldg(t.bwu + u);
-      bwd_unit(t, c, L, ep, u, ud, bwd_fo(t, ud));
+      bwd_unit<TRACE>(t, c, L, ep, u, ud, bwd_fo(t, ud));
       continue;
     }
     const uint4 nu = u + W < ns ? __ldg(t.bwu + u + W) : none;
-    bwd_unit(t, c, L, ep, u, ud, bwd_fo(t, ud));
+    bwd_unit<TRACE>(t, c, L, ep, u, ud, bwd_fo(t, ud));
     u += W;
     ud = nu;
   }
@@ -1168,7 +1171,7 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_ker
       nfo = bwd_fo(t, nx);                   // next unit's fan-out records (its record arrived)
       if (u + 2 * W < ns) nnx = __ldg(t.bwu + u + 2 * W);
     }
-    bwd_unit(t, c, L, ep, u, ud, fo);
+    bwd_unit<TRACE>(t, c, L, ep, u, ud, fo);
     if (!dyn) {
       u += W;
       ud = nx;
@@ -1179,7 +1182,7 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_ker
 #endif
 }
 
-template <bool SMEM_LUT>
+template <bool SMEM_LUT, bool TRACE>
 __global__ void __launch_bounds__(kThreads) bwd_stage_kernel(Topo t, CornerDev c, uint32_t u0, uint32_t u1,
                                                              uint32_t lut_f4) {
   const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
@@ -1190,7 +1193,7 @@ __global__ void __launch_bounds__(kThreads) bwd_stage_kernel(Topo t, CornerDev c
   pdl_wait();
   pdl_launch();
   if (u >= u1) return;
-  bwd_unit(t, c, L, epoch_of(c), u, ud, fo);
+  bwd_unit<TRACE>(t, c, L, epoch_of(c), u, ud, fo);
 }
 
 // ------------------------------------------------------- a5: WNS / TNS
@@ -1396,16 +1399,16 @@ cudaError_t launch_fwd_stage(const Topo& t, const CornerDev& c, uint32_t u0, uin
                              cudaStream_t s) {
   if (u1 <= u0) return cudaSuccess;
   const uint32_t g = blocks(32ull * (u1 - u0));
-  if (lut_f4) return pdl_launch_smem(fwd_stage_kernel<true>, g, kThreads, 16ull * lut_f4, s, t, c, u0, u1, lut_f4);
-  return pdl_launch_smem(fwd_stage_kernel<false>, g, kThreads, 0, s, t, c, u0, u1, lut_f4);
+  if (lut_f4) return pdl_launch_smem(fwd_stage_kernel<true, false>, g, kThreads, 16ull * lut_f4, s, t, c, u0, u1, lut_f4);
+  return pdl_launch_smem(fwd_stage_kernel<false, false>, g, kThreads, 0, s, t, c, u0, u1, lut_f4);
 }
 
 cudaError_t launch_bwd_stage(const Topo& t, const CornerDev& c, uint32_t u0, uint32_t u1, uint32_t lut_f4,
                              cudaStream_t s) {
   if (u1 <= u0) return cudaSuccess;
   const uint32_t g = blocks(32ull * (u1 - u0));
-  if (lut_f4) return pdl_launch_smem(bwd_stage_kernel<true>, g, kThreads, 16ull * lut_f4, s, t, c, u0, u1, lut_f4);
-  return pdl_launch_smem(bwd_stage_kernel<false>, g, kThreads, 0, s, t, c, u0, u1, lut_f4);
+  if (lut_f4) return pdl_launch_smem(bwd_stage_kernel<true, false>, g, kThreads, 16ull * lut_f4, s, t, c, u0, u1, lut_f4);
+  return pdl_launch_smem(bwd_stage_kernel<false, false>, g, kThreads, 0, s, t, c, u0, u1, lut_f4);
 }
 
 cudaError_t launch_reduce(const Topo& t, const CornerDev& c, cudaStream_t s) {
@@ -1431,15 +1434,22 @@ uint32_t persistent_grid(uint32_t lut_f4, int which) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
   if (!coop) return 0;
-  const size_t smem = 16ull * lut_f4;
-  if (which == 0)
+  const size_t smem = lut_f4 ? 16ull * lut_f4 : 0;
+  // the same grid serves the traced instantiation: the smaller of the two
+  int nt = 0;
+  if (which == 0) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &nb, lut_f4 ? fwd_persistent_kernel<true> : fwd_persistent_kernel<false>, kFwdThreads, lut_f4 ? smem : 0);
-  else
+        &nb, lut_f4 ? fwd_persistent_kernel<true, false> : fwd_persistent_kernel<false, false>, kFwdThreads, smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &nb, lut_f4 ? bwd_persistent_kernel<true> : bwd_persistent_kernel<false>, kBwdThreads, lut_f4 ? smem : 0);
+        &nt, lut_f4 ? fwd_persistent_kernel<true, true> : fwd_persistent_kernel<false, true>, kFwdThreads, smem);
+  } else {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &nb, lut_f4 ? bwd_persistent_kernel<true, false> : bwd_persistent_kernel<false, false>, kBwdThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &nt, lut_f4 ? bwd_persistent_kernel<true, true> : bwd_persistent_kernel<false, true>, kBwdThreads, smem);
+  }
   cudaGetLastError();
-  return (uint32_t)(nb * sms);
+  return (uint32_t)(std::min(nb, nt) * sms);
 }
 
 template <class K>
@@ -1460,24 +1470,34 @@ cudaError_t coop_launch(K kernel, uint32_t grid, uint32_t block, size_t smem, cu
 
 cudaError_t launch_fwd_persistent(const Topo& t, const CornerDev& c, uint32_t grid, uint32_t lut_f4, cudaStream_t s) {
   if (!t.NP) return cudaSuccess;
-  return lut_f4 ? coop_launch(fwd_persistent_kernel<true>, grid, kFwdThreads, 16ull * lut_f4, s, t, c, lut_f4)
-                : coop_launch(fwd_persistent_kernel<false>, grid, kFwdThreads, 0, s, t, c, lut_f4);
+  // STA_TRACE builds per-unit timestamps into a separate instantiation
+  if (c.trace)
+    return lut_f4 ? coop_launch(fwd_persistent_kernel<true, true>, grid, kFwdThreads, 16ull * lut_f4, s, t, c, lut_f4)
+                  : coop_launch(fwd_persistent_kernel<false, true>, grid, kFwdThreads, 0, s, t, c, lut_f4);
+  return lut_f4 ? coop_launch(fwd_persistent_kernel<true, false>, grid, kFwdThreads, 16ull * lut_f4, s, t, c, lut_f4)
+                : coop_launch(fwd_persistent_kernel<false, false>, grid, kFwdThreads, 0, s, t, c, lut_f4);
 }
 
 cudaError_t launch_bwd_persistent(const Topo& t, const CornerDev& c, uint32_t grid, uint32_t lut_f4, cudaStream_t s) {
   if (!t.n_bwu) return cudaSuccess;
-  return lut_f4 ? coop_launch(bwd_persistent_kernel<true>, grid, kBwdThreads, 16ull * lut_f4, s, t, c, lut_f4)
-                : coop_launch(bwd_persistent_kernel<false>, grid, kBwdThreads, 0, s, t, c, lut_f4);
+  if (c.trace)
+    return lut_f4 ? coop_launch(bwd_persistent_kernel<true, true>, grid, kBwdThreads, 16ull * lut_f4, s, t, c, lut_f4)
+                  : coop_launch(bwd_persistent_kernel<false, true>, grid, kBwdThreads, 0, s, t, c, lut_f4);
+  return lut_f4 ? coop_launch(bwd_persistent_kernel<true, false>, grid, kBwdThreads, 16ull * lut_f4, s, t, c, lut_f4)
+                : coop_launch(bwd_persistent_kernel<false, false>, grid, kBwdThreads, 0, s, t, c, lut_f4);
 }
 
 cudaError_t set_lut_smem_limit(size_t bytes) {
-  cudaError_t e = cudaFuncSetAttribute(fwd_stage_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(bwd_stage_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(fwd_persistent_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(bwd_persistent_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  const int b = (int)bytes;
+  cudaError_t e = cudaFuncSetAttribute(fwd_stage_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(bwd_stage_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  for (int tr = 0; tr < 2 && e == cudaSuccess; ++tr) {
+    e = cudaFuncSetAttribute(tr ? fwd_persistent_kernel<true, true> : fwd_persistent_kernel<true, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(tr ? bwd_persistent_kernel<true, true> : bwd_persistent_kernel<true, false>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  }
   return e;
 }
 
