@@ -730,12 +730,12 @@ void build_rc(sta_ctx c) {
       if (!seen[c->net_pins[x]]) fail(STA_ERR_RC, "rc net %u: sink pin %u has no RC node", n, c->net_pins[x]);
   }
 
-  // nets in driver order j; each net's RC nodes renumbered in DFS preorder
+  // nets in caller order j; each net's RC nodes renumbered in DFS preorder
   // (children in increasing index order) into "internal nodes", so that a
   // subtree is a contiguous range [pos, end) and the kernels read topology
   // contiguously.  Internal nodes are grouped by tier: nets of 1..32 nodes
   // (warp tiles), then 33..kBNet (block tiles, packed densely), then larger
-  // (tier C), each group in driver order.  R and Cw stay in the caller's
+  // (tier C), each group in net order.  R and Cw stay in the caller's
   // node order (borrowed zero-copy), addressed through node_user.
   struct Group {
     std::vector<u32> user, meta, tag;
@@ -749,10 +749,12 @@ void build_rc(sta_ctx c) {
   std::vector<u32> lumped_j, tierC;
   std::vector<u32> tc_user, tc_int, tc_end, tc_start, tc_enter, tc_ev, tc_root, tc_drv;
   u32 wt_fill = 0;
-  for (u32 i = 0; i < c->NP; ++i) {
-    if (c->user_of_int[i] == kNone) continue;
-    const u32 n = c->pin_net[c->user_of_int[i]];
-    if (n == kNone) continue;
+  // nets in the caller's net order: the caller's R / Cw arrays (borrowed,
+  // node order of the caller) are then read nearly contiguously; the
+  // scattered 4-byte outputs (load per driver, Elmore per sink) stay in L2
+  for (u32 n = 0; n < N; ++n) {
+    const u32 i = c->drv_of_net[n];
+    if (i == kNone) continue;
     const u32 j = (u32)net_drv.size();
     const u32 ub = c->rc_ptr[n], m = c->rc_ptr[n + 1] - ub;
     net_drv.push_back(i);
