@@ -405,7 +405,10 @@ constexpr int kTcThreads = 512;
 #ifndef STA_TC_BLOCKS
 #define STA_TC_BLOCKS 1                      // blocks per SM of the tier-C kernel
 #endif
-constexpr int kTcBatch = 4;                  // elements in flight per thread
+#ifndef STA_TC_BATCH
+#define STA_TC_BATCH 8
+#endif
+constexpr int kTcBatch = STA_TC_BATCH;       // elements in flight per thread
 
 __device__ __forceinline__ void tc_grid_barrier(uint32_t* bar, uint32_t nblocks) {
   __syncthreads();
@@ -464,20 +467,34 @@ __device__ __forceinline__ double tc_scan_range(double* x, size_t lo, size_t hi,
   const double off = tc_block_offset(sums, blockIdx.x, s_red);
   const size_t n = hi - lo, K = (n + blockDim.x - 1) / blockDim.x;
   const size_t a = lo + min(n, (size_t)threadIdx.x * K), b = lo + min(n, (size_t)(threadIdx.x + 1) * K);
+  // (loads in groups of 8 ahead of the stores: a load after a store to the
+  // same array cannot be hoisted by the compiler and would pay a full memory
+  // latency per element)
+  constexpr int kG = 8;
   double csum = 0.0;
-#pragma unroll 8
-  for (size_t i = a; i < b; ++i) csum += x[i];    // the block's own writes (barrier above)
+  for (size_t i0 = a; i0 < b; i0 += kG) {
+    double v[kG];
+#pragma unroll
+    for (int k = 0; k < kG; ++k) v[k] = i0 + k < b ? x[i0 + k] : 0.0;
+#pragma unroll
+    for (int k = 0; k < kG; ++k) csum += v[k];
+  }
   double tot;
   double carry = off + block_excl_scan(csum, s_warp, &tot);
-#pragma unroll 8
-  for (size_t i = a; i < b; ++i) {
-    const double v = x[i];
-    if (INCLUSIVE) {
-      carry += v;
-      x[i] = carry;
-    } else {
-      x[i] = carry;
-      carry += v;
+  for (size_t i0 = a; i0 < b; i0 += kG) {
+    double v[kG];
+#pragma unroll
+    for (int k = 0; k < kG; ++k) v[k] = i0 + k < b ? x[i0 + k] : 0.0;
+#pragma unroll
+    for (int k = 0; k < kG; ++k) {
+      if (i0 + k >= b) break;
+      if (INCLUSIVE) {
+        carry += v[k];
+        x[i0 + k] = carry;
+      } else {
+        x[i0 + k] = carry;
+        carry += v[k];
+      }
     }
   }
   return off + tot;
