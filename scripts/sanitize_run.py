@@ -1,0 +1,28 @@
+"""Small updates for compute-sanitizer (memcheck / racecheck / synccheck):
+c17, a 2k-cell synthetic design with high-fan-out nets, wide gates and
+two-output cells; both launchers; compared with the oracle."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+import paper_2511_11660_b200 as sta  # noqa: E402
+import synth  # noqa: E402
+from tests.parity import compare_update  # noqa: E402
+from tests.test_gpu_parity import _wide_multi_output_design  # noqa: E402
+
+designs = [synth.c17(), synth.generate(2000, 16, seed=4, n_hfn=2, hfn_range=(40, 400), period=200.0),
+           _wide_multi_output_design()]
+for mode in ("0", "1"):
+    os.environ["STA_STAGE_KERNELS"] = mode
+    for d in designs:
+        ctx = sta.Context(0, 1)
+        sta.load_design(ctx, d)
+        for _ in range(2):
+            ctx.update_timing()
+        ctx.synchronize()
+        compare_update(ctx, oracle.update(d))
+        ctx.close()
+        print("ok", mode, d.name, flush=True)
