@@ -903,6 +903,7 @@ void prepare(sta_ctx c) {
   c->pgrid = c->use_persistent ? sta::persistent_grid(c->lut_f4, 0) : 0;
   c->pgrid_b = c->use_persistent ? sta::persistent_grid(c->lut_f4, 1) : 0;
   const u32 P = c->P;
+  if (c->NP >= 0x80000000u) fail(STA_ERR_ARG, "too many pins for the backward records");
   std::vector<u32> pi_idx(P, kNone), po_idx(P, kNone);
   for (u32 k = 0; k < c->pi_pin.size(); ++k) pi_idx[c->pi_pin[k]] = k;
   for (u32 k = 0; k < c->po_pin.size(); ++k) po_idx[c->po_pin[k]] = k;
@@ -938,8 +939,14 @@ void prepare(sta_ctx c) {
     }
   };
   std::vector<uint4> sinkfo(2 * (size_t)c->NS), pullfo(2 * (size_t)c->NP);
-  for (u32 k = 0; k < c->NS; ++k)
-    fo_rec(&sinkfo[2 * (size_t)k], c->sink_drv[k], pin_ep[c->NP + k], c->sfo_p, c->sfo_dst, c->sfo_info, k);
+  for (u32 k = 0; k < c->NS; ++k) {
+    // driver field bit 31: the driver has its own endpoint or direct cell
+    // fan-out (its pullfo record must be read); most drivers have neither
+    const u32 v = c->sink_drv[k];
+    const bool work = pin_ep[v] != kNone || c->pfo_p[v + 1] != c->pfo_p[v];
+    fo_rec(&sinkfo[2 * (size_t)k], v | (work ? 0x80000000u : 0u), pin_ep[c->NP + k], c->sfo_p, c->sfo_dst,
+           c->sfo_info, k);
+  }
   for (u32 i = 0; i < c->NP; ++i) fo_rec(&pullfo[2 * (size_t)i], 0, pin_ep[i], c->pfo_p, c->pfo_dst, c->pfo_info, i);
   // stage-0 seeds
   std::vector<u32> seed(c->n0, kNone);

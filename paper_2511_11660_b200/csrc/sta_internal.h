@@ -113,7 +113,7 @@ struct Topo {
   uint32_t n_bwu_static;         // units [0, n_bwu_static) statically assigned; the rest (stage 0,
                                  // no dependencies among them) handed out by a ticket counter
   // backward fan-out records, two uint4 per sink (sinkfo) / pull pin (pullfo):
-  //   a = {driver (sinks; 0 for pull pins), nfo = cell fan-out terms, f0 =
+  //   a = {driver | has-pullfo-work << 31 (sinks; 0 for pull pins), nfo = cell fan-out terms, f0 =
   //        first term in sfo_* / pfo_*, endpoint index or kNone}
   //   b = non-endpoints: {dst, sense | delay slot << 3} of the first two fan-out terms (kNone
   //       dst if absent); endpoints: {check table or kNone, PO index or

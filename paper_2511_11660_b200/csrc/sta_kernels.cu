@@ -1041,13 +1041,14 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
     const uint32_t k = ud.x + lane;
     const bool act = k < ud.y;
     const uint4 fa = fo.a, fb = fo.b;
-    v = act ? fa.x : kNone;
+    v = act ? fa.x & 0x7FFFFFFFu : kNone;
+    const bool drv_work = (fa.x >> 31) != 0;   // the driver has an endpoint / direct fan-out
     const uint32_t vp = __shfl_up_sync(kFull, v, 1);
     head = act && (lane == 0 || vp != v);    // first lane of its driver
     if (act) {
       const float elm = __ldcg(c.elm + k);
       load_rec(c, v, at_v, sl_v);
-      if (head) {
+      if (head && drv_work) {
         pa = __ldg(t.pullfo + 2 * (size_t)v);
         pb = __ldg(t.pullfo + 2 * (size_t)v + 1);
       }
