@@ -1,3 +1,7 @@
+#!/usr/bin/env bash
+# One gpurun call: build, GPU tests (TESTS=1), one bench line per build-flag
+# set in NBS (comma-separated nvcc -D flags per set), and an STA_TRACE
+# timeline of the default build.   T=tag NBS="-DSTA_FWD_BLOCKS=4 ..." bash scripts/gpu_sweep.sh
 set -u
 mkdir -p gpurun_out
 T=${T:-x}
