@@ -1174,27 +1174,48 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_ker
   (void)fo;
   (void)nx;
 #else
-  for (;;) {
+  // one call site of bwd_unit (a second inlined copy of the large unit body
+  // measured 40% slower: instruction-cache pressure)
+  bool dyn = u >= ns;
+  if (dyn) {                                 // no static unit: first ticket
+    uint32_t x = 0;
+    if (lane == 0) x = atomicAdd(c.red_cnt + 1, 1u);
+    u = ns + __shfl_sync(kFull, x, 0);
+    ud = u < t.n_bwu ? __ldg(t.bwu + u) : none;
+    fo = bwd_fo(t, ud);
+  }
+  while (u < t.n_bwu) {
     SinkFo nfo = fo;
     uint4 nnx = none;
-    const bool dyn = u >= ns;
+    uint32_t un = 0;
     if (dyn) {
-      uint32_t x = 0;
-      if (lane == 0) x = atomicAdd(c.red_cnt + 1, 1u);
-      u = ns + __shfl_sync(kFull, x, 0);
-      if (u >= t.n_bwu) break;
-      ud = __ldg(t.bwu + u);
-      fo = bwd_fo(t, ud);
+      // the next ticket and its unit record are fetched before this unit
+      // runs, so the atomic and the record load overlap its work
+      uint32_t xn = 0;
+      if (lane == 0) xn = atomicAdd(c.red_cnt + 1, 1u);
+      un = ns + __shfl_sync(kFull, xn, 0);
+      nx = un < t.n_bwu ? __ldg(t.bwu + un) : none;
     } else {
       nfo = bwd_fo(t, nx);                   // next unit's fan-out records (its record arrived)
       if (u + 2 * W < ns) nnx = __ldg(t.bwu + u + 2 * W);
     }
     bwd_unit<TRACE>(t, c, L, ep, u, ud, fo);
-    if (!dyn) {
+    if (dyn) {
+      u = un;
+      ud = nx;
+      fo = bwd_fo(t, ud);
+    } else if (u + W < ns) {
       u += W;
       ud = nx;
       fo = nfo;
       nx = nnx;
+    } else {                                 // static part done: first ticket
+      dyn = true;
+      uint32_t x = 0;
+      if (lane == 0) x = atomicAdd(c.red_cnt + 1, 1u);
+      u = ns + __shfl_sync(kFull, x, 0);
+      ud = u < t.n_bwu ? __ldg(t.bwu + u) : none;
+      fo = bwd_fo(t, ud);
     }
   }
 #endif
