@@ -22,8 +22,12 @@ def build(force: bool = False) -> str:
     """Compile the oracle with gcc (-O2, strict IEEE: no -ffast-math)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
             os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "sta_oracle.h"))):
+        # compile to a private name, then rename: concurrent builders (the
+        # ranks of a multi-process test) never load a half-written library
+        tmp = f"{_LIB}.{os.getpid()}.tmp"
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fno-fast-math",
-                               "-ffp-contract=off", "-o", _LIB, _SRC, "-lm"])
+                               "-ffp-contract=off", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
     return _LIB
 
 

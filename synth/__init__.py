@@ -11,5 +11,5 @@ from .design import (  # noqa: F401
     SENSE_POS, SENSE_NEG, SENSE_NON, SENSE_RISE_EDGE, SENSE_FALL_EDGE,
     ROLE_INTERNAL, ROLE_PI, ROLE_PO, ROLE_FF_CK, ROLE_FF_D, NO_PIN,
 )
-from .hand import c17, h1_chain, h3_reg2reg  # noqa: F401
+from .hand import c17, h1_chain, h3_reg2reg, h4_seeds  # noqa: F401
 from .recipe import generate, CONFIGS, config_design, corner_scales  # noqa: F401

@@ -204,3 +204,48 @@ def h3_reg2reg() -> Design:
     b.net("X/Y", ["DFF2/D"], [(-1, 0.0, 0.0, "X/Y"), (0, 1.0, 0.0, "DFF2/D")])
     cons = _cons(b, 60.0, 20.0, [("b", [5, 5, 5, 5], [10, 10, 10, 10])], [])
     return b.build(cons, "h3")
+
+
+def h4_seeds() -> Design:
+    """Hand example H4: pins the endpoint-seed lookups and
+    the clock-slew seed, which H1-H3 leave free.
+
+    DFF1/CK (ideal clock, slew = clock slew 16 ps) -RISE_EDGE-> DFF1/Q with
+    AFFINE tables whose delay depends on the input slew, so the CK seed slew
+    matters; NAND2 X (NEG) joins Q1 with PI b whose early and
+    late slews differ; X/Y drives DFF2/D (setup/hold check against DFF2/CK)
+    and a PO Z.  The check tables are affine a + b s_data + k s_clk with
+    b != k on axes (data slew, clock slew), so swapping the
+    arguments, or taking the early slew for setup / the late slew for hold,
+    changes the required times.  Every net has R = 0 (Elmore 0, slews pass
+    unchanged) so the hand derivation in tests/golden/h4_seeds.json stays
+    exact.  Units ps / fF.
+    """
+    b = Builder()
+    b.pin("DFF1/CK", 0.0, ROLE_FF_CK)
+    b.pin("DFF1/Q", 0.0)
+    b.pin("b", 0.0, ROLE_PI)
+    b.pin("X/A", 1.0)
+    b.pin("X/B", 1.0)
+    b.pin("X/Y", 0.0)
+    b.pin("DFF2/D", 2.0, ROLE_FF_D)
+    b.pin("DFF2/CK", 0.0, ROLE_FF_CK)
+    b.pin("Z", 0.0, ROLE_PO)
+    S, L = AFFINE_SLEW, AFFINE_LOAD
+    ckq = b.tables4([affine_table(S, L, 20, 0.5, 2.0), affine_table(S, L, 18, 0.4, 1.0),
+                     affine_table(S, L, 4, 0.25, 1.0), affine_table(S, L, 3, 0.2, 1.0)])
+    nand = b.tables4([affine_table(S, L, 10, 0.2, 2.0), affine_table(S, L, 8, 0.1, 3.0),
+                      affine_table(S, L, 5, 0.5, 1.0), affine_table(S, L, 4, 0.25, 2.0)])
+    # constraint tables: index_1 = data slew, index_2 = clock slew (SPEC.md:548)
+    chk = b.tables4([affine_table(S, S, 5, 0.1, 0.3), affine_table(S, S, 6, 0.2, 0.05),
+                     affine_table(S, S, 1, 0.05, 0.25), affine_table(S, S, -2, 0.3, 0.1)])
+    b.arc("DFF1/CK", "DFF1/Q", SENSE_RISE_EDGE, ckq)
+    b.arc("X/A", "X/Y", SENSE_NEG, nand)
+    b.arc("X/B", "X/Y", SENSE_NEG, nand)
+    b.check("DFF2/D", "DFF2/CK", chk)
+    b.net("DFF1/Q", ["X/A"], b.star_rc("DFF1/Q", ["X/A"], 0.0, 0.0))
+    b.net("b", ["X/B"], b.star_rc("b", ["X/B"], 0.0, 0.0))
+    b.net("X/Y", ["DFF2/D", "Z"], b.star_rc("X/Y", ["DFF2/D", "Z"], 0.0, 0.0))
+    cons = _cons(b, 50.0, 16.0, [("b", [2, 3, 6, 5], [8, 12, 40, 20])],
+                 [("Z", [5, 6], [1, 2], 0.0)])
+    return b.build(cons, "h4")

@@ -10,9 +10,9 @@ the quantities the value is computed from (DESIGN.md §2 reading R17):
     cancels against the clock period (e.g. 15837 - 15969 = -132 ps carries
     the rounding of 1.6e4-sized operands);
   * slack = RAT - AT: scale = max(|AT|, |RAT|, T) of the same component;
-  * WNS: the largest endpoint slack scale; TNS: the sum of the slack bounds of
-    the endpoints whose oracle worst slack is below their bound (each
-    contributes at most its own error; the others contribute 0).
+  * WNS and TNS: scale = |oracle value| (SURVEY §8(c) rule #17 as written;
+    tightened in round 2 from the per-endpoint slack scales, VERDICT r1
+    "What's weak" #2).
 Infinite values (undefined quantities) must match exactly.
 Levels and permutations are integers: bit-exact.
 """
@@ -69,23 +69,9 @@ def compare_update(ctx, ref, corner=0, report=None, period=None):
     check_close("rat", rat, ref["rat"], scale=np.maximum(fr, T), report=report)
     sc = np.maximum(np.maximum(fa, fr), T)
     check_close("slack", slack, ref["slack"], scale=sc, report=report)
-    ep = ref["ep_pin"]
     r = ref["res"]
-    if ep.size:
-        ep_sc = sc[ep]
-        sc_s = np.max(ep_sc[:, 2:], axis=1)
-        sc_h = np.max(ep_sc[:, :2], axis=1)
-        ws = ref["ep_ws"]
-        tns_s_tol = float(np.sum(np.where(ws[:, 0] < bound(sc_s), bound(sc_s), 0.0))) + ABS
-        tns_h_tol = float(np.sum(np.where(ws[:, 1] < bound(sc_h), bound(sc_h), 0.0))) + ABS
-        wns_s_sc, wns_h_sc = float(sc_s.max()), float(sc_h.max())
-    else:
-        tns_s_tol = tns_h_tol = ABS
-        wns_s_sc = wns_h_sc = 0.0
-    check_close("wns_setup", [res[0]], [r[0]], scale=[wns_s_sc], report=report)
-    check_close("wns_hold", [res[2]], [r[2]], scale=[wns_h_sc], report=report)
-    for name, g, o, tol in (("tns_setup", res[1], r[1], tns_s_tol), ("tns_hold", res[3], r[3], tns_h_tol)):
-        if report is not None:
-            report[name] = dict(abs_err=abs(g - o), bound=tol)
-        assert abs(g - o) <= tol, f"{name}: gpu {g} oracle {o} bound {tol}"
+    check_close("wns_setup", [res[0]], [r[0]], report=report)
+    check_close("wns_hold", [res[2]], [r[2]], report=report)
+    check_close("tns_setup", [res[1]], [r[1]], report=report)
+    check_close("tns_hold", [res[3]], [r[3]], report=report)
     return res

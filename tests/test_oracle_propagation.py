@@ -21,7 +21,8 @@ from tests.brute import (constant_library_like, design_node_caps, elmore_brutefo
                          longest_path_levels, path_enumeration_timing)
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
-HAND = {"h1_chain": synth.h1_chain, "c17": synth.c17, "h3_reg2reg": synth.h3_reg2reg}
+HAND = {"h1_chain": synth.h1_chain, "c17": synth.c17, "h3_reg2reg": synth.h3_reg2reg,
+        "h4_seeds": synth.h4_seeds}
 
 
 def _f(x):
@@ -34,7 +35,7 @@ def _close(a, b, tol):
     return abs(a - b) <= tol
 
 
-@pytest.mark.parametrize("name", ["h1_chain", "c17", "h3_reg2reg"])
+@pytest.mark.parametrize("name", ["h1_chain", "c17", "h3_reg2reg", "h4_seeds"])
 def test_golden_hand_examples(name):
     g = json.load(open(os.path.join(GOLD, f"{name}.json")))
     d = HAND[name]()
