@@ -39,7 +39,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=CONFIG)
+    ap.add_argument("--config", default=None,
+                    help="c3_superblue (default at N=1), c5_multicorner (default at N>1), c2_tau, c4_tdp")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip e2e/profile/cpu legs (ncu runs)")
     return ap.parse_args()
@@ -161,11 +162,13 @@ def run_reference(args, world, rank):
     import oracle
     import synth
     oracle.build()
-    cfg = dict(synth.CONFIGS[args.config])
+    name = args.config or (CONFIG if world == 1 else "c5_multicorner")
+    cfg = dict(synth.CONFIGS[name])
     scale = 10                                   # bounded sample: 1/10 of the cells
     cfg["n_cells"] //= scale
-    d = synth.generate(name=args.config, **cfg)
-    d.cons.period = synth.recipe.lookup_period(args.config) or d.cons.period
+    cfg["corners"] = 1
+    d = synth.generate(name=name, **cfg)
+    d.cons.period = synth.recipe.lookup_period(name) or d.cons.period
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -180,10 +183,29 @@ def run_reference(args, world, rank):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "pins/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config} (sample)", "pins": d.num_pins},
-            "cpu_baseline": {"value": v, "unit": "pins/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "config": {"workload": f"{name} (sample)", "pins": d.num_pins},
+            "cpu_baseline": {"value": v, "unit": "pins/s", "cores": 1, "host_cores": os.cpu_count(),
+                             "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "pins/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def config_line(name, info, K_local, world, gen_s, load_s):
+    if name == "c5_multicorner":
+        w = (f"{name}: BASELINE.json configs[4] multi-corner sign-off, 8 corners x ~2M-pin synthetic "
+             f"design, {K_local} corner(s) per GPU traversed by the same launches, one NCCL all_reduce of "
+             f"the per-corner WNS/TNS rows per step")
+    else:
+        w = (f"{name}: BASELINE.json configs[2] superblue-shaped synthetic netlist, one corner per GPU"
+             if name == "c3_superblue" else f"{name} (synthetic, DESIGN.md §3)")
+    return {"workload": w, "pins_per_corner": info["num_pins"], "corners_per_gpu": K_local,
+            "pin_levels": info["num_levels"], "gate_stages": info["num_stages"],
+            "cell_arcs": info["num_cell_arcs"], "net_arcs": info["num_net_arcs"],
+            "endpoints": info["num_endpoints"], "heavy_drivers": info["num_heavy_drivers"],
+            "parallelism": f"corners x{world}",
+            "l2": "no flush: per-update working set > 1.5 GB >> 126 MB L2" if info["num_pins"] * K_local > 5e6
+            else "no flush: the working set exceeds L2 only partly (small config)",
+            "gen_s": round(gen_s, 1), "load_graph_s": round(load_s, 2)}
 
 
 def main():
@@ -199,33 +221,45 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2511_11660_b200 as pkg
     from paper_2511_11660_b200 import build as pbuild
+    from paper_2511_11660_b200 import multicorner as mc
     pbuild.build()
+    name = args.config or (CONFIG if world == 1 else "c5_multicorner")
 
     # one dedicated stream carries the STA kernels, the NCCL allreduce and the
     # timing events (the legacy default stream cannot be shared by handle)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     t0 = time.perf_counter()
-    d = corner_design(args.config, rank)
+    if name == "c5_multicorner":
+        import synth
+        d = synth.config_design(name)            # all 8 corners; this rank loads its share
+        mine = list(mc.corners_of_rank(d.num_corners, rank, world))
+        K_total = d.num_corners
+    else:
+        d = corner_design(name, rank)            # one corner per rank (weak scaling)
+        mine = [0]
+        K_total = world
     gen_s = time.perf_counter() - t0
-    ctx = pkg.Context(local, 1, stream=stream.cuda_stream)
+    K = len(mine)
+    ctx = pkg.Context(local, K, stream=stream.cuda_stream)
     t0 = time.perf_counter()
-    pkg.load_design(ctx, d)
+    pkg.load_design(ctx, d, corners=mine)
     torch.cuda.synchronize()
     load_s = time.perf_counter() - t0
     # inputs resident in HBM for the device-timed value: borrowed RC tensors
-    res_d = torch.from_numpy(d.rc[0].res).cuda()
-    cap_d = torch.from_numpy(d.rc[0].cap).cuda()
-    ctx.set_rc_values(0, res_d, cap_d)
-    rows = torch.zeros((world, 4), dtype=torch.float64, device="cuda")
-
-    from paper_2511_11660_b200 import multicorner as mc
+    res_d = [torch.from_numpy(d.rc[c].res).cuda() for c in mine]
+    cap_d = [torch.from_numpy(d.rc[c].cap).cuda() for c in mine]
+    for k in range(K):
+        ctx.set_rc_values(k, res_d[k], cap_d[k])
+    rows = torch.zeros((K_total, 4), dtype=torch.float64, device="cuda")
+    row0 = mine[0] if name == "c5_multicorner" else rank
 
     def step():
         ctx.update_timing()
         if world > 1:
             rows.zero_()
-            ctx.report_wns_tns_device(0, rows[rank])
+            for k in range(K):
+                ctx.report_wns_tns_device(k, rows[row0 + k])
             mc.combine_rows(rows)          # one NCCL allreduce of the per-corner rows
 
     def barrier():
@@ -257,25 +291,28 @@ def main():
         ms = float(t.item())
     info = ctx.info()
     P = info["num_pins"]
-    value = world * P / (ms / 1e3)
+    total_pins = P * (K_total if name == "c5_multicorner" else world)
+    value = total_pins / (ms / 1e3)
+    res_own = [ctx.report_slack(k)[0] for k in range(K)]
     res_global = None
-    res_own, _ = ctx.report_slack(0)
-    if world > 1:
-        res_global = [float(x) for x in mc.global_report(rows.cpu())]
+    if world > 1 or K > 1:
+        full = torch.zeros((K_total, 4), dtype=torch.float64)
+        for k in range(K):
+            full[row0 + k] = torch.from_numpy(res_own[k])
+        if world > 1:
+            full = full.cuda()
+            mc.combine_rows(full)
+        res_global = [float(x) for x in mc.global_report(full.cpu())]
 
     line = {"metric": METRIC, "value": value, "unit": "pins/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if name == "c5_multicorner" else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config}: BASELINE.json configs[2] superblue-shaped synthetic "
-                                   f"netlist, one corner per GPU",
-                       "pins_per_gpu": P, "pin_levels": info["num_levels"], "gate_stages": info["num_stages"],
-                       "cell_arcs": info["num_cell_arcs"], "net_arcs": info["num_net_arcs"],
-                       "endpoints": info["num_endpoints"], "heavy_drivers": info["num_heavy_drivers"],
-                       "corners_per_gpu": 1, "parallelism": f"corners x{world}",
-                       "l2": "no flush: per-update working set > 1.5 GB >> 126 MB L2",
-                       "gen_s": round(gen_s, 1), "load_graph_s": round(load_s, 2)},
+            "config": config_line(name, info, K, world, gen_s, load_s),
             "gpu_launches": info["kernels_per_update"] * args.steps,
-            "clocks": clk, "wns_tns": [float(x) for x in res_own]}
+            "clocks": clk, "wns_tns": [float(x) for x in res_own[0]]}
+    if name == "c5_multicorner":
+        line["corner_updates_per_s"] = K_total / (ms / 1e3)
     if res_global:
         line["wns_tns_global"] = res_global
 
@@ -288,7 +325,7 @@ def main():
         ctx.profile_enable(False)
         nu = max(prof["updates"], 1)
         ph_ms = {k: v / nu for k, v in prof["ms"].items()}
-        ab = algorithmic_bytes(d, info)
+        ab = {k: v * K for k, v in algorithmic_bytes(d, info).items()}
         peak, peak_src = measured_peaks()
         dom = max(("forward", "backward"), key=lambda k: ph_ms[k])
         ach = ab[dom] / (ph_ms[dom] / 1e3) / 1e9
@@ -304,20 +341,19 @@ def main():
         line["update_model_bytes"] = whole
         line["update_frac_hbm"] = whole / (ms / 1e3) / 1e9 / peak
 
-        # e2e: public API with host buffers; per step H2D of the RC values
-        # (the per-iteration inputs of an optimization loop) from pinned memory,
-        # update, D2H of WNS/TNS
-        res_h = torch.from_numpy(d.rc[0].res).pin_memory()
-        cap_h = torch.from_numpy(d.rc[0].cap).pin_memory()
-        res_s = torch.empty_like(res_d)
-        cap_s = torch.empty_like(cap_d)
+        # e2e through the public C ABI with HOST buffers: per step the RC
+        # values of every local corner (the per-iteration inputs of an
+        # optimization loop) go host -> device from page-locked memory
+        # (sta_set_rc_values, STA_MEM_HOST), then the update, then the
+        # WNS/TNS rows device -> host (sta_report_slack, STA_MEM_HOST)
+        res_h = [torch.from_numpy(d.rc[c].res).pin_memory() for c in mine]
+        cap_h = [torch.from_numpy(d.rc[c].cap).pin_memory() for c in mine]
 
         def e2e_step():
-            res_s.copy_(res_h, non_blocking=True)
-            cap_s.copy_(cap_h, non_blocking=True)
-            ctx.set_rc_values(0, res_s, cap_s)
+            for k in range(K):
+                ctx.set_rc_values(k, res_h[k].numpy(), cap_h[k].numpy())
             ctx.update_timing()
-            return ctx.report_slack(0)[0]          # D2H of the step's result, synchronizes
+            return [ctx.report_slack(k)[0] for k in range(K)]
 
         for _ in range(2):
             e2e_step()
@@ -332,23 +368,28 @@ def main():
             t = torch.tensor([ms_e2e], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_e2e = float(t.item())
-        line["e2e"] = {"value": world * P / (ms_e2e / 1e3), "unit": "pins/s",
-                       "h2d_bytes_per_step": int(res_h.numel() * 4 + cap_h.numel() * 4),
-                       "d2h_bytes_per_step": 32, "ms_per_step": ms_e2e}
-        ctx.set_rc_values(0, res_d, cap_d)
+        line["e2e"] = {"value": total_pins / (ms_e2e / 1e3), "unit": "pins/s",
+                       "h2d_bytes_per_step": int(sum(x.numel() * 4 for x in res_h + cap_h)),
+                       "d2h_bytes_per_step": 32 * K, "ms_per_step": ms_e2e,
+                       "path": "sta_set_rc_values(STA_MEM_HOST, page-locked) + sta_update_timing + "
+                               "sta_report_slack(STA_MEM_HOST)"}
+        for k in range(K):
+            ctx.set_rc_values(k, res_d[k], cap_d[k])
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.quick:
         import oracle
         oracle.build()
         t0 = time.perf_counter()
-        ref = oracle.update(d, 0, want_all=False)
+        ref = oracle.update(d, mine[0], want_all=False)
         cpu_s = time.perf_counter() - t0
-        line["cpu_baseline"] = {"value": P / cpu_s, "unit": "pins/s", "cores": 1, "kind": "oracle",
-                                "sample": f"one full update of the same {P}-pin design, fp64, single thread "
-                                          f"({cpu_s:.1f} s)"}
+        line["cpu_baseline"] = {"value": P / cpu_s, "unit": "pins/s", "cores": 1,
+                                "host_cores": os.cpu_count(),
+                                "affinity_cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+                                "sample": f"one full update of corner {mine[0]} of the same {P}-pin design, fp64, "
+                                          f"single thread ({cpu_s:.1f} s) on a host with {os.cpu_count()} cores"}
         r = ref["res"]
         line["parity_wns_tns"] = {"oracle": [float(x) for x in r],
-                                  "abs_err": [float(abs(a - b)) for a, b in zip(res_own, r)]}
+                                  "abs_err": [float(abs(a - b)) for a, b in zip(res_own[0], r)]}
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -152,7 +152,8 @@ STA_API sta_status sta_load_graph(sta_ctx ctx, const sta_graph_desc* desc);
  * Table t: n1[t], n2[t] in 1..8, data[off[t] ...] = index_1[n1] (input slew
  * ps; data slew for constraint tables), index_2[n2] (load fF; clock slew for
  * constraint tables), values[n1][n2] row-major (ps).  Axes strictly
- * ascending.  Copied (small).  Errors: STA_ERR_ARG, STA_ERR_LUT. */
+ * ascending.  Corners may use different axes (pool sizes may differ).
+ * Copied (small).  Errors: STA_ERR_ARG, STA_ERR_LUT. */
 STA_API sta_status sta_set_library(sta_ctx ctx, uint32_t corner, sta_mem mem, uint32_t num_tables,
                            const uint8_t* n1, const uint8_t* n2, const uint32_t* off,
                            const float* data, uint32_t data_len);
@@ -171,12 +172,16 @@ STA_API sta_status sta_set_rc_tree(sta_ctx ctx, sta_mem mem, const uint32_t* rc_
 
 /* Per-corner RC values: res[i] = resistance of the edge parent -> i (kOhm,
  * ignored at node 0), cap[i] = wire capacitance to ground at node i (fF);
- * both num_nodes long, >= 0 and finite.  HOST: copied (validated).  DEVICE:
- * BORROWED, zero copy -- the caller keeps both arrays alive and unmodified
- * until the next sta_update_timing has completed on the ctx stream; a bad
- * value is detected on the device and reported as STA_ERR_RC by the next
- * synchronizing call.  This is the per-iteration call of an optimization
- * loop. */
+ * both num_nodes long, >= 0 and finite.  HOST: copied into ctx-owned device
+ * buffers in stream order before the call returns (page-locked buffers move
+ * by DMA at link speed).  DEVICE: BORROWED, zero copy -- the caller keeps both
+ * arrays alive and unmodified until the next sta_update_timing has completed
+ * on the ctx stream; the call itself never blocks the host (the pointer pair
+ * is published by a stream-ordered one-thread kernel), so the next
+ * iteration's inputs can be produced while an update runs.  In both cases the
+ * values are validated on the device by the RC kernels: a bad value is
+ * reported as STA_ERR_RC by the next synchronizing call.  This is the
+ * per-iteration call of an optimization loop. */
 STA_API sta_status sta_set_rc_values(sta_ctx ctx, uint32_t corner, sta_mem mem, const float* res,
                              const float* cap);
 
@@ -209,7 +214,8 @@ STA_API sta_status sta_set_constraints(sta_ctx ctx, const sta_constraints* cons)
 /* One full timing update for every corner of ctx, enqueued on the ctx
  * stream: Elmore RC and loads, forward AT/slew with NLDM cell delays, endpoint
  * required-time seeds, backward RAT, per-pin slack, WNS/TNS (SURVEY.md §8(a)
- * a1-a5).  Requires sta_load_graph, sta_set_rc_tree, sta_set_constraints and,
+ * a1-a5).  Up to 8 corners are traversed by the same kernel launches (their
+ * level-by-level wavefronts advance together).  Requires sta_load_graph, sta_set_rc_tree, sta_set_constraints and,
  * for every corner, sta_set_library and sta_set_rc_values (else
  * STA_ERR_ORDER).  Asynchronous: errors of the kernels surface at the next
  * synchronizing call. */
@@ -257,6 +263,7 @@ typedef struct {
   uint32_t num_sink_pins;    /* net sinks */
   uint32_t num_heavy_drivers;
   uint32_t kernels_per_update; /* kernel launches of one sta_update_timing */
+  uint32_t lut_smem_bytes;   /* largest per-launch NLDM image staged in shared memory (0: global lookups) */
   uint64_t device_bytes;     /* device memory held by ctx */
 } sta_info;
 STA_API sta_status sta_get_info(sta_ctx ctx, sta_info* out);

@@ -75,14 +75,16 @@ struct Arena {
 
 // copy caller input (HOST or DEVICE) into a host vector
 template <class T>
-std::vector<T> fetch(const T* p, size_t n, sta_mem mem, const char* name) {
+std::vector<T> fetch(const T* p, size_t n, sta_mem mem, const char* name, cudaStream_t s) {
   std::vector<T> v(n);
   if (n == 0) return v;
   if (!p) fail(STA_ERR_ARG, "%s: NULL pointer for %zu elements", name, n);
   if (mem == STA_MEM_HOST) {
     std::memcpy(v.data(), p, n * sizeof(T));
   } else if (mem == STA_MEM_DEVICE) {
-    ck(cudaMemcpy(v.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost), name);
+    // stream ordered: after every kernel the caller queued on the ctx stream
+    ck(cudaMemcpyAsync(v.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost, s), name);
+    ck(cudaStreamSynchronize(s), name);
   } else {
     fail(STA_ERR_ARG, "%s: bad sta_mem %d", name, (int)mem);
   }
@@ -94,7 +96,6 @@ struct CornerState {
   Arena lib_arena, rc_arena, state_arena, ptr_arena;
   const float* rc_res = nullptr;   // active R / Cw arrays (owned or borrowed)
   const float* rc_cap = nullptr;
-  const float** rc_ptr_host = nullptr;   // pinned staging of {res, cap}
   size_t lut_bytes = 0;                  // device table pool size
   sta::CornerDev dev{};
 };
@@ -142,6 +143,8 @@ struct sta_ctx_s {
   u32 big_total = 0;              // tier-C nodes
   std::vector<u32> node_user;     // internal RC node -> caller node id
   std::vector<u32> node_meta_h, node_tag_h;   // host copies (packed node records, prepare())
+  std::vector<u32> node_z_h;      // rc_node .z: caller offset in the warp tile (tier A) / caller id (B)
+  std::vector<u32> tc_end_h;      // tier-C node: global position one past its subtree
   u32 n_rc_ab = 0;                // internal RC nodes of tiers A and B (they come first)
   std::vector<u32> rc_net_j;      // net j (driver order) -> internal driver id
 
@@ -161,7 +164,8 @@ struct sta_ctx_s {
   sta_profile profile{};
   cudaEvent_t ev[STA_NUM_PHASES * 2] = {};
   u32 launches_per_update = 0;
-  u32 lut_f4 = 0;                 // table pool staged in shared memory (float4s)
+  u32 smem_f4 = 0;                // largest batch LUT image staged in shared memory (float4s; 0: global)
+  u32 wgrid = 0;                  // co-resident grid of the tier-A RC kernel
   // the update as one CUDA graph (captured lazily, invalidated by any input
   // change except sta_set_rc_values, which only rewrites a device-side
   // pointer pair)
@@ -738,17 +742,17 @@ void build_rc(sta_ctx c) {
   // (tier C), each group in net order.  R and Cw stay in the caller's
   // node order (borrowed zero-copy), addressed through node_user.
   struct Group {
-    std::vector<u32> user, meta, tag;
+    std::vector<u32> user, meta, tag, z;
   } grp[3];
   std::vector<u32> net_drv;
   net_drv.reserve(N);
   std::vector<u32> cnt, ch, pos, endp, pre;
   std::vector<std::pair<u32, u32>> stack;
-  std::vector<uint2> wtiles;                // warp tiles of nets with 1..32 nodes
+  std::vector<uint4> wtiles;                // warp tiles of nets with 1..32 nodes
   std::vector<uint2> btiles;                // block tiles of nets with 33..kBNet nodes (group-1 offsets)
   std::vector<u32> lumped_j, tierC;
-  std::vector<u32> tc_user, tc_int, tc_end, tc_start, tc_enter, tc_ev, tc_root, tc_drv;
-  u32 wt_fill = 0;
+  std::vector<u32> tc_end, tc_ev;
+  u32 wt_fill = 0, wt_cend = kNone;         // open warp tile: nodes, caller node one past its last
   // nets in the caller's net order: the caller's R / Cw arrays (borrowed,
   // node order of the caller) are then read nearly contiguously; the
   // scattered 4-byte outputs (load per driver, Elmore per sink) stay in L2
@@ -791,10 +795,17 @@ void build_rc(sta_ctx c) {
         stack.pop_back();
       }
     }
+    if (tier == 0 && (wtiles.empty() || wt_fill + m > 32 || ub != wt_cend)) {
+      // a warp tile's caller nodes must be one contiguous range (the kernel
+      // loads them by lane and permutes with a shuffle)
+      wtiles.push_back(make_uint4(x0, 0, ub, 0));
+      wt_fill = 0;
+    }
     for (u32 t2 = 0; t2 < m; ++t2) {
       const u32 q = pre[t2];
       const u32 un = ub + q;
       G.user.push_back(un);
+      G.z.push_back(tier == 0 ? un - wtiles.back().z : un);
       if (tier == 0) {
         const u32 ppos = q ? pos[(u32)c->rc_parent[un]] : 0xFFu;
         G.meta.push_back(t2 | (ppos << 8) | (endp[t2] << 16));
@@ -811,12 +822,9 @@ void build_rc(sta_ctx c) {
       G.tag.push_back(tag);
     }
     if (tier == 0) {
-      if (wtiles.empty() || wt_fill + m > 32) {
-        wtiles.push_back(make_uint2(x0, 0));
-        wt_fill = 0;
-      }
       wtiles.back().y += m;
       wt_fill += m;
+      wt_cend = ub + m;
     } else if (tier == 1) {
       if (btiles.empty() || btiles.back().y + m > sta::kBNet) btiles.push_back(make_uint2(x0, 0));
       btiles.back().y += m;
@@ -826,30 +834,22 @@ void build_rc(sta_ctx c) {
       // (before entering position t2: exit every node whose subtree ends
       // there, deepest first; after the last node: exit the rest)
       tierC.push_back(j);
-      const u32 g0 = (u32)tc_user.size();   // == x0: tier-C positions are group-2 internal offsets
+      const u32 g0 = x0;                    // tier-C positions are group-2 internal offsets
       std::vector<std::vector<u32>> ends_at(m + 1);
       for (u32 a2 = 0; a2 < m; ++a2) ends_at[endp[a2]].push_back(a2);
-      tc_enter.resize(g0 + m);
       for (u32 t2 = 0; t2 <= m; ++t2) {
         for (auto it = ends_at[t2].rbegin(); it != ends_at[t2].rend(); ++it) tc_ev.push_back((g0 + *it) | 0x80000000u);
         if (t2 == m) break;
-        tc_enter[g0 + t2] = (u32)tc_ev.size();
         tc_ev.push_back(g0 + t2);
-        tc_user.push_back(ub + pre[t2]);
-        tc_int.push_back((x0 + t2) | (t2 == 0 ? 0x80000000u : 0u));
         tc_end.push_back(g0 + endp[t2]);
-        tc_start.push_back(g0);
       }
       if (tc_ev.size() != 2 * (size_t)(g0 + m)) fail(STA_ERR_RC, "internal error: Euler tour of net %u", n);
-      tc_root.push_back(g0);
-      tc_drv.push_back(i);
     }
   }
   // concatenate the groups; rebase block tiles and tier-C internal ids
   const u32 nA = (u32)grp[0].user.size(), nB = (u32)grp[1].user.size();
   for (uint2& b : btiles) b.x += nA;
-  for (u32& x : tc_int) x += nA + nB;       // root bit (bit 31) unaffected: ids < 2^31
-  std::vector<u32> node_user, node_meta, node_tag;
+  std::vector<u32> node_user, node_meta, node_tag, node_z;
   node_user.reserve(c->n_rc);
   node_meta.reserve(c->n_rc);
   node_tag.reserve(c->n_rc);
@@ -857,23 +857,23 @@ void build_rc(sta_ctx c) {
     node_user.insert(node_user.end(), G.user.begin(), G.user.end());
     node_meta.insert(node_meta.end(), G.meta.begin(), G.meta.end());
     node_tag.insert(node_tag.end(), G.tag.begin(), G.tag.end());
+    node_z.insert(node_z.end(), G.z.begin(), G.z.end());
     G = Group{};
   }
   if (node_user.size() != c->n_rc)   // nets without a driver-order entry cannot exist
     fail(STA_ERR_RC, "internal error: %zu of %u RC nodes placed", node_user.size(), c->n_rc);
 
-  c->big_total = (u32)tc_user.size();
+  c->big_total = (u32)tc_end.size();
 
   cudaStream_t s = c->stream;
   c->tree_arena.release();
   Arena& g = c->tree_arena;
   sta::Topo& t = c->topo;
   t.net_drv = g.upload(net_drv, s);
-  t.node_user = g.upload(node_user, s);
-  t.node_meta = g.upload(node_meta, s);
-  t.node_tag = g.upload(node_tag, s);
   c->node_meta_h = node_meta;
   c->node_tag_h = node_tag;
+  c->node_z_h = std::move(node_z);
+  c->tc_end_h = std::move(tc_end);
   c->n_rc_ab = nA + nB;
   t.n_wtiles = (u32)wtiles.size();
   t.wtiles = g.upload(wtiles, s);
@@ -883,25 +883,50 @@ void build_rc(sta_ctx c) {
   t.lumped_j = g.upload(lumped_j, s);
   t.nC = (u32)tierC.size();
   t.nCn = c->big_total;
-  t.tc_user = g.upload(tc_user, s);
-  t.tc_int = g.upload(tc_int, s);
-  t.tc_end = g.upload(tc_end, s);
-  t.tc_start = g.upload(tc_start, s);
-  t.tc_enter = g.upload(tc_enter, s);
   t.tc_ev = g.upload(tc_ev, s);
-  t.tc_root = g.upload(tc_root, s);
-  t.tc_drv = g.upload(tc_drv, s);
   c->node_user = std::move(node_user);
   c->rc_net_j = std::move(net_drv);
   ck(cudaStreamSynchronize(s), "rc upload");
 }
 
 // constraints + tree dependent arrays (endpoints, seeds, static node caps)
+// The corners of ctx in launch batches of <= kMaxBatch, each corner's table
+// pool placed in the batch's shared-memory image (global lookups if the image
+// exceeds kLutSmemMax).
+std::vector<sta::Batch> make_batches(sta_ctx c) {
+  std::vector<sta::Batch> out;
+  for (u32 k0 = 0; k0 < c->K; k0 += sta::kMaxBatch) {
+    sta::Batch b{};
+    b.K = std::min<u32>(sta::kMaxBatch, c->K - k0);
+    u32 off = 0;
+    for (u32 k = 0; k < b.K; ++k) {
+      sta::CornerDev d = c->corners[k0 + k].dev;
+      d.lut_off4 = off;
+      off += d.lut_n4;
+      b.c[k] = d;
+    }
+    b.smem_f4 = 16ull * off <= sta::kLutSmemMax ? off : 0;
+    out.push_back(b);
+  }
+  return out;
+}
+
+// shared-memory limit and co-resident grids of the persistent kernels for
+// the largest batch image
+void size_kernels(sta_ctx c) {
+  u32 mx = 0;
+  for (const sta::Batch& b : make_batches(c)) mx = std::max(mx, b.smem_f4);
+  c->smem_f4 = mx;
+  if (16ull * mx > 48 * 1024) ck(sta::set_lut_smem_limit(16ull * mx), "smem attribute");
+  c->pgrid = c->use_persistent ? sta::persistent_grid(mx, 0) : 0;
+  c->pgrid_b = c->use_persistent ? sta::persistent_grid(mx, 1) : 0;
+  if (!c->wgrid) c->wgrid = sta::rc_warp_grid();
+}
+
 void prepare(sta_ctx c) {
   if (c->prepared) return;
   invalidate_graph(c);
-  c->pgrid = c->use_persistent ? sta::persistent_grid(c->lut_f4, 0) : 0;
-  c->pgrid_b = c->use_persistent ? sta::persistent_grid(c->lut_f4, 1) : 0;
+  size_kernels(c);
   const u32 P = c->P;
   if (c->NP >= 0x80000000u) fail(STA_ERR_ARG, "too many pins for the backward records");
   std::vector<u32> pi_idx(P, kNone), po_idx(P, kNone);
@@ -993,16 +1018,24 @@ void prepare(sta_ctx c) {
   t.po_out_min = reinterpret_cast<const float2*>(g.upload(c->po_out_min, s));
   t.period = c->period;
   t.clock_slew = c->clock_slew;
-  t.rc_scap = g.upload(scap, s);
   t.net_lumped = g.upload(lumped, s);
   {   // packed per-node records of the small-net RC kernels (tiers A and B)
     std::vector<uint4> nodes(c->n_rc_ab);
     for (u32 x = 0; x < c->n_rc_ab; ++x) {
       u32 sc;
       std::memcpy(&sc, &scap[x], 4);
-      nodes[x] = make_uint4(c->node_meta_h[x], c->node_tag_h[x], c->node_user[x], sc);
+      nodes[x] = make_uint4(c->node_meta_h[x], c->node_tag_h[x], c->node_z_h[x], sc);
     }
     t.rc_node = g.upload(nodes, s);
+    // tier C: {caller node, tag, subtree end, static cap}
+    std::vector<uint4> tcn(c->big_total);
+    for (u32 gq = 0; gq < c->big_total; ++gq) {
+      const u32 x = c->n_rc_ab + gq;
+      u32 sc;
+      std::memcpy(&sc, &scap[x], 4);
+      tcn[gq] = make_uint4(c->node_user[x], c->node_tag_h[x], c->tc_end_h[gq], sc);
+    }
+    t.tc_node = g.upload(tcn, s);
   }
 
   // per-corner state buffers
@@ -1043,52 +1076,52 @@ void prepare(sta_ctx c) {
   c->prepared = true;
 }
 
-// Kernel sequence of one update of one corner (see sta_kernels.cu).
-u32 enqueue_corner(sta_ctx c, const sta::CornerDev& d) {
+// Kernel sequence of one update of one batch of corners (see sta_kernels.cu).
+u32 enqueue_batch(sta_ctx c, const sta::Batch& b) {
   const sta::Topo& t = c->topo;
   cudaStream_t s = c->stream;
   u32 launches = 0;
   prof_mark(c, 0);
   if (t.nC && std::getenv("STA_RC_SERIAL")) {
-    ck(sta::launch_rc_tierC(t, d, s), "rc tier-C kernels");
+    ck(sta::launch_rc_tierC(t, b, s), "rc tier-C kernels");
   } else if (t.nC) {                         // tier C concurrently with the small nets
     ck(cudaEventRecord(c->fork_ev, s), "fork");
     ck(cudaStreamWaitEvent(c->side, c->fork_ev, 0), "fork wait");
-    ck(sta::launch_rc_tierC(t, d, c->side), "rc tier-C kernels");
+    ck(sta::launch_rc_tierC(t, b, c->side), "rc tier-C kernels");
     ck(cudaEventRecord(c->join_ev, c->side), "join");
   }
-  ck(sta::launch_rc(t, d, s), "rc kernel");
+  ck(sta::launch_rc(t, b, c->wgrid, s), "rc kernel");
   if (t.nC && !std::getenv("STA_RC_SERIAL")) ck(cudaStreamWaitEvent(s, c->join_ev, 0), "join wait");
-  launches += (t.n_wtiles ? 1 : 0) + (t.n_btiles ? 1 : 0) + (t.n_lumped ? 1 : 0) + (t.nC ? 1 : 0);
+  launches += (t.n_wtiles ? 1 : 0) + (t.n_btiles ? 1 : 0) + (t.n_lumped ? 1 : 0) + (t.nC ? 3 : 0);
   prof_mark(c, 1);
   if (c->use_persistent && c->pgrid && c->pgrid_b) {
     prof_mark(c, 2);
-    ck(sta::launch_fwd_persistent(t, d, c->pgrid, c->lut_f4, s), "forward persistent kernel");
+    ck(sta::launch_fwd_persistent(t, b, c->pgrid, s), "forward persistent kernel");
     prof_mark(c, 3);
     prof_mark(c, 4);
-    ck(sta::launch_bwd_persistent(t, d, c->pgrid_b, c->lut_f4, s), "backward persistent kernel");
+    ck(sta::launch_bwd_persistent(t, b, c->pgrid_b, s), "backward persistent kernel");
     prof_mark(c, 5);
     prof_mark(c, 6);
-    ck(sta::launch_reduce(t, d, s), "reduce kernel");
+    ck(sta::launch_reduce(t, b, s), "reduce kernel");
     prof_mark(c, 7);
     return launches + 3;
   }
   prof_mark(c, 2);
   for (u32 st = 0; st < c->S; ++st) {
     const u32 u0 = c->fwu_stage_ptr[st], u1 = c->fwu_stage_ptr[st + 1];
-    ck(sta::launch_fwd_stage(t, d, u0, u1, c->lut_f4, s), "forward kernel");
+    ck(sta::launch_fwd_stage(t, b, u0, u1, s), "forward kernel");
     launches += u1 > u0 ? 1 : 0;
   }
   prof_mark(c, 3);
   prof_mark(c, 4);
   for (u32 st = c->S; st-- > 0;) {
     const u32 u0 = c->bwu_stage_lo[st], u1 = c->bwu_stage_hi[st];
-    ck(sta::launch_bwd_stage(t, d, u0, u1, c->lut_f4, s), "backward kernel");
+    ck(sta::launch_bwd_stage(t, b, u0, u1, s), "backward kernel");
     launches += u1 > u0 ? 1 : 0;
   }
   prof_mark(c, 5);
   prof_mark(c, 6);
-  ck(sta::launch_reduce(t, d, s), "reduce kernel");
+  ck(sta::launch_reduce(t, b, s), "reduce kernel");
   launches += 1;
   prof_mark(c, 7);
   return launches;
@@ -1119,8 +1152,11 @@ void dump_trace(sta_ctx c) {
 
 void enqueue_update(sta_ctx c) {
   cudaStream_t s = c->stream;
+  const std::vector<sta::Batch> batches = make_batches(c);
   if (!c->trace_path.empty()) {
-    for (CornerState& cs : c->corners) c->launches_per_update = enqueue_corner(c, cs.dev);
+    u32 launches = 0;
+    for (const sta::Batch& b : batches) launches += enqueue_batch(c, b);
+    c->launches_per_update = launches;
     dump_trace(c);
     return;
   }
@@ -1130,7 +1166,7 @@ void enqueue_update(sta_ctx c) {
       ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
       u32 launches = 0;
       try {
-        for (CornerState& cs : c->corners) launches += enqueue_corner(c, cs.dev);
+        for (const sta::Batch& b : batches) launches += enqueue_batch(c, b);
       } catch (...) {
         cudaStreamEndCapture(s, &g);
         if (g) cudaGraphDestroy(g);
@@ -1147,8 +1183,8 @@ void enqueue_update(sta_ctx c) {
   }
   u32 launches = 0;
   prof_mark(c, 8);
-  for (CornerState& cs : c->corners) {
-    launches += enqueue_corner(c, cs.dev);
+  for (const sta::Batch& b : batches) {
+    launches += enqueue_batch(c, b);
     if (c->prof) {
       // accumulate per phase (synchronous read of the event pairs)
       ck(cudaEventSynchronize(c->ev[7]), "event sync");
@@ -1177,9 +1213,10 @@ void check_flags(sta_ctx c) {
     CornerState& cs = c->corners[k];
     if (!cs.dev.err_flag) continue;
     u32 f = 0;
-    ck(cudaMemcpy(&f, cs.dev.err_flag, sizeof f, cudaMemcpyDeviceToHost), "flag D2H");
+    ck(cudaMemcpyAsync(&f, cs.dev.err_flag, sizeof f, cudaMemcpyDeviceToHost, c->stream), "flag D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
     if (f) {
-      ck(cudaMemset(cs.dev.err_flag, 0, sizeof f), "memset");
+      ck(cudaMemsetAsync(cs.dev.err_flag, 0, sizeof f, c->stream), "memset");
       fail(STA_ERR_RC, "corner %zu: negative or non-finite RC value in the borrowed arrays", k);
     }
   }
@@ -1249,20 +1286,12 @@ void deliver_pins(sta_ctx c, float* dst, const sta::CornerDev& d, int what, sta_
   if (mem != STA_MEM_DEVICE) deliver(c, reinterpret_cast<float4*>(dst), out, P, STA_MEM_HOST);
 }
 
-// per-corner {res, cap} device pointer pair, updated in stream order so a
-// captured update graph stays valid when borrowed arrays change
+// per-corner {res, cap} device pointer pair, rewritten in stream order by a
+// one-thread kernel (no host staging, no host synchronization), so a captured
+// update graph stays valid when the borrowed arrays change
 void publish_rc_pointers(sta_ctx c, CornerState& cs) {
-  if (!cs.rc_ptr_host) {
-    void* h = nullptr;
-    ck(cudaHostAlloc(&h, 2 * sizeof(float*), cudaHostAllocDefault), "cudaHostAlloc");
-    cs.rc_ptr_host = static_cast<const float**>(h);
-    cs.dev.rc_vals = cs.ptr_arena.alloc<const float*>(2);
-  }
-  ck(cudaStreamSynchronize(c->stream), "sync");   // staging buffer reuse
-  cs.rc_ptr_host[0] = cs.rc_res;
-  cs.rc_ptr_host[1] = cs.rc_cap;
-  ck(cudaMemcpyAsync(const_cast<const float**>(cs.dev.rc_vals), cs.rc_ptr_host, 2 * sizeof(float*),
-                     cudaMemcpyHostToDevice, c->stream), "H2D rc pointers");
+  if (!cs.dev.rc_vals) cs.dev.rc_vals = cs.ptr_arena.alloc<const float*>(2);
+  ck(sta::launch_set_ptrs(cs.dev.rc_vals, cs.rc_res, cs.rc_cap, c->stream), "rc pointer kernel");
 }
 
 }  // namespace
@@ -1337,7 +1366,6 @@ sta_status sta_destroy(sta_ctx c) {
     cs.rc_arena.release();
     cs.state_arena.release();
     cs.ptr_arena.release();
-    if (cs.rc_ptr_host) cudaFreeHost(cs.rc_ptr_host);
   }
   invalidate_graph(c);
   for (auto& e : c->ev)
@@ -1361,18 +1389,18 @@ sta_status sta_load_graph(sta_ctx c, const sta_graph_desc* d) {
     c->tree_arena.release();
     c->cons_arena.release();
     c->P = d->num_pins; c->N = d->num_nets; c->A = d->num_arcs; c->C = d->num_checks; c->T = d->num_tables;
-    c->pin_cap = fetch(d->pin_cap, c->P, d->mem, "pin_cap");
-    c->pin_role = fetch(d->pin_role, c->P, d->mem, "pin_role");
-    c->net_ptr = fetch(d->net_ptr, c->N ? c->N + 1 : 0, d->mem, "net_ptr");
+    c->pin_cap = fetch(d->pin_cap, c->P, d->mem, "pin_cap", c->stream);
+    c->pin_role = fetch(d->pin_role, c->P, d->mem, "pin_role", c->stream);
+    c->net_ptr = fetch(d->net_ptr, c->N ? c->N + 1 : 0, d->mem, "net_ptr", c->stream);
     const u32 nnp = c->N ? c->net_ptr[c->N] : 0;
-    c->net_pins = fetch(d->net_pins, nnp, d->mem, "net_pins");
-    c->arc_from = fetch(d->arc_from, c->A, d->mem, "arc_from");
-    c->arc_to = fetch(d->arc_to, c->A, d->mem, "arc_to");
-    c->arc_sense = fetch(d->arc_sense, c->A, d->mem, "arc_sense");
-    c->arc_tab = fetch(d->arc_tab, c->A, d->mem, "arc_tab");
-    c->chk_d = fetch(d->chk_d, c->C, d->mem, "chk_d");
-    c->chk_ck = fetch(d->chk_ck, c->C, d->mem, "chk_ck");
-    c->chk_tab = fetch(d->chk_tab, c->C, d->mem, "chk_tab");
+    c->net_pins = fetch(d->net_pins, nnp, d->mem, "net_pins", c->stream);
+    c->arc_from = fetch(d->arc_from, c->A, d->mem, "arc_from", c->stream);
+    c->arc_to = fetch(d->arc_to, c->A, d->mem, "arc_to", c->stream);
+    c->arc_sense = fetch(d->arc_sense, c->A, d->mem, "arc_sense", c->stream);
+    c->arc_tab = fetch(d->arc_tab, c->A, d->mem, "arc_tab", c->stream);
+    c->chk_d = fetch(d->chk_d, c->C, d->mem, "chk_d", c->stream);
+    c->chk_ck = fetch(d->chk_ck, c->C, d->mem, "chk_ck", c->stream);
+    c->chk_tab = fetch(d->chk_tab, c->C, d->mem, "chk_tab", c->stream);
     validate_graph(c);
     build_plan(c);
     c->has_graph = true;
@@ -1385,10 +1413,10 @@ sta_status sta_set_library(sta_ctx c, uint32_t corner, sta_mem mem, uint32_t num
     CornerState& cs = corner_of(c, corner);
     if (!c->has_graph) fail(STA_ERR_ORDER, "sta_set_library before sta_load_graph");
     if (num_tables != c->T) fail(STA_ERR_ARG, "library has %u tables, graph expects %u", num_tables, c->T);
-    auto h1 = fetch(n1, num_tables, mem, "n1");
-    auto h2 = fetch(n2, num_tables, mem, "n2");
-    auto ho = fetch(off, num_tables, mem, "off");
-    auto hd = fetch(data, data_len, mem, "data");
+    auto h1 = fetch(n1, num_tables, mem, "n1", c->stream);
+    auto h2 = fetch(n2, num_tables, mem, "n2", c->stream);
+    auto ho = fetch(off, num_tables, mem, "off", c->stream);
+    auto hd = fetch(data, data_len, mem, "data", c->stream);
     // device pool (sta_internal.h): table blocks of kTabStride floats, then
     // deduplicated 16-byte aligned axis templates of kTmplStride floats
     const size_t tmpl0 = ((size_t)num_tables * sta::kTabStride + 3) / 4 * 4;
@@ -1435,14 +1463,11 @@ sta_status sta_set_library(sta_ctx c, uint32_t corner, sta_mem mem, uint32_t num
     invalidate_graph(c);
     ck(cudaStreamSynchronize(c->stream), "sync");
     cs.lib_arena.release();
+    while (rec.size() % 4) rec.push_back(0.f);
     cs.dev.lut = cs.lib_arena.upload(rec, c->stream);
     cs.lut_bytes = rec.size() * sizeof(float);
-    size_t bytes = 0;                          // the staged pool must fit every corner's
-    for (const CornerState& o : c->corners) bytes = std::max(bytes, o.lut_bytes);
-    c->lut_f4 = bytes <= sta::kLutSmemMax ? (u32)(bytes / 16) : 0;
-    if (c->lut_f4 && bytes > 48 * 1024) ck(sta::set_lut_smem_limit(bytes), "smem attribute");
-    c->pgrid = c->use_persistent ? sta::persistent_grid(c->lut_f4, 0) : 0;
-  c->pgrid_b = c->use_persistent ? sta::persistent_grid(c->lut_f4, 1) : 0;
+    cs.dev.lut_n4 = (u32)(rec.size() / 4);   // each corner stages its own pool size
+    size_kernels(c);
     ck(cudaStreamSynchronize(c->stream), "library upload");
     cs.lib = true;
   });
@@ -1456,9 +1481,9 @@ sta_status sta_set_rc_tree(sta_ctx c, sta_mem mem, const uint32_t* rc_ptr, uint3
     c->prepared = false;
     for (CornerState& cs : c->corners) cs.rcv = false;
     c->n_rc = num_nodes;
-    c->rc_ptr = fetch(rc_ptr, c->N + 1, mem, "rc_ptr");
-    c->rc_parent = fetch(parent, num_nodes, mem, "parent");
-    c->rc_node_pin = fetch(node_pin, num_nodes, mem, "node_pin");
+    c->rc_ptr = fetch(rc_ptr, c->N + 1, mem, "rc_ptr", c->stream);
+    c->rc_parent = fetch(parent, num_nodes, mem, "parent", c->stream);
+    c->rc_node_pin = fetch(node_pin, num_nodes, mem, "node_pin", c->stream);
     build_rc(c);
     c->has_tree = true;
   });
@@ -1470,35 +1495,33 @@ sta_status sta_set_rc_values(sta_ctx c, uint32_t corner, sta_mem mem, const floa
     if (!c->has_tree) fail(STA_ERR_ORDER, "sta_set_rc_values before sta_set_rc_tree");
     if (c->n_rc && (!res || !cap)) fail(STA_ERR_ARG, "res/cap NULL");
     if (mem == STA_MEM_DEVICE) {
-      ck(cudaStreamSynchronize(c->stream), "sync");   // owned buffers may be in use
-      cs.rc_arena.release();
+      if (!cs.rc_arena.ptrs.empty()) {         // owned buffers of an earlier HOST call may be in use
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        cs.rc_arena.release();
+      }
       cs.rc_res = res;
       cs.rc_cap = cap;
     } else if (mem == STA_MEM_HOST) {
-      for (u32 i = 0; i < c->n_rc; ++i) {
-        if (!(res[i] >= 0.f) || !std::isfinite(res[i])) fail(STA_ERR_RC, "node %u: bad resistance", i);
-        if (!(cap[i] >= 0.f) || !std::isfinite(cap[i])) fail(STA_ERR_RC, "node %u: bad capacitance", i);
-      }
-      if (!cs.rc_arena.ptrs.empty() && cs.rc_res && cs.rc_arena.bytes >= 2ull * c->n_rc * sizeof(float)) {
-        // reuse owned buffers
-      } else {
+      // copied into owned device buffers in stream order (page-locked caller
+      // buffers: DMA at link speed); the values are validated on the device by
+      // the RC kernels (STA_ERR_RC at the next synchronizing call)
+      if (cs.rc_arena.ptrs.empty() || cs.rc_arena.bytes < 2ull * c->n_rc * sizeof(float)) {
+        ck(cudaStreamSynchronize(c->stream), "sync");
         cs.rc_arena.release();
-        float* r = cs.rc_arena.alloc<float>(c->n_rc);
-        float* k = cs.rc_arena.alloc<float>(c->n_rc);
-        cs.rc_res = r;
-        cs.rc_cap = k;
+        cs.rc_res = cs.rc_arena.alloc<float>(c->n_rc);
+        cs.rc_cap = cs.rc_arena.alloc<float>(c->n_rc);
       }
       if (c->n_rc) {
         ck(cudaMemcpyAsync(const_cast<float*>(cs.rc_res), res, sizeof(float) * c->n_rc, cudaMemcpyHostToDevice,
                            c->stream), "H2D");
         ck(cudaMemcpyAsync(const_cast<float*>(cs.rc_cap), cap, sizeof(float) * c->n_rc, cudaMemcpyHostToDevice,
                            c->stream), "H2D");
-        ck(cudaStreamSynchronize(c->stream), "sync");
       }
     } else {
       fail(STA_ERR_ARG, "bad sta_mem %d", (int)mem);
     }
     publish_rc_pointers(c, cs);
+    if (mem == STA_MEM_HOST) ck(cudaStreamSynchronize(c->stream), "sync");   // host buffers read before return
     cs.rcv = true;
   });
 }
@@ -1509,13 +1532,13 @@ sta_status sta_set_constraints(sta_ctx c, const sta_constraints* k) {
     if (!c->has_graph) fail(STA_ERR_ORDER, "sta_set_constraints before sta_load_graph");
     if (!(k->period_ps > 0.f) || !std::isfinite(k->period_ps)) fail(STA_ERR_ARG, "period must be > 0");
     if (!(k->clock_slew_ps >= 0.f) || !std::isfinite(k->clock_slew_ps)) fail(STA_ERR_ARG, "clock slew must be >= 0");
-    auto pi_pin = fetch(k->pi_pin, k->n_pi, k->mem, "pi_pin");
-    auto pi_at = fetch(k->pi_at, 4ull * k->n_pi, k->mem, "pi_at");
-    auto pi_slew = fetch(k->pi_slew, 4ull * k->n_pi, k->mem, "pi_slew");
-    auto po_pin = fetch(k->po_pin, k->n_po, k->mem, "po_pin");
-    auto po_max = fetch(k->po_out_max, 2ull * k->n_po, k->mem, "po_out_max");
-    auto po_min = fetch(k->po_out_min, 2ull * k->n_po, k->mem, "po_out_min");
-    auto po_ld = fetch(k->po_load_ff, k->n_po, k->mem, "po_load_ff");
+    auto pi_pin = fetch(k->pi_pin, k->n_pi, k->mem, "pi_pin", c->stream);
+    auto pi_at = fetch(k->pi_at, 4ull * k->n_pi, k->mem, "pi_at", c->stream);
+    auto pi_slew = fetch(k->pi_slew, 4ull * k->n_pi, k->mem, "pi_slew", c->stream);
+    auto po_pin = fetch(k->po_pin, k->n_po, k->mem, "po_pin", c->stream);
+    auto po_max = fetch(k->po_out_max, 2ull * k->n_po, k->mem, "po_out_max", c->stream);
+    auto po_min = fetch(k->po_out_min, 2ull * k->n_po, k->mem, "po_out_min", c->stream);
+    auto po_ld = fetch(k->po_load_ff, k->n_po, k->mem, "po_load_ff", c->stream);
     std::vector<uint8_t> seen(c->P, 0);
     for (u32 i = 0; i < k->n_pi; ++i) {
       const u32 p = pi_pin[i];
@@ -1622,7 +1645,9 @@ sta_status sta_get_levels(sta_ctx c, uint32_t* level, uint32_t* perm, uint32_t* 
     auto put = [&](uint32_t* dst, const std::vector<u32>& v) {
       if (!dst || v.empty()) return;
       if (mem == STA_MEM_HOST) std::memcpy(dst, v.data(), v.size() * sizeof(u32));
-      else ck(cudaMemcpy(dst, v.data(), v.size() * sizeof(u32), cudaMemcpyHostToDevice), "H2D");
+      else if (mem == STA_MEM_DEVICE)
+        ck(cudaMemcpyAsync(dst, v.data(), v.size() * sizeof(u32), cudaMemcpyHostToDevice, c->stream), "H2D");
+      else fail(STA_ERR_ARG, "bad sta_mem %d", (int)mem);
     };
     put(level, c->level);
     put(perm, c->perm);
@@ -1645,6 +1670,7 @@ sta_status sta_get_info(sta_ctx c, sta_info* o) {
     o->num_sink_pins = c->NS;
     o->num_heavy_drivers = c->n_heavy;
     o->kernels_per_update = c->launches_per_update;
+    o->lut_smem_bytes = 16u * c->smem_f4;
     uint64_t b = c->graph_arena.bytes + c->tree_arena.bytes + c->cons_arena.bytes;
     for (auto& cs : c->corners) b += cs.lib_arena.bytes + cs.rc_arena.bytes + cs.state_arena.bytes;
     o->device_bytes = b;

@@ -27,28 +27,26 @@ constexpr uint32_t kBNet = 1024;               // RC tier B: nets of 33..1024 no
 constexpr uint32_t kChunk = 256;               // stage id padding; readiness group of the persistent kernels
 constexpr uint32_t kWarpUnit = 32;             // persistent kernels: items per warp unit
 constexpr uint32_t kFwdUnitTerms = 8;          // forward warp unit: fan-in terms (4 lanes each)
-// persistent kernels: co-resident 256-thread blocks per SM (register budget;
-// tuned on C3: the forward's short per-lane chains want many warps, the
-// backward's one-lane-per-sink chains want registers)
-#ifndef STA_FWD_BLOCKS
-#define STA_FWD_BLOCKS 4
-#endif
-#ifndef STA_BWD_BLOCKS
-#define STA_BWD_BLOCKS 5
-#endif
-constexpr int kFwdMinBlocks = STA_FWD_BLOCKS;
+// Persistent kernels: ONE block per SM holding all of the SM's warps, so the
+// staged NLDM pools of every corner of a batch exist once per SM (8 corners of
+// LIB-SYN = 190 KB).  Warps per SM are the register budget tuned on C3 (the
+// forward's short per-lane chains want many warps, the backward's one-lane-per-
+// sink chains want registers): 32 forward warps (<= 64 registers), 20 backward
+// warps (<= 102 registers).
 #ifndef STA_FWD_THREADS
-#define STA_FWD_THREADS 256
+#define STA_FWD_THREADS 1024
 #endif
 constexpr int kFwdThreads = STA_FWD_THREADS;    // forward persistent kernel block size
-constexpr int kBwdMinBlocks = STA_BWD_BLOCKS;
+constexpr int kFwdMinBlocks = 1;
 #ifndef STA_BWD_THREADS
-#define STA_BWD_THREADS 128
+#define STA_BWD_THREADS 640
 #endif
 constexpr int kBwdThreads = STA_BWD_THREADS;    // backward persistent kernel block size
+constexpr int kBwdMinBlocks = 1;
 #ifndef STA_BWD_PIPE
 #define STA_BWD_PIPE 1                          // backward: prefetch the next unit's fan-out records
 #endif
+constexpr uint32_t kMaxBatch = 8;               // corners traversed by one launch
 
 // Device NLDM table pool (built by sta_set_library), shared-memory friendly:
 //   * table t: a block of kTabStride = 65 floats at t * 65: word 0 = offset
@@ -132,38 +130,35 @@ struct Topo {
   // nodes, B: 33..kBNet, C: larger), each group in driver order.
   const uint32_t* net_drv;   // [N] internal pull id of the driver
   const float* net_lumped;   // [N] lumped load (nets without RC nodes)
-  const uint32_t* node_user; // [n_rc] caller node id (R / Cw are in caller order)
-  const uint32_t* node_meta; // [n_rc] pos | parent pos << 8 (0xFF: root) | end << 16 (nets <= 32 nodes)
-  const uint32_t* node_tag;  // [n_rc] sink index, driver | 0x80000000 at the root, or kNone
-  const float* rc_scap;      // [n_rc] pin cap + PO load at the node
-  const uint4* rc_node;      // [tier A + B nodes] {node_meta, node_tag, node_user, rc_scap bits} packed
-  uint32_t n_wtiles;         // warp tiles of nets with 1..32 nodes (no net straddles a tile)
-  const uint2* wtiles;       // {first internal node, node count}
+  // per internal RC node: meta = pos | parent pos << 8 (0xFF: root) | end << 16
+  // (tier A); tag = sink index, driver | 0x80000000 at the root, or kNone;
+  // scap = pin cap + PO load at the node (R / Cw stay in the caller's order)
+  const uint4* rc_node;      // [tier A + B nodes] {meta, tag, caller node (tier B) or caller
+                             //  offset in the warp tile (tier A), scap bits} packed
+  uint32_t n_wtiles;         // warp tiles of nets with 1..32 nodes (no net straddles a tile; the
+                             // tile's caller nodes are one contiguous range)
+  const uint4* wtiles;       // {first internal node, node count, first caller node, 0}
   // tier B: nets with 33..kBNet nodes, whole nets in block tiles of <= kBNet
   // contiguous nodes; their node_meta is pos | parent pos << 10 (0x7FF: root) | end << 21
   uint32_t n_btiles;
   const uint2* btiles;       // {first internal node, node count}
   uint32_t n_lumped;
   const uint32_t* lumped_j;  // nets without RC nodes
-  uint32_t nC;               // nets with > 32 nodes
-  // tier C (nets > kBNet nodes), Euler-tour form over ONE global preorder
-  // array of all tier-C nodes (each net contiguous, DFS preorder inside) and
-  // its Euler event sequence (enter / exit of every node, 2 per node; a net
-  // whose root sits at position g0 owns events [2 g0, 2 g0 + 2 m)):
-  // Cdown(g) = S[end(g)] - S[g] with S the global exclusive prefix sum of the
-  // node caps in preorder; with w = R Cdown, event values +w(a) at enter(a)
-  // and -w(a) at exit(a), and H their inclusive prefix sum,
-  // elm(g) = H[enter(g)] - H[2 g0 - 1] (the ancestors-or-self of g are exactly
-  // the nodes entered and not yet exited at enter(g)).
+  uint32_t nC;               // nets with > kBNet nodes (tier C)
+  // tier C (nets > kBNet nodes): segmented prefix sums over ONE global
+  // preorder array of their nodes (each net contiguous, DFS preorder inside,
+  // the net's root its segment head) and over its Euler event sequence
+  // (enter / exit of every node, 2 per node; a net whose root sits at
+  // position g0 owns events [2 g0, 2 g0 + 2 m), its first event entering the
+  // root).  With Sx / Si the segmented exclusive / inclusive sums of the node
+  // caps, Cdown(g) = Si[end(g) - 1] - Sx[g]; with w = R Cdown, event values
+  // +w(a) at enter(a), -w(a) at exit(a) and H their segmented inclusive sum,
+  // elm(g) = H[enter(g)] (the ancestors-or-self of g are exactly the nodes
+  // entered and not yet exited there).
   uint32_t nCn;               // tier-C nodes
-  const uint32_t* tc_user;    // [nCn] caller node id (R / Cw index)
-  const uint32_t* tc_int;     // [nCn] internal node id (scap / tag index) | 0x80000000 at a net root
-  const uint32_t* tc_end;     // [nCn] global position one past the subtree
-  const uint32_t* tc_start;   // [nCn] global position of the net's root
-  const uint32_t* tc_enter;   // [nCn] event position of enter(g)
+  const uint4* tc_node;       // [nCn] {caller node id, tag (as node_tag), end (global position one
+                              //  past the subtree), rc_scap bits}
   const uint32_t* tc_ev;      // [2 nCn] node position of each event | 0x80000000 for an exit
-  const uint32_t* tc_root;    // [nC] root position of each tier-C net
-  const uint32_t* tc_drv;     // [nC] its driver (internal pull id)
   // outputs to user order
   const uint32_t* int_of_user; // [P]
   const uint32_t* drv_of_net;  // [N] user net -> internal driver
@@ -187,41 +182,57 @@ struct CornerDev {
   float4* heavy_part; // [heavy tiles] partial required time of each heavy-driver tile
   uint32_t* heavy_cnt;// [n_heavy] finished tiles (self-resetting)
   const float* lut;   // table records (kTabStride floats each)
+  uint32_t lut_n4;    // float4s of this corner's pool
+  uint32_t lut_off4;  // float4 offset of this corner's pool in a batch's shared-memory image
   const float* const* rc_vals;  // device {res, cap} pointer pair (user node order)
-  double* scratch;    // tier-C scratch (tierC_scratch; tickets / flags zero between updates)
+  double* scratch;    // tier-C scratch (tierC_scratch)
   uint32_t* err_flag; // nonzero: bad RC value seen
   unsigned long long* trace;  // optional (STA_TRACE): per warp unit {start, ready, end} ns
+};
+
+// The corners one launch traverses.  Persistent kernels bind warp w to corner
+// w % K and walk that corner's unit list with stride W / K, so the K corners'
+// wavefronts advance together: one dependent-latency chain serves all K (a
+// corner's stage-to-stage latency is paid once per batch, not once per
+// corner), and the K warps reading the same unit's topology meet in L2.
+struct Batch {
+  CornerDev c[kMaxBatch];
+  uint32_t K;
+  uint32_t smem_f4;   // float4s of the staged LUT image (the K pools back to back); 0: global
 };
 
 constexpr int kRedBlocks = 4 * 148;
 
 // ---- launchers (sta_kernels.cu); all enqueue on `s` with programmatic
-// dependent launch, return cudaGetLastError()
+// dependent launch, return cudaGetLastError().  Every launch covers the
+// corners of batch b (grid.y = corner for the data-parallel kernels).
 // RC of nets with <= kBNet nodes and lumped nets; tier C (nets > kBNet nodes) is
-// independent of it and is enqueued on a second stream (1 cooperative launch)
-cudaError_t launch_rc(const Topo& t, const CornerDev& c, cudaStream_t s);
-cudaError_t launch_rc_tierC(const Topo& t, const CornerDev& c, cudaStream_t s);
-// tier-C scratch, doubles: S[n+1], H[2n], W[n], block sums[kTcMaxGrid], then
-// the grid barrier {count, generation} (u32, zero-initialised, self-resetting)
-constexpr uint32_t kTcMaxGrid = 1024;
-inline size_t tierC_scratch(uint32_t nCn) { return 4 * (size_t)nCn + 1 + kTcMaxGrid + 1; }
-// lut_f4: float4 count of the table pool staged in shared memory per block
-// (0: the pool is too large, lookups read global memory)
-// units [u0, u1) of one gate stage (one launch per stage)
-cudaError_t launch_fwd_stage(const Topo& t, const CornerDev& c, uint32_t u0, uint32_t u1, uint32_t lut_f4,
-                             cudaStream_t s);
-cudaError_t launch_bwd_stage(const Topo& t, const CornerDev& c, uint32_t u0, uint32_t u1, uint32_t lut_f4,
-                             cudaStream_t s);
+// independent of it and is enqueued on a second stream (3 launches)
+cudaError_t launch_rc(const Topo& t, const Batch& b, uint32_t wgrid, cudaStream_t s);
+cudaError_t launch_rc_tierC(const Topo& t, const Batch& b, cudaStream_t s);
+// tier-C scratch (doubles): Sx/Si pairs [2 nCn], event sums [2 nCn], then per
+// scan (2) and block: {aggregate, carry, first head, has head}, then the two
+// last-block counters (u32, zero-initialised, self-resetting)
+constexpr uint32_t kTcTile = 2048;              // elements per tier-C block (256 threads x 8)
+__host__ __device__ inline uint32_t tierC_blocks(uint64_t n) { return (uint32_t)((n + kTcTile - 1) / kTcTile); }
+__host__ __device__ inline size_t tierC_scratch(uint32_t nCn) {
+  return 4 * (size_t)nCn + 2 * 4 * (size_t)tierC_blocks(2ull * nCn) + 2;
+}
+uint32_t rc_warp_grid();                        // co-resident grid of the tier-A kernel (per corner)
+// units [u0, u1) of one gate stage (one launch per stage, grid.y = corner)
+cudaError_t launch_fwd_stage(const Topo& t, const Batch& b, uint32_t u0, uint32_t u1, cudaStream_t s);
+cudaError_t launch_bwd_stage(const Topo& t, const Batch& b, uint32_t u0, uint32_t u1, cudaStream_t s);
 cudaError_t set_lut_smem_limit(size_t bytes);
 // persistent (cooperative, sync-free dataflow) forward / backward passes;
-// grid = co-resident blocks.  persistent_grid returns 0 if unsupported.
-uint32_t persistent_grid(uint32_t lut_f4, int which);
-cudaError_t launch_fwd_persistent(const Topo& t, const CornerDev& c, uint32_t grid, uint32_t lut_f4, cudaStream_t s);
-cudaError_t launch_bwd_persistent(const Topo& t, const CornerDev& c, uint32_t grid, uint32_t lut_f4, cudaStream_t s);
-constexpr size_t kLutSmemMax = 160 * 1024;   // larger pools stay in global memory
-cudaError_t launch_reduce(const Topo& t, const CornerDev& c, cudaStream_t s);
+// grid = co-resident blocks (one per SM).  persistent_grid returns 0 if unsupported.
+uint32_t persistent_grid(uint32_t smem_f4, int which);
+cudaError_t launch_fwd_persistent(const Topo& t, const Batch& b, uint32_t grid, cudaStream_t s);
+cudaError_t launch_bwd_persistent(const Topo& t, const Batch& b, uint32_t grid, cudaStream_t s);
+constexpr size_t kLutSmemMax = 200 * 1024;   // larger batch images stay in global memory
+cudaError_t launch_reduce(const Topo& t, const Batch& b, cudaStream_t s);
 cudaError_t launch_gather_pins(const Topo& t, const CornerDev& c, int what, float4* dst, cudaStream_t s);
 cudaError_t launch_gather_rc(const Topo& t, const CornerDev& c, float* net_load, float* pin_elm, cudaStream_t s);
 cudaError_t launch_init_corner(const Topo& t, const CornerDev& c, uint32_t n_heavy, cudaStream_t s);
+cudaError_t launch_set_ptrs(const float* const* dst, const float* a, const float* b, cudaStream_t s);
 
 }  // namespace sta

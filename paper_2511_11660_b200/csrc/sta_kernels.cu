@@ -110,18 +110,29 @@ __device__ __forceinline__ int primary_irf(uint32_t sense, int orf) {
   return sense == 1 ? 1 - orf : sense == 3 ? 0 : sense == 4 ? 1 : orf;
 }
 
-// Copy the table records into shared memory (static data: may run before
-// griddepcontrol.wait).  Returns the pointer lookups should use.  SMEM is a
-// compile-time choice so that lookups compile to LDS (a pointer that may be
-// shared or global compiles to slow generic loads).
+// Copy the table pools of the batch's corners into shared memory, each at its
+// lut_off4 (static data: may run before griddepcontrol.wait); `only` < K
+// stages one corner.  Each corner copies its OWN pool size (pools of
+// different corners may differ).  SMEM is a compile-time choice so that
+// lookups compile to LDS (a pointer that may be shared or global compiles to
+// slow generic loads).
 extern __shared__ float4 s_dyn[];
 template <bool SMEM>
-__device__ __forceinline__ const float* stage_lut(const CornerDev& c, uint32_t n_f4) {
-  if (!SMEM) return c.lut;                   // pool too large: global / L1
-  const float4* g = reinterpret_cast<const float4*>(c.lut);
-  for (uint32_t x = threadIdx.x; x < n_f4; x += blockDim.x) s_dyn[x] = __ldg(g + x);
-  __syncthreads();
-  return reinterpret_cast<const float*>(s_dyn);
+__device__ __forceinline__ void stage_luts(const Batch& b, uint32_t only) {
+  if constexpr (SMEM) {                      // else pools too large: global / L1
+    for (uint32_t k = 0; k < b.K; ++k) {
+      if (only < b.K && k != only) continue;
+      const CornerDev& c = b.c[k];
+      const float4* g = reinterpret_cast<const float4*>(c.lut);
+      for (uint32_t x = threadIdx.x; x < c.lut_n4; x += blockDim.x) s_dyn[c.lut_off4 + x] = __ldg(g + x);
+    }
+    __syncthreads();
+  }
+}
+// the pool lookups of corner c should use
+template <bool SMEM>
+__device__ __forceinline__ const float* lut_of(const CornerDev& c) {
+  return SMEM ? reinterpret_cast<const float*>(s_dyn + c.lut_off4) : c.lut;
 }
 
 // Net arc driver -> sink: AT + elm, slew = sqrt(slew^2 + (ln9 elm)^2) (PERI,
@@ -147,15 +158,18 @@ __device__ __forceinline__ void net_hop(Q4& at, Q4& sl, float e) {
 // needed, and a consumer detects readiness with the same L2 round trip that
 // fetches the data (a producer -> consumer hop measured 265 ns vs 920 ns for
 // data + release flag + poll + load, scripts/ubench/pingpong.cu).
+// Each {value, tag} half is ONE 64-bit access (ld/st .v2.u64: two single-copy
+// atomic 8-byte elements), so a reader can never pair a new tag with a stale
+// value; the u32 view {value, tag, value, tag} is the same bytes.
 __device__ __forceinline__ uint4 ld_ll(const uint4* p) {
-  uint4 w;
-  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w) : "l"(p) : "memory");
-  return w;
+  unsigned long long a, b;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+  return make_uint4((uint32_t)a, (uint32_t)(a >> 32), (uint32_t)b, (uint32_t)(b >> 32));
 }
 __device__ __forceinline__ void st_ll(uint4* p, float a, float b, uint32_t ep) {
-  asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};"
-               ::"l"(p), "r"(__float_as_uint(a)), "r"(ep), "r"(__float_as_uint(b)), "r"(ep) : "memory");
+  const unsigned long long x = (unsigned long long)__float_as_uint(a) | ((unsigned long long)ep << 32);
+  const unsigned long long y = (unsigned long long)__float_as_uint(b) | ((unsigned long long)ep << 32);
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(x), "l"(y) : "memory");
 }
 __device__ __forceinline__ bool ll_ok(const uint4& w, uint32_t ep) { return w.y == ep && w.w == ep; }
 // polling backoff cap: a waiter notices a completed record at most this late
@@ -191,35 +205,48 @@ __device__ __forceinline__ bool bad_rc(float r, float cw) {
   return !(r >= 0.f) || !(cw >= 0.f) || !(r < CUDART_INF_F) || !(cw < CUDART_INF_F);
 }
 
-// Nets with 1..32 RC nodes: one warp tile holds whole nets, one lane per
+// Tier A, nets with 1..32 RC nodes: a warp tile holds whole nets, one lane per
 // node in DFS preorder.  Cdown(p) = S[end(p)] - S[p] with S the segmented
 // exclusive prefix sum of node caps (shuffle scan), Elmore(p) = sum of
 // R * Cdown over the root path by pointer jumping over parent lanes (5
-// rounds), all in fp64; every node is read once, coalesced.
-__global__ void __launch_bounds__(kThreads) rc_warp_kernel(Topo t, CornerDev c) {
-  pdl_wait();
-  pdl_launch();
+// rounds), all in fp64.  A tile's nodes are one contiguous range of the
+// caller's (borrowed) R / Cw arrays, so lane l loads caller node base + l
+// together with its topology record -- one memory round trip, no dependent
+// gather -- and the values move to their preorder lanes by a shuffle.  Warps
+// are persistent (grid = co-resident warps per corner) and load the next tile
+// while the current one computes.
+struct WTile {
+  uint4 tile;     // {first internal node, node count, first caller node, 0}
+  uint4 nd;       // this lane's node record
+  float r, cw;    // caller node base + lane
+};
+
+__device__ __forceinline__ void wtile_load(const Topo& t, const float* __restrict__ R, const float* __restrict__ Cw,
+                                           const uint4& tile, WTile& w) {
   const int lane = threadIdx.x & 31;
-  const uint32_t wt = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (wt >= t.n_wtiles) return;
-  const uint2 tile = t.wtiles[wt];
-  const bool act = lane < (int)tile.y;
-  const uint32_t x = tile.x + lane;
-  uint32_t meta = 0, tag = kNone;
-  double C = 0.0;
-  float r = 0.f;
-  bool bad = false;
-  if (act) {
-    const uint4 nd = __ldg(t.rc_node + x);   // {meta, tag, caller node, static cap}
-    meta = nd.x;
-    tag = nd.y;
-    const float cw = c.rc_vals[1][nd.z];
-    const bool root = ((meta >> 8) & 0xFFu) == 0xFFu;
-    r = root ? 0.f : c.rc_vals[0][nd.z];
-    bad = bad_rc(r, cw);
-    C = (double)cw + (double)__uint_as_float(nd.w);
+  w.tile = tile;
+  w.nd = make_uint4(0, kNone, 0, 0);
+  w.r = 0.f;
+  w.cw = 0.f;
+  if (lane < (int)tile.y) {
+    w.nd = __ldg(t.rc_node + tile.x + lane);
+    w.r = __ldcs(R + tile.z + lane);
+    w.cw = __ldcs(Cw + tile.z + lane);
   }
+}
+
+__device__ __forceinline__ void wtile_run(const CornerDev& c, const WTile& w) {
+  const int lane = threadIdx.x & 31;
+  const bool act = lane < (int)w.tile.y;
+  const uint32_t meta = w.nd.x, tag = w.nd.y;
+  const int q = (int)(w.nd.z & 31u);
+  const float rr = __shfl_sync(0xFFFFFFFFu, w.r, q);      // R / Cw of this lane's caller node
+  const float cw = __shfl_sync(0xFFFFFFFFu, w.cw, q);
   const int pos = (int)(meta & 0xFFu), ppos = (int)((meta >> 8) & 0xFFu), epos = (int)((meta >> 16) & 0xFFu);
+  const bool root = ppos == 0xFF;
+  const float r = root ? 0.f : rr;
+  const bool bad = act && bad_rc(r, cw);
+  const double C = act ? (double)cw + (double)__uint_as_float(w.nd.w) : 0.0;
   // segmented inclusive scan of C (a net's lanes are contiguous; pos resets)
   double inc = C;
 #pragma unroll
@@ -233,8 +260,8 @@ __global__ void __launch_bounds__(kThreads) rc_warp_kernel(Topo t, CornerDev c) 
   const double s_end = __shfl_sync(0xFFFFFFFFu, inc, act ? seg0 + epos - 1 : lane);
   const double cd = s_end - exc;            // subtree cap of this node
   // root path sums of w = R * Cdown by pointer jumping
-  double val = (act && ppos != 0xFF) ? (double)r * cd : 0.0;
-  int pl = (act && ppos != 0xFF) ? seg0 + ppos : -1;
+  double val = (act && !root) ? (double)r * cd : 0.0;
+  int pl = (act && !root) ? seg0 + ppos : -1;
 #pragma unroll
   for (int k = 0; k < 5; ++k) {
     const double pv = __shfl_sync(0xFFFFFFFFu, val, pl >= 0 ? pl : lane);
@@ -249,6 +276,28 @@ __global__ void __launch_bounds__(kThreads) rc_warp_kernel(Topo t, CornerDev c) 
     else c.elm[tag] = (float)val;
   }
   if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(c.err_flag, 1u);
+}
+
+__global__ void __launch_bounds__(kThreads) rc_warp_kernel(Topo t, const __grid_constant__ Batch B) {
+  pdl_wait();
+  pdl_launch();
+  const CornerDev& c = B.c[blockIdx.y];
+  const float* R = c.rc_vals[0];
+  const float* Cw = c.rc_vals[1];
+  const uint32_t W = gridDim.x * (kThreads / 32);
+  uint32_t x = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  if (x >= t.n_wtiles) return;
+  const uint4 none = make_uint4(0, 0, 0, 0);
+  WTile cur;
+  wtile_load(t, R, Cw, __ldg(t.wtiles + x), cur);
+  uint4 nx = x + W < t.n_wtiles ? __ldg(t.wtiles + x + W) : none;
+  for (; x < t.n_wtiles; x += W) {
+    WTile nxt;
+    wtile_load(t, R, Cw, nx, nxt);          // next tile's loads in flight during this one
+    if (x + 2 * W < t.n_wtiles) nx = __ldg(t.wtiles + x + 2 * W);
+    wtile_run(c, cur);
+    cur = nxt;
+  }
 }
 
 __device__ __forceinline__ double block_excl_scan(double v, double* s_warp, double* total) {
@@ -286,12 +335,13 @@ __device__ __forceinline__ double block_excl_scan(double v, double* s_warp, doub
 // slots until every node reaches its root, fp64 throughout.
 constexpr uint32_t kBPer = kBNet / kThreads;
 
-__global__ void __launch_bounds__(kThreads) rc_block_kernel(Topo t, CornerDev c) {
+__global__ void __launch_bounds__(kThreads) rc_block_kernel(Topo t, const __grid_constant__ Batch B) {
   __shared__ double s_S[kBNet + 1], s_v[kBNet];
   __shared__ int16_t s_p[kBNet];
   __shared__ double s_warp[32];
   pdl_wait();
   pdl_launch();
+  const CornerDev& c = B.c[blockIdx.y];
   const uint2 tile = t.btiles[blockIdx.x];
   const uint32_t i0 = threadIdx.x * kBPer;
   uint32_t meta[kBPer], tag[kBPer];
@@ -369,9 +419,10 @@ __global__ void __launch_bounds__(kThreads) rc_block_kernel(Topo t, CornerDev c)
 }
 
 // nets without RC nodes: load = their pins' caps, no wire delay
-__global__ void __launch_bounds__(kThreads) rc_lumped_kernel(Topo t, CornerDev c) {
+__global__ void __launch_bounds__(kThreads) rc_lumped_kernel(Topo t, const __grid_constant__ Batch B) {
   pdl_wait();
   pdl_launch();
+  const CornerDev& c = B.c[blockIdx.y];
   const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= t.n_lumped) return;
   const uint32_t j = t.lumped_j[x];
@@ -380,242 +431,232 @@ __global__ void __launch_bounds__(kThreads) rc_lumped_kernel(Topo t, CornerDev c
   for (uint32_t k = t.sink_ptr[drv]; k < t.sink_ptr[drv + 1]; ++k) c.elm[k] = 0.f;
 }
 
-// L2-only loads (ld.global.cg): the records reached L2 before the flag
-// (producer fence), the consumer's record loads are issued only after the
-// flag value returned (control dependency), and no L1 copy can be stale.  An
-// ld.acquire.gpu here would compile to CCTL.IVALL (whole-L1 invalidate),
-// which profiling showed to cost half of the kernel time.
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
+// ---- tier C: segmented prefix sums over ONE global preorder array of the
+// large nets' nodes and over its Euler event sequence (layout in
+// sta_internal.h).  Three data-parallel launches per corner on a side stream,
+// concurrent with tiers A and B:
+//   tc_node_kernel   node caps C -> block-local segmented inclusive sums Si
+//                    (segment = net), block aggregates; the last block turns
+//                    the aggregates into per-block carries;
+//   tc_event_kernel  w(g) = R(g) Cdown(g), Cdown(g) = Si[end(g) - 1] - Si[g] +
+//                    C(g) (carried reads); event values +-w -> block-local
+//                    segmented sums H, block carries as above; net loads;
+//   tc_elm_kernel    elm(g) = H[enter(g)] (carried) for the sink nodes.
+// Every sum has a fixed association (thread-serial runs, fixed shuffle trees,
+// a fixed-order carry pass): bitwise reproducible.  A segmented scan never
+// crosses a net, so the sums stay small (no cancellation against the sums of
+// other nets) and a net's Elmore delays need no offset.
+struct SegSum {
+  double v;
+  uint32_t f;   // a segment head inside
+};
+// (a then b): b restarts at a head
+__device__ __forceinline__ SegSum seg_op(SegSum a, SegSum b) { return SegSum{b.f ? b.v : a.v + b.v, a.f | b.f}; }
+
+// Block-wide exclusive segmented scan of one SegSum per thread (kThreads
+// threads); *total receives the block's inclusive total.
+__device__ __forceinline__ SegSum seg_block_excl(SegSum x, SegSum* s_w, SegSum* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  SegSum inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    SegSum y{__shfl_up_sync(0xFFFFFFFFu, inc.v, o), __shfl_up_sync(0xFFFFFFFFu, inc.f, o)};
+    if (lane >= o) inc = seg_op(y, inc);
+  }
+  if (lane == 31) s_w[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    SegSum a = lane < kThreads / 32 ? s_w[lane] : SegSum{0.0, 0u};
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      SegSum y{__shfl_up_sync(0xFFFFFFFFu, a.v, o), __shfl_up_sync(0xFFFFFFFFu, a.f, o)};
+      if (lane >= o) a = seg_op(y, a);
+    }
+    s_w[lane] = a;                               // inclusive over warps
+  }
+  __syncthreads();
+  SegSum ex{__shfl_up_sync(0xFFFFFFFFu, inc.v, 1), __shfl_up_sync(0xFFFFFFFFu, inc.f, 1)};
+  if (lane == 0) ex = SegSum{0.0, 0u};
+  const SegSum r = w ? seg_op(s_w[w - 1], ex) : ex;
+  *total = s_w[kThreads / 32 - 1];
+  __syncthreads();
+  return r;
 }
 
-// ---- tier C: Euler-tour RC over one global preorder array (sta_internal.h)
-// One persistent cooperative kernel, two blocks per SM (a small footprint
-// next to the concurrently running small-net RC kernel), four phases
-// separated by grid barriers:
-//   1. S = exclusive prefix sum of the node caps (block ranges: local scan,
-//      block sums, barrier, offsets), S[n] = total;
-//   2. w(g) = R(g) (S[end(g)] - S[g]) in node order (0 at a net root), net loads;
-//   3. H = inclusive prefix sum of the Euler event values +-w;
-//   4. elm(g) = H[enter(g)] - H[2 g0 - 1].
-// Offsets are fixed-shape sums of the block sums: bitwise reproducible.
-constexpr int kTcThreads = 512;
-#ifndef STA_TC_BLOCKS
-#define STA_TC_BLOCKS 1                      // blocks per SM of the tier-C kernel
-#endif
-#ifndef STA_TC_BATCH
-#define STA_TC_BATCH 8
-#endif
-constexpr int kTcBatch = STA_TC_BATCH;       // elements in flight per thread
+constexpr int kTcPer = (int)(kTcTile / kThreads);   // consecutive elements per thread
 
-__device__ __forceinline__ void tc_grid_barrier(uint32_t* bar, uint32_t nblocks) {
-  __syncthreads();
+// per-scan block records in the scratch: agg[nb], carry[nb], first head[nb] (as double)
+struct TcScan {
+  double* agg;
+  double* carry;
+  double* fh;
+  double* hh;
+};
+__device__ __forceinline__ TcScan tc_scan(double* base, uint32_t nb) { return TcScan{base, base + nb, base + 2 * nb, base + 3 * nb}; }
+
+// Block b publishes {aggregate, first head, has head}; the last block to
+// finish turns all aggregates into carries (exclusive segmented scan over the
+// blocks, chunks of kThreads in a fixed order).
+__device__ void tc_publish(const TcScan& sc, uint32_t nb, SegSum agg, uint32_t first_head, uint32_t* counter,
+                           SegSum* s_w) {
+  __shared__ bool last;
   if (threadIdx.x == 0) {
-    const uint32_t gen = ld_acquire(bar + 1);
+    sc.agg[blockIdx.x] = agg.v;
+    sc.hh[blockIdx.x] = agg.f ? 1.0 : 0.0;
+    sc.fh[blockIdx.x] = (double)first_head;
     __threadfence();
-    if (atomicAdd(bar, 1u) == nblocks - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      uint32_t ns = 32;
-      while (ld_acquire(bar + 1) == gen) {
-        __nanosleep(ns);
-        ns = ns < 256 ? 2 * ns : ns;
-      }
-    }
-    __threadfence();
+    last = atomicAdd(counter, 1u) == nb - 1;
   }
   __syncthreads();
+  if (!last) return;
+  __threadfence();
+  SegSum run{0.0, 0u};
+  for (uint32_t b0 = 0; b0 < nb; b0 += kThreads) {
+    const uint32_t b = b0 + threadIdx.x;
+    const SegSum x = b < nb ? SegSum{__ldcg(sc.agg + b), __ldcg(sc.hh + b) != 0.0 ? 1u : 0u} : SegSum{0.0, 0u};
+    SegSum tot;
+    const SegSum ex = seg_block_excl(x, s_w, &tot);
+    if (b < nb) sc.carry[b] = seg_op(run, ex).v;
+    run = seg_op(run, tot);
+  }
+  if (threadIdx.x == 0) *counter = 0;          // self-reset for the next update
 }
 
-// fixed-tree sum of sums[0 .. b) (the offset of block b)
-__device__ __forceinline__ double tc_block_offset(const double* sums, uint32_t b, double* s_red) {
-  double v = 0.0;
-  for (uint32_t q = threadIdx.x; q < b; q += blockDim.x) v += __ldcg(sums + q);
-  s_red[threadIdx.x] = v;
-  __syncthreads();
-  for (int o = kTcThreads / 2; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) s_red[threadIdx.x] += s_red[threadIdx.x + o];
-    __syncthreads();
-  }
-  const double off = s_red[0];
-  __syncthreads();
-  return off;
+// carried read of a block-local segmented sum at global position g
+__device__ __forceinline__ double tc_read(const double* loc, const TcScan& sc, uint32_t g) {
+  const uint32_t b = g / kTcTile;
+  const double v = __ldcg(loc + g);
+  return (double)g < __ldcg(sc.fh + b) ? v + __ldcg(sc.carry + b) : v;
 }
 
-// Device-wide prefix scan of x, whose block range [lo, hi) the block wrote
-// with the strided mapping i = lo + threadIdx.x + k blockDim.x, each thread
-// also accumulating `part` (its values in that order).  Block sums, grid
-// barrier, offsets, then within the block: each thread sums a contiguous
-// chunk, one block-wide scan of the chunk sums, each thread rescans its chunk
-// (one block scan instead of one per row of blockDim.x values).  Fixed
-// shapes: bitwise reproducible.  Returns the inclusive prefix at hi.
-template <bool INCLUSIVE>
-__device__ __forceinline__ double tc_scan_range(double* x, size_t lo, size_t hi, double part, double* sums,
-                                                uint32_t* bar, double* s_warp, double* s_red) {
-  s_red[threadIdx.x] = part;
-  __syncthreads();
-  for (int o = kTcThreads / 2; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) s_red[threadIdx.x] += s_red[threadIdx.x + o];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) sums[blockIdx.x] = s_red[0];
-  tc_grid_barrier(bar, gridDim.x);
-  const double off = tc_block_offset(sums, blockIdx.x, s_red);
-  const size_t n = hi - lo, K = (n + blockDim.x - 1) / blockDim.x;
-  const size_t a = lo + min(n, (size_t)threadIdx.x * K), b = lo + min(n, (size_t)(threadIdx.x + 1) * K);
-  // (loads in groups of 8 ahead of the stores: a load after a store to the
-  // same array cannot be hoisted by the compiler and would pay a full memory
-  // latency per element)
-  constexpr int kG = 8;
-  double csum = 0.0;
-  for (size_t i0 = a; i0 < b; i0 += kG) {
-    double v[kG];
-#pragma unroll
-    for (int k = 0; k < kG; ++k) v[k] = i0 + k < b ? x[i0 + k] : 0.0;
-#pragma unroll
-    for (int k = 0; k < kG; ++k) csum += v[k];
-  }
-  double tot;
-  double carry = off + block_excl_scan(csum, s_warp, &tot);
-  for (size_t i0 = a; i0 < b; i0 += kG) {
-    double v[kG];
-#pragma unroll
-    for (int k = 0; k < kG; ++k) v[k] = i0 + k < b ? x[i0 + k] : 0.0;
-#pragma unroll
-    for (int k = 0; k < kG; ++k) {
-      if (i0 + k >= b) break;
-      if (INCLUSIVE) {
-        carry += v[k];
-        x[i0 + k] = carry;
-      } else {
-        x[i0 + k] = carry;
-        carry += v[k];
-      }
-    }
-  }
-  return off + tot;
-}
+__device__ __forceinline__ bool tc_head(uint32_t tag) { return tag != kNone && (tag & 0x80000000u); }
 
-__global__ void __launch_bounds__(kTcThreads, 2) tc_persistent_kernel(Topo t, CornerDev c) {
-  __shared__ double s_warp[32], s_red[kTcThreads];
+__global__ void __launch_bounds__(kThreads) tc_node_kernel(Topo t, const __grid_constant__ Batch B) {
+  __shared__ SegSum s_w[32];
   pdl_wait();
   pdl_launch();
-  const uint32_t n = t.nCn, G = gridDim.x, B = blockIdx.x, BD = blockDim.x;
-  const size_t m = 2 * (size_t)n;
-  double* S = c.scratch;                     // [n + 1]
-  double* H = S + n + 1;                     // [2n]
-  double* W = H + m;                         // [n]
-  double* sums = W + n;                      // [kTcMaxGrid]
-  uint32_t* bar = reinterpret_cast<uint32_t*>(sums + kTcMaxGrid);
+  const CornerDev& c = B.c[blockIdx.y];
+  const uint32_t n = t.nCn, nb = tierC_blocks(n);
+  double* Si = c.scratch;                                   // [nCn]
+  const TcScan sc = tc_scan(c.scratch + 4 * (size_t)n, nb);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(c.scratch + 4 * (size_t)n + 8 * (size_t)tierC_blocks(2ull * n));
+  const float* Cw = c.rc_vals[1];
+  const uint32_t g0 = blockIdx.x * kTcTile + threadIdx.x * kTcPer;
+  double v[kTcPer];
+  uint32_t hd = 0;
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < kTcPer; ++j) {
+    const uint32_t g = g0 + j;
+    v[j] = 0.0;
+    if (g < n) {
+      const uint4 nd = __ldg(t.tc_node + g);
+      const float cw = Cw[nd.x];
+      bad |= bad_rc(0.f, cw);
+      v[j] = (double)cw + (double)__uint_as_float(nd.w);
+      if (tc_head(nd.y)) hd |= 1u << j;
+    }
+  }
+  SegSum run{0.0, 0u};                       // thread-serial segmented inclusive run
+#pragma unroll
+  for (int j = 0; j < kTcPer; ++j) {
+    run = seg_op(run, SegSum{v[j], (hd >> j) & 1u});
+    v[j] = run.v;
+  }
+  SegSum tot;
+  const SegSum ex = seg_block_excl(run, s_w, &tot);
+#pragma unroll
+  for (int j = 0; j < kTcPer; ++j) {
+    const uint32_t g = g0 + j;
+    const bool before = (hd & ((2u << j) - 1u)) == 0;       // no head in this thread up to j
+    if (g < n) Si[g] = before ? ex.v + v[j] : v[j];
+  }
+  // first head of the block
+  __shared__ uint32_t s_fh;
+  if (threadIdx.x == 0) s_fh = kTcTile;
+  __syncthreads();
+  if (hd) atomicMin(&s_fh, threadIdx.x * kTcPer + (uint32_t)(__ffs(hd) - 1));
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(c.err_flag, 1u);
+  tc_publish(sc, nb, tot, blockIdx.x * kTcTile + s_fh, cnt, s_w);
+}
+
+__global__ void __launch_bounds__(kThreads) tc_event_kernel(Topo t, const __grid_constant__ Batch B) {
+  __shared__ SegSum s_w[32];
+  pdl_wait();
+  pdl_launch();
+  const CornerDev& c = B.c[blockIdx.y];
+  const uint32_t n = t.nCn, m = 2 * n, nbn = tierC_blocks(n), nb = tierC_blocks(m);
+  const double* Si = c.scratch;
+  double* H = c.scratch + n;                                // [2 nCn]
+  const TcScan scn = tc_scan(c.scratch + 4 * (size_t)n, nbn);
+  const TcScan sc = tc_scan(c.scratch + 4 * (size_t)n + 4 * (size_t)nb, nb);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(c.scratch + 4 * (size_t)n + 8 * (size_t)nb) + 1;
   const float* R = c.rc_vals[0];
   const float* Cw = c.rc_vals[1];
-  const size_t lo = (size_t)n * B / G, hi = (size_t)n * (B + 1) / G;
-  const size_t elo = m * B / G, ehi = m * (B + 1) / G;
-  const size_t step = (size_t)BD * kTcBatch;
-
-  // 1. node caps -> S (exclusive)
+  const uint32_t e0 = blockIdx.x * kTcTile + threadIdx.x * kTcPer;
+  double v[kTcPer];
+  uint32_t hd = 0;
   bool bad = false;
-  double part = 0.0;
-  for (size_t i0 = lo + threadIdx.x; i0 < hi; i0 += step) {
-    float cw[kTcBatch], sc[kTcBatch];
 #pragma unroll
-    for (int k = 0; k < kTcBatch; ++k) {
-      const size_t i = i0 + (size_t)k * BD;
-      const bool in = i < hi;
-      const uint32_t u = in ? t.tc_user[i] : 0u, ti = in ? t.tc_int[i] : 0u;
-      cw[k] = in ? Cw[u] : 0.f;
-      sc[k] = in ? t.rc_scap[ti & 0x7FFFFFFFu] : 0.f;
-    }
-#pragma unroll
-    for (int k = 0; k < kTcBatch; ++k) {
-      const size_t i = i0 + (size_t)k * BD;
-      if (i < hi) {
-        bad |= bad_rc(0.f, cw[k]);
-        const double v = (double)cw[k] + (double)sc[k];
-        S[i] = v;
-        part += v;
-      }
-    }
-  }
-  const double total = tc_scan_range<false>(S, lo, hi, part, sums, bar, s_warp, s_red);
-  if (B == G - 1 && threadIdx.x == 0) S[n] = total;
-  tc_grid_barrier(bar, G);
-
-  // 2. w in node order; net loads
-  for (size_t i0 = lo + threadIdx.x; i0 < hi; i0 += step) {
-    double w[kTcBatch];
-#pragma unroll
-    for (int k = 0; k < kTcBatch; ++k) {
-      const size_t i = i0 + (size_t)k * BD;
-      w[k] = 0.0;
-      if (i < hi && !(t.tc_int[i] & 0x80000000u)) {
-        const float r = R[t.tc_user[i]];
+  for (int j = 0; j < kTcPer; ++j) {
+    const uint32_t e = e0 + j;
+    v[j] = 0.0;
+    if (e < m) {
+      const uint32_t ev = __ldg(t.tc_ev + e);
+      const uint32_t g = ev & 0x7FFFFFFFu;
+      const bool exit = (ev >> 31) != 0;
+      const uint4 nd = __ldg(t.tc_node + g);
+      const bool root = tc_head(nd.y);
+      const double C = (double)Cw[nd.x] + (double)__uint_as_float(nd.w);
+      const double cd = tc_read(Si, scn, nd.z - 1) - tc_read(Si, scn, g) + C;
+      double w = 0.0;
+      if (!root) {
+        const float r = R[nd.x];
         bad |= bad_rc(r, 0.f);
-        w[k] = (double)r * (__ldcg(S + t.tc_end[i]) - __ldcg(S + i));
+        w = (double)r * cd;
+      } else if (!exit) {
+        c.load[nd.y & 0x7FFFFFFFu] = (float)cd;            // net load = Cdown(root)
+        hd |= 1u << j;                                      // a net's events start at its root's enter
       }
+      v[j] = exit ? -w : w;
     }
+  }
+  SegSum run{0.0, 0u};
 #pragma unroll
-    for (int k = 0; k < kTcBatch; ++k) {
-      const size_t i = i0 + (size_t)k * BD;
-      if (i < hi) W[i] = w[k];
-    }
+  for (int j = 0; j < kTcPer; ++j) {
+    run = seg_op(run, SegSum{v[j], (hd >> j) & 1u});
+    v[j] = run.v;
   }
-  for (uint32_t j = B * BD + threadIdx.x; j < t.nC; j += G * BD) {
-    const uint32_t r = t.tc_root[j];
-    c.load[t.tc_drv[j]] = (float)(__ldcg(S + t.tc_end[r]) - __ldcg(S + r));
+  SegSum tot;
+  const SegSum ex = seg_block_excl(run, s_w, &tot);
+#pragma unroll
+  for (int j = 0; j < kTcPer; ++j) {
+    const uint32_t e = e0 + j;
+    const bool before = (hd & ((2u << j) - 1u)) == 0;
+    if (e < m) H[e] = before ? ex.v + v[j] : v[j];
   }
+  __shared__ uint32_t s_fh;
+  if (threadIdx.x == 0) s_fh = kTcTile;
+  __syncthreads();
+  if (hd) atomicMin(&s_fh, threadIdx.x * kTcPer + (uint32_t)(__ffs(hd) - 1));
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(c.err_flag, 1u);
-  tc_grid_barrier(bar, G);
+  tc_publish(sc, nb, tot, blockIdx.x * kTcTile + s_fh, cnt, s_w);
+}
 
-  // 3. Euler event values -> H (inclusive)
-  part = 0.0;
-  for (size_t e0 = elo + threadIdx.x; e0 < ehi; e0 += step) {
-    double x[kTcBatch];
-#pragma unroll
-    for (int k = 0; k < kTcBatch; ++k) {
-      const size_t e = e0 + (size_t)k * BD;
-      x[k] = 0.0;
-      if (e < ehi) {
-        const uint32_t ev = t.tc_ev[e];
-        const double w = __ldcg(W + (ev & 0x7FFFFFFFu));
-        x[k] = (ev & 0x80000000u) ? -w : w;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < kTcBatch; ++k) {
-      const size_t e = e0 + (size_t)k * BD;
-      if (e < ehi) {
-        H[e] = x[k];
-        part += x[k];
-      }
-    }
-  }
-  tc_scan_range<true>(H, elo, ehi, part, sums, bar, s_warp, s_red);
-  tc_grid_barrier(bar, G);
-
-  // 4. elm of the sink nodes
-  for (size_t i0 = lo + threadIdx.x; i0 < hi; i0 += step) {
-    uint32_t k2[kTcBatch];
-    float v[kTcBatch];
-#pragma unroll
-    for (int k = 0; k < kTcBatch; ++k) {
-      const size_t i = i0 + (size_t)k * BD;
-      k2[k] = kNone;
-      v[k] = 0.f;
-      if (i < hi) {
-        k2[k] = t.node_tag[t.tc_int[i] & 0x7FFFFFFFu];
-        const uint32_t g0 = t.tc_start[i];
-        v[k] = (float)(__ldcg(H + t.tc_enter[i]) - (g0 ? __ldcg(H + 2 * (size_t)g0 - 1) : 0.0));
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < kTcBatch; ++k)
-      if (k2[k] != kNone && !(k2[k] & 0x80000000u)) c.elm[k2[k]] = v[k];
-  }
+__global__ void __launch_bounds__(kThreads) tc_elm_kernel(Topo t, const __grid_constant__ Batch B) {
+  pdl_wait();
+  pdl_launch();
+  const CornerDev& c = B.c[blockIdx.y];
+  const uint32_t n = t.nCn, m = 2 * n, nb = tierC_blocks(m);
+  const double* H = c.scratch + n;
+  const TcScan sc = tc_scan(c.scratch + 4 * (size_t)n + 4 * (size_t)nb, nb);
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  const uint32_t ev = __ldg(t.tc_ev + e);
+  if (ev >> 31) return;                                     // exit event
+  const uint32_t tag = __ldg(&t.tc_node[ev].y);
+  if (tag == kNone || (tag & 0x80000000u)) return;          // Steiner node or root
+  c.elm[tag] = (float)tc_read(H, sc, e);
 }
 
 // ------------------------------------------- a2-a5: propagation work units
@@ -836,29 +877,36 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
 }
 
 template <bool SMEM_LUT, bool TRACE>
-__global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) fwd_persistent_kernel(Topo t, CornerDev c,
-                                                                                   uint32_t lut_f4) {
-  const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
+__global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) fwd_persistent_kernel(Topo t,
+                                                                                   const __grid_constant__ Batch B) {
+  stage_luts<SMEM_LUT>(B, kNone);
+  // warp gw serves corner gw % K and walks its unit list with stride Wc
+  const uint32_t K = B.K, gw = blockIdx.x * (kFwdThreads / 32) + (threadIdx.x >> 5);
+  const uint32_t Wc = gridDim.x * (kFwdThreads / 32) / K;
+  if (gw >= Wc * K) return;
+  const CornerDev& c = B.c[gw % K];
+  const float* L = lut_of<SMEM_LUT>(c);
   const uint32_t ep = epoch_of(c);
   const uint32_t tl = (threadIdx.x & 31) >> 2;
-  const uint32_t W = gridDim.x * (kFwdThreads / 32);
-  uint32_t u = blockIdx.x * (kFwdThreads / 32) + (threadIdx.x >> 5);
+  uint32_t u = gw / K;
   // software pipeline: the next unit's term slot is in flight while a unit
   // waits for its producers (the RC results are loaded by the unit itself: prefetching them too
   // measured slower on C3)
   uint4 nx = u < t.n_fwu ? __ldg(t.fterm + (size_t)kFwdTerms * u + tl) : make_uint4(0, 0, 0, 0);
-  for (; u < t.n_fwu; u += W) {
+  for (; u < t.n_fwu; u += Wc) {
     const uint4 tr = nx;
-    if (u + W < t.n_fwu) nx = __ldg(t.fterm + (size_t)kFwdTerms * (u + W) + tl);   // prefetch the next unit
+    if (u + Wc < t.n_fwu) nx = __ldg(t.fterm + (size_t)kFwdTerms * (u + Wc) + tl);   // prefetch the next unit
     fwd_unit<TRACE>(t, c, L, ep, u, tr, fwd_rc(c, tr));
   }
 }
 
-// units [u0, u1) of one gate stage, one warp each
+// units [u0, u1) of one gate stage, one warp each; grid.y = corner
 template <bool SMEM_LUT, bool TRACE>
-__global__ void __launch_bounds__(kThreads) fwd_stage_kernel(Topo t, CornerDev c, uint32_t u0, uint32_t u1,
-                                                             uint32_t lut_f4) {
-  const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
+__global__ void __launch_bounds__(kThreads) fwd_stage_kernel(Topo t, const __grid_constant__ Batch B, uint32_t u0,
+                                                             uint32_t u1) {
+  stage_luts<SMEM_LUT>(B, blockIdx.y);
+  const CornerDev& c = B.c[blockIdx.y];
+  const float* L = lut_of<SMEM_LUT>(c);
   const uint32_t u = u0 + blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
   const uint4 tr = u < u1 ? __ldg(t.fterm + (size_t)kFwdTerms * u + ((threadIdx.x & 31) >> 2)) : make_uint4(0, 0, 0, 0);
   pdl_wait();
@@ -1135,13 +1183,16 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
 }
 
 template <bool SMEM_LUT, bool TRACE>
-__global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_kernel(Topo t, CornerDev c,
-                                                                                   uint32_t lut_f4) {
-  const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
+__global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_kernel(Topo t,
+                                                                                   const __grid_constant__ Batch B) {
+  stage_luts<SMEM_LUT>(B, kNone);
+  const uint32_t K = B.K, gw = blockIdx.x * (kBwdThreads / 32) + (threadIdx.x >> 5);
+  const uint32_t W = gridDim.x * (kBwdThreads / 32) / K;    // warps of this corner
+  if (gw >= W * K) return;
+  const CornerDev& c = B.c[gw % K];
+  const float* L = lut_of<SMEM_LUT>(c);
   const uint32_t ep = epoch_of(c);
-  const uint32_t warp = threadIdx.x >> 5;
-  const uint32_t W = gridDim.x * (kBwdThreads / 32);
-  uint32_t u = blockIdx.x * (kBwdThreads / 32) + warp;
+  uint32_t u = gw / K;
   // software pipeline: the unit record two units ahead, the sinks' fan-out
   // records one unit ahead are in flight while a unit waits for its producers
   // (issued at the start of the previous unit, so they overlap its work)
@@ -1222,9 +1273,11 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_ker
 }
 
 template <bool SMEM_LUT, bool TRACE>
-__global__ void __launch_bounds__(kThreads) bwd_stage_kernel(Topo t, CornerDev c, uint32_t u0, uint32_t u1,
-                                                             uint32_t lut_f4) {
-  const float* L = stage_lut<SMEM_LUT>(c, lut_f4);
+__global__ void __launch_bounds__(kThreads) bwd_stage_kernel(Topo t, const __grid_constant__ Batch B, uint32_t u0,
+                                                             uint32_t u1) {
+  stage_luts<SMEM_LUT>(B, blockIdx.y);
+  const CornerDev& c = B.c[blockIdx.y];
+  const float* L = lut_of<SMEM_LUT>(c);
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t u = u0 + blockIdx.x * (kThreads / 32) + warp;
   const uint4 ud = u < u1 ? __ldg(t.bwu + u) : make_uint4(0, 0, 0, 0);
@@ -1252,13 +1305,14 @@ __device__ __forceinline__ void block_tree(float (*s_w)[kThreads], double (*s_t)
   }
 }
 
-__global__ void __launch_bounds__(kThreads) reduce_kernel(Topo t, CornerDev c) {
+__global__ void __launch_bounds__(kThreads) reduce_kernel(Topo t, const __grid_constant__ Batch B) {
   constexpr int kU = 4;                      // loads in flight per thread
   __shared__ double s_t[2][kThreads];
   __shared__ float s_w[2][kThreads];
   __shared__ bool last;
   pdl_wait();
   pdl_launch();
+  const CornerDev& c = B.c[blockIdx.y];
   const uint32_t n = t.n_ep;
   const uint32_t lo = (uint32_t)((uint64_t)n * blockIdx.x / gridDim.x);
   const uint32_t hi = (uint32_t)((uint64_t)n * (blockIdx.x + 1) / gridDim.x);
@@ -1368,9 +1422,9 @@ inline uint32_t blocks(uint64_t n, uint32_t th = kThreads) { return (uint32_t)((
 
 // launch with programmatic dependent launch enabled
 template <class K, class... A>
-cudaError_t pdl_launch_smem(K kernel, uint32_t grid, uint32_t block, size_t smem, cudaStream_t s, A... args) {
+cudaError_t pdl_launch_smem(K kernel, dim3 grid, uint32_t block, size_t smem, cudaStream_t s, A... args) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
+  cfg.gridDim = grid;
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
@@ -1389,69 +1443,64 @@ cudaError_t pdl_launch_smem(K kernel, uint32_t grid, uint32_t block, size_t smem
 }
 
 template <class K, class... A>
-cudaError_t pdl_launch_kernel(K kernel, uint32_t grid, uint32_t block, cudaStream_t s, A... args) {
+cudaError_t pdl_launch_kernel(K kernel, dim3 grid, uint32_t block, cudaStream_t s, A... args) {
   return pdl_launch_smem(kernel, grid, block, 0, s, args...);
+}
+
+__global__ void set_ptrs_kernel(const float** dst, const float* a, const float* b) {
+  dst[0] = a;
+  dst[1] = b;
 }
 
 }  // namespace
 
-cudaError_t launch_rc(const Topo& t, const CornerDev& c, cudaStream_t s) {
+uint32_t rc_warp_grid() {
+  int dev = 0, sms = 0, nb = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, rc_warp_kernel, kThreads, 0);
+  cudaGetLastError();
+  return (uint32_t)std::max(nb, 1) * (uint32_t)std::max(sms, 1);
+}
+
+cudaError_t launch_rc(const Topo& t, const Batch& b, uint32_t wgrid, cudaStream_t s) {
   cudaError_t e = cudaSuccess;
-  if (t.n_wtiles && e == cudaSuccess) e = pdl_launch_kernel(rc_warp_kernel, blocks(32ull * t.n_wtiles), kThreads, s, t, c);
-  if (t.n_btiles && e == cudaSuccess) e = pdl_launch_kernel(rc_block_kernel, t.n_btiles, kThreads, s, t, c);
-  if (t.n_lumped && e == cudaSuccess) e = pdl_launch_kernel(rc_lumped_kernel, blocks(t.n_lumped), kThreads, s, t, c);
-  return e != cudaSuccess ? e : cudaGetLastError();
-}
-
-cudaError_t launch_rc_tierC(const Topo& t, const CornerDev& c, cudaStream_t s) {
-  if (!t.nC) return cudaSuccess;
-  static uint32_t grid = 0;
-  if (!grid) {
-    int dev = 0, sms = 0, nb = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tc_persistent_kernel, kTcThreads, 0);
-    // one block per SM: the small-net RC kernels on the main stream need the
-    // rest of the register file to run beside it (two blocks per SM filled
-    // it and serialised the two)
-    grid = (uint32_t)std::min<int>(std::min(std::max(nb, 0), STA_TC_BLOCKS) * sms, (int)kTcMaxGrid);
-    if (!grid) return cudaErrorCooperativeLaunchTooLarge;
+  const uint32_t K = b.K;
+  if (t.n_wtiles && e == cudaSuccess) {
+    // co-resident warps shared by the K corners, at most one tile per warp
+    const uint32_t g = std::max<uint32_t>(1, std::min<uint32_t>(wgrid / K, blocks(32ull * t.n_wtiles)));
+    e = pdl_launch_kernel(rc_warp_kernel, dim3(g, K), kThreads, s, t, b);
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kTcThreads);
-  cfg.stream = s;
-  int prio = 0;
-  cudaStreamGetPriority(s, &prio);
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  attr[1].id = cudaLaunchAttributePriority;
-  attr[1].val.priority = prio;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_persistent_kernel, t, c);
+  if (t.n_btiles && e == cudaSuccess) e = pdl_launch_kernel(rc_block_kernel, dim3(t.n_btiles, K), kThreads, s, t, b);
+  if (t.n_lumped && e == cudaSuccess) e = pdl_launch_kernel(rc_lumped_kernel, dim3(blocks(t.n_lumped), K), kThreads, s, t, b);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-cudaError_t launch_fwd_stage(const Topo& t, const CornerDev& c, uint32_t u0, uint32_t u1, uint32_t lut_f4,
-                             cudaStream_t s) {
-  if (u1 <= u0) return cudaSuccess;
-  const uint32_t g = blocks(32ull * (u1 - u0));
-  if (lut_f4) return pdl_launch_smem(fwd_stage_kernel<true, false>, g, kThreads, 16ull * lut_f4, s, t, c, u0, u1, lut_f4);
-  return pdl_launch_smem(fwd_stage_kernel<false, false>, g, kThreads, 0, s, t, c, u0, u1, lut_f4);
+cudaError_t launch_rc_tierC(const Topo& t, const Batch& b, cudaStream_t s) {
+  if (!t.nC) return cudaSuccess;
+  const uint32_t K = b.K;
+  cudaError_t e = pdl_launch_kernel(tc_node_kernel, dim3(tierC_blocks(t.nCn), K), kThreads, s, t, b);
+  if (e == cudaSuccess) e = pdl_launch_kernel(tc_event_kernel, dim3(tierC_blocks(2ull * t.nCn), K), kThreads, s, t, b);
+  if (e == cudaSuccess) e = pdl_launch_kernel(tc_elm_kernel, dim3(blocks(2ull * t.nCn), K), kThreads, s, t, b);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-cudaError_t launch_bwd_stage(const Topo& t, const CornerDev& c, uint32_t u0, uint32_t u1, uint32_t lut_f4,
-                             cudaStream_t s) {
+cudaError_t launch_fwd_stage(const Topo& t, const Batch& b, uint32_t u0, uint32_t u1, cudaStream_t s) {
   if (u1 <= u0) return cudaSuccess;
-  const uint32_t g = blocks(32ull * (u1 - u0));
-  if (lut_f4) return pdl_launch_smem(bwd_stage_kernel<true, false>, g, kThreads, 16ull * lut_f4, s, t, c, u0, u1, lut_f4);
-  return pdl_launch_smem(bwd_stage_kernel<false, false>, g, kThreads, 0, s, t, c, u0, u1, lut_f4);
+  const dim3 g(blocks(32ull * (u1 - u0)), b.K);
+  if (b.smem_f4) return pdl_launch_smem(fwd_stage_kernel<true, false>, g, kThreads, 16ull * b.smem_f4, s, t, b, u0, u1);
+  return pdl_launch_smem(fwd_stage_kernel<false, false>, g, kThreads, 0, s, t, b, u0, u1);
 }
 
-cudaError_t launch_reduce(const Topo& t, const CornerDev& c, cudaStream_t s) {
-  return pdl_launch_kernel(reduce_kernel, (uint32_t)kRedBlocks, kThreads, s, t, c);
+cudaError_t launch_bwd_stage(const Topo& t, const Batch& b, uint32_t u0, uint32_t u1, cudaStream_t s) {
+  if (u1 <= u0) return cudaSuccess;
+  const dim3 g(blocks(32ull * (u1 - u0)), b.K);
+  if (b.smem_f4) return pdl_launch_smem(bwd_stage_kernel<true, false>, g, kThreads, 16ull * b.smem_f4, s, t, b, u0, u1);
+  return pdl_launch_smem(bwd_stage_kernel<false, false>, g, kThreads, 0, s, t, b, u0, u1);
+}
+
+cudaError_t launch_reduce(const Topo& t, const Batch& b, cudaStream_t s) {
+  return pdl_launch_kernel(reduce_kernel, dim3((uint32_t)kRedBlocks, b.K), kThreads, s, t, b);
 }
 
 cudaError_t launch_gather_pins(const Topo& t, const CornerDev& c, int what, float4* dst, cudaStream_t s) {
@@ -1465,35 +1514,40 @@ cudaError_t launch_gather_rc(const Topo& t, const CornerDev& c, float* net_load,
   return cudaGetLastError();
 }
 
+cudaError_t launch_set_ptrs(const float* const* dst, const float* a, const float* b, cudaStream_t s) {
+  set_ptrs_kernel<<<1, 1, 0, s>>>(const_cast<const float**>(dst), a, b);
+  return cudaGetLastError();
+}
+
 // co-resident grid of the persistent forward (which = 0) or backward (1)
 // kernel: blocks per SM from the occupancy calculator x SMs; 0 if unsupported
-uint32_t persistent_grid(uint32_t lut_f4, int which) {
+uint32_t persistent_grid(uint32_t smem_f4, int which) {
   int dev = 0, sms = 0, nb = 0, coop = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
   if (!coop) return 0;
-  const size_t smem = lut_f4 ? 16ull * lut_f4 : 0;
+  const size_t smem = 16ull * smem_f4;
   // the same grid serves the traced instantiation: the smaller of the two
   int nt = 0;
   if (which == 0) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &nb, lut_f4 ? fwd_persistent_kernel<true, false> : fwd_persistent_kernel<false, false>, kFwdThreads, smem);
+        &nb, smem_f4 ? fwd_persistent_kernel<true, false> : fwd_persistent_kernel<false, false>, kFwdThreads, smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &nt, lut_f4 ? fwd_persistent_kernel<true, true> : fwd_persistent_kernel<false, true>, kFwdThreads, smem);
+        &nt, smem_f4 ? fwd_persistent_kernel<true, true> : fwd_persistent_kernel<false, true>, kFwdThreads, smem);
   } else {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &nb, lut_f4 ? bwd_persistent_kernel<true, false> : bwd_persistent_kernel<false, false>, kBwdThreads, smem);
+        &nb, smem_f4 ? bwd_persistent_kernel<true, false> : bwd_persistent_kernel<false, false>, kBwdThreads, smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &nt, lut_f4 ? bwd_persistent_kernel<true, true> : bwd_persistent_kernel<false, true>, kBwdThreads, smem);
+        &nt, smem_f4 ? bwd_persistent_kernel<true, true> : bwd_persistent_kernel<false, true>, kBwdThreads, smem);
   }
   cudaGetLastError();
   return (uint32_t)(std::min(nb, nt) * sms);
 }
 
-template <class K>
-cudaError_t coop_launch(K kernel, uint32_t grid, uint32_t block, size_t smem, cudaStream_t s, const Topo& t,
-                        const CornerDev& c, uint32_t lut_f4) {
+template <class Kern>
+cudaError_t coop_launch(Kern kernel, uint32_t grid, uint32_t block, size_t smem, cudaStream_t s, const Topo& t,
+                        const Batch& b) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
@@ -1504,26 +1558,30 @@ cudaError_t coop_launch(K kernel, uint32_t grid, uint32_t block, size_t smem, cu
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kernel, t, c, lut_f4);
+  return cudaLaunchKernelEx(&cfg, kernel, t, b);
 }
 
-cudaError_t launch_fwd_persistent(const Topo& t, const CornerDev& c, uint32_t grid, uint32_t lut_f4, cudaStream_t s) {
+static bool traced(const Batch& b) { return b.c[0].trace != nullptr; }
+
+cudaError_t launch_fwd_persistent(const Topo& t, const Batch& b, uint32_t grid, cudaStream_t s) {
   if (!t.NP) return cudaSuccess;
+  const size_t sm = 16ull * b.smem_f4;
   // STA_TRACE builds per-unit timestamps into a separate instantiation
-  if (c.trace)
-    return lut_f4 ? coop_launch(fwd_persistent_kernel<true, true>, grid, kFwdThreads, 16ull * lut_f4, s, t, c, lut_f4)
-                  : coop_launch(fwd_persistent_kernel<false, true>, grid, kFwdThreads, 0, s, t, c, lut_f4);
-  return lut_f4 ? coop_launch(fwd_persistent_kernel<true, false>, grid, kFwdThreads, 16ull * lut_f4, s, t, c, lut_f4)
-                : coop_launch(fwd_persistent_kernel<false, false>, grid, kFwdThreads, 0, s, t, c, lut_f4);
+  if (traced(b))
+    return b.smem_f4 ? coop_launch(fwd_persistent_kernel<true, true>, grid, kFwdThreads, sm, s, t, b)
+                     : coop_launch(fwd_persistent_kernel<false, true>, grid, kFwdThreads, 0, s, t, b);
+  return b.smem_f4 ? coop_launch(fwd_persistent_kernel<true, false>, grid, kFwdThreads, sm, s, t, b)
+                   : coop_launch(fwd_persistent_kernel<false, false>, grid, kFwdThreads, 0, s, t, b);
 }
 
-cudaError_t launch_bwd_persistent(const Topo& t, const CornerDev& c, uint32_t grid, uint32_t lut_f4, cudaStream_t s) {
+cudaError_t launch_bwd_persistent(const Topo& t, const Batch& b, uint32_t grid, cudaStream_t s) {
   if (!t.n_bwu) return cudaSuccess;
-  if (c.trace)
-    return lut_f4 ? coop_launch(bwd_persistent_kernel<true, true>, grid, kBwdThreads, 16ull * lut_f4, s, t, c, lut_f4)
-                  : coop_launch(bwd_persistent_kernel<false, true>, grid, kBwdThreads, 0, s, t, c, lut_f4);
-  return lut_f4 ? coop_launch(bwd_persistent_kernel<true, false>, grid, kBwdThreads, 16ull * lut_f4, s, t, c, lut_f4)
-                : coop_launch(bwd_persistent_kernel<false, false>, grid, kBwdThreads, 0, s, t, c, lut_f4);
+  const size_t sm = 16ull * b.smem_f4;
+  if (traced(b))
+    return b.smem_f4 ? coop_launch(bwd_persistent_kernel<true, true>, grid, kBwdThreads, sm, s, t, b)
+                     : coop_launch(bwd_persistent_kernel<false, true>, grid, kBwdThreads, 0, s, t, b);
+  return b.smem_f4 ? coop_launch(bwd_persistent_kernel<true, false>, grid, kBwdThreads, sm, s, t, b)
+                   : coop_launch(bwd_persistent_kernel<false, false>, grid, kBwdThreads, 0, s, t, b);
 }
 
 cudaError_t set_lut_smem_limit(size_t bytes) {

@@ -59,7 +59,7 @@ class Info(C.Structure):
     _fields_ = [(n, C.c_uint32) for n in (
         "num_pins", "num_nets", "num_net_arcs", "num_cell_arcs", "num_checks", "num_endpoints",
         "num_levels", "num_stages", "num_pull_pins", "num_sink_pins", "num_heavy_drivers",
-        "kernels_per_update")] + [("device_bytes", C.c_uint64)]
+        "kernels_per_update", "lut_smem_bytes")] + [("device_bytes", C.c_uint64)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -114,19 +114,36 @@ def _is_torch_cuda(x) -> bool:
     return hasattr(x, "is_cuda") and hasattr(x, "data_ptr") and bool(x.is_cuda)
 
 
-class _Args:
-    """Marshals a group of arrays that must share one memory kind."""
+def _torch_dtypes(dtype):
+    """torch dtypes whose bytes are the C type `dtype` (u32 arrays may come as int32)."""
+    import torch
+    return {np.float32: (torch.float32,), np.int32: (torch.int32,), np.uint8: (torch.uint8,),
+            np.uint32: tuple(t for t in (getattr(torch, "uint32", None), torch.int32) if t is not None),
+            np.float64: (torch.float64,)}[np.dtype(dtype).type]
 
-    def __init__(self):
+
+class _Args:
+    """Marshals a group of arrays that must share one memory kind.  Device
+    tensors are passed zero-copy, so they must already have the C element
+    type, be contiguous and live on the ctx's device (no silent conversion:
+    a converted copy would be made on torch's current stream, not the ctx's)."""
+
+    def __init__(self, device: Optional[int] = None):
         self.keep = []
         self.mem = None
+        self.device = device
 
     def ptr(self, x, dtype):
         if x is None:
             return None
         if _is_torch_cuda(x):
             self._kind(STA_MEM_DEVICE)
-            x = x.contiguous()
+            if x.dtype not in _torch_dtypes(dtype):
+                raise TypeError(f"device tensor of dtype {x.dtype} where {np.dtype(dtype).name} is expected")
+            if not x.is_contiguous():
+                raise ValueError("device tensors must be contiguous")
+            if self.device is not None and x.device.index != self.device:
+                raise ValueError(f"device tensor on cuda:{x.device.index}, ctx is on cuda:{self.device}")
             self.keep.append(x)
             return x.data_ptr() if x.numel() else None
         self._kind(STA_MEM_HOST)
@@ -155,6 +172,7 @@ class Context:
         if st:
             raise StaError(st, "sta_create failed (no CUDA device?)")
         self.h = h
+        self.device = int(device)
         self.num_corners = num_corners
         self.num_pins = 0
         self.num_nets = 0
@@ -183,7 +201,7 @@ class Context:
     # ------------------------------------------------------------ inputs
     def load_graph(self, pin_cap, pin_role, net_ptr, net_pins, arc_from, arc_to, arc_sense,
                    arc_tab, chk_d, chk_ck, chk_tab, num_tables: int):
-        a = _Args()
+        a = _Args(self.device)
         d = GraphDesc()
         d.num_pins = len(pin_cap)
         d.pin_cap = a.ptr(pin_cap, np.float32)
@@ -206,18 +224,18 @@ class Context:
         self.num_pins, self.num_nets = d.num_pins, d.num_nets
 
     def set_library(self, corner: int, n1, n2, off, data):
-        a = _Args()
+        a = _Args(self.device)
         p = [a.ptr(n1, np.uint8), a.ptr(n2, np.uint8), a.ptr(off, np.uint32), a.ptr(data, np.float32)]
         self._check(self._L.sta_set_library(self.h, int(corner), a.kind, len(n1), *p, len(data)))
 
     def set_rc_tree(self, rc_ptr, parent, node_pin):
-        a = _Args()
+        a = _Args(self.device)
         p = [a.ptr(rc_ptr, np.uint32), None, a.ptr(parent, np.int32), a.ptr(node_pin, np.uint32)]
         self._check(self._L.sta_set_rc_tree(self.h, a.kind, p[0], len(parent), p[2], p[3]))
 
     def set_rc_values(self, corner: int, res, cap):
         """Device tensors are BORROWED until the next update completes."""
-        a = _Args()
+        a = _Args(self.device)
         pr, pc = a.ptr(res, np.float32), a.ptr(cap, np.float32)
         self._borrowed = getattr(self, "_borrowed", {})
         self._borrowed[corner] = a.keep       # keep torch tensors alive
@@ -225,7 +243,7 @@ class Context:
 
     def set_constraints(self, period, clock_slew, pi_pin, pi_at, pi_slew, po_pin, po_out_max,
                         po_out_min, po_load):
-        a = _Args()
+        a = _Args(self.device)
         k = ConstraintsDesc()
         k.period_ps = float(period)
         k.clock_slew_ps = float(clock_slew)
@@ -313,17 +331,30 @@ class Context:
 
 
 # ---------------------------------------------------------------- helpers
-def load_design(ctx: Context, d, corners=None, device_rc: bool = False):
+def _dev(x):
+    """numpy array -> torch CUDA tensor of the same bytes (u32 as int32)."""
+    import torch
+    a = np.ascontiguousarray(x)
+    if a.dtype == np.uint32:
+        a = a.view(np.int32)
+    return torch.from_numpy(a).cuda()
+
+
+def load_design(ctx: Context, d, corners=None, device_rc: bool = False, device_graph: bool = False):
     """Load a synth.Design (netlist, libraries, RC, constraints) into ctx.
-    corners: which design corners map to ctx corners 0..K-1 (default all)."""
-    ctx.load_graph(d.pin_cap, d.pin_role, d.net_ptr, d.net_pins, d.arc_from, d.arc_to,
-                   d.arc_sense, d.arc_tab, d.chk_d, d.chk_ck, d.chk_tab, d.libs[0].num_tables)
+    corners: which design corners map to ctx corners 0..K-1 (default all);
+    device_rc / device_graph: pass the RC values / the netlist, RC tree,
+    libraries and constraints as device tensors (STA_MEM_DEVICE)."""
+    g = _dev if device_graph else (lambda x: x)
+    ctx.load_graph(g(d.pin_cap), g(d.pin_role), g(d.net_ptr), g(d.net_pins), g(d.arc_from),
+                   g(d.arc_to), g(d.arc_sense), g(d.arc_tab), g(d.chk_d), g(d.chk_ck), g(d.chk_tab),
+                   d.libs[0].num_tables)
     corners = list(range(ctx.num_corners)) if corners is None else list(corners)
     for k, c in enumerate(corners):
         L = d.libs[c]
-        ctx.set_library(k, L.n1, L.n2, L.off, L.data)
+        ctx.set_library(k, g(L.n1), g(L.n2), g(L.off), g(L.data))
     rc0 = d.rc[corners[0]]
-    ctx.set_rc_tree(rc0.rc_ptr, rc0.parent, rc0.node_pin)
+    ctx.set_rc_tree(g(rc0.rc_ptr), g(rc0.parent), g(rc0.node_pin))
     for k, c in enumerate(corners):
         rc = d.rc[c]
         if device_rc:
@@ -332,5 +363,5 @@ def load_design(ctx: Context, d, corners=None, device_rc: bool = False):
         else:
             ctx.set_rc_values(k, rc.res, rc.cap)
     k = d.cons
-    ctx.set_constraints(k.period, k.clock_slew, k.pi_pin, k.pi_at, k.pi_slew, k.po_pin,
-                        k.po_out_max, k.po_out_min, k.po_load)
+    ctx.set_constraints(k.period, k.clock_slew, g(k.pi_pin), g(k.pi_at), g(k.pi_slew), g(k.po_pin),
+                        g(k.po_out_max), g(k.po_out_min), g(k.po_load))

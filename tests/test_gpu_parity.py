@@ -51,9 +51,10 @@ def check_rc(ctx, d, corner=0, design_corner=0):
     check_close("elm", elm, re)
 
 
-@pytest.mark.parametrize("name", ["h1_chain", "c17", "h3_reg2reg"])
+@pytest.mark.parametrize("name", ["h1_chain", "c17", "h3_reg2reg", "h4_seeds"])
 def test_hand_examples(sta, name):
-    d = {"h1_chain": synth.h1_chain, "c17": synth.c17, "h3_reg2reg": synth.h3_reg2reg}[name]()
+    d = {"h1_chain": synth.h1_chain, "c17": synth.c17, "h3_reg2reg": synth.h3_reg2reg,
+         "h4_seeds": synth.h4_seeds}[name]()
     ctx = run(sta, d)
     ref = oracle.update(d)
     compare_update(ctx, ref)
