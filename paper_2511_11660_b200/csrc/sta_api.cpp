@@ -5,6 +5,7 @@
 // Every arithmetic step of the timing update runs in sta_kernels.cu; this file
 // only arranges data (integer bookkeeping) and enqueues kernels.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -25,6 +26,19 @@ using u32 = uint32_t;
 using u64 = uint64_t;
 
 namespace {
+
+// STA_TIMING=1: host phase times of sta_load_graph / sta_set_rc_tree on stderr
+struct PhaseTimer {
+  bool on = std::getenv("STA_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[sta timing] %-28s %9.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  }
+};
 
 struct StaError {
   sta_status st;
@@ -252,48 +266,53 @@ void group_arcs(const std::vector<u32>& key, u32 P, std::vector<u32>& ptr, std::
 // ------------------------------------------------------------------ plan
 void build_plan(sta_ctx c) {
   const u32 P = c->P;
-  std::vector<u32> fi_ptr, fi_ids, fo_ptr, fo_ids;
-  group_arcs(c->arc_to, P, fi_ptr, fi_ids);
-  group_arcs(c->arc_from, P, fo_ptr, fo_ids);
+  PhaseTimer tm;
+  // row a0 on the device (sta_levelize.cu): cell-arc CSR by target / source,
+  // Kahn-frontier levels, perm = stable sort by (level, id)
+  std::vector<u32> fi_ptr(P + 1), fi_ids(c->A), fo_ptr(P + 1), fo_ids(c->A);
+  c->level.assign(P, 0);
+  c->perm.assign(P, 0);
+  {
+    Arena a;
+    cudaStream_t s = c->stream;
+    try {
+      const u32* d_np = a.upload(c->net_ptr, s);
+      const u32* d_pins = a.upload(c->net_pins, s);
+      const u32* d_from = a.upload(c->arc_from, s);
+      const u32* d_to = a.upload(c->arc_to, s);
+      u32* d_level = a.alloc<u32>(P);
+      u32* d_perm = a.alloc<u32>(P);
+      u32* d_fip = a.alloc<u32>(P + 1);
+      u32* d_fii = a.alloc<u32>(c->A);
+      u32* d_fop = a.alloc<u32>(P + 1);
+      u32* d_foi = a.alloc<u32>(c->A);
+      u32 cyc = kNone;
+      ck(sta::levelize_device(P, c->N, c->A, d_np, d_pins, d_from, d_to, d_level, d_perm, d_fip, d_fii, d_fop, d_foi,
+                              &c->num_levels, &cyc, s), "levelize kernels");
+      if (cyc != kNone) fail(STA_ERR_CYCLE, "combinational cycle through pin %u", cyc);
+      ck(cudaMemcpyAsync(c->level.data(), d_level, 4ull * P, cudaMemcpyDeviceToHost, s), "D2H level");
+      ck(cudaMemcpyAsync(c->perm.data(), d_perm, 4ull * P, cudaMemcpyDeviceToHost, s), "D2H perm");
+      ck(cudaMemcpyAsync(fi_ptr.data(), d_fip, 4ull * (P + 1), cudaMemcpyDeviceToHost, s), "D2H csr");
+      ck(cudaMemcpyAsync(fo_ptr.data(), d_fop, 4ull * (P + 1), cudaMemcpyDeviceToHost, s), "D2H csr");
+      if (c->A) {
+        ck(cudaMemcpyAsync(fi_ids.data(), d_fii, 4ull * c->A, cudaMemcpyDeviceToHost, s), "D2H csr");
+        ck(cudaMemcpyAsync(fo_ids.data(), d_foi, 4ull * c->A, cudaMemcpyDeviceToHost, s), "D2H csr");
+      }
+      ck(cudaStreamSynchronize(s), "levelize");
+    } catch (...) {
+      cudaStreamSynchronize(s);
+      a.release();
+      throw;
+    }
+    cudaStreamSynchronize(s);
+    a.release();
+  }
+  tm.mark("plan: device levelize + CSR");
   for (u32 p = 0; p < P; ++p)
     if (c->pin_role[p] == STA_PIN_PI || c->pin_role[p] == STA_PIN_FF_CK)
       if (fi_ptr[p + 1] != fi_ptr[p])
         fail(STA_ERR_ARG, "pin %u: role %s must not have fan-in", p, c->pin_role[p] == STA_PIN_PI ? "PI" : "FF_CK");
   auto driver_of = [&](u32 p) { return c->net_pins[c->net_ptr[c->pin_net[p]]]; };
-
-  // Kahn levelization over net + cell arcs, FIFO seeded in id order
-  // (SPEC.md:257).  level = longest path depth.
-  std::vector<u32> indeg(P), order;
-  order.reserve(P);
-  c->level.assign(P, 0);
-  for (u32 p = 0; p < P; ++p) {
-    indeg[p] = (c->is_sink[p] ? 1u : 0u) + (fi_ptr[p + 1] - fi_ptr[p]);
-    if (!indeg[p]) order.push_back(p);
-  }
-  for (size_t h = 0; h < order.size(); ++h) {
-    const u32 u = order[h];
-    auto relax = [&](u32 v) {
-      if (c->level[u] + 1 > c->level[v]) c->level[v] = c->level[u] + 1;
-      if (--indeg[v] == 0) order.push_back(v);
-    };
-    const u32 n = c->pin_net[u];
-    if (n != kNone && !c->is_sink[u])
-      for (u32 k = c->net_ptr[n] + 1; k < c->net_ptr[n + 1]; ++k) relax(c->net_pins[k]);
-    for (u32 x = fo_ptr[u]; x < fo_ptr[u + 1]; ++x) relax(c->arc_to[fo_ids[x]]);
-  }
-  if (order.size() != P) {
-    for (u32 p = 0; p < P; ++p)
-      if (indeg[p]) fail(STA_ERR_CYCLE, "combinational cycle through pin %u", p);
-  }
-  c->num_levels = 0;
-  for (u32 p = 0; p < P; ++p) c->num_levels = std::max(c->num_levels, c->level[p] + 1);
-  {
-    std::vector<u32> start(c->num_levels + 1, 0);
-    for (u32 p = 0; p < P; ++p) start[c->level[p] + 1]++;
-    for (u32 l = 0; l < c->num_levels; ++l) start[l + 1] += start[l];
-    c->perm.resize(P);
-    for (u32 p = 0; p < P; ++p) c->perm[start[c->level[p]]++] = p;
-  }
 
   // gate stages in pin-level order
   c->stage.assign(P, 0);
@@ -378,6 +397,7 @@ void build_plan(sta_ctx c) {
   c->sink_stage_ptr.assign(S + 1, 0);
   for (u32 s = 0; s <= S; ++s) c->sink_stage_ptr[s] = c->sink_ptr[c->pull_stage_ptr[s]];
 
+  tm.mark("plan: stages + numbering");
   // A non-unate arc's (irf -> orf) pairs are the union of the positive- and
   // negative-unate pairs, so it becomes two terms with the same
   // tables; every kernel item then evaluates exactly one pair per output edge
@@ -443,6 +463,7 @@ void build_plan(sta_ctx c) {
   }
   pfo_p[NP] = (u32)pfo_dst.size();
 
+  tm.mark("plan: fan-in / fan-out terms");
   // backward warp tiles per stage: runs of <= 32 consecutive sinks that never
   // split a driver with <= 32 sinks; a driver with more sinks gets its own
   // tiles (heavy slot: atomics + last-tile finish).  Stage pins without sinks
@@ -605,6 +626,7 @@ void build_plan(sta_ctx c) {
     for (u32& x : sfo_info) x = (fi_info[x] & 7u) | term_slot[x] << 3;
     for (u32& x : pfo_info) x = (fi_info[x] & 7u) | term_slot[x] << 3;
   }
+  tm.mark("plan: forward units");
   c->fwu_stage_ptr.assign(S + 1, 0);
   for (u32 s : fwu_stage) c->fwu_stage_ptr[s + 1]++;
   for (u32 s = 0; s < S; ++s) c->fwu_stage_ptr[s + 1] += c->fwu_stage_ptr[s];
@@ -676,6 +698,7 @@ void build_plan(sta_ctx c) {
   c->pfo_dst = pfo_dst;
   c->pfo_info = pfo_info;
 
+  tm.mark("plan: backward units");
   // upload
   cudaStream_t s = c->stream;
   Arena& g = c->graph_arena;
@@ -702,10 +725,12 @@ void build_plan(sta_ctx c) {
   t.int_of_user = g.upload(c->int_of_user, s);
   t.drv_of_net = g.upload(c->drv_of_net, s);
   ck(cudaStreamSynchronize(s), "plan upload");
+  tm.mark("plan: upload");
 }
 
 // RC tree topology: validation and per-net schedules (tree scope)
 void build_rc(sta_ctx c) {
+  PhaseTimer tm;
   const u32 N = c->N;
   // validation
   if (c->rc_ptr.size() != N + 1) fail(STA_ERR_ARG, "rc_ptr must have num_nets + 1 entries");
@@ -887,6 +912,7 @@ void build_rc(sta_ctx c) {
   c->node_user = std::move(node_user);
   c->rc_net_j = std::move(net_drv);
   ck(cudaStreamSynchronize(s), "rc upload");
+  tm.mark("rc tree: validate + schedule + upload");
 }
 
 // constraints + tree dependent arrays (endpoints, seeds, static node caps)
@@ -1382,6 +1408,7 @@ const char* sta_last_error(sta_ctx c) { return c ? c->err.c_str() : "null ctx"; 
 
 sta_status sta_load_graph(sta_ctx c, const sta_graph_desc* d) {
   return guard(c, [&] {
+    PhaseTimer tm;
     if (!d) fail(STA_ERR_ARG, "desc is NULL");
     c->has_graph = c->has_tree = c->has_cons = c->prepared = false;
     for (CornerState& cs : c->corners) { cs.lib = false; cs.rcv = false; }
@@ -1401,7 +1428,9 @@ sta_status sta_load_graph(sta_ctx c, const sta_graph_desc* d) {
     c->chk_d = fetch(d->chk_d, c->C, d->mem, "chk_d", c->stream);
     c->chk_ck = fetch(d->chk_ck, c->C, d->mem, "chk_ck", c->stream);
     c->chk_tab = fetch(d->chk_tab, c->C, d->mem, "chk_tab", c->stream);
+    tm.mark("load: fetch");
     validate_graph(c);
+    tm.mark("load: validate");
     build_plan(c);
     c->has_graph = true;
   });

@@ -235,4 +235,12 @@ cudaError_t launch_gather_rc(const Topo& t, const CornerDev& c, float* net_load,
 cudaError_t launch_init_corner(const Topo& t, const CornerDev& c, uint32_t n_heavy, cudaStream_t s);
 cudaError_t launch_set_ptrs(const float* const* dst, const float* a, const float* b, cudaStream_t s);
 
+// ---- row a0 on the device (sta_levelize.cu): cell-arc fan-in / fan-out CSR
+// (segments in arc id order), Kahn-frontier levels over net + cell arcs and
+// perm = pins stably sorted by (level, id).  Device pointers; synchronizes s.
+cudaError_t levelize_device(uint32_t P, uint32_t N, uint32_t A, const uint32_t* net_ptr, const uint32_t* net_pins,
+                            const uint32_t* arc_from, const uint32_t* arc_to, uint32_t* level, uint32_t* perm,
+                            uint32_t* fi_ptr, uint32_t* fi_ids, uint32_t* fo_ptr, uint32_t* fo_ids,
+                            uint32_t* num_levels, uint32_t* cycle_pin, cudaStream_t s);
+
 }  // namespace sta

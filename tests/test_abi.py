@@ -129,9 +129,6 @@ def test_library_rc_constraint_errors_and_order():
     npin[1] = 0                  # maps a pin of another net
     _expect(pkg, "STA_ERR_RC", lambda: ctx.set_rc_tree(rc.rc_ptr, rc.parent, npin))
     ctx.set_rc_tree(rc.rc_ptr, rc.parent, rc.node_pin)
-    res = rc.res.copy()
-    res[1] = -1
-    _expect(pkg, "STA_ERR_RC", lambda: ctx.set_rc_values(0, res, rc.cap))
     k = d.cons
     _expect(pkg, "STA_ERR_ARG", lambda: ctx.set_constraints(-1, k.clock_slew, k.pi_pin, k.pi_at, k.pi_slew,
                                                             k.po_pin, k.po_out_max, k.po_out_min, k.po_load))
@@ -146,6 +143,16 @@ def test_library_rc_constraint_errors_and_order():
     ctx.update_timing()
     res4, _ = ctx.report_slack()
     assert res4[0] == pytest.approx(-4.053684, abs=1e-3)
+    # host RC values are validated on the device (no host pass over 10^7
+    # values per optimization step): a negative R surfaces at the next sync
+    res = rc.res.copy()
+    res[1] = -1
+    ctx.set_rc_values(0, res, rc.cap)
+    ctx.update_timing()
+    _expect(pkg, "STA_ERR_RC", lambda: ctx.synchronize())
+    ctx.set_rc_values(0, rc.res, rc.cap)
+    ctx.update_timing()
+    assert ctx.report_slack()[0][0] == pytest.approx(-4.053684, abs=1e-3)
     ctx.close()
 
 
