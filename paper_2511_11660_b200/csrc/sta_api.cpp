@@ -771,7 +771,7 @@ void build_rc(sta_ctx c) {
   } grp[3];
   std::vector<u32> net_drv;
   net_drv.reserve(N);
-  std::vector<u32> cnt, ch, pos, endp, pre;
+  std::vector<u32> cnt, ch, pos, endp, pre, dp;
   std::vector<std::pair<u32, u32>> stack;
   std::vector<uint4> wtiles;                // warp tiles of nets with 1..32 nodes
   std::vector<uint2> btiles;                // block tiles of nets with 33..kBNet nodes (group-1 offsets)
@@ -850,6 +850,15 @@ void build_rc(sta_ctx c) {
       wtiles.back().y += m;
       wt_fill += m;
       wt_cend = ub + m;
+      // rounds the warp kernel needs for this tile: ceil(log2) of the
+      // largest net (segmented scan) and of the deepest root path (pointer
+      // jumping; the root itself carries no resistance)
+      u32 depth = 0;
+      dp.assign(m, 0);
+      for (u32 q = 1; q < m; ++q) depth = std::max(depth, dp[q] = dp[(u32)c->rc_parent[ub + q]] + 1);
+      auto lg = [](u32 x) { u32 r = 0; while ((1u << r) < x) ++r; return r; };
+      uint4& wt = wtiles.back();
+      wt.w = std::max(wt.w & 0xFFu, lg(m)) | (std::max((wt.w >> 8) & 0xFFu, lg(depth)) << 8);
     } else if (tier == 1) {
       if (btiles.empty() || btiles.back().y + m > sta::kBNet) btiles.push_back(make_uint2(x0, 0));
       btiles.back().y += m;
@@ -1071,6 +1080,7 @@ void prepare(sta_ctx c) {
     sta::CornerDev& d = cs.dev;
     d.rec = a.alloc<uint4>(4 * (size_t)c->NP);
     d.rat_ll = a.alloc<uint4>(2 * (size_t)c->NP);
+    d.at4 = a.alloc<float4>(c->NP);
     d.tdel = a.alloc<float4>(std::max<u32>(c->n_dslots, 1));
     d.epoch = a.alloc<u32>(1);
     ck(cudaMemsetAsync(d.rec, 0, sizeof(uint4) * 4 * (size_t)c->NP, s), "memset");

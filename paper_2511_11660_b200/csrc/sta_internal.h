@@ -168,6 +168,9 @@ struct Topo {
 struct CornerDev {
   uint4* rec;         // [4 NP]: tagged forward records of pull pins (sta_kernels.cu: ld_ll)
   uint4* rat_ll;      // [2 NP]: tagged required times of pull pins
+  float4* at4;        // [NP]: untagged copy of the pull pins' arrival times, written by the
+                      // forward next to the tagged record, read by the backward (which runs
+                      // after the forward kernel: no readiness tags needed; 16 B instead of 64 B)
   uint32_t* epoch;    // [1] tag of the current update (advanced by reduce_kernel)
   float4* tdel;       // [delay slots] cell-arc delays of each fan-in term, (el, orf) order,
                       // written by the forward, read by the backward

@@ -189,6 +189,21 @@ __device__ __forceinline__ uint4 spin_ll(const uint4* p, uint32_t ep) {
 }
 __device__ __forceinline__ uint32_t epoch_of(const CornerDev& c) { return __ldcg(c.epoch); }
 
+// arrival times of pull pin i completed by an earlier kernel (compact copy)
+__device__ __forceinline__ Q4 load_at(const CornerDev& c, uint32_t i) { return to_q(__ldcg(c.at4 + i)); }
+// slews of pull pin i from its forward record (the backward needs them at endpoints only)
+__device__ __forceinline__ Q4 load_slew(const CornerDev& c, uint32_t i) {
+  Q4 sl;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) sl.v[q] = __uint_as_float(__ldcg(c.rec + 4 * (size_t)i + q).z);
+  return sl;
+}
+// AT part of net_hop (bit-identical: the same intrinsic)
+__device__ __forceinline__ void hop_at(Q4& at, float e) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) at.v[q] = fin(at.v[q]) ? __fadd_rn(at.v[q], e) : at.v[q];
+}
+
 // forward records completed by an earlier kernel: L2 loads (keep L1 for LUTs)
 __device__ __forceinline__ void load_rec(const CornerDev& c, uint32_t i, Q4& at, Q4& sl) {
 #pragma unroll
@@ -216,7 +231,7 @@ __device__ __forceinline__ bool bad_rc(float r, float cw) {
 // are persistent (grid = co-resident warps per corner) and load the next tile
 // while the current one computes.
 struct WTile {
-  uint4 tile;     // {first internal node, node count, first caller node, 0}
+  uint4 tile;     // {first internal node, node count, first caller node, scan rounds | jump rounds << 8}
   uint4 nd;       // this lane's node record
   float r, cw;    // caller node base + lane
 };
@@ -247,10 +262,11 @@ __device__ __forceinline__ void wtile_run(const CornerDev& c, const WTile& w) {
   const float r = root ? 0.f : rr;
   const bool bad = act && bad_rc(r, cw);
   const double C = act ? (double)cw + (double)__uint_as_float(w.nd.w) : 0.0;
-  // segmented inclusive scan of C (a net's lanes are contiguous; pos resets)
+  // segmented inclusive scan of C (a net's lanes are contiguous; pos resets);
+  // ceil(log2(largest net of the tile)) rounds (warp-uniform, from the tile)
+  const int scan_rounds = (int)(w.tile.w & 0xFFu), jump_rounds = (int)((w.tile.w >> 8) & 0xFFu);
   double inc = C;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
+  for (int r = 0, o = 1; r < scan_rounds; ++r, o <<= 1) {
     const double y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
     if (pos >= o) inc += y;
   }
@@ -259,11 +275,11 @@ __device__ __forceinline__ void wtile_run(const CornerDev& c, const WTile& w) {
   const int seg0 = lane - pos;
   const double s_end = __shfl_sync(0xFFFFFFFFu, inc, act ? seg0 + epos - 1 : lane);
   const double cd = s_end - exc;            // subtree cap of this node
-  // root path sums of w = R * Cdown by pointer jumping
+  // root path sums of w = R * Cdown by pointer jumping: ceil(log2(deepest
+  // root path of the tile)) rounds
   double val = (act && !root) ? (double)r * cd : 0.0;
   int pl = (act && !root) ? seg0 + ppos : -1;
-#pragma unroll
-  for (int k = 0; k < 5; ++k) {
+  for (int k = 0; k < jump_rounds; ++k) {
     const double pv = __shfl_sync(0xFFFFFFFFu, val, pl >= 0 ? pl : lane);
     const int pp = __shfl_sync(0xFFFFFFFFu, pl, pl >= 0 ? pl : lane);
     if (pl >= 0) {
@@ -526,7 +542,7 @@ __device__ void tc_publish(const TcScan& sc, uint32_t nb, SegSum agg, uint32_t f
 __device__ __forceinline__ double tc_read(const double* loc, const TcScan& sc, uint32_t g) {
   const uint32_t b = g / kTcTile;
   const double v = __ldcg(loc + g);
-  return (double)g < __ldcg(sc.fh + b) ? v + __ldcg(sc.carry + b) : v;
+  return (double)g < __ldg(sc.fh + b) ? v + __ldg(sc.carry + b) : v;
 }
 
 __device__ __forceinline__ bool tc_head(uint32_t tag) { return tag != kNone && (tag & 0x80000000u); }
@@ -545,16 +561,19 @@ __global__ void __launch_bounds__(kThreads) tc_node_kernel(Topo t, const __grid_
   double v[kTcPer];
   uint32_t hd = 0;
   bool bad = false;
+  uint4 nd[kTcPer];
+#pragma unroll
+  for (int j = 0; j < kTcPer; ++j) nd[j] = g0 + j < n ? __ldg(t.tc_node + g0 + j) : make_uint4(0, kNone, 0, 0);
+  float cw[kTcPer];
+#pragma unroll
+  for (int j = 0; j < kTcPer; ++j) cw[j] = g0 + j < n ? Cw[nd[j].x] : 0.f;
 #pragma unroll
   for (int j = 0; j < kTcPer; ++j) {
-    const uint32_t g = g0 + j;
     v[j] = 0.0;
-    if (g < n) {
-      const uint4 nd = __ldg(t.tc_node + g);
-      const float cw = Cw[nd.x];
-      bad |= bad_rc(0.f, cw);
-      v[j] = (double)cw + (double)__uint_as_float(nd.w);
-      if (tc_head(nd.y)) hd |= 1u << j;
+    if (g0 + j < n) {
+      bad |= bad_rc(0.f, cw[j]);
+      v[j] = (double)cw[j] + (double)__uint_as_float(nd[j].w);
+      if (tc_head(nd[j].y)) hd |= 1u << j;
     }
   }
   SegSum run{0.0, 0u};                       // thread-serial segmented inclusive run
@@ -597,30 +616,51 @@ __global__ void __launch_bounds__(kThreads) tc_event_kernel(Topo t, const __grid
   double v[kTcPer];
   uint32_t hd = 0;
   bool bad = false;
+  // all loads of the thread's events first (no store in between: the loads of
+  // the 8 events overlap instead of paying one dependent chain each)
+  uint32_t ev[kTcPer];
+  uint4 nd[kTcPer];
+#pragma unroll
+  for (int j = 0; j < kTcPer; ++j) ev[j] = e0 + j < m ? __ldg(t.tc_ev + e0 + j) : 0u;
+#pragma unroll
+  for (int j = 0; j < kTcPer; ++j) nd[j] = __ldg(t.tc_node + (ev[j] & 0x7FFFFFFFu));
+  float cw[kTcPer], rr[kTcPer];
+  double s_end[kTcPer], s_g[kTcPer];
+#pragma unroll
+  for (int j = 0; j < kTcPer; ++j) {
+    cw[j] = Cw[nd[j].x];
+    rr[j] = R[nd[j].x];
+    s_end[j] = tc_read(Si, scn, nd[j].z - 1);
+    s_g[j] = tc_read(Si, scn, ev[j] & 0x7FFFFFFFu);
+  }
+  uint32_t ld_drv[kTcPer];
+  float ld_val[kTcPer];
 #pragma unroll
   for (int j = 0; j < kTcPer; ++j) {
     const uint32_t e = e0 + j;
     v[j] = 0.0;
+    ld_drv[j] = kNone;
+    ld_val[j] = 0.f;
     if (e < m) {
-      const uint32_t ev = __ldg(t.tc_ev + e);
-      const uint32_t g = ev & 0x7FFFFFFFu;
-      const bool exit = (ev >> 31) != 0;
-      const uint4 nd = __ldg(t.tc_node + g);
-      const bool root = tc_head(nd.y);
-      const double C = (double)Cw[nd.x] + (double)__uint_as_float(nd.w);
-      const double cd = tc_read(Si, scn, nd.z - 1) - tc_read(Si, scn, g) + C;
+      const bool exit = (ev[j] >> 31) != 0;
+      const bool root = tc_head(nd[j].y);
+      const double C = (double)cw[j] + (double)__uint_as_float(nd[j].w);
+      const double cd = s_end[j] - s_g[j] + C;
       double w = 0.0;
       if (!root) {
-        const float r = R[nd.x];
-        bad |= bad_rc(r, 0.f);
-        w = (double)r * cd;
+        bad |= bad_rc(rr[j], 0.f);
+        w = (double)rr[j] * cd;
       } else if (!exit) {
-        c.load[nd.y & 0x7FFFFFFFu] = (float)cd;            // net load = Cdown(root)
+        ld_drv[j] = nd[j].y & 0x7FFFFFFFu;                  // net load = Cdown(root)
+        ld_val[j] = (float)cd;
         hd |= 1u << j;                                      // a net's events start at its root's enter
       }
       v[j] = exit ? -w : w;
     }
   }
+#pragma unroll
+  for (int j = 0; j < kTcPer; ++j)
+    if (ld_drv[j] != kNone) c.load[ld_drv[j]] = ld_val[j];
   SegSum run{0.0, 0u};
 #pragma unroll
   for (int j = 0; j < kTcPer; ++j) {
@@ -802,6 +842,7 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
         sl = reinterpret_cast<const float*>(t.pi_slew + s)[q];
       }
       st_ll(c.rec + 4 * (size_t)v + q, a, sl, ep);
+      reinterpret_cast<float*>(c.at4 + v)[q] = a;
     }
     trace_unit<TRACE>(c, u, t_start, t_start);
     return;
@@ -830,8 +871,9 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
     // overlapping windows are harmless)
     const uint32_t peers = __match_any_sync(kFull, item ? v : kNone);
     const uint32_t head_tl = (uint32_t)(__ffs(peers) - 1) >> 2, end_tl = (uint32_t)(31 - __clz(peers)) >> 2;
-#pragma unroll
-    for (uint32_t j = 1; j < kFwdTerms; j <<= 1) {
+    // rounds: enough for the unit's longest run of terms of one pin
+    const uint32_t nt = __reduce_max_sync(kFull, item ? (uint32_t)__popc(peers) >> 2 : 0u);
+    for (uint32_t j = 1; j < nt; j <<= 1) {
       const float oa = __shfl_down_sync(kFull, ca, 4 * j);
       const float os = __shfl_down_sync(kFull, cs, 4 * j);
       if (tl + j <= end_tl) {
@@ -839,7 +881,10 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
         merge_q(cs, os, el);
       }
     }
-    if (item && tl == head_tl) st_ll(c.rec + 4 * (size_t)v + q, ca, cs, ep);
+    if (item && tl == head_tl) {
+      st_ll(c.rec + 4 * (size_t)v + q, ca, cs, ep);
+      reinterpret_cast<float*>(c.at4 + v)[q] = ca;
+    }
   } else {                                   // one pin with > kFwdTerms terms: warp loop
     const uint32_t v = __shfl_sync(kFull, tr.w, 0), e0 = __shfl_sync(kFull, tr.y, 0), nterms = __shfl_sync(kFull, tr.z, 0);
     const uint32_t dbase = __shfl_sync(kFull, tr.y, 4);   // slot 1: first delay slot
@@ -864,7 +909,10 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
       merge_q(ca, __shfl_xor_sync(kFull, ca, o), el);
       merge_q(cs, __shfl_xor_sync(kFull, cs, o), el);
     }
-    if (tl == 0) st_ll(c.rec + 4 * (size_t)v + q, ca, cs, ep);
+    if (tl == 0) {
+      st_ll(c.rec + 4 * (size_t)v + q, ca, cs, ep);
+      reinterpret_cast<float*>(c.at4 + v)[q] = ca;
+    }
     t_ready = t_start;
   }
   if (TRACE) {                             // latest lane's data arrival
@@ -1095,7 +1143,7 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
     head = act && (lane == 0 || vp != v);    // first lane of its driver
     if (act) {
       const float elm = __ldcg(c.elm + k);
-      load_rec(c, v, at_v, sl_v);
+      at_v = load_at(c, v);
       if (head && drv_work) {
         pa = __ldg(t.pullfo + 2 * (size_t)v);
         pb = __ldg(t.pullfo + 2 * (size_t)v + 1);
@@ -1103,7 +1151,12 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
       const FoPre pre = bwd_pre(c, fa, fb, ep);
       if (TRACE) t_ready = gtimer();
       Q4 a = at_v, s = sl_v, r = undef_rat();
-      net_hop(a, s, elm);                    // the sink's own arrival / slew
+      if (fa.w != kNone) {                   // endpoint sink: its slews feed the check tables
+        s = load_slew(c, v);
+        net_hop(a, s, elm);                  // the sink's own arrival / slew
+      } else {
+        hop_at(a, elm);                      // the sink's own arrival (slews unused)
+      }
       bwd_pin(t, c, L, ep, fa, fb, pre, t.sfo_dst, t.sfo_info, a, s, r);
       if (TRACE) t_data = gtimer();
       c.rat[t.NP + k] = to_f4(r);
@@ -1120,8 +1173,9 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
     // instructions on heavy tiles
     const uint32_t peers = __match_any_sync(kFull, v);
     const uint32_t end = 31 - __clz(peers);
-#pragma unroll
-    for (uint32_t o = 1; o < 32; o <<= 1) {
+    // rounds: enough for the tile's longest run of sinks of one driver
+    const uint32_t run = __reduce_max_sync(kFull, act ? (uint32_t)__popc(peers) : 0u);
+    for (uint32_t o = 1; o < run; o <<= 1) {
       Q4 b;
 #pragma unroll
       for (int q = 0; q < 4; ++q) b.v[q] = __shfl_down_sync(kFull, acc.v[q], o);
@@ -1158,14 +1212,16 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
     v = ud.x + lane;                         // sink-less pins [x0, x1)
     head = v < ud.y;
     if (head) {
-      load_rec(c, v, at_v, sl_v);
+      at_v = load_at(c, v);
       pa = __ldg(t.pullfo + 2 * (size_t)v);
       pb = __ldg(t.pullfo + 2 * (size_t)v + 1);
     }
   }
   // finish driver / pin v
   if (head) {
-    bwd_pin(t, c, L, ep, pa, pb, bwd_pre(c, pa, pb, ep), t.pfo_dst, t.pfo_info, at_v, sl_v, acc);
+    const FoPre pre = bwd_pre(c, pa, pb, ep);
+    if (pa.w != kNone) sl_v = load_slew(c, v);   // the pin's own endpoint seed needs its slews
+    bwd_pin(t, c, L, ep, pa, pb, pre, t.pfo_dst, t.pfo_info, at_v, sl_v, acc);
     const Q4 sp = slack_of(at_v, acc);
     c.slack[v] = to_f4(sp);
     if (pa.w != kNone) write_ep(c, pa.w, sp);
@@ -1467,8 +1523,9 @@ cudaError_t launch_rc(const Topo& t, const Batch& b, uint32_t wgrid, cudaStream_
   cudaError_t e = cudaSuccess;
   const uint32_t K = b.K;
   if (t.n_wtiles && e == cudaSuccess) {
-    // co-resident warps shared by the K corners, at most one tile per warp
-    const uint32_t g = std::max<uint32_t>(1, std::min<uint32_t>(wgrid / K, blocks(32ull * t.n_wtiles)));
+    // 3/4 of the co-resident warps, shared by the K corners (the tier-C
+    // launches on the side stream need room beside it), at most one tile per warp
+    const uint32_t g = std::max<uint32_t>(1, std::min<uint32_t>(wgrid * 3 / 4 / K, blocks(32ull * t.n_wtiles)));
     e = pdl_launch_kernel(rc_warp_kernel, dim3(g, K), kThreads, s, t, b);
   }
   if (t.n_btiles && e == cudaSuccess) e = pdl_launch_kernel(rc_block_kernel, dim3(t.n_btiles, K), kThreads, s, t, b);
