@@ -39,34 +39,45 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = None, flags: str = "") -> str:
+    """Build libsta.so (or, for tuning experiments, a variant at `out` with
+    extra nvcc `flags`, e.g. "-DSTA_FWD_THREADS=640")."""
+    if out is None and not force and not _stale():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
+    lib = out or LIB
+    odir = os.path.dirname(os.path.abspath(lib))
+    os.makedirs(odir, exist_ok=True)
     objs = []
     for src in SOURCES:
-        obj = os.path.join(LIBDIR, src + ".o")
-        cmd = [nvcc(), *NVCC_FLAGS, *os.environ.get("STA_NVCC_FLAGS", "").split(), "-I", os.path.join(ROOT, "include"), "-c",
-               os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(odir, os.path.basename(lib) + "." + src + ".o")
+        cmd = [nvcc(), *NVCC_FLAGS, *os.environ.get("STA_NVCC_FLAGS", "").split(), *flags.split(),
+               "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose:
             sys.stderr.write(r.stderr)
-        with open(os.path.join(LIBDIR, src + ".ptxas.txt"), "w") as f:
+        with open(os.path.join(odir, (os.path.basename(lib) + "." if out else "") + src + ".ptxas.txt"), "w") as f:
             f.write(r.stderr)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
            "-Xcompiler", "-fPIC", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv))
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--out", default=None, help="variant library path (tuning experiments)")
+    ap.add_argument("--flags", default="", help="extra nvcc flags of the variant")
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=a.verbose, out=a.out, flags=a.flags))

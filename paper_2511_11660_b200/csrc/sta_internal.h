@@ -43,6 +43,12 @@ constexpr int kFwdMinBlocks = 1;
 #endif
 constexpr int kBwdThreads = STA_BWD_THREADS;    // backward persistent kernel block size
 constexpr int kBwdMinBlocks = 1;
+#ifndef STA_FWD_PF
+#define STA_FWD_PF 1                            // forward: prefetch term slots 2 and RC results 1 unit ahead
+#endif
+#ifndef STA_MERGE_BOUND
+#define STA_MERGE_BOUND 1                       // merge rounds bounded by the longest run in the warp
+#endif
 #ifndef STA_BWD_PIPE
 #define STA_BWD_PIPE 1                          // backward: prefetch the next unit's fan-out records
 #endif

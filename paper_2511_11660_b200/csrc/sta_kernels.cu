@@ -294,12 +294,34 @@ __device__ __forceinline__ void wtile_run(const CornerDev& c, const WTile& w) {
   if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(c.err_flag, 1u);
 }
 
+#ifndef STA_RCW_PERSIST
+#define STA_RCW_PERSIST 0
+#endif
+#ifndef STA_RCW_TPW
+#define STA_RCW_TPW 2
+#endif
+constexpr uint32_t kRcwTiles = STA_RCW_TPW;   // tiles per warp (non-persistent variant)
+
 __global__ void __launch_bounds__(kThreads) rc_warp_kernel(Topo t, const __grid_constant__ Batch B) {
   pdl_wait();
   pdl_launch();
   const CornerDev& c = B.c[blockIdx.y];
   const float* R = c.rc_vals[0];
   const float* Cw = c.rc_vals[1];
+#if !STA_RCW_PERSIST
+  // short-lived warps (so the tier-C launches on the side stream interleave
+  // with them): kRcwTiles consecutive tiles per warp, all loads issued first
+  const uint32_t x0 = (blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * kRcwTiles;
+  if (x0 >= t.n_wtiles) return;
+  uint4 tl[kRcwTiles];
+#pragma unroll
+  for (uint32_t j = 0; j < kRcwTiles; ++j) tl[j] = x0 + j < t.n_wtiles ? __ldg(t.wtiles + x0 + j) : make_uint4(0, 0, 0, 0);
+  WTile w[kRcwTiles];
+#pragma unroll
+  for (uint32_t j = 0; j < kRcwTiles; ++j) wtile_load(t, R, Cw, tl[j], w[j]);
+#pragma unroll
+  for (uint32_t j = 0; j < kRcwTiles; ++j) wtile_run(c, w[j]);
+#else
   const uint32_t W = gridDim.x * (kThreads / 32);
   uint32_t x = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
   if (x >= t.n_wtiles) return;
@@ -314,6 +336,7 @@ __global__ void __launch_bounds__(kThreads) rc_warp_kernel(Topo t, const __grid_
     wtile_run(c, cur);
     cur = nxt;
   }
+#endif
 }
 
 __device__ __forceinline__ double block_excl_scan(double v, double* s_warp, double* total) {
@@ -871,9 +894,14 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
     // overlapping windows are harmless)
     const uint32_t peers = __match_any_sync(kFull, item ? v : kNone);
     const uint32_t head_tl = (uint32_t)(__ffs(peers) - 1) >> 2, end_tl = (uint32_t)(31 - __clz(peers)) >> 2;
+#if STA_MERGE_BOUND
     // rounds: enough for the unit's longest run of terms of one pin
     const uint32_t nt = __reduce_max_sync(kFull, item ? (uint32_t)__popc(peers) >> 2 : 0u);
     for (uint32_t j = 1; j < nt; j <<= 1) {
+#else
+#pragma unroll
+    for (uint32_t j = 1; j < kFwdTerms; j <<= 1) {
+#endif
       const float oa = __shfl_down_sync(kFull, ca, 4 * j);
       const float os = __shfl_down_sync(kFull, cs, 4 * j);
       if (tl + j <= end_tl) {
@@ -937,15 +965,32 @@ __global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) fwd_persistent_ker
   const uint32_t ep = epoch_of(c);
   const uint32_t tl = (threadIdx.x & 31) >> 2;
   uint32_t u = gw / K;
+#if STA_FWD_PF
+  // software pipeline: term slots two units ahead, the RC results (Elmore
+  // delay of the input hop, load of the pin) one unit ahead, so neither
+  // round trip is exposed when a unit starts
+  const uint4 pad = make_uint4(kNone, kNone, 0, kNone);
+  uint4 tr = u < t.n_fwu ? __ldg(t.fterm + (size_t)kFwdTerms * u + tl) : pad;
+  uint4 nx = u + Wc < t.n_fwu ? __ldg(t.fterm + (size_t)kFwdTerms * (u + Wc) + tl) : pad;
+  FwdRc rc = fwd_rc(c, tr);
+  for (; u < t.n_fwu; u += Wc) {
+    const uint4 nnx = u + 2 * Wc < t.n_fwu ? __ldg(t.fterm + (size_t)kFwdTerms * (u + 2 * Wc) + tl) : pad;
+    const FwdRc nrc = fwd_rc(c, nx);         // nx arrived during the previous unit
+    fwd_unit<TRACE>(t, c, L, ep, u, tr, rc);
+    tr = nx;
+    nx = nnx;
+    rc = nrc;
+  }
+#else
   // software pipeline: the next unit's term slot is in flight while a unit
-  // waits for its producers (the RC results are loaded by the unit itself: prefetching them too
-  // measured slower on C3)
+  // waits for its producers
   uint4 nx = u < t.n_fwu ? __ldg(t.fterm + (size_t)kFwdTerms * u + tl) : make_uint4(0, 0, 0, 0);
   for (; u < t.n_fwu; u += Wc) {
     const uint4 tr = nx;
     if (u + Wc < t.n_fwu) nx = __ldg(t.fterm + (size_t)kFwdTerms * (u + Wc) + tl);   // prefetch the next unit
     fwd_unit<TRACE>(t, c, L, ep, u, tr, fwd_rc(c, tr));
   }
+#endif
 }
 
 // units [u0, u1) of one gate stage, one warp each; grid.y = corner
@@ -1148,8 +1193,13 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
         pa = __ldg(t.pullfo + 2 * (size_t)v);
         pb = __ldg(t.pullfo + 2 * (size_t)v + 1);
       }
-      const FoPre pre = bwd_pre(c, fa, fb, ep);
+      FoPre pre = bwd_pre(c, fa, fb, ep);
       if (TRACE) t_ready = gtimer();
+      // wait for the first fan-out pin's required times BEFORE anything needs
+      // the sink's own arrival: the arrival / Elmore loads issued above then
+      // complete during the wait instead of adding a round trip of their own
+      // (a pin's required-time words are always written, live arc or not)
+      if (fa.w == kNone && fa.y) spin_pair(c.rat_ll + 2 * (size_t)fb.x, pre.e0, pre.l0, ep);
       Q4 a = at_v, s = sl_v, r = undef_rat();
       if (fa.w != kNone) {                   // endpoint sink: its slews feed the check tables
         s = load_slew(c, v);
@@ -1173,9 +1223,14 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
     // instructions on heavy tiles
     const uint32_t peers = __match_any_sync(kFull, v);
     const uint32_t end = 31 - __clz(peers);
+#if STA_MERGE_BOUND
     // rounds: enough for the tile's longest run of sinks of one driver
     const uint32_t run = __reduce_max_sync(kFull, act ? (uint32_t)__popc(peers) : 0u);
     for (uint32_t o = 1; o < run; o <<= 1) {
+#else
+#pragma unroll
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+#endif
       Q4 b;
 #pragma unroll
       for (int q = 0; q < 4; ++q) b.v[q] = __shfl_down_sync(kFull, acc.v[q], o);
@@ -1523,9 +1578,13 @@ cudaError_t launch_rc(const Topo& t, const Batch& b, uint32_t wgrid, cudaStream_
   cudaError_t e = cudaSuccess;
   const uint32_t K = b.K;
   if (t.n_wtiles && e == cudaSuccess) {
+#if STA_RCW_PERSIST
     // 3/4 of the co-resident warps, shared by the K corners (the tier-C
     // launches on the side stream need room beside it), at most one tile per warp
     const uint32_t g = std::max<uint32_t>(1, std::min<uint32_t>(wgrid * 3 / 4 / K, blocks(32ull * t.n_wtiles)));
+#else
+    const uint32_t g = blocks(32ull * ((t.n_wtiles + kRcwTiles - 1) / kRcwTiles));
+#endif
     e = pdl_launch_kernel(rc_warp_kernel, dim3(g, K), kThreads, s, t, b);
   }
   if (t.n_btiles && e == cudaSuccess) e = pdl_launch_kernel(rc_block_kernel, dim3(t.n_btiles, K), kThreads, s, t, b);

@@ -15,7 +15,8 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libsta.so")
+# STA_LIB_PATH selects a tuning variant built by `build.py --out` (experiments only)
+LIB_PATH = os.environ.get("STA_LIB_PATH") or os.path.join(_HERE, "lib", "libsta.so")
 
 STA_MEM_HOST, STA_MEM_DEVICE = 0, 1
 STATUS = ["STA_OK", "STA_ERR_ARG", "STA_ERR_CSR", "STA_ERR_ID", "STA_ERR_MULTIDRIVER",
