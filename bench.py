@@ -43,6 +43,7 @@ def parse():
                     help="c3_superblue (default at N=1), c5_multicorner (default at N>1), c2_tau, c4_tdp")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip e2e/profile/cpu legs (ncu runs)")
+    ap.add_argument("--phases", action="store_true", help="with --quick: still measure the per-phase times")
     return ap.parse_args()
 
 
@@ -316,7 +317,7 @@ def main():
     if res_global:
         line["wns_tns_global"] = res_global
 
-    if not args.quick:
+    if not args.quick or args.phases:
         # roofline: per-phase device time with CUDA events on the ctx stream
         ctx.profile_enable(True)
         for _ in range(min(args.steps, 10)):
@@ -341,6 +342,7 @@ def main():
         line["update_model_bytes"] = whole
         line["update_frac_hbm"] = whole / (ms / 1e3) / 1e9 / peak
 
+    if not args.quick:
         # e2e through the public C ABI with HOST buffers: per step the RC
         # values of every local corner (the per-iteration inputs of an
         # optimization loop) go host -> device from page-locked memory

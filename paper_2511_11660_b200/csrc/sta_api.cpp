@@ -14,6 +14,7 @@
 #include <limits>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -39,6 +40,40 @@ struct PhaseTimer {
     t0 = t1;
   }
 };
+
+// Host parallel-for over [0, n) in T contiguous chunks f(lo, hi, t) (the
+// planner's loops are memory-latency bound and scale with host threads).  f
+// must not throw.
+unsigned host_threads() {
+  static const unsigned T = [] {
+    if (const char* e = std::getenv("STA_HOST_THREADS")) return (unsigned)std::max(1, std::atoi(e));
+    return std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 32u);
+  }();
+  return T;
+}
+template <class F>
+void par_chunks(uint64_t n, F&& f) {
+  const unsigned T = n < 65536 ? 1u : host_threads();
+  if (T == 1) {
+    f((uint64_t)0, n, 0u);
+    return;
+  }
+  std::vector<std::thread> th;
+  th.reserve(T);
+  for (unsigned t = 0; t < T; ++t) th.emplace_back([&f, n, t, T] { f(n * t / T, n * (t + 1) / T, t); });
+  for (auto& x : th) x.join();
+}
+// in-place exclusive prefix sum; returns the total
+template <class T>
+T excl_prefix(std::vector<T>& v) {
+  T run = 0;
+  for (T& x : v) {
+    const T y = x;
+    x = run;
+    run += y;
+  }
+  return run;
+}
 
 struct StaError {
   sta_status st;
@@ -314,15 +349,25 @@ void build_plan(sta_ctx c) {
         fail(STA_ERR_ARG, "pin %u: role %s must not have fan-in", p, c->pin_role[p] == STA_PIN_PI ? "PI" : "FF_CK");
   auto driver_of = [&](u32 p) { return c->net_pins[c->net_ptr[c->pin_net[p]]]; };
 
-  // gate stages in pin-level order
+  // gate stages in pin-level order (the pins of one level are independent)
   c->stage.assign(P, 0);
-  for (u32 p : c->perm) {
-    if (c->is_sink[p]) {
-      c->stage[p] = c->stage[driver_of(p)];
-    } else if (fi_ptr[p + 1] != fi_ptr[p]) {
-      u32 s = 0;
-      for (u32 x = fi_ptr[p]; x < fi_ptr[p + 1]; ++x) s = std::max(s, c->stage[c->arc_from[fi_ids[x]]] + 1);
-      c->stage[p] = s;
+  {
+    std::vector<u32> lptr(c->num_levels + 1, 0);
+    for (u32 p = 0; p < P; ++p) lptr[c->level[p] + 1]++;
+    for (u32 l = 0; l < c->num_levels; ++l) lptr[l + 1] += lptr[l];
+    for (u32 l = 0; l < c->num_levels; ++l) {
+      par_chunks(lptr[l + 1] - lptr[l], [&](uint64_t lo, uint64_t hi, unsigned) {
+        for (uint64_t j = lptr[l] + lo; j < lptr[l] + hi; ++j) {
+          const u32 p = c->perm[j];
+          if (c->is_sink[p]) {
+            c->stage[p] = c->stage[driver_of(p)];
+          } else if (fi_ptr[p + 1] != fi_ptr[p]) {
+            u32 st = 0;
+            for (u32 x = fi_ptr[p]; x < fi_ptr[p + 1]; ++x) st = std::max(st, c->stage[c->arc_from[fi_ids[x]]] + 1);
+            c->stage[p] = st;
+          }
+        }
+      });
     }
   }
 
@@ -365,35 +410,64 @@ void build_plan(sta_ctx c) {
       return 1;
     };
     std::vector<uint8_t> cls(P, 0);
-    for (u32 p = 0; p < P; ++p)
-      if (!c->is_sink[p]) cls[p] = (uint8_t)pin_class(p);
-    for (int pass = 0; pass < 3; ++pass)
-      for (u32 p = 0; p < P; ++p)
-      if (!c->is_sink[p] && cls[p] == pass) {
-        const u32 i = fill[c->stage[p]]++;
-        c->int_of_user[p] = i;
-        c->user_of_int[i] = p;
-      }
+    par_chunks(P, [&](uint64_t lo, uint64_t hi, unsigned) {
+      for (uint64_t p = lo; p < hi; ++p)
+        if (!c->is_sink[p]) cls[p] = (uint8_t)pin_class((u32)p);
+    });
+    // position of pull pin p: its stage's base, then the pins of lower
+    // classes of the stage, then those of its class with a smaller id --
+    // counted per (class, stage, id chunk) so the chunks fill in parallel
+    const unsigned T = P < 65536 ? 1u : host_threads();
+    std::vector<u32> cnt((size_t)T * 3 * S, 0);   // [class][stage][chunk]
+    auto at = [&](u32 cl, u32 st, unsigned t) -> u32& { return cnt[((size_t)cl * S + st) * T + t]; };
+    par_chunks(P, [&](uint64_t lo, uint64_t hi, unsigned t) {
+      for (uint64_t p = lo; p < hi; ++p)
+        if (!c->is_sink[p]) at(cls[p], c->stage[p], t)++;
+    });
+    for (u32 st = 0; st < S; ++st) {
+      u32 run = c->pull_stage_ptr[st];
+      for (u32 cl = 0; cl < 3; ++cl)
+        for (unsigned t = 0; t < T; ++t) {
+          const u32 y = at(cl, st, t);
+          at(cl, st, t) = run;
+          run += y;
+        }
+    }
+    par_chunks(P, [&](uint64_t lo, uint64_t hi, unsigned t) {
+      for (uint64_t p = lo; p < hi; ++p)
+        if (!c->is_sink[p]) {
+          const u32 i = at(cls[p], c->stage[p], t)++;
+          c->int_of_user[p] = i;
+          c->user_of_int[i] = (u32)p;
+        }
+    });
+    (void)fill;
   }
   c->sink_ptr.assign(NP + 1, 0);
   c->drv_of_net.assign(c->N, kNone);
-  u32 k = 0;
-  for (u32 i = 0; i < NP; ++i) {
-    const u32 p = c->user_of_int[i];
-    c->sink_ptr[i] = k;
-    if (p == kNone) continue;                 // padding
-    const u32 n = c->pin_net[p];
-    if (n != kNone) {   // p is the driver of n
-      c->drv_of_net[n] = i;
-      for (u32 x = c->net_ptr[n] + 1; x < c->net_ptr[n + 1]; ++x) {
-        const u32 s = c->net_pins[x];
-        c->int_of_user[s] = NP + k;
-        c->user_of_int[NP + k] = s;
-        ++k;
+  par_chunks(NP, [&](uint64_t lo, uint64_t hi, unsigned) {
+    for (uint64_t i = lo; i < hi; ++i) {
+      const u32 p = c->user_of_int[i];
+      const u32 n = p == kNone ? kNone : c->pin_net[p];
+      c->sink_ptr[i] = n == kNone ? 0 : c->net_ptr[n + 1] - c->net_ptr[n] - 1;
+    }
+  });
+  excl_prefix(c->sink_ptr);
+  par_chunks(NP, [&](uint64_t lo, uint64_t hi, unsigned) {
+    for (uint64_t i = lo; i < hi; ++i) {
+      const u32 p = c->user_of_int[i];
+      if (p == kNone) continue;               // padding
+      const u32 n = c->pin_net[p];
+      if (n == kNone) continue;
+      c->drv_of_net[n] = (u32)i;              // p is the driver of n
+      u32 k = c->sink_ptr[i];
+      for (u32 x = c->net_ptr[n] + 1; x < c->net_ptr[n + 1]; ++x, ++k) {
+        const u32 sp = c->net_pins[x];
+        c->int_of_user[sp] = NP + k;
+        c->user_of_int[NP + k] = sp;
       }
     }
-  }
-  c->sink_ptr[NP] = k;
+  });
   c->sink_stage_ptr.assign(S + 1, 0);
   for (u32 s = 0; s <= S; ++s) c->sink_stage_ptr[s] = c->sink_ptr[c->pull_stage_ptr[s]];
 
@@ -409,59 +483,76 @@ void build_plan(sta_ctx c) {
     return sta::pack_info(sense, c->arc_tab[a]);
   };
 
-  // forward fan-in terms of pull pins (cell arcs, arc id order)
-  std::vector<u32> fi_p(NP + 1, 0), fi_src, fi_hop, fi_info, arc_term(c->A, kNone);
-  fi_src.reserve(c->A);
-  fi_hop.reserve(c->A);
-  fi_info.reserve(c->A);
-  for (u32 i = 0; i < NP; ++i) {
-    const u32 p = c->user_of_int[i];
-    fi_p[i] = (u32)fi_src.size();
-    if (p == kNone) continue;
-    for (u32 x = fi_ptr[p]; x < fi_ptr[p + 1]; ++x) {
-      const u32 a = fi_ids[x], u = c->arc_from[a];
-      arc_term[a] = (u32)fi_src.size();
-      for (u32 q = 0; q < n_terms(a); ++q) {
-        if (c->is_sink[u]) {
-          fi_src.push_back(c->int_of_user[driver_of(u)]);
-          fi_hop.push_back(c->int_of_user[u] - NP);
-        } else {
-          fi_src.push_back(c->int_of_user[u]);
-          fi_hop.push_back(kNone);
+  // forward fan-in terms of pull pins (cell arcs, arc id order): counted,
+  // prefix-summed, then filled in parallel
+  std::vector<u32> fi_p(NP + 1, 0), arc_term(c->A, kNone);
+  par_chunks(NP, [&](uint64_t lo, uint64_t hi, unsigned) {
+    for (uint64_t i = lo; i < hi; ++i) {
+      const u32 p = c->user_of_int[i];
+      u32 n = 0;
+      if (p != kNone)
+        for (u32 x = fi_ptr[p]; x < fi_ptr[p + 1]; ++x) n += n_terms(fi_ids[x]);
+      fi_p[i] = n;
+    }
+  });
+  const u32 n_fi = excl_prefix(fi_p);
+  std::vector<u32> fi_src(n_fi), fi_hop(n_fi), fi_info(n_fi);
+  par_chunks(NP, [&](uint64_t lo, uint64_t hi, unsigned) {
+    for (uint64_t i = lo; i < hi; ++i) {
+      const u32 p = c->user_of_int[i];
+      if (p == kNone) continue;
+      u32 e = fi_p[i];
+      for (u32 x = fi_ptr[p]; x < fi_ptr[p + 1]; ++x) {
+        const u32 a = fi_ids[x], u = c->arc_from[a];
+        arc_term[a] = e;
+        for (u32 q = 0; q < n_terms(a); ++q, ++e) {
+          if (c->is_sink[u]) {
+            fi_src[e] = c->int_of_user[driver_of(u)];
+            fi_hop[e] = c->int_of_user[u] - NP;
+          } else {
+            fi_src[e] = c->int_of_user[u];
+            fi_hop[e] = kNone;
+          }
+          fi_info[e] = term_info(a, q);
         }
-        fi_info.push_back(term_info(a, q));
       }
     }
-  }
-  fi_p[NP] = (u32)fi_src.size();
+  });
 
-  // backward: cell fan-out of sinks and of pull pins
-  std::vector<u32> sfo_p(c->NS + 1, 0), sfo_dst, sfo_info, pfo_p(NP + 1, 0), pfo_dst, pfo_info;
-  for (u32 kk = 0; kk < c->NS; ++kk) {
-    const u32 u = c->user_of_int[NP + kk];
-    sfo_p[kk] = (u32)sfo_dst.size();
+  // backward: cell fan-out of sinks and of pull pins (same two passes)
+  std::vector<u32> sfo_p(c->NS + 1, 0), pfo_p(NP + 1, 0);
+  auto fo_count = [&](u32 u) {
+    u32 n = 0;
+    for (u32 x = fo_ptr[u]; x < fo_ptr[u + 1]; ++x) n += n_terms(fo_ids[x]);
+    return n;
+  };
+  par_chunks(c->NS, [&](uint64_t lo, uint64_t hi, unsigned) {
+    for (uint64_t kk = lo; kk < hi; ++kk) sfo_p[kk] = fo_count(c->user_of_int[NP + kk]);
+  });
+  par_chunks(NP, [&](uint64_t lo, uint64_t hi, unsigned) {
+    for (uint64_t i = lo; i < hi; ++i) {
+      const u32 u = c->user_of_int[i];
+      pfo_p[i] = u == kNone ? 0 : fo_count(u);
+    }
+  });
+  const u32 n_sfo = excl_prefix(sfo_p), n_pfo = excl_prefix(pfo_p);
+  std::vector<u32> sfo_dst(n_sfo), sfo_info(n_sfo), pfo_dst(n_pfo), pfo_info(n_pfo);
+  auto fo_fill = [&](u32 u, u32 e, std::vector<u32>& dst, std::vector<u32>& info) {
     for (u32 x = fo_ptr[u]; x < fo_ptr[u + 1]; ++x) {
       const u32 a = fo_ids[x];
-      for (u32 q = 0; q < n_terms(a); ++q) {
-        sfo_dst.push_back(c->int_of_user[c->arc_to[a]]);
-        sfo_info.push_back(arc_term[a] + q);   // term index; becomes sense | delay slot << 3 below
+      for (u32 q = 0; q < n_terms(a); ++q, ++e) {
+        dst[e] = c->int_of_user[c->arc_to[a]];
+        info[e] = arc_term[a] + q;             // term index; becomes sense | delay slot << 3 below
       }
     }
-  }
-  sfo_p[c->NS] = (u32)sfo_dst.size();
-  for (u32 i = 0; i < NP; ++i) {
-    const u32 u = c->user_of_int[i];
-    pfo_p[i] = (u32)pfo_dst.size();
-    if (u == kNone) continue;
-    for (u32 x = fo_ptr[u]; x < fo_ptr[u + 1]; ++x) {
-      const u32 a = fo_ids[x];
-      for (u32 q = 0; q < n_terms(a); ++q) {
-        pfo_dst.push_back(c->int_of_user[c->arc_to[a]]);
-        pfo_info.push_back(arc_term[a] + q);
-      }
-    }
-  }
-  pfo_p[NP] = (u32)pfo_dst.size();
+  };
+  par_chunks(c->NS, [&](uint64_t lo, uint64_t hi, unsigned) {
+    for (uint64_t kk = lo; kk < hi; ++kk) fo_fill(c->user_of_int[NP + kk], sfo_p[kk], sfo_dst, sfo_info);
+  });
+  par_chunks(NP, [&](uint64_t lo, uint64_t hi, unsigned) {
+    for (uint64_t i = lo; i < hi; ++i)
+      if (c->user_of_int[i] != kNone) fo_fill(c->user_of_int[i], pfo_p[i], pfo_dst, pfo_info);
+  });
 
   tm.mark("plan: fan-in / fan-out terms");
   // backward warp tiles per stage: runs of <= 32 consecutive sinks that never
@@ -771,16 +862,32 @@ void build_rc(sta_ctx c) {
   } grp[3];
   std::vector<u32> net_drv;
   net_drv.reserve(N);
-  std::vector<u32> cnt, ch, pos, endp, pre, dp;
-  std::vector<std::pair<u32, u32>> stack;
   std::vector<uint4> wtiles;                // warp tiles of nets with 1..32 nodes
   std::vector<uint2> btiles;                // block tiles of nets with 33..kBNet nodes (group-1 offsets)
   std::vector<u32> lumped_j, tierC;
   std::vector<u32> tc_end, tc_ev;
+  auto tier_of = [](u32 m) { return m <= 32 ? 0 : m <= sta::kBNet ? 1 : 2; };
+  auto lg = [](u32 x) { u32 r = 0; while ((1u << r) < x) ++r; return r; };
+  // (1, parallel) depth of the deepest root path of every tier-A net
+  std::vector<uint8_t> depth_lg(N, 0);
+  par_chunks(N, [&](uint64_t lo, uint64_t hi, unsigned) {
+    std::vector<u32> dp;
+    for (uint64_t n = lo; n < hi; ++n) {
+      const u32 ub = c->rc_ptr[n], m = c->rc_ptr[n + 1] - ub;
+      if (m == 0 || m > 32) continue;
+      u32 depth = 0;
+      dp.assign(m, 0);
+      for (u32 q = 1; q < m; ++q) depth = std::max(depth, dp[q] = dp[(u32)c->rc_parent[ub + q]] + 1);
+      depth_lg[n] = (uint8_t)lg(depth);
+    }
+  });
+  // (2, sequential, sizes only) nets in the caller's net order: the caller's
+  // R / Cw arrays (borrowed, node order of the caller) are then read nearly
+  // contiguously; the scattered 4-byte outputs (load per driver, Elmore per
+  // sink) stay in L2.  Group offsets, warp / block tiles.
+  std::vector<u32> net_x0(N, kNone), net_tile(N, kNone);
+  u32 gsz[3] = {0, 0, 0};
   u32 wt_fill = 0, wt_cend = kNone;         // open warp tile: nodes, caller node one past its last
-  // nets in the caller's net order: the caller's R / Cw arrays (borrowed,
-  // node order of the caller) are then read nearly contiguously; the
-  // scattered 4-byte outputs (load per driver, Elmore per sink) stay in L2
   for (u32 n = 0; n < N; ++n) {
     const u32 i = c->drv_of_net[n];
     if (i == kNone) continue;
@@ -791,94 +898,123 @@ void build_rc(sta_ctx c) {
       lumped_j.push_back(j);
       continue;
     }
-    const int tier = m <= 32 ? 0 : m <= sta::kBNet ? 1 : 2;
-    Group& G = grp[tier];
-    const u32 x0 = (u32)G.user.size();
-    cnt.assign(m + 1, 0);
-    ch.resize(m);
-    pos.resize(m);
-    endp.resize(m);
-    pre.clear();
-    for (u32 q = 1; q < m; ++q) cnt[(u32)c->rc_parent[ub + q] + 1]++;
-    for (u32 q = 0; q < m; ++q) cnt[q + 1] += cnt[q];
-    {
-      std::vector<u32> fill(cnt.begin(), cnt.end() - 1);
-      for (u32 q = 1; q < m; ++q) ch[fill[(u32)c->rc_parent[ub + q]]++] = q;
-    }
-    stack.assign(1, {0u, 0u});
-    pos[0] = 0;
-    pre.push_back(0);
-    while (!stack.empty()) {
-      const u32 nd = stack.back().first;
-      if (cnt[nd] + stack.back().second < cnt[nd + 1]) {
-        const u32 cld = ch[cnt[nd] + stack.back().second++];
-        pos[cld] = (u32)pre.size();
-        pre.push_back(cld);
-        stack.push_back({cld, 0u});
-      } else {
-        endp[pos[nd]] = (u32)pre.size();
-        stack.pop_back();
-      }
-    }
-    if (tier == 0 && (wtiles.empty() || wt_fill + m > 32 || ub != wt_cend)) {
-      // a warp tile's caller nodes must be one contiguous range (the kernel
-      // loads them by lane and permutes with a shuffle)
-      wtiles.push_back(make_uint4(x0, 0, ub, 0));
-      wt_fill = 0;
-    }
-    for (u32 t2 = 0; t2 < m; ++t2) {
-      const u32 q = pre[t2];
-      const u32 un = ub + q;
-      G.user.push_back(un);
-      G.z.push_back(tier == 0 ? un - wtiles.back().z : un);
-      if (tier == 0) {
-        const u32 ppos = q ? pos[(u32)c->rc_parent[un]] : 0xFFu;
-        G.meta.push_back(t2 | (ppos << 8) | (endp[t2] << 16));
-      } else if (tier == 1) {
-        const u32 ppos = q ? pos[(u32)c->rc_parent[un]] : 0x7FFu;
-        G.meta.push_back(t2 | (ppos << 10) | (endp[t2] << 21));
-      } else {
-        G.meta.push_back(0);                // tier C: tc_* arrays
-      }
-      const u32 pin = c->rc_node_pin[un];
-      u32 tag = kNone;
-      if (t2 == 0) tag = i | 0x80000000u;                      // root: the driver
-      else if (pin != kNone && c->is_sink[pin]) tag = c->int_of_user[pin] - c->NP;
-      G.tag.push_back(tag);
-    }
+    const int tier = tier_of(m);
+    const u32 x0 = gsz[tier];
+    net_x0[n] = x0;
+    gsz[tier] += m;
     if (tier == 0) {
-      wtiles.back().y += m;
+      if (wtiles.empty() || wt_fill + m > 32 || ub != wt_cend) {
+        // a warp tile's caller nodes must be one contiguous range (the kernel
+        // loads them by lane and permutes with a shuffle)
+        wtiles.push_back(make_uint4(x0, 0, ub, 0));
+        wt_fill = 0;
+      }
+      uint4& wt = wtiles.back();
+      wt.y += m;
       wt_fill += m;
       wt_cend = ub + m;
       // rounds the warp kernel needs for this tile: ceil(log2) of the
       // largest net (segmented scan) and of the deepest root path (pointer
       // jumping; the root itself carries no resistance)
-      u32 depth = 0;
-      dp.assign(m, 0);
-      for (u32 q = 1; q < m; ++q) depth = std::max(depth, dp[q] = dp[(u32)c->rc_parent[ub + q]] + 1);
-      auto lg = [](u32 x) { u32 r = 0; while ((1u << r) < x) ++r; return r; };
-      uint4& wt = wtiles.back();
-      wt.w = std::max(wt.w & 0xFFu, lg(m)) | (std::max((wt.w >> 8) & 0xFFu, lg(depth)) << 8);
+      wt.w = std::max(wt.w & 0xFFu, lg(m)) | (std::max((wt.w >> 8) & 0xFFu, (u32)depth_lg[n]) << 8);
+      net_tile[n] = (u32)wtiles.size() - 1;
     } else if (tier == 1) {
       if (btiles.empty() || btiles.back().y + m > sta::kBNet) btiles.push_back(make_uint2(x0, 0));
       btiles.back().y += m;
     } else {
-      // tier C (> kBNet nodes): one global array of their nodes (each net in
-      // preorder, as internally), subtree ends, and the Euler event sequence
-      // (before entering position t2: exit every node whose subtree ends
-      // there, deepest first; after the last node: exit the rest)
-      tierC.push_back(j);
-      const u32 g0 = x0;                    // tier-C positions are group-2 internal offsets
-      std::vector<std::vector<u32>> ends_at(m + 1);
-      for (u32 a2 = 0; a2 < m; ++a2) ends_at[endp[a2]].push_back(a2);
-      for (u32 t2 = 0; t2 <= m; ++t2) {
-        for (auto it = ends_at[t2].rbegin(); it != ends_at[t2].rend(); ++it) tc_ev.push_back((g0 + *it) | 0x80000000u);
-        if (t2 == m) break;
-        tc_ev.push_back(g0 + t2);
-        tc_end.push_back(g0 + endp[t2]);
-      }
-      if (tc_ev.size() != 2 * (size_t)(g0 + m)) fail(STA_ERR_RC, "internal error: Euler tour of net %u", n);
+      tierC.push_back(n);
     }
+  }
+  for (int g = 0; g < 3; ++g) {
+    grp[g].user.resize(gsz[g]);
+    grp[g].meta.resize(gsz[g]);
+    grp[g].tag.resize(gsz[g]);
+    grp[g].z.resize(gsz[g]);
+  }
+  tc_end.resize(gsz[2]);
+  // (3, parallel) each net's nodes renumbered in DFS preorder (children in
+  // increasing index order)
+  struct Dfs {
+    std::vector<u32> cnt, ch, pos, endp, pre;
+    std::vector<std::pair<u32, u32>> stack;
+    void run(const int32_t* par, u32 m) {
+      cnt.assign(m + 1, 0);
+      ch.resize(m);
+      pos.resize(m);
+      endp.resize(m);
+      pre.clear();
+      for (u32 q = 1; q < m; ++q) cnt[(u32)par[q] + 1]++;
+      for (u32 q = 0; q < m; ++q) cnt[q + 1] += cnt[q];
+      {
+        std::vector<u32> fill(cnt.begin(), cnt.end() - 1);
+        for (u32 q = 1; q < m; ++q) ch[fill[(u32)par[q]]++] = q;
+      }
+      stack.assign(1, {0u, 0u});
+      pos[0] = 0;
+      pre.push_back(0);
+      while (!stack.empty()) {
+        const u32 nd = stack.back().first;
+        if (cnt[nd] + stack.back().second < cnt[nd + 1]) {
+          const u32 cld = ch[cnt[nd] + stack.back().second++];
+          pos[cld] = (u32)pre.size();
+          pre.push_back(cld);
+          stack.push_back({cld, 0u});
+        } else {
+          endp[pos[nd]] = (u32)pre.size();
+          stack.pop_back();
+        }
+      }
+    }
+  };
+  par_chunks(N, [&](uint64_t lo, uint64_t hi, unsigned) {
+    Dfs D;
+    for (uint64_t n = lo; n < hi; ++n) {
+      const u32 x0 = net_x0[n];
+      if (x0 == kNone) continue;
+      const u32 i = c->drv_of_net[n];
+      const u32 ub = c->rc_ptr[n], m = c->rc_ptr[n + 1] - ub;
+      const int tier = tier_of(m);
+      Group& G = grp[tier];
+      D.run(c->rc_parent.data() + ub, m);
+      const u32 zb = tier == 0 ? wtiles[net_tile[n]].z : 0;
+      for (u32 t2 = 0; t2 < m; ++t2) {
+        const u32 q = D.pre[t2];
+        const u32 un = ub + q;
+        G.user[x0 + t2] = un;
+        G.z[x0 + t2] = un - zb;
+        if (tier == 0) {
+          const u32 ppos = q ? D.pos[(u32)c->rc_parent[un]] : 0xFFu;
+          G.meta[x0 + t2] = t2 | (ppos << 8) | (D.endp[t2] << 16);
+        } else if (tier == 1) {
+          const u32 ppos = q ? D.pos[(u32)c->rc_parent[un]] : 0x7FFu;
+          G.meta[x0 + t2] = t2 | (ppos << 10) | (D.endp[t2] << 21);
+        } else {
+          G.meta[x0 + t2] = 0;                // tier C: tc_* arrays
+          tc_end[x0 + t2] = x0 + D.endp[t2];
+        }
+        const u32 pin = c->rc_node_pin[un];
+        u32 tag = kNone;
+        if (t2 == 0) tag = i | 0x80000000u;                      // root: the driver
+        else if (pin != kNone && c->is_sink[pin]) tag = c->int_of_user[pin] - c->NP;
+        G.tag[x0 + t2] = tag;
+      }
+    }
+  });
+  // (4) tier C (> kBNet nodes): one global array of their nodes (each net in
+  // preorder, as internally), subtree ends, and the Euler event sequence
+  // (before entering position t2: exit every node whose subtree ends there,
+  // deepest first; after the last node: exit the rest)
+  tc_ev.reserve(2ull * gsz[2]);
+  for (u32 n : tierC) {
+    const u32 g0 = net_x0[n], m = c->rc_ptr[n + 1] - c->rc_ptr[n];
+    std::vector<std::vector<u32>> ends_at(m + 1);
+    for (u32 a2 = 0; a2 < m; ++a2) ends_at[tc_end[g0 + a2] - g0].push_back(a2);
+    for (u32 t2 = 0; t2 <= m; ++t2) {
+      for (auto it = ends_at[t2].rbegin(); it != ends_at[t2].rend(); ++it) tc_ev.push_back((g0 + *it) | 0x80000000u);
+      if (t2 == m) break;
+      tc_ev.push_back(g0 + t2);
+    }
+    if (tc_ev.size() != 2 * (size_t)(g0 + m)) fail(STA_ERR_RC, "internal error: Euler tour of net %u", n);
   }
   // concatenate the groups; rebase block tiles and tier-C internal ids
   const u32 nA = (u32)grp[0].user.size(), nB = (u32)grp[1].user.size();
