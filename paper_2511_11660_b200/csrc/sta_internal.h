@@ -37,12 +37,21 @@ constexpr uint32_t kFwdUnitTerms = 8;          // forward warp unit: fan-in term
 #define STA_FWD_THREADS 1024
 #endif
 constexpr int kFwdThreads = STA_FWD_THREADS;    // forward persistent kernel block size
-constexpr int kFwdMinBlocks = 1;
+#ifndef STA_FWD_MINB
+#define STA_FWD_MINB 1
+#endif
+constexpr int kFwdMinBlocks = STA_FWD_MINB;
 #ifndef STA_BWD_THREADS
 #define STA_BWD_THREADS 640
 #endif
 constexpr int kBwdThreads = STA_BWD_THREADS;    // backward persistent kernel block size
-constexpr int kBwdMinBlocks = 1;
+#ifndef STA_BWD_MINB
+#define STA_BWD_MINB 1
+#endif
+constexpr int kBwdMinBlocks = STA_BWD_MINB;
+#ifndef STA_BWD_SPIN_FIRST
+#define STA_BWD_SPIN_FIRST 0                    // wait on the first fan-out pin before loading the arrival
+#endif
 #ifndef STA_FWD_PF
 #define STA_FWD_PF 1                            // forward: prefetch term slots 2 and RC results 1 unit ahead
 #endif

@@ -107,7 +107,9 @@ __device__ __forceinline__ float lut(const float* __restrict__ L, uint32_t tab, 
 // falling edge from f.  Non-unate arcs (all four pairs) never reach the
 // kernels: the plan expands each into a positive- and a negative-unate term.
 __device__ __forceinline__ int primary_irf(uint32_t sense, int orf) {
-  return sense == 1 ? 1 - orf : sense == 3 ? 0 : sense == 4 ? 1 : orf;
+  // bit (2 sense + orf) of 0x306: POS r<-r f<-f, NEG crossed, RISE_EDGE r,
+  // FALL_EDGE f (branch-free: 3 instructions instead of a compare chain)
+  return (int)((0x306u >> (2 * sense + (uint32_t)orf)) & 1u);
 }
 
 // Copy the table pools of the batch's corners into shared memory, each at its
@@ -1199,7 +1201,9 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
       // the sink's own arrival: the arrival / Elmore loads issued above then
       // complete during the wait instead of adding a round trip of their own
       // (a pin's required-time words are always written, live arc or not)
+#if STA_BWD_SPIN_FIRST
       if (fa.w == kNone && fa.y) spin_pair(c.rat_ll + 2 * (size_t)fb.x, pre.e0, pre.l0, ep);
+#endif
       Q4 a = at_v, s = sl_v, r = undef_rat();
       if (fa.w != kNone) {                   // endpoint sink: its slews feed the check tables
         s = load_slew(c, v);
