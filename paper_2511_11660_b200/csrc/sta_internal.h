@@ -31,8 +31,8 @@ constexpr uint32_t kFwdUnitTerms = 8;          // forward warp unit: fan-in term
 // staged NLDM pools of every corner of a batch exist once per SM (8 corners of
 // LIB-SYN = 190 KB).  Warps per SM are the register budget tuned on C3 (the
 // forward's short per-lane chains want many warps, the backward's one-lane-per-
-// sink chains want registers): 32 forward warps (<= 64 registers), 20 backward
-// warps (<= 102 registers).
+// sink chains want registers): 32 forward warps (<= 64 registers), 24 backward
+// warps (<= 85 registers); more forward warps measured slower (r2 sweep).
 #ifndef STA_FWD_THREADS
 #define STA_FWD_THREADS 1024
 #endif
@@ -42,7 +42,7 @@ constexpr int kFwdThreads = STA_FWD_THREADS;    // forward persistent kernel blo
 #endif
 constexpr int kFwdMinBlocks = STA_FWD_MINB;
 #ifndef STA_BWD_THREADS
-#define STA_BWD_THREADS 640
+#define STA_BWD_THREADS 768
 #endif
 constexpr int kBwdThreads = STA_BWD_THREADS;    // backward persistent kernel block size
 #ifndef STA_BWD_MINB
@@ -56,7 +56,7 @@ constexpr int kBwdMinBlocks = STA_BWD_MINB;
 #define STA_FWD_PF 1                            // forward: prefetch term slots 2 and RC results 1 unit ahead
 #endif
 #ifndef STA_MERGE_BOUND
-#define STA_MERGE_BOUND 1                       // merge rounds bounded by the longest run in the warp
+#define STA_MERGE_BOUND 0                       // 1: merge rounds bounded by the longest run in the warp (measured slower)
 #endif
 #ifndef STA_BWD_PIPE
 #define STA_BWD_PIPE 1                          // backward: prefetch the next unit's fan-out records
