@@ -178,13 +178,22 @@ __device__ __forceinline__ bool ll_ok(const uint4& w, uint32_t ep) { return w.y 
 #ifndef STA_MAX_SLEEP_NS
 #define STA_MAX_SLEEP_NS 128
 #endif
+#ifndef STA_MIN_SLEEP_NS
+#define STA_MIN_SLEEP_NS 32
+#endif
 constexpr uint32_t kMaxSleepNs = STA_MAX_SLEEP_NS;
-__device__ __forceinline__ uint4 spin_ll(const uint4* p, uint32_t ep) {
-  uint4 w = ld_ll(p);
-  uint32_t ns = 32;
-  while (!ll_ok(w, ep)) {
+constexpr uint32_t kMinSleepNs = STA_MIN_SLEEP_NS;
+__device__ __forceinline__ void backoff(uint32_t& ns) {
+  if (kMaxSleepNs) {
     __nanosleep(ns);
     ns = ns < kMaxSleepNs ? 2 * ns : ns;
+  }
+}
+__device__ __forceinline__ uint4 spin_ll(const uint4* p, uint32_t ep) {
+  uint4 w = ld_ll(p);
+  uint32_t ns = kMinSleepNs;
+  while (!ll_ok(w, ep)) {
+    backoff(ns);
     w = ld_ll(p);
   }
   return w;
@@ -1094,8 +1103,8 @@ __device__ __forceinline__ FoPre bwd_pre(const CornerDev& c, const uint4& fa, co
 }
 
 __device__ __forceinline__ void spin_pair(const uint4* p, uint4& we, uint4& wl, uint32_t ep) {
-  for (uint32_t ns = 32; !ll_ok(we, ep) || !ll_ok(wl, ep); ns = ns < kMaxSleepNs ? 2 * ns : ns) {
-    __nanosleep(ns);
+  for (uint32_t ns = kMinSleepNs; !ll_ok(we, ep) || !ll_ok(wl, ep);) {
+    backoff(ns);
     if (!ll_ok(we, ep)) we = ld_ll(p);
     if (!ll_ok(wl, ep)) wl = ld_ll(p + 1);
   }
