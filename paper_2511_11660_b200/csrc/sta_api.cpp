@@ -1264,7 +1264,7 @@ u32 enqueue_batch(sta_ctx c, const sta::Batch& b) {
   }
   ck(sta::launch_rc(t, b, c->wgrid, s), "rc kernel");
   if (t.nC && !std::getenv("STA_RC_SERIAL")) ck(cudaStreamWaitEvent(s, c->join_ev, 0), "join wait");
-  launches += (t.n_wtiles ? 1 : 0) + (t.n_btiles ? 1 : 0) + (t.n_lumped ? 1 : 0) + (t.nC ? 3 : 0);
+  launches += (t.n_wtiles ? 1 : 0) + (t.n_btiles ? 1 : 0) + (t.n_lumped ? 1 : 0) + (t.nC ? 2 : 0);
   prof_mark(c, 1);
   if (c->use_persistent && c->pgrid && c->pgrid_b) {
     prof_mark(c, 2);

@@ -55,6 +55,9 @@ constexpr int kBwdMinBlocks = STA_BWD_MINB;
 #ifndef STA_FWD_PF
 #define STA_FWD_PF 1                            // forward: prefetch term slots 2 and RC results 1 unit ahead
 #endif
+#ifndef STA_FWD_RECPF
+#define STA_FWD_RECPF 1                         // forward: next unit's record words loaded speculatively
+#endif
 #ifndef STA_MERGE_BOUND
 #define STA_MERGE_BOUND 0                       // 1: merge rounds bounded by the longest run in the warp (measured slower)
 #endif
@@ -225,16 +228,17 @@ constexpr int kRedBlocks = 4 * 148;
 // dependent launch, return cudaGetLastError().  Every launch covers the
 // corners of batch b (grid.y = corner for the data-parallel kernels).
 // RC of nets with <= kBNet nodes and lumped nets; tier C (nets > kBNet nodes) is
-// independent of it and is enqueued on a second stream (3 launches)
+// independent of it and is enqueued on a second stream (2 launches)
 cudaError_t launch_rc(const Topo& t, const Batch& b, uint32_t wgrid, cudaStream_t s);
 cudaError_t launch_rc_tierC(const Topo& t, const Batch& b, cudaStream_t s);
-// tier-C scratch (doubles): Sx/Si pairs [2 nCn], event sums [2 nCn], then per
-// scan (2) and block: {aggregate, carry, first head, has head}, then the two
-// last-block counters (u32, zero-initialised, self-resetting)
+// tier-C scratch: Si [nCn] (double), block aggregates of the node and the
+// event scans [nbn + nbe] (double), their flags [nbn + nbe] (u32 {has head,
+// epoch}) and the two tile tickets (u32, zero-initialised, monotonic)
 constexpr uint32_t kTcTile = 2048;              // elements per tier-C block (256 threads x 8)
 __host__ __device__ inline uint32_t tierC_blocks(uint64_t n) { return (uint32_t)((n + kTcTile - 1) / kTcTile); }
 __host__ __device__ inline size_t tierC_scratch(uint32_t nCn) {
-  return 4 * (size_t)nCn + 2 * 4 * (size_t)tierC_blocks(2ull * nCn) + 2;
+  const size_t nb = (size_t)tierC_blocks(nCn) + tierC_blocks(2ull * nCn);
+  return (size_t)nCn + nb + (nb + 2 + 1) / 2 + 1;
 }
 uint32_t rc_warp_grid();                        // co-resident grid of the tier-A kernel (per corner)
 // units [u0, u1) of one gate stage (one launch per stage, grid.y = corner)

@@ -483,19 +483,21 @@ __global__ void __launch_bounds__(kThreads) rc_lumped_kernel(Topo t, const __gri
 
 // ---- tier C: segmented prefix sums over ONE global preorder array of the
 // large nets' nodes and over its Euler event sequence (layout in
-// sta_internal.h).  Three data-parallel launches per corner on a side stream,
+// sta_internal.h).  Two single-pass launches per corner on a side stream,
 // concurrent with tiers A and B:
-//   tc_node_kernel   node caps C -> block-local segmented inclusive sums Si
-//                    (segment = net), block aggregates; the last block turns
-//                    the aggregates into per-block carries;
+//   tc_node_kernel   node caps C -> segmented inclusive sums Si (segment =
+//                    net), stored;
 //   tc_event_kernel  w(g) = R(g) Cdown(g), Cdown(g) = Si[end(g) - 1] - Si[g] +
-//                    C(g) (carried reads); event values +-w -> block-local
-//                    segmented sums H, block carries as above; net loads;
-//   tc_elm_kernel    elm(g) = H[enter(g)] (carried) for the sink nodes.
-// Every sum has a fixed association (thread-serial runs, fixed shuffle trees,
-// a fixed-order carry pass): bitwise reproducible.  A segmented scan never
-// crosses a net, so the sums stay small (no cancellation against the sums of
-// other nets) and a net's Elmore delays need no offset.
+//                    C(g); event values +-w -> segmented inclusive sums H;
+//                    elm(g) = H[enter(g)] written directly, net loads.
+// Each block scans its tile locally, publishes its segmented aggregate and
+// takes its carry-in from its predecessors by a look-back over their
+// AGGREGATES only (back to the nearest block holding a segment head), summed
+// in a fixed order: the association never depends on timing, so the sums
+// are bitwise reproducible.  Tiles are handed out by a ticket in block start
+// order, so a block only ever waits for blocks that are already running.  A
+// segmented scan never crosses a net: the sums stay small (no cancellation
+// against other nets) and a net's Elmore delays need no offset.
 struct SegSum {
   double v;
   uint32_t f;   // a segment head inside
@@ -535,63 +537,84 @@ __device__ __forceinline__ SegSum seg_block_excl(SegSum x, SegSum* s_w, SegSum* 
 
 constexpr int kTcPer = (int)(kTcTile / kThreads);   // consecutive elements per thread
 
-// per-scan block records in the scratch: agg[nb], carry[nb], first head[nb] (as double)
+// per-scan block records in the scratch: aggregate[nb] (double), flag[nb] (u32
+// {has head, epoch}: bit 31 = has head, bits 0..30 = epoch)
 struct TcScan {
   double* agg;
-  double* carry;
-  double* fh;
-  double* hh;
+  uint32_t* flag;
 };
-__device__ __forceinline__ TcScan tc_scan(double* base, uint32_t nb) { return TcScan{base, base + nb, base + 2 * nb, base + 3 * nb}; }
 
-// Block b publishes {aggregate, first head, has head}; the last block to
-// finish turns all aggregates into carries (exclusive segmented scan over the
-// blocks, chunks of kThreads in a fixed order).
-__device__ void tc_publish(const TcScan& sc, uint32_t nb, SegSum agg, uint32_t first_head, uint32_t* counter,
-                           SegSum* s_w) {
-  __shared__ bool last;
-  if (threadIdx.x == 0) {
-    sc.agg[blockIdx.x] = agg.v;
-    sc.hh[blockIdx.x] = agg.f ? 1.0 : 0.0;
-    sc.fh[blockIdx.x] = (double)first_head;
-    __threadfence();
-    last = atomicAdd(counter, 1u) == nb - 1;
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  SegSum run{0.0, 0u};
-  for (uint32_t b0 = 0; b0 < nb; b0 += kThreads) {
-    const uint32_t b = b0 + threadIdx.x;
-    const SegSum x = b < nb ? SegSum{__ldcg(sc.agg + b), __ldcg(sc.hh + b) != 0.0 ? 1u : 0u} : SegSum{0.0, 0u};
-    SegSum tot;
-    const SegSum ex = seg_block_excl(x, s_w, &tot);
-    if (b < nb) sc.carry[b] = seg_op(run, ex).v;
-    run = seg_op(run, tot);
-  }
-  if (threadIdx.x == 0) *counter = 0;          // self-reset for the next update
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
-// carried read of a block-local segmented sum at global position g
-__device__ __forceinline__ double tc_read(const double* loc, const TcScan& sc, uint32_t g) {
-  const uint32_t b = g / kTcTile;
-  const double v = __ldcg(loc + g);
-  return (double)g < __ldg(sc.fh + b) ? v + __ldg(sc.carry + b) : v;
+// Block b: publish the aggregate (the sum after its last head, or the whole
+// tile), then return the carry-in of its elements before its first head: the
+// fixed-order sum of the aggregates of b - 1, b - 2, ... down to and
+// including the nearest block that holds a head.  Warp 0 looks back 32
+// blocks per round trip.
+__device__ double tc_lookback(const TcScan& sc, uint32_t b, SegSum tot, uint32_t ep) {
+  __shared__ double s_carry;
+  if (threadIdx.x == 0) {
+    sc.agg[b] = tot.v;
+    __threadfence();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(sc.flag + b), "r"((tot.f ? 0x80000000u : 0u) | ep)
+                 : "memory");
+  }
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double carry = 0.0;
+    bool done = b == 0;
+    for (int64_t p0 = (int64_t)b - 1; !done; p0 -= 32) {
+      const int64_t p = p0 - lane;                  // lane 0 = nearest predecessor
+      uint32_t f = 0x80000000u;                    // past block 0: a virtual head
+      double v = 0.0;
+      if (p >= 0) {
+        do {
+          f = ld_acquire_u32(sc.flag + p);
+        } while ((f & 0x7FFFFFFFu) != ep);
+        v = __ldcg(sc.agg + p);
+      }
+      const uint32_t heads = __ballot_sync(0xFFFFFFFFu, (f >> 31) != 0);
+      const int stop = heads ? __ffs(heads) - 1 : 31;   // nearest head in this window
+      // fixed-order sum of lanes 0..stop (nearest first), then into carry
+      double x = lane <= stop ? v : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xFFFFFFFFu, x, o);
+      carry += __shfl_sync(0xFFFFFFFFu, x, 0);
+      done = heads != 0;
+    }
+    if (lane == 0) s_carry = carry;
+  }
+  __syncthreads();
+  return s_carry;
 }
 
 __device__ __forceinline__ bool tc_head(uint32_t tag) { return tag != kNone && (tag & 0x80000000u); }
+
+// tile of this block: handed out in block start order
+__device__ __forceinline__ uint32_t tc_ticket(uint32_t* counter, uint32_t nb) {
+  __shared__ uint32_t s_b;
+  if (threadIdx.x == 0) s_b = atomicAdd(counter, 1u) % nb;   // nb tickets per update
+  __syncthreads();
+  return s_b;
+}
 
 __global__ void __launch_bounds__(kThreads) tc_node_kernel(Topo t, const __grid_constant__ Batch B) {
   __shared__ SegSum s_w[32];
   pdl_wait();
   pdl_launch();
   const CornerDev& c = B.c[blockIdx.y];
-  const uint32_t n = t.nCn, nb = tierC_blocks(n);
+  const uint32_t n = t.nCn, nb = tierC_blocks(n), nbe = tierC_blocks(2ull * n);
   double* Si = c.scratch;                                   // [nCn]
-  const TcScan sc = tc_scan(c.scratch + 4 * (size_t)n, nb);
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(c.scratch + 4 * (size_t)n + 8 * (size_t)tierC_blocks(2ull * n));
+  const TcScan sc{c.scratch + n, reinterpret_cast<uint32_t*>(c.scratch + n + nb + nbe)};
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(c.scratch + n + nb + nbe) + nb + nbe;
+  const uint32_t ep = __ldcg(c.epoch) & 0x7FFFFFFFu;
+  const uint32_t b = tc_ticket(cnt, nb);
   const float* Cw = c.rc_vals[1];
-  const uint32_t g0 = blockIdx.x * kTcTile + threadIdx.x * kTcPer;
+  const uint32_t g0 = b * kTcTile + threadIdx.x * kTcPer;
   double v[kTcPer];
   uint32_t hd = 0;
   bool bad = false;
@@ -617,20 +640,15 @@ __global__ void __launch_bounds__(kThreads) tc_node_kernel(Topo t, const __grid_
     v[j] = run.v;
   }
   SegSum tot;
-  const SegSum ex = seg_block_excl(run, s_w, &tot);
+  SegSum ex = seg_block_excl(run, s_w, &tot);
+  const double carry = tc_lookback(sc, b, tot, ep);
+  if (!ex.f) ex.v += carry;                  // no head before this thread in the tile
 #pragma unroll
   for (int j = 0; j < kTcPer; ++j) {
-    const uint32_t g = g0 + j;
     const bool before = (hd & ((2u << j) - 1u)) == 0;       // no head in this thread up to j
-    if (g < n) Si[g] = before ? ex.v + v[j] : v[j];
+    if (g0 + j < n) Si[g0 + j] = before ? ex.v + v[j] : v[j];
   }
-  // first head of the block
-  __shared__ uint32_t s_fh;
-  if (threadIdx.x == 0) s_fh = kTcTile;
-  __syncthreads();
-  if (hd) atomicMin(&s_fh, threadIdx.x * kTcPer + (uint32_t)(__ffs(hd) - 1));
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(c.err_flag, 1u);
-  tc_publish(sc, nb, tot, blockIdx.x * kTcTile + s_fh, cnt, s_w);
 }
 
 __global__ void __launch_bounds__(kThreads) tc_event_kernel(Topo t, const __grid_constant__ Batch B) {
@@ -640,18 +658,18 @@ __global__ void __launch_bounds__(kThreads) tc_event_kernel(Topo t, const __grid
   const CornerDev& c = B.c[blockIdx.y];
   const uint32_t n = t.nCn, m = 2 * n, nbn = tierC_blocks(n), nb = tierC_blocks(m);
   const double* Si = c.scratch;
-  double* H = c.scratch + n;                                // [2 nCn]
-  const TcScan scn = tc_scan(c.scratch + 4 * (size_t)n, nbn);
-  const TcScan sc = tc_scan(c.scratch + 4 * (size_t)n + 4 * (size_t)nb, nb);
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(c.scratch + 4 * (size_t)n + 8 * (size_t)nb) + 1;
+  const TcScan sc{c.scratch + n + nbn, reinterpret_cast<uint32_t*>(c.scratch + n + nbn + nb) + nbn};
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(c.scratch + n + nbn + nb) + nbn + nb + 1;
+  const uint32_t ep = __ldcg(c.epoch) & 0x7FFFFFFFu;
+  const uint32_t b = tc_ticket(cnt, nb);
   const float* R = c.rc_vals[0];
   const float* Cw = c.rc_vals[1];
-  const uint32_t e0 = blockIdx.x * kTcTile + threadIdx.x * kTcPer;
+  const uint32_t e0 = b * kTcTile + threadIdx.x * kTcPer;
   double v[kTcPer];
   uint32_t hd = 0;
   bool bad = false;
   // all loads of the thread's events first (no store in between: the loads of
-  // the 8 events overlap instead of paying one dependent chain each)
+  // the events overlap instead of paying one dependent chain each)
   uint32_t ev[kTcPer];
   uint4 nd[kTcPer];
 #pragma unroll
@@ -664,8 +682,8 @@ __global__ void __launch_bounds__(kThreads) tc_event_kernel(Topo t, const __grid
   for (int j = 0; j < kTcPer; ++j) {
     cw[j] = Cw[nd[j].x];
     rr[j] = R[nd[j].x];
-    s_end[j] = tc_read(Si, scn, nd[j].z - 1);
-    s_g[j] = tc_read(Si, scn, ev[j] & 0x7FFFFFFFu);
+    s_end[j] = __ldcg(Si + nd[j].z - 1);
+    s_g[j] = __ldcg(Si + (ev[j] & 0x7FFFFFFFu));
   }
   uint32_t ld_drv[kTcPer];
   float ld_val[kTcPer];
@@ -692,9 +710,6 @@ __global__ void __launch_bounds__(kThreads) tc_event_kernel(Topo t, const __grid
       v[j] = exit ? -w : w;
     }
   }
-#pragma unroll
-  for (int j = 0; j < kTcPer; ++j)
-    if (ld_drv[j] != kNone) c.load[ld_drv[j]] = ld_val[j];
   SegSum run{0.0, 0u};
 #pragma unroll
   for (int j = 0; j < kTcPer; ++j) {
@@ -702,35 +717,19 @@ __global__ void __launch_bounds__(kThreads) tc_event_kernel(Topo t, const __grid
     v[j] = run.v;
   }
   SegSum tot;
-  const SegSum ex = seg_block_excl(run, s_w, &tot);
+  SegSum ex = seg_block_excl(run, s_w, &tot);
+  const double carry = tc_lookback(sc, b, tot, ep);
+  if (!ex.f) ex.v += carry;
 #pragma unroll
   for (int j = 0; j < kTcPer; ++j) {
-    const uint32_t e = e0 + j;
+    if (ld_drv[j] != kNone) c.load[ld_drv[j]] = ld_val[j];
+    // elm(g) = H at enter(g) (exit events and Steiner / root nodes write nothing)
     const bool before = (hd & ((2u << j) - 1u)) == 0;
-    if (e < m) H[e] = before ? ex.v + v[j] : v[j];
+    const uint32_t tag = nd[j].y;
+    if (e0 + j < m && !(ev[j] >> 31) && tag != kNone && !(tag & 0x80000000u))
+      c.elm[tag] = (float)(before ? ex.v + v[j] : v[j]);
   }
-  __shared__ uint32_t s_fh;
-  if (threadIdx.x == 0) s_fh = kTcTile;
-  __syncthreads();
-  if (hd) atomicMin(&s_fh, threadIdx.x * kTcPer + (uint32_t)(__ffs(hd) - 1));
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(c.err_flag, 1u);
-  tc_publish(sc, nb, tot, blockIdx.x * kTcTile + s_fh, cnt, s_w);
-}
-
-__global__ void __launch_bounds__(kThreads) tc_elm_kernel(Topo t, const __grid_constant__ Batch B) {
-  pdl_wait();
-  pdl_launch();
-  const CornerDev& c = B.c[blockIdx.y];
-  const uint32_t n = t.nCn, m = 2 * n, nb = tierC_blocks(m);
-  const double* H = c.scratch + n;
-  const TcScan sc = tc_scan(c.scratch + 4 * (size_t)n + 4 * (size_t)nb, nb);
-  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= m) return;
-  const uint32_t ev = __ldg(t.tc_ev + e);
-  if (ev >> 31) return;                                     // exit event
-  const uint32_t tag = __ldg(&t.tc_node[ev].y);
-  if (tag == kNone || (tag & 0x80000000u)) return;          // Steiner node or root
-  c.elm[tag] = (float)tc_read(H, sc, e);
 }
 
 // ------------------------------------------- a2-a5: propagation work units
@@ -854,9 +853,19 @@ __device__ __forceinline__ FwdRc fwd_rc(const CornerDev& c, const uint4& tr) {
 
 // forward unit u; tr = this lane's term slot of the unit, rc its RC results
 // (loaded by the caller, software-pipelined one unit ahead)
+// the record word a term lane reads: (el, irf) of its source
+__device__ __forceinline__ const uint4* fwd_word(const CornerDev& c, const uint4& tr) {
+  const uint32_t q = threadIdx.x & 3;
+  const int el = (int)(q >> 1), orf = (int)(q & 1);
+  return c.rec + 4 * (size_t)tr.x + (el * 2 + primary_irf(tr.z & 7u, orf));
+}
+
+// pre: this lane's record word loaded speculatively one unit early (valid
+// if its tags match the epoch, else it is polled again)
 template <bool TRACE>
 __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, const float* __restrict__ L,
-                                         uint32_t ep, uint32_t u, const uint4& tr, FwdRc rc) {
+                                         uint32_t ep, uint32_t u, const uint4& tr, FwdRc rc,
+                                         uint4 pre = make_uint4(0, 0, 0, 0)) {
   const uint32_t lane = threadIdx.x & 31, tl = lane >> 2, q = lane & 3;
   const int el = (int)(q >> 1), orf = (int)(q & 1);
   const float undef = el ? -CUDART_INF_F : CUDART_INF_F;
@@ -891,7 +900,12 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
     float ca = undef, cs = undef;
     if (item) {
       const FwdTabs f = fwd_tabs(L, info, orf, ld);   // before waiting for the producer
+#if STA_FWD_RECPF
+      uint4 w = pre;
+      if (!ll_ok(w, ep)) w = spin_ll(wp, ep);
+#else
       const uint4 w = spin_ll(wp, ep);
+#endif
       if (TRACE) t_data = gtimer();
       float a_in = __uint_as_float(w.x), s_in = __uint_as_float(w.z);
       if (tr.y != kNone) hop_q(a_in, s_in, elm);
@@ -984,10 +998,22 @@ __global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) fwd_persistent_ker
   uint4 tr = u < t.n_fwu ? __ldg(t.fterm + (size_t)kFwdTerms * u + tl) : pad;
   uint4 nx = u + Wc < t.n_fwu ? __ldg(t.fterm + (size_t)kFwdTerms * (u + Wc) + tl) : pad;
   FwdRc rc = fwd_rc(c, tr);
+#if STA_FWD_RECPF
+  // the record words of the next unit, loaded speculatively one unit early:
+  // in the wide stages the producers are long done and the unit starts with
+  // its data in registers; in the narrow ones the word is stale and re-polled
+  uint4 rec = make_uint4(0, 0, 0, 0);
+#endif
   for (; u < t.n_fwu; u += Wc) {
     const uint4 nnx = u + 2 * Wc < t.n_fwu ? __ldg(t.fterm + (size_t)kFwdTerms * (u + 2 * Wc) + tl) : pad;
     const FwdRc nrc = fwd_rc(c, nx);         // nx arrived during the previous unit
+#if STA_FWD_RECPF
+    const uint4 nrec = nx.x < kHeavyMark ? ld_ll(fwd_word(c, nx)) : make_uint4(0, 0, 0, 0);
+    fwd_unit<TRACE>(t, c, L, ep, u, tr, rc, rec);
+    rec = nrec;
+#else
     fwd_unit<TRACE>(t, c, L, ep, u, tr, rc);
+#endif
     tr = nx;
     nx = nnx;
     rc = nrc;
@@ -1610,7 +1636,6 @@ cudaError_t launch_rc_tierC(const Topo& t, const Batch& b, cudaStream_t s) {
   const uint32_t K = b.K;
   cudaError_t e = pdl_launch_kernel(tc_node_kernel, dim3(tierC_blocks(t.nCn), K), kThreads, s, t, b);
   if (e == cudaSuccess) e = pdl_launch_kernel(tc_event_kernel, dim3(tierC_blocks(2ull * t.nCn), K), kThreads, s, t, b);
-  if (e == cudaSuccess) e = pdl_launch_kernel(tc_elm_kernel, dim3(blocks(2ull * t.nCn), K), kThreads, s, t, b);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
