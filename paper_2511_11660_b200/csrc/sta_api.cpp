@@ -1088,7 +1088,7 @@ void size_kernels(sta_ctx c) {
   u32 mx = 0;
   for (const sta::Batch& b : make_batches(c)) mx = std::max(mx, b.smem_f4);
   c->smem_f4 = mx;
-  if (16ull * mx > 48 * 1024) ck(sta::set_lut_smem_limit(16ull * mx), "smem attribute");
+  if (16ull * mx + sta::kBwdExtraSmem > 48 * 1024) ck(sta::set_lut_smem_limit(16ull * mx), "smem attribute");
   c->pgrid = c->use_persistent ? sta::persistent_grid(mx, 0) : 0;
   c->pgrid_b = c->use_persistent ? sta::persistent_grid(mx, 1) : 0;
   if (!c->wgrid) c->wgrid = sta::rc_warp_grid();

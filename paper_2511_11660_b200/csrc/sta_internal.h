@@ -62,9 +62,12 @@ constexpr int kBwdMinBlocks = STA_BWD_MINB;
 #define STA_MERGE_BOUND 0                       // 1: merge rounds bounded by the longest run in the warp (measured slower)
 #endif
 #ifndef STA_BWD_PIPE
-#define STA_BWD_PIPE 1                          // backward: prefetch the next unit's fan-out records
+#define STA_BWD_PIPE 2                          // backward: next unit's fan-out records: 1 registers, 2 TMA
 #endif
 constexpr uint32_t kMaxBatch = 8;               // corners traversed by one launch
+// backward persistent kernel: per-warp TMA staging buffer of the next unit's
+// fan-out records (1 KB) and its mbarrier, after the LUT image
+constexpr size_t kBwdExtraSmem = STA_BWD_PIPE == 2 ? (size_t)(kBwdThreads / 32) * (1024 + 8) : 0;
 
 // Device NLDM table pool (built by sta_set_library), shared-memory friendly:
 //   * table t: a block of kTabStride = 65 floats at t * 65: word 0 = offset
@@ -234,7 +237,10 @@ cudaError_t launch_rc_tierC(const Topo& t, const Batch& b, cudaStream_t s);
 // tier-C scratch: Si [nCn] (double), block aggregates of the node and the
 // event scans [nbn + nbe] (double), their flags [nbn + nbe] (u32 {has head,
 // epoch}) and the two tile tickets (u32, zero-initialised, monotonic)
-constexpr uint32_t kTcTile = 2048;              // elements per tier-C block (256 threads x 8)
+#ifndef STA_TC_TILE
+#define STA_TC_TILE 2048
+#endif
+constexpr uint32_t kTcTile = STA_TC_TILE;       // elements per tier-C block (256 threads x 8)
 __host__ __device__ inline uint32_t tierC_blocks(uint64_t n) { return (uint32_t)((n + kTcTile - 1) / kTcTile); }
 __host__ __device__ inline size_t tierC_scratch(uint32_t nCn) {
   const size_t nb = (size_t)tierC_blocks(nCn) + tierC_blocks(2ull * nCn);
@@ -251,6 +257,7 @@ uint32_t persistent_grid(uint32_t smem_f4, int which);
 cudaError_t launch_fwd_persistent(const Topo& t, const Batch& b, uint32_t grid, cudaStream_t s);
 cudaError_t launch_bwd_persistent(const Topo& t, const Batch& b, uint32_t grid, cudaStream_t s);
 constexpr size_t kLutSmemMax = 200 * 1024;   // larger batch images stay in global memory
+                                             // (+ kBwdExtraSmem stays under the 227 KB per block)
 cudaError_t launch_reduce(const Topo& t, const Batch& b, cudaStream_t s);
 cudaError_t launch_gather_pins(const Topo& t, const CornerDev& c, int what, float4* dst, cudaStream_t s);
 cudaError_t launch_gather_rc(const Topo& t, const CornerDev& c, float* net_load, float* pin_elm, cudaStream_t s);

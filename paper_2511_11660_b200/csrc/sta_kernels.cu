@@ -112,23 +112,59 @@ __device__ __forceinline__ int primary_irf(uint32_t sense, int orf) {
   return (int)((0x306u >> (2 * sense + (uint32_t)orf)) & 1u);
 }
 
+// ---- TMA bulk copies (cp.async.bulk, 1-D: no tensor map) with an mbarrier
+// carrying the transaction count; sizes and addresses are multiples of 16 B.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
 // Copy the table pools of the batch's corners into shared memory, each at its
-// lut_off4 (static data: may run before griddepcontrol.wait); `only` < K
-// stages one corner.  Each corner copies its OWN pool size (pools of
-// different corners may differ).  SMEM is a compile-time choice so that
-// lookups compile to LDS (a pointer that may be shared or global compiles to
-// slow generic loads).
+// lut_off4, with TMA bulk copies (static data: may run before
+// griddepcontrol.wait); `only` < K stages one corner.  Each corner copies its
+// OWN pool size (pools of different corners may differ).  SMEM is a
+// compile-time choice so that lookups compile to LDS (a pointer that may be
+// shared or global compiles to slow generic loads).
 extern __shared__ float4 s_dyn[];
+constexpr uint32_t kBulkMax = 1u << 16;       // bytes per bulk copy instruction
 template <bool SMEM>
 __device__ __forceinline__ void stage_luts(const Batch& b, uint32_t only) {
   if constexpr (SMEM) {                      // else pools too large: global / L1
-    for (uint32_t k = 0; k < b.K; ++k) {
-      if (only < b.K && k != only) continue;
-      const CornerDev& c = b.c[k];
-      const float4* g = reinterpret_cast<const float4*>(c.lut);
-      for (uint32_t x = threadIdx.x; x < c.lut_n4; x += blockDim.x) s_dyn[c.lut_off4 + x] = __ldg(g + x);
+    __shared__ uint64_t s_bar;
+    if (threadIdx.x == 0) {
+      mbar_init(&s_bar, 1);
+      uint32_t bytes = 0;
+      for (uint32_t k = 0; k < b.K; ++k)
+        if (!(only < b.K && k != only)) bytes += 16u * b.c[k].lut_n4;
+      mbar_expect_tx(&s_bar, bytes);
+      for (uint32_t k = 0; k < b.K; ++k) {
+        if (only < b.K && k != only) continue;
+        const CornerDev& c = b.c[k];
+        const char* g = reinterpret_cast<const char*>(c.lut);
+        char* d = reinterpret_cast<char*>(s_dyn + c.lut_off4);
+        for (uint32_t o = 0; o < 16u * c.lut_n4; o += kBulkMax)
+          bulk_g2s(d + o, g + o, min(kBulkMax, 16u * c.lut_n4 - o), &s_bar);
+      }
     }
-    __syncthreads();
+    __syncthreads();                         // the barrier is initialised
+    mbar_wait(&s_bar, 0);
   }
 }
 // the pool lookups of corner c should use
@@ -537,6 +573,9 @@ __device__ __forceinline__ SegSum seg_block_excl(SegSum x, SegSum* s_w, SegSum* 
 
 constexpr int kTcPer = (int)(kTcTile / kThreads);   // consecutive elements per thread
 
+#ifndef STA_TC_RELAXED
+#define STA_TC_RELAXED 0
+#endif
 // per-scan block records in the scratch: aggregate[nb] (double), flag[nb] (u32
 // {has head, epoch}: bit 31 = has head, bits 0..30 = epoch)
 struct TcScan {
@@ -572,9 +611,17 @@ __device__ double tc_lookback(const TcScan& sc, uint32_t b, SegSum tot, uint32_t
       uint32_t f = 0x80000000u;                    // past block 0: a virtual head
       double v = 0.0;
       if (p >= 0) {
+#if STA_TC_RELAXED
+        // relaxed polling (no L1 invalidation per poll); the aggregate is read
+        // from L2 after the flag returned (control dependency), like the records
+        do {
+          asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(sc.flag + p) : "memory");
+        } while ((f & 0x7FFFFFFFu) != ep);
+#else
         do {
           f = ld_acquire_u32(sc.flag + p);
         } while ((f & 0x7FFFFFFFu) != ep);
+#endif
         v = __ldcg(sc.agg + p);
       }
       const uint32_t heads = __ballot_sync(0xFFFFFFFFu, (f >> 31) != 0);
@@ -602,7 +649,10 @@ __device__ __forceinline__ uint32_t tc_ticket(uint32_t* counter, uint32_t nb) {
   return s_b;
 }
 
-__global__ void __launch_bounds__(kThreads) tc_node_kernel(Topo t, const __grid_constant__ Batch B) {
+#ifndef STA_TC_MINB
+#define STA_TC_MINB 1
+#endif
+__global__ void __launch_bounds__(kThreads, STA_TC_MINB) tc_node_kernel(Topo t, const __grid_constant__ Batch B) {
   __shared__ SegSum s_w[32];
   pdl_wait();
   pdl_launch();
@@ -651,7 +701,7 @@ __global__ void __launch_bounds__(kThreads) tc_node_kernel(Topo t, const __grid_
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(c.err_flag, 1u);
 }
 
-__global__ void __launch_bounds__(kThreads) tc_event_kernel(Topo t, const __grid_constant__ Batch B) {
+__global__ void __launch_bounds__(kThreads, STA_TC_MINB) tc_event_kernel(Topo t, const __grid_constant__ Batch B) {
   __shared__ SegSum s_w[32];
   pdl_wait();
   pdl_launch();
@@ -1374,6 +1424,76 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_ker
   }
   (void)fo;
   (void)nx;
+#elif STA_BWD_PIPE == 2
+  // The sinks' fan-out records of the warp's next unit are streamed into a
+  // per-warp shared-memory buffer by a TMA bulk copy (one 32 B record per
+  // sink, the unit's sinks are contiguous: <= 1 KB), issued when the current
+  // unit starts; the unit reads its own records from shared memory.  No
+  // register holds a prefetched record across the unit body.
+  const uint32_t wib = threadIdx.x >> 5;
+  uint4* fbuf = reinterpret_cast<uint4*>(s_dyn + B.smem_f4) + wib * 64;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_dyn + B.smem_f4 + (kBwdThreads / 32) * 64) + wib;
+  if (lane == 0) mbar_init(bar, 1);
+  __syncwarp();
+  uint32_t phase = 0;
+  auto issue = [&](const uint4& un) {
+    if (lane == 0) {
+      const uint32_t n = (un.w != 1 && un.y > un.x) ? (un.y - un.x) * 32u : 0u;
+      mbar_expect_tx(bar, n);
+      if (n) bulk_g2s(fbuf, t.sinkfo + 2 * (size_t)un.x, n, bar);
+    }
+  };
+  auto take = [&](const uint4& un) {       // this unit's records, then the buffer is free
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    SinkFo f{make_uint4(kNone, 0, 0, kNone), make_uint4(kNone, 0, kNone, 0)};
+    if (un.w != 1 && un.x + lane < un.y) {
+      f.a = fbuf[2 * lane];
+      f.b = fbuf[2 * lane + 1];
+    }
+    __syncwarp();
+    return f;
+  };
+  (void)fo;
+  bool dyn = u >= ns;
+  if (!dyn) issue(ud);
+  if (dyn) {                                 // no static unit: first ticket
+    uint32_t x = 0;
+    if (lane == 0) x = atomicAdd(c.red_cnt + 1, 1u);
+    u = ns + __shfl_sync(kFull, x, 0);
+    ud = u < t.n_bwu ? __ldg(t.bwu + u) : none;
+  }
+  while (u < t.n_bwu) {
+    uint4 nnx = none;
+    uint32_t un = 0;
+    SinkFo cf;
+    if (dyn) {
+      uint32_t xn = 0;
+      if (lane == 0) xn = atomicAdd(c.red_cnt + 1, 1u);
+      un = ns + __shfl_sync(kFull, xn, 0);
+      nx = un < t.n_bwu ? __ldg(t.bwu + un) : none;
+      cf = bwd_fo(t, ud);
+    } else {
+      cf = take(ud);
+      issue(nx);                             // the next unit's records stream in meanwhile
+      if (u + 2 * W < ns) nnx = __ldg(t.bwu + u + 2 * W);
+    }
+    bwd_unit<TRACE>(t, c, L, ep, u, ud, cf);
+    if (dyn) {
+      u = un;
+      ud = nx;
+    } else if (u + W < ns) {
+      u += W;
+      ud = nx;
+      nx = nnx;
+    } else {                                 // static part done: first ticket
+      dyn = true;
+      uint32_t x = 0;
+      if (lane == 0) x = atomicAdd(c.red_cnt + 1, 1u);
+      u = ns + __shfl_sync(kFull, x, 0);
+      ud = u < t.n_bwu ? __ldg(t.bwu + u) : none;
+    }
+  }
 #else
   // one call site of bwd_unit (a second inlined copy of the large unit body
   // measured 40% slower: instruction-cache pressure)
@@ -1691,9 +1811,11 @@ uint32_t persistent_grid(uint32_t smem_f4, int which) {
         &nt, smem_f4 ? fwd_persistent_kernel<true, true> : fwd_persistent_kernel<false, true>, kFwdThreads, smem);
   } else {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &nb, smem_f4 ? bwd_persistent_kernel<true, false> : bwd_persistent_kernel<false, false>, kBwdThreads, smem);
+        &nb, smem_f4 ? bwd_persistent_kernel<true, false> : bwd_persistent_kernel<false, false>, kBwdThreads,
+        smem + kBwdExtraSmem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &nt, smem_f4 ? bwd_persistent_kernel<true, true> : bwd_persistent_kernel<false, true>, kBwdThreads, smem);
+        &nt, smem_f4 ? bwd_persistent_kernel<true, true> : bwd_persistent_kernel<false, true>, kBwdThreads,
+        smem + kBwdExtraSmem);
   }
   cudaGetLastError();
   return (uint32_t)(std::min(nb, nt) * sms);
@@ -1730,12 +1852,12 @@ cudaError_t launch_fwd_persistent(const Topo& t, const Batch& b, uint32_t grid, 
 
 cudaError_t launch_bwd_persistent(const Topo& t, const Batch& b, uint32_t grid, cudaStream_t s) {
   if (!t.n_bwu) return cudaSuccess;
-  const size_t sm = 16ull * b.smem_f4;
+  const size_t sm = 16ull * b.smem_f4 + kBwdExtraSmem;
   if (traced(b))
     return b.smem_f4 ? coop_launch(bwd_persistent_kernel<true, true>, grid, kBwdThreads, sm, s, t, b)
-                     : coop_launch(bwd_persistent_kernel<false, true>, grid, kBwdThreads, 0, s, t, b);
+                     : coop_launch(bwd_persistent_kernel<false, true>, grid, kBwdThreads, kBwdExtraSmem, s, t, b);
   return b.smem_f4 ? coop_launch(bwd_persistent_kernel<true, false>, grid, kBwdThreads, sm, s, t, b)
-                   : coop_launch(bwd_persistent_kernel<false, false>, grid, kBwdThreads, 0, s, t, b);
+                   : coop_launch(bwd_persistent_kernel<false, false>, grid, kBwdThreads, kBwdExtraSmem, s, t, b);
 }
 
 cudaError_t set_lut_smem_limit(size_t bytes) {
@@ -1747,7 +1869,7 @@ cudaError_t set_lut_smem_limit(size_t bytes) {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, b);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(tr ? bwd_persistent_kernel<true, true> : bwd_persistent_kernel<true, false>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, b + (int)kBwdExtraSmem);
   }
   return e;
 }
