@@ -64,6 +64,9 @@ def lib():
         _lib.orc_rc.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         _lib.orc_update.restype = C.c_int
         _lib.orc_update.argtypes = [C.c_void_p] * 5 + [C.c_void_p] * 4
+        _lib.orc_paths.restype = C.c_int
+        _lib.orc_paths.argtypes = [C.c_void_p, C.c_int, C.c_uint32, C.c_uint32, C.c_double, C.c_uint32,
+                                   C.c_uint32] + [C.c_void_p] * 8
     return _lib
 
 
@@ -192,3 +195,39 @@ def update_all_corners(d):
     r = np.array([p["res"] for p in per])
     glob = np.array([r[:, 0].min(), r[:, 1].sum(), r[:, 2].min(), r[:, 3].sum()])
     return per, glob
+
+
+def paths(d, corner: int = 0, mode: str = "setup", k: int = 10, nworst: int = 1,
+          slack_lt: float = float("inf")):
+    """O10 top-k path report -> list of dicts {slack, ep, pins, rfs, at}
+    in report order (slack, endpoint id, backward (pin, rf) sequence)."""
+    m = _Marshal(d, corner)
+    P = d.num_pins
+    cap_paths = int(k)
+    cap_pins = int(k) * (P + 1)
+    while True:
+        ptr = np.zeros(cap_paths + 1, np.uint32)
+        pin = np.zeros(max(cap_pins, 1), np.uint32)
+        rf = np.zeros(max(cap_pins, 1), np.uint8)
+        at = np.zeros(max(cap_pins, 1), np.float64)
+        sl = np.zeros(max(cap_paths, 1), np.float64)
+        ep = np.zeros(max(cap_paths, 1), np.uint32)
+        n = np.zeros(1, np.uint32)
+        npin = np.zeros(1, np.uint32)
+        st = lib().orc_paths(m.ptr, 0 if mode == "setup" else 1, int(k), int(nworst), float(slack_lt),
+                             cap_paths, cap_pins, n.ctypes.data, npin.ctypes.data, _p(ptr), _p(pin),
+                             _p(rf), _p(at), _p(sl), _p(ep))
+        if st == 3:
+            cap_pins *= 2
+            continue
+        if st == 1:
+            raise ValueError("combinational cycle")
+        if st:
+            raise MemoryError("oracle allocation failed")
+        break
+    out = []
+    for i in range(int(n[0])):
+        a, b = int(ptr[i]), int(ptr[i + 1])
+        out.append(dict(slack=float(sl[i]), ep=int(ep[i]), pins=pin[a:b].tolist(), rfs=rf[a:b].tolist(),
+                        at=at[a:b].tolist()))
+    return out

@@ -223,9 +223,59 @@ static int sense_allows(uint8_t sense, int irf, int orf) {
   return 0;
 }
 
+/* ----------------------------------------------- O10: top-k path report */
+/* Request of a path report (run_update's hook: it runs after the backward
+ * pass, on the final arrivals, the recorded arc delays and the endpoint
+ * seeds). */
+typedef struct {
+  int mode;                 /* 0 setup (late), 1 hold (early) */
+  uint32_t k, nworst;
+  double slack_lt;
+  /* outputs (capacities in brackets) */
+  uint32_t cap_paths, cap_pins;
+  uint32_t n_paths, n_pins;
+  uint32_t* path_ptr;       /* [cap_paths + 1] */
+  uint32_t* path_pin;       /* [cap_pins] startpoint first */
+  uint8_t* path_rf;         /* [cap_pins] */
+  double* path_at;          /* [cap_pins] arrival of the path at each of its pins */
+  double* path_slack;       /* [cap_paths] */
+  uint32_t* path_ep;        /* [cap_paths] */
+} orc_path_req;
+
+static int path_report(const orc_design* d, const arcs_t* g, const uint32_t* order, const double* at,
+                       const double* elm, const double* dly, const double* seed, orc_path_req* q);
+
 /* --------------------------------------------------------- O4-O8: update */
+static int run_update(const orc_design* d, double* at, double* slew, double* rat, double* slack,
+                      double res[4], uint32_t* ep_pin, double* ep_ws, uint32_t* n_ep_out, orc_path_req* pq);
+
 int orc_update(const orc_design* d, double* at, double* slew, double* rat, double* slack,
                double res[4], uint32_t* ep_pin, double* ep_ws, uint32_t* n_ep_out) {
+  return run_update(d, at, slew, rat, slack, res, ep_pin, ep_ws, n_ep_out, NULL);
+}
+
+int orc_paths(const orc_design* d, int mode, uint32_t k, uint32_t nworst, double slack_lt, uint32_t cap_paths,
+              uint32_t cap_pins, uint32_t* n_paths, uint32_t* n_pins, uint32_t* path_ptr, uint32_t* path_pin,
+              uint8_t* path_rf, double* path_at, double* path_slack, uint32_t* path_ep) {
+  orc_path_req q;
+  memset(&q, 0, sizeof q);
+  q.mode = mode; q.k = k; q.nworst = nworst; q.slack_lt = slack_lt;
+  q.cap_paths = cap_paths; q.cap_pins = cap_pins;
+  q.path_ptr = path_ptr; q.path_pin = path_pin; q.path_rf = path_rf; q.path_at = path_at;
+  q.path_slack = path_slack; q.path_ep = path_ep;
+  double res[4];
+  uint32_t P = d->num_pins;
+  double* at = malloc(sizeof(double) * 4 * (size_t)(P + 1));
+  if (!at) return 2;
+  int st = run_update(d, at, NULL, NULL, NULL, res, NULL, NULL, NULL, &q);
+  free(at);
+  *n_paths = q.n_paths;
+  *n_pins = q.n_pins;
+  return st;
+}
+
+static int run_update(const orc_design* d, double* at, double* slew, double* rat, double* slack,
+                      double res[4], uint32_t* ep_pin, double* ep_ws, uint32_t* n_ep_out, orc_path_req* pq) {
   const uint32_t P = d->num_pins;
   const double LN9 = log(9.0);
   arcs_t g; memset(&g, 0, sizeof g);
@@ -343,6 +393,16 @@ int orc_update(const orc_design* d, double* at, double* slew, double* rat, doubl
       }
     }
   }
+  if (pq) {   /* O10 needs each endpoint's own seed (its check), before the backward */
+    double* seed = malloc(sizeof(double) * 4 * (size_t)(P + 1));
+    if (!seed) { st = 2; goto done; }
+    memcpy(seed, rat, sizeof(double) * 4 * (size_t)P);
+    for (uint32_t p = 0; p < P; p++)
+      if (!is_ep[p]) for (int q = 0; q < 4; q++) seed[4 * p + q] = q < 2 ? -INF : INF;
+    st = path_report(d, &g, order, at, elm, dly, seed, pq);
+    free(seed);
+    goto done;
+  }
   for (uint32_t k = P; k-- > 0;) {
     uint32_t u = order[k];
     for (uint32_t x = g.fo_ptr[u]; x < g.fo_ptr[u + 1]; x++) {
@@ -400,5 +460,168 @@ done:
   free_arcs(&g);
   free(level); free(order); free(load); free(elm); free(drv_load); free(dly);
   free(own_slew); free(own_rat); free(own_slack); free(is_ep);
+  return st;
+}
+
+/* ----------------------------------------------- O10: top-k path report */
+/* SURVEY.md §8(f) row 3; PAPER.md:187-190 ("top-k path reports ... controlled
+ * with top-k, per-endpoint report limit, and slack-less-than thresholds ...
+ * flattened CSR-based path pin arrays with slacks").
+ * Readings (P1-P4): a path is a sequence of (pin, transition)
+ * nodes from a startpoint with a defined arrival to an endpoint with a
+ * defined seed, along enabled arcs with the transition pairs their sense
+ * allows; its arrival is the startpoint's arrival plus the delays the update
+ * used on its arcs (graph-based: recorded cell delays, Elmore net delays);
+ * setup slack = seed_L - arrival_L, hold slack = arrival_E - seed_E, the
+ * seed being the endpoint's own required time (its check / output delay).
+ * Report order: slack, then endpoint pin id, then the node sequence read
+ * backwards from the endpoint ((pin, rf) lexicographic).  Selection walks
+ * that order keeping at most nworst paths per endpoint, slack < slack_lt,
+ * k paths in all.
+ * Plain dynamic program: the m = min(nworst, k) first partial paths into
+ * every (pin, rf) in that order, in topological order, each extending a
+ * partial path of a fan-in (u, irf) by the arc's delay -- a path among the m
+ * first into (v, rf) has its prefix among the m first into its predecessor,
+ * so the lists are exact.  Ties between equal arrivals at a node compare
+ * the predecessor (pin, rf) and then its rank there, which is the backward
+ * sequence order. */
+typedef struct {
+  double a;                 /* arrival of the partial path at this node */
+  uint32_t pin;             /* predecessor pin (ORC_NO_PIN at a startpoint) */
+  uint32_t rf;              /* predecessor transition */
+  uint32_t rank;            /* predecessor's rank in its list */
+} pent;
+
+static int g_late;          /* comparator mode (single-threaded oracle) */
+
+static int cmp_pent(const void* x, const void* y) {
+  const pent* a = (const pent*)x;
+  const pent* b = (const pent*)y;
+  if (a->a != b->a) return g_late ? (a->a > b->a ? -1 : 1) : (a->a < b->a ? -1 : 1);
+  if (a->pin != b->pin) return a->pin < b->pin ? -1 : 1;
+  if (a->rf != b->rf) return a->rf < b->rf ? -1 : 1;
+  return a->rank < b->rank ? -1 : (a->rank > b->rank ? 1 : 0);
+}
+
+typedef struct {
+  double slack;
+  uint32_t ep, rf, rank;
+} pcand;
+
+static int cmp_pcand(const void* x, const void* y) {
+  const pcand* a = (const pcand*)x;
+  const pcand* b = (const pcand*)y;
+  if (a->slack != b->slack) return a->slack < b->slack ? -1 : 1;
+  if (a->ep != b->ep) return a->ep < b->ep ? -1 : 1;
+  if (a->rf != b->rf) return a->rf < b->rf ? -1 : 1;
+  return a->rank < b->rank ? -1 : (a->rank > b->rank ? 1 : 0);
+}
+
+static int path_report(const orc_design* d, const arcs_t* g, const uint32_t* order, const double* at,
+                       const double* elm, const double* dly, const double* seed, orc_path_req* q) {
+  const uint32_t P = d->num_pins;
+  const int late = q->mode == 0, el = late ? 1 : 0;
+  const uint32_t m = q->nworst < q->k ? q->nworst : q->k;
+  q->n_paths = q->n_pins = 0;
+  if (m == 0) return 0;
+  pent* L = malloc(sizeof(pent) * 2 * (size_t)P * m + 1);
+  uint32_t* cnt = calloc(2 * (size_t)P + 1, sizeof(uint32_t));
+  uint32_t maxfi = 1;
+  for (uint32_t v = 0; v < P; v++) {
+    uint32_t f = g->fi_ptr[v + 1] - g->fi_ptr[v];
+    if (f > maxfi) maxfi = f;
+  }
+  pent* cand = malloc(sizeof(pent) * 2 * (size_t)maxfi * m + 1);
+  if (!L || !cnt || !cand) { free(L); free(cnt); free(cand); return 2; }
+  g_late = late;
+  /* the m first partial paths into every (pin, rf), in topological order */
+  for (uint32_t k = 0; k < P; k++) {
+    const uint32_t v = order[k];
+    for (int rf = 0; rf < 2; rf++) {
+      pent* lv = L + ((size_t)v * 2 + rf) * m;
+      uint32_t nc = 0;
+      if (g->fi_ptr[v + 1] == g->fi_ptr[v]) {            /* startpoint: its own arrival */
+        if (isfinite(at[4 * v + Q(el, rf)])) {
+          lv[0].a = at[4 * v + Q(el, rf)]; lv[0].pin = ORC_NO_PIN; lv[0].rf = 0; lv[0].rank = 0;
+          cnt[2 * v + rf] = 1;
+        }
+        continue;
+      }
+      for (uint32_t x = g->fi_ptr[v]; x < g->fi_ptr[v + 1]; x++) {
+        const uint32_t e = g->fi[x], u = g->from[e];
+        for (int irf = 0; irf < 2; irf++) {
+          double dd;
+          if (e < g->En) {                                 /* net arc: positive unate, Elmore */
+            if (irf != rf) continue;
+            dd = elm[v];
+          } else {
+            const uint32_t a = g->cell[e];
+            if (!sense_allows(d->arc_sense[a], irf, rf)) continue;
+            dd = dly[8 * (size_t)a + 4 * el + 2 * irf + rf];
+          }
+          const pent* lu = L + ((size_t)u * 2 + irf) * m;
+          for (uint32_t j = 0; j < cnt[2 * u + irf]; j++) {
+            cand[nc].a = lu[j].a + dd; cand[nc].pin = u; cand[nc].rf = (uint32_t)irf; cand[nc].rank = j;
+            nc++;
+          }
+        }
+      }
+      qsort(cand, nc, sizeof(pent), cmp_pent);
+      if (nc > m) nc = m;
+      memcpy(lv, cand, sizeof(pent) * nc);
+      cnt[2 * v + rf] = nc;
+    }
+  }
+  /* endpoint candidates, in report order */
+  size_t ncand = 0;
+  for (uint32_t p = 0; p < P; p++)
+    for (int rf = 0; rf < 2; rf++) ncand += cnt[2 * p + rf];
+  pcand* pc = malloc(sizeof(pcand) * (ncand + 1));
+  uint32_t* kept = calloc(P + 1, sizeof(uint32_t));
+  uint32_t* chain = malloc(sizeof(uint32_t) * 3 * (size_t)(P + 1));
+  if (!pc || !kept || !chain) { free(L); free(cnt); free(cand); free(pc); free(kept); free(chain); return 2; }
+  size_t n = 0;
+  for (uint32_t p = 0; p < P; p++) {
+    for (int rf = 0; rf < 2; rf++) {
+      const double sd = seed[4 * p + Q(el, rf)];
+      if (!isfinite(sd)) continue;                       /* not an endpoint, or no seed */
+      const pent* lp = L + ((size_t)p * 2 + rf) * m;
+      for (uint32_t j = 0; j < cnt[2 * p + rf]; j++) {
+        pc[n].slack = late ? sd - lp[j].a : lp[j].a - sd;
+        pc[n].ep = p; pc[n].rf = (uint32_t)rf; pc[n].rank = j;
+        n++;
+      }
+    }
+  }
+  qsort(pc, n, sizeof(pcand), cmp_pcand);
+  int st = 0;
+  for (size_t i = 0; i < n && q->n_paths < q->k; i++) {
+    if (!(pc[i].slack < q->slack_lt)) break;
+    if (kept[pc[i].ep] >= q->nworst) continue;
+    kept[pc[i].ep]++;
+    /* the node chain, endpoint first */
+    uint32_t len = 0, v = pc[i].ep, rf = pc[i].rf, r = pc[i].rank;
+    for (;;) {
+      chain[3 * len] = v; chain[3 * len + 1] = rf; chain[3 * len + 2] = r;
+      len++;
+      const pent* e = L + ((size_t)v * 2 + rf) * m + r;
+      if (e->pin == ORC_NO_PIN) break;
+      v = e->pin; rf = e->rf; r = e->rank;
+    }
+    if (q->n_paths + 1 > q->cap_paths || q->n_pins + len > q->cap_pins) { st = 3; break; }
+    q->path_ptr[q->n_paths] = q->n_pins;
+    for (uint32_t t = 0; t < len; t++) {                 /* startpoint first */
+      const uint32_t* c = chain + 3 * (len - 1 - t);
+      q->path_pin[q->n_pins + t] = c[0];
+      q->path_rf[q->n_pins + t] = (uint8_t)c[1];
+      q->path_at[q->n_pins + t] = L[((size_t)c[0] * 2 + c[1]) * m + c[2]].a;
+    }
+    q->n_pins += len;
+    q->path_slack[q->n_paths] = pc[i].slack;
+    q->path_ep[q->n_paths] = pc[i].ep;
+    q->n_paths++;
+    q->path_ptr[q->n_paths] = q->n_pins;
+  }
+  free(L); free(cnt); free(cand); free(pc); free(kept); free(chain);
   return st;
 }

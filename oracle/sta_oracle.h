@@ -91,6 +91,17 @@ void orc_rc(const orc_design* d, double* load, double* elm);
 int orc_update(const orc_design* d, double* at, double* slew, double* rat, double* slack,
                double res[4], uint32_t* ep_pin, double* ep_ws, uint32_t* n_ep);
 
+/* O10: top-k path report (the
+ * readings are in sta_oracle.c and DESIGN.md).  mode 0 setup, 1 hold; k >= 1
+ * paths in all, nworst >= 1 per endpoint, slack < slack_lt.  CSR output:
+ * path i = pins path_pin[path_ptr[i] .. path_ptr[i+1]) (startpoint first) with
+ * their transitions (0 rise, 1 fall) and the path's arrival at each;
+ * path_slack / path_ep per path, in report order.  Returns 0, 1 on a cycle,
+ * 2 on allocation failure, 3 when a capacity is too small. */
+int orc_paths(const orc_design* d, int mode, uint32_t k, uint32_t nworst, double slack_lt, uint32_t cap_paths,
+              uint32_t cap_pins, uint32_t* n_paths, uint32_t* n_pins, uint32_t* path_ptr, uint32_t* path_pin,
+              uint8_t* path_rf, double* path_at, double* path_slack, uint32_t* path_ep);
+
 #ifdef __cplusplus
 }
 #endif

@@ -234,3 +234,100 @@ def design_node_caps(d, corner=0):
     has = rc.node_pin != NO_PIN
     caps[has] += d.pin_cap[rc.node_pin[has]].astype(np.float64) + po_ld[rc.node_pin[has]]
     return caps
+
+
+def path_list_bruteforce(d, elm_of_pin, mode="setup"):
+    """Every timing path of a frozen-delay design by exhaustive DFS (SPEC.md
+    path-report acceptance: "report_paths(k=inf) returns exactly the set of
+    valid paths found by exhaustive DFS ... identical sort order"), as
+    (slack, endpoint, ((pin, rf), ...) startpoint first, arrivals), sorted in
+    report order: slack, endpoint id, then the (pin, rf) sequence read
+    backwards from the endpoint.  Startpoints: pins without fan-in carrying a
+    PI / ideal-clock arrival; endpoints: POs and checked D pins with a seed
+    for that transition (PO: T - out_max / -out_min; check: T - setup /
+    hold, defined where the data arrival of that edge is)."""
+    lib = d.libs[0]
+    cons = d.cons
+    T = float(cons.period)
+    late = mode == "setup"
+    arcs = _fanin_lists(d)
+    P = d.num_pins
+    succ = defaultdict(list)
+    indeg = np.zeros(P, int)
+    for (u, v, kind, sense, tab) in arcs:
+        if kind == "net":
+            dl = {(0, 0): elm_of_pin[v], (1, 1): elm_of_pin[v]}
+        else:
+            dl = {(i, o): max(0.0, const_value(lib, tab + o)) for (i, o) in _pairs(sense)}
+        succ[u].append((v, dl))
+        indeg[v] += 1
+    seed_at = {}
+    for k in range(cons.pi_pin.size):
+        p = int(cons.pi_pin[k])
+        if indeg[p] == 0:
+            seed_at[p] = [float(x) for x in cons.pi_at[k]]
+    for p in range(P):
+        if int(d.pin_role[p]) == ROLE_FF_CK and indeg[p] == 0:
+            seed_at[p] = [0.0, T / 2, 0.0, T / 2]
+    # arrivals (for the data-arrival condition of the check seeds)
+    reach = defaultdict(bool)
+
+    def mark(v, rf):
+        if reach[(v, rf)]:
+            return
+        reach[(v, rf)] = True
+        for (w, dl) in succ[v]:
+            for (i, o) in dl:
+                if i == rf:
+                    mark(w, o)
+    for s in seed_at:
+        for rf in (0, 1):
+            mark(s, rf)
+    seed = {}
+    for k in range(cons.po_pin.size):
+        p = int(cons.po_pin[k])
+        for rf in (0, 1):
+            x = T - float(cons.po_out_max[k, rf]) if late else -float(cons.po_out_min[k, rf])
+            old = seed.get((p, rf))
+            seed[(p, rf)] = x if old is None else (min(old, x) if late else max(old, x))
+    for c in range(d.num_checks):
+        p, tb = int(d.chk_d[c]), int(d.chk_tab[c])
+        for rf in (0, 1):
+            if reach[(p, rf)]:
+                x = T - const_value(lib, tb + rf) if late else const_value(lib, tb + 2 + rf)
+                old = seed.get((p, rf))
+                seed[(p, rf)] = x if old is None else (min(old, x) if late else max(old, x))
+    out = []
+
+    def walk(v, rf, acc, nodes, ats):
+        nodes.append((v, rf))
+        ats.append(acc)
+        if (v, rf) in seed:
+            sl = seed[(v, rf)] - acc if late else acc - seed[(v, rf)]
+            out.append((sl, v, tuple(nodes), tuple(ats)))
+        for (w, dl) in succ[v]:
+            for (i, o), x in dl.items():
+                if i == rf:
+                    walk(w, o, acc + x, nodes, ats)
+        nodes.pop()
+        ats.pop()
+
+    for s, a in seed_at.items():
+        for rf in (0, 1):
+            walk(s, rf, a[2 + rf] if late else a[rf], [], [])
+    out.sort(key=lambda t: (t[0], t[1], tuple(reversed(t[2]))))
+    return out
+
+
+def select_paths(paths, k, nworst, slack_lt=INF):
+    """Report selection over a sorted path list: slack < slack_lt, at most
+    nworst per endpoint, k in all."""
+    kept, cnt = [], defaultdict(int)
+    for p in paths:
+        if len(kept) >= k or not p[0] < slack_lt:
+            break
+        if cnt[p[1]] >= nworst:
+            continue
+        cnt[p[1]] += 1
+        kept.append(p)
+    return kept

@@ -333,3 +333,67 @@ def test_negative_table_values_clamp_to_zero():
     assert list(r["slew"][y]) == [0, 0, 0, 0]
     assert list(r["rat"][D, 2:]) == [14, 14]        # T - (-4)
     assert list(r["rat"][D, :2]) == [-6, -6]        # hold value, negative allowed
+
+
+# ------------------------------------------- O10: top-k path report (f3)
+from tests.brute import path_list_bruteforce, select_paths  # noqa: E402
+
+
+def _same_paths(got, exp):
+    assert len(got) == len(exp), (len(got), len(exp))
+    for g, e in zip(got, exp):
+        assert abs(g["slack"] - e[0]) <= 1e-9 * max(1.0, abs(e[0])), (g["slack"], e[0])
+        assert g["ep"] == e[1]
+        assert list(zip(g["pins"], g["rfs"])) == list(e[2]), (g, e)
+        assert np.allclose(g["at"], e[3], rtol=1e-12, atol=1e-9)
+
+
+@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("mode", ["setup", "hold"])
+def test_paths_vs_exhaustive_enumeration(seed, mode):
+    """SPEC.md path-report acceptance: with k = inf the report is exactly the
+    set of paths found by exhaustive DFS, same slacks, same order (frozen
+    delays: constant tables, all five senses, undefined sources)."""
+    d = _tiny(seed)
+    allp = path_list_bruteforce(d, _bf_elm(d), mode)
+    big = 10 ** 6
+    _same_paths(oracle.paths(d, mode=mode, k=big, nworst=big), allp)
+    # selections: k, nworst, slack-less-than
+    for k, nw in [(1, 1), (3, 1), (5, 2), (7, 100)]:
+        _same_paths(oracle.paths(d, mode=mode, k=k, nworst=nw), select_paths(allp, k, nw))
+    if allp:
+        thr = allp[len(allp) // 2][0]
+        _same_paths(oracle.paths(d, mode=mode, k=big, nworst=3, slack_lt=thr),
+                    select_paths(allp, big, 3, thr))
+
+
+def test_paths_golden_h3():
+    """Hand example H3 (tests/golden/h3_reg2reg.json): the worst setup path
+    is CK1 rise -> Q rise -> X/A rise -> X/Y fall -> D fall with slack 8 =
+    WNS_setup; the worst hold path starts at PI b with slack 15 = WNS_hold."""
+    d = synth.h3_reg2reg()
+    names = d.meta["pin_names"]
+    s = oracle.paths(d, mode="setup", k=1, nworst=1)[0]
+    assert s["slack"] == pytest.approx(8.0, abs=1e-9)
+    assert [names[p] for p in s["pins"]] == ["DFF1/CK", "DFF1/Q", "X/A", "X/Y", "DFF2/D"]
+    assert s["rfs"] == [0, 0, 0, 1, 1] and s["at"] == pytest.approx([0, 30, 31, 42, 43])
+    h = oracle.paths(d, mode="hold", k=1, nworst=1)[0]
+    assert h["slack"] == pytest.approx(15.0, abs=1e-9) and names[h["pins"][0]] == "b"
+
+
+@pytest.mark.parametrize("seed", [11, 12])
+def test_paths_worst_equals_wns(seed):
+    """SPEC path-report invariant: the first setup path's slack is WNS
+    (endpoints without fan-out), slacks are non-decreasing, nworst holds, and
+    each path's arrivals are its startpoint arrival plus the arc delays."""
+    d = synth.generate(300, 12, seed=seed, period=150.0)
+    r = oracle.update(d)
+    for mode, col in (("setup", 0), ("hold", 2)):
+        ps = oracle.paths(d, mode=mode, k=200, nworst=3)
+        assert ps[0]["slack"] == pytest.approx(r["res"][col], abs=1e-9)
+        sl = [p["slack"] for p in ps]
+        assert all(a <= b for a, b in zip(sl, sl[1:]))
+        from collections import Counter
+        assert max(Counter(p["ep"] for p in ps).values()) <= 3
+        for p in ps:
+            assert all(b >= a - 1e-12 for a, b in zip(p["at"], p["at"][1:]))   # delays >= 0
