@@ -254,6 +254,44 @@ STA_API sta_status sta_get_rc(sta_ctx ctx, uint32_t corner, float* net_load, flo
 STA_API sta_status sta_get_levels(sta_ctx ctx, uint32_t* level, uint32_t* perm, uint32_t* num_levels,
                           sta_mem mem);
 
+/* Top-k path report of `corner` after the last update (
+ * "top-k path reports ... controlled with top-k,
+ * per-endpoint report limit, and slack-less-than thresholds ... flattened
+ * CSR-based path pin arrays with slacks").  A path is a sequence of
+ * (pin, transition) from a startpoint with an arrival (PI, ideal clock pin)
+ * to an endpoint (PO, checked data pin) along enabled arcs; its arrival is
+ * the startpoint's plus the delays the update used on its arcs (graph-based);
+ * setup slack = the endpoint's own required time (check / output delay) -
+ * arrival (late), hold slack = arrival - required (early).  Paths are
+ * reported in the order (slack, endpoint pin id, the (pin, transition)
+ * sequence read backwards from the endpoint), keeping slack < slack_lt, at
+ * most nworst per endpoint, k in all (1 <= min(k, nworst) <= 255).
+ * The first setup path's slack is the worst endpoint slack.
+ * Output (in `mem` memory; capacities cap_paths >= k and cap_pins, e.g.
+ * k * (num_levels + 1)): path i has pins path_pin[path_ptr[i] ..
+ * path_ptr[i + 1]) startpoint first, their transitions path_rf (0 rise,
+ * 1 fall) and the path's arrival at each (path_at, ps); path_slack[i],
+ * path_ep[i] (endpoint pin).  If the pins do not fit, STA_ERR_ARG with
+ * n_paths / n_pins set to the sizes needed.  Synchronizes. */
+typedef struct {
+  uint32_t mode;        /* 0 setup (late), 1 hold (early) */
+  uint32_t k;           /* paths in all */
+  uint32_t nworst;      /* paths per endpoint */
+  float slack_lt;       /* report slack < slack_lt only (INFINITY: all) */
+} sta_path_query;
+typedef struct {
+  uint32_t cap_paths, cap_pins;  /* in */
+  uint32_t n_paths, n_pins;      /* out */
+  uint32_t* path_ptr;            /* [cap_paths + 1] */
+  uint32_t* path_pin;            /* [cap_pins] */
+  uint8_t* path_rf;              /* [cap_pins] */
+  float* path_at;                /* [cap_pins] */
+  float* path_slack;             /* [cap_paths] */
+  uint32_t* path_ep;             /* [cap_paths] */
+} sta_path_set;
+STA_API sta_status sta_report_paths(sta_ctx ctx, uint32_t corner, const sta_path_query* q, sta_path_set* out,
+                                    sta_mem mem);
+
 /* Counters describing the loaded graph and the last update. */
 typedef struct {
   uint32_t num_pins, num_nets, num_net_arcs, num_cell_arcs, num_checks, num_endpoints;

@@ -183,6 +183,9 @@ struct sta_ctx_s {
   std::vector<u32> sfo_p, pfo_p, sink_drv;      // host copies for prepare()
   std::vector<u32> sfo_dst, sfo_info, pfo_dst, pfo_info;
   std::vector<u32> fwu_stage_ptr;                // [S + 1] forward units of each stage
+  std::vector<u32> fi_p_h, fi_slot_h, ep_int_h;  // path report: term ranges, delay slots, endpoint ids
+  Arena path_arena;                              // path report: their device copies + user_of_int
+  const u32 *fi_p_d = nullptr, *fi_slot_d = nullptr, *ep_int_d = nullptr, *uoi_d = nullptr;
   std::vector<u32> bwu_stage_lo, bwu_stage_hi;   // [S] backward units of each stage (descending list)
 
   // ---- RC tree (host)
@@ -782,6 +785,8 @@ void build_plan(sta_ctx c) {
   sink_drv.assign(c->NS, 0);
   for (u32 i = 0; i < NP; ++i)
     for (u32 x = c->sink_ptr[i]; x < c->sink_ptr[i + 1]; ++x) sink_drv[x] = i;
+  c->fi_p_h = fi_p;                        // (the path report's per-pin term ranges / delay slots)
+  c->fi_slot_h = term_slot;
   c->sfo_p = sfo_p;
   c->pfo_p = pfo_p;
   c->sfo_dst = sfo_dst;
@@ -1108,6 +1113,10 @@ void prepare(sta_ctx c) {
 
   // endpoints in increasing user pin id
   std::vector<u32> pin_ep(c->Pi, kNone);
+  std::vector<u32>& ep_int = c->ep_int_h;
+  ep_int.clear();
+  c->path_arena.release();                 // the path report's device arrays are rebuilt lazily
+  c->fi_p_d = c->fi_slot_d = c->ep_int_d = c->uoi_d = nullptr;
   std::vector<sta::EpRec> ep;
   for (u32 p = 0; p < P; ++p) {
     if (po_idx[p] == kNone && c->chk_of_pin[p] == kNone) continue;
@@ -1115,6 +1124,7 @@ void prepare(sta_ctx c) {
     r.po = po_idx[p];
     r.chk_tab = c->chk_of_pin[p] == kNone ? kNone : c->chk_tab[c->chk_of_pin[p]];
     pin_ep[c->int_of_user[p]] = (u32)ep.size();
+    ep_int.push_back(c->int_of_user[p]);
     ep.push_back(r);
   }
   c->n_ep = (u32)ep.size();
@@ -1533,6 +1543,7 @@ sta_status sta_destroy(sta_ctx c) {
   c->tree_arena.release();
   c->cons_arena.release();
   c->tmp_arena.release();
+  c->path_arena.release();
   for (CornerState& cs : c->corners) {
     cs.lib_arena.release();
     cs.rc_arena.release();
@@ -1561,6 +1572,8 @@ sta_status sta_load_graph(sta_ctx c, const sta_graph_desc* d) {
     c->graph_arena.release();
     c->tree_arena.release();
     c->cons_arena.release();
+    c->path_arena.release();
+    c->fi_p_d = c->fi_slot_d = c->ep_int_d = c->uoi_d = nullptr;
     c->P = d->num_pins; c->N = d->num_nets; c->A = d->num_arcs; c->C = d->num_checks; c->T = d->num_tables;
     c->pin_cap = fetch(d->pin_cap, c->P, d->mem, "pin_cap", c->stream);
     c->pin_role = fetch(d->pin_role, c->P, d->mem, "pin_role", c->stream);
@@ -1826,6 +1839,77 @@ sta_status sta_get_levels(sta_ctx c, uint32_t* level, uint32_t* perm, uint32_t* 
     };
     put(level, c->level);
     put(perm, c->perm);
+  });
+}
+
+sta_status sta_report_paths(sta_ctx c, uint32_t corner, const sta_path_query* q, sta_path_set* out, sta_mem mem) {
+  return guard(c, [&] {
+    CornerState& cs = corner_of(c, corner);
+    require_updated(c);
+    if (!q || !out) fail(STA_ERR_ARG, "query / output NULL");
+    if (q->mode > 1) fail(STA_ERR_ARG, "mode %u (0 setup, 1 hold)", q->mode);
+    if (q->k == 0 || q->nworst == 0) fail(STA_ERR_ARG, "k and nworst must be >= 1");
+    if (mem != STA_MEM_HOST && mem != STA_MEM_DEVICE) fail(STA_ERR_ARG, "bad sta_mem %d", (int)mem);
+    const u32 m = std::min(q->k, q->nworst);
+    if (m > 255) fail(STA_ERR_ARG, "min(k, nworst) = %u exceeds 255", m);
+    cudaStream_t s = c->stream;
+    if (!c->fi_p_d) {                        // lazily: the report's static arrays
+      Arena& g = c->path_arena;
+      c->fi_p_d = g.upload(c->fi_p_h, s);
+      c->fi_slot_d = g.upload(c->fi_slot_h, s);
+      c->ep_int_d = g.upload(c->ep_int_h, s);
+      c->uoi_d = g.upload(c->user_of_int, s);
+    }
+    Arena tmp;
+    try {
+      sta::PathArgs pa{};
+      pa.mode = q->mode;
+      pa.m = m;
+      pa.lists = tmp.alloc<sta::PathEnt>(2ull * c->NP * m);
+      pa.cnt = tmp.alloc<uint8_t>(2ull * c->NP);
+      pa.fi_p = c->fi_p_d;
+      pa.fi_slot = c->fi_slot_d;
+      pa.uoi = c->uoi_d;
+      pa.ep_int = c->ep_int_d;
+      const size_t nc = (size_t)c->n_ep * m;
+      pa.cand_key = tmp.alloc<unsigned long long>(nc);
+      pa.cand_ref = tmp.alloc<u32>(nc);
+      pa.cand_sub = tmp.alloc<u32>(nc);
+      pa.cand_slack = tmp.alloc<float>(nc);
+      const bool dev = mem == STA_MEM_DEVICE;
+      const u32 cp = out->cap_paths, cq = out->cap_pins;
+      pa.path_ptr = dev ? out->path_ptr : tmp.alloc<u32>((size_t)cp + 1);
+      pa.path_pin = dev ? out->path_pin : tmp.alloc<u32>(cq);
+      pa.path_rf = dev ? out->path_rf : tmp.alloc<uint8_t>(cq);
+      pa.path_at = dev ? out->path_at : tmp.alloc<float>(cq);
+      pa.path_slack = dev ? out->path_slack : tmp.alloc<float>(cp);
+      pa.path_ep = dev ? out->path_ep : tmp.alloc<u32>(cp);
+      if (!pa.path_ptr || !pa.path_pin || !pa.path_rf || !pa.path_at || !pa.path_slack || !pa.path_ep)
+        fail(STA_ERR_ARG, "output arrays NULL");
+      u32 np = 0, npin = 0;
+      bool fits = true;
+      const u32 kk = std::min(q->k, cp);
+      ck(sta::run_path_report(c->topo, cs.dev, pa, c->pull_stage_ptr.data(), c->S, kk, q->slack_lt, cq, &np,
+                              &npin, &fits, s), "path report kernels");
+      out->n_paths = np;
+      out->n_pins = npin;
+      if (q->k > cp && np == cp) fail(STA_ERR_ARG, "cap_paths %u < k %u", cp, q->k);
+      if (!fits) fail(STA_ERR_ARG, "cap_pins %u < %u pins of the %u paths", cq, npin, np);
+      if (!dev && np) {
+        ck(cudaMemcpyAsync(out->path_ptr, pa.path_ptr, 4ull * (np + 1), cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaMemcpyAsync(out->path_pin, pa.path_pin, 4ull * npin, cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaMemcpyAsync(out->path_rf, pa.path_rf, npin, cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaMemcpyAsync(out->path_at, pa.path_at, 4ull * npin, cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaMemcpyAsync(out->path_slack, pa.path_slack, 4ull * np, cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaMemcpyAsync(out->path_ep, pa.path_ep, 4ull * np, cudaMemcpyDeviceToHost, s), "D2H");
+      }
+      ck(cudaStreamSynchronize(s), "sync");
+    } catch (...) {
+      cudaStreamSynchronize(s);
+      tmp.release();
+      throw;
+    }
+    tmp.release();
   });
 }
 

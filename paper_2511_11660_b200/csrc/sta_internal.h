@@ -264,6 +264,41 @@ cudaError_t launch_gather_rc(const Topo& t, const CornerDev& c, float* net_load,
 cudaError_t launch_init_corner(const Topo& t, const CornerDev& c, uint32_t n_heavy, cudaStream_t s);
 cudaError_t launch_set_ptrs(const float* const* dst, const float* a, const float* b, cudaStream_t s);
 
+// ---- row f3: top-k path report (sta_kernels.cu, path_*_kernel)
+struct PathEnt {        // one partial path into a (pull pin, transition)
+  float a;              // its arrival there
+  uint32_t term;        // the fan-in term it came through (kNone: startpoint)
+  uint32_t rr;          // input transition << 31 | rank in the source's list
+};
+struct PathArgs {
+  uint32_t mode, m;                 // 0 setup (late), 1 hold (early); list length
+  PathEnt* lists;                   // [NP][2][m]
+  uint8_t* cnt;                     // [NP][2]
+  const uint32_t* fi_p;             // [NP + 1] fan-in terms of each pull pin
+  const uint32_t* fi_slot;          // [terms] delay slot (tdel) of each term
+  const uint32_t* uoi;              // [NP + NS] internal id -> user pin id
+  const uint32_t* ep_int;           // [n_ep] internal id of each endpoint
+  unsigned long long* cand_key;     // [n_ep * m] (orderable slack << 32 | user id)
+  uint32_t* cand_ref;               // [n_ep * m] endpoint index
+  uint32_t* cand_sub;               // [n_ep * m] transition << 31 | rank
+  float* cand_slack;                // [n_ep * m]
+  const uint32_t* sorted_ref;       // report order
+  const uint32_t* sorted_sub;
+  const float* sorted_slack;
+  uint32_t* path_ptr;               // outputs (device)
+  uint32_t* path_pin;
+  uint8_t* path_rf;
+  float* path_at;
+  float* path_slack;
+  uint32_t* path_ep;
+};
+// Enqueue the report on s and return the selected path and pin counts
+// (synchronizes s).  pin capacity of pa.path_* = cap_pins; if the pins do
+// not fit, only the counts are returned (*fits = false).
+cudaError_t run_path_report(const Topo& t, const CornerDev& c, PathArgs pa, const uint32_t* stage_ptr, uint32_t S,
+                            uint32_t k, float slack_lt, uint32_t cap_pins, uint32_t* n_paths, uint32_t* n_pins,
+                            bool* fits, cudaStream_t s);
+
 // ---- row a0 on the device (sta_levelize.cu): cell-arc fan-in / fan-out CSR
 // (segments in arc id order), Kahn-frontier levels over net + cell arcs and
 // perm = pins stably sorted by (level, id).  Device pointers; synchronizes s.

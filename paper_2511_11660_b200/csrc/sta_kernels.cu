@@ -27,6 +27,10 @@
 #include <math_constants.h>
 
 #include <algorithm>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "sta_internal.h"
 
@@ -1717,6 +1721,198 @@ cudaError_t pdl_launch_kernel(K kernel, dim3 grid, uint32_t block, cudaStream_t 
   return pdl_launch_smem(kernel, grid, block, 0, s, args...);
 }
 
+// ------------------------------------------------ f3: top-k path report
+// SURVEY.md §8(f) row 3; PAPER.md:187-190 ("top-k path reports ... top-k,
+// per-endpoint report limit, and slack-less-than thresholds ... flattened
+// CSR-based path pin arrays with slacks").  Same definition as the oracle's
+// O10 (readings P1-P4 in DESIGN.md): the m = min(nworst, k) first partial
+// paths into every (pull pin, transition), gate stage by gate stage, each
+// extending a partial path of a fan-in term's source by the delays the update
+// used (the term's stored cell delay, plus the Elmore delay of its net hop),
+// in the order (arrival: late descending / early ascending, predecessor pin
+// id, predecessor transition, predecessor rank).  The sums are the
+// forward's own fp32 additions, so the first path into a pin has exactly
+// the pin's arrival.  Net sinks stay implicit (pull-through): a sink's lists
+// are its driver's lists plus its Elmore delay.
+__device__ __forceinline__ bool path_better(bool late, float a1, uint32_t p1, uint32_t r1, float a2, uint32_t p2,
+                                            uint32_t r2) {
+  if (a1 != a2) return late ? a1 > a2 : a1 < a2;
+  if (p1 != p2) return p1 < p2;
+  return r1 < r2;                            // (transition << 31 | rank)
+}
+
+constexpr uint32_t kPathMaxTerms = 48;       // terms merged with per-term heads (more: rescans)
+
+__global__ void __launch_bounds__(kThreads) path_dp_kernel(Topo t, CornerDev c, PathArgs pa, uint32_t v0,
+                                                           uint32_t v1) {
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t v = v0 + (x >> 1), rf = x & 1u;
+  if (v >= v1) return;
+  const bool late = pa.mode == 0;
+  const uint32_t el = late ? 1u : 0u, m = pa.m;
+  PathEnt* out = pa.lists + ((size_t)v * 2 + rf) * m;
+  const uint32_t e0 = pa.fi_p[v], e1 = pa.fi_p[v + 1];
+  if (e0 == e1) {                            // startpoint (stage 0): its own arrival
+    const float a = reinterpret_cast<const float*>(c.at4 + v)[el * 2 + rf];
+    const bool ok = pa.uoi[v] != kNone && fin(a);
+    if (ok) out[0] = PathEnt{a, kNone, 0u};
+    pa.cnt[(size_t)v * 2 + rf] = ok ? 1 : 0;
+    return;
+  }
+  // per term: the source list (its length and input edge), the added delay,
+  // the predecessor's user pin id; merged by heads
+  const uint32_t nt = e1 - e0;
+  uint8_t head[kPathMaxTerms];
+  uint32_t n = 0;
+  uint32_t prev_p = 0, prev_r = 0;
+  float prev_a = 0.f;
+  for (; n < m; ++n) {
+    bool found = false;
+    float ba = 0.f;
+    uint32_t bp = 0, br = 0, bt = 0, brank = 0, birf = 0;
+    for (uint32_t q = 0; q < nt; ++q) {
+      const uint32_t e = e0 + q;
+      const uint32_t info = __ldg(t.fi_info + e), src = __ldg(t.fi_src + e), hop = __ldg(t.fi_hop + e);
+      const uint32_t irf = (uint32_t)primary_irf(info & 7u, (int)rf);
+      const uint32_t len = pa.cnt[(size_t)src * 2 + irf];
+      // the term's first entry not yet taken: its head, or (many terms) the
+      // first entry after the previous pick in the merge order
+      uint32_t j = 0;
+      const uint32_t pred = pa.uoi[hop != kNone ? t.NP + hop : src];
+      const float dl = reinterpret_cast<const float*>(c.tdel + __ldg(pa.fi_slot + e))[el * 2 + rf];
+      const float em = hop != kNone ? __ldcg(c.elm + hop) : 0.f;
+      const PathEnt* ls = pa.lists + ((size_t)src * 2 + irf) * m;
+      auto cand_a = [&](uint32_t jj) {
+        const float a0 = ls[jj].a;
+        return __fadd_rn(hop != kNone ? __fadd_rn(a0, em) : a0, dl);
+      };
+      if (nt <= kPathMaxTerms) {
+        j = n == 0 ? 0u : head[q];
+      } else {
+        while (j < len && n && !path_better(late, prev_a, prev_p, prev_r, cand_a(j), pred, (irf << 31) | j)) ++j;
+      }
+      if (j >= len) continue;
+      const float a = cand_a(j);
+      const uint32_t r = (irf << 31) | j;
+      if (!found || path_better(late, a, pred, r, ba, bp, br)) {
+        found = true;
+        ba = a; bp = pred; br = r; bt = e; brank = j; birf = irf;
+      }
+    }
+    if (n == 0 && nt <= kPathMaxTerms)
+      for (uint32_t q = 0; q < nt; ++q) head[q] = 0;
+    if (!found) break;
+    out[n] = PathEnt{ba, bt, (birf << 31) | brank};
+    if (nt <= kPathMaxTerms) head[bt - e0]++;
+    prev_a = ba; prev_p = bp; prev_r = br;
+  }
+  pa.cnt[(size_t)v * 2 + rf] = (uint8_t)n;
+}
+
+// per endpoint: its own seeds (the check / output delay),
+// then its candidate paths: the two transitions' lists merged by slack
+// (ties: rise first, then rank), at most m; key = (orderable slack, user id)
+__device__ __forceinline__ uint32_t ordered_bits(float f) {
+  const uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+__global__ void __launch_bounds__(kThreads) path_ep_kernel(Topo t, CornerDev c, PathArgs pa) {
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= t.n_ep) return;
+  const bool late = pa.mode == 0;
+  const uint32_t el = late ? 1u : 0u, m = pa.m;
+  const uint32_t i = pa.ep_int[x], pu = pa.uoi[i];
+  const bool sink = i >= t.NP;
+  const uint32_t src = sink ? __ldg(t.sink_drv + (i - t.NP)) : i;
+  const float em = sink ? __ldcg(c.elm + (i - t.NP)) : 0.f;
+  // the endpoint's arrival / slew (its own, or its driver's through the net hop)
+  Q4 at, sl;
+  load_rec(c, src, at, sl);
+  if (sink) net_hop(at, sl, em);
+  const EpRec er = t.ep[x];
+  Q4 sd = undef_rat();
+  seed4(t, c.lut, er.chk_tab, er.po, at, sl, sd);
+  const float S[2] = {sd.v[el * 2], sd.v[el * 2 + 1]};
+  uint32_t h0 = 0, h1 = 0;
+  const uint32_t n0 = fin(S[0]) ? pa.cnt[(size_t)src * 2] : 0, n1 = fin(S[1]) ? pa.cnt[(size_t)src * 2 + 1] : 0;
+  auto slack_of_e = [&](uint32_t rf, uint32_t j) {
+    const float a0 = pa.lists[((size_t)src * 2 + rf) * m + j].a;
+    const float a = sink ? __fadd_rn(a0, em) : a0;
+    return late ? __fsub_rn(S[rf], a) : __fsub_rn(a, S[rf]);
+  };
+  for (uint32_t n = 0; n < m; ++n) {
+    const size_t o = (size_t)x * m + n;
+    const bool has0 = h0 < n0, has1 = h1 < n1;
+    if (!has0 && !has1) {
+      pa.cand_key[o] = ~0ull;
+      pa.cand_ref[o] = kNone;
+      continue;
+    }
+    const float s0 = has0 ? slack_of_e(0, h0) : 0.f, s1 = has1 ? slack_of_e(1, h1) : 0.f;
+    const bool take0 = has0 && (!has1 || s0 <= s1);
+    const float sl_ = take0 ? s0 : s1;
+    const uint32_t rf = take0 ? 0u : 1u, j = take0 ? h0++ : h1++;
+    pa.cand_key[o] = ((unsigned long long)ordered_bits(sl_) << 32) | pu;
+    pa.cand_ref[o] = x | 0u;
+    pa.cand_sub[o] = (rf << 31) | j;
+    pa.cand_slack[o] = sl_;
+  }
+}
+
+// selected path s (sorted position s): its length, then its pins
+__device__ __forceinline__ uint32_t path_walk(const Topo& t, const CornerDev& c, const PathArgs& pa, uint32_t s,
+                                              uint32_t* pins, uint8_t* rfs, float* ats, uint32_t at_end) {
+  const uint32_t ref = pa.sorted_ref[s];
+  const uint32_t sub = pa.sorted_sub[s];
+  const uint32_t i = pa.ep_int[ref];
+  uint32_t rf = sub >> 31, j = sub & 0x7FFFFFFFu, len = 0;
+  const uint32_t m = pa.m;
+  const bool late = pa.mode == 0;
+  const uint32_t el = late ? 1u : 0u;
+  uint32_t v = i >= t.NP ? __ldg(t.sink_drv + (i - t.NP)) : i;
+  auto put = [&](uint32_t pin, uint32_t r, float a) {
+    if (pins) {
+      pins[at_end - 1 - len] = pin;
+      rfs[at_end - 1 - len] = (uint8_t)r;
+      ats[at_end - 1 - len] = a;
+    }
+    ++len;
+  };
+  if (i >= t.NP) {                           // the endpoint sink, then its driver
+    const float a = __fadd_rn(pa.lists[((size_t)v * 2 + rf) * m + j].a, __ldcg(c.elm + (i - t.NP)));
+    put(pa.uoi[i], rf, a);
+  }
+  for (;;) {
+    const PathEnt en = pa.lists[((size_t)v * 2 + rf) * m + j];
+    put(pa.uoi[v], rf, en.a);
+    if (en.term == kNone) break;             // startpoint
+    const uint32_t e = en.term, src = __ldg(t.fi_src + e), hop = __ldg(t.fi_hop + e);
+    const uint32_t irf = en.rr >> 31, jj = en.rr & 0x7FFFFFFFu;
+    if (hop != kNone)                        // the input sink of the term
+      put(pa.uoi[t.NP + hop], irf,
+          __fadd_rn(pa.lists[((size_t)src * 2 + irf) * m + jj].a, __ldcg(c.elm + hop)));
+    v = src;
+    rf = irf;
+    j = jj;
+  }
+  (void)el;
+  return len;
+}
+
+__global__ void __launch_bounds__(kThreads) path_len_kernel(Topo t, CornerDev c, PathArgs pa, uint32_t n_sel) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < n_sel) pa.path_ptr[s] = path_walk(t, c, pa, s, nullptr, nullptr, nullptr, 0);
+}
+
+__global__ void __launch_bounds__(kThreads) path_fill_kernel(Topo t, CornerDev c, PathArgs pa, uint32_t n_sel) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_sel) return;
+  path_walk(t, c, pa, s, pa.path_pin, pa.path_rf, pa.path_at, pa.path_ptr[s + 1]);
+  pa.path_slack[s] = pa.sorted_slack[s];
+  pa.path_ep[s] = pa.uoi[pa.ep_int[pa.sorted_ref[s]]];
+}
+
 __global__ void set_ptrs_kernel(const float** dst, const float* a, const float* b) {
   dst[0] = a;
   dst[1] = b;
@@ -1786,6 +1982,96 @@ cudaError_t launch_gather_rc(const Topo& t, const CornerDev& c, float* net_load,
   const uint32_t n = t.N > t.P ? t.N : t.P;
   if (n) gather_rc_kernel<<<blocks(n), kThreads, 0, s>>>(t, c, net_load, pin_elm);
   return cudaGetLastError();
+}
+
+namespace {
+__global__ void path_iota(uint32_t* x, uint32_t n) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = i;
+}
+__global__ void path_gather(PathArgs pa, const uint32_t* idx, uint32_t n, uint32_t* ref, uint32_t* sub, float* sl,
+                            const unsigned long long* keys, float slack_lt, uint32_t* count) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t j = idx[i];
+  ref[i] = pa.cand_ref[j];
+  sub[i] = pa.cand_sub[j];
+  sl[i] = pa.cand_slack[j];
+  if (keys[i] != ~0ull && pa.cand_slack[j] < slack_lt) atomicAdd(count, 1u);
+}
+}  // namespace
+
+cudaError_t run_path_report(const Topo& t, const CornerDev& c, PathArgs pa, const uint32_t* stage_ptr, uint32_t S,
+                            uint32_t k, float slack_lt, uint32_t cap_pins, uint32_t* n_paths, uint32_t* n_pins,
+                            bool* fits, cudaStream_t s) {
+  *n_paths = *n_pins = 0;
+  *fits = true;
+  for (uint32_t st = 0; st < S; ++st) {       // gate stages in order
+    const uint32_t v0 = stage_ptr[st], v1 = stage_ptr[st + 1];
+    if (v1 > v0) path_dp_kernel<<<blocks(2ull * (v1 - v0)), kThreads, 0, s>>>(t, c, pa, v0, v1);
+  }
+  const uint32_t n = t.n_ep * pa.m;
+  if (t.n_ep) path_ep_kernel<<<blocks(t.n_ep), kThreads, 0, s>>>(t, c, pa);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || n == 0) return e;
+  // report order: stable radix sort of the candidates (per endpoint they are
+  // already in order) by (slack, endpoint user id)
+  std::vector<void*> tmp;
+  auto alloc = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, std::max<size_t>(bytes, 16), s) != cudaSuccess) return nullptr;
+    tmp.push_back(p);
+    return p;
+  };
+  auto done = [&](cudaError_t r) {
+    for (void* p : tmp) cudaFreeAsync(p, s);
+    return r;
+  };
+  auto* idx_in = static_cast<uint32_t*>(alloc(4ull * n));
+  auto* idx_out = static_cast<uint32_t*>(alloc(4ull * n));
+  auto* key_out = static_cast<unsigned long long*>(alloc(8ull * n));
+  auto* ref = static_cast<uint32_t*>(alloc(4ull * n));
+  auto* sub = static_cast<uint32_t*>(alloc(4ull * n));
+  auto* sl = static_cast<float*>(alloc(4ull * n));
+  auto* cnt = static_cast<uint32_t*>(alloc(8));
+  if (!idx_in || !idx_out || !key_out || !ref || !sub || !sl || !cnt) return done(cudaErrorMemoryAllocation);
+  path_iota<<<blocks(n), kThreads, 0, s>>>(idx_in, n);
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, pa.cand_key, key_out, idx_in, idx_out, (int)n, 0, 64, s);
+  void* tsort = alloc(tb);
+  if (!tsort) return done(cudaErrorMemoryAllocation);
+  if ((e = cub::DeviceRadixSort::SortPairs(tsort, tb, pa.cand_key, key_out, idx_in, idx_out, (int)n, 0, 64, s)) !=
+      cudaSuccess)
+    return done(e);
+  cudaMemsetAsync(cnt, 0, 8, s);
+  path_gather<<<blocks(n), kThreads, 0, s>>>(pa, idx_out, n, ref, sub, sl, key_out, slack_lt, cnt);
+  uint32_t n_ok = 0;
+  cudaMemcpyAsync(&n_ok, cnt, 4, cudaMemcpyDeviceToHost, s);
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return done(e);
+  const uint32_t n_sel = std::min(n_ok, k);
+  *n_paths = n_sel;
+  if (!n_sel) return done(cudaSuccess);
+  pa.sorted_ref = ref;
+  pa.sorted_sub = sub;
+  pa.sorted_slack = sl;
+  path_len_kernel<<<blocks(n_sel), kThreads, 0, s>>>(t, c, pa, n_sel);
+  cudaMemsetAsync(pa.path_ptr + n_sel, 0, 4, s);
+  size_t ts = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, ts, pa.path_ptr, pa.path_ptr, (int)n_sel + 1, s);
+  void* tscan = alloc(ts);
+  if (!tscan) return done(cudaErrorMemoryAllocation);
+  if ((e = cub::DeviceScan::ExclusiveSum(tscan, ts, pa.path_ptr, pa.path_ptr, (int)n_sel + 1, s)) != cudaSuccess)
+    return done(e);
+  cudaMemcpyAsync(n_pins, pa.path_ptr + n_sel, 4, cudaMemcpyDeviceToHost, s);
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return done(e);
+  if (*n_pins > cap_pins) {
+    *fits = false;
+    return done(cudaSuccess);
+  }
+  path_fill_kernel<<<blocks(n_sel), kThreads, 0, s>>>(t, c, pa, n_sel);
+  e = cudaGetLastError();
+  cudaError_t e2 = cudaStreamSynchronize(s);
+  return done(e != cudaSuccess ? e : e2);
 }
 
 cudaError_t launch_set_ptrs(const float* const* dst, const float* a, const float* b, cudaStream_t s) {

@@ -29,7 +29,7 @@ EXPORTS = ["sta_create", "sta_destroy", "sta_last_error", "sta_status_string", "
            "sta_set_library", "sta_set_rc_tree", "sta_set_rc_values", "sta_set_constraints",
            "sta_update_timing", "sta_report_slack", "sta_get_timing", "sta_get_rc",
            "sta_get_levels", "sta_get_info", "sta_synchronize", "sta_profile_enable",
-           "sta_profile_read"]
+           "sta_profile_read", "sta_report_paths"]
 
 
 class StaError(RuntimeError):
@@ -64,6 +64,17 @@ class Info(C.Structure):
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+class PathQuery(C.Structure):
+    _fields_ = [("mode", C.c_uint32), ("k", C.c_uint32), ("nworst", C.c_uint32), ("slack_lt", C.c_float)]
+
+
+class PathSet(C.Structure):
+    _fields_ = [("cap_paths", C.c_uint32), ("cap_pins", C.c_uint32), ("n_paths", C.c_uint32),
+                ("n_pins", C.c_uint32), ("path_ptr", C.c_void_p), ("path_pin", C.c_void_p),
+                ("path_rf", C.c_void_p), ("path_at", C.c_void_p), ("path_slack", C.c_void_p),
+                ("path_ep", C.c_void_p)]
 
 
 class Profile(C.Structure):
@@ -102,6 +113,7 @@ def lib():
             "sta_synchronize": (i32, [vp]),
             "sta_profile_enable": (i32, [vp, i32]),
             "sta_profile_read": (i32, [vp, C.POINTER(Profile)]),
+            "sta_report_paths": (i32, [vp, u32, C.POINTER(PathQuery), C.POINTER(PathSet), i32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -314,6 +326,36 @@ class Context:
                                            perm.ctypes.data if P else None, C.byref(nl),
                                            STA_MEM_HOST))
         return level, perm, nl.value
+
+    def report_paths(self, corner: int = 0, mode: str = "setup", k: int = 10, nworst: int = 1,
+                     slack_lt: float = float("inf")):
+        """Top-k path report (sta_report_paths) -> list of dicts {slack, ep,
+        pins, rfs, at} in report order (host arrays)."""
+        q = PathQuery(0 if mode == "setup" else 1, int(k), int(nworst), float(slack_lt))
+        info = self.info()
+        cap_paths = int(k)
+        cap_pins = int(k) * (info["num_levels"] + 1)
+        while True:
+            ptr = np.zeros(cap_paths + 1, np.uint32)
+            pin = np.zeros(max(cap_pins, 1), np.uint32)
+            rf = np.zeros(max(cap_pins, 1), np.uint8)
+            at = np.zeros(max(cap_pins, 1), np.float32)
+            sl = np.zeros(max(cap_paths, 1), np.float32)
+            ep = np.zeros(max(cap_paths, 1), np.uint32)
+            o = PathSet(cap_paths, cap_pins, 0, 0, ptr.ctypes.data, pin.ctypes.data, rf.ctypes.data,
+                        at.ctypes.data, sl.ctypes.data, ep.ctypes.data)
+            st = self._L.sta_report_paths(self.h, int(corner), C.byref(q), C.byref(o), STA_MEM_HOST)
+            if st == 1 and o.n_pins > cap_pins:
+                cap_pins = int(o.n_pins)
+                continue
+            self._check(st)
+            break
+        out = []
+        for i in range(o.n_paths):
+            a, b = int(ptr[i]), int(ptr[i + 1])
+            out.append(dict(slack=float(sl[i]), ep=int(ep[i]), pins=pin[a:b].tolist(), rfs=rf[a:b].tolist(),
+                            at=at[a:b].tolist()))
+        return out
 
     def info(self) -> dict:
         i = Info()
