@@ -62,7 +62,7 @@ constexpr int kBwdMinBlocks = STA_BWD_MINB;
 #define STA_MERGE_BOUND 0                       // 1: merge rounds bounded by the longest run in the warp (measured slower)
 #endif
 #ifndef STA_BWD_PIPE
-#define STA_BWD_PIPE 2                          // backward: next unit's fan-out records: 1 registers, 2 TMA
+#define STA_BWD_PIPE 1                          // backward: next unit's fan-out records: 1 registers, 2 TMA (slower, r2)
 #endif
 constexpr uint32_t kMaxBatch = 8;               // corners traversed by one launch
 // backward persistent kernel: per-warp TMA staging buffer of the next unit's

@@ -1442,6 +1442,9 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_ker
   uint32_t phase = 0;
   auto issue = [&](const uint4& un) {
     if (lane == 0) {
+      // the warp's generic-proxy reads of the buffer (take) are ordered
+      // before the bulk copy's async-proxy writes into it
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       const uint32_t n = (un.w != 1 && un.y > un.x) ? (un.y - un.x) * 32u : 0u;
       mbar_expect_tx(bar, n);
       if (n) bulk_g2s(fbuf, t.sinkfo + 2 * (size_t)un.x, n, bar);
@@ -1455,6 +1458,10 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_ker
       f.a = fbuf[2 * lane];
       f.b = fbuf[2 * lane + 1];
     }
+    // every lane's reads complete (the values are in registers) before lane 0
+    // lets the next bulk copy overwrite the buffer
+    asm volatile("" ::"r"(f.a.x), "r"(f.a.y), "r"(f.a.z), "r"(f.a.w), "r"(f.b.x), "r"(f.b.y), "r"(f.b.z),
+                 "r"(f.b.w) : "memory");
     __syncwarp();
     return f;
   };
