@@ -538,6 +538,14 @@ __global__ void __launch_bounds__(kThreads) rc_lumped_kernel(Topo t, const __gri
 // order, so a block only ever waits for blocks that are already running.  A
 // segmented scan never crosses a net: the sums stay small (no cancellation
 // against other nets) and a net's Elmore delays need no offset.
+// Small blocks (128 threads, <= 56 registers: one block fits in the slot a
+// retiring tier-A block frees), so these launches -- on a high-priority side
+// stream -- actually run beside the tier-A kernel instead of starving until it
+// drains.
+#ifndef STA_TC_THREADS
+#define STA_TC_THREADS 128
+#endif
+constexpr int kTcThreads = STA_TC_THREADS;
 struct SegSum {
   double v;
   uint32_t f;   // a segment head inside
@@ -545,7 +553,7 @@ struct SegSum {
 // (a then b): b restarts at a head
 __device__ __forceinline__ SegSum seg_op(SegSum a, SegSum b) { return SegSum{b.f ? b.v : a.v + b.v, a.f | b.f}; }
 
-// Block-wide exclusive segmented scan of one SegSum per thread (kThreads
+// Block-wide exclusive segmented scan of one SegSum per thread (kTcThreads
 // threads); *total receives the block's inclusive total.
 __device__ __forceinline__ SegSum seg_block_excl(SegSum x, SegSum* s_w, SegSum* total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -558,7 +566,7 @@ __device__ __forceinline__ SegSum seg_block_excl(SegSum x, SegSum* s_w, SegSum* 
   if (lane == 31) s_w[w] = inc;
   __syncthreads();
   if (w == 0) {
-    SegSum a = lane < kThreads / 32 ? s_w[lane] : SegSum{0.0, 0u};
+    SegSum a = lane < kTcThreads / 32 ? s_w[lane] : SegSum{0.0, 0u};
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       SegSum y{__shfl_up_sync(0xFFFFFFFFu, a.v, o), __shfl_up_sync(0xFFFFFFFFu, a.f, o)};
@@ -570,12 +578,12 @@ __device__ __forceinline__ SegSum seg_block_excl(SegSum x, SegSum* s_w, SegSum* 
   SegSum ex{__shfl_up_sync(0xFFFFFFFFu, inc.v, 1), __shfl_up_sync(0xFFFFFFFFu, inc.f, 1)};
   if (lane == 0) ex = SegSum{0.0, 0u};
   const SegSum r = w ? seg_op(s_w[w - 1], ex) : ex;
-  *total = s_w[kThreads / 32 - 1];
+  *total = s_w[kTcThreads / 32 - 1];
   __syncthreads();
   return r;
 }
 
-constexpr int kTcPer = (int)(kTcTile / kThreads);   // consecutive elements per thread
+constexpr int kTcPer = (int)(kTcTile / kTcThreads);   // consecutive elements per thread
 
 #ifndef STA_TC_RELAXED
 #define STA_TC_RELAXED 0
@@ -656,7 +664,7 @@ __device__ __forceinline__ uint32_t tc_ticket(uint32_t* counter, uint32_t nb) {
 #ifndef STA_TC_MINB
 #define STA_TC_MINB 1
 #endif
-__global__ void __launch_bounds__(kThreads, STA_TC_MINB) tc_node_kernel(Topo t, const __grid_constant__ Batch B) {
+__global__ void __launch_bounds__(kTcThreads, STA_TC_MINB) tc_node_kernel(Topo t, const __grid_constant__ Batch B) {
   __shared__ SegSum s_w[32];
   pdl_wait();
   pdl_launch();
@@ -705,7 +713,7 @@ __global__ void __launch_bounds__(kThreads, STA_TC_MINB) tc_node_kernel(Topo t, 
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(c.err_flag, 1u);
 }
 
-__global__ void __launch_bounds__(kThreads, STA_TC_MINB) tc_event_kernel(Topo t, const __grid_constant__ Batch B) {
+__global__ void __launch_bounds__(kTcThreads, STA_TC_MINB) tc_event_kernel(Topo t, const __grid_constant__ Batch B) {
   __shared__ SegSum s_w[32];
   pdl_wait();
   pdl_launch();
@@ -1957,8 +1965,8 @@ cudaError_t launch_rc(const Topo& t, const Batch& b, uint32_t wgrid, cudaStream_
 cudaError_t launch_rc_tierC(const Topo& t, const Batch& b, cudaStream_t s) {
   if (!t.nC) return cudaSuccess;
   const uint32_t K = b.K;
-  cudaError_t e = pdl_launch_kernel(tc_node_kernel, dim3(tierC_blocks(t.nCn), K), kThreads, s, t, b);
-  if (e == cudaSuccess) e = pdl_launch_kernel(tc_event_kernel, dim3(tierC_blocks(2ull * t.nCn), K), kThreads, s, t, b);
+  cudaError_t e = pdl_launch_kernel(tc_node_kernel, dim3(tierC_blocks(t.nCn), K), kTcThreads, s, t, b);
+  if (e == cudaSuccess) e = pdl_launch_kernel(tc_event_kernel, dim3(tierC_blocks(2ull * t.nCn), K), kTcThreads, s, t, b);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
