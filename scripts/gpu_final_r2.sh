@@ -1,0 +1,30 @@
+#!/usr/bin/env bash
+# End-of-round evidence (one gpurun call): tests, smoke, bench lines (C3, C5,
+# reference arm), per-config numbers, C4 loop, ncu launch list + full
+# captures, sanitizers.  Outputs in gpurun_out/, copied to profiles/ by hand.
+set -u
+T=${TAG:-r2final}
+mkdir -p gpurun_out
+python __graft_entry__.py > gpurun_out/build_${T}.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_${T}.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_${T}.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_${T}.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke_${T}.log
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_${T}.json 2> gpurun_out/bench_${T}.err
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_${T}.json 2>&1
+timeout 900 python bench.py --config c5_multicorner --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench_c5_${T}.json 2> gpurun_out/bench_c5_${T}.err
+timeout 1200 python scripts/bench_configs.py > gpurun_out/bench_configs_${T}.json 2> gpurun_out/bench_configs_${T}.err
+timeout 900 python scripts/bench_tdp.py --iters 1000 --check > gpurun_out/bench_c4_${T}.json 2> gpurun_out/bench_c4_${T}.err
+if [ "${NCU:-1}" = 1 ]; then
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/launches_${T}.csv python bench.py --steps 3 --warmup 3 --quick > gpurun_out/ncu_launch_${T}.log 2>&1
+for K in fwd_persistent bwd_persistent rc_warp tc_event; do
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:${K} \
+    --launch-skip 3 --launch-count 1 -o gpurun_out/prof_${T}_${K} \
+    python bench.py --steps 1 --warmup 3 --quick > gpurun_out/ncu_${K}_${T}.log 2>&1
+done
+fi
+if [ "${SAN:-1}" = 1 ]; then
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_run.py > gpurun_out/sanitizer_${tool}_${T}.log 2>&1
+  echo "$tool rc=$?" >> gpurun_out/sanitizer_${tool}_${T}.log
+done
+fi

@@ -1,4 +1,4 @@
-"""Small updates for compute-sanitizer (memcheck / racecheck / synccheck):
+"""Small updates for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
 c17, a 2k-cell synthetic design with high-fan-out nets, wide gates and
 two-output cells; both launchers; compared with the oracle."""
 import os
@@ -14,15 +14,20 @@ from tests.parity import compare_update  # noqa: E402
 from tests.test_gpu_parity import _wide_multi_output_design  # noqa: E402
 
 designs = [synth.c17(), synth.generate(2000, 16, seed=4, n_hfn=2, hfn_range=(40, 400), period=200.0),
-           _wide_multi_output_design()]
+           _wide_multi_output_design(),
+           # tier-C RC (nets > 1024 nodes), 3 corners in one launch batch
+           synth.generate(3000, 16, seed=6, n_hfn=2, hfn_range=(1500, 2500), corners=3, corner_recipe="c5",
+                          period=250.0)]
 for mode in ("0", "1"):
     os.environ["STA_STAGE_KERNELS"] = mode
     for d in designs:
-        ctx = sta.Context(0, 1)
+        ctx = sta.Context(0, d.num_corners)
         sta.load_design(ctx, d)
         for _ in range(2):
             ctx.update_timing()
         ctx.synchronize()
-        compare_update(ctx, oracle.update(d))
+        for c in range(d.num_corners):
+            compare_update(ctx, oracle.update(d, c), corner=c)
+        ctx.report_paths(0, "setup", k=20, nworst=2)       # row f3 kernels
         ctx.close()
         print("ok", mode, d.name, flush=True)
