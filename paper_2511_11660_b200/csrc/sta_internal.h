@@ -238,9 +238,9 @@ cudaError_t launch_rc_tierC(const Topo& t, const Batch& b, cudaStream_t s);
 // event scans [nbn + nbe] (double), their flags [nbn + nbe] (u32 {has head,
 // epoch}) and the two tile tickets (u32, zero-initialised, monotonic)
 #ifndef STA_TC_TILE
-#define STA_TC_TILE 512
+#define STA_TC_TILE 2048
 #endif
-constexpr uint32_t kTcTile = STA_TC_TILE;       // elements per tier-C block (128 threads x 4)
+constexpr uint32_t kTcTile = STA_TC_TILE;       // elements per tier-C block (256 threads x 8)
 __host__ __device__ inline uint32_t tierC_blocks(uint64_t n) { return (uint32_t)((n + kTcTile - 1) / kTcTile); }
 __host__ __device__ inline size_t tierC_scratch(uint32_t nCn) {
   const size_t nb = (size_t)tierC_blocks(nCn) + tierC_blocks(2ull * nCn);
