@@ -5,6 +5,7 @@
 // Every arithmetic step of the timing update runs in sta_kernels.cu; this file
 // only arranges data (integer bookkeeping) and enqueues kernels.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -14,6 +15,8 @@
 #include <limits>
 #include <new>
 #include <string>
+#include <condition_variable>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -63,6 +66,44 @@ void par_chunks(uint64_t n, F&& f) {
   for (unsigned t = 0; t < T; ++t) th.emplace_back([&f, n, t, T] { f(n * t / T, n * (t + 1) / T, t); });
   for (auto& x : th) x.join();
 }
+// Host parallel loop over a sequence of dependent phases: T threads run
+// f(phase, lo, hi) on their chunk of [0, n(phase)) for every phase in order,
+// with a barrier between phases (one thread team for all phases instead of
+// one spawn per phase).  f must not throw.
+template <class N, class F>
+void par_phases(uint32_t phases, N&& n_of, F&& f) {
+  const unsigned T = host_threads();
+  if (T == 1) {
+    for (uint32_t ph = 0; ph < phases; ++ph) f(ph, (uint64_t)0, (uint64_t)n_of(ph));
+    return;
+  }
+  std::mutex mu;
+  std::condition_variable cv;
+  unsigned arrived = 0, gen = 0;
+  auto barrier = [&] {
+    std::unique_lock<std::mutex> lk(mu);
+    const unsigned g = gen;
+    if (++arrived == T) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  };
+  std::vector<std::thread> th;
+  th.reserve(T);
+  for (unsigned t = 0; t < T; ++t)
+    th.emplace_back([&, t] {
+      for (uint32_t ph = 0; ph < phases; ++ph) {
+        const uint64_t n = n_of(ph);
+        f(ph, n * t / T, n * (t + 1) / T);
+        barrier();
+      }
+    });
+  for (auto& x : th) x.join();
+}
+
 // in-place exclusive prefix sum; returns the total
 template <class T>
 T excl_prefix(std::vector<T>& v) {
@@ -358,20 +399,19 @@ void build_plan(sta_ctx c) {
     std::vector<u32> lptr(c->num_levels + 1, 0);
     for (u32 p = 0; p < P; ++p) lptr[c->level[p] + 1]++;
     for (u32 l = 0; l < c->num_levels; ++l) lptr[l + 1] += lptr[l];
-    for (u32 l = 0; l < c->num_levels; ++l) {
-      par_chunks(lptr[l + 1] - lptr[l], [&](uint64_t lo, uint64_t hi, unsigned) {
-        for (uint64_t j = lptr[l] + lo; j < lptr[l] + hi; ++j) {
-          const u32 p = c->perm[j];
-          if (c->is_sink[p]) {
-            c->stage[p] = c->stage[driver_of(p)];
-          } else if (fi_ptr[p + 1] != fi_ptr[p]) {
-            u32 st = 0;
-            for (u32 x = fi_ptr[p]; x < fi_ptr[p + 1]; ++x) st = std::max(st, c->stage[c->arc_from[fi_ids[x]]] + 1);
-            c->stage[p] = st;
-          }
+    par_phases(c->num_levels, [&](uint32_t l) { return (uint64_t)(lptr[l + 1] - lptr[l]); },
+               [&](uint32_t l, uint64_t lo, uint64_t hi) {
+      for (uint64_t j = lptr[l] + lo; j < lptr[l] + hi; ++j) {
+        const u32 p = c->perm[j];
+        if (c->is_sink[p]) {
+          c->stage[p] = c->stage[driver_of(p)];
+        } else if (fi_ptr[p + 1] != fi_ptr[p]) {
+          u32 st = 0;
+          for (u32 x = fi_ptr[p]; x < fi_ptr[p + 1]; ++x) st = std::max(st, c->stage[c->arc_from[fi_ids[x]]] + 1);
+          c->stage[p] = st;
         }
-      });
-    }
+      }
+    });
   }
 
   // internal numbering: pull pins by (stage, id); sinks grouped by driver
@@ -676,38 +716,56 @@ void build_plan(sta_ctx c) {
         items += n;
         ++p;
       }
-      u32 kmax = 0;
-      for (u32 e = fi_p[q0]; e < fi_p[q0] + items; ++e) kmax = std::max(kmax, fwu_of_pin[fi_src[e]]);
-      key.push_back((u64)kmax << 32 | su.size());
       su.push_back(make_uint3(q0, fi_p[q0], items));
     }
+    // sort keys (parallel: random reads of the producers' unit positions)
+    key.resize(su.size());
+    par_chunks(su.size(), [&](uint64_t lo, uint64_t hi, unsigned) {
+      for (uint64_t x = lo; x < hi; ++x) {
+        u32 kmax = 0;
+        for (u32 e = su[x].y; e < su[x].y + su[x].z; ++e) kmax = std::max(kmax, fwu_of_pin[fi_src[e]]);
+        key[x] = (u64)kmax << 32 | x;
+      }
+    });
     std::sort(key.begin(), key.end());
-    for (u64 kk : key) {
-      const uint3 un = su[(u32)kk];
-      const u32 q0 = un.x, e0 = un.y, items = un.z;
-      const u32 upos = (u32)fwu_stage.size();
-      for (u32 e = e0; e < e0 + items; ++e) fwu_of_pin[fi_pin[e]] = upos;
-      if (items > sta::kFwdUnitTerms) {    // one pin with many terms: the warp loops over fi_*
-        // slot 0: {mark, first term, terms, pin}; slot 1: {mark, first delay slot}
-        // (the delays of these terms live past the unit slots)
-        heavy_units.push_back((u32)fterm.size());
-        fterm.push_back(make_uint4(sta::kHeavyMark, e0, items, q0));
-        fterm.push_back(make_uint4(sta::kHeavyMark, 0, 0, 0));
-        for (u32 x = 2; x < sta::kFwdUnitTerms; ++x) fterm.push_back(make_uint4(sta::kHeavyMark, e0, items, q0));
-      } else {
-        for (u32 x = 0; x < sta::kFwdUnitTerms; ++x) {
-          if (x >= items) {
-            fterm.push_back(pad);
-            continue;
+    // emission in sorted order: unit r of the stage takes slots [8 (u0 + r), 8 (u0 + r + 1))
+    const u32 u0 = (u32)fwu_stage.size();
+    const size_t f0 = fterm.size();
+    fterm.resize(f0 + (size_t)sta::kFwdUnitTerms * su.size());
+    fwu_stage.resize(u0 + su.size(), s);
+    std::vector<uint8_t> heavy_flag(su.size(), 0);
+    std::atomic<bool> too_large{false};
+    par_chunks(su.size(), [&](uint64_t lo, uint64_t hi, unsigned) {
+      for (uint64_t r = lo; r < hi; ++r) {
+        const uint3 un = su[(u32)key[r]];
+        const u32 q0 = un.x, e0 = un.y, items = un.z;
+        const u32 upos = u0 + (u32)r;
+        uint4* ft = fterm.data() + f0 + (size_t)sta::kFwdUnitTerms * r;
+        for (u32 e = e0; e < e0 + items; ++e) fwu_of_pin[fi_pin[e]] = upos;
+        if (items > sta::kFwdUnitTerms) {  // one pin with many terms: the warp loops over fi_*
+          // slot 0: {mark, first term, terms, pin}; slot 1: {mark, first delay slot}
+          // (the delays of these terms live past the unit slots)
+          heavy_flag[r] = 1;
+          ft[0] = make_uint4(sta::kHeavyMark, e0, items, q0);
+          ft[1] = make_uint4(sta::kHeavyMark, 0, 0, 0);
+          for (u32 x = 2; x < sta::kFwdUnitTerms; ++x) ft[x] = make_uint4(sta::kHeavyMark, e0, items, q0);
+        } else {
+          for (u32 x = 0; x < sta::kFwdUnitTerms; ++x) {
+            if (x >= items) {
+              ft[x] = pad;
+              continue;
+            }
+            const u32 e = e0 + x;
+            if (fi_info[e] >> 31) too_large = true;
+            term_slot[e] = (u32)(f0 + (size_t)sta::kFwdUnitTerms * r + x);
+            ft[x] = make_uint4(fi_src[e], fi_hop[e], fi_info[e], fi_pin[e]);
           }
-          const u32 e = e0 + x;
-          if (fi_info[e] >> 31) fail(STA_ERR_LUT, "table id too large for the forward plan");
-          term_slot[e] = (u32)fterm.size();
-          fterm.push_back(make_uint4(fi_src[e], fi_hop[e], fi_info[e], fi_pin[e]));
         }
       }
-      fwu_stage.push_back(s);
-    }
+    });
+    if (too_large) fail(STA_ERR_LUT, "table id too large for the forward plan");
+    for (size_t r = 0; r < su.size(); ++r)
+      if (heavy_flag[r]) heavy_units.push_back((u32)(f0 + (size_t)sta::kFwdUnitTerms * r));
   }
   {
     u32 next = (u32)fterm.size();
@@ -742,23 +800,31 @@ void build_plan(sta_ctx c) {
     };
     for (u32 x = c->tile_stage_ptr[s]; x < c->tile_stage_ptr[s + 1]; ++x) {
       const u32 k1 = x + 1 < c->tile_stage_ptr[s + 1] ? tiles[x + 1].x : stage_sink_end[s];
-      u32 kmax = 0;
-      for (u32 k = tiles[x].x; k < k1; ++k) {
-        for (u32 f = sfo_p[k]; f < sfo_p[k + 1]; ++f) kmax = std::max(kmax, bwu_of_pin[sfo_dst[f]]);
-        if (k == tiles[x].x || drv_of_sink[k] != drv_of_sink[k - 1]) reads_pin(drv_of_sink[k], kmax);
-      }
-      key.push_back((u64)kmax << 32 | su.size());
       su.push_back(make_uint4(tiles[x].x, k1, tiles[x].y, tile_part[x] == kNone ? 0 : 2 + tile_part[x]));
     }
     const u32 ncap = unit_cap(c->nosink_stage_ptr[s + 1] - c->nosink_stage_ptr[s], sta::kTile, bwd_warps);
     for (u32 x = c->nosink_stage_ptr[s]; x < c->nosink_stage_ptr[s + 1]; x += ncap) {
       const u32 x1 = std::min<u32>(x + ncap, c->nosink_stage_ptr[s + 1]);
       if (nosink[x1 - 1] - nosink[x] != x1 - 1 - x) fail(STA_ERR_ARG, "internal: sink-less pins not contiguous");
-      u32 kmax = 0;
-      for (u32 i = nosink[x]; i <= nosink[x1 - 1]; ++i) reads_pin(i, kmax);
-      key.push_back((u64)kmax << 32 | su.size());
       su.push_back(make_uint4(nosink[x], nosink[x1 - 1] + 1, 0, 1));
     }
+    // sort keys in parallel (random reads of the producers' unit positions)
+    key.resize(su.size());
+    par_chunks(su.size(), [&](uint64_t lo, uint64_t hi, unsigned) {
+      for (uint64_t x = lo; x < hi; ++x) {
+        const uint4 un = su[x];
+        u32 kmax = 0;
+        if (un.w == 1) {
+          for (u32 i = un.x; i < un.y; ++i) reads_pin(i, kmax);
+        } else {
+          for (u32 k = un.x; k < un.y; ++k) {
+            for (u32 f = sfo_p[k]; f < sfo_p[k + 1]; ++f) kmax = std::max(kmax, bwu_of_pin[sfo_dst[f]]);
+            if (k == un.x || drv_of_sink[k] != drv_of_sink[k - 1]) reads_pin(drv_of_sink[k], kmax);
+          }
+        }
+        key[x] = (u64)kmax << 32 | x;
+      }
+    });
     std::sort(key.begin(), key.end());
     for (u64 kk : key) {
       const uint4 un = su[(u32)kk];

@@ -282,15 +282,15 @@ cudaError_t levelize_device(uint32_t P, uint32_t N, uint32_t A, const uint32_t* 
   std::vector<void*> tmp;
   auto alloc = [&](size_t bytes) -> uint32_t* {
     void* p = nullptr;
-    if (cudaMalloc(&p, std::max<size_t>(bytes, 4)) != cudaSuccess) return nullptr;
+    if (cudaMallocAsync(&p, std::max<size_t>(bytes, 4), s) != cudaSuccess) return nullptr;
     tmp.push_back(p);
     return static_cast<uint32_t*>(p);
   };
   cudaError_t e = cudaSuccess;
   uint32_t* h = nullptr;                           // pinned: {next count, cycle pin}
   auto done = [&](cudaError_t r) {
+    for (void* p : tmp) cudaFreeAsync(p, s);
     cudaStreamSynchronize(s);
-    for (void* p : tmp) cudaFree(p);
     if (h) cudaFreeHost(h);
     return r;
   };
