@@ -170,6 +170,38 @@ STA_API sta_status sta_set_library(sta_ctx ctx, uint32_t corner, sta_mem mem, ui
 STA_API sta_status sta_set_rc_tree(sta_ctx ctx, sta_mem mem, const uint32_t* rc_ptr, uint32_t num_nodes,
                            const int32_t* parent, const uint32_t* node_pin);
 
+/* Built-in Steiner RC estimation from pin positions (
+ * "A placer only needs to provide HeteroSTA with pin
+ * positions and unit resistance/capacitance values along x/y directions";
+ * construction SPEC.md:322-331 with its decisions SPEC.md:338-343).  For
+ * every net of the loaded graph: its pins (driver, then sinks by pin id) are
+ * joined by a rectilinear minimum spanning tree (Prim from the driver, fp32
+ * Manhattan distances, ties by the smaller pin id), every tree edge is
+ * embedded as an L (horizontal leg first from the parent, one Steiner node
+ * at the bend when both legs are non-zero), a leg of length L along x/y has
+ * resistance L * res_x/res_y (zero clamped to 1e-6 kOhm) and puts
+ * L * cap_x/cap_y / 2 on each end node.  Runs on the device (one warp or
+ * block per net); Prim is O(m^2) in the net's pin count m.
+ *  - pin_x[P], pin_y[P]: positions (distance units), finite, in `mem`
+ *    memory; units: all >= 0 and finite.
+ *  - outputs, in `mem` memory, in the layout sta_set_rc_tree /
+ *    sta_set_rc_values take: rc_ptr[N+1]; parent, node_pin, res, cap of
+ *    node_capacity entries, which must be >= 2 * (pins on nets) - N (the
+ *    largest possible node count); *num_nodes (host) receives the count.
+ *  Nodes of a net are in Prim order, each Steiner node right before its
+ *  pin; node 0 is the driver.  The call synchronizes the ctx stream.
+ * Errors: STA_ERR_ORDER (no graph), STA_ERR_ARG (capacity, units, NULL
+ * outputs, non-finite host positions), STA_ERR_CUDA. */
+typedef struct {
+  float res_x, res_y;   /* kOhm per distance unit */
+  float cap_x, cap_y;   /* fF per distance unit */
+} sta_steiner_units;
+
+STA_API sta_status sta_build_steiner(sta_ctx ctx, sta_mem mem, const float* pin_x, const float* pin_y,
+                             const sta_steiner_units* units, uint32_t node_capacity, uint32_t* rc_ptr,
+                             int32_t* parent, uint32_t* node_pin, float* res, float* cap,
+                             uint32_t* num_nodes);
+
 /* Per-corner RC values: res[i] = resistance of the edge parent -> i (kOhm,
  * ignored at node 0), cap[i] = wire capacitance to ground at node i (fF);
  * both num_nodes long, >= 0 and finite.  HOST: copied into ctx-owned device

@@ -67,6 +67,9 @@ def lib():
         _lib.orc_paths.restype = C.c_int
         _lib.orc_paths.argtypes = [C.c_void_p, C.c_int, C.c_uint32, C.c_uint32, C.c_double, C.c_uint32,
                                    C.c_uint32] + [C.c_void_p] * 8
+        _lib.orc_steiner.restype = C.c_uint32
+        _lib.orc_steiner.argtypes = [C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_double, C.c_double, C.c_double, C.c_double] + [C.c_void_p] * 5
     return _lib
 
 
@@ -231,3 +234,24 @@ def paths(d, corner: int = 0, mode: str = "setup", k: int = 10, nworst: int = 1,
         out.append(dict(slack=float(sl[i]), ep=int(ep[i]), pins=pin[a:b].tolist(), rfs=rf[a:b].tolist(),
                         at=at[a:b].tolist()))
     return out
+
+
+def steiner(net_ptr, net_pins, x, y, res_x, res_y, cap_x, cap_y):
+    """O11 Steiner RC from pin positions -> (rc_ptr, parent, node_pin, res,
+    cap) in the sta_set_rc_tree / sta_set_rc_values layout."""
+    net_ptr = np.ascontiguousarray(net_ptr, np.uint32)
+    net_pins = np.ascontiguousarray(net_pins, np.uint32)
+    x = np.ascontiguousarray(x, np.float32)
+    y = np.ascontiguousarray(y, np.float32)
+    N = net_ptr.size - 1
+    cap_n = max(2 * int(net_ptr[-1]) - N, 1)
+    rc_ptr = np.zeros(N + 1, np.uint32)
+    parent = np.zeros(cap_n, np.int32)
+    node_pin = np.zeros(cap_n, np.uint32)
+    res = np.zeros(cap_n, np.float32)
+    cap = np.zeros(cap_n, np.float32)
+    # unit values are float32 inputs (the device reads them as float)
+    u = [float(np.float32(v)) for v in (res_x, res_y, cap_x, cap_y)]
+    n = lib().orc_steiner(N, _p(net_ptr), _p(net_pins), _p(x), _p(y), *u, _p(rc_ptr), _p(parent),
+                          _p(node_pin), _p(res), _p(cap))
+    return rc_ptr, parent[:n], node_pin[:n], res[:n], cap[:n]

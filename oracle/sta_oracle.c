@@ -625,3 +625,117 @@ static int path_report(const orc_design* d, const arcs_t* g, const uint32_t* ord
   free(L); free(cnt); free(cand); free(pc); free(kept); free(chain);
   return st;
 }
+
+/* ------------------------------------------------- O11: built-in Steiner RC */
+/* SURVEY.md §8(f) row 2; PAPER.md:178-179 ("A placer only needs to provide
+ * HeteroSTA with pin positions and unit resistance/capacitance values along
+ * x/y directions"); the construction is SPEC.md:322-331 with its decisions
+ * SPEC.md:338-343 (FLUTE's tables are out of scope there too):
+ *   1. a net's pins: the driver, then its sinks sorted by pin id;
+ *   2. rectilinear minimum spanning tree by Prim from the driver, Manhattan
+ *      distance, the next pin = smallest distance to the tree, ties by the
+ *      smaller pin id; a pin's tree parent = the tree pin that first gave it
+ *      its final distance (strict improvement only: DESIGN.md reading S2);
+ *   3. each tree edge parent -> child embedded as an L, horizontal leg first
+ *      from the parent (reading S3): one Steiner node at (x_child, y_parent)
+ *      when both legs are non-zero;
+ *   4. a leg of length L in direction d: resistance L * unit_res_d, and
+ *      L * unit_cap_d split half to each end node; zero resistances clamped to
+ *      1e-6 kOhm.
+ * Distances (the MST decisions) are fp32, as on the device (S1);
+ * resistances and capacitances are accumulated in fp64 and stored as float.
+ * Output in the sta_set_rc_tree layout: net n owns nodes [rc_ptr[n],
+ * rc_ptr[n+1]), node 0 the driver (parent -1), parents local and < child;
+ * nodes in Prim order, each Steiner node right before its pin.  Capacity of
+ * the node arrays: 2 * net_ptr[N] - N suffices.  Returns the node count. */
+static int cmp_u32(const void* a, const void* b) {
+  const uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+  return x < y ? -1 : x > y;
+}
+
+static float mdist(const float* x, const float* y, uint32_t a, uint32_t b) {
+  return fabsf(x[a] - x[b]) + fabsf(y[a] - y[b]);
+}
+
+uint32_t orc_steiner(uint32_t N, const uint32_t* net_ptr, const uint32_t* net_pins, const float* x,
+                     const float* y, double rx, double ry, double cx, double cy, uint32_t* rc_ptr,
+                     int32_t* parent, uint32_t* node_pin, float* res, float* cap) {
+  uint32_t nn = 0, maxn = 1;
+  for (uint32_t n = 0; n < N; ++n)
+    if (net_ptr[n + 1] - net_ptr[n] > maxn) maxn = net_ptr[n + 1] - net_ptr[n];
+  uint32_t* pin = malloc(sizeof(uint32_t) * maxn);     /* step 1: driver, sinks by id */
+  uint32_t* par = malloc(sizeof(uint32_t) * maxn);     /* tree parent (index into pin) */
+  uint32_t* node_of = malloc(sizeof(uint32_t) * maxn); /* local node of each pin */
+  char* in_tree = malloc(maxn);
+  float* key = malloc(sizeof(float) * maxn);
+  double* c = malloc(sizeof(double) * 2 * maxn);       /* node caps of the net */
+  for (uint32_t n = 0; n < N; ++n) {
+    const uint32_t m = net_ptr[n + 1] - net_ptr[n], base = nn;
+    rc_ptr[n] = nn;
+    for (uint32_t k = 0; k < m; ++k) pin[k] = net_pins[net_ptr[n] + k];
+    if (m > 1) qsort(pin + 1, m - 1, sizeof(uint32_t), cmp_u32);
+    /* step 2: Prim */
+    for (uint32_t k = 0; k < m; ++k) {
+      in_tree[k] = k == 0;
+      key[k] = k ? mdist(x, y, pin[0], pin[k]) : 0.f;
+      par[k] = 0;
+    }
+    uint32_t local = 0;
+    parent[base] = -1;
+    node_pin[base] = pin[0];
+    res[base] = 0.f;
+    c[0] = 0.0;
+    node_of[0] = local++;
+    for (uint32_t step = 1; step < m; ++step) {
+      uint32_t best = 0;
+      for (uint32_t k = 1; k < m; ++k) {
+        if (in_tree[k]) continue;
+        if (!best || key[k] < key[best] || (key[k] == key[best] && pin[k] < pin[best])) best = k;
+      }
+      in_tree[best] = 1;
+      /* step 3: emit the edge par[best] -> best as an L, horizontal leg first */
+      const uint32_t p = par[best], u = pin[p], v = pin[best];
+      const float dx = fabsf(x[v] - x[u]), dy = fabsf(y[v] - y[u]);
+      uint32_t up = node_of[p];
+      if (dx != 0.f && dy != 0.f) {                    /* Steiner bend at (x_v, y_u) */
+        const uint32_t b = local++;
+        parent[base + b] = (int32_t)up;
+        node_pin[base + b] = ORC_NO_PIN;
+        res[base + b] = (float)((double)dx * rx > 0 ? (double)dx * rx : 1e-6);
+        c[up] += 0.5 * dx * cx;
+        c[b] = 0.5 * dx * cx + 0.5 * dy * cy;
+        up = b;
+        const uint32_t w = local++;
+        parent[base + w] = (int32_t)up;
+        node_pin[base + w] = v;
+        res[base + w] = (float)((double)dy * ry > 0 ? (double)dy * ry : 1e-6);
+        c[w] = 0.5 * dy * cy;
+        node_of[best] = w;
+      } else {                                         /* one straight leg (or none) */
+        const double L_r = dy == 0.f ? (double)dx * rx : (double)dy * ry;
+        const double L_c = dy == 0.f ? (double)dx * cx : (double)dy * cy;
+        const uint32_t w = local++;
+        parent[base + w] = (int32_t)up;
+        node_pin[base + w] = v;
+        res[base + w] = (float)(L_r > 0 ? L_r : 1e-6);
+        c[up] += 0.5 * L_c;
+        c[w] = 0.5 * L_c;
+        node_of[best] = w;
+      }
+      /* Prim key update with the new tree pin */
+      for (uint32_t k = 1; k < m; ++k) {
+        if (in_tree[k]) continue;
+        const float d = mdist(x, y, v, pin[k]);
+        if (d < key[k]) {
+          key[k] = d;
+          par[k] = best;
+        }
+      }
+    }
+    for (uint32_t k = 0; k < local; ++k) cap[base + k] = (float)c[k];
+    nn += local;
+  }
+  rc_ptr[N] = nn;
+  free(pin); free(par); free(node_of); free(in_tree); free(key); free(c);
+  return nn;
+}

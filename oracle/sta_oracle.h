@@ -102,6 +102,16 @@ int orc_paths(const orc_design* d, int mode, uint32_t k, uint32_t nworst, double
               uint32_t cap_pins, uint32_t* n_paths, uint32_t* n_pins, uint32_t* path_ptr, uint32_t* path_pin,
               uint8_t* path_rf, double* path_at, double* path_slack, uint32_t* path_ep);
 
+/* O11: built-in Steiner RC from pin positions (
+ * PAPER.md:178-179): rectilinear MST by Prim from the
+ * driver (fp32 Manhattan distances, ties by smaller pin id), L-embedded edges
+ * (horizontal leg first from the parent), half-split leg caps.  Writes the
+ * sta_set_rc_tree / sta_set_rc_values arrays (rc_ptr[N+1]; parent, node_pin,
+ * res, cap with capacity >= 2 * net_ptr[N] - N) and returns the node count. */
+uint32_t orc_steiner(uint32_t N, const uint32_t* net_ptr, const uint32_t* net_pins, const float* x,
+                     const float* y, double rx, double ry, double cx, double cy, uint32_t* rc_ptr,
+                     int32_t* parent, uint32_t* node_pin, float* res, float* cap);
+
 #ifdef __cplusplus
 }
 #endif

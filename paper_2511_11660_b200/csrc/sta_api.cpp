@@ -226,6 +226,13 @@ struct sta_ctx_s {
   std::vector<u32> fwu_stage_ptr;                // [S + 1] forward units of each stage
   std::vector<u32> fi_p_h, fi_slot_h, ep_int_h;  // path report: term ranges, delay slots, endpoint ids
   Arena path_arena;                              // path report: their device copies + user_of_int
+  Arena steiner_arena;                           // Steiner RC (row f2): static plan + scratch, lazily
+  bool steiner_ready = false;
+  const u32 *st_net_ptr = nullptr, *st_spins = nullptr, *st_warp = nullptr, *st_smem = nullptr, *st_big = nullptr;
+  u32 st_n_warp = 0, st_n_smem = 0, st_n_big = 0, st_max_smem = 0;
+  sta::SteinerArgs st_args{};
+  void* st_scan = nullptr;
+  size_t st_scan_bytes = 0;
   const u32 *fi_p_d = nullptr, *fi_slot_d = nullptr, *ep_int_d = nullptr, *uoi_d = nullptr;
   std::vector<u32> bwu_stage_lo, bwu_stage_hi;   // [S] backward units of each stage (descending list)
 
@@ -1542,6 +1549,50 @@ void publish_rc_pointers(sta_ctx c, CornerState& cs) {
   ck(sta::launch_set_ptrs(cs.dev.rc_vals, cs.rc_res, cs.rc_cap, c->stream), "rc pointer kernel");
 }
 
+// ------------------------------------------------------------- row f2: Steiner RC
+// Static plan of the construction (once per graph): each net's pins as
+// driver then sinks by pin id, the nets by size class, the scratch arrays.
+void steiner_plan(sta_ctx c) {
+  if (c->steiner_ready) return;
+  const u32 N = c->N, NNP = N ? c->net_ptr[N] : 0;
+  std::vector<u32> spins(c->net_pins);
+  std::vector<u32> warp, smem, big;
+  u32 max_smem = 0;
+  const u32 lim = sta::steiner_smem_pins();
+  for (u32 n = 0; n < N; ++n) {
+    const u32 a = c->net_ptr[n], b = c->net_ptr[n + 1], m = b - a;
+    std::sort(spins.begin() + a + 1, spins.begin() + b);
+    if (m >= 2 && m <= 32) warp.push_back(n);
+    else if (m > 32 && m <= lim) { smem.push_back(n); max_smem = std::max(max_smem, m); }
+    else if (m > lim) big.push_back(n);
+  }
+  Arena& g = c->steiner_arena;
+  cudaStream_t s = c->stream;
+  c->st_net_ptr = g.upload(c->net_ptr, s);
+  c->st_spins = g.upload(spins, s);
+  c->st_warp = g.upload(warp, s);
+  c->st_smem = g.upload(smem, s);
+  c->st_big = g.upload(big, s);
+  c->st_n_warp = (u32)warp.size();
+  c->st_n_smem = (u32)smem.size();
+  c->st_n_big = (u32)big.size();
+  c->st_max_smem = max_smem;
+  sta::SteinerArgs& a = c->st_args;
+  a = sta::SteinerArgs{};
+  a.net_ptr = c->st_net_ptr;
+  a.spins = c->st_spins;
+  a.ord = g.alloc<u32>(NNP);
+  a.ppos = g.alloc<u32>(NNP);
+  a.nodeix = g.alloc<u32>(NNP);
+  a.cnt = g.alloc<u32>(N + 1);
+  ck(cudaMemsetAsync(a.cnt, 0, sizeof(u32) * (N + 1), s), "memset");
+  a.scratch = big.empty() ? nullptr : g.alloc<float4>(NNP);
+  c->st_scan_bytes = sta::steiner_scan_bytes(N);
+  c->st_scan = g.alloc<char>(c->st_scan_bytes);
+  ck(cudaStreamSynchronize(s), "steiner plan");
+  c->steiner_ready = true;
+}
+
 }  // namespace
 
 // ====================================================================== ABI
@@ -1640,6 +1691,8 @@ sta_status sta_load_graph(sta_ctx c, const sta_graph_desc* d) {
     c->cons_arena.release();
     c->path_arena.release();
     c->fi_p_d = c->fi_slot_d = c->ep_int_d = c->uoi_d = nullptr;
+    c->steiner_arena.release();
+    c->steiner_ready = false;
     c->P = d->num_pins; c->N = d->num_nets; c->A = d->num_arcs; c->C = d->num_checks; c->T = d->num_tables;
     c->pin_cap = fetch(d->pin_cap, c->P, d->mem, "pin_cap", c->stream);
     c->pin_role = fetch(d->pin_role, c->P, d->mem, "pin_role", c->stream);
@@ -1724,6 +1777,60 @@ sta_status sta_set_library(sta_ctx c, uint32_t corner, sta_mem mem, uint32_t num
     size_kernels(c);
     ck(cudaStreamSynchronize(c->stream), "library upload");
     cs.lib = true;
+  });
+}
+
+
+sta_status sta_build_steiner(sta_ctx c, sta_mem mem, const float* pin_x, const float* pin_y,
+                             const sta_steiner_units* u, uint32_t node_capacity, uint32_t* rc_ptr,
+                             int32_t* parent, uint32_t* node_pin, float* res, float* cap, uint32_t* num_nodes) {
+  return guard(c, [&] {
+    if (!c->has_graph) fail(STA_ERR_ORDER, "sta_build_steiner before sta_load_graph");
+    if (mem != STA_MEM_HOST && mem != STA_MEM_DEVICE) fail(STA_ERR_ARG, "bad sta_mem %d", (int)mem);
+    if (!u) fail(STA_ERR_ARG, "units NULL");
+    for (float v : {u->res_x, u->res_y, u->cap_x, u->cap_y})
+      if (!(v >= 0.f) || !std::isfinite(v)) fail(STA_ERR_ARG, "Steiner units must be finite and >= 0");
+    const u32 N = c->N, P = c->P, NNP = N ? c->net_ptr[N] : 0;
+    const uint64_t need = 2ull * NNP - N;
+    if (node_capacity < need) fail(STA_ERR_ARG, "node_capacity %u < %llu (2 * pins on nets - nets)",
+                                   node_capacity, (unsigned long long)need);
+    if (!rc_ptr || !parent || !node_pin || !res || !cap) fail(STA_ERR_ARG, "output arrays NULL");
+    if (P && (!pin_x || !pin_y)) fail(STA_ERR_ARG, "positions NULL");
+    steiner_plan(c);
+    cudaStream_t s = c->stream;
+    sta::SteinerArgs a = c->st_args;
+    a.rx = u->res_x; a.ry = u->res_y; a.cx = u->cap_x; a.cy = u->cap_y;
+    Arena tmp;
+    struct Free { Arena& t; cudaStream_t s; ~Free() { cudaStreamSynchronize(s); t.release(); } } fr{tmp, s};
+    if (mem == STA_MEM_HOST) {
+      std::vector<float> hx(pin_x, pin_x + P), hy(pin_y, pin_y + P);
+      for (u32 p = 0; p < P; ++p)
+        if (!std::isfinite(hx[p]) || !std::isfinite(hy[p])) fail(STA_ERR_ARG, "pin %u: non-finite position", p);
+      a.x = tmp.upload(hx, s);
+      a.y = tmp.upload(hy, s);
+      a.rc_ptr = tmp.alloc<u32>(N + 1);
+      a.parent = tmp.alloc<int32_t>(need);
+      a.node_pin = tmp.alloc<u32>(need);
+      a.res = tmp.alloc<float>(need);
+      a.cap = tmp.alloc<float>(need);
+    } else {
+      a.x = pin_x; a.y = pin_y;
+      a.rc_ptr = rc_ptr; a.parent = parent; a.node_pin = node_pin; a.res = res; a.cap = cap;
+    }
+    ck(sta::run_steiner(a, N, c->st_warp, c->st_n_warp, c->st_smem, c->st_n_smem, c->st_big, c->st_n_big,
+                        c->st_max_smem, c->st_scan, c->st_scan_bytes, s), "steiner kernels");
+    u32 nn = 0;
+    ck(cudaMemcpyAsync(&nn, a.rc_ptr + N, sizeof(u32), cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "steiner");
+    if (num_nodes) *num_nodes = nn;
+    if (mem == STA_MEM_HOST) {
+      ck(cudaMemcpyAsync(rc_ptr, a.rc_ptr, sizeof(u32) * (N + 1), cudaMemcpyDeviceToHost, s), "D2H");
+      ck(cudaMemcpyAsync(parent, a.parent, sizeof(int32_t) * nn, cudaMemcpyDeviceToHost, s), "D2H");
+      ck(cudaMemcpyAsync(node_pin, a.node_pin, sizeof(u32) * nn, cudaMemcpyDeviceToHost, s), "D2H");
+      ck(cudaMemcpyAsync(res, a.res, sizeof(float) * nn, cudaMemcpyDeviceToHost, s), "D2H");
+      ck(cudaMemcpyAsync(cap, a.cap, sizeof(float) * nn, cudaMemcpyDeviceToHost, s), "D2H");
+      ck(cudaStreamSynchronize(s), "D2H");
+    }
   });
 }
 

@@ -307,4 +307,31 @@ cudaError_t levelize_device(uint32_t P, uint32_t N, uint32_t A, const uint32_t* 
                             uint32_t* fi_ptr, uint32_t* fi_ids, uint32_t* fo_ptr, uint32_t* fo_ids,
                             uint32_t* num_levels, uint32_t* cycle_pin, cudaStream_t s);
 
+// ---- NEXT row f2: built-in Steiner RC from pin positions (sta_steiner.cu)
+struct SteinerArgs {
+  const uint32_t* net_ptr;        // [N + 1] the graph's net CSR offsets
+  const uint32_t* spins;          // [net_ptr[N]] per net: driver, then sinks by pin id
+  const float* x;                 // [P] pin positions
+  const float* y;
+  float rx, ry, cx, cy;           // unit R (kOhm) / C (fF) per distance unit along x / y
+  uint32_t* ord;                  // [net_ptr[N]] Prim order (position in spins of the k-th tree pin)
+  uint32_t* ppos;                 // [net_ptr[N]] Prim position of its tree parent (kNone at the root)
+  uint32_t* nodeix;               // [net_ptr[N]] local node of the k-th tree pin
+  uint32_t* cnt;                  // [N + 1] nodes per net (cnt[N] = 0)
+  float4* scratch;                // [net_ptr[N]] per-pin Prim state of nets too large for shared memory
+  uint32_t* rc_ptr;               // outputs (sta_set_rc_tree / sta_set_rc_values layout)
+  int32_t* parent;
+  uint32_t* node_pin;
+  float* res;
+  float* cap;
+};
+// Enqueue the construction on s.  warp_nets: nets of 2..32 pins; smem_nets:
+// 33..steiner_smem_pins() pins (max_smem_pins = their largest); big_nets:
+// larger.  scan_tmp: steiner_scan_bytes(N) bytes.
+cudaError_t run_steiner(const SteinerArgs& a, uint32_t N, const uint32_t* warp_nets, uint32_t n_warp,
+                        const uint32_t* smem_nets, uint32_t n_smem, const uint32_t* big_nets, uint32_t n_big,
+                        uint32_t max_smem_pins, void* scan_tmp, size_t scan_bytes, cudaStream_t s);
+size_t steiner_scan_bytes(uint32_t N);
+uint32_t steiner_smem_pins();
+
 }  // namespace sta

@@ -29,7 +29,7 @@ EXPORTS = ["sta_create", "sta_destroy", "sta_last_error", "sta_status_string", "
            "sta_set_library", "sta_set_rc_tree", "sta_set_rc_values", "sta_set_constraints",
            "sta_update_timing", "sta_report_slack", "sta_get_timing", "sta_get_rc",
            "sta_get_levels", "sta_get_info", "sta_synchronize", "sta_profile_enable",
-           "sta_profile_read", "sta_report_paths"]
+           "sta_profile_read", "sta_report_paths", "sta_build_steiner"]
 
 
 class StaError(RuntimeError):
@@ -77,6 +77,10 @@ class PathSet(C.Structure):
                 ("path_ep", C.c_void_p)]
 
 
+class SteinerUnits(C.Structure):
+    _fields_ = [("res_x", C.c_float), ("res_y", C.c_float), ("cap_x", C.c_float), ("cap_y", C.c_float)]
+
+
 class Profile(C.Structure):
     _fields_ = [("ms", C.c_double * NUM_PHASES), ("launches", C.c_uint32 * NUM_PHASES),
                 ("updates", C.c_uint32)]
@@ -114,6 +118,8 @@ def lib():
             "sta_profile_enable": (i32, [vp, i32]),
             "sta_profile_read": (i32, [vp, C.POINTER(Profile)]),
             "sta_report_paths": (i32, [vp, u32, C.POINTER(PathQuery), C.POINTER(PathSet), i32]),
+            "sta_build_steiner": (i32, [vp, i32, vp, vp, C.POINTER(SteinerUnits), u32, vp, vp, vp, vp, vp,
+                                        C.POINTER(u32)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -189,6 +195,7 @@ class Context:
         self.num_corners = num_corners
         self.num_pins = 0
         self.num_nets = 0
+        self._net_pins_total = 0
 
     def close(self):
         if getattr(self, "h", None):
@@ -235,6 +242,7 @@ class Context:
         d.mem = a.kind
         self._check(self._L.sta_load_graph(self.h, C.byref(d)))
         self.num_pins, self.num_nets = d.num_pins, d.num_nets
+        self._net_pins_total = len(net_pins)
 
     def set_library(self, corner: int, n1, n2, off, data):
         a = _Args(self.device)
@@ -271,6 +279,35 @@ class Context:
         k.po_load_ff = a.ptr(po_load, np.float32)
         k.mem = a.kind
         self._check(self._L.sta_set_constraints(self.h, C.byref(k)))
+
+    def build_steiner(self, x, y, res_x: float, res_y: float, cap_x: float, cap_y: float,
+                      net_pins_total: Optional[int] = None):
+        """Steiner RC from pin positions (sta_build_steiner).  Host positions
+        -> numpy arrays; torch CUDA positions -> torch CUDA tensors (device
+        outputs, ready for set_rc_tree / set_rc_values).  Returns
+        (rc_ptr, parent, node_pin, res, cap) trimmed to the node count."""
+        N = self.num_nets
+        nnp = int(net_pins_total) if net_pins_total is not None else self._net_pins_total
+        capn = max(2 * nnp - N, 1)
+        u = SteinerUnits(float(res_x), float(res_y), float(cap_x), float(cap_y))
+        nn = C.c_uint32()
+        a = _Args(self.device)
+        px, py = a.ptr(x, np.float32), a.ptr(y, np.float32)
+        if a.kind == STA_MEM_DEVICE:
+            import torch
+            dev = x.device
+            rc_ptr = torch.empty(N + 1, dtype=torch.int32, device=dev)
+            outs = [torch.empty(capn, dtype=t, device=dev)
+                    for t in (torch.int32, torch.int32, torch.float32, torch.float32)]
+            ptrs = [rc_ptr.data_ptr()] + [o.data_ptr() for o in outs]
+        else:
+            rc_ptr = np.zeros(N + 1, np.uint32)
+            outs = [np.zeros(capn, np.int32), np.zeros(capn, np.uint32), np.zeros(capn, np.float32),
+                    np.zeros(capn, np.float32)]
+            ptrs = [rc_ptr.ctypes.data] + [o.ctypes.data for o in outs]
+        self._check(self._L.sta_build_steiner(self.h, a.kind, px, py, C.byref(u), capn, *ptrs, C.byref(nn)))
+        n = nn.value
+        return (rc_ptr,) + tuple(o[:n] for o in outs)
 
     # ------------------------------------------------------------ update
     def update_timing(self):

@@ -14,7 +14,7 @@ assert a in s, a
 open('oracle/sta_oracle.c', 'w').write(s.replace(a, b, 1))
 PY
   rm -f oracle/liboracle.so
-  if timeout 600 python -m pytest tests/test_oracle_lut_rc.py tests/test_oracle_propagation.py -q -x >/dev/null 2>&1; then
+  if timeout 600 python -m pytest tests/test_oracle_lut_rc.py tests/test_oracle_propagation.py tests/test_oracle_steiner.py -q -x >/dev/null 2>&1; then
     echo "NOT CAUGHT: $1"; fail=1; return 1
   else echo "caught: $1"; fi
 }
@@ -47,4 +47,13 @@ mut 'double ld = drv_load[v];' 'double ld = drv_load[u];'
 mut 'if (wh < 0) tns_h += wh;' 'if (wh < 0) tns_h += ws;'
 mut 'uint32_t j = seg(y, n2, c);' 'uint32_t j = seg(y, n2, s);'
 mut 'slew[4 * p + q] = d->pi_slew[4 * k + q];' 'slew[4 * p + q] = d->pi_slew[4 * k + (q ^ 1)];'
+# Steiner RC (O11, row f2)
+mut '(key[k] == key[best] && pin[k] < pin[best])) best = k;' '(key[k] == key[best] && pin[k] > pin[best])) best = k;'
+mut 'if (d < key[k]) {' 'if (d <= key[k]) {'
+mut 'const float d = mdist(x, y, v, pin[k]);' 'const float d = mdist(x, y, pin[0], pin[k]);'
+mut 'c[up] += 0.5 * dx * cx;' 'c[up] += dx * cx;'
+mut 'c[b] = 0.5 * dx * cx + 0.5 * dy * cy;' 'c[b] = 0.5 * dx * cy + 0.5 * dy * cx;'
+mut 'res[base + b] = (float)((double)dx * rx > 0 ? (double)dx * rx : 1e-6);' 'res[base + b] = (float)((double)dx * ry > 0 ? (double)dx * ry : 1e-6);'
+mut 'res[base + w] = (float)(L_r > 0 ? L_r : 1e-6);' 'res[base + w] = (float)L_r;'
+mut 'const double L_r = dy == 0.f ? (double)dx * rx : (double)dy * ry;' 'const double L_r = dx == 0.f ? (double)dx * rx : (double)dy * ry;'
 exit $fail

@@ -13,3 +13,4 @@ from .design import (  # noqa: F401
 )
 from .hand import c17, h1_chain, h3_reg2reg, h4_seeds  # noqa: F401
 from .recipe import generate, CONFIGS, config_design, corner_scales  # noqa: F401
+from .place import placement, UNITS as STEINER_UNITS  # noqa: F401
