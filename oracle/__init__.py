@@ -48,6 +48,7 @@ class _Design(C.Structure):
         ("pi_slew", C.c_void_p),
         ("n_po", C.c_uint32), ("po_pin", C.c_void_p), ("po_out_max", C.c_void_p),
         ("po_out_min", C.c_void_p), ("po_load", C.c_void_p),
+        ("net_model", C.c_int32), ("arnoldi_q", C.c_uint32),
     ]
 
 
@@ -67,6 +68,11 @@ def lib():
         _lib.orc_paths.restype = C.c_int
         _lib.orc_paths.argtypes = [C.c_void_p, C.c_int, C.c_uint32, C.c_uint32, C.c_double, C.c_uint32,
                                    C.c_uint32] + [C.c_void_p] * 8
+        _lib.orc_arnoldi_reduce.restype = C.c_int
+        _lib.orc_arnoldi_reduce.argtypes = [C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32,
+                                            C.c_void_p, C.c_void_p]
+        _lib.orc_arnoldi_delay.restype = C.c_double
+        _lib.orc_arnoldi_delay.argtypes = [C.c_uint32, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p]
         _lib.orc_steiner.restype = C.c_uint32
         _lib.orc_steiner.argtypes = [C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                      C.c_double, C.c_double, C.c_double, C.c_double] + [C.c_void_p] * 5
@@ -80,7 +86,7 @@ def _p(a):
 class _Marshal:
     """Holds contiguous copies alive while the C call runs."""
 
-    def __init__(self, d, corner: int = 0):
+    def __init__(self, d, corner: int = 0, net_model: str = "elmore", q: int = 4):
         keep = []
 
         def arr(x, dt):
@@ -128,6 +134,8 @@ class _Marshal:
         s.po_out_max = _p(arr(cons.po_out_max, np.float32))
         s.po_out_min = _p(arr(cons.po_out_min, np.float32))
         s.po_load = _p(arr(cons.po_load, np.float32))
+        s.net_model = {"elmore": 0, "arnoldi": 1}[net_model]
+        s.arnoldi_q = int(q)
         self.s = s
         self.keep = keep
 
@@ -164,10 +172,11 @@ def rc(d, corner: int = 0):
     return load[:d.num_nets], elm[:d.num_pins]
 
 
-def update(d, corner: int = 0, want_all: bool = True):
+def update(d, corner: int = 0, want_all: bool = True, net_model: str = "elmore", q: int = 4):
     """Full update for one corner -> dict(at, slew, rat, slack [P,4] f64,
-    res[4] = (WNS_setup, TNS_setup, WNS_hold, TNS_hold), ep_pin, ep_ws)."""
-    m = _Marshal(d, corner)
+    res[4] = (WNS_setup, TNS_setup, WNS_hold, TNS_hold), ep_pin, ep_ws).
+    net_model "arnoldi": net arcs by the O12 reduced model of order q."""
+    m = _Marshal(d, corner, net_model, q)
     P = d.num_pins
     at = np.zeros((max(P, 1), 4))
     slew = np.zeros((max(P, 1), 4)) if want_all else None
@@ -255,3 +264,25 @@ def steiner(net_ptr, net_pins, x, y, res_x, res_y, cap_x, cap_y):
     n = lib().orc_steiner(N, _p(net_ptr), _p(net_pins), _p(x), _p(y), *u, _p(rc_ptr), _p(parent),
                           _p(node_pin), _p(res), _p(cap))
     return rc_ptr, parent[:n], node_pin[:n], res[:n], cap[:n]
+
+
+def arnoldi_reduce(parent, res, cap, q: int = 4):
+    """O12 reduced model of one net's RC tree -> (order, lam[order],
+    resid[m][q]); order -1: unstable."""
+    parent = np.ascontiguousarray(parent, np.int32)
+    res = np.ascontiguousarray(res, np.float32)
+    cap = np.ascontiguousarray(cap, np.float64)
+    m = parent.size
+    lam = np.zeros(max(q, 1), np.float64)
+    resid = np.zeros((max(m, 1), max(q, 1)), np.float64)
+    qq = lib().orc_arnoldi_reduce(m, _p(parent), _p(res), _p(cap), int(q), _p(lam), _p(resid))
+    return qq, lam[:max(qq, 0)], resid[:m]
+
+
+def arnoldi_delay(lam, k, slew):
+    """O12 ramp response of a reduced model -> (delay, out_slew)."""
+    lam = np.ascontiguousarray(lam, np.float64)
+    k = np.ascontiguousarray(k, np.float64)
+    os_ = np.zeros(1, np.float64)
+    dl = lib().orc_arnoldi_delay(int(lam.size), _p(lam), _p(k), float(slew), _p(os_))
+    return dl, float(os_[0])

@@ -209,6 +209,173 @@ void orc_rc(const orc_design* d, double* load, double* elm) {
   free(cd); free(el); free(po_ld);
 }
 
+
+/* --------------------------------------------------- O12: Arnoldi net model */
+/* "Per-net Lanczos on trees (q = 4) with O(n) tree
+ * solves; delay and slew from the ramp response" ("an
+ * Arnoldi-based reduced-order model").  The driver node 0 is
+ * driven by the ideal source; the unknowns are nodes 1..m-1 with
+ * C v' + G v = b u, G the conductance Laplacian.  A = G^-1 C is self-adjoint
+ * in <x, y> = sum_i C_i x_i y_i and G^-1 b = 1, so V(s)/U(s) = (I + s A)^-1 1.
+ * A x is one tree solve (the RC-tree moment recursion): subtree sums of
+ * C_j x_j, then root-path sums of R_a times them. */
+static void tree_apply(uint32_t m, const int32_t* parent, const float* res, const double* cap, const double* x,
+                       double* y, double* t) {
+  t[0] = 0.0;
+  for (uint32_t i = 1; i < m; i++) t[i] = cap[i] * x[i];
+  for (uint32_t i = m - 1; i >= 1; i--) t[parent[i]] += t[i];
+  y[0] = 0.0;
+  for (uint32_t i = 1; i < m; i++) y[i] = y[parent[i]] + (double)res[i] * t[i];
+}
+
+static double cdot(uint32_t m, const double* cap, const double* x, const double* y) {
+  double s = 0.0;
+  for (uint32_t i = 1; i < m; i++) s += cap[i] * x[i] * y[i];
+  return s;
+}
+
+/* cyclic Jacobi eigen-decomposition of the symmetric n x n matrix a (row
+ * major, destroyed): eigenvalues in w, eigenvectors in the columns of v */
+static void jacobi_eig(uint32_t n, double* a, double* w, double* v) {
+  for (uint32_t i = 0; i < n; i++)
+    for (uint32_t j = 0; j < n; j++) v[i * n + j] = i == j;
+  for (int sweep = 0; sweep < 100; sweep++) {
+    double off = 0.0, nrm = 0.0;
+    for (uint32_t i = 0; i < n; i++)
+      for (uint32_t j = 0; j < n; j++) {
+        nrm += a[i * n + j] * a[i * n + j];
+        if (i != j) off += a[i * n + j] * a[i * n + j];
+      }
+    if (off <= 1e-30 * nrm || off == 0.0) break;
+    for (uint32_t p = 0; p < n; p++)
+      for (uint32_t q = p + 1; q < n; q++) {
+        double apq = a[p * n + q];
+        if (apq == 0.0) continue;
+        double theta = (a[q * n + q] - a[p * n + p]) / (2.0 * apq);
+        double tt = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        double c = 1.0 / sqrt(tt * tt + 1.0), sn = tt * c;
+        for (uint32_t k = 0; k < n; k++) {          /* rotate rows / columns p, q */
+          double akp = a[k * n + p], akq = a[k * n + q];
+          a[k * n + p] = c * akp - sn * akq;
+          a[k * n + q] = sn * akp + c * akq;
+        }
+        for (uint32_t k = 0; k < n; k++) {
+          double apk = a[p * n + k], aqk = a[q * n + k];
+          a[p * n + k] = c * apk - sn * aqk;
+          a[q * n + k] = sn * apk + c * aqk;
+        }
+        for (uint32_t k = 0; k < n; k++) {
+          double vkp = v[k * n + p], vkq = v[k * n + q];
+          v[k * n + p] = c * vkp - sn * vkq;
+          v[k * n + q] = sn * vkp + c * vkq;
+        }
+      }
+  }
+  for (uint32_t i = 0; i < n; i++) w[i] = a[i * n + i];
+}
+
+int orc_arnoldi_reduce(uint32_t m, const int32_t* parent, const float* res, const double* cap, uint32_t q,
+                       double* lam, double* resid) {
+  double ctot = 0.0;
+  for (uint32_t i = 1; i < m; i++) ctot += cap[i];
+  if (q < 1) q = 1;
+  if (m <= 1 || ctot <= 0.0) {               /* no dynamics: the output follows the input */
+    lam[0] = 0.0;
+    for (uint32_t i = 0; i < m; i++) { resid[(size_t)i * q] = 1.0; for (uint32_t k = 1; k < q; k++) resid[(size_t)i * q + k] = 0.0; }
+    return 1;
+  }
+  double* V = calloc((size_t)(q + 1) * m, sizeof(double));   /* Lanczos vectors, V[j*m + i] */
+  double* w = malloc(sizeof(double) * m);
+  double* t = malloc(sizeof(double) * m);
+  double alpha[16], beta[16];
+  /* step 1: v_1 = 1 / ||1||_C */
+  for (uint32_t i = 1; i < m; i++) V[i] = 1.0 / sqrt(ctot);
+  uint32_t qq = 0;
+  for (uint32_t j = 0; j < q; j++) {
+    /* step 2: w = A v_j - beta_{j-1} v_{j-1}; alpha_j = <w, v_j>; w -= alpha_j v_j */
+    tree_apply(m, parent, res, cap, V + (size_t)j * m, w, t);
+    if (j > 0) for (uint32_t i = 1; i < m; i++) w[i] -= beta[j - 1] * V[(size_t)(j - 1) * m + i];
+    alpha[j] = cdot(m, cap, w, V + (size_t)j * m);
+    for (uint32_t i = 1; i < m; i++) w[i] -= alpha[j] * V[(size_t)j * m + i];
+    /* full reorthogonalisation against v_1 .. v_j (twice) */
+    for (int pass = 0; pass < 2; pass++)
+      for (uint32_t k = 0; k <= j; k++) {
+        double c = cdot(m, cap, w, V + (size_t)k * m);
+        for (uint32_t i = 1; i < m; i++) w[i] -= c * V[(size_t)k * m + i];
+      }
+    qq = j + 1;
+    beta[j] = sqrt(cdot(m, cap, w, w));
+    /* step 3: breakdown (the Krylov space is exhausted) truncates the order */
+    if (j + 1 == q || !(beta[j] > 1e-10 * fabs(alpha[j]))) break;
+    for (uint32_t i = 1; i < m; i++) V[(size_t)(j + 1) * m + i] = w[i] / beta[j];
+  }
+  /* step 4: T = tridiag(beta, alpha, beta) = Q diag(lam) Q^T */
+  double T[256], Qm[256], ev[16];
+  for (uint32_t a = 0; a < qq; a++)
+    for (uint32_t b = 0; b < qq; b++)
+      T[a * qq + b] = a == b ? alpha[a] : (a + 1 == b ? beta[a] : (b + 1 == a ? beta[b] : 0.0));
+  jacobi_eig(qq, T, ev, Qm);
+  int stable = 1;
+  double lmax = 0.0;
+  for (uint32_t k = 0; k < qq; k++) if (ev[k] > lmax) lmax = ev[k];
+  for (uint32_t k = 0; k < qq; k++) {
+    if (ev[k] < -1e-9 * lmax) stable = 0;     /* a positive pole */
+    lam[k] = ev[k] < 0.0 ? 0.0 : ev[k];
+  }
+  /* step 5: residues H_i(s) = sqrt(Ctot) e_i^T V Q (I + s Lam)^-1 Q^T e_1 */
+  for (uint32_t i = 0; i < m; i++)
+    for (uint32_t k = 0; k < q; k++) {
+      double r = 0.0;
+      if (k < qq) {
+        if (i == 0) r = k == 0 ? 1.0 : 0.0;    /* the driven root follows the input */
+        else {
+          for (uint32_t j = 0; j < qq; j++) r += V[(size_t)j * m + i] * Qm[j * qq + k];
+          r *= sqrt(ctot) * Qm[0 * qq + k];
+        }
+      }
+      resid[(size_t)i * q + k] = r;
+    }
+  free(V); free(w); free(t);
+  return stable ? (int)qq : -1;
+}
+
+/* response of one reduced term 1 / (1 + s lam) to the saturated ramp of
+ * duration D (0: a step) at time t */
+static double ramp_term(double lam, double D, double t) {
+  if (t <= 0.0) return 0.0;
+  if (D <= 0.0) return lam > 0.0 ? 1.0 - exp(-t / lam) : 1.0;
+  double r1 = lam > 0.0 ? t - lam * (1.0 - exp(-t / lam)) : t;
+  double r2 = 0.0;
+  if (t > D) r2 = lam > 0.0 ? (t - D) - lam * (1.0 - exp(-(t - D) / lam)) : t - D;
+  return (r1 - r2) / D;
+}
+
+static double ramp_resp(uint32_t qq, const double* lam, const double* k, double D, double t) {
+  double y = 0.0;
+  for (uint32_t j = 0; j < qq; j++) y += k[j] * ramp_term(lam[j], D, t);
+  return y;
+}
+
+/* first time the response reaches theta, by bisection to 1e-6 ps */
+static double crossing(uint32_t qq, const double* lam, const double* k, double D, double theta) {
+  double lmax = 0.0;
+  for (uint32_t j = 0; j < qq; j++) if (lam[j] > lmax) lmax = lam[j];
+  double lo = 0.0, hi = D + 50.0 * lmax + 1e-3;
+  for (int g = 0; g < 60 && ramp_resp(qq, lam, k, D, hi) < theta; g++) hi *= 2.0;
+  for (int it = 0; it < 200 && hi - lo > 1e-6; it++) {
+    double mid = 0.5 * (lo + hi);
+    if (ramp_resp(qq, lam, k, D, mid) >= theta) hi = mid; else lo = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+
+double orc_arnoldi_delay(uint32_t qq, const double* lam, const double* k, double slew, double* out_slew) {
+  double D = slew / 0.6;                     /* 20-80 slew of a linear ramp is 0.6 D (reading A1) */
+  double t50 = crossing(qq, lam, k, D, 0.5);
+  if (out_slew) *out_slew = crossing(qq, lam, k, D, 0.8) - crossing(qq, lam, k, D, 0.2);
+  return t50 - 0.5 * D;
+}
+
 /* ------------------------------------------------------- sense pairs (O5) */
 /* SPEC.md:383 and SURVEY.md §8(c) O5: which (input edge -> output edge) pairs
  * an arc of a given sense propagates. */
@@ -290,18 +457,59 @@ static int run_update(const orc_design* d, double* at, double* slew, double* rat
   double* own_rat = rat ? NULL : malloc(sizeof(double) * 4 * (size_t)(P + 1));
   double* own_slack = slack ? NULL : malloc(sizeof(double) * 4 * (size_t)(P + 1));
   uint8_t* is_ep = calloc(P + 1, 1);
+  /* O12 (net_model 1): per sink pin its net's reduced model: order (0: Elmore
+   * fallback or lumped net), time constants, residues; and the per-component
+   * net-arc delays the forward used (the backward reuses them) */
+  const int arn = d->net_model == 1;
+  const uint32_t aq = arn ? (d->arnoldi_q ? d->arnoldi_q : 4) : 1;
+  uint32_t* a_qq = arn ? calloc(P + 1, sizeof(uint32_t)) : NULL;
+  double* a_lam = arn ? calloc((size_t)(P + 1) * aq, sizeof(double)) : NULL;
+  double* a_res = arn ? calloc((size_t)(P + 1) * aq, sizeof(double)) : NULL;
+  double* ndly = arn ? calloc(4 * (size_t)(P + 1), sizeof(double)) : NULL;
   int st = 0;
   if (!slew) slew = own_slew;
   if (!rat) rat = own_rat;
   if (!slack) slack = own_slack;
-  if (!level || !order || !load || !elm || !drv_load || !dly || !slew || !rat || !slack || !is_ep) {
+  if (!level || !order || !load || !elm || !drv_load || !dly || !slew || !rat || !slack || !is_ep ||
+      (arn && (!a_qq || !a_lam || !a_res || !ndly))) {
     st = 2; goto done;
   }
+  if (arn && pq) { st = 4; goto done; }     /* path reports: Elmore model only (A7) */
   if (kahn(d, &g, level, order)) { st = 1; goto done; }
 
   /* O3 */
   orc_rc(d, load, elm);
   for (uint32_t n = 0; n < d->num_nets; n++) drv_load[d->net_pins[d->net_ptr[n]]] = load[n];
+  if (arn) {                                 /* O12: one reduced model per net with RC nodes */
+    double* po_ld = calloc(P + 1, sizeof(double));
+    for (uint32_t k = 0; k < d->n_po; k++) po_ld[d->po_pin[k]] += d->po_load[k];
+    uint32_t maxn = 1;
+    for (uint32_t n = 0; n < d->num_nets; n++)
+      if (d->rc_ptr[n + 1] - d->rc_ptr[n] > maxn) maxn = d->rc_ptr[n + 1] - d->rc_ptr[n];
+    double* cap = malloc(sizeof(double) * maxn);
+    double* lam = malloc(sizeof(double) * aq);
+    double* rsd = malloc(sizeof(double) * (size_t)maxn * aq);
+    for (uint32_t n = 0; n < d->num_nets; n++) {
+      uint32_t b = d->rc_ptr[n], m = d->rc_ptr[n + 1] - b;
+      if (m == 0) continue;                  /* lumped: zero wire delay, the Elmore path */
+      for (uint32_t i = 0; i < m; i++) {
+        uint32_t p = d->rc_node_pin[b + i];
+        cap[i] = d->rc_cap[b + i] + (p != ORC_NO_PIN ? d->pin_cap[p] + po_ld[p] : 0.0);
+      }
+      int qq = orc_arnoldi_reduce(m, d->rc_parent + b, d->rc_res + b, cap, aq, lam, rsd);
+      if (qq < 0) continue;                  /* unstable: Elmore fallback */
+      for (uint32_t i = 1; i < m; i++) {
+        uint32_t p = d->rc_node_pin[b + i];
+        if (p == ORC_NO_PIN) continue;
+        a_qq[p] = (uint32_t)qq;
+        for (uint32_t k = 0; k < aq; k++) {
+          a_lam[(size_t)p * aq + k] = k < (uint32_t)qq ? lam[k] : 0.0;
+          a_res[(size_t)p * aq + k] = rsd[(size_t)i * aq + k];
+        }
+      }
+    }
+    free(cap); free(lam); free(rsd); free(po_ld);
+  }
 
   /* O4 seeds: everything undefined, then PIs and ideal-clock CK pins. */
   for (uint32_t p = 0; p < P; p++) {
@@ -336,7 +544,14 @@ static int run_update(const orc_design* d, double* at, double* slew, double* rat
           double s_in = slew[4 * u + Q(el, irf)];
           for (int orf = 0; orf < 2; orf++) {
             double ca, cs;
-            if (e < g.En) {                /* net arc: positive unate, Elmore */
+            if (e < g.En && arn && a_qq[v]) {   /* net arc, Arnoldi (O12) */
+              if (irf != orf) continue;
+              double os;
+              double dn = orc_arnoldi_delay(a_qq[v], a_lam + (size_t)v * aq, a_res + (size_t)v * aq, s_in, &os);
+              ndly[4 * (size_t)v + Q(el, orf)] = dn;
+              ca = a_in + dn;
+              cs = os;
+            } else if (e < g.En) {         /* net arc: positive unate, Elmore */
               if (irf != orf) continue;
               double imp = LN9 * elm[v];   /* SPEC.md:418 PERI */
               ca = a_in + elm[v];
@@ -412,7 +627,7 @@ static int run_update(const orc_design* d, double* at, double* slew, double* rat
           if (!isfinite(at[4 * u + Q(el, irf)])) continue;   /* only arcs O5 used */
           for (int orf = 0; orf < 2; orf++) {
             double dd;
-            if (e < g.En) { if (irf != orf) continue; dd = elm[v]; }
+            if (e < g.En) { if (irf != orf) continue; dd = arn && a_qq[v] ? ndly[4 * (size_t)v + Q(el, orf)] : elm[v]; }
             else {
               uint32_t a = g.cell[e];
               if (!sense_allows(d->arc_sense[a], irf, orf)) continue;
@@ -460,6 +675,7 @@ done:
   free_arcs(&g);
   free(level); free(order); free(load); free(elm); free(drv_load); free(dly);
   free(own_slew); free(own_rat); free(own_slack); free(is_ep);
+  free(a_qq); free(a_lam); free(a_res); free(ndly);
   return st;
 }
 

@@ -68,6 +68,10 @@ typedef struct {
   const float* po_out_max;   /* [n_po][2] rise, fall */
   const float* po_out_min;   /* [n_po][2] */
   const float* po_load;      /* [n_po] fF */
+  /* net-arc delay model: 0 Elmore (O3), 1 Arnoldi
+   * reduced-order model of order arnoldi_q (O12) */
+  int32_t net_model;
+  uint32_t arnoldi_q;
 } orc_design;
 
 /* O6: NLDM bilinear lookup, fp64.  `tab` points at
@@ -111,6 +115,24 @@ int orc_paths(const orc_design* d, int mode, uint32_t k, uint32_t nworst, double
 uint32_t orc_steiner(uint32_t N, const uint32_t* net_ptr, const uint32_t* net_pins, const float* x,
                      const float* y, double rx, double ry, double cx, double cy, uint32_t* rc_ptr,
                      int32_t* parent, uint32_t* node_pin, float* res, float* cap);
+
+/* O12: Arnoldi reduced-order net model (PAPER.md:182-183,
+ * 209; readings A1-A7 in DESIGN.md).
+ * orc_arnoldi_reduce: one net's RC tree (m nodes, node 0 the driven root,
+ * parent[i] < i local, res[i] of the edge parent -> i, cap[i] the node's total
+ * grounded cap incl. pin caps): Lanczos in the C-inner product on A = G^-1 C
+ * from the start vector G^-1 b = 1, each A application one O(m) tree solve,
+ * full reorthogonalisation, order <= q (breakdown truncates).  Writes the
+ * reduced time constants lam[k] = -1/pole_k (>= 0) and per-node residues
+ * resid[i*q + k] (H_i(s) = sum_k resid / (1 + s lam_k), sum_k resid = 1).
+ * Returns the achieved order, or -1 if the model is unstable (a negative
+ * time constant: callers fall back to Elmore).
+ * orc_arnoldi_delay: the response of the reduced model to a saturated ramp
+ * of 20-80 slew `slew` (duration slew / 0.6): delay = t50(out) - t50(in) and
+ * *out_slew = t80 - t20 of the output, crossings by bisection to 1e-6 ps. */
+int orc_arnoldi_reduce(uint32_t m, const int32_t* parent, const float* res, const double* cap, uint32_t q,
+                       double* lam, double* resid);
+double orc_arnoldi_delay(uint32_t qq, const double* lam, const double* k, double slew, double* out_slew);
 
 #ifdef __cplusplus
 }

@@ -14,7 +14,7 @@ assert a in s, a
 open('oracle/sta_oracle.c', 'w').write(s.replace(a, b, 1))
 PY
   rm -f oracle/liboracle.so
-  if timeout 600 python -m pytest tests/test_oracle_lut_rc.py tests/test_oracle_propagation.py tests/test_oracle_steiner.py -q -x >/dev/null 2>&1; then
+  if timeout 600 python -m pytest tests/test_oracle_lut_rc.py tests/test_oracle_propagation.py tests/test_oracle_steiner.py tests/test_oracle_arnoldi.py -q -x >/dev/null 2>&1; then
     echo "NOT CAUGHT: $1"; fail=1; return 1
   else echo "caught: $1"; fi
 }
@@ -56,4 +56,12 @@ mut 'c[b] = 0.5 * dx * cx + 0.5 * dy * cy;' 'c[b] = 0.5 * dx * cy + 0.5 * dy * c
 mut 'res[base + b] = (float)((double)dx * rx > 0 ? (double)dx * rx : 1e-6);' 'res[base + b] = (float)((double)dx * ry > 0 ? (double)dx * ry : 1e-6);'
 mut 'res[base + w] = (float)(L_r > 0 ? L_r : 1e-6);' 'res[base + w] = (float)L_r;'
 mut 'const double L_r = dy == 0.f ? (double)dx * rx : (double)dy * ry;' 'const double L_r = dx == 0.f ? (double)dx * rx : (double)dy * ry;'
+# Arnoldi net model (O12, row f1)
+mut 'for (uint32_t i = 1; i < m; i++) y[i] = y[parent[i]] + (double)res[i] * t[i];' 'for (uint32_t i = 1; i < m; i++) y[i] = y[parent[i]] + (double)res[i] * cap[i];'
+mut 'double D = slew / 0.6;' 'double D = slew / 0.8;'
+mut 'r *= sqrt(ctot) * Qm[0 * qq + k];' 'r *= sqrt(ctot);'
+mut 'dd = arn && a_qq[v] ? ndly[4 * (size_t)v + Q(el, orf)] : elm[v];' 'dd = elm[v];'
+mut 'cs = os;' 'cs = s_in;'
+mut 'if (t > D) r2 = lam > 0.0 ? (t - D) - lam * (1.0 - exp(-(t - D) / lam)) : t - D;' ''
+mut 'return t50 - 0.5 * D;' 'return t50;'
 exit $fail
