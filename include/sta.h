@@ -202,6 +202,22 @@ STA_API sta_status sta_build_steiner(sta_ctx ctx, sta_mem mem, const float* pin_
                              int32_t* parent, uint32_t* node_pin, float* res, float* cap,
                              uint32_t* num_nodes);
 
+/* Net-arc delay model of the next updates (
+ * "The Elmore model is the fastest yet not accurate
+ * enough in late design stages, where Arnoldi might be a better option";
+ * SPEC.md:398-418).  STA_NET_ELMORE (default): Elmore delay, PERI slew.
+ * STA_NET_ARNOLDI: per net and corner a Lanczos (Arnoldi on the symmetric
+ * RC-tree pencil) reduced-order model of order q (1..4) is built on the
+ * device every update; a sink's delay and slew are the response of that
+ * model to a saturated ramp of the driver's 20-80 slew (delay = 50% crossing
+ * minus the input's, slew = 20-80 crossing difference), evaluated wherever
+ * the sink's arrival is needed; an unstable model falls back to Elmore for
+ * its net.  Readings A1-A7 in DESIGN.md.  The top-k path report is Elmore
+ * only (sta_report_paths returns STA_ERR_ORDER under Arnoldi).
+ * Errors: STA_ERR_ARG (model, q). */
+typedef enum { STA_NET_ELMORE = 0, STA_NET_ARNOLDI = 1 } sta_net_model;
+STA_API sta_status sta_set_net_model(sta_ctx ctx, sta_net_model model, uint32_t q);
+
 /* Per-corner RC values: res[i] = resistance of the edge parent -> i (kOhm,
  * ignored at node 0), cap[i] = wire capacitance to ground at node i (fF);
  * both num_nodes long, >= 0 and finite.  HOST: copied into ctx-owned device

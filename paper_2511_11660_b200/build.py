@@ -11,8 +11,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libsta.so")
-SOURCES = ["sta_api.cpp", "sta_kernels.cu", "sta_levelize.cu", "sta_steiner.cu"]
-HEADERS = ["sta_internal.h", os.path.join("..", "..", "include", "sta.h")]
+SOURCES = ["sta_api.cpp", "sta_kernels.cu", "sta_levelize.cu", "sta_steiner.cu", "sta_arnoldi.cu"]
+HEADERS = ["sta_internal.h", "sta_arnoldi.cuh", os.path.join("..", "..", "include", "sta.h")]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",

@@ -226,6 +226,9 @@ struct sta_ctx_s {
   std::vector<u32> fwu_stage_ptr;                // [S + 1] forward units of each stage
   std::vector<u32> fi_p_h, fi_slot_h, ep_int_h;  // path report: term ranges, delay slots, endpoint ids
   Arena path_arena;                              // path report: their device copies + user_of_int
+  int net_model = 0;                             // row f1: 0 Elmore, 1 Arnoldi (order arn_q)
+  u32 arn_q = 4;
+  Arena arn_arena;                               // Arnoldi layout (prepare)
   Arena steiner_arena;                           // Steiner RC (row f2): static plan + scratch, lazily
   bool steiner_ready = false;
   const u32 *st_net_ptr = nullptr, *st_spins = nullptr, *st_warp = nullptr, *st_smem = nullptr, *st_big = nullptr;
@@ -1291,6 +1294,41 @@ void prepare(sta_ctx c) {
     }
     t.tc_node = g.upload(tcn, s);
   }
+  // row f1: the Arnoldi layout (internal nodes: each net contiguous in DFS
+  // preorder) -- parents / subtree ends from the caller's tree
+  c->arn_arena.release();
+  t.net_model = (u32)c->net_model;
+  t.arn_q = c->arn_q;
+  t.n_arn_nets = 0;
+  t.n_rc_nodes = c->n_rc;
+  if (c->net_model == 1) {
+    std::vector<u32> inv(c->n_rc);
+    for (u32 x = 0; x < c->n_rc; ++x) inv[c->node_user[x]] = x;
+    std::vector<uint4> an(c->n_rc), nets;
+    std::vector<u32> sz;
+    for (u32 n = 0; n < c->N; ++n) {
+      const u32 drv = c->drv_of_net[n];
+      if (drv == kNone) continue;
+      const u32 b = c->rc_ptr[n], m = c->rc_ptr[n + 1] - b;
+      if (!m) {
+        nets.push_back(make_uint4(0, 0, drv, 0));
+        continue;
+      }
+      sz.assign(m, 1);
+      for (u32 i = m - 1; i >= 1; --i) sz[(u32)c->rc_parent[b + i]] += sz[i];
+      for (u32 i = 0; i < m; ++i) {
+        const u32 x = inv[b + i];
+        const u32 tag = c->node_tag_h[x];
+        an[x] = make_uint4(b + i, i ? inv[b + (u32)c->rc_parent[b + i]] : kNone, x + sz[i],
+                           (i && !(tag & 0x80000000u)) ? tag : kNone);
+      }
+      nets.push_back(make_uint4(inv[b], m, drv, 0));
+    }
+    t.n_arn_nets = (u32)nets.size();
+    t.arn_nets = c->arn_arena.upload(nets, s);
+    t.arn_node = c->arn_arena.upload(an, s);
+    t.arn_scap = c->arn_arena.upload(scap, s);
+  }
 
   // per-corner state buffers
   for (CornerState& cs : c->corners) {
@@ -1325,6 +1363,16 @@ void prepare(sta_ctx c) {
       ck(cudaMemsetAsync(d.trace, 0, n * sizeof(unsigned long long), s), "memset");
     }
     ck(cudaMemsetAsync(d.load, 0, sizeof(float) * std::max<u32>(c->NP, 1), s), "memset");
+    d.arn_lam = nullptr;
+    d.arn_res = nullptr;
+    d.arn_scr = nullptr;
+    if (c->net_model == 1) {
+      d.arn_lam = a.alloc<float4>(c->NP);
+      d.arn_res = a.alloc<float4>(c->NS);
+      d.arn_scr = a.alloc<double>(((size_t)c->arn_q + 4) * std::max<u32>(c->n_rc, 1));
+      // drivers without a net: no sink reads them; mark every entry "Elmore" first
+      ck(cudaMemsetAsync(d.arn_lam, 0xFF, sizeof(float4) * std::max<u32>(c->NP, 1), s), "memset");
+    }
     ck(sta::launch_init_corner(t, d, c->n_heavy, s), "init kernel");
   }
   ck(cudaStreamSynchronize(s), "prepare upload");
@@ -1348,6 +1396,10 @@ u32 enqueue_batch(sta_ctx c, const sta::Batch& b) {
   ck(sta::launch_rc(t, b, c->wgrid, s), "rc kernel");
   if (t.nC && !std::getenv("STA_RC_SERIAL")) ck(cudaStreamWaitEvent(s, c->join_ev, 0), "join wait");
   launches += (t.n_wtiles ? 1 : 0) + (t.n_btiles ? 1 : 0) + (t.n_lumped ? 1 : 0) + (t.nC ? 2 : 0);
+  if (t.net_model == 1) {                    // row f1: the nets' reduced-order models
+    ck(sta::launch_arn_reduce(t, b, s), "arnoldi kernel");
+    launches += t.n_arn_nets ? 1 : 0;
+  }
   prof_mark(c, 1);
   if (c->use_persistent && c->pgrid && c->pgrid_b) {
     prof_mark(c, 2);
@@ -1781,6 +1833,20 @@ sta_status sta_set_library(sta_ctx c, uint32_t corner, sta_mem mem, uint32_t num
 }
 
 
+sta_status sta_set_net_model(sta_ctx c, sta_net_model model, uint32_t q) {
+  return guard(c, [&] {
+    if (model != STA_NET_ELMORE && model != STA_NET_ARNOLDI) fail(STA_ERR_ARG, "net model %d", (int)model);
+    if (model == STA_NET_ARNOLDI && (q < 1 || q > 4)) fail(STA_ERR_ARG, "Arnoldi order %u outside 1..4", q);
+    if (c->net_model != (int)model || (model == STA_NET_ARNOLDI && c->arn_q != q)) {
+      ck(cudaStreamSynchronize(c->stream), "sync");
+      c->net_model = (int)model;
+      if (model == STA_NET_ARNOLDI) c->arn_q = q;
+      c->prepared = false;                   // layout / scratch / kernels of the next update
+      invalidate_graph(c);
+    }
+  });
+}
+
 sta_status sta_build_steiner(sta_ctx c, sta_mem mem, const float* pin_x, const float* pin_y,
                              const sta_steiner_units* u, uint32_t node_capacity, uint32_t* rc_ptr,
                              int32_t* parent, uint32_t* node_pin, float* res, float* cap, uint32_t* num_nodes) {
@@ -2022,6 +2088,7 @@ sta_status sta_report_paths(sta_ctx c, uint32_t corner, const sta_path_query* q,
     if (!q || !out) fail(STA_ERR_ARG, "query / output NULL");
     if (q->mode > 1) fail(STA_ERR_ARG, "mode %u (0 setup, 1 hold)", q->mode);
     if (q->k == 0 || q->nworst == 0) fail(STA_ERR_ARG, "k and nworst must be >= 1");
+    if (c->net_model != 0) fail(STA_ERR_ORDER, "the path report needs the Elmore net model");
     if (mem != STA_MEM_HOST && mem != STA_MEM_DEVICE) fail(STA_ERR_ARG, "bad sta_mem %d", (int)mem);
     const u32 m = std::min(q->k, q->nworst);
     if (m > 255) fail(STA_ERR_ARG, "min(k, nworst) = %u exceeds 255", m);

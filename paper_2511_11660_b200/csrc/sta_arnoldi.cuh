@@ -1,0 +1,105 @@
+// sta_arnoldi.cuh -- NEXT row f1: the net-arc delay / slew of the Arnoldi
+// reduced-order model (SPEC.md:407-418,
+// readings A1-A7 in DESIGN.md), evaluated wherever a sink's arrival is
+// needed (the forward's term lanes, the backward's sink lanes): the model
+// H(s) = sum_k res_k / (1 + s lam_k) (lam: time constants, ps; res: the
+// sink's residues, sum 1) driven by a saturated ramp whose 20-80 slew is the
+// driver's slew s (duration D = s / 0.6): delay = t50(out) - D / 2, slew =
+// t80 - t20.  Crossings by safeguarded Newton in fp32 (the response and its
+// derivative in closed form, expm1-based so the small-t region keeps its
+// precision).  Every caller uses these __noinline__ functions, so a sink's
+// delay is bit-identical wherever it is recomputed.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace sta {
+
+// y(t) and y'(t) of the ramp response, order <= 4 (unused terms res 0)
+__device__ __forceinline__ void arn_resp(const float4& lam, const float4& res, float D, float t, float& y,
+                                         float& dy) {
+  const float L[4] = {lam.x, lam.y, lam.z, lam.w}, K[4] = {res.x, res.y, res.z, res.w};
+  y = 0.f;
+  dy = 0.f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float l = L[k];
+    float g, dg;
+    if (t <= 0.f) {
+      g = 0.f;
+      dg = 0.f;
+    } else if (D <= 0.f) {                     // a step
+      if (l > 0.f) {
+        const float e = __expf(-t / l);
+        g = -expm1f(-t / l);
+        dg = e / l;
+      } else {
+        g = 1.f;
+        dg = 0.f;
+      }
+    } else if (t <= D) {                       // on the ramp: (t + l expm1(-t/l)) / D
+      if (l > 0.f) {
+        const float em = expm1f(-t / l);
+        g = (t + l * em) / D;
+        dg = -em / D;
+      } else {
+        g = t / D;
+        dg = 1.f / D;
+      }
+    } else {                                   // after it: 1 - (l / D) (e^{-(t-D)/l} - e^{-t/l})
+      if (l > 0.f) {
+        // e^{-t/l} expm1(D/l) while D/l < 1 (no cancellation, no overflow),
+        // the plain difference beyond (its cancellation is bounded there)
+        const float r = D / l;
+        const float a = r < 1.f ? __expf(-t / l) * expm1f(r) : __expf(-(t - D) / l) - __expf(-t / l);
+        g = 1.f - (l / D) * a;
+        dg = a / D;
+      } else {
+        g = 1.f;
+        dg = 0.f;
+      }
+    }
+    y += K[k] * g;
+    dy += K[k] * dg;
+  }
+}
+
+// first time the response reaches theta: Newton inside a shrinking bracket,
+// bisection when a step leaves it
+__device__ __noinline__ float arn_cross(float4 lam, float4 res, float D, float theta) {
+  const float lmax = fmaxf(fmaxf(lam.x, lam.y), fmaxf(lam.z, lam.w));
+  float lo = 0.f, hi = D + 50.f * lmax + 1e-3f;
+  float y, dy;
+  for (int g = 0; g < 24; ++g) {
+    arn_resp(lam, res, D, hi, y, dy);
+    if (y >= theta) break;
+    hi *= 2.f;
+  }
+  float t = fminf(0.5f * D + 0.7f * lmax, 0.5f * hi);
+  for (int it = 0; it < 60; ++it) {
+    arn_resp(lam, res, D, t, y, dy);
+    if (y >= theta) hi = t;
+    else lo = t;
+    float tn = dy > 0.f ? t - (y - theta) / dy : 0.5f * (lo + hi);
+    if (!(tn > lo && tn < hi)) tn = 0.5f * (lo + hi);
+    const float step = fabsf(tn - t);
+    t = tn;
+    if (step <= 1e-7f * fmaxf(t, 1e-3f) || hi - lo <= 1e-7f * fmaxf(hi, 1e-3f)) break;
+  }
+  return t;
+}
+
+__device__ __forceinline__ float arn_duration(float s) { return __fdiv_rn(s, 0.6f); }
+
+// the net-arc delay for a driver slew s (bit-identical in every caller)
+__device__ __noinline__ float arn_delay(float4 lam, float4 res, float s) {
+  const float D = arn_duration(s);
+  return __fsub_rn(arn_cross(lam, res, D, 0.5f), __fmul_rn(0.5f, D));
+}
+
+// the sink's 20-80 slew
+__device__ __noinline__ float arn_slew(float4 lam, float4 res, float s) {
+  const float D = arn_duration(s);
+  return __fsub_rn(arn_cross(lam, res, D, 0.8f), arn_cross(lam, res, D, 0.2f));
+}
+
+}  // namespace sta

@@ -183,6 +183,16 @@ struct Topo {
   // outputs to user order
   const uint32_t* int_of_user; // [P]
   const uint32_t* drv_of_net;  // [N] user net -> internal driver
+  // NEXT row f1: net-arc delay model (0 Elmore, 1 Arnoldi reduced order
+  // arn_q <= 4; sta_arnoldi.cu / sta_arnoldi.cuh).  Arnoldi layout over the
+  // internal RC nodes (each net contiguous in DFS preorder):
+  uint32_t net_model, arn_q;
+  uint32_t n_arn_nets;
+  const uint4* arn_nets;      // {first internal node, nodes (0: lumped net), internal driver, 0}
+  const uint4* arn_node;      // [n_rc] {caller node id, internal parent or kNone at the root,
+                              //  subtree end (internal), sink index or kNone}
+  const float* arn_scap;      // [n_rc] pin + PO cap at the node
+  uint64_t n_rc_nodes;
 };
 
 // Per-corner device state.
@@ -211,6 +221,9 @@ struct CornerDev {
   const float* const* rc_vals;  // device {res, cap} pointer pair (user node order)
   double* scratch;    // tier-C scratch (tierC_scratch)
   uint32_t* err_flag; // nonzero: bad RC value seen
+  float4* arn_lam;    // [NP] Arnoldi time constants of the net each pull pin drives (x < 0: Elmore)
+  float4* arn_res;    // [NS] residues of each sink
+  double* arn_scr;    // [(arn_q + 4) n_rc] Lanczos scratch
   unsigned long long* trace;  // optional (STA_TRACE): per warp unit {start, ready, end} ns
 };
 
@@ -306,6 +319,9 @@ cudaError_t levelize_device(uint32_t P, uint32_t N, uint32_t A, const uint32_t* 
                             const uint32_t* arc_from, const uint32_t* arc_to, uint32_t* level, uint32_t* perm,
                             uint32_t* fi_ptr, uint32_t* fi_ids, uint32_t* fo_ptr, uint32_t* fo_ids,
                             uint32_t* num_levels, uint32_t* cycle_pin, cudaStream_t s);
+
+// ---- NEXT row f1: Arnoldi reduced-order models of every net (sta_arnoldi.cu)
+cudaError_t launch_arn_reduce(const Topo& t, const Batch& b, cudaStream_t s);
 
 // ---- NEXT row f2: built-in Steiner RC from pin positions (sta_steiner.cu)
 struct SteinerArgs {

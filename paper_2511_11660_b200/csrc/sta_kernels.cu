@@ -32,6 +32,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include "sta_arnoldi.cuh"
 #include "sta_internal.h"
 
 namespace sta {
@@ -907,17 +908,66 @@ __device__ __forceinline__ void hop_q(float& a_in, float& s_in, float elm) {
   s_in = __fsqrt_rn(__fmaf_rn(s_in, s_in, __fmul_rn(imp, imp)));
 }
 
-// RC results a term slot needs: {Elmore delay of its sink input, load of its pin}
+// RC results a term slot needs: {Elmore delay of its sink input, load of its
+// pin}; under the Arnoldi model also the reduced model of the sink input
+// (its net's time constants, the sink's residues)
+template <bool ARN>
 struct FwdRc {
   float elm, ld;
 };
-__device__ __forceinline__ FwdRc fwd_rc(const CornerDev& c, const uint4& tr) {
-  FwdRc r{0.f, 0.f};
+template <>
+struct FwdRc<true> {
+  float elm, ld;
+  float4 lam, res;
+};
+template <bool ARN>
+__device__ __forceinline__ FwdRc<ARN> fwd_rc(const CornerDev& c, const uint4& tr) {
+  FwdRc<ARN> r{};
   if (tr.x < kHeavyMark) {                   // a term (not padding / seed / heavy marker)
-    if (tr.y != kNone) r.elm = __ldcg(c.elm + tr.y);
+    if (tr.y != kNone) {
+      r.elm = __ldcg(c.elm + tr.y);
+      if constexpr (ARN) {
+        r.lam = __ldcg(c.arn_lam + tr.x);
+        r.res = __ldcg(c.arn_res + tr.y);
+      }
+    }
     r.ld = __ldcg(c.load + tr.w);
   }
   return r;
+}
+
+// net hop of one component under the Arnoldi model (row f1): the reduced
+// model's ramp response; an unstable / lumped net (lam.x < 0 or NaN) keeps
+// the Elmore hop
+__device__ __forceinline__ void arn_hop_q(float& a_in, float& s_in, float elm, const float4& lam, const float4& res) {
+  if (!(lam.x >= 0.f)) {
+    hop_q(a_in, s_in, elm);
+    return;
+  }
+  if (!fin(a_in)) return;
+  const float d = arn_delay(lam, res, s_in);
+  const float so = arn_slew(lam, res, s_in);
+  a_in = __fadd_rn(a_in, d);
+  s_in = so;
+}
+// all four components (the backward's and the output gather's recomputation);
+// slews only if wanted (undefined components keep undefined slews)
+__device__ __forceinline__ void arn_net_hop(Q4& at, Q4& sl, float elm, const float4& lam, const float4& res,
+                                            bool slews, Q4* dly = nullptr) {
+  if (!(lam.x >= 0.f)) {
+    if (dly) for (int q = 0; q < 4; ++q) dly->v[q] = elm;
+    if (slews) net_hop(at, sl, elm);
+    else hop_at(at, elm);
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const bool ok = fin(at.v[q]);
+    const float d = ok ? arn_delay(lam, res, sl.v[q]) : 0.f;
+    if (dly) dly->v[q] = d;
+    if (slews) sl.v[q] = ok ? arn_slew(lam, res, sl.v[q]) : (q < 2 ? CUDART_INF_F : -CUDART_INF_F);
+    at.v[q] = ok ? __fadd_rn(at.v[q], d) : at.v[q];
+  }
 }
 
 // forward unit u; tr = this lane's term slot of the unit, rc its RC results
@@ -931,9 +981,9 @@ __device__ __forceinline__ const uint4* fwd_word(const CornerDev& c, const uint4
 
 // pre: this lane's record word loaded speculatively one unit early (valid
 // if its tags match the epoch, else it is polled again)
-template <bool TRACE>
+template <bool TRACE, bool ARN>
 __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, const float* __restrict__ L,
-                                         uint32_t ep, uint32_t u, const uint4& tr, FwdRc rc,
+                                         uint32_t ep, uint32_t u, const uint4& tr, FwdRc<ARN> rc,
                                          uint4 pre = make_uint4(0, 0, 0, 0)) {
   const uint32_t lane = threadIdx.x & 31, tl = lane >> 2, q = lane & 3;
   const int el = (int)(q >> 1), orf = (int)(q & 1);
@@ -977,7 +1027,10 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
 #endif
       if (TRACE) t_data = gtimer();
       float a_in = __uint_as_float(w.x), s_in = __uint_as_float(w.z);
-      if (tr.y != kNone) hop_q(a_in, s_in, elm);
+      if (tr.y != kNone) {
+        if constexpr (ARN) arn_hop_q(a_in, s_in, elm, rc.lam, rc.res);
+        else hop_q(a_in, s_in, elm);
+      }
       float dl;
       fwd_lane(f, el, a_in, s_in, ca, cs, dl);
       reinterpret_cast<float*>(c.tdel + (size_t)kFwdTerms * u + tl)[q] = dl;
@@ -1019,7 +1072,11 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
       const FwdTabs f = fwd_tabs(L, info, orf, ld);
       const uint4 w = spin_ll(c.rec + 4 * (size_t)t.fi_src[e] + (el * 2 + irf), ep);
       float a_in = __uint_as_float(w.x), s_in = __uint_as_float(w.z);
-      if (h != kNone) hop_q(a_in, s_in, __ldcg(c.elm + h));
+      if (h != kNone) {
+        if constexpr (ARN)
+          arn_hop_q(a_in, s_in, __ldcg(c.elm + h), __ldcg(c.arn_lam + t.fi_src[e]), __ldcg(c.arn_res + h));
+        else hop_q(a_in, s_in, __ldcg(c.elm + h));
+      }
       float oa, os, dl;
       fwd_lane(f, el, a_in, s_in, oa, os, dl);
       reinterpret_cast<float*>(c.tdel + dbase + b)[q] = dl;
@@ -1046,13 +1103,12 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
   trace_unit<TRACE>(c, u, t_start, t_ready, t_data);
 }
 
-template <bool SMEM_LUT, bool TRACE>
-__global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) fwd_persistent_kernel(Topo t,
-                                                                                   const __grid_constant__ Batch B) {
+template <bool SMEM_LUT, bool TRACE, bool ARN, int NT>
+__device__ __forceinline__ void fwd_persistent_body(const Topo& t, const Batch& B) {
   stage_luts<SMEM_LUT>(B, kNone);
   // warp gw serves corner gw % K and walks its unit list with stride Wc
-  const uint32_t K = B.K, gw = blockIdx.x * (kFwdThreads / 32) + (threadIdx.x >> 5);
-  const uint32_t Wc = gridDim.x * (kFwdThreads / 32) / K;
+  const uint32_t K = B.K, gw = blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
+  const uint32_t Wc = gridDim.x * (NT / 32) / K;
   if (gw >= Wc * K) return;
   const CornerDev& c = B.c[gw % K];
   const float* L = lut_of<SMEM_LUT>(c);
@@ -1066,7 +1122,7 @@ __global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) fwd_persistent_ker
   const uint4 pad = make_uint4(kNone, kNone, 0, kNone);
   uint4 tr = u < t.n_fwu ? __ldg(t.fterm + (size_t)kFwdTerms * u + tl) : pad;
   uint4 nx = u + Wc < t.n_fwu ? __ldg(t.fterm + (size_t)kFwdTerms * (u + Wc) + tl) : pad;
-  FwdRc rc = fwd_rc(c, tr);
+  FwdRc<ARN> rc = fwd_rc<ARN>(c, tr);
 #if STA_FWD_RECPF
   // the record words of the next unit, loaded speculatively one unit early:
   // in the wide stages the producers are long done and the unit starts with
@@ -1075,13 +1131,13 @@ __global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) fwd_persistent_ker
 #endif
   for (; u < t.n_fwu; u += Wc) {
     const uint4 nnx = u + 2 * Wc < t.n_fwu ? __ldg(t.fterm + (size_t)kFwdTerms * (u + 2 * Wc) + tl) : pad;
-    const FwdRc nrc = fwd_rc(c, nx);         // nx arrived during the previous unit
+    const FwdRc<ARN> nrc = fwd_rc<ARN>(c, nx);         // nx arrived during the previous unit
 #if STA_FWD_RECPF
     const uint4 nrec = nx.x < kHeavyMark ? ld_ll(fwd_word(c, nx)) : make_uint4(0, 0, 0, 0);
-    fwd_unit<TRACE>(t, c, L, ep, u, tr, rc, rec);
+    fwd_unit<TRACE, ARN>(t, c, L, ep, u, tr, rc, rec);
     rec = nrec;
 #else
-    fwd_unit<TRACE>(t, c, L, ep, u, tr, rc);
+    fwd_unit<TRACE, ARN>(t, c, L, ep, u, tr, rc);
 #endif
     tr = nx;
     nx = nnx;
@@ -1094,9 +1150,23 @@ __global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) fwd_persistent_ker
   for (; u < t.n_fwu; u += Wc) {
     const uint4 tr = nx;
     if (u + Wc < t.n_fwu) nx = __ldg(t.fterm + (size_t)kFwdTerms * (u + Wc) + tl);   // prefetch the next unit
-    fwd_unit<TRACE>(t, c, L, ep, u, tr, fwd_rc(c, tr));
+    fwd_unit<TRACE, ARN>(t, c, L, ep, u, tr, fwd_rc<ARN>(c, tr));
   }
 #endif
+}
+
+template <bool SMEM_LUT, bool TRACE>
+__global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) fwd_persistent_kernel(Topo t,
+                                                                                   const __grid_constant__ Batch B) {
+  fwd_persistent_body<SMEM_LUT, TRACE, false, kFwdThreads>(t, B);
+}
+
+// the Arnoldi-model instantiation (row f1): its hop solver needs registers,
+// so fewer warps per block
+constexpr int kFwdArnThreads = 512;
+template <bool SMEM_LUT>
+__global__ void __launch_bounds__(kFwdArnThreads, 1) fwd_persistent_arn_kernel(Topo t, const __grid_constant__ Batch B) {
+  fwd_persistent_body<SMEM_LUT, false, true, kFwdArnThreads>(t, B);
 }
 
 // units [u0, u1) of one gate stage, one warp each; grid.y = corner
@@ -1111,7 +1181,7 @@ __global__ void __launch_bounds__(kThreads) fwd_stage_kernel(Topo t, const __gri
   pdl_wait();
   pdl_launch();
   if (u >= u1) return;
-  fwd_unit<TRACE>(t, c, L, epoch_of(c), u, tr, fwd_rc(c, tr));
+  fwd_unit<TRACE, false>(t, c, L, epoch_of(c), u, tr, fwd_rc<false>(c, tr));
 }
 
 // ---- backward: one lane per sink / pin (all four components in the lane)
@@ -1274,7 +1344,7 @@ __device__ __forceinline__ SinkFo bwd_fo(const Topo& t, const uint4& ud) {
   return f;
 }
 
-template <bool TRACE>
+template <bool TRACE, bool ARN>
 __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, const float* __restrict__ L,
                                          uint32_t ep, uint32_t u, const uint4& ud, const SinkFo& fo) {
   const uint32_t lane = threadIdx.x & 31;
@@ -1309,7 +1379,11 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
       if (fa.w == kNone && fa.y) spin_pair(c.rat_ll + 2 * (size_t)fb.x, pre.e0, pre.l0, ep);
 #endif
       Q4 a = at_v, s = sl_v, r = undef_rat();
-      if (fa.w != kNone) {                   // endpoint sink: its slews feed the check tables
+      Q4 nd{{elm, elm, elm, elm}};           // the net arc's delay per component
+      if constexpr (ARN) {                   // row f1: the driver's slews drive the reduced model
+        s = load_slew(c, v);
+        arn_net_hop(a, s, elm, __ldcg(c.arn_lam + v), __ldcg(c.arn_res + k), fa.w != kNone, &nd);
+      } else if (fa.w != kNone) {            // endpoint sink: its slews feed the check tables
         s = load_slew(c, v);
         net_hop(a, s, elm);                  // the sink's own arrival / slew
       } else {
@@ -1323,7 +1397,7 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
       if (fa.w != kNone) write_ep(c, fa.w, sk);
 #pragma unroll
       for (int q = 0; q < 4; ++q)            // through the net arc (edges the forward used)
-        if (fin(at_v.v[q])) acc.v[q] = __fsub_rn(r.v[q], elm);
+        if (fin(at_v.v[q])) acc.v[q] = __fsub_rn(r.v[q], nd.v[q]);
     }
     // merge the sinks of each driver (contiguous lanes) into its first lane:
     // log-step doubling (max / min are idempotent: overlapping windows are
@@ -1401,12 +1475,11 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
   trace_unit<TRACE>(c, (size_t)t.n_fwu + u, t_start, t_ready ? t_ready : t_start, t_data);
 }
 
-template <bool SMEM_LUT, bool TRACE>
-__global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_kernel(Topo t,
-                                                                                   const __grid_constant__ Batch B) {
+template <bool SMEM_LUT, bool TRACE, bool ARN, int NT>
+__device__ __forceinline__ void bwd_persistent_body(const Topo& t, const Batch& B) {
   stage_luts<SMEM_LUT>(B, kNone);
-  const uint32_t K = B.K, gw = blockIdx.x * (kBwdThreads / 32) + (threadIdx.x >> 5);
-  const uint32_t W = gridDim.x * (kBwdThreads / 32) / K;    // warps of this corner
+  const uint32_t K = B.K, gw = blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
+  const uint32_t W = gridDim.x * (NT / 32) / K;    // warps of this corner
   if (gw >= W * K) return;
   const CornerDev& c = B.c[gw % K];
   const float* L = lut_of<SMEM_LUT>(c);
@@ -1433,11 +1506,11 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_ker
       u = ns + __shfl_sync(kFull, x, 0);
       if (u >= t.n_bwu) break;
       ud = __ldg(t.bwu + u);
-      bwd_unit<TRACE>(t, c, L, ep, u, ud, bwd_fo(t, ud));
+      bwd_unit<TRACE, ARN>(t, c, L, ep, u, ud, bwd_fo(t, ud));
       continue;
     }
     const uint4 nu = u + W < ns ? __ldg(t.bwu + u + W) : none;
-    bwd_unit<TRACE>(t, c, L, ep, u, ud, bwd_fo(t, ud));
+    bwd_unit<TRACE, ARN>(t, c, L, ep, u, ud, bwd_fo(t, ud));
     u += W;
     ud = nu;
   }
@@ -1451,7 +1524,7 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_ker
   // register holds a prefetched record across the unit body.
   const uint32_t wib = threadIdx.x >> 5;
   uint4* fbuf = reinterpret_cast<uint4*>(s_dyn + B.smem_f4) + wib * 64;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(s_dyn + B.smem_f4 + (kBwdThreads / 32) * 64) + wib;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_dyn + B.smem_f4 + (NT / 32) * 64) + wib;
   if (lane == 0) mbar_init(bar, 1);
   __syncwarp();
   uint32_t phase = 0;
@@ -1504,7 +1577,7 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_ker
       issue(nx);                             // the next unit's records stream in meanwhile
       if (u + 2 * W < ns) nnx = __ldg(t.bwu + u + 2 * W);
     }
-    bwd_unit<TRACE>(t, c, L, ep, u, ud, cf);
+    bwd_unit<TRACE, ARN>(t, c, L, ep, u, ud, cf);
     if (dyn) {
       u = un;
       ud = nx;
@@ -1546,7 +1619,7 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_ker
       nfo = bwd_fo(t, nx);                   // next unit's fan-out records (its record arrived)
       if (u + 2 * W < ns) nnx = __ldg(t.bwu + u + 2 * W);
     }
-    bwd_unit<TRACE>(t, c, L, ep, u, ud, fo);
+    bwd_unit<TRACE, ARN>(t, c, L, ep, u, ud, fo);
     if (dyn) {
       u = un;
       ud = nx;
@@ -1569,6 +1642,18 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_ker
 }
 
 template <bool SMEM_LUT, bool TRACE>
+__global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_kernel(Topo t,
+                                                                                   const __grid_constant__ Batch B) {
+  bwd_persistent_body<SMEM_LUT, TRACE, false, kBwdThreads>(t, B);
+}
+
+constexpr int kBwdArnThreads = 512;
+template <bool SMEM_LUT>
+__global__ void __launch_bounds__(kBwdArnThreads, 1) bwd_persistent_arn_kernel(Topo t, const __grid_constant__ Batch B) {
+  bwd_persistent_body<SMEM_LUT, false, true, kBwdArnThreads>(t, B);
+}
+
+template <bool SMEM_LUT, bool TRACE>
 __global__ void __launch_bounds__(kThreads) bwd_stage_kernel(Topo t, const __grid_constant__ Batch B, uint32_t u0,
                                                              uint32_t u1) {
   stage_luts<SMEM_LUT>(B, blockIdx.y);
@@ -1581,7 +1666,7 @@ __global__ void __launch_bounds__(kThreads) bwd_stage_kernel(Topo t, const __gri
   pdl_wait();
   pdl_launch();
   if (u >= u1) return;
-  bwd_unit<TRACE>(t, c, L, epoch_of(c), u, ud, fo);
+  bwd_unit<TRACE, false>(t, c, L, epoch_of(c), u, ud, fo);
 }
 
 // ------------------------------------------------------- a5: WNS / TNS
@@ -1690,7 +1775,8 @@ __global__ void gather_pins_kernel(Topo t, CornerDev c, int what, float4* __rest
   const uint32_t k = i - t.NP;
   Q4 at, sl;
   load_rec(c, t.sink_drv[k], at, sl);
-  net_hop(at, sl, c.elm[k]);
+  if (t.net_model == 1) arn_net_hop(at, sl, c.elm[k], c.arn_lam[t.sink_drv[k]], c.arn_res[k], true);
+  else net_hop(at, sl, c.elm[k]);
   dst[p] = to_f4(what == 0 ? at : sl);
 }
 
@@ -2117,13 +2203,22 @@ uint32_t persistent_grid(uint32_t smem_f4, int which) {
         &nb, smem_f4 ? fwd_persistent_kernel<true, false> : fwd_persistent_kernel<false, false>, kFwdThreads, smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &nt, smem_f4 ? fwd_persistent_kernel<true, true> : fwd_persistent_kernel<false, true>, kFwdThreads, smem);
-  } else {
+  } else if (which == 1) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &nb, smem_f4 ? bwd_persistent_kernel<true, false> : bwd_persistent_kernel<false, false>, kBwdThreads,
         smem + kBwdExtraSmem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &nt, smem_f4 ? bwd_persistent_kernel<true, true> : bwd_persistent_kernel<false, true>, kBwdThreads,
         smem + kBwdExtraSmem);
+  } else if (which == 2) {                   // Arnoldi-model instantiations (row f1)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &nb, smem_f4 ? fwd_persistent_arn_kernel<true> : fwd_persistent_arn_kernel<false>, kFwdArnThreads, smem);
+    nt = nb;
+  } else {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &nb, smem_f4 ? bwd_persistent_arn_kernel<true> : bwd_persistent_arn_kernel<false>, kBwdArnThreads,
+        smem + kBwdExtraSmem);
+    nt = nb;
   }
   cudaGetLastError();
   return (uint32_t)(std::min(nb, nt) * sms);
@@ -2150,6 +2245,12 @@ static bool traced(const Batch& b) { return b.c[0].trace != nullptr; }
 cudaError_t launch_fwd_persistent(const Topo& t, const Batch& b, uint32_t grid, cudaStream_t s) {
   if (!t.NP) return cudaSuccess;
   const size_t sm = 16ull * b.smem_f4;
+  if (t.net_model == 1) {                    // row f1: the Arnoldi-model instantiation
+    const uint32_t g = persistent_grid(b.smem_f4, 2);
+    if (!g) return cudaErrorCooperativeLaunchTooLarge;
+    return b.smem_f4 ? coop_launch(fwd_persistent_arn_kernel<true>, g, kFwdArnThreads, sm, s, t, b)
+                     : coop_launch(fwd_persistent_arn_kernel<false>, g, kFwdArnThreads, 0, s, t, b);
+  }
   // STA_TRACE builds per-unit timestamps into a separate instantiation
   if (traced(b))
     return b.smem_f4 ? coop_launch(fwd_persistent_kernel<true, true>, grid, kFwdThreads, sm, s, t, b)
@@ -2161,6 +2262,12 @@ cudaError_t launch_fwd_persistent(const Topo& t, const Batch& b, uint32_t grid, 
 cudaError_t launch_bwd_persistent(const Topo& t, const Batch& b, uint32_t grid, cudaStream_t s) {
   if (!t.n_bwu) return cudaSuccess;
   const size_t sm = 16ull * b.smem_f4 + kBwdExtraSmem;
+  if (t.net_model == 1) {
+    const uint32_t g = persistent_grid(b.smem_f4, 3);
+    if (!g) return cudaErrorCooperativeLaunchTooLarge;
+    return b.smem_f4 ? coop_launch(bwd_persistent_arn_kernel<true>, g, kBwdArnThreads, sm, s, t, b)
+                     : coop_launch(bwd_persistent_arn_kernel<false>, g, kBwdArnThreads, kBwdExtraSmem, s, t, b);
+  }
   if (traced(b))
     return b.smem_f4 ? coop_launch(bwd_persistent_kernel<true, true>, grid, kBwdThreads, sm, s, t, b)
                      : coop_launch(bwd_persistent_kernel<false, true>, grid, kBwdThreads, kBwdExtraSmem, s, t, b);
@@ -2172,6 +2279,11 @@ cudaError_t set_lut_smem_limit(size_t bytes) {
   const int b = (int)bytes;
   cudaError_t e = cudaFuncSetAttribute(fwd_stage_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(bwd_stage_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(fwd_persistent_arn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(bwd_persistent_arn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             b + (int)kBwdExtraSmem);
   for (int tr = 0; tr < 2 && e == cudaSuccess; ++tr) {
     e = cudaFuncSetAttribute(tr ? fwd_persistent_kernel<true, true> : fwd_persistent_kernel<true, false>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, b);

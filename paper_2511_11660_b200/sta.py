@@ -29,7 +29,7 @@ EXPORTS = ["sta_create", "sta_destroy", "sta_last_error", "sta_status_string", "
            "sta_set_library", "sta_set_rc_tree", "sta_set_rc_values", "sta_set_constraints",
            "sta_update_timing", "sta_report_slack", "sta_get_timing", "sta_get_rc",
            "sta_get_levels", "sta_get_info", "sta_synchronize", "sta_profile_enable",
-           "sta_profile_read", "sta_report_paths", "sta_build_steiner"]
+           "sta_profile_read", "sta_report_paths", "sta_build_steiner", "sta_set_net_model"]
 
 
 class StaError(RuntimeError):
@@ -120,6 +120,7 @@ def lib():
             "sta_report_paths": (i32, [vp, u32, C.POINTER(PathQuery), C.POINTER(PathSet), i32]),
             "sta_build_steiner": (i32, [vp, i32, vp, vp, C.POINTER(SteinerUnits), u32, vp, vp, vp, vp, vp,
                                         C.POINTER(u32)]),
+            "sta_set_net_model": (i32, [vp, i32, u32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -308,6 +309,11 @@ class Context:
         self._check(self._L.sta_build_steiner(self.h, a.kind, px, py, C.byref(u), capn, *ptrs, C.byref(nn)))
         n = nn.value
         return (rc_ptr,) + tuple(o[:n] for o in outs)
+
+    def set_net_model(self, model: str = "elmore", q: int = 4):
+        """Net-arc delay model of the next updates: "elmore" or "arnoldi"
+        (reduced order q in 1..4)."""
+        self._check(self._L.sta_set_net_model(self.h, {"elmore": 0, "arnoldi": 1}[model], int(q)))
 
     # ------------------------------------------------------------ update
     def update_timing(self):
