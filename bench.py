@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip e2e/profile/cpu legs (ncu runs)")
     ap.add_argument("--phases", action="store_true", help="with --quick: still measure the per-phase times")
+    ap.add_argument("--net-model", default="elmore", choices=["elmore", "arnoldi"],
+                    help="net-arc delay model (row f1: arnoldi = reduced order 4)")
     return ap.parse_args()
 
 
@@ -245,6 +247,8 @@ def main():
     ctx = pkg.Context(local, K, stream=stream.cuda_stream)
     t0 = time.perf_counter()
     pkg.load_design(ctx, d, corners=mine)
+    if args.net_model != "elmore":
+        ctx.set_net_model(args.net_model, 4)
     torch.cuda.synchronize()
     load_s = time.perf_counter() - t0
     # inputs resident in HBM for the device-timed value: borrowed RC tensors
@@ -309,7 +313,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if name == "c5_multicorner" else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": config_line(name, info, K, world, gen_s, load_s),
+            "config": dict(config_line(name, info, K, world, gen_s, load_s), net_model=args.net_model),
             "gpu_launches": info["kernels_per_update"] * args.steps,
             "clocks": clk, "wns_tns": [float(x) for x in res_own[0]]}
     if name == "c5_multicorner":

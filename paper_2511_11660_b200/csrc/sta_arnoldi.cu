@@ -144,10 +144,7 @@ __global__ void __launch_bounds__(kArnThreads) arn_reduce_kernel(Topo t, const _
   const uint4 net = __ldg(t.arn_nets + w);
   const uint32_t x0 = net.x, m = net.y, drv = net.z;
   const int q = (int)t.arn_q;
-  if (m == 0) {                                // lumped net: no wire delay (the Elmore path)
-    if (lane == 0) c.arn_lam[drv] = make_float4(-1.f, 0.f, 0.f, 0.f);
-    return;
-  }
+  if (m <= 32) return;                         // arn_small_kernel
   const float* R = c.rc_vals[0];
   const float* Cw = c.rc_vals[1];
   const size_t n = t.n_rc_nodes;
@@ -278,11 +275,120 @@ __global__ void __launch_bounds__(kArnThreads) arn_reduce_kernel(Topo t, const _
   }
 }
 
+
+// Nets of <= 32 RC nodes (nearly all): one lane per node in preorder, the
+// Lanczos vectors in registers, the tree solve by a warp scan (subtree sums)
+// and pointer jumping over parent lanes (root-path sums): no scratch.
+__global__ void __launch_bounds__(kArnThreads) arn_small_kernel(Topo t, const __grid_constant__ Batch B) {
+  const uint32_t w = (blockIdx.x * kArnThreads + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= t.n_arn_nets) return;
+  const CornerDev& c = B.c[blockIdx.y];
+  const uint4 net = __ldg(t.arn_nets + w);
+  const uint32_t x0 = net.x, m = net.y, drv = net.z;
+  const int q = (int)t.arn_q;
+  if (m == 0) {                                // lumped net: no wire delay (the Elmore path)
+    if (lane == 0) c.arn_lam[drv] = make_float4(-1.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  if (m > 32) return;                          // arn_reduce_kernel
+  const bool act = (uint32_t)lane < m;
+  uint4 nd = make_uint4(0, kNone, 0, kNone);
+  double C = 0.0, R = 0.0;
+  if (act) {
+    nd = __ldg(t.arn_node + x0 + lane);
+    if (nd.y != kNone) {
+      C = (double)c.rc_vals[1][nd.x] + (double)__ldg(t.arn_scap + x0 + lane);
+      R = (double)c.rc_vals[0][nd.x];
+    }
+  }
+  const int par = (act && nd.y != kNone) ? (int)(nd.y - x0) : -1;
+  const int endl = act ? (int)(nd.z - x0) : 0;
+  const double ctot = warp_sum(C);
+  if (!(ctot > 0.0) || m <= 1) {               // no dynamics: the output follows the input
+    if (lane == 0) c.arn_lam[drv] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (act && nd.w != kNone) c.arn_res[nd.w] = make_float4(1.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  // A x on the lanes (x = this lane's component)
+  auto apply = [&](double x) {
+    const double tv = C * x;
+    const double inc = warp_incl_scan(tv, lane);
+    const double exc = inc - tv;
+    const double total = __shfl_sync(kFull, inc, 31);
+    const double pend = __shfl_sync(kFull, exc, endl < 32 ? endl : lane);
+    const double S = (endl == (int)m ? total : pend) - exc;
+    double acc = par >= 0 ? R * S : 0.0;
+    int ptr = par;
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      const int src = ptr >= 0 ? ptr : lane;
+      const double pa = __shfl_sync(kFull, acc, src);
+      const int pp = __shfl_sync(kFull, ptr, src);
+      if (ptr >= 0) {
+        acc += pa;
+        ptr = pp;
+      }
+    }
+    return acc;
+  };
+  double V[5] = {0, 0, 0, 0, 0};
+  V[0] = par >= 0 ? 1.0 / sqrt(ctot) : 0.0;
+  double alpha[4] = {0, 0, 0, 0}, beta[4] = {0, 0, 0, 0};
+  int qq = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (j >= q) break;
+    double wv = apply(V[j]);
+    if (j > 0) wv -= beta[j - 1] * V[j - 1];
+    double d[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) d[k] = k <= j ? warp_sum(C * wv * V[k]) : 0.0;
+    alpha[j] = d[j];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k <= j) wv -= d[k] * V[k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) d[k] = k <= j ? warp_sum(C * wv * V[k]) : 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k <= j) wv -= d[k] * V[k];
+    beta[j] = sqrt(warp_sum(C * wv * wv));
+    qq = j + 1;
+    if (j + 1 == q || !(beta[j] > 1e-10 * fabs(alpha[j]))) break;
+    V[j + 1] = wv / beta[j];
+  }
+  double T[4][4], Q[4][4], ev[4];
+  for (int a = 0; a < 4; ++a)
+    for (int b = 0; b < 4; ++b)
+      T[a][b] = (a >= qq || b >= qq) ? 0.0 : a == b ? alpha[a] : (a + 1 == b ? beta[a] : (b + 1 == a ? beta[b] : 0.0));
+  jacobi4(qq, T, ev, Q);
+  double lmax = 0.0;
+  for (int k = 0; k < qq; ++k) lmax = fmax(lmax, ev[k]);
+  bool stable = true;
+  float lam[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int k = 0; k < qq; ++k) {
+    if (ev[k] < -1e-9 * lmax) stable = false;
+    lam[k] = ev[k] < 0.0 ? 0.f : (float)ev[k];
+  }
+  if (lane == 0) c.arn_lam[drv] = stable ? make_float4(lam[0], lam[1], lam[2], lam[3]) : make_float4(-1.f, 0.f, 0.f, 0.f);
+  if (!stable || !act || nd.w == kNone) return;
+  const double sq = sqrt(ctot);
+  float r[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int k = 0; k < qq; ++k) {
+    double a = 0.0;
+    for (int j = 0; j < qq; ++j) a += V[j] * Q[j][k];
+    r[k] = (float)(a * sq * Q[0][k]);
+  }
+  c.arn_res[nd.w] = make_float4(r[0], r[1], r[2], r[3]);
+}
+
 }  // namespace
 
 cudaError_t launch_arn_reduce(const Topo& t, const Batch& b, cudaStream_t s) {
   if (!t.n_arn_nets) return cudaSuccess;
   const dim3 g((uint32_t)((32ull * t.n_arn_nets + kArnThreads - 1) / kArnThreads), b.K);
+  arn_small_kernel<<<g, kArnThreads, 0, s>>>(t, b);
   arn_reduce_kernel<<<g, kArnThreads, 0, s>>>(t, b);
   return cudaGetLastError();
 }

@@ -14,33 +14,39 @@
 
 namespace sta {
 
-// y(t) and y'(t) of the ramp response, order <= 4 (unused terms res 0)
-__device__ __forceinline__ void arn_resp(const float4& lam, const float4& res, float D, float t, float& y,
-                                         float& dy) {
-  const float L[4] = {lam.x, lam.y, lam.z, lam.w}, K[4] = {res.x, res.y, res.z, res.w};
+// per-term constants of one crossing solve: 1 / lam, and e^{D/lam} - 1 for
+// the post-ramp tail while D / lam < 1
+struct ArnTerm {
+  float k, l, il, eD;
+  bool live, small;
+};
+
+// y(t) and y'(t) of the ramp response, order <= 4 (terms with residue 0 skipped)
+__device__ __forceinline__ void arn_resp(const ArnTerm (&T)[4], float D, float t, float& y, float& dy) {
   y = 0.f;
   dy = 0.f;
+  if (t <= 0.f) return;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const float l = L[k];
+    if (!T[k].live) continue;
+    const float l = T[k].l;
     float g, dg;
-    if (t <= 0.f) {
-      g = 0.f;
-      dg = 0.f;
-    } else if (D <= 0.f) {                     // a step
+    if (D <= 0.f) {                            // a step
       if (l > 0.f) {
-        const float e = __expf(-t / l);
-        g = -expm1f(-t / l);
-        dg = e / l;
+        const float x = t * T[k].il;
+        const float e = __expf(-x);
+        g = x < 0.25f ? -expm1f(-x) : 1.f - e;
+        dg = e * T[k].il;
       } else {
         g = 1.f;
         dg = 0.f;
       }
-    } else if (t <= D) {                       // on the ramp: (t + l expm1(-t/l)) / D
+    } else if (t <= D) {                       // on the ramp: (t - l (1 - e^{-t/l})) / D
       if (l > 0.f) {
-        const float em = expm1f(-t / l);
-        g = (t + l * em) / D;
-        dg = -em / D;
+        const float x = t * T[k].il;
+        const float om = x < 0.25f ? -expm1f(-x) : 1.f - __expf(-x);
+        g = (t - l * om) / D;
+        dg = om / D;
       } else {
         g = t / D;
         dg = 1.f / D;
@@ -49,8 +55,8 @@ __device__ __forceinline__ void arn_resp(const float4& lam, const float4& res, f
       if (l > 0.f) {
         // e^{-t/l} expm1(D/l) while D/l < 1 (no cancellation, no overflow),
         // the plain difference beyond (its cancellation is bounded there)
-        const float r = D / l;
-        const float a = r < 1.f ? __expf(-t / l) * expm1f(r) : __expf(-(t - D) / l) - __expf(-t / l);
+        const float et = __expf(-t * T[k].il);
+        const float a = T[k].small ? et * T[k].eD : __expf(-(t - D) * T[k].il) - et;
         g = 1.f - (l / D) * a;
         dg = a / D;
       } else {
@@ -58,32 +64,50 @@ __device__ __forceinline__ void arn_resp(const float4& lam, const float4& res, f
         dg = 0.f;
       }
     }
-    y += K[k] * g;
-    dy += K[k] * dg;
+    y += T[k].k * g;
+    dy += T[k].k * dg;
   }
 }
 
-// first time the response reaches theta: Newton inside a shrinking bracket,
-// bisection when a step leaves it
+// first time the response reaches theta: Newton inside a shrinking bracket
+// (bisection when a step leaves it), from the single-pole estimate with the
+// model's first moment
 __device__ __noinline__ float arn_cross(float4 lam, float4 res, float D, float theta) {
-  const float lmax = fmaxf(fmaxf(lam.x, lam.y), fmaxf(lam.z, lam.w));
+  const float L[4] = {lam.x, lam.y, lam.z, lam.w}, K[4] = {res.x, res.y, res.z, res.w};
+  ArnTerm T[4];
+  float lmax = 0.f, m1 = 0.f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    T[k].k = K[k];
+    T[k].l = L[k];
+    T[k].live = K[k] != 0.f;
+    T[k].il = L[k] > 0.f ? 1.f / L[k] : 0.f;
+    const float r = L[k] > 0.f ? D * T[k].il : 2.f;
+    T[k].small = r < 1.f;
+    T[k].eD = T[k].small ? expm1f(r) : 0.f;
+    if (T[k].live) {
+      lmax = fmaxf(lmax, L[k]);
+      m1 += K[k] * L[k];
+    }
+  }
   float lo = 0.f, hi = D + 50.f * lmax + 1e-3f;
   float y, dy;
   for (int g = 0; g < 24; ++g) {
-    arn_resp(lam, res, D, hi, y, dy);
+    arn_resp(T, D, hi, y, dy);
     if (y >= theta) break;
     hi *= 2.f;
   }
-  float t = fminf(0.5f * D + 0.7f * lmax, 0.5f * hi);
-  for (int it = 0; it < 60; ++it) {
-    arn_resp(lam, res, D, t, y, dy);
+  float t = fminf(fmaxf(theta * D + __logf(1.f / (1.f - theta)) * fmaxf(m1, 0.f), 1e-6f), 0.5f * hi);
+  for (int it = 0; it < 40; ++it) {
+    arn_resp(T, D, t, y, dy);
     if (y >= theta) hi = t;
     else lo = t;
+    if (y == theta) break;
     float tn = dy > 0.f ? t - (y - theta) / dy : 0.5f * (lo + hi);
     if (!(tn > lo && tn < hi)) tn = 0.5f * (lo + hi);
     const float step = fabsf(tn - t);
     t = tn;
-    if (step <= 1e-7f * fmaxf(t, 1e-3f) || hi - lo <= 1e-7f * fmaxf(hi, 1e-3f)) break;
+    if (step <= 3e-7f * fmaxf(t, 1e-3f) || hi - lo <= 3e-7f * fmaxf(hi, 1e-3f)) break;
   }
   return t;
 }
