@@ -13,10 +13,17 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 timeout 900 python bench.py --config c5_multicorner --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench_c5_${T}.json 2> gpurun_out/bench_c5_${T}.err
 timeout 1200 python scripts/bench_configs.py > gpurun_out/bench_configs_${T}.json 2> gpurun_out/bench_configs_${T}.err
 timeout 900 python scripts/bench_tdp.py --iters 1000 --check > gpurun_out/bench_c4_${T}.json 2> gpurun_out/bench_c4_${T}.err
+# rows f1 / f2: Arnoldi net model (C2 / C4 / C3), Steiner RC (C4 with full parity, C3), latency probe
+for cfg in c2_tau c4_tdp c3_superblue; do
+timeout 600 python bench.py --config $cfg --net-model arnoldi --steps 10 --warmup 3 --no-cpu-baseline --quick --phases > gpurun_out/bench_arnoldi_${cfg}_${T}.json 2> gpurun_out/bench_arnoldi_${cfg}_${T}.err
+done
+timeout 900 python scripts/bench_steiner.py c4_tdp --full-parity > gpurun_out/steiner_c4_${T}.json 2> gpurun_out/steiner_c4_${T}.err
+timeout 900 python scripts/bench_steiner.py c3_superblue --reps 3 > gpurun_out/steiner_c3_${T}.json 2> gpurun_out/steiner_c3_${T}.err
+timeout 600 python scripts/latency_probe.py > gpurun_out/latency_${T}.txt 2>&1
 if [ "${NCU:-1}" = 1 ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_${T}.csv python bench.py --steps 3 --warmup 3 --quick > gpurun_out/ncu_launch_${T}.log 2>&1
-for K in fwd_persistent bwd_persistent rc_warp tc_event; do
+for K in fwd_persistent bwd_persistent rc_warp tc_event tc_node; do
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:${K} \
     --launch-skip 3 --launch-count 1 -o gpurun_out/prof_${T}_${K} \
     python bench.py --steps 1 --warmup 3 --quick > gpurun_out/ncu_${K}_${T}.log 2>&1

@@ -31,3 +31,17 @@ for mode in ("0", "1"):
         ctx.report_paths(0, "setup", k=20, nworst=2)       # row f3 kernels
         ctx.close()
         print("ok", mode, d.name, flush=True)
+
+# rows f1 (Arnoldi net model, persistent kernels) and f2 (Steiner RC)
+os.environ["STA_STAGE_KERNELS"] = "0"
+for d in designs[:2]:
+    ctx = sta.Context(0, d.num_corners)
+    sta.load_design(ctx, d)
+    ctx.set_net_model("arnoldi", 4)
+    ctx.update_timing()
+    ctx.synchronize()
+    compare_update(ctx, oracle.update(d, net_model="arnoldi"))
+    x, y = synth.placement(d, seed=2, grid=True)
+    g = ctx.build_steiner(x, y, **synth.STEINER_UNITS)
+    ctx.close()
+    print("ok arnoldi + steiner", d.name, int(g[0][-1]), flush=True)
