@@ -232,7 +232,7 @@ struct sta_ctx_s {
   Arena steiner_arena;                           // Steiner RC (row f2): static plan + scratch, lazily
   bool steiner_ready = false;
   const u32 *st_net_ptr = nullptr, *st_spins = nullptr, *st_warp = nullptr, *st_smem = nullptr, *st_big = nullptr;
-  u32 st_n_warp = 0, st_n_smem = 0, st_n_big = 0, st_max_smem = 0;
+  u32 st_n_warp = 0, st_n_smem = 0, st_n_big = 0, st_max_smem = 0, st_max_big = 0;
   sta::SteinerArgs st_args{};
   void* st_scan = nullptr;
   size_t st_scan_bytes = 0;
@@ -1300,6 +1300,7 @@ void prepare(sta_ctx c) {
   t.net_model = (u32)c->net_model;
   t.arn_q = c->arn_q;
   t.n_arn_nets = 0;
+  t.n_arn_big = 0;
   t.n_rc_nodes = c->n_rc;
   if (c->net_model == 1) {
     std::vector<u32> inv(c->n_rc);
@@ -1326,6 +1327,11 @@ void prepare(sta_ctx c) {
     }
     t.n_arn_nets = (u32)nets.size();
     t.arn_nets = c->arn_arena.upload(nets, s);
+    std::vector<u32> big;
+    for (u32 j = 0; j < t.n_arn_nets; ++j)
+      if (nets[j].y > 1024) big.push_back(j);
+    t.n_arn_big = (u32)big.size();
+    t.arn_big = c->arn_arena.upload(big, s);
     t.arn_node = c->arn_arena.upload(an, s);
     t.arn_scap = c->arn_arena.upload(scap, s);
   }
@@ -1609,14 +1615,14 @@ void steiner_plan(sta_ctx c) {
   const u32 N = c->N, NNP = N ? c->net_ptr[N] : 0;
   std::vector<u32> spins(c->net_pins);
   std::vector<u32> warp, smem, big;
-  u32 max_smem = 0;
+  u32 max_smem = 0, max_big = 0;
   const u32 lim = sta::steiner_smem_pins();
   for (u32 n = 0; n < N; ++n) {
     const u32 a = c->net_ptr[n], b = c->net_ptr[n + 1], m = b - a;
     std::sort(spins.begin() + a + 1, spins.begin() + b);
     if (m >= 2 && m <= 32) warp.push_back(n);
     else if (m > 32 && m <= lim) { smem.push_back(n); max_smem = std::max(max_smem, m); }
-    else if (m > lim) big.push_back(n);
+    else if (m > lim) { big.push_back(n); max_big = std::max(max_big, m); }
   }
   Arena& g = c->steiner_arena;
   cudaStream_t s = c->stream;
@@ -1629,6 +1635,7 @@ void steiner_plan(sta_ctx c) {
   c->st_n_smem = (u32)smem.size();
   c->st_n_big = (u32)big.size();
   c->st_max_smem = max_smem;
+  c->st_max_big = max_big;
   sta::SteinerArgs& a = c->st_args;
   a = sta::SteinerArgs{};
   a.net_ptr = c->st_net_ptr;
@@ -1884,7 +1891,7 @@ sta_status sta_build_steiner(sta_ctx c, sta_mem mem, const float* pin_x, const f
       a.rc_ptr = rc_ptr; a.parent = parent; a.node_pin = node_pin; a.res = res; a.cap = cap;
     }
     ck(sta::run_steiner(a, N, c->st_warp, c->st_n_warp, c->st_smem, c->st_n_smem, c->st_big, c->st_n_big,
-                        c->st_max_smem, c->st_scan, c->st_scan_bytes, s), "steiner kernels");
+                        c->st_max_smem, c->st_max_big, c->st_scan, c->st_scan_bytes, s), "steiner kernels");
     u32 nn = 0;
     ck(cudaMemcpyAsync(&nn, a.rc_ptr + N, sizeof(u32), cudaMemcpyDeviceToHost, s), "D2H");
     ck(cudaStreamSynchronize(s), "steiner");

@@ -27,6 +27,8 @@ namespace {
 
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 constexpr int kArnThreads = 256;
+constexpr uint32_t kArnBlockMin = 1024;        // nets above: one block of kArnBlock threads each
+constexpr int kArnBlock = 1024;
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(kArnThreads) arn_reduce_kernel(Topo t, const _
   const uint4 net = __ldg(t.arn_nets + w);
   const uint32_t x0 = net.x, m = net.y, drv = net.z;
   const int q = (int)t.arn_q;
-  if (m <= 32) return;                         // arn_small_kernel
+  if (m <= 32 || m > kArnBlockMin) return;    // arn_small_kernel / arn_block_kernel
   const float* R = c.rc_vals[0];
   const float* Cw = c.rc_vals[1];
   const size_t n = t.n_rc_nodes;
@@ -383,6 +385,222 @@ __global__ void __launch_bounds__(kArnThreads) arn_small_kernel(Topo t, const __
   c.arn_res[nd.w] = make_float4(r[0], r[1], r[2], r[3]);
 }
 
+
+// ---- nets of more than kArnBlockMin RC nodes: one block of kArnBlock
+// threads per net, the same passes in 1024-node chunks (block scans and sums
+// through shared memory, the in-chunk pointer jumping in shared memory).
+struct BlkSh {
+  double red[kArnBlock / 32][4];
+  double acc[kArnBlock];
+  uint32_t ptr[kArnBlock];
+  double carry;
+};
+
+// sums of up to 4 values over the block (every thread gets them)
+__device__ __forceinline__ void block_sum4(double (&v)[4], int nv, BlkSh& sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int k = 0; k < nv; ++k) v[k] = warp_sum(v[k]);
+  __syncthreads();
+  if (lane == 0)
+    for (int k = 0; k < nv; ++k) sh.red[wid][k] = v[k];
+  __syncthreads();
+  for (int k = 0; k < nv; ++k) {
+    double x = lane < kArnBlock / 32 ? sh.red[lane][k] : 0.0;
+    v[k] = warp_sum(x);
+  }
+}
+
+// inclusive scan over the block; *total = the block's sum
+__device__ __forceinline__ double block_incl_scan(double v, BlkSh& sh, double* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const double inc = warp_incl_scan(v, lane);
+  __syncthreads();
+  if (lane == 31) sh.red[wid][0] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    const double x = lane < kArnBlock / 32 ? sh.red[lane][0] : 0.0;
+    sh.red[lane][1] = warp_incl_scan(x, lane);
+  }
+  __syncthreads();
+  *total = sh.red[kArnBlock / 32 - 1][1];
+  return inc + (wid ? sh.red[wid - 1][1] : 0.0);
+}
+
+__device__ void tree_apply_blk(const Topo& t, const float* __restrict__ R, const ArnScr& s, const double* x,
+                               uint32_t x0, uint32_t m, BlkSh& sh) {
+  const int tid = threadIdx.x;
+  double carry = 0.0;
+  for (uint32_t c0 = 0; c0 < m; c0 += kArnBlock) {
+    const uint32_t i = x0 + c0 + tid;
+    const double v = c0 + tid < m ? s.C[i] * x[i] : 0.0;
+    double tot;
+    const double inc = block_incl_scan(v, sh, &tot);
+    if (c0 + tid < m) s.P[i] = carry + inc - v;
+    carry += tot;
+  }
+  const double total = carry;
+  __syncthreads();
+  for (uint32_t c0 = 0; c0 < m; c0 += kArnBlock) {
+    const uint32_t i = x0 + c0 + tid;
+    const bool act = c0 + tid < m;
+    double acc = 0.0;
+    uint32_t ptr = kNone;
+    if (act) {
+      const uint4 nd = __ldg(t.arn_node + i);
+      if (nd.y != kNone) {
+        const double S = (nd.z == x0 + m ? total : s.P[nd.z]) - s.P[i];
+        acc = (double)R[nd.x] * S;
+        ptr = nd.y;
+      }
+    }
+    const uint32_t cs = x0 + c0;
+    sh.acc[tid] = acc;
+    sh.ptr[tid] = ptr;
+    __syncthreads();
+    for (int r = 0; r < 10; ++r) {
+      const bool in = ptr != kNone && ptr >= cs;
+      double pa = 0.0;
+      uint32_t pp = ptr;
+      if (in) {
+        pa = sh.acc[ptr - cs];
+        pp = sh.ptr[ptr - cs];
+      }
+      __syncthreads();
+      if (in) {
+        acc += pa;
+        ptr = pp;
+        sh.acc[tid] = acc;
+        sh.ptr[tid] = ptr;
+      }
+      const int more = __syncthreads_or(ptr != kNone && ptr >= cs);
+      if (!more) break;
+    }
+    if (act) s.W[i] = acc + (ptr != kNone ? s.W[ptr] : 0.0);
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kArnBlock, 1) arn_block_kernel(Topo t, const __grid_constant__ Batch B,
+                                                                 const uint32_t* __restrict__ big, uint32_t n_big) {
+  __shared__ BlkSh sh;
+  const int tid = threadIdx.x;
+  const CornerDev& c = B.c[blockIdx.y];
+  const uint4 net = __ldg(t.arn_nets + big[blockIdx.x]);
+  const uint32_t x0 = net.x, m = net.y, drv = net.z;
+  const int q = (int)t.arn_q;
+  const float* R = c.rc_vals[0];
+  const float* Cw = c.rc_vals[1];
+  const size_t n = t.n_rc_nodes;
+  ArnScr s{c.arn_scr, c.arn_scr + n, c.arn_scr + (size_t)(q + 2) * n, c.arn_scr + (size_t)(q + 3) * n, n};
+  double v4[4] = {0, 0, 0, 0};
+  for (uint32_t c0 = 0; c0 < m; c0 += kArnBlock) {
+    const uint32_t i = x0 + c0 + tid;
+    if (c0 + tid < m) {
+      const uint4 nd = __ldg(t.arn_node + i);
+      const double C = nd.y == kNone ? 0.0 : (double)Cw[nd.x] + (double)__ldg(t.arn_scap + i);
+      s.C[i] = C;
+      v4[0] += C;
+    }
+  }
+  block_sum4(v4, 1, sh);
+  const double ctot = v4[0];
+  if (!(ctot > 0.0)) {
+    if (tid == 0) c.arn_lam[drv] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint32_t c0 = 0; c0 < m; c0 += kArnBlock) {
+      const uint32_t i = x0 + c0 + tid;
+      if (c0 + tid < m) {
+        const uint32_t tag = __ldg(t.arn_node + i).w;
+        if (tag != kNone) c.arn_res[tag] = make_float4(1.f, 0.f, 0.f, 0.f);
+      }
+    }
+    return;
+  }
+  const double inv = 1.0 / sqrt(ctot);
+  for (uint32_t c0 = 0; c0 < m; c0 += kArnBlock) {
+    const uint32_t i = x0 + c0 + tid;
+    if (c0 + tid < m) s.V[i] = __ldg(t.arn_node + i).y != kNone ? inv : 0.0;
+  }
+  __syncthreads();
+  double alpha[4] = {0, 0, 0, 0}, beta[4] = {0, 0, 0, 0};
+  int qq = 0;
+  for (int j = 0; j < q; ++j) {
+    tree_apply_blk(t, R, s, s.V + (size_t)j * n, x0, m, sh);
+    double d[4] = {0, 0, 0, 0};
+    for (uint32_t c0 = 0; c0 < m; c0 += kArnBlock) {
+      const uint32_t i = x0 + c0 + tid;
+      if (c0 + tid < m) {
+        double wi = s.W[i];
+        if (j > 0) wi -= beta[j - 1] * s.V[(size_t)(j - 1) * n + i];
+        s.W[i] = wi;
+        const double cw = s.C[i] * wi;
+        for (int k = 0; k <= j; ++k) d[k] += cw * s.V[(size_t)k * n + i];
+      }
+    }
+    block_sum4(d, j + 1, sh);
+    alpha[j] = d[j];
+    double e[4] = {0, 0, 0, 0};
+    for (uint32_t c0 = 0; c0 < m; c0 += kArnBlock) {
+      const uint32_t i = x0 + c0 + tid;
+      if (c0 + tid < m) {
+        double wi = s.W[i];
+        for (int k = 0; k <= j; ++k) wi -= d[k] * s.V[(size_t)k * n + i];
+        s.W[i] = wi;
+        const double cw = s.C[i] * wi;
+        for (int k = 0; k <= j; ++k) e[k] += cw * s.V[(size_t)k * n + i];
+      }
+    }
+    block_sum4(e, j + 1, sh);
+    double nn[4] = {0, 0, 0, 0};
+    for (uint32_t c0 = 0; c0 < m; c0 += kArnBlock) {
+      const uint32_t i = x0 + c0 + tid;
+      if (c0 + tid < m) {
+        double wi = s.W[i];
+        for (int k = 0; k <= j; ++k) wi -= e[k] * s.V[(size_t)k * n + i];
+        s.W[i] = wi;
+        nn[0] += s.C[i] * wi * wi;
+      }
+    }
+    block_sum4(nn, 1, sh);
+    beta[j] = sqrt(nn[0]);
+    qq = j + 1;
+    if (j + 1 == q || !(beta[j] > 1e-10 * fabs(alpha[j]))) break;
+    for (uint32_t c0 = 0; c0 < m; c0 += kArnBlock) {
+      const uint32_t i = x0 + c0 + tid;
+      if (c0 + tid < m) s.V[(size_t)(j + 1) * n + i] = s.W[i] / beta[j];
+    }
+    __syncthreads();
+  }
+  double T[4][4], Q[4][4], ev[4];
+  for (int a = 0; a < 4; ++a)
+    for (int b = 0; b < 4; ++b)
+      T[a][b] = (a >= qq || b >= qq) ? 0.0 : a == b ? alpha[a] : (a + 1 == b ? beta[a] : (b + 1 == a ? beta[b] : 0.0));
+  jacobi4(qq, T, ev, Q);
+  double lmax = 0.0;
+  for (int k = 0; k < qq; ++k) lmax = fmax(lmax, ev[k]);
+  bool stable = true;
+  float lam[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int k = 0; k < qq; ++k) {
+    if (ev[k] < -1e-9 * lmax) stable = false;
+    lam[k] = ev[k] < 0.0 ? 0.f : (float)ev[k];
+  }
+  if (tid == 0) c.arn_lam[drv] = stable ? make_float4(lam[0], lam[1], lam[2], lam[3]) : make_float4(-1.f, 0.f, 0.f, 0.f);
+  if (!stable) return;
+  const double sq = sqrt(ctot);
+  for (uint32_t c0 = 0; c0 < m; c0 += kArnBlock) {
+    const uint32_t i = x0 + c0 + tid;
+    if (c0 + tid >= m) continue;
+    const uint32_t tag = __ldg(t.arn_node + i).w;
+    if (tag == kNone) continue;
+    float r[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int k = 0; k < qq; ++k) {
+      double a = 0.0;
+      for (int j = 0; j < qq; ++j) a += s.V[(size_t)j * n + i] * Q[j][k];
+      r[k] = (float)(a * sq * Q[0][k]);
+    }
+    c.arn_res[tag] = make_float4(r[0], r[1], r[2], r[3]);
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_arn_reduce(const Topo& t, const Batch& b, cudaStream_t s) {
@@ -390,6 +608,7 @@ cudaError_t launch_arn_reduce(const Topo& t, const Batch& b, cudaStream_t s) {
   const dim3 g((uint32_t)((32ull * t.n_arn_nets + kArnThreads - 1) / kArnThreads), b.K);
   arn_small_kernel<<<g, kArnThreads, 0, s>>>(t, b);
   arn_reduce_kernel<<<g, kArnThreads, 0, s>>>(t, b);
+  if (t.n_arn_big) arn_block_kernel<<<dim3(t.n_arn_big, b.K), kArnBlock, 0, s>>>(t, b, t.arn_big, t.n_arn_big);
   return cudaGetLastError();
 }
 

@@ -192,6 +192,8 @@ struct Topo {
   const uint4* arn_node;      // [n_rc] {caller node id, internal parent or kNone at the root,
                               //  subtree end (internal), sink index or kNone}
   const float* arn_scap;      // [n_rc] pin + PO cap at the node
+  uint32_t n_arn_big;
+  const uint32_t* arn_big;    // indices (into arn_nets) of the nets of more than 1024 RC nodes
   uint64_t n_rc_nodes;
 };
 
@@ -343,10 +345,13 @@ struct SteinerArgs {
 };
 // Enqueue the construction on s.  warp_nets: nets of 2..32 pins; smem_nets:
 // 33..steiner_smem_pins() pins (max_smem_pins = their largest); big_nets:
-// larger.  scan_tmp: steiner_scan_bytes(N) bytes.
+// larger (max_big_pins = their largest: one 8-CTA cluster per net up to
+// 102,400 pins, one block with a global scratch beyond).  scan_tmp:
+// steiner_scan_bytes(N) bytes.
 cudaError_t run_steiner(const SteinerArgs& a, uint32_t N, const uint32_t* warp_nets, uint32_t n_warp,
                         const uint32_t* smem_nets, uint32_t n_smem, const uint32_t* big_nets, uint32_t n_big,
-                        uint32_t max_smem_pins, void* scan_tmp, size_t scan_bytes, cudaStream_t s);
+                        uint32_t max_smem_pins, uint32_t max_big_pins, void* scan_tmp, size_t scan_bytes,
+                        cudaStream_t s);
 size_t steiner_scan_bytes(uint32_t N);
 uint32_t steiner_smem_pins();
 

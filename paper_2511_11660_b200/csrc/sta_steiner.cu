@@ -24,6 +24,7 @@
 // then emits the nodes in Prim order (caps summed in that fixed order:
 // deterministic).  Prim is O(m^2) per net, as the specified algorithm is;
 // the high-fan-out nets dominate the time.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cub/device/device_scan.cuh>
@@ -174,6 +175,102 @@ __global__ void __launch_bounds__(kPrimThreads) prim_block_kernel(SteinerArgs a,
   if (threadIdx.x == 0) a.cnt[n] = m + s_nb;
 }
 
+
+// Nets too large for one block's shared memory (> kSmemPins pins): one
+// thread-block CLUSTER of kClusterCtas CTAs per net (distributed shared
+// memory).  CTA r holds the per-pin state of pins [r chunk, (r+1) chunk);
+// every step each CTA relaxes its pins against the pin added last and
+// reduces its arg-min, the CTAs exchange their minima through DSMEM (one
+// cluster barrier per step, double-buffered by step parity), every warp
+// reduces the kClusterCtas minima itself, and the owner of the winner marks
+// it and records it.  Same decisions as the single-block kernel.
+constexpr int kClusterCtas = 8;
+constexpr int kClusterThreads = 1024;
+constexpr uint32_t kClusterChunk = 12800;      // pins per CTA: 200 KB of state
+
+__global__ void __launch_bounds__(kClusterThreads, 1) prim_cluster_kernel(SteinerArgs a, const uint32_t* __restrict__ nets,
+                                                                          uint32_t n_nets) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ float4 s_pin[];
+  __shared__ unsigned long long s_red[kClusterThreads / 32];
+  __shared__ unsigned long long s_cmin[2];
+  __shared__ uint32_t s_nb;
+  const uint32_t rank = cluster.block_rank();
+  const uint32_t n = nets[blockIdx.x / kClusterCtas], off = a.net_ptr[n], m = a.net_ptr[n + 1] - off;
+  const uint32_t chunk = (m + kClusterCtas - 1) / kClusterCtas;
+  const uint32_t k0 = rank * chunk, k1 = min(m, k0 + chunk);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_nb = 0;
+  const float x0 = a.x[a.spins[off]], y0 = a.y[a.spins[off]];
+  for (uint32_t k = k0 + threadIdx.x; k < k1; k += kClusterThreads) {
+    const uint32_t p = a.spins[off + k];
+    const float px = a.x[p], py = a.y[p];
+    s_pin[k - k0] = make_float4(px, py, k ? mdist(x0, y0, px, py) : -1.f, __uint_as_float(0u));
+  }
+  if (rank == 0 && threadIdx.x == 0) {
+    a.ord[off] = 0;
+    a.ppos[off] = kNone;
+  }
+  cluster.sync();
+  float bx = x0, by = y0;
+  for (uint32_t step = 1; step < m; ++step) {
+    unsigned long long best = ~0ull;
+    for (uint32_t k = k0 + threadIdx.x; k < k1; k += kClusterThreads) {
+      float4 st = s_pin[k - k0];
+      if (st.z < 0.f) continue;
+      if (step > 1) {
+        const float d = mdist(bx, by, st.x, st.y);
+        if (d < st.z) {
+          st.z = d;
+          st.w = __uint_as_float(step - 1);
+          s_pin[k - k0] = st;
+        }
+      }
+      const unsigned long long kk = akey(st.z, k);
+      best = kk < best ? kk : best;
+    }
+    best = warp_min64(best);
+    if (lane == 0) s_red[wid] = best;
+    __syncthreads();
+    if (wid == 0) {
+      unsigned long long v = s_red[lane];      // kClusterThreads / 32 == 32 warps
+      v = warp_min64(v);
+      if (lane == 0) s_cmin[step & 1] = v;
+    }
+    cluster.sync();                            // every CTA's minimum of this step is visible
+    unsigned long long g = ~0ull;
+    if (lane < kClusterCtas) g = *cluster.map_shared_rank(&s_cmin[step & 1], lane);
+    g = warp_min64(g);
+    const uint32_t wk = (uint32_t)g, owner = wk / chunk;
+    float4 ws = make_float4(0.f, 0.f, 0.f, 0.f);   // the winner's position, read by lane 0 of each warp
+    if (lane == 0) ws = *cluster.map_shared_rank(&s_pin[wk - owner * chunk], owner);
+    bx = __shfl_sync(kFull, ws.x, 0);
+    by = __shfl_sync(kFull, ws.y, 0);
+    if (owner == rank && (wk - k0) % kClusterThreads == threadIdx.x) {   // the winner's own thread
+      a.ord[off + step] = wk;
+      a.ppos[off + step] = __float_as_uint(s_pin[wk - k0].w);
+      s_pin[wk - k0].z = -1.f;
+    }
+  }
+  cluster.sync();
+  // bends of the pins this CTA owns (by Prim position), summed on rank 0
+  uint32_t nb = 0;
+  for (uint32_t q = 1 + rank * kClusterThreads + threadIdx.x; q < m; q += kClusterCtas * kClusterThreads) {
+    const uint32_t k = a.ord[off + q], pk = a.ord[off + a.ppos[off + q]];
+    const uint32_t pv = a.spins[off + k], pu = a.spins[off + pk];
+    nb += fabsf(a.x[pv] - a.x[pu]) != 0.f && fabsf(a.y[pv] - a.y[pu]) != 0.f;
+  }
+  atomicAdd(&s_nb, nb);
+  cluster.sync();
+  if (rank == 0 && threadIdx.x == 0) {
+    uint32_t tot = 0;
+    for (int r = 0; r < kClusterCtas; ++r) tot += *cluster.map_shared_rank(&s_nb, r);
+    a.cnt[n] = m + tot;
+  }
+  cluster.sync();                              // no CTA exits while rank 0 reads its s_nb
+}
+
 // one thread per net: nodes in Prim order (a Steiner node right before its
 // pin), caps summed in that order
 __global__ void __launch_bounds__(256) steiner_fill_kernel(SteinerArgs a, uint32_t N) {
@@ -239,7 +336,8 @@ inline uint32_t cdiv(uint64_t a, uint64_t b) { return (uint32_t)((a + b - 1) / b
 
 cudaError_t run_steiner(const SteinerArgs& a, uint32_t N, const uint32_t* warp_nets, uint32_t n_warp,
                         const uint32_t* smem_nets, uint32_t n_smem, const uint32_t* big_nets, uint32_t n_big,
-                        uint32_t max_smem_pins, void* scan_tmp, size_t scan_bytes, cudaStream_t s) {
+                        uint32_t max_smem_pins, uint32_t max_big_pins, void* scan_tmp, size_t scan_bytes,
+                        cudaStream_t s) {
   if (!N) return cudaSuccess;
   steiner_small_kernel<<<cdiv(N, 256), 256, 0, s>>>(a, N);
   if (n_warp) prim_warp_kernel<<<cdiv(32ull * n_warp, 256), 256, 0, s>>>(a, warp_nets, n_warp);
@@ -249,7 +347,31 @@ cudaError_t run_steiner(const SteinerArgs& a, uint32_t N, const uint32_t* warp_n
     if (e != cudaSuccess) return e;
     prim_block_kernel<true><<<n_smem, kPrimThreads, sm, s>>>(a, smem_nets, n_smem);
   }
-  if (n_big) prim_block_kernel<false><<<n_big, kPrimThreads, 0, s>>>(a, big_nets, n_big);
+  if (n_big) {
+    // distributed over a cluster when the largest fits 8 CTAs' shared memory
+    if (max_big_pins <= kClusterCtas * kClusterChunk) {
+      uint32_t chunk = (max_big_pins + kClusterCtas - 1) / kClusterCtas;
+      const size_t sm = 16ull * chunk;
+      cudaError_t e = cudaFuncSetAttribute(prim_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e != cudaSuccess) return e;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(n_big * kClusterCtas);
+      cfg.blockDim = dim3(kClusterThreads);
+      cfg.dynamicSmemBytes = sm;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = kClusterCtas;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      e = cudaLaunchKernelEx(&cfg, prim_cluster_kernel, a, big_nets, n_big);
+      if (e != cudaSuccess) return e;
+    } else {
+      prim_block_kernel<false><<<n_big, kPrimThreads, 0, s>>>(a, big_nets, n_big);
+    }
+  }
   // rc_ptr = exclusive scan of the node counts (cnt has N + 1 entries, the last 0)
   cudaError_t e = cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, a.cnt, a.rc_ptr, N + 1, s);
   if (e != cudaSuccess) return e;
