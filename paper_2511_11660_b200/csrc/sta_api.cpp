@@ -25,11 +25,19 @@
 #include "../../include/sta.h"
 #include "sta_internal.h"
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: API ranges for nsys / ncu timelines
+
 using sta::kNone;
 using u32 = uint32_t;
 using u64 = uint64_t;
 
 namespace {
+
+// NVTX range of one API call (visible in an nsys / ncu --nvtx timeline)
+struct Nvtx {
+  explicit Nvtx(const char* n) { nvtxRangePushA(n); }
+  ~Nvtx() { nvtxRangePop(); }
+};
 
 // STA_TIMING=1: host phase times of sta_load_graph / sta_set_rc_tree on stderr
 struct PhaseTimer {
@@ -1741,6 +1749,7 @@ const char* sta_last_error(sta_ctx c) { return c ? c->err.c_str() : "null ctx"; 
 
 sta_status sta_load_graph(sta_ctx c, const sta_graph_desc* d) {
   return guard(c, [&] {
+    Nvtx nvtx_range("sta_load_graph");
     PhaseTimer tm;
     if (!d) fail(STA_ERR_ARG, "desc is NULL");
     c->has_graph = c->has_tree = c->has_cons = c->prepared = false;
@@ -1776,6 +1785,7 @@ sta_status sta_load_graph(sta_ctx c, const sta_graph_desc* d) {
 sta_status sta_set_library(sta_ctx c, uint32_t corner, sta_mem mem, uint32_t num_tables, const uint8_t* n1,
                            const uint8_t* n2, const uint32_t* off, const float* data, uint32_t data_len) {
   return guard(c, [&] {
+    Nvtx nvtx_range("sta_set_library");
     CornerState& cs = corner_of(c, corner);
     if (!c->has_graph) fail(STA_ERR_ORDER, "sta_set_library before sta_load_graph");
     if (num_tables != c->T) fail(STA_ERR_ARG, "library has %u tables, graph expects %u", num_tables, c->T);
@@ -1842,6 +1852,7 @@ sta_status sta_set_library(sta_ctx c, uint32_t corner, sta_mem mem, uint32_t num
 
 sta_status sta_set_net_model(sta_ctx c, sta_net_model model, uint32_t q) {
   return guard(c, [&] {
+    Nvtx nvtx_range("sta_set_net_model");
     if (model != STA_NET_ELMORE && model != STA_NET_ARNOLDI) fail(STA_ERR_ARG, "net model %d", (int)model);
     if (model == STA_NET_ARNOLDI && (q < 1 || q > 4)) fail(STA_ERR_ARG, "Arnoldi order %u outside 1..4", q);
     if (c->net_model != (int)model || (model == STA_NET_ARNOLDI && c->arn_q != q)) {
@@ -1858,6 +1869,7 @@ sta_status sta_build_steiner(sta_ctx c, sta_mem mem, const float* pin_x, const f
                              const sta_steiner_units* u, uint32_t node_capacity, uint32_t* rc_ptr,
                              int32_t* parent, uint32_t* node_pin, float* res, float* cap, uint32_t* num_nodes) {
   return guard(c, [&] {
+    Nvtx nvtx_range("sta_build_steiner");
     if (!c->has_graph) fail(STA_ERR_ORDER, "sta_build_steiner before sta_load_graph");
     if (mem != STA_MEM_HOST && mem != STA_MEM_DEVICE) fail(STA_ERR_ARG, "bad sta_mem %d", (int)mem);
     if (!u) fail(STA_ERR_ARG, "units NULL");
@@ -1910,6 +1922,7 @@ sta_status sta_build_steiner(sta_ctx c, sta_mem mem, const float* pin_x, const f
 sta_status sta_set_rc_tree(sta_ctx c, sta_mem mem, const uint32_t* rc_ptr, uint32_t num_nodes,
                            const int32_t* parent, const uint32_t* node_pin) {
   return guard(c, [&] {
+    Nvtx nvtx_range("sta_set_rc_tree");
     if (!c->has_graph) fail(STA_ERR_ORDER, "sta_set_rc_tree before sta_load_graph");
     c->has_tree = false;
     c->prepared = false;
@@ -1925,6 +1938,7 @@ sta_status sta_set_rc_tree(sta_ctx c, sta_mem mem, const uint32_t* rc_ptr, uint3
 
 sta_status sta_set_rc_values(sta_ctx c, uint32_t corner, sta_mem mem, const float* res, const float* cap) {
   return guard(c, [&] {
+    Nvtx nvtx_range("sta_set_rc_values");
     CornerState& cs = corner_of(c, corner);
     if (!c->has_tree) fail(STA_ERR_ORDER, "sta_set_rc_values before sta_set_rc_tree");
     if (c->n_rc && (!res || !cap)) fail(STA_ERR_ARG, "res/cap NULL");
@@ -1962,6 +1976,7 @@ sta_status sta_set_rc_values(sta_ctx c, uint32_t corner, sta_mem mem, const floa
 
 sta_status sta_set_constraints(sta_ctx c, const sta_constraints* k) {
   return guard(c, [&] {
+    Nvtx nvtx_range("sta_set_constraints");
     if (!k) fail(STA_ERR_ARG, "constraints NULL");
     if (!c->has_graph) fail(STA_ERR_ORDER, "sta_set_constraints before sta_load_graph");
     if (!(k->period_ps > 0.f) || !std::isfinite(k->period_ps)) fail(STA_ERR_ARG, "period must be > 0");
@@ -2009,6 +2024,7 @@ sta_status sta_set_constraints(sta_ctx c, const sta_constraints* k) {
 
 sta_status sta_update_timing(sta_ctx c) {
   return guard(c, [&] {
+    Nvtx nvtx_range("sta_update_timing");
     if (!c->has_graph) fail(STA_ERR_ORDER, "sta_update_timing before sta_load_graph");
     if (!c->has_tree) fail(STA_ERR_ORDER, "sta_update_timing before sta_set_rc_tree");
     if (!c->has_cons) fail(STA_ERR_ORDER, "sta_update_timing before sta_set_constraints");
@@ -2030,6 +2046,7 @@ sta_status sta_synchronize(sta_ctx c) {
 
 sta_status sta_report_slack(sta_ctx c, uint32_t corner, double* res4, float* pin_slack, sta_mem mem) {
   return guard(c, [&] {
+    Nvtx nvtx_range("sta_report_slack");
     CornerState& cs = corner_of(c, corner);
     require_updated(c);
     if (res4) {
@@ -2042,6 +2059,7 @@ sta_status sta_report_slack(sta_ctx c, uint32_t corner, double* res4, float* pin
 
 sta_status sta_get_timing(sta_ctx c, uint32_t corner, float* at, float* slew, float* rat, sta_mem mem) {
   return guard(c, [&] {
+    Nvtx nvtx_range("sta_get_timing");
     CornerState& cs = corner_of(c, corner);
     require_updated(c);
     deliver_pins(c, at, cs.dev, 0, mem);
@@ -2090,6 +2108,7 @@ sta_status sta_get_levels(sta_ctx c, uint32_t* level, uint32_t* perm, uint32_t* 
 
 sta_status sta_report_paths(sta_ctx c, uint32_t corner, const sta_path_query* q, sta_path_set* out, sta_mem mem) {
   return guard(c, [&] {
+    Nvtx nvtx_range("sta_report_paths");
     CornerState& cs = corner_of(c, corner);
     require_updated(c);
     if (!q || !out) fail(STA_ERR_ARG, "query / output NULL");

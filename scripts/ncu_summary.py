@@ -52,12 +52,22 @@ def main():
         for n, v, _ in data:
             tot[n] = tot.get(n, 0) + v
             cnt[n] = cnt.get(n, 0) + 1
-        allt = sum(tot.values())
+        # sta_load_graph's device levelizer (row a0) runs once per design;
+        # the update shares are taken over the update kernels only
+        load = lambda n: n.startswith("k_") or n.startswith("scan_") or n in (
+            "init_corner_kernel", "set_ptrs_kernel") or n.startswith("array<")
+        upd = {n: v for n, v in tot.items() if not load(n)}
+        allu = sum(upd.values()) or 1.0
         md += ["## Launch list (`--metrics gpu__time_duration.sum --clock-control none`, serialised, cold)", "",
-               "| kernel | launches | avg us | share |", "|---|---|---|---|"]
-        for n in sorted(tot, key=lambda k: -tot[k]):
-            md.append(f"| {n} | {cnt[n]} | {tot[n] / cnt[n]:.2f} | {tot[n] / allt:.1%} |")
-        js["launch_share"] = {n: tot[n] / allt for n in tot}
+               "Per-update kernels (share of the update kernels' time):", "",
+               "| kernel | launches | avg us | share of update |", "|---|---|---|---|"]
+        for n in sorted(upd, key=lambda k: -upd[k]):
+            md.append(f"| {n} | {cnt[n]} | {tot[n] / cnt[n]:.2f} | {tot[n] / allu:.1%} |")
+        md += ["", "Once per design (`sta_load_graph`: device levelizer / CSR builder, setup):", "",
+               "| kernel | launches | avg us | total us |", "|---|---|---|---|"]
+        for n in sorted((n for n in tot if load(n)), key=lambda k: -tot[k]):
+            md.append(f"| {n} | {cnt[n]} | {tot[n] / cnt[n]:.2f} | {tot[n]:.1f} |")
+        js["launch_share"] = {n: upd[n] / allu for n in upd}
         md.append("")
     for rep in reps:
         for row in raw(rep):
