@@ -49,6 +49,9 @@ class _Design(C.Structure):
         ("n_po", C.c_uint32), ("po_pin", C.c_void_p), ("po_out_max", C.c_void_p),
         ("po_out_min", C.c_void_p), ("po_load", C.c_void_p),
         ("net_model", C.c_int32), ("arnoldi_q", C.c_uint32),
+        ("n_exc", C.c_uint32), ("exc_kind", C.c_void_p), ("exc_value", C.c_void_p),
+        ("exc_from_ptr", C.c_void_p), ("exc_from", C.c_void_p), ("exc_to_ptr", C.c_void_p),
+        ("exc_to", C.c_void_p),
     ]
 
 
@@ -136,6 +139,15 @@ class _Marshal:
         s.po_load = _p(arr(cons.po_load, np.float32))
         s.net_model = {"elmore": 0, "arnoldi": 1}[net_model]
         s.arnoldi_q = int(q)
+        ex = getattr(d, "exceptions", None)
+        s.n_exc = ex.num if ex is not None else 0
+        if s.n_exc:
+            s.exc_kind = _p(arr(ex.kind, np.uint8))
+            s.exc_value = _p(arr(ex.value, np.float32))
+            s.exc_from_ptr = _p(arr(ex.from_ptr, np.uint32))
+            s.exc_from = _p(arr(ex.from_pins, np.uint32))
+            s.exc_to_ptr = _p(arr(ex.to_ptr, np.uint32))
+            s.exc_to = _p(arr(ex.to_pins, np.uint32))
         self.s = s
         self.keep = keep
 
@@ -192,6 +204,8 @@ def update(d, corner: int = 0, want_all: bool = True, net_model: str = "elmore",
                           res.ctypes.data, _p(ep_pin), _p(ep_ws), n_ep.ctypes.data)
     if st == 1:
         raise ValueError("combinational cycle")
+    if st == 5:
+        raise ValueError("too many exceptions (32) or startpoint tags (64)")
     if st:
         raise MemoryError("oracle allocation failed")
     ne = int(n_ep[0])

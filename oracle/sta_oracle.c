@@ -414,11 +414,135 @@ static int path_report(const orc_design* d, const arcs_t* g, const uint32_t* ord
 
 /* --------------------------------------------------------- O4-O8: update */
 static int run_update(const orc_design* d, double* at, double* slew, double* rat, double* slack,
-                      double res[4], uint32_t* ep_pin, double* ep_ws, uint32_t* n_ep_out, orc_path_req* pq);
+                      double res[4], uint32_t* ep_pin, double* ep_ws, uint32_t* n_ep_out, orc_path_req* pq,
+                      const uint8_t* seed_on, const double* ep_ovr);
+static int run_tagged(const orc_design* d, double* at, double* slew, double* rat, double* slack,
+                      double res[4], uint32_t* ep_pin, double* ep_ws, uint32_t* n_ep_out);
+
+
+/* --------------------------------------- O13: -from / -to timing exceptions */
+/* SURVEY.md §8(f) row 4 (reduced: no -through, no case analysis, one clock);
+ * PAPER.md:113, 160-163 ("false paths, multi-cycle paths ... can
+ * significantly complicate the data structures and states in timing
+ * propagation"); the tag model of SPEC.md:465-509 with -from / -to
+ * exceptions only: a path's tag is the set of exceptions whose -from list
+ * holds its startpoint (exceptions without -from hold for every tag); tags
+ * never change along a path, so each tag is propagated on its own (the
+ * startpoints of that tag seeded, the others undefined) and per endpoint the
+ * tag's exception is resolved (X1-X6):
+ *   late check: false path > max delay v (RAT_L = v) > multicycle N (capture
+ *   at N T: RAT_L + (N-1) T); early check: false path > min delay v (RAT_E =
+ *   v) > multicycle N (hold edge (N-1) T: RAT_E + (N-1) T); among exceptions
+ *   of one kind the first listed wins.  Results: per pin the early / late
+ *   extreme over tags of AT / slew / RAT and the minimum slack; per endpoint
+ *   the worst slack over tags (a false path contributes none).
+ * ep_ovr per pin: {late mode, late value, early mode, early value}, mode 0:
+ * shift by the value, 1: replace by it, 2: no seed (false path). */
+static void exc_apply(const double* o, double* rl, double* re) {
+  if (o[0] == 2) *rl = INF; else if (o[0] == 1) *rl = o[1]; else *rl += o[1];
+  if (o[2] == 2) *re = -INF; else if (o[2] == 1) *re = o[3]; else *re += o[3];
+}
+
+static int in_list(const uint32_t* a, uint32_t lo, uint32_t hi, uint32_t p) {
+  for (uint32_t i = lo; i < hi; i++) if (a[i] == p) return 1;
+  return 0;
+}
+
+enum { EXC_FALSE = 0, EXC_MULTICYCLE = 1, EXC_MAX = 2, EXC_MIN = 3 };
+
+static int run_tagged(const orc_design* d, double* at, double* slew, double* rat, double* slack,
+                      double res[4], uint32_t* ep_pin, double* ep_ws, uint32_t* n_ep_out) {
+  const uint32_t P = d->num_pins, E = d->n_exc;
+  if (E > 32) return 5;
+  /* step 1: the tag (exception bitset) of every pin that could be a startpoint */
+  uint32_t* tag = calloc(P + 1, sizeof(uint32_t));
+  for (uint32_t e = 0; e < E; e++)
+    for (uint32_t i = d->exc_from_ptr[e]; i < d->exc_from_ptr[e + 1]; i++) tag[d->exc_from[i]] |= 1u << e;
+  /* step 2: the distinct tags of the startpoints, in pin order */
+  uint32_t tags[64], T = 0;
+  int bad = 0;
+  for (uint32_t p = 0; p < P; p++) {
+    int sp = d->pin_role[p] == ORC_FF_CK;
+    for (uint32_t k = 0; k < d->n_pi && !sp; k++) sp = d->pi_pin[k] == p;
+    if (!sp) continue;
+    uint32_t j = 0;
+    while (j < T && tags[j] != tag[p]) j++;
+    if (j == T) { if (T == 64) { bad = 1; break; } tags[T++] = tag[p]; }
+  }
+  if (T == 0) tags[T++] = 0;
+  int st = bad ? 5 : 0;
+  const size_t P4 = 4 * (size_t)(P + 1);
+  double *t_at = malloc(sizeof(double) * P4), *t_sl = malloc(sizeof(double) * P4);
+  double *t_rat = malloc(sizeof(double) * P4), *t_sk = malloc(sizeof(double) * P4);
+  double* ovr = malloc(sizeof(double) * P4);
+  uint8_t* on = malloc(P + 1);
+  uint32_t n_ep_max = d->n_po + d->num_checks + 1, n_ep = 0;
+  uint32_t* t_ep = malloc(sizeof(uint32_t) * n_ep_max);
+  double* t_ws = malloc(sizeof(double) * 2 * n_ep_max);
+  double* m_ws = malloc(sizeof(double) * 2 * n_ep_max);
+  double t_res[4];
+  for (uint32_t j = 0; j < T && !st; j++) {
+    /* step 3: tag j: its startpoints seeded; each endpoint's exception */
+    for (uint32_t p = 0; p < P; p++) on[p] = tag[p] == tags[j];
+    for (uint32_t p = 0; p < P; p++) {
+      double* o = ovr + 4 * (size_t)p;
+      o[0] = o[1] = o[2] = o[3] = 0.0;
+      int lf = -1, lm = -1, lc = -1, ef = -1, em = -1, ec = -1;
+      for (uint32_t e = 0; e < E; e++) {
+        const int has_from = d->exc_from_ptr[e + 1] > d->exc_from_ptr[e];
+        const int has_to = d->exc_to_ptr[e + 1] > d->exc_to_ptr[e];
+        if (has_from && !((tags[j] >> e) & 1u)) continue;
+        if (has_to && !in_list(d->exc_to, d->exc_to_ptr[e], d->exc_to_ptr[e + 1], p)) continue;
+        switch (d->exc_kind[e]) {
+          case EXC_FALSE: if (lf < 0) lf = (int)e; if (ef < 0) ef = (int)e; break;
+          case EXC_MAX: if (lm < 0) lm = (int)e; break;
+          case EXC_MIN: if (em < 0) em = (int)e; break;
+          case EXC_MULTICYCLE: if (lc < 0) lc = (int)e; if (ec < 0) ec = (int)e; break;
+        }
+      }
+      if (lf >= 0) o[0] = 2;
+      else if (lm >= 0) { o[0] = 1; o[1] = d->exc_value[lm]; }
+      else if (lc >= 0) o[1] = (d->exc_value[lc] - 1.0) * d->period;
+      if (ef >= 0) o[2] = 2;
+      else if (em >= 0) { o[2] = 1; o[3] = d->exc_value[em]; }
+      else if (ec >= 0) o[3] = (d->exc_value[ec] - 1.0) * d->period;
+    }
+    st = run_update(d, t_at, t_sl, t_rat, t_sk, t_res, t_ep, t_ws, &n_ep, NULL, on, ovr);
+    if (st) break;
+    /* step 4: merge over tags */
+    for (size_t i = 0; i < 4 * (size_t)P; i++) {
+      const int e = (i & 3) < 2;            /* early component */
+      if (j == 0) { at[i] = t_at[i]; if (slew) slew[i] = t_sl[i]; if (rat) rat[i] = t_rat[i]; if (slack) slack[i] = t_sk[i]; continue; }
+      at[i] = e ? fmin(at[i], t_at[i]) : fmax(at[i], t_at[i]);
+      if (slew) slew[i] = e ? fmin(slew[i], t_sl[i]) : fmax(slew[i], t_sl[i]);
+      if (rat) rat[i] = e ? fmax(rat[i], t_rat[i]) : fmin(rat[i], t_rat[i]);
+      if (slack) slack[i] = fmin(slack[i], t_sk[i]);
+    }
+    for (uint32_t k = 0; k < 2 * n_ep; k++) m_ws[k] = j == 0 ? t_ws[k] : fmin(m_ws[k], t_ws[k]);
+  }
+  if (!st) {
+    double ws = INF, tns = 0.0, wh = INF, tnh = 0.0;
+    for (uint32_t k = 0; k < n_ep; k++) {
+      const double s = m_ws[2 * k], h = m_ws[2 * k + 1];
+      if (s < ws) ws = s;
+      if (s < 0) tns += s;
+      if (h < wh) wh = h;
+      if (h < 0) tnh += h;
+      if (ep_pin) ep_pin[k] = t_ep[k];
+      if (ep_ws) { ep_ws[2 * k] = s; ep_ws[2 * k + 1] = h; }
+    }
+    res[0] = ws; res[1] = tns; res[2] = wh; res[3] = tnh;
+    if (n_ep_out) *n_ep_out = n_ep;
+  }
+  free(tag); free(t_at); free(t_sl); free(t_rat); free(t_sk); free(ovr); free(on);
+  free(t_ep); free(t_ws); free(m_ws);
+  return st;
+}
 
 int orc_update(const orc_design* d, double* at, double* slew, double* rat, double* slack,
                double res[4], uint32_t* ep_pin, double* ep_ws, uint32_t* n_ep_out) {
-  return run_update(d, at, slew, rat, slack, res, ep_pin, ep_ws, n_ep_out, NULL);
+  if (d->n_exc) return run_tagged(d, at, slew, rat, slack, res, ep_pin, ep_ws, n_ep_out);
+  return run_update(d, at, slew, rat, slack, res, ep_pin, ep_ws, n_ep_out, NULL, NULL, NULL);
 }
 
 int orc_paths(const orc_design* d, int mode, uint32_t k, uint32_t nworst, double slack_lt, uint32_t cap_paths,
@@ -434,7 +558,8 @@ int orc_paths(const orc_design* d, int mode, uint32_t k, uint32_t nworst, double
   uint32_t P = d->num_pins;
   double* at = malloc(sizeof(double) * 4 * (size_t)(P + 1));
   if (!at) return 2;
-  int st = run_update(d, at, NULL, NULL, NULL, res, NULL, NULL, NULL, &q);
+  if (d->n_exc) { free(at); return 4; }      /* path reports: no exceptions (X6) */
+  int st = run_update(d, at, NULL, NULL, NULL, res, NULL, NULL, NULL, &q, NULL, NULL);
   free(at);
   *n_paths = q.n_paths;
   *n_pins = q.n_pins;
@@ -442,7 +567,8 @@ int orc_paths(const orc_design* d, int mode, uint32_t k, uint32_t nworst, double
 }
 
 static int run_update(const orc_design* d, double* at, double* slew, double* rat, double* slack,
-                      double res[4], uint32_t* ep_pin, double* ep_ws, uint32_t* n_ep_out, orc_path_req* pq) {
+                      double res[4], uint32_t* ep_pin, double* ep_ws, uint32_t* n_ep_out, orc_path_req* pq,
+                      const uint8_t* seed_on, const double* ep_ovr) {
   const uint32_t P = d->num_pins;
   const double LN9 = log(9.0);
   arcs_t g; memset(&g, 0, sizeof g);
@@ -521,10 +647,12 @@ static int run_update(const orc_design* d, double* at, double* slew, double* rat
   for (uint32_t k = 0; k < d->n_pi; k++) {
     uint32_t p = d->pi_pin[k];
     if (g.fi_ptr[p + 1] != g.fi_ptr[p]) continue;
+    if (seed_on && !seed_on[p]) continue;    /* O13: a startpoint of another tag */
     for (int q = 0; q < 4; q++) { at[4 * p + q] = d->pi_at[4 * k + q]; slew[4 * p + q] = d->pi_slew[4 * k + q]; }
   }
   for (uint32_t p = 0; p < P; p++) {
     if (d->pin_role[p] != ORC_FF_CK || g.fi_ptr[p + 1] != g.fi_ptr[p]) continue;
+    if (seed_on && !seed_on[p]) continue;
     /* ideal clock, rising edge at 0, waveform (0, T/2) */
     at[4 * p + Q(0, 0)] = 0.0; at[4 * p + Q(0, 1)] = d->period / 2;
     at[4 * p + Q(1, 0)] = 0.0; at[4 * p + Q(1, 1)] = d->period / 2;
@@ -590,6 +718,7 @@ static int run_update(const orc_design* d, double* at, double* slew, double* rat
     for (int rf = 0; rf < 2; rf++) {
       double rl = d->period - d->po_out_max[2 * k + rf];
       double re = -(double)d->po_out_min[2 * k + rf];
+      if (ep_ovr) exc_apply(ep_ovr + 4 * (size_t)p, &rl, &re);
       if (rl < rat[4 * p + Q(1, rf)]) rat[4 * p + Q(1, rf)] = rl;
       if (re > rat[4 * p + Q(0, rf)]) rat[4 * p + Q(0, rf)] = re;
     }
@@ -600,10 +729,14 @@ static int run_update(const orc_design* d, double* at, double* slew, double* rat
     for (int rf = 0; rf < 2; rf++) {
       if (isfinite(at[4 * p + Q(1, rf)])) {   /* setup: index_1 data slew, index_2 clock slew */
         double rl = d->period - lut_id(d, tb + (uint32_t)rf, slew[4 * p + Q(1, rf)], d->clock_slew);
+        double dummy = -INF;
+        if (ep_ovr) exc_apply(ep_ovr + 4 * (size_t)p, &rl, &dummy);
         if (rl < rat[4 * p + Q(1, rf)]) rat[4 * p + Q(1, rf)] = rl;
       }
       if (isfinite(at[4 * p + Q(0, rf)])) {   /* hold */
         double re = lut_id(d, tb + 2 + (uint32_t)rf, slew[4 * p + Q(0, rf)], d->clock_slew);
+        double dummy = INF;
+        if (ep_ovr) exc_apply(ep_ovr + 4 * (size_t)p, &dummy, &re);
         if (re > rat[4 * p + Q(0, rf)]) rat[4 * p + Q(0, rf)] = re;
       }
     }

@@ -72,6 +72,16 @@ typedef struct {
    * reduced-order model of order arnoldi_q (O12) */
   int32_t net_model;
   uint32_t arnoldi_q;
+  /* -from / -to timing exceptions: kind 0 false
+   * path, 1 multicycle (value N), 2 max delay (value ps), 3 min delay (value
+   * ps); CSR lists of startpoint / endpoint pins (an empty list: any) */
+  uint32_t n_exc;
+  const uint8_t* exc_kind;
+  const float* exc_value;
+  const uint32_t* exc_from_ptr;
+  const uint32_t* exc_from;
+  const uint32_t* exc_to_ptr;
+  const uint32_t* exc_to;
 } orc_design;
 
 /* O6: NLDM bilinear lookup, fp64.  `tab` points at

@@ -14,7 +14,7 @@ assert a in s, a
 open('oracle/sta_oracle.c', 'w').write(s.replace(a, b, 1))
 PY
   rm -f oracle/liboracle.so
-  if timeout 600 python -m pytest tests/test_oracle_lut_rc.py tests/test_oracle_propagation.py tests/test_oracle_steiner.py tests/test_oracle_arnoldi.py -q -x >/dev/null 2>&1; then
+  if timeout 600 python -m pytest tests/test_oracle_lut_rc.py tests/test_oracle_propagation.py tests/test_oracle_steiner.py tests/test_oracle_arnoldi.py tests/test_oracle_exceptions.py -q -x >/dev/null 2>&1; then
     echo "NOT CAUGHT: $1"; fail=1; return 1
   else echo "caught: $1"; fi
 }
@@ -64,4 +64,11 @@ mut 'dd = arn && a_qq[v] ? ndly[4 * (size_t)v + Q(el, orf)] : elm[v];' 'dd = elm
 mut 'cs = os;' 'cs = s_in;'
 mut 'if (t > D) r2 = lam > 0.0 ? (t - D) - lam * (1.0 - exp(-(t - D) / lam)) : t - D;' ''
 mut 'return t50 - 0.5 * D;' 'return t50;'
+# -from / -to exceptions (O13, row f4 reduced)
+mut 'else if (lc >= 0) o[1] = (d->exc_value[lc] - 1.0) * d->period;' 'else if (lc >= 0) o[1] = d->exc_value[lc] * d->period;'
+mut '    if (seed_on && !seed_on[p]) continue;    /* O13: a startpoint of another tag */' ''
+mut '      if (slack) slack[i] = fmin(slack[i], t_sk[i]);' '      if (slack) slack[i] = fmax(slack[i], t_sk[i]);'
+mut '        if (has_from && !((tags[j] >> e) & 1u)) continue;' ''
+mut 'else if (ec >= 0) o[3] = (d->exc_value[ec] - 1.0) * d->period;' ''
+mut '    for (uint32_t k = 0; k < 2 * n_ep; k++) m_ws[k] = j == 0 ? t_ws[k] : fmin(m_ws[k], t_ws[k]);' '    for (uint32_t k = 0; k < 2 * n_ep; k++) m_ws[k] = t_ws[k];'
 exit $fail

@@ -103,6 +103,37 @@ class Constraints:
 
 
 @dataclass
+class Exceptions:
+    """-from / -to timing exceptions (reduced): kind 0
+    false path, 1 multicycle (value N), 2 max delay, 3 min delay (value ps);
+    CSR lists of startpoint / endpoint pins (an empty list: any)."""
+    kind: np.ndarray       # uint8 [E]
+    value: np.ndarray      # float32 [E]
+    from_ptr: np.ndarray   # uint32 [E+1]
+    from_pins: np.ndarray  # uint32
+    to_ptr: np.ndarray     # uint32 [E+1]
+    to_pins: np.ndarray    # uint32
+
+    @property
+    def num(self) -> int:
+        return int(self.kind.shape[0])
+
+    @staticmethod
+    def build(items) -> "Exceptions":
+        """items: sequence of (kind, value, from_pins, to_pins)."""
+        kind = np.array([k for k, _, _, _ in items], np.uint8)
+        value = np.array([v for _, v, _, _ in items], np.float32)
+        fp, tp, fr, to = [0], [0], [], []
+        for _, _, f, t in items:
+            fr += list(f)
+            to += list(t)
+            fp.append(len(fr))
+            tp.append(len(to))
+        return Exceptions(kind, value, np.array(fp, np.uint32), np.array(fr, np.uint32),
+                          np.array(tp, np.uint32), np.array(to, np.uint32))
+
+
+@dataclass
 class Design:
     num_pins: int
     pin_cap: np.ndarray      # float32 [P]
@@ -121,6 +152,7 @@ class Design:
     cons: Constraints
     name: str = "design"
     meta: dict = field(default_factory=dict)
+    exceptions: Optional["Exceptions"] = None
 
     @property
     def num_nets(self) -> int:

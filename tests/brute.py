@@ -331,3 +331,131 @@ def select_paths(paths, k, nworst, slack_lt=INF):
         cnt[p[1]] += 1
         kept.append(p)
     return kept
+
+
+def exception_of(ex, tag, e, late):
+    """The exception a path of startpoint tag `tag` (bitset over ex) meets at
+    endpoint e, for the late (setup) or early (hold) check: DESIGN.md X2-X3
+    precedence -- false path, then max (late) / min (early) delay, then
+    multicycle; the first listed of a kind.  -> (mode, value): mode 0 shift,
+    1 replace, 2 no check; None without exception."""
+    cand = {0: None, 2 if late else 3: None, 1: None}
+    for k in range(ex.num):
+        f0, f1 = int(ex.from_ptr[k]), int(ex.from_ptr[k + 1])
+        t0, t1 = int(ex.to_ptr[k]), int(ex.to_ptr[k + 1])
+        if f1 > f0 and not (tag >> k) & 1:
+            continue
+        if t1 > t0 and e not in set(int(x) for x in ex.to_pins[t0:t1]):
+            continue
+        kk = int(ex.kind[k])
+        if kk in cand and cand[kk] is None:
+            cand[kk] = k
+    return cand
+
+
+def path_slacks_with_exceptions(d, elm_of_pin):
+    """Frozen-delay brute force of the -from / -to exceptions (d.exceptions):
+    every startpoint -> endpoint path is enumerated; a path's required time
+    is its endpoint's seed modified by the exception of (its startpoint's tag,
+    its endpoint); the setup / hold slack of a (pin, rf) is the minimum over
+    the complete paths through it, an endpoint's worst slack the minimum over
+    the paths ending there (false paths excluded).  Returns slack [P][4] and
+    res (WNS_s, TNS_s, WNS_h, TNS_h)."""
+    lib = d.libs[0]
+    cons = d.cons
+    ex = d.exceptions
+    T = float(cons.period)
+    arcs = _fanin_lists(d)
+    P = d.num_pins
+    succ = defaultdict(list)
+    indeg = np.zeros(P, int)
+    for (u, v, kind, sense, tab) in arcs:
+        if kind == "net":
+            dl = {(0, 0): elm_of_pin[v], (1, 1): elm_of_pin[v]}
+        else:
+            dl = {(i, o): max(0.0, const_value(lib, tab + o)) for (i, o) in _pairs(sense)}
+        succ[u].append((v, dl))
+        indeg[v] += 1
+    tag = np.zeros(P, np.int64)
+    for k in range(ex.num):
+        for p in ex.from_pins[int(ex.from_ptr[k]):int(ex.from_ptr[k + 1])]:
+            tag[int(p)] |= 1 << k
+    seed_at = {}
+    for k in range(cons.pi_pin.size):
+        p = int(cons.pi_pin[k])
+        if indeg[p] == 0:
+            seed_at[p] = [float(x) for x in cons.pi_at[k]]
+    for p in range(P):
+        if int(d.pin_role[p]) == ROLE_FF_CK and indeg[p] == 0:
+            seed_at[p] = [0.0, T / 2, 0.0, T / 2]
+    base_l = defaultdict(lambda: [INF, INF])
+    base_e = defaultdict(lambda: [-INF, -INF])
+    po_l, po_e, ck_l, ck_e = {}, {}, {}, {}
+    for k in range(cons.po_pin.size):
+        p = int(cons.po_pin[k])
+        po_l.setdefault(p, []).append([T - float(cons.po_out_max[k, rf]) for rf in (0, 1)])
+        po_e.setdefault(p, []).append([-float(cons.po_out_min[k, rf]) for rf in (0, 1)])
+    for c in range(d.num_checks):
+        p, tb = int(d.chk_d[c]), int(d.chk_tab[c])
+        ck_l.setdefault(p, []).append([T - const_value(lib, tb + rf) for rf in (0, 1)])
+        ck_e.setdefault(p, []).append([const_value(lib, tb + 2 + rf) for rf in (0, 1)])
+    endpoints = sorted(set(po_l) | set(ck_l))
+
+    def mod(v, ov):
+        if ov is None:
+            return v
+        mode, val = ov
+        return INF if mode == 2 else (val if mode == 1 else v + val)
+
+    def req(e, rf, tg, late):
+        c = exception_of(ex, tg, e, late)
+        ov = None
+        if c[0] is not None:
+            ov = (2, 0.0)
+        elif c[2 if late else 3] is not None:
+            ov = (1, float(ex.value[c[2 if late else 3]]))
+        elif c[1] is not None:
+            ov = (0, (float(ex.value[c[1]]) - 1.0) * T)
+        vals = [x[rf] for x in (po_l if late else po_e).get(e, [])] + [x[rf] for x in (ck_l if late else ck_e).get(e, [])]
+        if not vals:
+            return None
+        if late:
+            return min(mod(x, ov) for x in vals)
+        r = [mod(x, ov) for x in vals]
+        r = [(-INF if ov is not None and ov[0] == 2 else x) for x in r]
+        return max(r)
+
+    slack = np.full((P, 4), INF)
+    ws = {e: INF for e in endpoints}
+    wh = {e: INF for e in endpoints}
+
+    def walk(stack, v, rf, acc, s, s_rf):
+        stack.append((v, rf))
+        if v in po_l or v in ck_l:
+            tg = int(tag[s])
+            rl = req(v, rf, tg, True)
+            if rl is not None and rl < INF:
+                sl = rl - (seed_at[s][2 + s_rf] + acc)
+                ws[v] = min(ws[v], sl)
+                for (x, r) in stack:
+                    slack[x, 2 + r] = min(slack[x, 2 + r], sl)
+            re = req(v, rf, tg, False)
+            if re is not None and re > -INF:
+                sh = (seed_at[s][s_rf] + acc) - re
+                wh[v] = min(wh[v], sh)
+                for (x, r) in stack:
+                    slack[x, r] = min(slack[x, r], sh)
+        for (w, dl) in succ[v]:
+            for (i, o), x in dl.items():
+                if i == rf:
+                    walk(stack, w, o, acc + x, s, s_rf)
+        stack.pop()
+
+    for s in seed_at:
+        for rf in (0, 1):
+            walk([], s, rf, 0.0, s, rf)
+    wsv = [ws[e] for e in endpoints]
+    whv = [wh[e] for e in endpoints]
+    res = (min(wsv, default=INF), sum(min(0.0, x) for x in wsv if x < INF),
+           min(whv, default=INF), sum(min(0.0, x) for x in whv if x < INF))
+    return slack, res

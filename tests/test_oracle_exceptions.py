@@ -1,0 +1,101 @@
+"""Pins of the oracle's -from / -to timing exceptions (O13; SURVEY.md §8(f)
+row 4, reduced to -from / -to false paths, multicycles and max / min delays
+on one clock): exhaustive path
+enumeration on tiny frozen-delay designs (every path's required time from
+its own (startpoint, endpoint) exception), hand examples, and the identity
+without exceptions."""
+import copy
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth.design import Exceptions
+from tests.brute import path_enumeration_timing, path_slacks_with_exceptions
+from tests.test_oracle_propagation import _bf_elm, _tiny
+
+
+def _startpoints(d):
+    sp = [int(p) for p in d.cons.pi_pin]
+    sp += [p for p in range(d.num_pins) if int(d.pin_role[p]) == synth.ROLE_FF_CK]
+    return sorted(set(sp))
+
+
+def _endpoints(d):
+    return sorted(set(int(p) for p in d.cons.po_pin) | set(int(p) for p in d.chk_d))
+
+
+def random_exceptions(d, rng, n):
+    sp, ep = _startpoints(d), _endpoints(d)
+    items = []
+    for _ in range(n):
+        kind = int(rng.integers(0, 4))
+        value = float(rng.integers(2, 4)) if kind == 1 else float(np.round(rng.uniform(-20, 120), 2))
+        fr = list(rng.choice(sp, size=int(rng.integers(0, min(3, len(sp)) + 1)), replace=False)) if sp else []
+        to = list(rng.choice(ep, size=int(rng.integers(0, min(3, len(ep)) + 1)), replace=False)) if ep else []
+        items.append((kind, value, fr, to))
+    return Exceptions.build(items)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_exceptions_vs_path_enumeration(seed):
+    d = _tiny(seed)
+    rng = np.random.default_rng(1000 + seed)
+    d.exceptions = random_exceptions(d, rng, int(rng.integers(1, 5)))
+    elm = _bf_elm(d)
+    slack, res = path_slacks_with_exceptions(d, elm)
+    o = oracle.update(d)
+    # arrivals are the untagged ones (tags partition the startpoints)
+    at_bf, _, _, _ = path_enumeration_timing(d, elm)
+    fin = np.isfinite(at_bf)
+    assert np.array_equal(fin, np.isfinite(o["at"]))
+    np.testing.assert_allclose(o["at"][fin], at_bf[fin], rtol=0, atol=1e-9)
+    fs = np.isfinite(slack)
+    assert np.array_equal(fs, np.isfinite(o["slack"])), (np.argwhere(fs != np.isfinite(o["slack"]))[:5])
+    np.testing.assert_allclose(o["slack"][fs], slack[fs], rtol=0, atol=1e-9)
+    for a, b in zip(o["res"], res):
+        assert (a == b) or abs(a - b) <= 1e-9 * max(1.0, abs(b))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_no_exception_is_identity(seed):
+    d = _tiny(seed)
+    base = oracle.update(d)
+    d2 = copy.copy(d)
+    d2.exceptions = Exceptions.build([])
+    o = oracle.update(d2)
+    for k in ("at", "slew", "rat", "slack"):
+        assert np.array_equal(np.nan_to_num(o[k], posinf=1e300, neginf=-1e300),
+                              np.nan_to_num(base[k], posinf=1e300, neginf=-1e300))
+
+
+def test_hand_examples():
+    # H3 (register to register): a false path to the D endpoint removes its
+    # setup / hold slack from WNS / TNS; a multicycle 2 adds exactly T to its
+    # setup slack and T to its hold requirement; max delay replaces RAT_L
+    d = synth.h3_reg2reg()
+    base = oracle.update(d)
+    T = float(d.cons.period)
+    ep = _endpoints(d)
+    d1 = copy.copy(d)
+    d1.exceptions = Exceptions.build([(0, 0.0, [], ep)])
+    o1 = oracle.update(d1)
+    assert o1["res"][0] == np.inf and o1["res"][1] == 0.0 and o1["res"][2] == np.inf
+    d2 = copy.copy(d)
+    d2.exceptions = Exceptions.build([(1, 2.0, [], ep)])
+    o2 = oracle.update(d2)
+    for p in ep:
+        np.testing.assert_allclose(o2["slack"][p][2:], base["slack"][p][2:] + T, atol=1e-9)
+        np.testing.assert_allclose(o2["slack"][p][:2], base["slack"][p][:2] - T, atol=1e-9)
+    d3 = copy.copy(d)
+    d3.exceptions = Exceptions.build([(2, 123.0, [], ep)])
+    o3 = oracle.update(d3)
+    for p in ep:
+        for rf in (0, 1):
+            if np.isfinite(o3["at"][p][2 + rf]):
+                np.testing.assert_allclose(o3["slack"][p][2 + rf], 123.0 - o3["at"][p][2 + rf], atol=1e-9)
+    # precedence: a false path beats a multicycle on the same endpoint
+    d4 = copy.copy(d)
+    d4.exceptions = Exceptions.build([(1, 3.0, [], ep), (0, 0.0, [], ep)])
+    assert oracle.update(d4)["res"][0] == np.inf
