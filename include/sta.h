@@ -218,6 +218,39 @@ STA_API sta_status sta_build_steiner(sta_ctx ctx, sta_mem mem, const float* pin_
 typedef enum { STA_NET_ELMORE = 0, STA_NET_ARNOLDI = 1 } sta_net_model;
 STA_API sta_status sta_set_net_model(sta_ctx ctx, sta_net_model model, uint32_t q);
 
+/* -from / -to timing exceptions (reduced: no
+ * -through, no case analysis, one clock; "false
+ * paths, multi-cycle paths, case analysis, and cross clock region paths ...
+ * complicate the data structures and states in timing propagation"; the tag
+ * model of SPEC.md:465-509).  Exception i: kind[i] (STA_EXC_*), value[i]
+ * (multicycle: N >= 1; max / min delay: ps), startpoint pins
+ * from_pins[from_ptr[i] .. from_ptr[i+1]) and endpoint pins
+ * to_pins[to_ptr[i] .. to_ptr[i+1]) (an empty list: any).  A path's tag is
+ * the set of exceptions whose -from list holds its startpoint; every tag is
+ * propagated on its own (one forward / backward pass per tag, RC shared),
+ * and per endpoint and tag the exception is resolved: setup (late): false
+ * path > max delay (RAT_L = value) > multicycle (capture at N T); hold
+ * (early): false path > min delay (RAT_E = value) > multicycle (hold edge
+ * (N-1) T); the first listed of a kind wins.  Reports merge the tags: per
+ * pin the early / late extreme of AT, slew, RAT and the minimum slack; per
+ * endpoint the worst slack over tags (false paths contribute none) for
+ * WNS / TNS.  num = 0 clears.  At most 32 exceptions and 16 startpoint tags.
+ * The top-k path report needs no exceptions (STA_ERR_ORDER).  Arrays in
+ * `mem`, copied.  Errors: STA_ERR_ORDER (no graph), STA_ERR_ARG, STA_ERR_ID. */
+typedef enum { STA_EXC_FALSE_PATH = 0, STA_EXC_MULTICYCLE = 1, STA_EXC_MAX_DELAY = 2,
+               STA_EXC_MIN_DELAY = 3 } sta_exception_kind;
+typedef struct {
+  sta_mem mem;
+  uint32_t num;
+  const uint8_t* kind;
+  const float* value;
+  const uint32_t* from_ptr;
+  const uint32_t* from_pins;
+  const uint32_t* to_ptr;
+  const uint32_t* to_pins;
+} sta_exceptions;
+STA_API sta_status sta_set_exceptions(sta_ctx ctx, const sta_exceptions* ex);
+
 /* Per-corner RC values: res[i] = resistance of the edge parent -> i (kOhm,
  * ignored at node 0), cap[i] = wire capacitance to ground at node i (fF);
  * both num_nodes long, >= 0 and finite.  HOST: copied into ctx-owned device

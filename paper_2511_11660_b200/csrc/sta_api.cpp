@@ -234,6 +234,14 @@ struct sta_ctx_s {
   std::vector<u32> fwu_stage_ptr;                // [S + 1] forward units of each stage
   std::vector<u32> fi_p_h, fi_slot_h, ep_int_h;  // path report: term ranges, delay slots, endpoint ids
   Arena path_arena;                              // path report: their device copies + user_of_int
+  // row f4 (reduced): -from / -to exceptions; per startpoint tag a seed array
+  // and endpoint overrides (prepare)
+  std::vector<uint8_t> exc_kind;
+  std::vector<float> exc_value;
+  std::vector<u32> exc_from_ptr, exc_from, exc_to_ptr, exc_to;
+  Arena exc_arena;
+  std::vector<const u32*> exc_seed_d;
+  std::vector<const uint4*> exc_ovr_d;
   int net_model = 0;                             // row f1: 0 Elmore, 1 Arnoldi (order arn_q)
   u32 arn_q = 4;
   Arena arn_arena;                               // Arnoldi layout (prepare)
@@ -1277,6 +1285,65 @@ void prepare(sta_ctx c) {
   t.po_seed = g.upload(po_seed, s);
   t.ep = g.upload(ep, s);
   t.seed = g.upload(seed, s);
+  t.ep_ovr = nullptr;
+  // row f4: startpoint tags (the exception sets of the -from lists holding
+  // each seeded stage-0 pin), one seed array and one endpoint-override array
+  // per tag (X1-X6; the oracle's O13)
+  c->exc_arena.release();
+  c->exc_seed_d.clear();
+  c->exc_ovr_d.clear();
+  if (!c->exc_kind.empty()) {
+    const u32 E = (u32)c->exc_kind.size();
+    std::vector<u32> tagp(P, 0);
+    for (u32 e = 0; e < E; ++e)
+      for (u32 x = c->exc_from_ptr[e]; x < c->exc_from_ptr[e + 1]; ++x) tagp[c->exc_from[x]] |= 1u << e;
+    std::vector<u32> tags;
+    for (u32 p = 0; p < P; ++p) {
+      const u32 i = c->int_of_user[p];
+      if (i >= c->n0 || seed[i] == kNone) continue;
+      if (std::find(tags.begin(), tags.end(), tagp[p]) == tags.end()) tags.push_back(tagp[p]);
+    }
+    if (tags.empty()) tags.push_back(0);
+    if (tags.size() > 16) fail(STA_ERR_ARG, "%zu startpoint tags (at most 16)", tags.size());
+    std::vector<std::vector<uint8_t>> in_to(E);
+    for (u32 e = 0; e < E; ++e) {
+      in_to[e].assign(P, 0);
+      for (u32 x = c->exc_to_ptr[e]; x < c->exc_to_ptr[e + 1]; ++x) in_to[e][c->exc_to[x]] = 1;
+    }
+    for (u32 tg : tags) {
+      std::vector<u32> sd(seed);
+      for (u32 i = 0; i < c->n0; ++i) {
+        const u32 p = c->user_of_int[i];
+        if (p != kNone && sd[i] != kNone && tagp[p] != tg) sd[i] = kNone;   // another tag's startpoint
+      }
+      std::vector<uint4> ov(c->n_ep);
+      for (u32 k = 0; k < c->n_ep; ++k) {
+        const u32 p = c->user_of_int[ep_int[k]];
+        int lf = -1, lm = -1, lc = -1, ef = -1, em = -1, ec = -1;
+        for (u32 e = 0; e < E; ++e) {
+          if (c->exc_from_ptr[e + 1] > c->exc_from_ptr[e] && !((tg >> e) & 1u)) continue;
+          if (c->exc_to_ptr[e + 1] > c->exc_to_ptr[e] && !in_to[e][p]) continue;
+          switch (c->exc_kind[e]) {
+            case STA_EXC_FALSE_PATH: if (lf < 0) lf = (int)e; if (ef < 0) ef = (int)e; break;
+            case STA_EXC_MAX_DELAY: if (lm < 0) lm = (int)e; break;
+            case STA_EXC_MIN_DELAY: if (em < 0) em = (int)e; break;
+            case STA_EXC_MULTICYCLE: if (lc < 0) lc = (int)e; if (ec < 0) ec = (int)e; break;
+          }
+        }
+        auto bits = [](float f) { u32 u; std::memcpy(&u, &f, 4); return u; };
+        uint4 o = make_uint4(0, bits(0.f), 0, bits(0.f));
+        if (lf >= 0) o.x = 2;
+        else if (lm >= 0) { o.x = 1; o.y = bits(c->exc_value[lm]); }
+        else if (lc >= 0) o.y = bits((float)(((double)c->exc_value[lc] - 1.0) * (double)c->period));
+        if (ef >= 0) o.z = 2;
+        else if (em >= 0) { o.z = 1; o.w = bits(c->exc_value[em]); }
+        else if (ec >= 0) o.w = bits((float)(((double)c->exc_value[ec] - 1.0) * (double)c->period));
+        ov[k] = o;
+      }
+      c->exc_seed_d.push_back(c->exc_arena.upload(sd, s));
+      c->exc_ovr_d.push_back(c->exc_arena.upload(ov, s));
+    }
+  }
   t.pi_at = reinterpret_cast<const float4*>(g.upload(c->pi_at, s));
   t.pi_slew = reinterpret_cast<const float4*>(g.upload(c->pi_slew, s));
   t.po_out_max = reinterpret_cast<const float2*>(g.upload(c->po_out_max, s));
@@ -1377,6 +1444,12 @@ void prepare(sta_ctx c) {
       ck(cudaMemsetAsync(d.trace, 0, n * sizeof(unsigned long long), s), "memset");
     }
     ck(cudaMemsetAsync(d.load, 0, sizeof(float) * std::max<u32>(c->NP, 1), s), "memset");
+    d.m_pin = nullptr;
+    d.m_ep_ws = nullptr;
+    if (!c->exc_kind.empty()) {
+      d.m_pin = a.alloc<float4>(4 * (size_t)std::max<u32>(P, 1));
+      d.m_ep_ws = a.alloc<float2>(std::max<u32>(c->n_ep, 1));
+    }
     d.arn_lam = nullptr;
     d.arn_res = nullptr;
     d.arn_scr = nullptr;
@@ -1394,12 +1467,13 @@ void prepare(sta_ctx c) {
 }
 
 // Kernel sequence of one update of one batch of corners (see sta_kernels.cu).
-u32 enqueue_batch(sta_ctx c, const sta::Batch& b) {
-  const sta::Topo& t = c->topo;
+u32 enqueue_batch(sta_ctx c, const sta::Batch& b, const sta::Topo& t, bool rc) {
   cudaStream_t s = c->stream;
   u32 launches = 0;
   prof_mark(c, 0);
-  if (t.nC && std::getenv("STA_RC_SERIAL")) {
+  if (!rc) {
+    // a later exception tag of the same update (row f4): the RC results are shared
+  } else if (t.nC && std::getenv("STA_RC_SERIAL")) {
     ck(sta::launch_rc_tierC(t, b, s), "rc tier-C kernels");
   } else if (t.nC) {                         // tier C concurrently with the small nets
     ck(cudaEventRecord(c->fork_ev, s), "fork");
@@ -1407,10 +1481,12 @@ u32 enqueue_batch(sta_ctx c, const sta::Batch& b) {
     ck(sta::launch_rc_tierC(t, b, c->side), "rc tier-C kernels");
     ck(cudaEventRecord(c->join_ev, c->side), "join");
   }
-  ck(sta::launch_rc(t, b, c->wgrid, s), "rc kernel");
-  if (t.nC && !std::getenv("STA_RC_SERIAL")) ck(cudaStreamWaitEvent(s, c->join_ev, 0), "join wait");
-  launches += (t.n_wtiles ? 1 : 0) + (t.n_btiles ? 1 : 0) + (t.n_lumped ? 1 : 0) + (t.nC ? 2 : 0);
-  if (t.net_model == 1) {                    // row f1: the nets' reduced-order models
+  if (rc) {
+    ck(sta::launch_rc(t, b, c->wgrid, s), "rc kernel");
+    if (t.nC && !std::getenv("STA_RC_SERIAL")) ck(cudaStreamWaitEvent(s, c->join_ev, 0), "join wait");
+    launches += (t.n_wtiles ? 1 : 0) + (t.n_btiles ? 1 : 0) + (t.n_lumped ? 1 : 0) + (t.nC ? 2 : 0);
+  }
+  if (rc && t.net_model == 1) {              // row f1: the nets' reduced-order models
     ck(sta::launch_arn_reduce(t, b, s), "arnoldi kernel");
     launches += t.n_arn_nets ? 1 : 0;
   }
@@ -1448,6 +1524,34 @@ u32 enqueue_batch(sta_ctx c, const sta::Batch& b) {
   return launches;
 }
 
+// One update of every batch; with exceptions (row f4) one forward / backward
+// pass per startpoint tag (RC in the first only), each folded into the merged
+// arrays, then WNS / TNS from the merged per-endpoint worst slacks.
+u32 enqueue_all(sta_ctx c, const std::vector<sta::Batch>& batches) {
+  u32 launches = 0;
+  if (c->exc_seed_d.empty()) {
+    for (const sta::Batch& b : batches) launches += enqueue_batch(c, b, c->topo, true);
+    return launches;
+  }
+  for (size_t j = 0; j < c->exc_seed_d.size(); ++j) {
+    sta::Topo tj = c->topo;
+    tj.seed = c->exc_seed_d[j];
+    tj.ep_ovr = c->exc_ovr_d[j];
+    for (const sta::Batch& b : batches) {
+      launches += enqueue_batch(c, b, tj, j == 0);
+      for (u32 k = 0; k < b.K; ++k) ck(sta::launch_merge_tag(tj, b.c[k], j == 0 ? 1 : 0, c->stream), "merge kernel");
+      launches += b.K;
+    }
+  }
+  for (const sta::Batch& b : batches) {
+    sta::Batch bm = b;
+    for (u32 k = 0; k < b.K; ++k) bm.c[k].ep_ws = bm.c[k].m_ep_ws;
+    ck(sta::launch_reduce(c->topo, bm, c->stream), "merged reduce kernel");
+    launches += 1;
+  }
+  return launches;
+}
+
 // STA_TRACE=<path>: after an update, write the persistent kernels' per-chunk
 // and per-unit {start, ready, end} timestamps of corner 0 and the stage of
 // every chunk / unit (debug tooling: scripts/trace_report.py)
@@ -1476,7 +1580,7 @@ void enqueue_update(sta_ctx c) {
   const std::vector<sta::Batch> batches = make_batches(c);
   if (!c->trace_path.empty()) {
     u32 launches = 0;
-    for (const sta::Batch& b : batches) launches += enqueue_batch(c, b);
+    launches += enqueue_all(c, batches);
     c->launches_per_update = launches;
     dump_trace(c);
     return;
@@ -1487,7 +1591,7 @@ void enqueue_update(sta_ctx c) {
       ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
       u32 launches = 0;
       try {
-        for (const sta::Batch& b : batches) launches += enqueue_batch(c, b);
+        launches += enqueue_all(c, batches);
       } catch (...) {
         cudaStreamEndCapture(s, &g);
         if (g) cudaGraphDestroy(g);
@@ -1504,8 +1608,10 @@ void enqueue_update(sta_ctx c) {
   }
   u32 launches = 0;
   prof_mark(c, 8);
+  if (!c->exc_seed_d.empty()) launches += enqueue_all(c, batches);   // (per-phase times: not split)
   for (const sta::Batch& b : batches) {
-    launches += enqueue_batch(c, b);
+    if (!c->exc_seed_d.empty()) break;
+    launches += enqueue_batch(c, b, c->topo, true);
     if (c->prof) {
       // accumulate per phase (synchronous read of the event pairs)
       ck(cudaEventSynchronize(c->ev[7]), "event sync");
@@ -1761,6 +1867,12 @@ sta_status sta_load_graph(sta_ctx c, const sta_graph_desc* d) {
     c->fi_p_d = c->fi_slot_d = c->ep_int_d = c->uoi_d = nullptr;
     c->steiner_arena.release();
     c->steiner_ready = false;
+    c->exc_kind.clear();
+    c->exc_value.clear();
+    c->exc_from_ptr.clear();
+    c->exc_from.clear();
+    c->exc_to_ptr.clear();
+    c->exc_to.clear();
     c->P = d->num_pins; c->N = d->num_nets; c->A = d->num_arcs; c->C = d->num_checks; c->T = d->num_tables;
     c->pin_cap = fetch(d->pin_cap, c->P, d->mem, "pin_cap", c->stream);
     c->pin_role = fetch(d->pin_role, c->P, d->mem, "pin_role", c->stream);
@@ -1849,6 +1961,47 @@ sta_status sta_set_library(sta_ctx c, uint32_t corner, sta_mem mem, uint32_t num
   });
 }
 
+
+sta_status sta_set_exceptions(sta_ctx c, const sta_exceptions* ex) {
+  return guard(c, [&] {
+    Nvtx nvtx_range("sta_set_exceptions");
+    if (!ex) fail(STA_ERR_ARG, "exceptions NULL");
+    if (!c->has_graph) fail(STA_ERR_ORDER, "sta_set_exceptions before sta_load_graph");
+    const u32 E = ex->num;
+    if (E > 32) fail(STA_ERR_ARG, "%u exceptions (at most 32)", E);
+    std::vector<uint8_t> kind;
+    std::vector<float> value;
+    std::vector<u32> fp, fr, tp, to;
+    if (E) {
+      kind = fetch(ex->kind, E, ex->mem, "kind", c->stream);
+      value = fetch(ex->value, E, ex->mem, "value", c->stream);
+      fp = fetch(ex->from_ptr, E + 1, ex->mem, "from_ptr", c->stream);
+      tp = fetch(ex->to_ptr, E + 1, ex->mem, "to_ptr", c->stream);
+      if (fp[0] != 0 || tp[0] != 0) fail(STA_ERR_CSR, "from_ptr / to_ptr must start at 0");
+      for (u32 e = 0; e < E; ++e)
+        if (fp[e + 1] < fp[e] || tp[e + 1] < tp[e]) fail(STA_ERR_CSR, "exception %u: offsets not monotone", e);
+      fr = fetch(ex->from_pins, fp[E], ex->mem, "from_pins", c->stream);
+      to = fetch(ex->to_pins, tp[E], ex->mem, "to_pins", c->stream);
+      for (u32 p : fr) if (p >= c->P) fail(STA_ERR_ID, "exception -from pin %u out of range", p);
+      for (u32 p : to) if (p >= c->P) fail(STA_ERR_ID, "exception -to pin %u out of range", p);
+      for (u32 e = 0; e < E; ++e) {
+        if (kind[e] > STA_EXC_MIN_DELAY) fail(STA_ERR_ARG, "exception %u: kind %u", e, kind[e]);
+        if (!std::isfinite(value[e])) fail(STA_ERR_ARG, "exception %u: non-finite value", e);
+        if (kind[e] == STA_EXC_MULTICYCLE && !(value[e] >= 1.f && value[e] == std::floor(value[e])))
+          fail(STA_ERR_ARG, "exception %u: multicycle needs an integer N >= 1", e);
+      }
+    }
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    c->exc_kind = std::move(kind);
+    c->exc_value = std::move(value);
+    c->exc_from_ptr = std::move(fp);
+    c->exc_from = std::move(fr);
+    c->exc_to_ptr = std::move(tp);
+    c->exc_to = std::move(to);
+    c->prepared = false;                     // tags, seeds, overrides and merged arrays next update
+    invalidate_graph(c);
+  });
+}
 
 sta_status sta_set_net_model(sta_ctx c, sta_net_model model, uint32_t q) {
   return guard(c, [&] {
@@ -2115,6 +2268,7 @@ sta_status sta_report_paths(sta_ctx c, uint32_t corner, const sta_path_query* q,
     if (q->mode > 1) fail(STA_ERR_ARG, "mode %u (0 setup, 1 hold)", q->mode);
     if (q->k == 0 || q->nworst == 0) fail(STA_ERR_ARG, "k and nworst must be >= 1");
     if (c->net_model != 0) fail(STA_ERR_ORDER, "the path report needs the Elmore net model");
+    if (!c->exc_kind.empty()) fail(STA_ERR_ORDER, "the path report needs no timing exceptions");
     if (mem != STA_MEM_HOST && mem != STA_MEM_DEVICE) fail(STA_ERR_ARG, "bad sta_mem %d", (int)mem);
     const u32 m = std::min(q->k, q->nworst);
     if (m > 255) fail(STA_ERR_ARG, "min(k, nworst) = %u exceeds 255", m);

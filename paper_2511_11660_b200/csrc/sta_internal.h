@@ -192,6 +192,10 @@ struct Topo {
   const uint4* arn_node;      // [n_rc] {caller node id, internal parent or kNone at the root,
                               //  subtree end (internal), sink index or kNone}
   const float* arn_scap;      // [n_rc] pin + PO cap at the node
+  // NEXT row f4 (reduced): endpoint overrides of the tag this pass propagates
+  // (nullptr: no exceptions), per endpoint {late mode, late value bits,
+  // early mode, early value bits}; mode 0 shift, 1 replace, 2 no seed
+  const uint4* ep_ovr;
   uint32_t n_arn_big;
   const uint32_t* arn_big;    // indices (into arn_nets) of the nets of more than 1024 RC nodes
   uint64_t n_rc_nodes;
@@ -223,6 +227,8 @@ struct CornerDev {
   const float* const* rc_vals;  // device {res, cap} pointer pair (user node order)
   double* scratch;    // tier-C scratch (tierC_scratch)
   uint32_t* err_flag; // nonzero: bad RC value seen
+  float4* m_pin;      // exceptions (row f4): [4][P] user order, at / slew / rat / slack merged over tags
+  float2* m_ep_ws;    // [n_ep] worst setup / hold slack per endpoint merged over tags
   float4* arn_lam;    // [NP] Arnoldi time constants of the net each pull pin drives (x < 0: Elmore)
   float4* arn_res;    // [NS] residues of each sink
   double* arn_scr;    // [(arn_q + 4) n_rc] Lanczos scratch
@@ -321,6 +327,9 @@ cudaError_t levelize_device(uint32_t P, uint32_t N, uint32_t A, const uint32_t* 
                             const uint32_t* arc_from, const uint32_t* arc_to, uint32_t* level, uint32_t* perm,
                             uint32_t* fi_ptr, uint32_t* fi_ids, uint32_t* fo_ptr, uint32_t* fo_ids,
                             uint32_t* num_levels, uint32_t* cycle_pin, cudaStream_t s);
+
+// ---- NEXT row f4 (reduced): merge one tag's results into the merged arrays
+cudaError_t launch_merge_tag(const Topo& t, const CornerDev& c, int first, cudaStream_t s);
 
 // ---- NEXT row f1: Arnoldi reduced-order models of every net (sta_arnoldi.cu)
 cudaError_t launch_arn_reduce(const Topo& t, const Batch& b, cudaStream_t s);

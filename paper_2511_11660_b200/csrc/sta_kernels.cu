@@ -1227,22 +1227,34 @@ __device__ __forceinline__ bool arc_live(uint32_t info, const Q4& a) {
 // clock slew), RAT_E = hold(slew_E(D), clock slew), only where the arrival
 // exists.  chk / po: from the pin's fan-out record.
 __device__ __forceinline__ void seed4(const Topo& t, const float* __restrict__ L, uint32_t chk, uint32_t po,
-                                      const Q4& a, const Q4& s, Q4& r) {
+                                      const Q4& a, const Q4& s, Q4& r, uint32_t e = kNone) {
+  Q4 sd = undef_rat();
   if (po != kNone) {
     const float4 ps = __ldg(t.po_seed + po);
-    r.v[0] = fmaxf(r.v[0], ps.x);
-    r.v[1] = fmaxf(r.v[1], ps.y);
-    r.v[2] = fminf(r.v[2], ps.z);
-    r.v[3] = fminf(r.v[3], ps.w);
+    sd.v[0] = ps.x;
+    sd.v[1] = ps.y;
+    sd.v[2] = ps.z;
+    sd.v[3] = ps.w;
   }
   if (chk != kNone) {
 #pragma unroll
     for (int rf = 0; rf < 2; ++rf) {
       if (fin(a.v[2 + rf]))
-        r.v[2 + rf] = fminf(r.v[2 + rf], __fsub_rn(t.period, lut(L, chk + rf, s.v[2 + rf], t.clock_slew)));
-      if (fin(a.v[rf])) r.v[rf] = fmaxf(r.v[rf], lut(L, chk + 2 + rf, s.v[rf], t.clock_slew));
+        sd.v[2 + rf] = fminf(sd.v[2 + rf], __fsub_rn(t.period, lut(L, chk + rf, s.v[2 + rf], t.clock_slew)));
+      if (fin(a.v[rf])) sd.v[rf] = fmaxf(sd.v[rf], lut(L, chk + 2 + rf, s.v[rf], t.clock_slew));
     }
   }
+  if (t.ep_ovr && e != kNone) {              // row f4: this tag's exception at the endpoint
+    const uint4 o = __ldg(t.ep_ovr + e);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t mode = q < 2 ? o.z : o.x;
+      const float v = __uint_as_float(q < 2 ? o.w : o.y);
+      if (!fin(sd.v[q])) continue;           // no base seed of this kind
+      sd.v[q] = mode == 2 ? (q < 2 ? -CUDART_INF_F : CUDART_INF_F) : mode == 1 ? v : __fadd_rn(sd.v[q], v);
+    }
+  }
+  combine(r, sd);
 }
 
 // Loads of the two inline fan-out terms of a pin's fan-out record (fa, fb),
@@ -1285,7 +1297,7 @@ __device__ __forceinline__ void bwd_pin(const Topo& t, const CornerDev& c, const
   const uint32_t nfo = fa.y;
   uint32_t f = 0;
   if (fa.w != kNone) {
-    seed4(t, L, fb.x, fb.y, a, s, r);
+    seed4(t, L, fb.x, fb.y, a, s, r, fa.w);
   } else if (nfo) {
     const bool l0 = arc_live(fb.y, a), l1 = nfo > 1 && arc_live(fb.w, a), shared = fb.z == fb.x;
     if (l0 || (l1 && shared)) spin_pair(c.rat_ll + 2 * (size_t)fb.x, p.e0, p.l0, ep);
@@ -1749,9 +1761,62 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(Topo t, const __grid_c
 // ----------------------------------------------------- outputs / setup
 // what: 0 at, 1 slew, 2 rat, 3 slack, in user pin order; sink arrivals and
 // slews are recomputed from their drivers exactly as the kernels do.
+// a user pin's at / slew / rat / slack (what 0..3) from the internal records
+__device__ __forceinline__ float4 pin_value(const Topo& t, const CornerDev& c, uint32_t p, int what) {
+  const uint32_t i = t.int_of_user[p];
+  if (what == 3) return c.slack[i];
+  if (what == 2) {                           // pull pins: tagged words {(el, r), (el, f)}
+    if (i >= t.NP) return c.rat[i];
+    const uint4 e = __ldcg(c.rat_ll + 2 * (size_t)i), l = __ldcg(c.rat_ll + 2 * (size_t)i + 1);
+    return make_float4(__uint_as_float(e.x), __uint_as_float(e.z), __uint_as_float(l.x), __uint_as_float(l.z));
+  }
+  Q4 at, sl;
+  if (i < t.NP) {
+    load_rec(c, i, at, sl);
+    return to_f4(what == 0 ? at : sl);
+  }
+  const uint32_t k = i - t.NP;
+  load_rec(c, t.sink_drv[k], at, sl);
+  if (t.net_model == 1) arn_net_hop(at, sl, c.elm[k], c.arn_lam[t.sink_drv[k]], c.arn_res[k], true);
+  else net_hop(at, sl, c.elm[k]);
+  return to_f4(what == 0 ? at : sl);
+}
+
+// row f4: fold this tag's results into the merged arrays (user order)
+__global__ void merge_tag_kernel(Topo t, CornerDev c, int first) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < t.n_ep) {
+    const float2 w = c.ep_ws[p];
+    if (first) c.m_ep_ws[p] = w;
+    else {
+      const float2 m = c.m_ep_ws[p];
+      c.m_ep_ws[p] = make_float2(fminf(m.x, w.x), fminf(m.y, w.y));
+    }
+  }
+  if (p >= t.P) return;
+#pragma unroll
+  for (int what = 0; what < 4; ++what) {
+    const float4 v = pin_value(t, c, p, what);
+    float4* m = c.m_pin + (size_t)what * t.P + p;
+    if (first) {
+      *m = v;
+      continue;
+    }
+    const float4 o = *m;
+    // early components: AT / slew min, RAT max; late: AT / slew max, RAT min; slack min
+    if (what < 2) *m = make_float4(fminf(o.x, v.x), fminf(o.y, v.y), fmaxf(o.z, v.z), fmaxf(o.w, v.w));
+    else if (what == 2) *m = make_float4(fmaxf(o.x, v.x), fmaxf(o.y, v.y), fminf(o.z, v.z), fminf(o.w, v.w));
+    else *m = make_float4(fminf(o.x, v.x), fminf(o.y, v.y), fminf(o.z, v.z), fminf(o.w, v.w));
+  }
+}
+
 __global__ void gather_pins_kernel(Topo t, CornerDev c, int what, float4* __restrict__ dst) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= t.P) return;
+  if (c.m_pin) {                             // exceptions: the results merged over tags
+    dst[p] = c.m_pin[(size_t)what * t.P + p];
+    return;
+  }
   const uint32_t i = t.int_of_user[p];
   if (what == 3) {
     dst[p] = c.slack[i];
@@ -2083,6 +2148,12 @@ cudaError_t launch_reduce(const Topo& t, const Batch& b, cudaStream_t s) {
 
 cudaError_t launch_gather_pins(const Topo& t, const CornerDev& c, int what, float4* dst, cudaStream_t s) {
   if (t.P) gather_pins_kernel<<<blocks(t.P), kThreads, 0, s>>>(t, c, what, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge_tag(const Topo& t, const CornerDev& c, int first, cudaStream_t s) {
+  const uint32_t n = t.P > t.n_ep ? t.P : t.n_ep;
+  if (n) merge_tag_kernel<<<blocks(n), kThreads, 0, s>>>(t, c, first);
   return cudaGetLastError();
 }
 

@@ -29,7 +29,8 @@ EXPORTS = ["sta_create", "sta_destroy", "sta_last_error", "sta_status_string", "
            "sta_set_library", "sta_set_rc_tree", "sta_set_rc_values", "sta_set_constraints",
            "sta_update_timing", "sta_report_slack", "sta_get_timing", "sta_get_rc",
            "sta_get_levels", "sta_get_info", "sta_synchronize", "sta_profile_enable",
-           "sta_profile_read", "sta_report_paths", "sta_build_steiner", "sta_set_net_model"]
+           "sta_profile_read", "sta_report_paths", "sta_build_steiner", "sta_set_net_model",
+           "sta_set_exceptions"]
 
 
 class StaError(RuntimeError):
@@ -77,6 +78,12 @@ class PathSet(C.Structure):
                 ("path_ep", C.c_void_p)]
 
 
+class ExceptionsDesc(C.Structure):
+    _fields_ = [("mem", C.c_int), ("num", C.c_uint32), ("kind", C.c_void_p), ("value", C.c_void_p),
+                ("from_ptr", C.c_void_p), ("from_pins", C.c_void_p), ("to_ptr", C.c_void_p),
+                ("to_pins", C.c_void_p)]
+
+
 class SteinerUnits(C.Structure):
     _fields_ = [("res_x", C.c_float), ("res_y", C.c_float), ("cap_x", C.c_float), ("cap_y", C.c_float)]
 
@@ -121,6 +128,7 @@ def lib():
             "sta_build_steiner": (i32, [vp, i32, vp, vp, C.POINTER(SteinerUnits), u32, vp, vp, vp, vp, vp,
                                         C.POINTER(u32)]),
             "sta_set_net_model": (i32, [vp, i32, u32]),
+            "sta_set_exceptions": (i32, [vp, C.POINTER(ExceptionsDesc)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -310,6 +318,20 @@ class Context:
         n = nn.value
         return (rc_ptr,) + tuple(o[:n] for o in outs)
 
+    def set_exceptions(self, kind=(), value=(), from_ptr=(0,), from_pins=(), to_ptr=(0,), to_pins=()):
+        """-from / -to timing exceptions (sta_set_exceptions); no arguments clear them."""
+        a = _Args(self.device)
+        e = ExceptionsDesc()
+        e.num = len(kind)
+        e.kind = a.ptr(kind, np.uint8)
+        e.value = a.ptr(value, np.float32)
+        e.from_ptr = a.ptr(from_ptr, np.uint32)
+        e.from_pins = a.ptr(from_pins, np.uint32)
+        e.to_ptr = a.ptr(to_ptr, np.uint32)
+        e.to_pins = a.ptr(to_pins, np.uint32)
+        e.mem = a.kind
+        self._check(self._L.sta_set_exceptions(self.h, C.byref(e)))
+
     def set_net_model(self, model: str = "elmore", q: int = 4):
         """Net-arc delay model of the next updates: "elmore" or "arnoldi"
         (reduced order q in 1..4)."""
@@ -451,3 +473,6 @@ def load_design(ctx: Context, d, corners=None, device_rc: bool = False, device_g
     k = d.cons
     ctx.set_constraints(k.period, k.clock_slew, g(k.pi_pin), g(k.pi_at), g(k.pi_slew), g(k.po_pin),
                         g(k.po_out_max), g(k.po_out_min), g(k.po_load))
+    ex = getattr(d, "exceptions", None)
+    if ex is not None and ex.num:
+        ctx.set_exceptions(ex.kind, ex.value, ex.from_ptr, ex.from_pins, ex.to_ptr, ex.to_pins)

@@ -1,0 +1,120 @@
+"""GPU parity of the -from / -to timing exceptions (SURVEY.md §8(f) row 4,
+reduced; sta_set_exceptions) against the oracle's O13: every pin's merged
+arrival / slew / required time / slack and WNS / TNS element by element.
+
+Run on a B200 via gpurun:  python -m pytest tests -m gpu -x -q
+"""
+import copy
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth.design import Exceptions
+from tests.parity import compare_update
+from tests.test_oracle_exceptions import random_exceptions, _endpoints, _startpoints
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sta():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device: GPU tests must run on the B200 (there is no CPU fallback)")
+    import paper_2511_11660_b200 as pkg
+    return pkg
+
+
+def run(sta, d, corners=1, model="elmore"):
+    ctx = sta.Context(0, corners)
+    sta.load_design(ctx, d)
+    if model != "elmore":
+        ctx.set_net_model(model, 4)
+    ctx.update_timing()
+    return ctx
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_exceptions(sta, seed):
+    d = synth.generate(2500, 18, seed=200 + seed, period=400.0)
+    rng = np.random.default_rng(seed)
+    d.exceptions = random_exceptions(d, rng, int(rng.integers(1, 7)))
+    ctx = run(sta, d)
+    compare_update(ctx, oracle.update(d))
+    ctx.close()
+
+
+def test_tags_from_startpoints(sta):
+    # several -from classes (up to 7 tags) mixing every kind, -to on subsets
+    d = synth.generate(6000, 24, seed=210, period=500.0)
+    sp, ep = _startpoints(d), _endpoints(d)
+    rng = np.random.default_rng(3)
+    perm = list(rng.permutation(sp))
+    g = len(sp) // 8
+    items = []
+    for k in range(6):
+        fr = perm[k * g:(k + 1) * g] + (perm[:g // 2] if k == 5 else [])   # disjoint classes + one overlap
+        to = list(rng.choice(ep, size=len(ep) // 3, replace=False)) if k % 2 else []
+        kind = k % 4
+        val = 2.0 if kind == 1 else (350.0 if kind == 2 else 5.0)
+        items.append((kind, val, fr, to))
+    d.exceptions = Exceptions.build(items)
+    ctx = run(sta, d)
+    compare_update(ctx, oracle.update(d))
+    ctx.close()
+
+
+def test_exceptions_clear_and_paths(sta):
+    d = synth.generate(1500, 14, seed=220, period=300.0)
+    d.exceptions = Exceptions.build([(0, 0.0, [], _endpoints(d)[:5]), (1, 2.0, [], [])])
+    ctx = run(sta, d)
+    compare_update(ctx, oracle.update(d))
+    with pytest.raises(sta.StaError) as e:
+        ctx.report_paths(0, "setup", k=3)
+    assert e.value.name == "STA_ERR_ORDER"
+    ctx.set_exceptions()                       # cleared: the plain update again
+    ctx.update_timing()
+    d0 = copy.copy(d)
+    d0.exceptions = None
+    compare_update(ctx, oracle.update(d0))
+    ctx.report_paths(0, "setup", k=3)
+    ctx.close()
+
+
+def test_exceptions_multicorner_arnoldi(sta):
+    d = synth.generate(2000, 14, seed=230, corners=2, period=400.0)
+    rng = np.random.default_rng(9)
+    d.exceptions = random_exceptions(d, rng, 4)
+    ctx = run(sta, d, corners=2, model="arnoldi")
+    for k in range(2):
+        compare_update(ctx, oracle.update(d, corner=k, net_model="arnoldi"), corner=k)
+    ctx.close()
+
+
+def test_exceptions_c2(sta):
+    d = synth.config_design("c2_tau", corners=1)
+    sp, ep = _startpoints(d), _endpoints(d)
+    rng = np.random.default_rng(11)
+    d.exceptions = Exceptions.build([
+        (0, 0.0, list(rng.choice(sp, 20, replace=False)), []),
+        (1, 2.0, [], list(rng.choice(ep, 200, replace=False))),
+        (2, 900.0, list(rng.choice(sp, 30, replace=False)), list(rng.choice(ep, 300, replace=False))),
+        (3, 3.0, [], list(rng.choice(ep, 100, replace=False)))])
+    ctx = run(sta, d)
+    compare_update(ctx, oracle.update(d))
+    ctx.close()
+
+
+def test_exception_errors(sta):
+    d = synth.generate(300, 8, seed=240, period=300.0)
+    ctx = sta.Context(0, 1)
+    sta.load_design(ctx, d)
+    with pytest.raises(sta.StaError) as e:
+        ctx.set_exceptions([1], [1.5], [0, 0], [], [0, 0], [])       # multicycle N not integral
+    assert e.value.name == "STA_ERR_ARG"
+    with pytest.raises(sta.StaError) as e:
+        ctx.set_exceptions([0], [0.0], [0, 1], [d.num_pins], [0, 0], [])
+    assert e.value.name == "STA_ERR_ID"
+    ctx.close()
