@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--phases", action="store_true", help="with --quick: still measure the per-phase times")
     ap.add_argument("--net-model", default="elmore", choices=["elmore", "arnoldi"],
                     help="net-arc delay model (row f1: arnoldi = reduced order 4)")
+    ap.add_argument("--exceptions", action="store_true",
+                    help="row f4: a seeded set of -from / -to exceptions (3 startpoint tags)")
     return ap.parse_args()
 
 
@@ -65,6 +67,25 @@ def corner_design(name, corner):
         d.libs = [d.libs[0].scaled(ls)]
         d.rc = [d.rc[0].scaled(rs, cs)]
     return d
+
+
+def bench_exceptions(d):
+    """Row f4 workload: false path from 1% of the startpoints, multicycle 2 to
+    5% of the endpoints, max delay T/2 from another 1% to 5%, min delay 3 ps
+    to 2% (seeded; 3 startpoint tags)."""
+    import synth
+    from synth.design import Exceptions
+    rng = np.random.default_rng(0xE7C)
+    sp = sorted(set(int(p) for p in d.cons.pi_pin) |
+                set(int(p) for p in np.nonzero(d.pin_role == synth.ROLE_FF_CK)[0]))
+    ep = sorted(set(int(p) for p in d.cons.po_pin) | set(int(p) for p in d.chk_d))
+    sp_p = rng.permutation(sp)
+    n_s, n_e = max(1, len(sp) // 100), max(1, len(ep) // 20)
+    return Exceptions.build([
+        (0, 0.0, list(sp_p[:n_s]), []),
+        (1, 2.0, [], list(rng.choice(ep, n_e, replace=False))),
+        (2, float(d.cons.period) / 2, list(sp_p[n_s:2 * n_s]), list(rng.choice(ep, n_e, replace=False))),
+        (3, 3.0, [], list(rng.choice(ep, max(1, len(ep) // 50), replace=False)))])
 
 
 def measured_peaks():
@@ -246,6 +267,8 @@ def main():
     K = len(mine)
     ctx = pkg.Context(local, K, stream=stream.cuda_stream)
     t0 = time.perf_counter()
+    if args.exceptions:
+        d.exceptions = bench_exceptions(d)
     pkg.load_design(ctx, d, corners=mine)
     if args.net_model != "elmore":
         ctx.set_net_model(args.net_model, 4)
@@ -313,7 +336,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if name == "c5_multicorner" else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": dict(config_line(name, info, K, world, gen_s, load_s), net_model=args.net_model),
+            "config": dict(config_line(name, info, K, world, gen_s, load_s), net_model=args.net_model,
+                           exceptions=bool(args.exceptions)),
             "gpu_launches": info["kernels_per_update"] * args.steps,
             "clocks": clk, "wns_tns": [float(x) for x in res_own[0]]}
     if name == "c5_multicorner":

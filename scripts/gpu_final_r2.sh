@@ -17,6 +17,9 @@ timeout 900 python scripts/bench_tdp.py --iters 1000 --check > gpurun_out/bench_
 for cfg in c2_tau c4_tdp c3_superblue; do
 timeout 600 python bench.py --config $cfg --net-model arnoldi --steps 10 --warmup 3 --no-cpu-baseline --quick --phases > gpurun_out/bench_arnoldi_${cfg}_${T}.json 2> gpurun_out/bench_arnoldi_${cfg}_${T}.err
 done
+for cfg in c2_tau c3_superblue; do
+timeout 600 python bench.py --config $cfg --exceptions --steps 10 --warmup 3 --no-cpu-baseline --quick > gpurun_out/bench_exc_${cfg}_${T}.json 2> gpurun_out/bench_exc_${cfg}_${T}.err
+done
 timeout 900 python scripts/bench_steiner.py c4_tdp --full-parity > gpurun_out/steiner_c4_${T}.json 2> gpurun_out/steiner_c4_${T}.err
 timeout 900 python scripts/bench_steiner.py c3_superblue --reps 3 > gpurun_out/steiner_c3_${T}.json 2> gpurun_out/steiner_c3_${T}.err
 timeout 600 python scripts/latency_probe.py > gpurun_out/latency_${T}.txt 2>&1
