@@ -1447,7 +1447,7 @@ void prepare(sta_ctx c) {
     d.m_pin = nullptr;
     d.m_ep_ws = nullptr;
     if (!c->exc_kind.empty()) {
-      d.m_pin = a.alloc<float4>(4 * (size_t)std::max<u32>(P, 1));
+      d.m_pin = a.alloc<float4>(4 * (size_t)std::max<u32>(c->Pi, 1));
       d.m_ep_ws = a.alloc<float2>(std::max<u32>(c->n_ep, 1));
     }
     d.arn_lam = nullptr;

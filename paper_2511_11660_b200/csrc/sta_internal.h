@@ -227,7 +227,7 @@ struct CornerDev {
   const float* const* rc_vals;  // device {res, cap} pointer pair (user node order)
   double* scratch;    // tier-C scratch (tierC_scratch)
   uint32_t* err_flag; // nonzero: bad RC value seen
-  float4* m_pin;      // exceptions (row f4): [4][P] user order, at / slew / rat / slack merged over tags
+  float4* m_pin;      // exceptions (row f4): [4][NP + NS] internal order, at / slew / rat / slack merged over tags
   float2* m_ep_ws;    // [n_ep] worst setup / hold slack per endpoint merged over tags
   float4* arn_lam;    // [NP] Arnoldi time constants of the net each pull pin drives (x < 0: Elmore)
   float4* arn_res;    // [NS] residues of each sink

@@ -1761,52 +1761,47 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(Topo t, const __grid_c
 // ----------------------------------------------------- outputs / setup
 // what: 0 at, 1 slew, 2 rat, 3 slack, in user pin order; sink arrivals and
 // slews are recomputed from their drivers exactly as the kernels do.
-// a user pin's at / slew / rat / slack (what 0..3) from the internal records
-__device__ __forceinline__ float4 pin_value(const Topo& t, const CornerDev& c, uint32_t p, int what) {
-  const uint32_t i = t.int_of_user[p];
-  if (what == 3) return c.slack[i];
-  if (what == 2) {                           // pull pins: tagged words {(el, r), (el, f)}
-    if (i >= t.NP) return c.rat[i];
-    const uint4 e = __ldcg(c.rat_ll + 2 * (size_t)i), l = __ldcg(c.rat_ll + 2 * (size_t)i + 1);
-    return make_float4(__uint_as_float(e.x), __uint_as_float(e.z), __uint_as_float(l.x), __uint_as_float(l.z));
+// row f4: fold this tag's results into the merged arrays, internal order
+// (pin i: its record read once for arrival and slew; a sink's driver record
+// is shared by its neighbours in the sink order)
+__global__ void merge_tag_kernel(Topo t, CornerDev c, int first) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < t.n_ep) {
+    const float2 w = c.ep_ws[i];
+    if (first) c.m_ep_ws[i] = w;
+    else {
+      const float2 m = c.m_ep_ws[i];
+      c.m_ep_ws[i] = make_float2(fminf(m.x, w.x), fminf(m.y, w.y));
+    }
   }
+  const size_t Pi = (size_t)t.NP + t.NS;
+  if (i >= Pi) return;
   Q4 at, sl;
+  float4 rt;
   if (i < t.NP) {
     load_rec(c, i, at, sl);
-    return to_f4(what == 0 ? at : sl);
+    const uint4 e = __ldcg(c.rat_ll + 2 * (size_t)i), l = __ldcg(c.rat_ll + 2 * (size_t)i + 1);
+    rt = make_float4(__uint_as_float(e.x), __uint_as_float(e.z), __uint_as_float(l.x), __uint_as_float(l.z));
+  } else {
+    const uint32_t k = i - t.NP, dv = t.sink_drv[k];
+    load_rec(c, dv, at, sl);
+    if (t.net_model == 1) arn_net_hop(at, sl, c.elm[k], c.arn_lam[dv], c.arn_res[k], true);
+    else net_hop(at, sl, c.elm[k]);
+    rt = c.rat[i];
   }
-  const uint32_t k = i - t.NP;
-  load_rec(c, t.sink_drv[k], at, sl);
-  if (t.net_model == 1) arn_net_hop(at, sl, c.elm[k], c.arn_lam[t.sink_drv[k]], c.arn_res[k], true);
-  else net_hop(at, sl, c.elm[k]);
-  return to_f4(what == 0 ? at : sl);
-}
-
-// row f4: fold this tag's results into the merged arrays (user order)
-__global__ void merge_tag_kernel(Topo t, CornerDev c, int first) {
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < t.n_ep) {
-    const float2 w = c.ep_ws[p];
-    if (first) c.m_ep_ws[p] = w;
-    else {
-      const float2 m = c.m_ep_ws[p];
-      c.m_ep_ws[p] = make_float2(fminf(m.x, w.x), fminf(m.y, w.y));
-    }
-  }
-  if (p >= t.P) return;
+  const float4 v[4] = {to_f4(at), to_f4(sl), rt, c.slack[i]};
 #pragma unroll
   for (int what = 0; what < 4; ++what) {
-    const float4 v = pin_value(t, c, p, what);
-    float4* m = c.m_pin + (size_t)what * t.P + p;
+    float4* m = c.m_pin + (size_t)what * Pi + i;
     if (first) {
-      *m = v;
+      *m = v[what];
       continue;
     }
-    const float4 o = *m;
+    const float4 o = *m, x = v[what];
     // early components: AT / slew min, RAT max; late: AT / slew max, RAT min; slack min
-    if (what < 2) *m = make_float4(fminf(o.x, v.x), fminf(o.y, v.y), fmaxf(o.z, v.z), fmaxf(o.w, v.w));
-    else if (what == 2) *m = make_float4(fmaxf(o.x, v.x), fmaxf(o.y, v.y), fminf(o.z, v.z), fminf(o.w, v.w));
-    else *m = make_float4(fminf(o.x, v.x), fminf(o.y, v.y), fminf(o.z, v.z), fminf(o.w, v.w));
+    if (what < 2) *m = make_float4(fminf(o.x, x.x), fminf(o.y, x.y), fmaxf(o.z, x.z), fmaxf(o.w, x.w));
+    else if (what == 2) *m = make_float4(fmaxf(o.x, x.x), fmaxf(o.y, x.y), fminf(o.z, x.z), fminf(o.w, x.w));
+    else *m = make_float4(fminf(o.x, x.x), fminf(o.y, x.y), fminf(o.z, x.z), fminf(o.w, x.w));
   }
 }
 
@@ -1814,7 +1809,7 @@ __global__ void gather_pins_kernel(Topo t, CornerDev c, int what, float4* __rest
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= t.P) return;
   if (c.m_pin) {                             // exceptions: the results merged over tags
-    dst[p] = c.m_pin[(size_t)what * t.P + p];
+    dst[p] = c.m_pin[(size_t)what * ((size_t)t.NP + t.NS) + t.int_of_user[p]];
     return;
   }
   const uint32_t i = t.int_of_user[p];
@@ -2152,7 +2147,8 @@ cudaError_t launch_gather_pins(const Topo& t, const CornerDev& c, int what, floa
 }
 
 cudaError_t launch_merge_tag(const Topo& t, const CornerDev& c, int first, cudaStream_t s) {
-  const uint32_t n = t.P > t.n_ep ? t.P : t.n_ep;
+  const uint64_t pi = (uint64_t)t.NP + t.NS;
+  const uint64_t n = pi > t.n_ep ? pi : t.n_ep;
   if (n) merge_tag_kernel<<<blocks(n), kThreads, 0, s>>>(t, c, first);
   return cudaGetLastError();
 }
