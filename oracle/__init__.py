@@ -52,6 +52,7 @@ class _Design(C.Structure):
         ("n_exc", C.c_uint32), ("exc_kind", C.c_void_p), ("exc_value", C.c_void_p),
         ("exc_from_ptr", C.c_void_p), ("exc_from", C.c_void_p), ("exc_to_ptr", C.c_void_p),
         ("exc_to", C.c_void_p),
+        ("n_clk", C.c_uint32), ("clk_period", C.c_void_p), ("pin_clk", C.c_void_p),
     ]
 
 
@@ -148,6 +149,11 @@ class _Marshal:
             s.exc_from = _p(arr(ex.from_pins, np.uint32))
             s.exc_to_ptr = _p(arr(ex.to_ptr, np.uint32))
             s.exc_to = _p(arr(ex.to_pins, np.uint32))
+        ck = getattr(d, "clocks", None)
+        s.n_clk = int(ck.period.shape[0]) if ck is not None else 0
+        if s.n_clk:
+            s.clk_period = _p(arr(ck.period, np.float32))
+            s.pin_clk = _p(arr(ck.pin_clk, np.uint32))
         self.s = s
         self.keep = keep
 

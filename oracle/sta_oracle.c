@@ -450,16 +450,39 @@ static int in_list(const uint32_t* a, uint32_t lo, uint32_t hi, uint32_t p) {
 
 enum { EXC_FALSE = 0, EXC_MULTICYCLE = 1, EXC_MAX = 2, EXC_MIN = 3 };
 
+/* O14: setup / hold relationships between a launch clock of period TL and a
+ * capture clock of period TC (rising edges at multiples of the period; the
+ * "bounded hyperperiod" of SPEC.md:504 = the first 1000 launch edges,
+ * DESIGN.md X7): for launch edge a the setup capture edge is the first
+ * capture edge strictly after a, the hold edge the capture edge before it;
+ * setup = the smallest (capture - launch), hold = the largest (hold edge -
+ * launch).  One clock: setup T, hold 0. */
+static void clk_rel(double TL, double TC, double* rs, double* rh) {
+  double s = INF, h = -INF;
+  for (int i = 0; i < 1000; i++) {
+    const double a = i * TL;
+    const double nxt = (floor(a / TC) + 1.0) * TC;
+    if (nxt - a < s) s = nxt - a;
+    if (nxt - TC - a > h) h = nxt - TC - a;
+  }
+  *rs = s;
+  *rh = h;
+}
+
 static int run_tagged(const orc_design* d, double* at, double* slew, double* rat, double* slack,
                       double res[4], uint32_t* ep_pin, double* ep_ws, uint32_t* n_ep_out) {
   const uint32_t P = d->num_pins, E = d->n_exc;
   if (E > 32) return 5;
-  /* step 1: the tag (exception bitset) of every pin that could be a startpoint */
-  uint32_t* tag = calloc(P + 1, sizeof(uint32_t));
+  /* step 1: the tag of every pin that could be a startpoint: its launch
+   * clock (bits 32+) and the exceptions whose -from holds it (bits 0..31) */
+  uint64_t* tag = calloc(P + 1, sizeof(uint64_t));
   for (uint32_t e = 0; e < E; e++)
-    for (uint32_t i = d->exc_from_ptr[e]; i < d->exc_from_ptr[e + 1]; i++) tag[d->exc_from[i]] |= 1u << e;
+    for (uint32_t i = d->exc_from_ptr[e]; i < d->exc_from_ptr[e + 1]; i++) tag[d->exc_from[i]] |= 1ull << e;
+  if (d->n_clk)
+    for (uint32_t p = 0; p < P; p++) tag[p] |= (uint64_t)d->pin_clk[p] << 32;
   /* step 2: the distinct tags of the startpoints, in pin order */
-  uint32_t tags[64], T = 0;
+  uint64_t tags[64];
+  uint32_t T = 0;
   int bad = 0;
   for (uint32_t p = 0; p < P; p++) {
     int sp = d->pin_role[p] == ORC_FF_CK;
@@ -484,9 +507,24 @@ static int run_tagged(const orc_design* d, double* at, double* slew, double* rat
   for (uint32_t j = 0; j < T && !st; j++) {
     /* step 3: tag j: its startpoints seeded; each endpoint's exception */
     for (uint32_t p = 0; p < P; p++) on[p] = tag[p] == tags[j];
+    const uint32_t lclk = (uint32_t)(tags[j] >> 32);
     for (uint32_t p = 0; p < P; p++) {
       double* o = ovr + 4 * (size_t)p;
       o[0] = o[1] = o[2] = o[3] = 0.0;
+      /* O14: the capture clock of endpoint p (a PO's own, a D pin's register
+       * clock) and the relationship to this tag's launch clock; the base
+       * seeds assume the single clock `period` (setup T, hold 0) */
+      double Tcap = d->period;
+      if (d->n_clk) {
+        uint32_t cc = d->pin_clk[p];
+        for (uint32_t c = 0; c < d->num_checks; c++)
+          if (d->chk_d[c] == p) { cc = d->pin_clk[d->chk_ck[c]]; break; }
+        Tcap = d->clk_period[cc];
+        double rs, rh;
+        clk_rel(d->clk_period[lclk], Tcap, &rs, &rh);
+        o[1] = rs - d->period;
+        o[3] = rh;
+      }
       int lf = -1, lm = -1, lc = -1, ef = -1, em = -1, ec = -1;
       for (uint32_t e = 0; e < E; e++) {
         const int has_from = d->exc_from_ptr[e + 1] > d->exc_from_ptr[e];
@@ -502,10 +540,10 @@ static int run_tagged(const orc_design* d, double* at, double* slew, double* rat
       }
       if (lf >= 0) o[0] = 2;
       else if (lm >= 0) { o[0] = 1; o[1] = d->exc_value[lm]; }
-      else if (lc >= 0) o[1] = (d->exc_value[lc] - 1.0) * d->period;
+      else if (lc >= 0) o[1] += (d->exc_value[lc] - 1.0) * Tcap;
       if (ef >= 0) o[2] = 2;
       else if (em >= 0) { o[2] = 1; o[3] = d->exc_value[em]; }
-      else if (ec >= 0) o[3] = (d->exc_value[ec] - 1.0) * d->period;
+      else if (ec >= 0) o[3] += (d->exc_value[ec] - 1.0) * Tcap;
     }
     st = run_update(d, t_at, t_sl, t_rat, t_sk, t_res, t_ep, t_ws, &n_ep, NULL, on, ovr);
     if (st) break;
@@ -541,7 +579,7 @@ static int run_tagged(const orc_design* d, double* at, double* slew, double* rat
 
 int orc_update(const orc_design* d, double* at, double* slew, double* rat, double* slack,
                double res[4], uint32_t* ep_pin, double* ep_ws, uint32_t* n_ep_out) {
-  if (d->n_exc) return run_tagged(d, at, slew, rat, slack, res, ep_pin, ep_ws, n_ep_out);
+  if (d->n_exc || d->n_clk) return run_tagged(d, at, slew, rat, slack, res, ep_pin, ep_ws, n_ep_out);
   return run_update(d, at, slew, rat, slack, res, ep_pin, ep_ws, n_ep_out, NULL, NULL, NULL);
 }
 
@@ -558,7 +596,7 @@ int orc_paths(const orc_design* d, int mode, uint32_t k, uint32_t nworst, double
   uint32_t P = d->num_pins;
   double* at = malloc(sizeof(double) * 4 * (size_t)(P + 1));
   if (!at) return 2;
-  if (d->n_exc) { free(at); return 4; }      /* path reports: no exceptions (X6) */
+  if (d->n_exc || d->n_clk) { free(at); return 4; }   /* path reports: one clock, no exceptions (X6) */
   int st = run_update(d, at, NULL, NULL, NULL, res, NULL, NULL, NULL, &q, NULL, NULL);
   free(at);
   *n_paths = q.n_paths;
@@ -653,9 +691,11 @@ static int run_update(const orc_design* d, double* at, double* slew, double* rat
   for (uint32_t p = 0; p < P; p++) {
     if (d->pin_role[p] != ORC_FF_CK || g.fi_ptr[p + 1] != g.fi_ptr[p]) continue;
     if (seed_on && !seed_on[p]) continue;
-    /* ideal clock, rising edge at 0, waveform (0, T/2) */
-    at[4 * p + Q(0, 0)] = 0.0; at[4 * p + Q(0, 1)] = d->period / 2;
-    at[4 * p + Q(1, 0)] = 0.0; at[4 * p + Q(1, 1)] = d->period / 2;
+    /* ideal clock, rising edge at 0, waveform (0, T/2); with
+     * several clocks the period of the pin's own clock (O14) */
+    const double Tc = d->n_clk ? (double)d->clk_period[d->pin_clk[p]] : d->period;
+    at[4 * p + Q(0, 0)] = 0.0; at[4 * p + Q(0, 1)] = Tc / 2;
+    at[4 * p + Q(1, 0)] = 0.0; at[4 * p + Q(1, 1)] = Tc / 2;
     for (int q = 0; q < 4; q++) slew[4 * p + q] = d->clock_slew;
   }
 

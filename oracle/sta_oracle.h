@@ -82,6 +82,12 @@ typedef struct {
   const uint32_t* exc_from;
   const uint32_t* exc_to_ptr;
   const uint32_t* exc_to;
+  /* multiple ideal clocks (row f4, O14): n_clk periods; pin_clk[P] = the
+   * clock of each FF_CK pin, the launch clock of each PI, the capture clock
+   * of each PO (n_clk = 0: the single clock `period`) */
+  uint32_t n_clk;
+  const float* clk_period;
+  const uint32_t* pin_clk;
 } orc_design;
 
 /* O6: NLDM bilinear lookup, fp64.  `tab` points at

@@ -65,10 +65,16 @@ mut 'cs = os;' 'cs = s_in;'
 mut 'if (t > D) r2 = lam > 0.0 ? (t - D) - lam * (1.0 - exp(-(t - D) / lam)) : t - D;' ''
 mut 'return t50 - 0.5 * D;' 'return t50;'
 # -from / -to exceptions (O13, row f4 reduced)
-mut 'else if (lc >= 0) o[1] = (d->exc_value[lc] - 1.0) * d->period;' 'else if (lc >= 0) o[1] = d->exc_value[lc] * d->period;'
+mut 'else if (lc >= 0) o[1] += (d->exc_value[lc] - 1.0) * Tcap;' 'else if (lc >= 0) o[1] += d->exc_value[lc] * Tcap;'
 mut '    if (seed_on && !seed_on[p]) continue;    /* O13: a startpoint of another tag */' ''
 mut '      if (slack) slack[i] = fmin(slack[i], t_sk[i]);' '      if (slack) slack[i] = fmax(slack[i], t_sk[i]);'
 mut '        if (has_from && !((tags[j] >> e) & 1u)) continue;' ''
-mut 'else if (ec >= 0) o[3] = (d->exc_value[ec] - 1.0) * d->period;' ''
+mut 'else if (ec >= 0) o[3] += (d->exc_value[ec] - 1.0) * Tcap;' ''
 mut '    for (uint32_t k = 0; k < 2 * n_ep; k++) m_ws[k] = j == 0 ? t_ws[k] : fmin(m_ws[k], t_ws[k]);' '    for (uint32_t k = 0; k < 2 * n_ep; k++) m_ws[k] = t_ws[k];'
+# multiple clocks (O14)
+mut '    if (nxt - TC - a > h) h = nxt - TC - a;' '    if (nxt - a > h) h = nxt - a;'
+mut '    const double nxt = (floor(a / TC) + 1.0) * TC;' '    const double nxt = ceil(a / TC) * TC;'
+mut '        for (uint32_t c = 0; c < d->num_checks; c++)
+mut '          if (d->chk_d[c] == p) { cc = d->pin_clk[d->chk_ck[c]]; break; }' '          if (d->chk_d[c] == p) { cc = d->pin_clk[p]; break; }'
+mut '    const double Tc = d->n_clk ? (double)d->clk_period[d->pin_clk[p]] : d->period;' '    const double Tc = d->period;'
 exit $fail

@@ -134,6 +134,15 @@ class Exceptions:
 
 
 @dataclass
+class Clocks:
+    """Multiple ideal clocks: period per clock; pin_clk[P]
+    = the clock of each FF_CK pin, the launch clock of each PI, the capture
+    clock of each PO (other entries unused)."""
+    period: np.ndarray     # float32 [n]
+    pin_clk: np.ndarray    # uint32 [P]
+
+
+@dataclass
 class Design:
     num_pins: int
     pin_cap: np.ndarray      # float32 [P]
@@ -153,6 +162,7 @@ class Design:
     name: str = "design"
     meta: dict = field(default_factory=dict)
     exceptions: Optional["Exceptions"] = None
+    clocks: Optional["Clocks"] = None
 
     @property
     def num_nets(self) -> int:

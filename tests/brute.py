@@ -365,6 +365,22 @@ def path_slacks_with_exceptions(d, elm_of_pin):
     cons = d.cons
     ex = d.exceptions
     T = float(cons.period)
+    ck = getattr(d, "clocks", None)
+
+    def clk_of(p):
+        return int(ck.pin_clk[p]) if ck is not None else 0
+
+    def per(c):
+        return float(ck.period[c]) if ck is not None else T
+
+    def rel(tl, tc):
+        """(setup, hold) relationship: first 1000 launch edges, next capture edge."""
+        s, h = INF, -INF
+        for i in range(1000):
+            a = i * tl
+            nxt = (math.floor(a / tc) + 1.0) * tc
+            s, h = min(s, nxt - a), max(h, nxt - tc - a)
+        return s, h
     arcs = _fanin_lists(d)
     P = d.num_pins
     succ = defaultdict(list)
@@ -377,9 +393,10 @@ def path_slacks_with_exceptions(d, elm_of_pin):
         succ[u].append((v, dl))
         indeg[v] += 1
     tag = np.zeros(P, np.int64)
-    for k in range(ex.num):
-        for p in ex.from_pins[int(ex.from_ptr[k]):int(ex.from_ptr[k + 1])]:
-            tag[int(p)] |= 1 << k
+    if ex is not None:
+        for k in range(ex.num):
+            for p in ex.from_pins[int(ex.from_ptr[k]):int(ex.from_ptr[k + 1])]:
+                tag[int(p)] |= 1 << k
     seed_at = {}
     for k in range(cons.pi_pin.size):
         p = int(cons.pi_pin[k])
@@ -387,7 +404,13 @@ def path_slacks_with_exceptions(d, elm_of_pin):
             seed_at[p] = [float(x) for x in cons.pi_at[k]]
     for p in range(P):
         if int(d.pin_role[p]) == ROLE_FF_CK and indeg[p] == 0:
-            seed_at[p] = [0.0, T / 2, 0.0, T / 2]
+            tc = per(clk_of(p))
+            seed_at[p] = [0.0, tc / 2, 0.0, tc / 2]
+    cap_clk = {}
+    for k in range(cons.po_pin.size):
+        cap_clk[int(cons.po_pin[k])] = clk_of(int(cons.po_pin[k]))
+    for c in range(d.num_checks):
+        cap_clk[int(d.chk_d[c])] = clk_of(int(d.chk_ck[c]))
     base_l = defaultdict(lambda: [INF, INF])
     base_e = defaultdict(lambda: [-INF, -INF])
     po_l, po_e, ck_l, ck_e = {}, {}, {}, {}
@@ -407,15 +430,20 @@ def path_slacks_with_exceptions(d, elm_of_pin):
         mode, val = ov
         return INF if mode == 2 else (val if mode == 1 else v + val)
 
-    def req(e, rf, tg, late):
-        c = exception_of(ex, tg, e, late)
-        ov = None
+    def req(e, rf, tg, late, s_clk=0):
+        # the clock relationship of (launch, capture) replaces the single-clock
+        # setup edge T / hold edge 0 of the base seeds
+        tcap = per(cap_clk.get(e, 0))
+        rs, rh = rel(per(s_clk), tcap)
+        shift = (rs - T) if late else rh
+        c = exception_of(ex, tg, e, late) if ex is not None else {0: None, 1: None, 2: None, 3: None}
+        ov = (0, shift)
         if c[0] is not None:
             ov = (2, 0.0)
         elif c[2 if late else 3] is not None:
             ov = (1, float(ex.value[c[2 if late else 3]]))
         elif c[1] is not None:
-            ov = (0, (float(ex.value[c[1]]) - 1.0) * T)
+            ov = (0, shift + (float(ex.value[c[1]]) - 1.0) * tcap)
         vals = [x[rf] for x in (po_l if late else po_e).get(e, [])] + [x[rf] for x in (ck_l if late else ck_e).get(e, [])]
         if not vals:
             return None
@@ -433,13 +461,13 @@ def path_slacks_with_exceptions(d, elm_of_pin):
         stack.append((v, rf))
         if v in po_l or v in ck_l:
             tg = int(tag[s])
-            rl = req(v, rf, tg, True)
+            rl = req(v, rf, tg, True, clk_of(s))
             if rl is not None and rl < INF:
                 sl = rl - (seed_at[s][2 + s_rf] + acc)
                 ws[v] = min(ws[v], sl)
                 for (x, r) in stack:
                     slack[x, 2 + r] = min(slack[x, 2 + r], sl)
-            re = req(v, rf, tg, False)
+            re = req(v, rf, tg, False, clk_of(s))
             if re is not None and re > -INF:
                 sh = (seed_at[s][s_rf] + acc) - re
                 wh[v] = min(wh[v], sh)
