@@ -251,6 +251,27 @@ typedef struct {
 } sta_exceptions;
 STA_API sta_status sta_set_exceptions(sta_ctx ctx, const sta_exceptions* ex);
 
+/* Multiple ideal clocks (reduced: "cross clock region
+ * paths"; the relationship rule of SPEC.md:504).  Clock k:
+ * period_ps[k], rising edges at multiples of the period, waveform (0, T/2).
+ * pin_clk[P]: the clock of each FF_CK pin (its register), the launch clock
+ * of each PI (the input delay's clock) and the capture clock of each PO
+ * (the output delay's clock); other entries are ignored.  Startpoints are
+ * tagged by their launch clock (and their -from exceptions) and propagated
+ * per tag; an endpoint's setup edge is the first capture edge after the
+ * launch edge, its hold edge the capture edge before that, taken over the
+ * first 1000 launch edges (the most restrictive pair); multicycle shifts use
+ * the capture period.  num_clocks = 0: one clock, the constraints' period.
+ * At most 16 clocks.  Arrays in `mem`, copied.  Errors: STA_ERR_ORDER,
+ * STA_ERR_ARG, STA_ERR_ID. */
+typedef struct {
+  sta_mem mem;
+  uint32_t num_clocks;
+  const float* period_ps;
+  const uint32_t* pin_clk;
+} sta_clocks;
+STA_API sta_status sta_set_clocks(sta_ctx ctx, const sta_clocks* clk);
+
 /* Per-corner RC values: res[i] = resistance of the edge parent -> i (kOhm,
  * ignored at node 0), cap[i] = wire capacitance to ground at node i (fF);
  * both num_nodes long, >= 0 and finite.  HOST: copied into ctx-owned device

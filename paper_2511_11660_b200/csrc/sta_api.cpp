@@ -236,6 +236,8 @@ struct sta_ctx_s {
   Arena path_arena;                              // path report: their device copies + user_of_int
   // row f4 (reduced): -from / -to exceptions; per startpoint tag a seed array
   // and endpoint overrides (prepare)
+  std::vector<float> clk_period;                 // multiple ideal clocks (row f4; empty: one clock)
+  std::vector<u32> pin_clk;
   std::vector<uint8_t> exc_kind;
   std::vector<float> exc_value;
   std::vector<u32> exc_from_ptr, exc_from, exc_to_ptr, exc_to;
@@ -1292,12 +1294,45 @@ void prepare(sta_ctx c) {
   c->exc_arena.release();
   c->exc_seed_d.clear();
   c->exc_ovr_d.clear();
-  if (!c->exc_kind.empty()) {
+  // multiple clocks: the clock pins' seeds become "virtual PI" entries after
+  // the real ones, one per clock: arrival (0, T_c / 2), the clock slew
+  std::vector<float> pi_at_v(c->pi_at), pi_slew_v(c->pi_slew);
+  const u32 n_clk = (u32)c->clk_period.size();
+  if (n_clk) {
+    const u32 base = (u32)(c->pi_at.size() / 4);
+    for (u32 k = 0; k < n_clk; ++k) {
+      const float h = 0.5f * c->clk_period[k];
+      const float a4[4] = {0.f, h, 0.f, h};
+      for (int q = 0; q < 4; ++q) {
+        pi_at_v.push_back(a4[q]);
+        pi_slew_v.push_back(c->clock_slew);
+      }
+    }
+    for (u32 i = 0; i < c->n0; ++i)
+      if (seed[i] == sta::kSeedClock) seed[i] = base + c->pin_clk[c->user_of_int[i]];
+    c->topo.seed = t.seed = g.upload(seed, s);
+  }
+  if (!c->exc_kind.empty() || n_clk) {
     const u32 E = (u32)c->exc_kind.size();
-    std::vector<u32> tagp(P, 0);
+    // a startpoint's tag: its launch clock (bits 32+) and the exceptions whose
+    // -from holds it (bits 0..31)
+    std::vector<uint64_t> tagp(P, 0);
     for (u32 e = 0; e < E; ++e)
-      for (u32 x = c->exc_from_ptr[e]; x < c->exc_from_ptr[e + 1]; ++x) tagp[c->exc_from[x]] |= 1u << e;
-    std::vector<u32> tags;
+      for (u32 x = c->exc_from_ptr[e]; x < c->exc_from_ptr[e + 1]; ++x) tagp[c->exc_from[x]] |= 1ull << e;
+    if (n_clk)
+      for (u32 p = 0; p < P; ++p) tagp[p] |= (uint64_t)c->pin_clk[p] << 32;
+    // (setup, hold) relationship of a launch / capture period pair: the
+    // first 1000 launch edges, the next capture edge (the oracle's O14)
+    auto rel = [](double TL, double TC, double& rs, double& rh) {
+      rs = std::numeric_limits<double>::infinity();
+      rh = -rs;
+      for (int i = 0; i < 1000; ++i) {
+        const double a = i * TL, nxt = (std::floor(a / TC) + 1.0) * TC;
+        rs = std::min(rs, nxt - a);
+        rh = std::max(rh, nxt - TC - a);
+      }
+    };
+    std::vector<uint64_t> tags;
     for (u32 p = 0; p < P; ++p) {
       const u32 i = c->int_of_user[p];
       if (i >= c->n0 || seed[i] == kNone) continue;
@@ -1310,7 +1345,8 @@ void prepare(sta_ctx c) {
       in_to[e].assign(P, 0);
       for (u32 x = c->exc_to_ptr[e]; x < c->exc_to_ptr[e + 1]; ++x) in_to[e][c->exc_to[x]] = 1;
     }
-    for (u32 tg : tags) {
+    for (uint64_t tg : tags) {
+      const u32 lclk = (u32)(tg >> 32);
       std::vector<u32> sd(seed);
       for (u32 i = 0; i < c->n0; ++i) {
         const u32 p = c->user_of_int[i];
@@ -1319,6 +1355,19 @@ void prepare(sta_ctx c) {
       std::vector<uint4> ov(c->n_ep);
       for (u32 k = 0; k < c->n_ep; ++k) {
         const u32 p = c->user_of_int[ep_int[k]];
+        // capture clock (a PO's own, a D pin's register clock) and the
+        // relationship to this tag's launch clock; the base seeds assume one
+        // clock of period T (setup T, hold 0)
+        double Tcap = c->period, sh_l = 0.0, sh_e = 0.0;
+        if (n_clk) {
+          u32 cc = c->pin_clk[p];
+          if (c->chk_of_pin[p] != kNone) cc = c->pin_clk[c->chk_ck[c->chk_of_pin[p]]];
+          Tcap = c->clk_period[cc];
+          double rs, rh;
+          rel(c->clk_period[lclk], Tcap, rs, rh);
+          sh_l = rs - (double)c->period;
+          sh_e = rh;
+        }
         int lf = -1, lm = -1, lc = -1, ef = -1, em = -1, ec = -1;
         for (u32 e = 0; e < E; ++e) {
           if (c->exc_from_ptr[e + 1] > c->exc_from_ptr[e] && !((tg >> e) & 1u)) continue;
@@ -1331,21 +1380,21 @@ void prepare(sta_ctx c) {
           }
         }
         auto bits = [](float f) { u32 u; std::memcpy(&u, &f, 4); return u; };
-        uint4 o = make_uint4(0, bits(0.f), 0, bits(0.f));
+        uint4 o = make_uint4(0, bits((float)sh_l), 0, bits((float)sh_e));
         if (lf >= 0) o.x = 2;
         else if (lm >= 0) { o.x = 1; o.y = bits(c->exc_value[lm]); }
-        else if (lc >= 0) o.y = bits((float)(((double)c->exc_value[lc] - 1.0) * (double)c->period));
+        else if (lc >= 0) o.y = bits((float)(sh_l + ((double)c->exc_value[lc] - 1.0) * Tcap));
         if (ef >= 0) o.z = 2;
         else if (em >= 0) { o.z = 1; o.w = bits(c->exc_value[em]); }
-        else if (ec >= 0) o.w = bits((float)(((double)c->exc_value[ec] - 1.0) * (double)c->period));
+        else if (ec >= 0) o.w = bits((float)(sh_e + ((double)c->exc_value[ec] - 1.0) * Tcap));
         ov[k] = o;
       }
       c->exc_seed_d.push_back(c->exc_arena.upload(sd, s));
       c->exc_ovr_d.push_back(c->exc_arena.upload(ov, s));
     }
   }
-  t.pi_at = reinterpret_cast<const float4*>(g.upload(c->pi_at, s));
-  t.pi_slew = reinterpret_cast<const float4*>(g.upload(c->pi_slew, s));
+  t.pi_at = reinterpret_cast<const float4*>(g.upload(pi_at_v, s));
+  t.pi_slew = reinterpret_cast<const float4*>(g.upload(pi_slew_v, s));
   t.po_out_max = reinterpret_cast<const float2*>(g.upload(c->po_out_max, s));
   t.po_out_min = reinterpret_cast<const float2*>(g.upload(c->po_out_min, s));
   t.period = c->period;
@@ -1446,7 +1495,7 @@ void prepare(sta_ctx c) {
     ck(cudaMemsetAsync(d.load, 0, sizeof(float) * std::max<u32>(c->NP, 1), s), "memset");
     d.m_pin = nullptr;
     d.m_ep_ws = nullptr;
-    if (!c->exc_kind.empty()) {
+    if (!c->exc_kind.empty() || !c->clk_period.empty()) {
       d.m_pin = a.alloc<float4>(4 * (size_t)std::max<u32>(c->Pi, 1));
       d.m_ep_ws = a.alloc<float2>(std::max<u32>(c->n_ep, 1));
     }
@@ -1873,6 +1922,8 @@ sta_status sta_load_graph(sta_ctx c, const sta_graph_desc* d) {
     c->exc_from.clear();
     c->exc_to_ptr.clear();
     c->exc_to.clear();
+    c->clk_period.clear();
+    c->pin_clk.clear();
     c->P = d->num_pins; c->N = d->num_nets; c->A = d->num_arcs; c->C = d->num_checks; c->T = d->num_tables;
     c->pin_cap = fetch(d->pin_cap, c->P, d->mem, "pin_cap", c->stream);
     c->pin_role = fetch(d->pin_role, c->P, d->mem, "pin_role", c->stream);
@@ -1999,6 +2050,30 @@ sta_status sta_set_exceptions(sta_ctx c, const sta_exceptions* ex) {
     c->exc_to_ptr = std::move(tp);
     c->exc_to = std::move(to);
     c->prepared = false;                     // tags, seeds, overrides and merged arrays next update
+    invalidate_graph(c);
+  });
+}
+
+sta_status sta_set_clocks(sta_ctx c, const sta_clocks* k) {
+  return guard(c, [&] {
+    Nvtx nvtx_range("sta_set_clocks");
+    if (!k) fail(STA_ERR_ARG, "clocks NULL");
+    if (!c->has_graph) fail(STA_ERR_ORDER, "sta_set_clocks before sta_load_graph");
+    std::vector<float> per;
+    std::vector<u32> pc;
+    if (k->num_clocks) {
+      if (k->num_clocks > 16) fail(STA_ERR_ARG, "%u clocks (at most 16)", k->num_clocks);
+      per = fetch(k->period_ps, k->num_clocks, k->mem, "period_ps", c->stream);
+      for (float v : per)
+        if (!(v > 0.f) || !std::isfinite(v)) fail(STA_ERR_ARG, "clock periods must be finite and > 0");
+      pc = fetch(k->pin_clk, c->P, k->mem, "pin_clk", c->stream);
+      for (u32 p = 0; p < c->P; ++p)
+        if (pc[p] >= k->num_clocks) fail(STA_ERR_ID, "pin %u: clock %u out of range", p, pc[p]);
+    }
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    c->clk_period = std::move(per);
+    c->pin_clk = std::move(pc);
+    c->prepared = false;
     invalidate_graph(c);
   });
 }
@@ -2268,7 +2343,8 @@ sta_status sta_report_paths(sta_ctx c, uint32_t corner, const sta_path_query* q,
     if (q->mode > 1) fail(STA_ERR_ARG, "mode %u (0 setup, 1 hold)", q->mode);
     if (q->k == 0 || q->nworst == 0) fail(STA_ERR_ARG, "k and nworst must be >= 1");
     if (c->net_model != 0) fail(STA_ERR_ORDER, "the path report needs the Elmore net model");
-    if (!c->exc_kind.empty()) fail(STA_ERR_ORDER, "the path report needs no timing exceptions");
+    if (!c->exc_kind.empty() || !c->clk_period.empty())
+      fail(STA_ERR_ORDER, "the path report needs one clock and no timing exceptions");
     if (mem != STA_MEM_HOST && mem != STA_MEM_DEVICE) fail(STA_ERR_ARG, "bad sta_mem %d", (int)mem);
     const u32 m = std::min(q->k, q->nworst);
     if (m > 255) fail(STA_ERR_ARG, "min(k, nworst) = %u exceeds 255", m);

@@ -30,7 +30,7 @@ EXPORTS = ["sta_create", "sta_destroy", "sta_last_error", "sta_status_string", "
            "sta_update_timing", "sta_report_slack", "sta_get_timing", "sta_get_rc",
            "sta_get_levels", "sta_get_info", "sta_synchronize", "sta_profile_enable",
            "sta_profile_read", "sta_report_paths", "sta_build_steiner", "sta_set_net_model",
-           "sta_set_exceptions"]
+           "sta_set_exceptions", "sta_set_clocks"]
 
 
 class StaError(RuntimeError):
@@ -84,6 +84,10 @@ class ExceptionsDesc(C.Structure):
                 ("to_pins", C.c_void_p)]
 
 
+class ClocksDesc(C.Structure):
+    _fields_ = [("mem", C.c_int), ("num_clocks", C.c_uint32), ("period_ps", C.c_void_p), ("pin_clk", C.c_void_p)]
+
+
 class SteinerUnits(C.Structure):
     _fields_ = [("res_x", C.c_float), ("res_y", C.c_float), ("cap_x", C.c_float), ("cap_y", C.c_float)]
 
@@ -129,6 +133,7 @@ def lib():
                                         C.POINTER(u32)]),
             "sta_set_net_model": (i32, [vp, i32, u32]),
             "sta_set_exceptions": (i32, [vp, C.POINTER(ExceptionsDesc)]),
+            "sta_set_clocks": (i32, [vp, C.POINTER(ClocksDesc)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -332,6 +337,16 @@ class Context:
         e.mem = a.kind
         self._check(self._L.sta_set_exceptions(self.h, C.byref(e)))
 
+    def set_clocks(self, period_ps=(), pin_clk=None):
+        """Multiple ideal clocks (sta_set_clocks); no arguments: one clock."""
+        a = _Args(self.device)
+        k = ClocksDesc()
+        k.num_clocks = len(period_ps)
+        k.period_ps = a.ptr(period_ps, np.float32)
+        k.pin_clk = a.ptr(pin_clk, np.uint32) if k.num_clocks else None
+        k.mem = a.kind
+        self._check(self._L.sta_set_clocks(self.h, C.byref(k)))
+
     def set_net_model(self, model: str = "elmore", q: int = 4):
         """Net-arc delay model of the next updates: "elmore" or "arnoldi"
         (reduced order q in 1..4)."""
@@ -473,6 +488,9 @@ def load_design(ctx: Context, d, corners=None, device_rc: bool = False, device_g
     k = d.cons
     ctx.set_constraints(k.period, k.clock_slew, g(k.pi_pin), g(k.pi_at), g(k.pi_slew), g(k.po_pin),
                         g(k.po_out_max), g(k.po_out_min), g(k.po_load))
+    ck = getattr(d, "clocks", None)
+    if ck is not None and len(ck.period):
+        ctx.set_clocks(ck.period, ck.pin_clk)
     ex = getattr(d, "exceptions", None)
     if ex is not None and ex.num:
         ctx.set_exceptions(ex.kind, ex.value, ex.from_ptr, ex.from_pins, ex.to_ptr, ex.to_pins)

@@ -118,3 +118,37 @@ def test_exception_errors(sta):
         ctx.set_exceptions([0], [0.0], [0, 1], [d.num_pins], [0, 0], [])
     assert e.value.name == "STA_ERR_ID"
     ctx.close()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_multiple_clocks(sta, seed):
+    # 2-3 ideal clocks (launch / capture relationships), half with exceptions on top
+    from tests.test_oracle_exceptions import random_clocks
+    d = synth.generate(3000, 20, seed=250 + seed, period=400.0)
+    rng = np.random.default_rng(50 + seed)
+    d.clocks = random_clocks(d, rng, int(rng.integers(2, 4)))
+    if seed % 2:
+        d.exceptions = random_exceptions(d, rng, 3)
+    ctx = run(sta, d)
+    compare_update(ctx, oracle.update(d))
+    ctx.close()
+
+
+def test_clocks_reset_and_errors(sta):
+    from tests.test_oracle_exceptions import random_clocks
+    d = synth.generate(1500, 12, seed=260, period=300.0)
+    d.clocks = random_clocks(d, np.random.default_rng(1), 2)
+    ctx = run(sta, d)
+    compare_update(ctx, oracle.update(d))
+    ctx.set_clocks()                           # back to the single clock
+    ctx.update_timing()
+    d0 = copy.copy(d)
+    d0.clocks = None
+    compare_update(ctx, oracle.update(d0))
+    with pytest.raises(sta.StaError) as e:
+        ctx.set_clocks([100.0, -1.0], np.zeros(d.num_pins, np.uint32))
+    assert e.value.name == "STA_ERR_ARG"
+    with pytest.raises(sta.StaError) as e:
+        ctx.set_clocks([100.0], np.full(d.num_pins, 3, np.uint32))
+    assert e.value.name == "STA_ERR_ID"
+    ctx.close()
