@@ -74,7 +74,6 @@ mut '    for (uint32_t k = 0; k < 2 * n_ep; k++) m_ws[k] = j == 0 ? t_ws[k] : fm
 # multiple clocks (O14)
 mut '    if (nxt - TC - a > h) h = nxt - TC - a;' '    if (nxt - a > h) h = nxt - a;'
 mut '    const double nxt = (floor(a / TC) + 1.0) * TC;' '    const double nxt = ceil(a / TC) * TC;'
-mut '        for (uint32_t c = 0; c < d->num_checks; c++)
 mut '          if (d->chk_d[c] == p) { cc = d->pin_clk[d->chk_ck[c]]; break; }' '          if (d->chk_d[c] == p) { cc = d->pin_clk[p]; break; }'
 mut '    const double Tc = d->n_clk ? (double)d->clk_period[d->pin_clk[p]] : d->period;' '    const double Tc = d->period;'
 exit $fail
