@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--phases", action="store_true", help="with --quick: still measure the per-phase times")
     ap.add_argument("--net-model", default="elmore", choices=["elmore", "arnoldi"],
                     help="net-arc delay model (row f1: arnoldi = reduced order 4)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo: several ranks may share one GPU -- a functional "
+                         "multi-rank check on a one-GPU box, not a scaling measurement)")
     ap.add_argument("--exceptions", action="store_true",
                     help="row f4: a seeded set of -from / -to exceptions (3 startpoint tags)")
     return ap.parse_args()
@@ -240,9 +243,13 @@ def main():
         return
     import torch
     import torch.distributed as dist
+    local = local % max(torch.cuda.device_count(), 1)   # ranks beyond the visible GPUs share them (gloo only)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     import paper_2511_11660_b200 as pkg
     from paper_2511_11660_b200 import build as pbuild
     from paper_2511_11660_b200 import multicorner as mc
@@ -337,7 +344,7 @@ def main():
             "scaling": "strong" if name == "c5_multicorner" else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": dict(config_line(name, info, K, world, gen_s, load_s), net_model=args.net_model,
-                           exceptions=bool(args.exceptions)),
+                           exceptions=bool(args.exceptions), dist_backend=args.dist_backend if world > 1 else None),
             "gpu_launches": info["kernels_per_update"] * args.steps,
             "clocks": clk, "wns_tns": [float(x) for x in res_own[0]]}
     if name == "c5_multicorner":
