@@ -23,6 +23,9 @@ done
 timeout 900 python scripts/bench_steiner.py c4_tdp --full-parity > gpurun_out/steiner_c4_${T}.json 2> gpurun_out/steiner_c4_${T}.err
 timeout 900 python scripts/bench_steiner.py c3_superblue --reps 3 > gpurun_out/steiner_c3_${T}.json 2> gpurun_out/steiner_c3_${T}.err
 timeout 600 python scripts/latency_probe.py > gpurun_out/latency_${T}.txt 2>&1
+# functional multi-rank check on the one GPU (gloo): C5 as 2 ranks x 4 corners
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 \
+    bench.py --gpus 2 --dist-backend gloo --steps 10 --warmup 3 --quick 2> gpurun_out/multirank_${T}.err | tail -1 > gpurun_out/multirank_${T}.json
 if [ "${NCU:-1}" = 1 ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_${T}.csv python bench.py --steps 3 --warmup 3 --quick > gpurun_out/ncu_launch_${T}.log 2>&1
