@@ -59,7 +59,8 @@ def build(force: bool = False, verbose: bool = False, out: str = None, flags: st
         if verbose:
             sys.stderr.write(r.stderr)
         with open(os.path.join(odir, (os.path.basename(lib) + "." if out else "") + src + ".ptxas.txt"), "w") as f:
-            f.write(r.stderr)
+            # resources only (compile times would churn the committed report)
+            f.write("".join(l for l in r.stderr.splitlines(True) if "Compile time" not in l))
         objs.append(obj)
     tmp = lib + ".tmp"
     cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
