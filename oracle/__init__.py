@@ -53,6 +53,7 @@ class _Design(C.Structure):
         ("exc_from_ptr", C.c_void_p), ("exc_from", C.c_void_p), ("exc_to_ptr", C.c_void_p),
         ("exc_to", C.c_void_p),
         ("n_clk", C.c_uint32), ("clk_period", C.c_void_p), ("pin_clk", C.c_void_p),
+        ("exc_thr_ptr", C.c_void_p), ("exc_seg_ptr", C.c_void_p), ("exc_seg", C.c_void_p),
     ]
 
 
@@ -149,6 +150,10 @@ class _Marshal:
             s.exc_from = _p(arr(ex.from_pins, np.uint32))
             s.exc_to_ptr = _p(arr(ex.to_ptr, np.uint32))
             s.exc_to = _p(arr(ex.to_pins, np.uint32))
+            if ex.thr_ptr is not None and int(ex.thr_ptr[-1]) > 0:   # O15: -through segments
+                s.exc_thr_ptr = _p(arr(ex.thr_ptr, np.uint32))
+                s.exc_seg_ptr = _p(arr(ex.seg_ptr, np.uint32))
+                s.exc_seg = _p(arr(ex.seg_pins, np.uint32))
         ck = getattr(d, "clocks", None)
         s.n_clk = int(ck.period.shape[0]) if ck is not None else 0
         if s.n_clk:
@@ -211,7 +216,7 @@ def update(d, corner: int = 0, want_all: bool = True, net_model: str = "elmore",
     if st == 1:
         raise ValueError("combinational cycle")
     if st == 5:
-        raise ValueError("too many exceptions (32) or startpoint tags (64)")
+        raise ValueError("too many exceptions (32), segments (32) or tags (64)")
     if st:
         raise MemoryError("oracle allocation failed")
     ne = int(n_ep[0])

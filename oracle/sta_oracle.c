@@ -413,23 +413,36 @@ static int path_report(const orc_design* d, const arcs_t* g, const uint32_t* ord
                        const double* elm, const double* dly, const double* seed, orc_path_req* q);
 
 /* --------------------------------------------------------- O4-O8: update */
+/* O15 handoff of one tag's pass at the -through pins (see run_tagged):
+ * dst[p] = the pass whose tag this pass's tag advances to at pin p
+ * (ORC_NO_PIN: none), thr[p] = p belongs to some -through segment; hand_at /
+ * hand_sl [n_tags][P][4] collect the arrivals handed to each pass, rhand
+ * [n_tags][P][4] the required times each pass computes at its through pins. */
+typedef struct {
+  uint32_t cur, P;
+  int fwd_only;
+  const uint32_t* dst;
+  const uint8_t* thr;
+  double *hand_at, *hand_sl, *rhand;
+} orc_thr;
+
 static int run_update(const orc_design* d, double* at, double* slew, double* rat, double* slack,
                       double res[4], uint32_t* ep_pin, double* ep_ws, uint32_t* n_ep_out, orc_path_req* pq,
-                      const uint8_t* seed_on, const double* ep_ovr);
+                      const uint8_t* seed_on, const double* ep_ovr, const orc_thr* th);
 static int run_tagged(const orc_design* d, double* at, double* slew, double* rat, double* slack,
                       double res[4], uint32_t* ep_pin, double* ep_ws, uint32_t* n_ep_out);
 
 
 /* --------------------------------------- O13: -from / -to timing exceptions */
-/* SURVEY.md §8(f) row 4 (reduced: no -through, no case analysis, one clock);
- * PAPER.md:113, 160-163 ("false paths, multi-cycle paths ... can
- * significantly complicate the data structures and states in timing
- * propagation"); the tag model of SPEC.md:465-509 with -from / -to
- * exceptions only: a path's tag is the set of exceptions whose -from list
- * holds its startpoint (exceptions without -from hold for every tag); tags
- * never change along a path, so each tag is propagated on its own (the
- * startpoints of that tag seeded, the others undefined) and per endpoint the
- * tag's exception is resolved (X1-X6):
+/* SURVEY.md §8(f) row 4 (reduced: no case analysis)
+ * ("false paths, multi-cycle paths ... can significantly complicate the data
+ * structures and states in timing propagation"); the tag model of
+ * a path's tag is its launch clock and the segment bits of
+ * the exceptions' -from / -through lists it has matched so far (O15 below);
+ * each tag is propagated on its own (the startpoints of that tag seeded, the
+ * others undefined; at -through pins arrivals move on to the advanced tag,
+ * O15) and per endpoint the exceptions the tag fully matches are resolved
+ * (X1-X6):
  *   late check: false path > max delay v (RAT_L = v) > multicycle N (capture
  *   at N T: RAT_L + (N-1) T); early check: false path > min delay v (RAT_E =
  *   v) > multicycle N (hold edge (N-1) T: RAT_E + (N-1) T); among exceptions
@@ -469,17 +482,81 @@ static void clk_rel(double TL, double TC, double* rs, double* rh) {
   *rh = h;
 }
 
+/* O15: -through ("tags
+ * advance their automaton bits at nodes belonging to a next-eligible
+ * segment"; "multiple -through patterns that eliminate only
+ * paths that go through a predefined pin sequence").  Exception e has the
+ * ordered segments [from (if listed), through_1 .. through_m], one tag bit
+ * each (bits base_e ..); a path's bits of e are always a prefix of its
+ * segments.  At its startpoint a path sets e's from bit if the startpoint is
+ * in the -from list; at every pin, while the next segment of e holds the pin,
+ * its bit is set (one pin may match consecutive segments, X8); an
+ * exception with a -from list that the startpoint missed never advances.
+ * The exception holds for a path when all its bits are set (and the endpoint
+ * is in its -to list).  adv() is that step. */
+typedef struct {
+  uint32_t base[32], nseg[32], has_from[32], total;
+} segmap;
+
+static int seg_map(const orc_design* d, segmap* m) {
+  m->total = 0;
+  for (uint32_t e = 0; e < d->n_exc; e++) {
+    m->has_from[e] = d->exc_from_ptr[e + 1] > d->exc_from_ptr[e];
+    m->nseg[e] = m->has_from[e] + (d->exc_thr_ptr ? d->exc_thr_ptr[e + 1] - d->exc_thr_ptr[e] : 0);
+    m->base[e] = m->total;
+    m->total += m->nseg[e];
+  }
+  return m->total <= 32;
+}
+
+/* does segment k of exception e hold pin p */
+static int seg_has(const orc_design* d, const segmap* m, uint32_t e, uint32_t k, uint32_t p) {
+  if (m->has_from[e] && k == 0) return in_list(d->exc_from, d->exc_from_ptr[e], d->exc_from_ptr[e + 1], p);
+  const uint32_t sg = d->exc_thr_ptr[e] + k - m->has_from[e];
+  return in_list(d->exc_seg, d->exc_seg_ptr[sg], d->exc_seg_ptr[sg + 1], p);
+}
+
+static uint32_t adv(const orc_design* d, const segmap* m, uint32_t bits, uint32_t p, int start) {
+  for (uint32_t e = 0; e < d->n_exc; e++) {
+    uint32_t k = 0;
+    while (k < m->nseg[e] && ((bits >> (m->base[e] + k)) & 1u)) k++;
+    if (m->has_from[e] && k == 0) {
+      if (!start || !seg_has(d, m, e, 0, p)) continue;
+      bits |= 1u << m->base[e];
+      k = 1;
+    }
+    while (k < m->nseg[e] && seg_has(d, m, e, k, p)) {
+      bits |= 1u << (m->base[e] + k);
+      k++;
+    }
+  }
+  return bits;
+}
+
+static int full(const segmap* m, uint32_t e, uint32_t bits) {
+  const uint32_t mask = m->nseg[e] >= 32 ? 0xFFFFFFFFu : ((1u << m->nseg[e]) - 1u);
+  return ((bits >> m->base[e]) & mask) == mask;
+}
+
+static int popc32(uint32_t x) {
+  int n = 0;
+  for (; x; x &= x - 1) n++;
+  return n;
+}
+
 static int run_tagged(const orc_design* d, double* at, double* slew, double* rat, double* slack,
                       double res[4], uint32_t* ep_pin, double* ep_ws, uint32_t* n_ep_out) {
   const uint32_t P = d->num_pins, E = d->n_exc;
   if (E > 32) return 5;
+  segmap m;
+  if (!seg_map(d, &m)) return 5;
   /* step 1: the tag of every pin that could be a startpoint: its launch
-   * clock (bits 32+) and the exceptions whose -from holds it (bits 0..31) */
+   * clock (bits 32+) and its segment bits after the startpoint (bits 0..31) */
   uint64_t* tag = calloc(P + 1, sizeof(uint64_t));
-  for (uint32_t e = 0; e < E; e++)
-    for (uint32_t i = d->exc_from_ptr[e]; i < d->exc_from_ptr[e + 1]; i++) tag[d->exc_from[i]] |= 1ull << e;
-  if (d->n_clk)
-    for (uint32_t p = 0; p < P; p++) tag[p] |= (uint64_t)d->pin_clk[p] << 32;
+  for (uint32_t p = 0; p < P; p++) {
+    tag[p] = adv(d, &m, 0u, p, 1);
+    if (d->n_clk) tag[p] |= (uint64_t)d->pin_clk[p] << 32;
+  }
   /* step 2: the distinct tags of the startpoints, in pin order */
   uint64_t tags[64];
   uint32_t T = 0;
@@ -493,23 +570,64 @@ static int run_tagged(const orc_design* d, double* at, double* slew, double* rat
     if (j == T) { if (T == 64) { bad = 1; break; } tags[T++] = tag[p]; }
   }
   if (T == 0) tags[T++] = 0;
+  /* O15: the tags reached by advancing at -through pins (closure), ordered
+   * by the number of set bits: a tag only advances to tags after it */
+  uint8_t* thr = calloc(P + 1, 1);
+  int any_thr = 0;
+  if (d->exc_thr_ptr)
+    for (uint32_t e = 0; e < E; e++)
+      for (uint32_t sg = d->exc_thr_ptr[e]; sg < d->exc_thr_ptr[e + 1]; sg++)
+        for (uint32_t i = d->exc_seg_ptr[sg]; i < d->exc_seg_ptr[sg + 1]; i++) { thr[d->exc_seg[i]] = 1; any_thr = 1; }
+  for (uint32_t i = 0; i < T && !bad; i++)
+    for (uint32_t p = 0; p < P && !bad; p++) {
+      if (!thr[p]) continue;
+      const uint64_t t2 = (tags[i] & ~0xFFFFFFFFull) | adv(d, &m, (uint32_t)tags[i], p, 0);
+      uint32_t j = 0;
+      while (j < T && tags[j] != t2) j++;
+      if (j == T) { if (T == 64) bad = 1; else tags[T++] = t2; }
+    }
+  for (uint32_t i = 1; i < T; i++)            /* stable insertion sort by set bits */
+    for (uint32_t j = i; j > 0 && popc32((uint32_t)tags[j - 1]) > popc32((uint32_t)tags[j]); j--) {
+      const uint64_t x = tags[j]; tags[j] = tags[j - 1]; tags[j - 1] = x;
+    }
   int st = bad ? 5 : 0;
   const size_t P4 = 4 * (size_t)(P + 1);
   double *t_at = malloc(sizeof(double) * P4), *t_sl = malloc(sizeof(double) * P4);
   double *t_rat = malloc(sizeof(double) * P4), *t_sk = malloc(sizeof(double) * P4);
-  double* ovr = malloc(sizeof(double) * P4);
-  uint8_t* on = malloc(P + 1);
+  double* ovr = malloc(sizeof(double) * P4 * (T ? T : 1));
+  uint8_t* on = malloc((size_t)(P + 1) * (T ? T : 1));
   uint32_t n_ep_max = d->n_po + d->num_checks + 1, n_ep = 0;
   uint32_t* t_ep = malloc(sizeof(uint32_t) * n_ep_max);
   double* t_ws = malloc(sizeof(double) * 2 * n_ep_max);
   double* m_ws = malloc(sizeof(double) * 2 * n_ep_max);
   double t_res[4];
+  /* O15 handoff buffers (tags x pins) and each pass's destination at every
+   * through pin */
+  const size_t TP4 = (size_t)T * P4;
+  uint32_t* dst = any_thr ? malloc(sizeof(uint32_t) * (size_t)T * (P + 1)) : NULL;
+  double* h_at = any_thr ? malloc(sizeof(double) * TP4) : NULL;
+  double* h_sl = any_thr ? malloc(sizeof(double) * TP4) : NULL;
+  double* h_rat = any_thr ? calloc(TP4, sizeof(double)) : NULL;
+  if (any_thr) {
+    for (size_t i = 0; i < TP4; i++) h_at[i] = h_sl[i] = (i & 3) < 2 ? INF : -INF;
+    for (uint32_t j = 0; j < T; j++)
+      for (uint32_t p = 0; p < P; p++) {
+        uint32_t to = ORC_NO_PIN;
+        if (thr[p]) {
+          const uint64_t t2 = (tags[j] & ~0xFFFFFFFFull) | adv(d, &m, (uint32_t)tags[j], p, 0);
+          if (t2 != tags[j])
+            for (uint32_t k = 0; k < T; k++) if (tags[k] == t2) to = k;
+        }
+        dst[(size_t)j * (P + 1) + p] = to;
+      }
+  }
   for (uint32_t j = 0; j < T && !st; j++) {
     /* step 3: tag j: its startpoints seeded; each endpoint's exception */
-    for (uint32_t p = 0; p < P; p++) on[p] = tag[p] == tags[j];
+    uint8_t* onj = on + (size_t)j * (P + 1);
+    for (uint32_t p = 0; p < P; p++) onj[p] = tag[p] == tags[j];
     const uint32_t lclk = (uint32_t)(tags[j] >> 32);
     for (uint32_t p = 0; p < P; p++) {
-      double* o = ovr + 4 * (size_t)p;
+      double* o = ovr + P4 * j + 4 * (size_t)p;
       o[0] = o[1] = o[2] = o[3] = 0.0;
       /* O14: the capture clock of endpoint p (a PO's own, a D pin's register
        * clock) and the relationship to this tag's launch clock; the base
@@ -527,9 +645,8 @@ static int run_tagged(const orc_design* d, double* at, double* slew, double* rat
       }
       int lf = -1, lm = -1, lc = -1, ef = -1, em = -1, ec = -1;
       for (uint32_t e = 0; e < E; e++) {
-        const int has_from = d->exc_from_ptr[e + 1] > d->exc_from_ptr[e];
         const int has_to = d->exc_to_ptr[e + 1] > d->exc_to_ptr[e];
-        if (has_from && !((tags[j] >> e) & 1u)) continue;
+        if (!full(&m, e, (uint32_t)tags[j])) continue;
         if (has_to && !in_list(d->exc_to, d->exc_to_ptr[e], d->exc_to_ptr[e + 1], p)) continue;
         switch (d->exc_kind[e]) {
           case EXC_FALSE: if (lf < 0) lf = (int)e; if (ef < 0) ef = (int)e; break;
@@ -545,18 +662,32 @@ static int run_tagged(const orc_design* d, double* at, double* slew, double* rat
       else if (em >= 0) { o[2] = 1; o[3] = d->exc_value[em]; }
       else if (ec >= 0) o[3] += (d->exc_value[ec] - 1.0) * Tcap;
     }
-    st = run_update(d, t_at, t_sl, t_rat, t_sk, t_res, t_ep, t_ws, &n_ep, NULL, on, ovr);
+  }
+  /* O15: a first sweep of the forwards in tag order collects every pass's
+   * handed-over arrivals; the full passes then run in reverse tag order so
+   * that the required times a pass takes over at its through pins exist */
+  if (any_thr)
+    for (uint32_t j = 0; j < T && !st; j++) {
+      orc_thr th = {j, P, 1, dst + (size_t)j * (P + 1), thr, h_at, h_sl, h_rat};
+      st = run_update(d, t_at, t_sl, t_rat, t_sk, t_res, t_ep, t_ws, &n_ep, NULL, on + (size_t)j * (P + 1),
+                      ovr + P4 * j, &th);
+    }
+  for (uint32_t jj = 0; jj < T && !st; jj++) {
+    const uint32_t j = any_thr ? T - 1 - jj : jj;
+    orc_thr th = {j, P, 0, any_thr ? dst + (size_t)j * (P + 1) : NULL, thr, h_at, h_sl, h_rat};
+    st = run_update(d, t_at, t_sl, t_rat, t_sk, t_res, t_ep, t_ws, &n_ep, NULL, on + (size_t)j * (P + 1),
+                    ovr + P4 * j, any_thr ? &th : NULL);
     if (st) break;
     /* step 4: merge over tags */
     for (size_t i = 0; i < 4 * (size_t)P; i++) {
       const int e = (i & 3) < 2;            /* early component */
-      if (j == 0) { at[i] = t_at[i]; if (slew) slew[i] = t_sl[i]; if (rat) rat[i] = t_rat[i]; if (slack) slack[i] = t_sk[i]; continue; }
+      if (jj == 0) { at[i] = t_at[i]; if (slew) slew[i] = t_sl[i]; if (rat) rat[i] = t_rat[i]; if (slack) slack[i] = t_sk[i]; continue; }
       at[i] = e ? fmin(at[i], t_at[i]) : fmax(at[i], t_at[i]);
       if (slew) slew[i] = e ? fmin(slew[i], t_sl[i]) : fmax(slew[i], t_sl[i]);
       if (rat) rat[i] = e ? fmax(rat[i], t_rat[i]) : fmin(rat[i], t_rat[i]);
       if (slack) slack[i] = fmin(slack[i], t_sk[i]);
     }
-    for (uint32_t k = 0; k < 2 * n_ep; k++) m_ws[k] = j == 0 ? t_ws[k] : fmin(m_ws[k], t_ws[k]);
+    for (uint32_t k = 0; k < 2 * n_ep; k++) m_ws[k] = jj == 0 ? t_ws[k] : fmin(m_ws[k], t_ws[k]);
   }
   if (!st) {
     double ws = INF, tns = 0.0, wh = INF, tnh = 0.0;
@@ -573,14 +704,14 @@ static int run_tagged(const orc_design* d, double* at, double* slew, double* rat
     if (n_ep_out) *n_ep_out = n_ep;
   }
   free(tag); free(t_at); free(t_sl); free(t_rat); free(t_sk); free(ovr); free(on);
-  free(t_ep); free(t_ws); free(m_ws);
+  free(t_ep); free(t_ws); free(m_ws); free(thr); free(dst); free(h_at); free(h_sl); free(h_rat);
   return st;
 }
 
 int orc_update(const orc_design* d, double* at, double* slew, double* rat, double* slack,
                double res[4], uint32_t* ep_pin, double* ep_ws, uint32_t* n_ep_out) {
   if (d->n_exc || d->n_clk) return run_tagged(d, at, slew, rat, slack, res, ep_pin, ep_ws, n_ep_out);
-  return run_update(d, at, slew, rat, slack, res, ep_pin, ep_ws, n_ep_out, NULL, NULL, NULL);
+  return run_update(d, at, slew, rat, slack, res, ep_pin, ep_ws, n_ep_out, NULL, NULL, NULL, NULL);
 }
 
 int orc_paths(const orc_design* d, int mode, uint32_t k, uint32_t nworst, double slack_lt, uint32_t cap_paths,
@@ -597,7 +728,7 @@ int orc_paths(const orc_design* d, int mode, uint32_t k, uint32_t nworst, double
   double* at = malloc(sizeof(double) * 4 * (size_t)(P + 1));
   if (!at) return 2;
   if (d->n_exc || d->n_clk) { free(at); return 4; }   /* path reports: one clock, no exceptions (X6) */
-  int st = run_update(d, at, NULL, NULL, NULL, res, NULL, NULL, NULL, &q, NULL, NULL);
+  int st = run_update(d, at, NULL, NULL, NULL, res, NULL, NULL, NULL, &q, NULL, NULL, NULL);
   free(at);
   *n_paths = q.n_paths;
   *n_pins = q.n_pins;
@@ -606,7 +737,7 @@ int orc_paths(const orc_design* d, int mode, uint32_t k, uint32_t nworst, double
 
 static int run_update(const orc_design* d, double* at, double* slew, double* rat, double* slack,
                       double res[4], uint32_t* ep_pin, double* ep_ws, uint32_t* n_ep_out, orc_path_req* pq,
-                      const uint8_t* seed_on, const double* ep_ovr) {
+                      const uint8_t* seed_on, const double* ep_ovr, const orc_thr* th) {
   const uint32_t P = d->num_pins;
   const double LN9 = log(9.0);
   arcs_t g; memset(&g, 0, sizeof g);
@@ -746,7 +877,28 @@ static int run_update(const orc_design* d, double* at, double* slew, double* rat
         }
       }
     }
+    /* O15: at a -through pin this tag's arrivals either move on to the tag
+     * it advances to (handed to that later pass, undefined here) or, if the
+     * tag is final at v, take in what earlier passes handed to it */
+    if (th && th->thr[v]) {
+      const uint32_t to = th->dst[v];
+      double* ha = (to != ORC_NO_PIN ? th->hand_at + ((size_t)to * th->P + v) * 4 : th->hand_at + ((size_t)th->cur * th->P + v) * 4);
+      double* hs = (to != ORC_NO_PIN ? th->hand_sl + ((size_t)to * th->P + v) * 4 : th->hand_sl + ((size_t)th->cur * th->P + v) * 4);
+      for (int q = 0; q < 4; q++) {
+        double* pa = &at[4 * v + q];
+        double* ps = &slew[4 * v + q];
+        if (to != ORC_NO_PIN) {
+          if (q < 2) { if (*pa < ha[q]) ha[q] = *pa; if (*ps < hs[q]) hs[q] = *ps; }
+          else       { if (*pa > ha[q]) ha[q] = *pa; if (*ps > hs[q]) hs[q] = *ps; }
+          *pa = *ps = q < 2 ? INF : -INF;
+        } else {
+          if (q < 2) { if (ha[q] < *pa) *pa = ha[q]; if (hs[q] < *ps) *ps = hs[q]; }
+          else       { if (ha[q] > *pa) *pa = ha[q]; if (hs[q] > *ps) *ps = hs[q]; }
+        }
+      }
+    }
   }
+  if (th && th->fwd_only) goto done;
 
   /* O7 endpoint seeds then backward in reverse order. */
   for (uint32_t p = 0; p < P; p++) {
@@ -812,6 +964,16 @@ static int run_update(const orc_design* d, double* at, double* slew, double* rat
             else         { if (cand > *pr) *pr = cand; }   /* early: max */
           }
         }
+      }
+    }
+    /* O15: at a -through pin the required times of the tag this one
+     * advances to (its paths continue as that tag); a final tag records
+     * its own for the earlier passes */
+    if (th && th->thr[u]) {
+      const uint32_t to = th->dst[u];
+      for (int q = 0; q < 4; q++) {
+        if (to != ORC_NO_PIN) rat[4 * u + q] = th->rhand[((size_t)to * th->P + u) * 4 + q];
+        else th->rhand[((size_t)th->cur * th->P + u) * 4 + q] = rat[4 * u + q];
       }
     }
   }

@@ -88,6 +88,13 @@ typedef struct {
   uint32_t n_clk;
   const float* clk_period;
   const uint32_t* pin_clk;
+  /* -through segments (row f4, O15): exception i's ordered
+   * through segments are the segment ids exc_thr_ptr[i] .. exc_thr_ptr[i+1];
+   * segment s holds the pins exc_seg[exc_seg_ptr[s] .. exc_seg_ptr[s+1]).
+   * exc_thr_ptr NULL: no exception has -through. */
+  const uint32_t* exc_thr_ptr;
+  const uint32_t* exc_seg_ptr;
+  const uint32_t* exc_seg;
 } orc_design;
 
 /* O6: NLDM bilinear lookup, fp64.  `tab` points at

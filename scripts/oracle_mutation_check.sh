@@ -68,12 +68,21 @@ mut 'return t50 - 0.5 * D;' 'return t50;'
 mut 'else if (lc >= 0) o[1] += (d->exc_value[lc] - 1.0) * Tcap;' 'else if (lc >= 0) o[1] += d->exc_value[lc] * Tcap;'
 mut '    if (seed_on && !seed_on[p]) continue;    /* O13: a startpoint of another tag */' ''
 mut '      if (slack) slack[i] = fmin(slack[i], t_sk[i]);' '      if (slack) slack[i] = fmax(slack[i], t_sk[i]);'
-mut '        if (has_from && !((tags[j] >> e) & 1u)) continue;' ''
+mut '        if (!full(&m, e, (uint32_t)tags[j])) continue;' ''
 mut 'else if (ec >= 0) o[3] += (d->exc_value[ec] - 1.0) * Tcap;' ''
-mut '    for (uint32_t k = 0; k < 2 * n_ep; k++) m_ws[k] = j == 0 ? t_ws[k] : fmin(m_ws[k], t_ws[k]);' '    for (uint32_t k = 0; k < 2 * n_ep; k++) m_ws[k] = t_ws[k];'
+mut '    for (uint32_t k = 0; k < 2 * n_ep; k++) m_ws[k] = jj == 0 ? t_ws[k] : fmin(m_ws[k], t_ws[k]);' '    for (uint32_t k = 0; k < 2 * n_ep; k++) m_ws[k] = t_ws[k];'
 # multiple clocks (O14)
 mut '    if (nxt - TC - a > h) h = nxt - TC - a;' '    if (nxt - a > h) h = nxt - a;'
 mut '    const double nxt = (floor(a / TC) + 1.0) * TC;' '    const double nxt = ceil(a / TC) * TC;'
 mut '          if (d->chk_d[c] == p) { cc = d->pin_clk[d->chk_ck[c]]; break; }' '          if (d->chk_d[c] == p) { cc = d->pin_clk[p]; break; }'
 mut '    const double Tc = d->n_clk ? (double)d->clk_period[d->pin_clk[p]] : d->period;' '    const double Tc = d->period;'
+# -through segments (O15)
+mut '          *pa = *ps = q < 2 ? INF : -INF;' ''
+mut '          if (q < 2) { if (ha[q] < *pa) *pa = ha[q]; if (hs[q] < *ps) *ps = hs[q]; }' ''
+mut 'if (to != ORC_NO_PIN) rat[4 * u + q] = th->rhand[((size_t)to * th->P + u) * 4 + q];' 'if (to != ORC_NO_PIN) {}'
+mut '    while (k < m->nseg[e] && seg_has(d, m, e, k, p)) {' '    if (k < m->nseg[e] && seg_has(d, m, e, k, p)) {'
+mut '      if (!start || !seg_has(d, m, e, 0, p)) continue;' '      if (!seg_has(d, m, e, 0, p)) continue;'
+mut '    const uint32_t j = any_thr ? T - 1 - jj : jj;' '    const uint32_t j = jj;'
+mut '  const uint32_t sg = d->exc_thr_ptr[e] + k - m->has_from[e];' '  const uint32_t sg = d->exc_thr_ptr[e] + k;'
+mut 'popc32((uint32_t)tags[j - 1]) > popc32((uint32_t)tags[j])' 'popc32((uint32_t)tags[j - 1]) < popc32((uint32_t)tags[j])'
 exit $fail

@@ -104,33 +104,50 @@ class Constraints:
 
 @dataclass
 class Exceptions:
-    """-from / -to timing exceptions (reduced): kind 0
-    false path, 1 multicycle (value N), 2 max delay, 3 min delay (value ps);
-    CSR lists of startpoint / endpoint pins (an empty list: any)."""
+    """Timing exceptions: kind 0 false path, 1
+    multicycle (value N), 2 max delay, 3 min delay (value ps); CSR lists of
+    startpoint / endpoint pins (an empty list: any) and ordered -through
+    segments: exception i's segments are thr_ptr[i] .. thr_ptr[i+1], segment
+    s the pins seg_pins[seg_ptr[s] .. seg_ptr[s+1])."""
     kind: np.ndarray       # uint8 [E]
     value: np.ndarray      # float32 [E]
     from_ptr: np.ndarray   # uint32 [E+1]
     from_pins: np.ndarray  # uint32
     to_ptr: np.ndarray     # uint32 [E+1]
     to_pins: np.ndarray    # uint32
+    thr_ptr: np.ndarray = None    # uint32 [E+1]
+    seg_ptr: np.ndarray = None    # uint32 [n_seg+1]
+    seg_pins: np.ndarray = None   # uint32
 
     @property
     def num(self) -> int:
         return int(self.kind.shape[0])
 
+    @property
+    def has_through(self) -> bool:
+        return self.thr_ptr is not None and int(self.thr_ptr[-1]) > 0
+
     @staticmethod
     def build(items) -> "Exceptions":
-        """items: sequence of (kind, value, from_pins, to_pins)."""
-        kind = np.array([k for k, _, _, _ in items], np.uint8)
-        value = np.array([v for _, v, _, _ in items], np.float32)
+        """items: sequence of (kind, value, from_pins, to_pins[, throughs]),
+        throughs a sequence of pin lists (the -through segments, in order)."""
+        items = [tuple(it) + ((),) * (5 - len(it)) for it in items]
+        kind = np.array([it[0] for it in items], np.uint8)
+        value = np.array([it[1] for it in items], np.float32)
         fp, tp, fr, to = [0], [0], [], []
-        for _, _, f, t in items:
+        thp, sgp, sg = [0], [0], []
+        for _, _, f, t, th in items:
             fr += list(f)
             to += list(t)
             fp.append(len(fr))
             tp.append(len(to))
+            for seg in th:
+                sg += list(seg)
+                sgp.append(len(sg))
+            thp.append(len(sgp) - 1)
         return Exceptions(kind, value, np.array(fp, np.uint32), np.array(fr, np.uint32),
-                          np.array(tp, np.uint32), np.array(to, np.uint32))
+                          np.array(tp, np.uint32), np.array(to, np.uint32),
+                          np.array(thp, np.uint32), np.array(sgp, np.uint32), np.array(sg, np.uint32))
 
 
 @dataclass

@@ -333,6 +333,32 @@ def select_paths(paths, k, nworst, slack_lt=INF):
     return kept
 
 
+def path_matches(ex, k, pins):
+    """a path (pin sequence, startpoint first) matches
+    exception k iff its startpoint is in the -from list (if any) and it
+    touches one pin of every -through segment in order -- positions
+    i_1 <= i_2 <= ... (one pin may serve consecutive segments, X8),
+    searched exhaustively."""
+    f0, f1 = int(ex.from_ptr[k]), int(ex.from_ptr[k + 1])
+    if f1 > f0 and pins[0] not in set(int(x) for x in ex.from_pins[f0:f1]):
+        return False
+    segs = []
+    if ex.thr_ptr is not None:
+        for sg in range(int(ex.thr_ptr[k]), int(ex.thr_ptr[k + 1])):
+            segs.append(set(int(x) for x in ex.seg_pins[int(ex.seg_ptr[sg]):int(ex.seg_ptr[sg + 1])]))
+
+    def rec(j, lo):
+        if j == len(segs):
+            return True
+        return any(pins[i] in segs[j] and rec(j + 1, i) for i in range(lo, len(pins)))
+    return rec(0, 0)
+
+
+def path_tag(ex, pins):
+    """bit k: the path matches exception k's -from / -through requirements"""
+    return sum(1 << k for k in range(ex.num) if path_matches(ex, k, pins))
+
+
 def exception_of(ex, tag, e, late):
     """The exception a path of startpoint tag `tag` (bitset over ex) meets at
     endpoint e, for the late (setup) or early (hold) check: DESIGN.md X2-X3
@@ -343,7 +369,8 @@ def exception_of(ex, tag, e, late):
     for k in range(ex.num):
         f0, f1 = int(ex.from_ptr[k]), int(ex.from_ptr[k + 1])
         t0, t1 = int(ex.to_ptr[k]), int(ex.to_ptr[k + 1])
-        if f1 > f0 and not (tag >> k) & 1:
+        has_thr = ex.thr_ptr is not None and int(ex.thr_ptr[k + 1]) > int(ex.thr_ptr[k])
+        if (f1 > f0 or has_thr) and not (tag >> k) & 1:
             continue
         if t1 > t0 and e not in set(int(x) for x in ex.to_pins[t0:t1]):
             continue
@@ -354,10 +381,10 @@ def exception_of(ex, tag, e, late):
 
 
 def path_slacks_with_exceptions(d, elm_of_pin):
-    """Frozen-delay brute force of the -from / -to exceptions (d.exceptions):
+    """Frozen-delay brute force of the timing exceptions (d.exceptions):
     every startpoint -> endpoint path is enumerated; a path's required time
-    is its endpoint's seed modified by the exception of (its startpoint's tag,
-    its endpoint); the setup / hold slack of a (pin, rf) is the minimum over
+    is its endpoint's seed modified by the exception of (the exceptions its
+    pin sequence matches, path_tag; its endpoint); the setup / hold slack of a (pin, rf) is the minimum over
     the complete paths through it, an endpoint's worst slack the minimum over
     the paths ending there (false paths excluded).  Returns slack [P][4] and
     res (WNS_s, TNS_s, WNS_h, TNS_h)."""
@@ -392,11 +419,6 @@ def path_slacks_with_exceptions(d, elm_of_pin):
             dl = {(i, o): max(0.0, const_value(lib, tab + o)) for (i, o) in _pairs(sense)}
         succ[u].append((v, dl))
         indeg[v] += 1
-    tag = np.zeros(P, np.int64)
-    if ex is not None:
-        for k in range(ex.num):
-            for p in ex.from_pins[int(ex.from_ptr[k]):int(ex.from_ptr[k + 1])]:
-                tag[int(p)] |= 1 << k
     seed_at = {}
     for k in range(cons.pi_pin.size):
         p = int(cons.pi_pin[k])
@@ -460,7 +482,7 @@ def path_slacks_with_exceptions(d, elm_of_pin):
     def walk(stack, v, rf, acc, s, s_rf):
         stack.append((v, rf))
         if v in po_l or v in ck_l:
-            tg = int(tag[s])
+            tg = path_tag(ex, [x for (x, _) in stack]) if ex is not None else 0
             rl = req(v, rf, tg, True, clk_of(s))
             if rl is not None and rl < INF:
                 sl = rl - (seed_at[s][2 + s_rf] + acc)
