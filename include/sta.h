@@ -218,25 +218,35 @@ STA_API sta_status sta_build_steiner(sta_ctx ctx, sta_mem mem, const float* pin_
 typedef enum { STA_NET_ELMORE = 0, STA_NET_ARNOLDI = 1 } sta_net_model;
 STA_API sta_status sta_set_net_model(sta_ctx ctx, sta_net_model model, uint32_t q);
 
-/* -from / -to timing exceptions (reduced: no
- * -through, no case analysis, one clock; "false
+/* Timing exceptions ("false
  * paths, multi-cycle paths, case analysis, and cross clock region paths ...
- * complicate the data structures and states in timing propagation"; the tag
- * model of SPEC.md:465-509).  Exception i: kind[i] (STA_EXC_*), value[i]
- * (multicycle: N >= 1; max / min delay: ps), startpoint pins
- * from_pins[from_ptr[i] .. from_ptr[i+1]) and endpoint pins
- * to_pins[to_ptr[i] .. to_ptr[i+1]) (an empty list: any).  A path's tag is
- * the set of exceptions whose -from list holds its startpoint; every tag is
- * propagated on its own (one forward / backward pass per tag, RC shared),
- * and per endpoint and tag the exception is resolved: setup (late): false
- * path > max delay (RAT_L = value) > multicycle (capture at N T); hold
+ * complicate the data structures and states in timing propagation"; PAPER.md:
+ * 250: "-through patterns that eliminate only paths that go through a
+ * predefined pin sequence"; the tag model of SPEC.md:465-509; no case
+ * analysis).  Exception i: kind[i] (STA_EXC_*), value[i] (multicycle:
+ * N >= 1; max / min delay: ps), startpoint pins from_pins[from_ptr[i] ..
+ * from_ptr[i+1]), endpoint pins to_pins[to_ptr[i] .. to_ptr[i+1]) (an empty
+ * list: any) and, if thr_ptr is not NULL, the ordered -through segments
+ * thr_ptr[i] .. thr_ptr[i+1], segment g holding the pins
+ * seg_pins[seg_ptr[g] .. seg_ptr[g+1]) (non-empty).  A path matches
+ * exception i when its startpoint is in the -from list and it passes a pin
+ * of every -through segment in order (X8: one pin may match
+ * consecutive segments).  A path's tag is its launch clock and the matched
+ * prefix of every exception's segments (one bit per segment); tags advance
+ * at -through pins; every tag is propagated as its own pass (RC shared; with
+ * -through a forward sweep hands the arrivals of advancing tags on, then
+ * full passes in reverse order take the required times back), and per
+ * endpoint and tag the fully matched exceptions are resolved: setup (late):
+ * false path > max delay (RAT_L = value) > multicycle (capture at N T); hold
  * (early): false path > min delay (RAT_E = value) > multicycle (hold edge
  * (N-1) T); the first listed of a kind wins.  Reports merge the tags: per
  * pin the early / late extreme of AT, slew, RAT and the minimum slack; per
  * endpoint the worst slack over tags (false paths contribute none) for
- * WNS / TNS.  num = 0 clears.  At most 32 exceptions and 16 startpoint tags.
- * The top-k path report needs no exceptions (STA_ERR_ORDER).  Arrays in
- * `mem`, copied.  Errors: STA_ERR_ORDER (no graph), STA_ERR_ARG, STA_ERR_ID. */
+ * WNS / TNS.  num = 0 clears.  At most 32 exceptions, 32 segments (-from
+ * lists and -through segments) and 32 tags.  The top-k path report needs no
+ * exceptions (STA_ERR_ORDER).  Arrays in `mem`, copied.  Errors:
+ * STA_ERR_ORDER (no graph), STA_ERR_ARG (kinds, values, limits), STA_ERR_CSR
+ * (offsets, empty segment), STA_ERR_ID (pin out of range). */
 typedef enum { STA_EXC_FALSE_PATH = 0, STA_EXC_MULTICYCLE = 1, STA_EXC_MAX_DELAY = 2,
                STA_EXC_MIN_DELAY = 3 } sta_exception_kind;
 typedef struct {
@@ -248,6 +258,9 @@ typedef struct {
   const uint32_t* from_pins;
   const uint32_t* to_ptr;
   const uint32_t* to_pins;
+  const uint32_t* thr_ptr;    /* [num + 1] or NULL: no -through */
+  const uint32_t* seg_ptr;    /* [thr_ptr[num] + 1] */
+  const uint32_t* seg_pins;
 } sta_exceptions;
 STA_API sta_status sta_set_exceptions(sta_ctx ctx, const sta_exceptions* ex);
 

@@ -241,9 +241,12 @@ struct sta_ctx_s {
   std::vector<uint8_t> exc_kind;
   std::vector<float> exc_value;
   std::vector<u32> exc_from_ptr, exc_from, exc_to_ptr, exc_to;
+  std::vector<u32> exc_thr_ptr, exc_seg_ptr, exc_seg;   // -through segments (empty: none)
   Arena exc_arena;
   std::vector<const u32*> exc_seed_d;
   std::vector<const uint4*> exc_ovr_d;
+  std::vector<const u32*> exc_thr_dst_d;         // per pass: thr_dst (with -through)
+  u32 n_thr = 0;                                 // through slots (pins of -through segments)
   int net_model = 0;                             // row f1: 0 Elmore, 1 Arnoldi (order arn_q)
   u32 arn_q = 4;
   Arena arn_arena;                               // Arnoldi layout (prepare)
@@ -1312,13 +1315,74 @@ void prepare(sta_ctx c) {
       if (seed[i] == sta::kSeedClock) seed[i] = base + c->pin_clk[c->user_of_int[i]];
     c->topo.seed = t.seed = g.upload(seed, s);
   }
+  c->exc_thr_dst_d.clear();
+  c->n_thr = 0;
+  t.thr_pull = t.thr_sink = t.thr_dst = nullptr;
+  t.thr_sk = nullptr;
+  t.n_thr = t.n_thr_sk = t.thr_cur = 0;
   if (!c->exc_kind.empty() || n_clk) {
     const u32 E = (u32)c->exc_kind.size();
-    // a startpoint's tag: its launch clock (bits 32+) and the exceptions whose
-    // -from holds it (bits 0..31)
+    // segment bits (the oracle's O15): exception e has the
+    // ordered segments [from (if listed), through_1 .. through_m], one tag
+    // bit each from base[e]; a path's bits of e are a prefix of them
+    const bool has_thr = !c->exc_thr_ptr.empty() && c->exc_thr_ptr[E] > 0;
+    std::vector<u32> base(E), nseg(E), has_from(E);
+    u32 total = 0;
+    for (u32 e = 0; e < E; ++e) {
+      has_from[e] = c->exc_from_ptr[e + 1] > c->exc_from_ptr[e];
+      nseg[e] = has_from[e] + (has_thr ? c->exc_thr_ptr[e + 1] - c->exc_thr_ptr[e] : 0);
+      base[e] = total;
+      total += nseg[e];
+    }
+    if (total > 32) fail(STA_ERR_ARG, "%u exception segments (-from and -through lists, at most 32)", total);
+    // membership of pin p in segment k of exception e (sorted pin lists)
+    std::vector<std::vector<u32>> segl(total);
+    for (u32 e = 0; e < E; ++e)
+      for (u32 k = 0; k < nseg[e]; ++k) {
+        std::vector<u32>& L = segl[base[e] + k];
+        if (has_from[e] && k == 0) {
+          L.assign(c->exc_from.begin() + c->exc_from_ptr[e], c->exc_from.begin() + c->exc_from_ptr[e + 1]);
+        } else {
+          const u32 sg = c->exc_thr_ptr[e] + k - has_from[e];
+          L.assign(c->exc_seg.begin() + c->exc_seg_ptr[sg], c->exc_seg.begin() + c->exc_seg_ptr[sg + 1]);
+        }
+        std::sort(L.begin(), L.end());
+      }
+    auto seg_has = [&](u32 e, u32 k, u32 p) {
+      const std::vector<u32>& L = segl[base[e] + k];
+      return std::binary_search(L.begin(), L.end(), p);
+    };
+    // one step of the tag automaton at pin p (start: p is the path's startpoint)
+    auto adv = [&](u32 bits, u32 p, bool start) {
+      for (u32 e = 0; e < E; ++e) {
+        u32 k = 0;
+        while (k < nseg[e] && ((bits >> (base[e] + k)) & 1u)) ++k;
+        if (has_from[e] && k == 0) {
+          if (!start || !seg_has(e, 0, p)) continue;
+          bits |= 1u << base[e];
+          k = 1;
+        }
+        while (k < nseg[e] && seg_has(e, k, p)) {
+          bits |= 1u << (base[e] + k);
+          ++k;
+        }
+      }
+      return bits;
+    };
+    auto full = [&](u32 e, uint64_t tg) {
+      const u32 mask = nseg[e] >= 32 ? 0xFFFFFFFFu : ((1u << nseg[e]) - 1u);
+      return (((u32)tg >> base[e]) & mask) == mask;
+    };
+    // a startpoint's tag: its launch clock (bits 32+) and its segment bits
     std::vector<uint64_t> tagp(P, 0);
     for (u32 e = 0; e < E; ++e)
-      for (u32 x = c->exc_from_ptr[e]; x < c->exc_from_ptr[e + 1]; ++x) tagp[c->exc_from[x]] |= 1ull << e;
+      if (has_from[e])
+        for (u32 x = c->exc_from_ptr[e]; x < c->exc_from_ptr[e + 1]; ++x) {
+          const u32 p = c->exc_from[x];
+          tagp[p] = adv((u32)tagp[p], p, true);
+        }
+    if (has_thr)   // a startpoint may also begin a -through segment (from-less exceptions)
+      for (u32 v : c->exc_seg) tagp[v] = adv((u32)tagp[v], v, true);
     if (n_clk)
       for (u32 p = 0; p < P; ++p) tagp[p] |= (uint64_t)c->pin_clk[p] << 32;
     // (setup, hold) relationship of a launch / capture period pair: the
@@ -1339,7 +1403,46 @@ void prepare(sta_ctx c) {
       if (std::find(tags.begin(), tags.end(), tagp[p]) == tags.end()) tags.push_back(tagp[p]);
     }
     if (tags.empty()) tags.push_back(0);
-    if (tags.size() > 16) fail(STA_ERR_ARG, "%zu startpoint tags (at most 16)", tags.size());
+    // -through: the tags reached by advancing at the segments' pins (closure),
+    // ordered by set segment bits (a tag only advances to tags after it)
+    std::vector<u32> slot_of(has_thr ? P : 0, kNone), thr_pins;
+    if (has_thr) {
+      for (u32 v : c->exc_seg)
+        if (slot_of[v] == kNone) { slot_of[v] = (u32)thr_pins.size(); thr_pins.push_back(v); }
+      for (size_t i = 0; i < tags.size() && tags.size() <= 32; ++i)
+        for (u32 v : thr_pins) {
+          const uint64_t t2 = (tags[i] & ~0xFFFFFFFFull) | adv((u32)tags[i], v, false);
+          if (std::find(tags.begin(), tags.end(), t2) == tags.end()) tags.push_back(t2);
+        }
+      std::stable_sort(tags.begin(), tags.end(), [](uint64_t a, uint64_t b) {
+        return __builtin_popcount((u32)a) < __builtin_popcount((u32)b);
+      });
+    }
+    if (tags.size() > 32) fail(STA_ERR_ARG, "%zu timing tags (at most 32)", tags.size());
+    if (has_thr) {
+      const u32 n_thr = (u32)thr_pins.size();
+      std::vector<u32> tp(c->NP, kNone), ts(c->NS, kNone);
+      std::vector<uint2> sk;
+      for (u32 x = 0; x < n_thr; ++x) {
+        const u32 i = c->int_of_user[thr_pins[x]];
+        if (i < c->NP) tp[i] = x;
+        else { ts[i - c->NP] = x; sk.push_back(make_uint2(i - c->NP, x)); }
+      }
+      c->n_thr = n_thr;
+      t.n_thr = n_thr;
+      t.n_thr_sk = (u32)sk.size();
+      t.thr_pull = c->exc_arena.upload(tp, s);
+      t.thr_sink = c->exc_arena.upload(ts, s);
+      t.thr_sk = sk.empty() ? nullptr : c->exc_arena.upload(sk, s);
+      for (uint64_t tg : tags) {
+        std::vector<u32> dst(n_thr, kNone);
+        for (u32 x = 0; x < n_thr; ++x) {
+          const uint64_t t2 = (tg & ~0xFFFFFFFFull) | adv((u32)tg, thr_pins[x], false);
+          if (t2 != tg) dst[x] = (u32)(std::find(tags.begin(), tags.end(), t2) - tags.begin());
+        }
+        c->exc_thr_dst_d.push_back(c->exc_arena.upload(dst, s));
+      }
+    }
     std::vector<std::vector<uint8_t>> in_to(E);
     for (u32 e = 0; e < E; ++e) {
       in_to[e].assign(P, 0);
@@ -1370,7 +1473,7 @@ void prepare(sta_ctx c) {
         }
         int lf = -1, lm = -1, lc = -1, ef = -1, em = -1, ec = -1;
         for (u32 e = 0; e < E; ++e) {
-          if (c->exc_from_ptr[e + 1] > c->exc_from_ptr[e] && !((tg >> e) & 1u)) continue;
+          if (!full(e, tg)) continue;        // the tag has not matched all of e's segments
           if (c->exc_to_ptr[e + 1] > c->exc_to_ptr[e] && !in_to[e][p]) continue;
           switch (c->exc_kind[e]) {
             case STA_EXC_FALSE_PATH: if (lf < 0) lf = (int)e; if (ef < 0) ef = (int)e; break;
@@ -1499,6 +1602,13 @@ void prepare(sta_ctx c) {
       d.m_pin = a.alloc<float4>(4 * (size_t)std::max<u32>(c->Pi, 1));
       d.m_ep_ws = a.alloc<float2>(std::max<u32>(c->n_ep, 1));
     }
+    d.thr_hat = d.thr_hsl = d.thr_hrat = nullptr;
+    if (c->n_thr) {                          // -through handoff, [tags][slots]
+      const size_t n = c->exc_thr_dst_d.size() * (size_t)c->n_thr;
+      d.thr_hat = a.alloc<float4>(n);
+      d.thr_hsl = a.alloc<float4>(n);
+      d.thr_hrat = a.alloc<float4>(n);
+    }
     d.arn_lam = nullptr;
     d.arn_res = nullptr;
     d.arn_scr = nullptr;
@@ -1515,14 +1625,12 @@ void prepare(sta_ctx c) {
   c->prepared = true;
 }
 
-// Kernel sequence of one update of one batch of corners (see sta_kernels.cu).
-u32 enqueue_batch(sta_ctx c, const sta::Batch& b, const sta::Topo& t, bool rc) {
+// RC of one batch (tier C on the side stream beside the small nets), then the
+// nets' reduced-order models under the Arnoldi model
+u32 enqueue_rc(sta_ctx c, const sta::Batch& b, const sta::Topo& t) {
   cudaStream_t s = c->stream;
   u32 launches = 0;
-  prof_mark(c, 0);
-  if (!rc) {
-    // a later exception tag of the same update (row f4): the RC results are shared
-  } else if (t.nC && std::getenv("STA_RC_SERIAL")) {
+  if (t.nC && std::getenv("STA_RC_SERIAL")) {
     ck(sta::launch_rc_tierC(t, b, s), "rc tier-C kernels");
   } else if (t.nC) {                         // tier C concurrently with the small nets
     ck(cudaEventRecord(c->fork_ev, s), "fork");
@@ -1530,17 +1638,27 @@ u32 enqueue_batch(sta_ctx c, const sta::Batch& b, const sta::Topo& t, bool rc) {
     ck(sta::launch_rc_tierC(t, b, c->side), "rc tier-C kernels");
     ck(cudaEventRecord(c->join_ev, c->side), "join");
   }
-  if (rc) {
-    ck(sta::launch_rc(t, b, c->wgrid, s), "rc kernel");
-    if (t.nC && !std::getenv("STA_RC_SERIAL")) ck(cudaStreamWaitEvent(s, c->join_ev, 0), "join wait");
-    launches += (t.n_wtiles ? 1 : 0) + (t.n_btiles ? 1 : 0) + (t.n_lumped ? 1 : 0) + (t.nC ? 2 : 0);
-  }
-  if (rc && t.net_model == 1) {              // row f1: the nets' reduced-order models
+  ck(sta::launch_rc(t, b, c->wgrid, s), "rc kernel");
+  if (t.nC && !std::getenv("STA_RC_SERIAL")) ck(cudaStreamWaitEvent(s, c->join_ev, 0), "join wait");
+  launches += (t.n_wtiles ? 1 : 0) + (t.n_btiles ? 1 : 0) + (t.n_lumped ? 1 : 0) + (t.nC ? 2 : 0);
+  if (t.net_model == 1) {                    // row f1: the nets' reduced-order models
     ck(sta::launch_arn_reduce(t, b, s), "arnoldi kernel");
     launches += t.n_arn_nets ? 1 : 0;
   }
+  return launches;
+}
+
+// Kernel sequence of one update of one batch of corners (see sta_kernels.cu);
+// rc = false: a later exception tag of the same update (row f4), the RC
+// results are shared
+u32 enqueue_batch(sta_ctx c, const sta::Batch& b, const sta::Topo& t, bool rc) {
+  cudaStream_t s = c->stream;
+  u32 launches = 0;
+  prof_mark(c, 0);
+  if (rc) launches += enqueue_rc(c, b, t);
   prof_mark(c, 1);
-  if (c->use_persistent && c->pgrid && c->pgrid_b) {
+  // (the Arnoldi and -through instantiations exist only as persistent kernels)
+  if ((c->use_persistent && c->pgrid && c->pgrid_b) || t.net_model == 1 || t.thr_pull) {
     prof_mark(c, 2);
     ck(sta::launch_fwd_persistent(t, b, c->pgrid, s), "forward persistent kernel");
     prof_mark(c, 3);
@@ -1574,21 +1692,56 @@ u32 enqueue_batch(sta_ctx c, const sta::Batch& b, const sta::Topo& t, bool rc) {
 }
 
 // One update of every batch; with exceptions (row f4) one forward / backward
-// pass per startpoint tag (RC in the first only), each folded into the merged
-// arrays, then WNS / TNS from the merged per-endpoint worst slacks.
+// pass per tag (RC in the first only), each folded into the merged arrays,
+// then WNS / TNS from the merged per-endpoint worst slacks.  With -through
+// segments (the oracle's O15): a forward sweep in tag order hands the
+// arrivals of advancing tags on (forward only, the record epoch advanced
+// after each), then the full passes run in reverse tag order, so that every
+// pass finds the arrivals handed to it and the required times it takes over.
 u32 enqueue_all(sta_ctx c, const std::vector<sta::Batch>& batches) {
   u32 launches = 0;
   if (c->exc_seed_d.empty()) {
     for (const sta::Batch& b : batches) launches += enqueue_batch(c, b, c->topo, true);
     return launches;
   }
-  for (size_t j = 0; j < c->exc_seed_d.size(); ++j) {
+  const size_t T = c->exc_seed_d.size();
+  const bool thr = c->n_thr != 0;
+  auto pass_topo = [&](size_t j) {
     sta::Topo tj = c->topo;
     tj.seed = c->exc_seed_d[j];
     tj.ep_ovr = c->exc_ovr_d[j];
+    if (thr) {
+      tj.thr_dst = c->exc_thr_dst_d[j];
+      tj.thr_cur = (u32)j;
+    }
+    return tj;
+  };
+  bool rc_done = false;
+  if (thr) {
     for (const sta::Batch& b : batches) {
-      launches += enqueue_batch(c, b, tj, j == 0);
-      for (u32 k = 0; k < b.K; ++k) ck(sta::launch_merge_tag(tj, b.c[k], j == 0 ? 1 : 0, c->stream), "merge kernel");
+      ck(sta::launch_thr_reset(c->topo, b, (u32)T, c->stream), "through reset kernel");
+      launches += 1;
+    }
+    for (size_t j = 0; j < T; ++j) {
+      const sta::Topo tj = pass_topo(j);
+      for (const sta::Batch& b : batches) {
+        if (j == 0) {
+          launches += enqueue_rc(c, b, tj);
+        }
+        ck(sta::launch_fwd_persistent(tj, b, c->pgrid, c->stream), "forward persistent kernel");
+        ck(sta::launch_thr_capture(tj, b, c->stream), "through capture kernel");
+        ck(sta::launch_bump_epoch(b, c->stream), "epoch kernel");
+        launches += 2 + (tj.n_thr_sk ? 1 : 0);
+      }
+    }
+    rc_done = true;
+  }
+  for (size_t jj = 0; jj < T; ++jj) {
+    const size_t j = thr ? T - 1 - jj : jj;
+    const sta::Topo tj = pass_topo(j);
+    for (const sta::Batch& b : batches) {
+      launches += enqueue_batch(c, b, tj, !rc_done && jj == 0);
+      for (u32 k = 0; k < b.K; ++k) ck(sta::launch_merge_tag(tj, b.c[k], jj == 0 ? 1 : 0, c->stream), "merge kernel");
       launches += b.K;
     }
   }
@@ -2022,7 +2175,7 @@ sta_status sta_set_exceptions(sta_ctx c, const sta_exceptions* ex) {
     if (E > 32) fail(STA_ERR_ARG, "%u exceptions (at most 32)", E);
     std::vector<uint8_t> kind;
     std::vector<float> value;
-    std::vector<u32> fp, fr, tp, to;
+    std::vector<u32> fp, fr, tp, to, th, sp, sg;
     if (E) {
       kind = fetch(ex->kind, E, ex->mem, "kind", c->stream);
       value = fetch(ex->value, E, ex->mem, "value", c->stream);
@@ -2035,6 +2188,22 @@ sta_status sta_set_exceptions(sta_ctx c, const sta_exceptions* ex) {
       to = fetch(ex->to_pins, tp[E], ex->mem, "to_pins", c->stream);
       for (u32 p : fr) if (p >= c->P) fail(STA_ERR_ID, "exception -from pin %u out of range", p);
       for (u32 p : to) if (p >= c->P) fail(STA_ERR_ID, "exception -to pin %u out of range", p);
+      if (ex->thr_ptr) {                     // ordered -through segments
+        th = fetch(ex->thr_ptr, E + 1, ex->mem, "thr_ptr", c->stream);
+        if (th[0] != 0) fail(STA_ERR_CSR, "thr_ptr must start at 0");
+        for (u32 e = 0; e < E; ++e)
+          if (th[e + 1] < th[e]) fail(STA_ERR_CSR, "exception %u: -through offsets not monotone", e);
+        if (th[E]) {
+          sp = fetch(ex->seg_ptr, th[E] + 1, ex->mem, "seg_ptr", c->stream);
+          if (sp[0] != 0) fail(STA_ERR_CSR, "seg_ptr must start at 0");
+          for (u32 g = 0; g < th[E]; ++g)
+            if (sp[g + 1] <= sp[g]) fail(STA_ERR_CSR, "-through segment %u: empty or offsets not monotone", g);
+          sg = fetch(ex->seg_pins, sp[th[E]], ex->mem, "seg_pins", c->stream);
+          for (u32 p : sg) if (p >= c->P) fail(STA_ERR_ID, "exception -through pin %u out of range", p);
+        } else {
+          th.clear();
+        }
+      }
       for (u32 e = 0; e < E; ++e) {
         if (kind[e] > STA_EXC_MIN_DELAY) fail(STA_ERR_ARG, "exception %u: kind %u", e, kind[e]);
         if (!std::isfinite(value[e])) fail(STA_ERR_ARG, "exception %u: non-finite value", e);
@@ -2049,6 +2218,9 @@ sta_status sta_set_exceptions(sta_ctx c, const sta_exceptions* ex) {
     c->exc_from = std::move(fr);
     c->exc_to_ptr = std::move(tp);
     c->exc_to = std::move(to);
+    c->exc_thr_ptr = std::move(th);
+    c->exc_seg_ptr = std::move(sp);
+    c->exc_seg = std::move(sg);
     c->prepared = false;                     // tags, seeds, overrides and merged arrays next update
     invalidate_graph(c);
   });

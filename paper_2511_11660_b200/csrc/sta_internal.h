@@ -199,6 +199,20 @@ struct Topo {
   uint32_t n_arn_big;
   const uint32_t* arn_big;    // indices (into arn_nets) of the nets of more than 1024 RC nodes
   uint64_t n_rc_nodes;
+  // row f4: -through exception segments (the oracle's O15; X8).
+  // The pins of any -through segment are "through slots" 0 .. n_thr-1;
+  // thr_pull [NP] / thr_sink [NS]: slot of a pull pin / sink or kNone
+  // (nullptr: no -through, the kernels' non-THR instantiations run).  This
+  // pass (tag thr_cur): thr_dst [n_thr] = the pass its tag advances to at the
+  // slot's pin (its arrivals there are handed over, its required times taken
+  // from that pass) or kNone (final there: it takes in the arrivals handed
+  // to it and records its required times).  thr_sk [n_thr_sk]: {sink, slot}
+  // of the sink slots (the handoff of sink arrivals, thr_capture_kernel).
+  const uint32_t* thr_pull;
+  const uint32_t* thr_sink;
+  const uint32_t* thr_dst;
+  const uint2* thr_sk;
+  uint32_t n_thr, n_thr_sk, thr_cur;
 };
 
 // Per-corner device state.
@@ -233,6 +247,12 @@ struct CornerDev {
   float4* arn_res;    // [NS] residues of each sink
   double* arn_scr;    // [(arn_q + 4) n_rc] Lanczos scratch
   unsigned long long* trace;  // optional (STA_TRACE): per warp unit {start, ready, end} ns
+  // row f4 -through handoff (Topo::thr_*), [tags][n_thr] each: arrivals / slews
+  // handed to a pass at its final through pins (merged, early min / late
+  // max), required times each pass computes at its final through pins
+  float4* thr_hat;
+  float4* thr_hsl;
+  float4* thr_hrat;
 };
 
 // The corners one launch traverses.  Persistent kernels bind warp w to corner
@@ -328,8 +348,15 @@ cudaError_t levelize_device(uint32_t P, uint32_t N, uint32_t A, const uint32_t* 
                             uint32_t* fi_ptr, uint32_t* fi_ids, uint32_t* fo_ptr, uint32_t* fo_ids,
                             uint32_t* num_levels, uint32_t* cycle_pin, cudaStream_t s);
 
-// ---- NEXT row f4 (reduced): merge one tag's results into the merged arrays
+// ---- NEXT row f4: merge one tag's results into the merged arrays
 cudaError_t launch_merge_tag(const Topo& t, const CornerDev& c, int first, cudaStream_t s);
+// -through handoff: reset every pass's handed arrivals (start of an update),
+// hand this pass's sink arrivals at its advancing through sinks to their
+// passes (after its forward), advance the record epoch (after a forward-only
+// pass: the next forward must not see this pass's records as current)
+cudaError_t launch_thr_reset(const Topo& t, const Batch& b, uint32_t n_tags, cudaStream_t s);
+cudaError_t launch_thr_capture(const Topo& t, const Batch& b, cudaStream_t s);
+cudaError_t launch_bump_epoch(const Batch& b, cudaStream_t s);
 
 // ---- NEXT row f1: Arnoldi reduced-order models of every net (sta_arnoldi.cu)
 cudaError_t launch_arn_reduce(const Topo& t, const Batch& b, cudaStream_t s);

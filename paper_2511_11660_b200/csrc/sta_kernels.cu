@@ -970,6 +970,60 @@ __device__ __forceinline__ void arn_net_hop(Q4& at, Q4& sl, float elm, const flo
   }
 }
 
+// ---- row f4: -through hooks (the oracle's O15; Topo::thr_*).  At a
+// through pin whose tag advances (thr_dst != kNone) this pass's arrivals are
+// handed to the advanced tag's pass and are undefined here, and its required
+// times are that pass's; where the tag is final the handed arrivals merge
+// into its own and its required times are recorded for the earlier passes.
+// Fan-in-free pins (seeds) take no forward hook, as in the oracle.
+__device__ __forceinline__ float* thr_word(float4* base, const Topo& t, uint32_t pass, uint32_t sl, int q) {
+  return reinterpret_cast<float*>(base + (size_t)pass * t.n_thr + sl) + q;
+}
+// component q of a pull pin's merged (arrival, slew), before it is stored
+__device__ __forceinline__ void thr_pull_q(const Topo& t, const CornerDev& c, uint32_t v, int q, float& a, float& s) {
+  const uint32_t sl = __ldg(t.thr_pull + v);
+  if (sl == kNone) return;
+  const bool early = q < 2;
+  const uint32_t d = __ldg(t.thr_dst + sl);
+  if (d != kNone) {                          // hand over (one writer per word in this pass)
+    float* ha = thr_word(c.thr_hat, t, d, sl, q);
+    float* hs = thr_word(c.thr_hsl, t, d, sl, q);
+    *ha = early ? fminf(*ha, a) : fmaxf(*ha, a);
+    *hs = early ? fminf(*hs, s) : fmaxf(*hs, s);
+    a = s = early ? CUDART_INF_F : -CUDART_INF_F;
+  } else {
+    const float ha = *thr_word(c.thr_hat, t, t.thr_cur, sl, q), hs = *thr_word(c.thr_hsl, t, t.thr_cur, sl, q);
+    a = early ? fminf(a, ha) : fmaxf(a, ha);
+    s = early ? fminf(s, hs) : fmaxf(s, hs);
+  }
+}
+// component q of a sink's arrival / slew (after its net hop); the handoff of
+// an advancing sink's arrivals is thr_capture_kernel's
+__device__ __forceinline__ void thr_sink_q(const Topo& t, const CornerDev& c, uint32_t k, int q, float& a, float& s) {
+  const uint32_t sl = __ldg(t.thr_sink + k);
+  if (sl == kNone) return;
+  const bool early = q < 2;
+  const uint32_t d = __ldg(t.thr_dst + sl);
+  if (d != kNone) {
+    a = s = early ? CUDART_INF_F : -CUDART_INF_F;
+  } else {
+    const float ha = *thr_word(c.thr_hat, t, t.thr_cur, sl, q), hs = *thr_word(c.thr_hsl, t, t.thr_cur, sl, q);
+    a = early ? fminf(a, ha) : fmaxf(a, ha);
+    s = early ? fminf(s, hs) : fmaxf(s, hs);
+  }
+}
+__device__ __forceinline__ void thr_sink4(const Topo& t, const CornerDev& c, uint32_t k, Q4& a, Q4& s) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) thr_sink_q(t, c, k, q, a.v[q], s.v[q]);
+}
+// required times of a through slot sl (kNone: not a through pin)
+__device__ __forceinline__ void thr_rat(const Topo& t, const CornerDev& c, uint32_t sl, Q4& r) {
+  if (sl == kNone) return;
+  const uint32_t d = __ldg(t.thr_dst + sl);
+  if (d != kNone) r = to_q(c.thr_hrat[(size_t)d * t.n_thr + sl]);
+  else c.thr_hrat[(size_t)t.thr_cur * t.n_thr + sl] = to_f4(r);
+}
+
 // forward unit u; tr = this lane's term slot of the unit, rc its RC results
 // (loaded by the caller, software-pipelined one unit ahead)
 // the record word a term lane reads: (el, irf) of its source
@@ -981,7 +1035,7 @@ __device__ __forceinline__ const uint4* fwd_word(const CornerDev& c, const uint4
 
 // pre: this lane's record word loaded speculatively one unit early (valid
 // if its tags match the epoch, else it is polled again)
-template <bool TRACE, bool ARN>
+template <bool TRACE, bool ARN, bool THR>
 __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, const float* __restrict__ L,
                                          uint32_t ep, uint32_t u, const uint4& tr, FwdRc<ARN> rc,
                                          uint4 pre = make_uint4(0, 0, 0, 0)) {
@@ -1030,6 +1084,7 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
       if (tr.y != kNone) {
         if constexpr (ARN) arn_hop_q(a_in, s_in, elm, rc.lam, rc.res);
         else hop_q(a_in, s_in, elm);
+        if constexpr (THR) thr_sink_q(t, c, tr.y, el * 2 + irf, a_in, s_in);
       }
       float dl;
       fwd_lane(f, el, a_in, s_in, ca, cs, dl);
@@ -1057,6 +1112,7 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
       }
     }
     if (item && tl == head_tl) {
+      if constexpr (THR) thr_pull_q(t, c, v, (int)q, ca, cs);
       st_ll(c.rec + 4 * (size_t)v + q, ca, cs, ep);
       reinterpret_cast<float*>(c.at4 + v)[q] = ca;
     }
@@ -1076,6 +1132,7 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
         if constexpr (ARN)
           arn_hop_q(a_in, s_in, __ldcg(c.elm + h), __ldcg(c.arn_lam + t.fi_src[e]), __ldcg(c.arn_res + h));
         else hop_q(a_in, s_in, __ldcg(c.elm + h));
+        if constexpr (THR) thr_sink_q(t, c, h, el * 2 + irf, a_in, s_in);
       }
       float oa, os, dl;
       fwd_lane(f, el, a_in, s_in, oa, os, dl);
@@ -1089,6 +1146,7 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
       merge_q(cs, __shfl_xor_sync(kFull, cs, o), el);
     }
     if (tl == 0) {
+      if constexpr (THR) thr_pull_q(t, c, v, (int)q, ca, cs);
       st_ll(c.rec + 4 * (size_t)v + q, ca, cs, ep);
       reinterpret_cast<float*>(c.at4 + v)[q] = ca;
     }
@@ -1103,7 +1161,7 @@ __device__ __forceinline__ void fwd_unit(const Topo& t, const CornerDev& c, cons
   trace_unit<TRACE>(c, u, t_start, t_ready, t_data);
 }
 
-template <bool SMEM_LUT, bool TRACE, bool ARN, int NT>
+template <bool SMEM_LUT, bool TRACE, bool ARN, bool THR, int NT>
 __device__ __forceinline__ void fwd_persistent_body(const Topo& t, const Batch& B) {
   stage_luts<SMEM_LUT>(B, kNone);
   // warp gw serves corner gw % K and walks its unit list with stride Wc
@@ -1134,10 +1192,10 @@ __device__ __forceinline__ void fwd_persistent_body(const Topo& t, const Batch& 
     const FwdRc<ARN> nrc = fwd_rc<ARN>(c, nx);         // nx arrived during the previous unit
 #if STA_FWD_RECPF
     const uint4 nrec = nx.x < kHeavyMark ? ld_ll(fwd_word(c, nx)) : make_uint4(0, 0, 0, 0);
-    fwd_unit<TRACE, ARN>(t, c, L, ep, u, tr, rc, rec);
+    fwd_unit<TRACE, ARN, THR>(t, c, L, ep, u, tr, rc, rec);
     rec = nrec;
 #else
-    fwd_unit<TRACE, ARN>(t, c, L, ep, u, tr, rc);
+    fwd_unit<TRACE, ARN, THR>(t, c, L, ep, u, tr, rc);
 #endif
     tr = nx;
     nx = nnx;
@@ -1150,7 +1208,7 @@ __device__ __forceinline__ void fwd_persistent_body(const Topo& t, const Batch& 
   for (; u < t.n_fwu; u += Wc) {
     const uint4 tr = nx;
     if (u + Wc < t.n_fwu) nx = __ldg(t.fterm + (size_t)kFwdTerms * (u + Wc) + tl);   // prefetch the next unit
-    fwd_unit<TRACE, ARN>(t, c, L, ep, u, tr, fwd_rc<ARN>(c, tr));
+    fwd_unit<TRACE, ARN, THR>(t, c, L, ep, u, tr, fwd_rc<ARN>(c, tr));
   }
 #endif
 }
@@ -1158,15 +1216,17 @@ __device__ __forceinline__ void fwd_persistent_body(const Topo& t, const Batch& 
 template <bool SMEM_LUT, bool TRACE>
 __global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) fwd_persistent_kernel(Topo t,
                                                                                    const __grid_constant__ Batch B) {
-  fwd_persistent_body<SMEM_LUT, TRACE, false, kFwdThreads>(t, B);
+  fwd_persistent_body<SMEM_LUT, TRACE, false, false, kFwdThreads>(t, B);
 }
 
 // the Arnoldi-model instantiation (row f1): its hop solver needs registers,
 // so fewer warps per block
 constexpr int kFwdArnThreads = 512;
-template <bool SMEM_LUT>
-__global__ void __launch_bounds__(kFwdArnThreads, 1) fwd_persistent_arn_kernel(Topo t, const __grid_constant__ Batch B) {
-  fwd_persistent_body<SMEM_LUT, false, true, kFwdArnThreads>(t, B);
+// the Arnoldi model (row f1) and / or -through hooks (row f4): 512 threads,
+// more registers per thread
+template <bool SMEM_LUT, bool ARN, bool THR>
+__global__ void __launch_bounds__(kFwdArnThreads, 1) fwd_persistent_ext_kernel(Topo t, const __grid_constant__ Batch B) {
+  fwd_persistent_body<SMEM_LUT, false, ARN, THR, kFwdArnThreads>(t, B);
 }
 
 // units [u0, u1) of one gate stage, one warp each; grid.y = corner
@@ -1181,7 +1241,7 @@ __global__ void __launch_bounds__(kThreads) fwd_stage_kernel(Topo t, const __gri
   pdl_wait();
   pdl_launch();
   if (u >= u1) return;
-  fwd_unit<TRACE, false>(t, c, L, epoch_of(c), u, tr, fwd_rc<false>(c, tr));
+  fwd_unit<TRACE, false, false>(t, c, L, epoch_of(c), u, tr, fwd_rc<false>(c, tr));
 }
 
 // ---- backward: one lane per sink / pin (all four components in the lane)
@@ -1356,7 +1416,7 @@ __device__ __forceinline__ SinkFo bwd_fo(const Topo& t, const uint4& ud) {
   return f;
 }
 
-template <bool TRACE, bool ARN>
+template <bool TRACE, bool ARN, bool THR>
 __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, const float* __restrict__ L,
                                          uint32_t ep, uint32_t u, const uint4& ud, const SinkFo& fo) {
   const uint32_t lane = threadIdx.x & 31;
@@ -1401,7 +1461,13 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
       } else {
         hop_at(a, elm);                      // the sink's own arrival (slews unused)
       }
+      uint32_t tsl = kNone;
+      if constexpr (THR) {                   // row f4: a -through sink
+        tsl = __ldg(t.thr_sink + k);
+        if (tsl != kNone) thr_sink4(t, c, k, a, s);
+      }
       bwd_pin(t, c, L, ep, fa, fb, pre, t.sfo_dst, t.sfo_info, a, s, r);
+      if constexpr (THR) thr_rat(t, c, tsl, r);
       if (TRACE) t_data = gtimer();
       c.rat[t.NP + k] = to_f4(r);
       const Q4 sk = slack_of(a, r);
@@ -1471,6 +1537,7 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
     const FoPre pre = bwd_pre(c, pa, pb, ep);
     if (pa.w != kNone) sl_v = load_slew(c, v);   // the pin's own endpoint seed needs its slews
     bwd_pin(t, c, L, ep, pa, pb, pre, t.pfo_dst, t.pfo_info, at_v, sl_v, acc);
+    if constexpr (THR) thr_rat(t, c, __ldg(t.thr_pull + v), acc);
     const Q4 sp = slack_of(at_v, acc);
     c.slack[v] = to_f4(sp);
     if (pa.w != kNone) write_ep(c, pa.w, sp);
@@ -1487,7 +1554,7 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
   trace_unit<TRACE>(c, (size_t)t.n_fwu + u, t_start, t_ready ? t_ready : t_start, t_data);
 }
 
-template <bool SMEM_LUT, bool TRACE, bool ARN, int NT>
+template <bool SMEM_LUT, bool TRACE, bool ARN, bool THR, int NT>
 __device__ __forceinline__ void bwd_persistent_body(const Topo& t, const Batch& B) {
   stage_luts<SMEM_LUT>(B, kNone);
   const uint32_t K = B.K, gw = blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
@@ -1518,11 +1585,11 @@ __device__ __forceinline__ void bwd_persistent_body(const Topo& t, const Batch& 
       u = ns + __shfl_sync(kFull, x, 0);
       if (u >= t.n_bwu) break;
       ud = __ldg(t.bwu + u);
-      bwd_unit<TRACE, ARN>(t, c, L, ep, u, ud, bwd_fo(t, ud));
+      bwd_unit<TRACE, ARN, THR>(t, c, L, ep, u, ud, bwd_fo(t, ud));
       continue;
     }
     const uint4 nu = u + W < ns ? __ldg(t.bwu + u + W) : none;
-    bwd_unit<TRACE, ARN>(t, c, L, ep, u, ud, bwd_fo(t, ud));
+    bwd_unit<TRACE, ARN, THR>(t, c, L, ep, u, ud, bwd_fo(t, ud));
     u += W;
     ud = nu;
   }
@@ -1589,7 +1656,7 @@ __device__ __forceinline__ void bwd_persistent_body(const Topo& t, const Batch& 
       issue(nx);                             // the next unit's records stream in meanwhile
       if (u + 2 * W < ns) nnx = __ldg(t.bwu + u + 2 * W);
     }
-    bwd_unit<TRACE, ARN>(t, c, L, ep, u, ud, cf);
+    bwd_unit<TRACE, ARN, THR>(t, c, L, ep, u, ud, cf);
     if (dyn) {
       u = un;
       ud = nx;
@@ -1631,7 +1698,7 @@ __device__ __forceinline__ void bwd_persistent_body(const Topo& t, const Batch& 
       nfo = bwd_fo(t, nx);                   // next unit's fan-out records (its record arrived)
       if (u + 2 * W < ns) nnx = __ldg(t.bwu + u + 2 * W);
     }
-    bwd_unit<TRACE, ARN>(t, c, L, ep, u, ud, fo);
+    bwd_unit<TRACE, ARN, THR>(t, c, L, ep, u, ud, fo);
     if (dyn) {
       u = un;
       ud = nx;
@@ -1656,13 +1723,13 @@ __device__ __forceinline__ void bwd_persistent_body(const Topo& t, const Batch& 
 template <bool SMEM_LUT, bool TRACE>
 __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_kernel(Topo t,
                                                                                    const __grid_constant__ Batch B) {
-  bwd_persistent_body<SMEM_LUT, TRACE, false, kBwdThreads>(t, B);
+  bwd_persistent_body<SMEM_LUT, TRACE, false, false, kBwdThreads>(t, B);
 }
 
 constexpr int kBwdArnThreads = 512;
-template <bool SMEM_LUT>
-__global__ void __launch_bounds__(kBwdArnThreads, 1) bwd_persistent_arn_kernel(Topo t, const __grid_constant__ Batch B) {
-  bwd_persistent_body<SMEM_LUT, false, true, kBwdArnThreads>(t, B);
+template <bool SMEM_LUT, bool ARN, bool THR>
+__global__ void __launch_bounds__(kBwdArnThreads, 1) bwd_persistent_ext_kernel(Topo t, const __grid_constant__ Batch B) {
+  bwd_persistent_body<SMEM_LUT, false, ARN, THR, kBwdArnThreads>(t, B);
 }
 
 template <bool SMEM_LUT, bool TRACE>
@@ -1678,7 +1745,7 @@ __global__ void __launch_bounds__(kThreads) bwd_stage_kernel(Topo t, const __gri
   pdl_wait();
   pdl_launch();
   if (u >= u1) return;
-  bwd_unit<TRACE, false>(t, c, L, epoch_of(c), u, ud, fo);
+  bwd_unit<TRACE, false, false>(t, c, L, epoch_of(c), u, ud, fo);
 }
 
 // ------------------------------------------------------- a5: WNS / TNS
@@ -1764,6 +1831,46 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(Topo t, const __grid_c
 // row f4: fold this tag's results into the merged arrays, internal order
 // (pin i: its record read once for arrival and slew; a sink's driver record
 // is shared by its neighbours in the sink order)
+// row f4 -through: every pass's handed arrivals / slews undefined (start of an update)
+__global__ void thr_reset_kernel(Topo t, const __grid_constant__ Batch B, uint32_t n) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const CornerDev& c = B.c[blockIdx.y];
+  const float4 u = make_float4(CUDART_INF_F, CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F);
+  c.thr_hat[i] = u;
+  c.thr_hsl[i] = u;
+}
+// after this pass's forward: its arrivals / slews at the through sinks where
+// its tag advances, handed to the advanced pass (recomputed from the driver
+// exactly as the kernels do)
+__global__ void thr_capture_kernel(Topo t, const __grid_constant__ Batch B) {
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= t.n_thr_sk) return;
+  const CornerDev& c = B.c[blockIdx.y];
+  const uint2 e = t.thr_sk[x];
+  const uint32_t d = t.thr_dst[e.y];
+  if (d == kNone) return;
+  const uint32_t k = e.x, dv = t.sink_drv[k];
+  Q4 at, sl;
+  load_rec(c, dv, at, sl);
+  if (t.net_model == 1) arn_net_hop(at, sl, c.elm[k], c.arn_lam[dv], c.arn_res[k], true);
+  else net_hop(at, sl, c.elm[k]);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float* ha = thr_word(c.thr_hat, t, d, e.y, q);
+    float* hs = thr_word(c.thr_hsl, t, d, e.y, q);
+    *ha = q < 2 ? fminf(*ha, at.v[q]) : fmaxf(*ha, at.v[q]);
+    *hs = q < 2 ? fminf(*hs, sl.v[q]) : fmaxf(*hs, sl.v[q]);
+  }
+}
+// the next record epoch (after a forward-only pass)
+__global__ void bump_epoch_kernel(const __grid_constant__ Batch B) {
+  const CornerDev& c = B.c[threadIdx.x];
+  if (threadIdx.x >= B.K) return;
+  const uint32_t e = *c.epoch + 1;
+  *c.epoch = e ? e : 1;
+}
+
 __global__ void merge_tag_kernel(Topo t, CornerDev c, int first) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < t.n_ep) {
@@ -1787,6 +1894,7 @@ __global__ void merge_tag_kernel(Topo t, CornerDev c, int first) {
     load_rec(c, dv, at, sl);
     if (t.net_model == 1) arn_net_hop(at, sl, c.elm[k], c.arn_lam[dv], c.arn_res[k], true);
     else net_hop(at, sl, c.elm[k]);
+    if (t.thr_sink) thr_sink4(t, c, k, at, sl);
     rt = c.rat[i];
   }
   const float4 v[4] = {to_f4(at), to_f4(sl), rt, c.slack[i]};
@@ -2153,6 +2261,22 @@ cudaError_t launch_merge_tag(const Topo& t, const CornerDev& c, int first, cudaS
   return cudaGetLastError();
 }
 
+cudaError_t launch_thr_reset(const Topo& t, const Batch& b, uint32_t n_tags, cudaStream_t s) {
+  const uint64_t n = (uint64_t)n_tags * t.n_thr;
+  if (n) thr_reset_kernel<<<dim3(blocks(n), b.K), kThreads, 0, s>>>(t, b, (uint32_t)n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_thr_capture(const Topo& t, const Batch& b, cudaStream_t s) {
+  if (t.n_thr_sk) thr_capture_kernel<<<dim3(blocks(t.n_thr_sk), b.K), kThreads, 0, s>>>(t, b);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bump_epoch(const Batch& b, cudaStream_t s) {
+  bump_epoch_kernel<<<1, kMaxBatch, 0, s>>>(b);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gather_rc(const Topo& t, const CornerDev& c, float* net_load, float* pin_elm, cudaStream_t s) {
   const uint32_t n = t.N > t.P ? t.N : t.P;
   if (n) gather_rc_kernel<<<blocks(n), kThreads, 0, s>>>(t, c, net_load, pin_elm);
@@ -2277,15 +2401,6 @@ uint32_t persistent_grid(uint32_t smem_f4, int which) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &nt, smem_f4 ? bwd_persistent_kernel<true, true> : bwd_persistent_kernel<false, true>, kBwdThreads,
         smem + kBwdExtraSmem);
-  } else if (which == 2) {                   // Arnoldi-model instantiations (row f1)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &nb, smem_f4 ? fwd_persistent_arn_kernel<true> : fwd_persistent_arn_kernel<false>, kFwdArnThreads, smem);
-    nt = nb;
-  } else {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &nb, smem_f4 ? bwd_persistent_arn_kernel<true> : bwd_persistent_arn_kernel<false>, kBwdArnThreads,
-        smem + kBwdExtraSmem);
-    nt = nb;
   }
   cudaGetLastError();
   return (uint32_t)(std::min(nb, nt) * sms);
@@ -2309,14 +2424,38 @@ cudaError_t coop_launch(Kern kernel, uint32_t grid, uint32_t block, size_t smem,
 
 static bool traced(const Batch& b) { return b.c[0].trace != nullptr; }
 
+using PersistentKern = void (*)(Topo, const Batch);
+// the Arnoldi / -through instantiations (fwd_persistent_ext_kernel, bwd_persistent_ext_kernel)
+static PersistentKern ext_kernel(bool fwd, bool sm, bool arn, bool thr) {
+  if (fwd) {
+    if (sm) return arn ? (thr ? fwd_persistent_ext_kernel<true, true, true> : fwd_persistent_ext_kernel<true, true, false>)
+                       : fwd_persistent_ext_kernel<true, false, true>;
+    return arn ? (thr ? fwd_persistent_ext_kernel<false, true, true> : fwd_persistent_ext_kernel<false, true, false>)
+               : fwd_persistent_ext_kernel<false, false, true>;
+  }
+  if (sm) return arn ? (thr ? bwd_persistent_ext_kernel<true, true, true> : bwd_persistent_ext_kernel<true, true, false>)
+                     : bwd_persistent_ext_kernel<true, false, true>;
+  return arn ? (thr ? bwd_persistent_ext_kernel<false, true, true> : bwd_persistent_ext_kernel<false, true, false>)
+             : bwd_persistent_ext_kernel<false, false, true>;
+}
+static uint32_t ext_grid(PersistentKern k, uint32_t threads, size_t smem) {
+  int dev = 0, sms = 0, nb = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, (int)threads, smem);
+  cudaGetLastError();
+  return (uint32_t)(nb * sms);
+}
+
 cudaError_t launch_fwd_persistent(const Topo& t, const Batch& b, uint32_t grid, cudaStream_t s) {
   if (!t.NP) return cudaSuccess;
   const size_t sm = 16ull * b.smem_f4;
-  if (t.net_model == 1) {                    // row f1: the Arnoldi-model instantiation
-    const uint32_t g = persistent_grid(b.smem_f4, 2);
+  const bool arn = t.net_model == 1, thr = t.thr_pull != nullptr;
+  if (arn || thr) {                          // row f1 Arnoldi model / row f4 -through hooks
+    const PersistentKern k = ext_kernel(true, b.smem_f4 != 0, arn, thr);
+    const uint32_t g = ext_grid(k, kFwdArnThreads, sm);
     if (!g) return cudaErrorCooperativeLaunchTooLarge;
-    return b.smem_f4 ? coop_launch(fwd_persistent_arn_kernel<true>, g, kFwdArnThreads, sm, s, t, b)
-                     : coop_launch(fwd_persistent_arn_kernel<false>, g, kFwdArnThreads, 0, s, t, b);
+    return coop_launch(k, g, kFwdArnThreads, sm, s, t, b);
   }
   // STA_TRACE builds per-unit timestamps into a separate instantiation
   if (traced(b))
@@ -2329,11 +2468,12 @@ cudaError_t launch_fwd_persistent(const Topo& t, const Batch& b, uint32_t grid, 
 cudaError_t launch_bwd_persistent(const Topo& t, const Batch& b, uint32_t grid, cudaStream_t s) {
   if (!t.n_bwu) return cudaSuccess;
   const size_t sm = 16ull * b.smem_f4 + kBwdExtraSmem;
-  if (t.net_model == 1) {
-    const uint32_t g = persistent_grid(b.smem_f4, 3);
+  const bool arn = t.net_model == 1, thr = t.thr_pull != nullptr;
+  if (arn || thr) {
+    const PersistentKern k = ext_kernel(false, b.smem_f4 != 0, arn, thr);
+    const uint32_t g = ext_grid(k, kBwdArnThreads, sm);
     if (!g) return cudaErrorCooperativeLaunchTooLarge;
-    return b.smem_f4 ? coop_launch(bwd_persistent_arn_kernel<true>, g, kBwdArnThreads, sm, s, t, b)
-                     : coop_launch(bwd_persistent_arn_kernel<false>, g, kBwdArnThreads, kBwdExtraSmem, s, t, b);
+    return coop_launch(k, g, kBwdArnThreads, sm, s, t, b);
   }
   if (traced(b))
     return b.smem_f4 ? coop_launch(bwd_persistent_kernel<true, true>, grid, kBwdThreads, sm, s, t, b)
@@ -2346,11 +2486,13 @@ cudaError_t set_lut_smem_limit(size_t bytes) {
   const int b = (int)bytes;
   cudaError_t e = cudaFuncSetAttribute(fwd_stage_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(bwd_stage_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(fwd_persistent_arn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(bwd_persistent_arn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             b + (int)kBwdExtraSmem);
+  for (int v = 0; v < 3 && e == cudaSuccess; ++v) {   // (arn, thr) = (1, 0), (0, 1), (1, 1)
+    const bool arn = v != 1, thr = v != 0;
+    e = cudaFuncSetAttribute(ext_kernel(true, true, arn, thr), cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(ext_kernel(false, true, arn, thr), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               b + (int)kBwdExtraSmem);
+  }
   for (int tr = 0; tr < 2 && e == cudaSuccess; ++tr) {
     e = cudaFuncSetAttribute(tr ? fwd_persistent_kernel<true, true> : fwd_persistent_kernel<true, false>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, b);

@@ -81,7 +81,8 @@ class PathSet(C.Structure):
 class ExceptionsDesc(C.Structure):
     _fields_ = [("mem", C.c_int), ("num", C.c_uint32), ("kind", C.c_void_p), ("value", C.c_void_p),
                 ("from_ptr", C.c_void_p), ("from_pins", C.c_void_p), ("to_ptr", C.c_void_p),
-                ("to_pins", C.c_void_p)]
+                ("to_pins", C.c_void_p), ("thr_ptr", C.c_void_p), ("seg_ptr", C.c_void_p),
+                ("seg_pins", C.c_void_p)]
 
 
 class ClocksDesc(C.Structure):
@@ -323,8 +324,10 @@ class Context:
         n = nn.value
         return (rc_ptr,) + tuple(o[:n] for o in outs)
 
-    def set_exceptions(self, kind=(), value=(), from_ptr=(0,), from_pins=(), to_ptr=(0,), to_pins=()):
-        """-from / -to timing exceptions (sta_set_exceptions); no arguments clear them."""
+    def set_exceptions(self, kind=(), value=(), from_ptr=(0,), from_pins=(), to_ptr=(0,), to_pins=(),
+                       thr_ptr=None, seg_ptr=(0,), seg_pins=()):
+        """Timing exceptions (sta_set_exceptions): -from / -to lists and, with
+        thr_ptr, ordered -through segments; no arguments clear them."""
         a = _Args(self.device)
         e = ExceptionsDesc()
         e.num = len(kind)
@@ -334,6 +337,10 @@ class Context:
         e.from_pins = a.ptr(from_pins, np.uint32)
         e.to_ptr = a.ptr(to_ptr, np.uint32)
         e.to_pins = a.ptr(to_pins, np.uint32)
+        if thr_ptr is not None:
+            e.thr_ptr = a.ptr(thr_ptr, np.uint32)
+            e.seg_ptr = a.ptr(seg_ptr, np.uint32)
+            e.seg_pins = a.ptr(seg_pins, np.uint32)
         e.mem = a.kind
         self._check(self._L.sta_set_exceptions(self.h, C.byref(e)))
 
@@ -493,4 +500,8 @@ def load_design(ctx: Context, d, corners=None, device_rc: bool = False, device_g
         ctx.set_clocks(ck.period, ck.pin_clk)
     ex = getattr(d, "exceptions", None)
     if ex is not None and ex.num:
-        ctx.set_exceptions(ex.kind, ex.value, ex.from_ptr, ex.from_pins, ex.to_ptr, ex.to_pins)
+        if getattr(ex, "has_through", False):
+            ctx.set_exceptions(ex.kind, ex.value, ex.from_ptr, ex.from_pins, ex.to_ptr, ex.to_pins,
+                               ex.thr_ptr, ex.seg_ptr, ex.seg_pins)
+        else:
+            ctx.set_exceptions(ex.kind, ex.value, ex.from_ptr, ex.from_pins, ex.to_ptr, ex.to_pins)

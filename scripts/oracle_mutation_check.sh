@@ -13,6 +13,7 @@ s = open('/tmp/orc_backup.c').read(); a, b = sys.argv[1], sys.argv[2]
 assert a in s, a
 open('oracle/sta_oracle.c', 'w').write(s.replace(a, b, 1))
 PY
+  if [ $? -ne 0 ]; then echo "NOT APPLIED (pattern missing): $1"; fail=1; return 1; fi
   rm -f oracle/liboracle.so
   if timeout 600 python -m pytest tests/test_oracle_lut_rc.py tests/test_oracle_propagation.py tests/test_oracle_steiner.py tests/test_oracle_arnoldi.py tests/test_oracle_exceptions.py -q -x >/dev/null 2>&1; then
     echo "NOT CAUGHT: $1"; fail=1; return 1
@@ -27,7 +28,7 @@ mut 'double re = -(double)d->po_out_min[2 * k + rf];' 'double re = (double)d->po
 mut 'double dd = lut_id(d, tb + (uint32_t)orf, s_in, ld);' 'double dd = lut_id(d, tb + (uint32_t)orf, ld, s_in);'
 mut 'return (1 - tx) * (1 - ty) * v00 + tx * (1 - ty) * v10' 'return (1 - tx) * (1 - ty) * v00 + tx * (1 - ty) * v01'
 mut 'if (ws < 0) tns_s += ws;' 'if (ws < 0) tns_s += wh;'
-mut 'at[4 * p + Q(0, 1)] = d->period / 2;' 'at[4 * p + Q(0, 1)] = d->period;'
+mut 'at[4 * p + Q(0, 1)] = Tc / 2;' 'at[4 * p + Q(0, 1)] = Tc;'
 mut 'if (!isfinite(at[4 * u + Q(el, irf)])) continue;   /* only arcs O5 used */' ''
 mut 'if (level[u] + 1 > level[v]) level[v] = level[u] + 1;' 'if (level[u] > level[v]) level[v] = level[u] + 1;'
 mut 'if (dd < 0) dd = 0;' ''
