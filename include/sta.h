@@ -288,8 +288,11 @@ STA_API sta_status sta_set_clocks(sta_ctx ctx, const sta_clocks* clk);
 /* Per-corner RC values: res[i] = resistance of the edge parent -> i (kOhm,
  * ignored at node 0), cap[i] = wire capacitance to ground at node i (fF);
  * both num_nodes long, >= 0 and finite.  HOST: copied into ctx-owned device
- * buffers in stream order before the call returns (page-locked buffers move
- * by DMA at link speed).  DEVICE: BORROWED, zero copy -- the caller keeps both
+ * buffers before the call returns (page-locked buffers move by DMA at link
+ * speed); the ctx keeps two buffer pairs per corner and copies on its own
+ * copy stream into the pair no enqueued update reads, so the copy of the
+ * next iteration's values runs beside an update still in flight; the next
+ * update is ordered after the copy.  DEVICE: BORROWED, zero copy -- the caller keeps both
  * arrays alive and unmodified until the next sta_update_timing has completed
  * on the ctx stream; the call itself never blocks the host (the pointer pair
  * is published by a stream-ordered one-thread kernel), so the next

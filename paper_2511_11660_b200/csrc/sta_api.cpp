@@ -194,6 +194,13 @@ struct CornerState {
   Arena lib_arena, rc_arena, state_arena, ptr_arena;
   const float* rc_res = nullptr;   // active R / Cw arrays (owned or borrowed)
   const float* rc_cap = nullptr;
+  // STA_MEM_HOST values: two owned {R, Cw} buffers, written alternately on the
+  // copy stream; free_ev[b] = the point of the ctx stream after which buffer b
+  // is no longer read (recorded when the other buffer becomes current)
+  float* hbuf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  int hcur = -1;                   // the current owned buffer (-1: borrowed or none)
+  cudaEvent_t free_ev[2] = {nullptr, nullptr};
+  bool free_rec[2] = {false, false};
   size_t lut_bytes = 0;                  // device table pool size
   sta::CornerDev dev{};
 };
@@ -206,6 +213,8 @@ struct sta_ctx_s {
   bool own_stream = false;
   cudaStream_t side = nullptr;    // tier-C RC branch (forked from / joined to `stream`)
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  cudaStream_t copy = nullptr;    // host RC values: H2D beside a running update (double-buffered)
+  cudaEvent_t copy_ev = nullptr;
   u32 K = 1;
   std::string err;
   bool poisoned = false;
@@ -2015,11 +2024,16 @@ sta_status sta_create(int cuda_device, uint32_t num_corners, void* cuda_stream, 
   if (cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi) != cudaSuccess ||
       cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->copy_ev, cudaEventDisableTiming) != cudaSuccess) {
     delete c;
     return STA_ERR_CUDA;
   }
   c->corners.resize(num_corners);
+  for (CornerState& cs : c->corners)
+    for (auto& e : cs.free_ev)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) { delete c; return STA_ERR_CUDA; }
   if (const char* g = std::getenv("STA_NO_GRAPH")) c->use_graph = g[0] == '0';
   if (const char* g = std::getenv("STA_STAGE_KERNELS")) c->use_persistent = g[0] == '0';
   if (const char* g = std::getenv("STA_TRACE")) c->trace_path = g;
@@ -2036,7 +2050,10 @@ sta_status sta_destroy(sta_ctx c) {
   c->cons_arena.release();
   c->tmp_arena.release();
   c->path_arena.release();
+  cudaStreamSynchronize(c->copy);
   for (CornerState& cs : c->corners) {
+    for (auto& e : cs.free_ev)
+      if (e) cudaEventDestroy(e);
     cs.lib_arena.release();
     cs.rc_arena.release();
     cs.state_arena.release();
@@ -2048,6 +2065,8 @@ sta_status sta_destroy(sta_ctx c) {
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   if (c->join_ev) cudaEventDestroy(c->join_ev);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->copy_ev) cudaEventDestroy(c->copy_ev);
+  if (c->copy) cudaStreamDestroy(c->copy);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return STA_OK;
@@ -2346,30 +2365,47 @@ sta_status sta_set_rc_values(sta_ctx c, uint32_t corner, sta_mem mem, const floa
       if (!cs.rc_arena.ptrs.empty()) {         // owned buffers of an earlier HOST call may be in use
         ck(cudaStreamSynchronize(c->stream), "sync");
         cs.rc_arena.release();
+        cs.hcur = -1;
+        cs.free_rec[0] = cs.free_rec[1] = false;
       }
       cs.rc_res = res;
       cs.rc_cap = cap;
+      publish_rc_pointers(c, cs);
     } else if (mem == STA_MEM_HOST) {
-      // copied into owned device buffers in stream order (page-locked caller
-      // buffers: DMA at link speed); the values are validated on the device by
-      // the RC kernels (STA_ERR_RC at the next synchronizing call)
-      if (cs.rc_arena.ptrs.empty() || cs.rc_arena.bytes < 2ull * c->n_rc * sizeof(float)) {
+      // copied into owned device buffers (page-locked caller buffers: DMA at
+      // link speed) on the copy stream, into the buffer the updates already
+      // enqueued do not read, so the copy runs beside an update still in
+      // flight (an optimization loop's next values during this update); the
+      // values are validated on the device by the RC kernels (STA_ERR_RC at
+      // the next synchronizing call)
+      if (cs.rc_arena.ptrs.empty() || cs.rc_arena.bytes < 4ull * c->n_rc * sizeof(float)) {
         ck(cudaStreamSynchronize(c->stream), "sync");
         cs.rc_arena.release();
-        cs.rc_res = cs.rc_arena.alloc<float>(c->n_rc);
-        cs.rc_cap = cs.rc_arena.alloc<float>(c->n_rc);
+        for (auto& b : cs.hbuf)
+          for (auto& x : b) x = cs.rc_arena.alloc<float>(c->n_rc);
+        cs.hcur = -1;
+        cs.free_rec[0] = cs.free_rec[1] = false;
       }
+      const int b = cs.hcur == 0 ? 1 : 0;
+      if (cs.free_rec[b]) ck(cudaStreamWaitEvent(c->copy, cs.free_ev[b], 0), "copy wait");
       if (c->n_rc) {
-        ck(cudaMemcpyAsync(const_cast<float*>(cs.rc_res), res, sizeof(float) * c->n_rc, cudaMemcpyHostToDevice,
-                           c->stream), "H2D");
-        ck(cudaMemcpyAsync(const_cast<float*>(cs.rc_cap), cap, sizeof(float) * c->n_rc, cudaMemcpyHostToDevice,
-                           c->stream), "H2D");
+        ck(cudaMemcpyAsync(cs.hbuf[b][0], res, sizeof(float) * c->n_rc, cudaMemcpyHostToDevice, c->copy), "H2D");
+        ck(cudaMemcpyAsync(cs.hbuf[b][1], cap, sizeof(float) * c->n_rc, cudaMemcpyHostToDevice, c->copy), "H2D");
       }
+      ck(cudaEventRecord(c->copy_ev, c->copy), "copy event");
+      ck(cudaStreamWaitEvent(c->stream, c->copy_ev, 0), "copy join");
+      cs.rc_res = cs.hbuf[b][0];
+      cs.rc_cap = cs.hbuf[b][1];
+      publish_rc_pointers(c, cs);
+      if (cs.hcur >= 0) {                    // the old buffer is free once the work before this point is done
+        ck(cudaEventRecord(cs.free_ev[cs.hcur], c->stream), "free event");
+        cs.free_rec[cs.hcur] = true;
+      }
+      cs.hcur = b;
+      ck(cudaStreamSynchronize(c->copy), "sync");   // host buffers read before return
     } else {
       fail(STA_ERR_ARG, "bad sta_mem %d", (int)mem);
     }
-    publish_rc_pointers(c, cs);
-    if (mem == STA_MEM_HOST) ck(cudaStreamSynchronize(c->stream), "sync");   // host buffers read before return
     cs.rcv = true;
   });
 }

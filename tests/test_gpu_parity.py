@@ -292,3 +292,36 @@ def test_repeated_updates_with_changing_rc(sta):
         ctx.synchronize()
         compare_update(ctx, oracle.update(di))
     ctx.close()
+
+
+def test_pipelined_host_rc_values(sta):
+    """Optimization-loop pipelining through the ABI: step i+1's HOST RC values
+    are handed over (copied on the ctx's copy stream into the other owned
+    buffer pair) while step i's update is still in flight; each step's
+    results must be those of its own values, and a DEVICE (borrowed) call in
+    between must hand the buffers back cleanly."""
+    import copy
+    import torch
+    d = synth.generate(30000, 40, seed=13, n_hfn=2, hfn_range=(200, 3000), period=300.0)
+    ctx = sta.Context(0, 1)
+    sta.load_design(ctx, d)
+    scales = [(1.0, 1.0), (1.3, 0.8), (0.7, 1.25), (1.1, 0.9), (0.9, 1.1)]
+    vals = [d.rc[0].scaled(rs, cs) for rs, cs in scales]
+    exp = []
+    for v in vals:
+        di = copy.copy(d)
+        di.rc = [v]
+        exp.append(oracle.update(di))
+    pinned = [(torch.from_numpy(v.res).pin_memory(), torch.from_numpy(v.cap).pin_memory()) for v in vals]
+    ctx.set_rc_values(0, pinned[0][0].numpy(), pinned[0][1].numpy())
+    for i in range(len(vals)):
+        ctx.update_timing()
+        if i + 1 < len(vals):
+            if i == 2:                         # a borrowed device pair in the middle of the loop
+                rd = torch.from_numpy(vals[i + 1].res).cuda()
+                cd = torch.from_numpy(vals[i + 1].cap).cuda()
+                ctx.set_rc_values(0, rd, cd)
+            else:
+                ctx.set_rc_values(0, pinned[i + 1][0].numpy(), pinned[i + 1][1].numpy())
+        compare_update(ctx, exp[i])
+    ctx.close()
