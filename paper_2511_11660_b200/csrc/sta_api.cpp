@@ -1164,7 +1164,14 @@ void build_rc(sta_ctx c) {
   t.lumped_j = g.upload(lumped_j, s);
   t.nC = (u32)tierC.size();
   t.nCn = c->big_total;
-  t.tc_ev = g.upload(tc_ev, s);
+  {   // static event records {position | exit << 31, output tag of an enter event (kNone for exits)}
+    std::vector<uint2> ev2(tc_ev.size());
+    for (size_t e = 0; e < tc_ev.size(); ++e) {
+      const u32 pos = tc_ev[e] & 0x7FFFFFFFu;
+      ev2[e] = make_uint2(tc_ev[e], (tc_ev[e] >> 31) ? kNone : node_tag[nA + nB + pos]);
+    }
+    t.tc_ev = g.upload(ev2, s);
+  }
   c->node_user = std::move(node_user);
   c->rc_net_j = std::move(net_drv);
   ck(cudaStreamSynchronize(s), "rc upload");
@@ -1649,7 +1656,7 @@ u32 enqueue_rc(sta_ctx c, const sta::Batch& b, const sta::Topo& t) {
   }
   ck(sta::launch_rc(t, b, c->wgrid, s), "rc kernel");
   if (t.nC && !std::getenv("STA_RC_SERIAL")) ck(cudaStreamWaitEvent(s, c->join_ev, 0), "join wait");
-  launches += (t.n_wtiles ? 1 : 0) + (t.n_btiles ? 1 : 0) + (t.n_lumped ? 1 : 0) + (t.nC ? 2 : 0);
+  launches += (t.n_wtiles ? 1 : 0) + (t.n_btiles ? 1 : 0) + (t.n_lumped ? 1 : 0) + (t.nC ? 3 : 0);
   if (t.net_model == 1) {                    // row f1: the nets' reduced-order models
     ck(sta::launch_arn_reduce(t, b, s), "arnoldi kernel");
     launches += t.n_arn_nets ? 1 : 0;

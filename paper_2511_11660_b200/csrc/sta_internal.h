@@ -179,7 +179,8 @@ struct Topo {
   uint32_t nCn;               // tier-C nodes
   const uint4* tc_node;       // [nCn] {caller node id, tag (as node_tag), end (global position one
                               //  past the subtree), rc_scap bits}
-  const uint32_t* tc_ev;      // [2 nCn] node position of each event | 0x80000000 for an exit
+  const uint2* tc_ev;         // [2 nCn] {node position of each event | 0x80000000 for an exit,
+                              //  the node's tag for an enter event, kNone for an exit}
   // outputs to user order
   const uint32_t* int_of_user; // [P]
   const uint32_t* drv_of_net;  // [N] user net -> internal driver
@@ -283,10 +284,12 @@ cudaError_t launch_rc_tierC(const Topo& t, const Batch& b, cudaStream_t s);
 #endif
 constexpr uint32_t kTcTile = STA_TC_TILE;       // elements per tier-C block (256 threads x 8)
 __host__ __device__ inline uint32_t tierC_blocks(uint64_t n) { return (uint32_t)((n + kTcTile - 1) / kTcTile); }
-__host__ __device__ inline size_t tierC_scratch(uint32_t nCn) {
+__host__ __device__ inline size_t tierC_scratch_scan(uint32_t nCn) {
   const size_t nb = (size_t)tierC_blocks(nCn) + tierC_blocks(2ull * nCn);
   return (size_t)nCn + nb + (nb + 2 + 1) / 2 + 1;
 }
+// ... followed by w [nCn] (double): R(g) Cdown(g) of every tier-C node (0 at a root)
+__host__ __device__ inline size_t tierC_scratch(uint32_t nCn) { return tierC_scratch_scan(nCn) + nCn; }
 uint32_t rc_warp_grid();                        // co-resident grid of the tier-A kernel (per corner)
 // units [u0, u1) of one gate stage (one launch per stage, grid.y = corner)
 cudaError_t launch_fwd_stage(const Topo& t, const Batch& b, uint32_t u0, uint32_t u1, cudaStream_t s);

@@ -533,13 +533,16 @@ __global__ void __launch_bounds__(kThreads) rc_lumped_kernel(Topo t, const __gri
 
 // ---- tier C: segmented prefix sums over ONE global preorder array of the
 // large nets' nodes and over its Euler event sequence (layout in
-// sta_internal.h).  Two single-pass launches per corner on a side stream,
-// concurrent with tiers A and B:
+// sta_internal.h).  Three launches per corner on a side stream, concurrent
+// with tiers A and B:
 //   tc_node_kernel   node caps C -> segmented inclusive sums Si (segment =
-//                    net), stored;
-//   tc_event_kernel  w(g) = R(g) Cdown(g), Cdown(g) = Si[end(g) - 1] - Si[g] +
-//                    C(g); event values +-w -> segmented inclusive sums H;
-//                    elm(g) = H[enter(g)] written directly, net loads.
+//                    net), stored (single pass);
+//   tc_w_kernel      w(g) = R(g) Cdown(g), Cdown(g) = Si[end(g) - 1] - Si[g] +
+//                    C(g), stored; net loads (a map over the nodes);
+//   tc_event_kernel  event values +-w -> segmented inclusive sums H (single
+//                    pass); elm(g) = H[enter(g)] written directly.
+// (w was computed inside the event scan until r2: three dependent gathers
+// per event at 114 registers, 2 blocks per SM: 60 us on C3's 2.2M events.)
 // Each block scans its tile locally, publishes its segmented aggregate and
 // takes its carry-in from its predecessors by a look-back over their
 // AGGREGATES only (back to the nearest block holding a segment head), summed
@@ -721,64 +724,62 @@ __global__ void __launch_bounds__(kTcThreads, STA_TC_MINB) tc_node_kernel(Topo t
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(c.err_flag, 1u);
 }
 
-__global__ void __launch_bounds__(kTcThreads, STA_TC_MINB) tc_event_kernel(Topo t, const __grid_constant__ Batch B) {
+// w(g) = R(g) Cdown(g) of every tier-C node, Cdown(g) = Si[end(g) - 1] - Si[g]
+// + C(g) (a plain map over the nodes: high occupancy, one dependent gather);
+// a net's root writes the net load instead (w = 0)
+__global__ void __launch_bounds__(kThreads) tc_w_kernel(Topo t, const __grid_constant__ Batch B) {
+  pdl_wait();
+  pdl_launch();
+  const CornerDev& c = B.c[blockIdx.y];
+  const uint32_t n = t.nCn, g = blockIdx.x * blockDim.x + threadIdx.x;
+  bool bad = false;
+  if (g < n) {
+    const double* Si = c.scratch;
+    double* w = c.scratch + tierC_scratch_scan(n);
+    const uint4 nd = __ldg(t.tc_node + g);
+    const float cw = c.rc_vals[1][nd.x], rr = c.rc_vals[0][nd.x];
+    const double C = (double)cw + (double)__uint_as_float(nd.w);
+    const double cd = __ldcg(Si + nd.z - 1) - __ldcg(Si + g) + C;
+    double x = 0.0;
+    if (tc_head(nd.y)) {
+      c.load[nd.y & 0x7FFFFFFFu] = (float)cd;               // net load = Cdown(root)
+    } else {
+      bad = bad_rc(rr, 0.f);
+      x = (double)rr * cd;
+    }
+    w[g] = x;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(c.err_flag, 1u);
+}
+
+// event values +-w(g) (enter / exit) -> segmented inclusive sums H; elm(g) =
+// H at enter(g), written for the nodes of sinks
+#ifndef STA_TC_EV_MINB
+#define STA_TC_EV_MINB 4
+#endif
+__global__ void __launch_bounds__(kTcThreads, STA_TC_EV_MINB) tc_event_kernel(Topo t, const __grid_constant__ Batch B) {
   __shared__ SegSum s_w[32];
   pdl_wait();
   pdl_launch();
   const CornerDev& c = B.c[blockIdx.y];
   const uint32_t n = t.nCn, m = 2 * n, nbn = tierC_blocks(n), nb = tierC_blocks(m);
-  const double* Si = c.scratch;
+  const double* w = c.scratch + tierC_scratch_scan(n);
   const TcScan sc{c.scratch + n + nbn, reinterpret_cast<uint32_t*>(c.scratch + n + nbn + nb) + nbn};
   uint32_t* cnt = reinterpret_cast<uint32_t*>(c.scratch + n + nbn + nb) + nbn + nb + 1;
   const uint32_t ep = __ldcg(c.epoch) & 0x7FFFFFFFu;
   const uint32_t b = tc_ticket(cnt, nb);
-  const float* R = c.rc_vals[0];
-  const float* Cw = c.rc_vals[1];
   const uint32_t e0 = b * kTcTile + threadIdx.x * kTcPer;
   double v[kTcPer];
   uint32_t hd = 0;
-  bool bad = false;
-  // all loads of the thread's events first (no store in between: the loads of
-  // the events overlap instead of paying one dependent chain each)
-  uint32_t ev[kTcPer];
-  uint4 nd[kTcPer];
+  uint2 ev[kTcPer];
 #pragma unroll
-  for (int j = 0; j < kTcPer; ++j) ev[j] = e0 + j < m ? __ldg(t.tc_ev + e0 + j) : 0u;
+  for (int j = 0; j < kTcPer; ++j) ev[j] = e0 + j < m ? __ldg(t.tc_ev + e0 + j) : make_uint2(0u, kNone);
 #pragma unroll
-  for (int j = 0; j < kTcPer; ++j) nd[j] = __ldg(t.tc_node + (ev[j] & 0x7FFFFFFFu));
-  float cw[kTcPer], rr[kTcPer];
-  double s_end[kTcPer], s_g[kTcPer];
+  for (int j = 0; j < kTcPer; ++j) v[j] = e0 + j < m ? __ldcg(w + (ev[j].x & 0x7FFFFFFFu)) : 0.0;
 #pragma unroll
   for (int j = 0; j < kTcPer; ++j) {
-    cw[j] = Cw[nd[j].x];
-    rr[j] = R[nd[j].x];
-    s_end[j] = __ldcg(Si + nd[j].z - 1);
-    s_g[j] = __ldcg(Si + (ev[j] & 0x7FFFFFFFu));
-  }
-  uint32_t ld_drv[kTcPer];
-  float ld_val[kTcPer];
-#pragma unroll
-  for (int j = 0; j < kTcPer; ++j) {
-    const uint32_t e = e0 + j;
-    v[j] = 0.0;
-    ld_drv[j] = kNone;
-    ld_val[j] = 0.f;
-    if (e < m) {
-      const bool exit = (ev[j] >> 31) != 0;
-      const bool root = tc_head(nd[j].y);
-      const double C = (double)cw[j] + (double)__uint_as_float(nd[j].w);
-      const double cd = s_end[j] - s_g[j] + C;
-      double w = 0.0;
-      if (!root) {
-        bad |= bad_rc(rr[j], 0.f);
-        w = (double)rr[j] * cd;
-      } else if (!exit) {
-        ld_drv[j] = nd[j].y & 0x7FFFFFFFu;                  // net load = Cdown(root)
-        ld_val[j] = (float)cd;
-        hd |= 1u << j;                                      // a net's events start at its root's enter
-      }
-      v[j] = exit ? -w : w;
-    }
+    if (ev[j].x >> 31) v[j] = -v[j];
+    if (tc_head(ev[j].y)) hd |= 1u << j;                   // a net's events start at its root's enter
   }
   SegSum run{0.0, 0u};
 #pragma unroll
@@ -792,14 +793,11 @@ __global__ void __launch_bounds__(kTcThreads, STA_TC_MINB) tc_event_kernel(Topo 
   if (!ex.f) ex.v += carry;
 #pragma unroll
   for (int j = 0; j < kTcPer; ++j) {
-    if (ld_drv[j] != kNone) c.load[ld_drv[j]] = ld_val[j];
     // elm(g) = H at enter(g) (exit events and Steiner / root nodes write nothing)
     const bool before = (hd & ((2u << j) - 1u)) == 0;
-    const uint32_t tag = nd[j].y;
-    if (e0 + j < m && !(ev[j] >> 31) && tag != kNone && !(tag & 0x80000000u))
-      c.elm[tag] = (float)(before ? ex.v + v[j] : v[j]);
+    const uint32_t tag = ev[j].y;
+    if (tag != kNone && !(tag & 0x80000000u)) c.elm[tag] = (float)(before ? ex.v + v[j] : v[j]);
   }
-  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(c.err_flag, 1u);
 }
 
 // ------------------------------------------- a2-a5: propagation work units
@@ -2227,6 +2225,7 @@ cudaError_t launch_rc_tierC(const Topo& t, const Batch& b, cudaStream_t s) {
   if (!t.nC) return cudaSuccess;
   const uint32_t K = b.K;
   cudaError_t e = pdl_launch_kernel(tc_node_kernel, dim3(tierC_blocks(t.nCn), K), kTcThreads, s, t, b);
+  if (e == cudaSuccess) e = pdl_launch_kernel(tc_w_kernel, dim3(blocks(t.nCn), K), kThreads, s, t, b);
   if (e == cudaSuccess) e = pdl_launch_kernel(tc_event_kernel, dim3(tierC_blocks(2ull * t.nCn), K), kTcThreads, s, t, b);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
