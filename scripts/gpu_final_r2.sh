@@ -19,7 +19,9 @@ timeout 600 python bench.py --config $cfg --net-model arnoldi --steps 10 --warmu
 done
 for cfg in c2_tau c3_superblue; do
 timeout 600 python bench.py --config $cfg --exceptions --steps 10 --warmup 3 --no-cpu-baseline --quick > gpurun_out/bench_exc_${cfg}_${T}.json 2> gpurun_out/bench_exc_${cfg}_${T}.err
+timeout 600 python bench.py --config $cfg --through --steps 5 --warmup 3 --no-cpu-baseline --quick > gpurun_out/bench_thr_${cfg}_${T}.json 2> gpurun_out/bench_thr_${cfg}_${T}.err
 done
+timeout 300 python scripts/load_time.py c3_superblue > gpurun_out/load_time_${T}.txt 2>&1
 timeout 900 python scripts/bench_steiner.py c4_tdp --full-parity > gpurun_out/steiner_c4_${T}.json 2> gpurun_out/steiner_c4_${T}.err
 timeout 900 python scripts/bench_steiner.py c3_superblue --reps 3 > gpurun_out/steiner_c3_${T}.json 2> gpurun_out/steiner_c3_${T}.err
 timeout 600 python scripts/latency_probe.py > gpurun_out/latency_${T}.txt 2>&1
@@ -29,7 +31,7 @@ timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --mast
 if [ "${NCU:-1}" = 1 ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_${T}.csv python bench.py --steps 3 --warmup 3 --quick > gpurun_out/ncu_launch_${T}.log 2>&1
-for K in fwd_persistent bwd_persistent rc_warp tc_event tc_node; do
+for K in fwd_persistent bwd_persistent rc_warp tc_event tc_node tc_w; do
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:${K} \
     --launch-skip 3 --launch-count 1 -o gpurun_out/prof_${T}_${K} \
     python bench.py --steps 1 --warmup 3 --quick > gpurun_out/ncu_${K}_${T}.log 2>&1

@@ -45,3 +45,24 @@ for d in designs[:2]:
     g = ctx.build_steiner(x, y, **synth.STEINER_UNITS)
     ctx.close()
     print("ok arnoldi + steiner", d.name, int(g[0][-1]), flush=True)
+
+# row f4: -from / -through / -to exceptions with 2 clocks (THR instantiations,
+# handoff / capture / epoch kernels), Elmore and Arnoldi, 3 corners
+import numpy as np  # noqa: E402
+from tests.test_oracle_exceptions import random_clocks, random_exceptions_through  # noqa: E402
+for model in ("elmore", "arnoldi"):
+    d = designs[3]
+    rng = np.random.default_rng(5)
+    d.exceptions = random_exceptions_through(d, rng, 3)
+    d.clocks = random_clocks(d, rng, 2)
+    ctx = sta.Context(0, d.num_corners)
+    sta.load_design(ctx, d)
+    if model == "arnoldi":
+        ctx.set_net_model("arnoldi", 4)
+    for _ in range(2):
+        ctx.update_timing()
+    ctx.synchronize()
+    for c in range(d.num_corners):
+        compare_update(ctx, oracle.update(d, c, net_model=model), corner=c)
+    ctx.close()
+    print("ok exceptions -through", model, flush=True)
