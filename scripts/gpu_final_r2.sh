@@ -37,7 +37,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:${K}
     python bench.py --steps 1 --warmup 3 --quick > gpurun_out/ncu_${K}_${T}.log 2>&1
 done
 fi
-if [ "${SAN:-1}" = 1 ]; then
+# compute-sanitizer is closed on the GPU pool since r2final2 (rc 86); opt in with SAN=1
+if [ "${SAN:-0}" = 1 ]; then
 for tool in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_run.py > gpurun_out/sanitizer_${tool}_${T}.log 2>&1
   echo "$tool rc=$?" >> gpurun_out/sanitizer_${tool}_${T}.log
