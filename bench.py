@@ -428,6 +428,13 @@ def main():
                 [ctx.report_slack(k)[0] for k in range(K)]
 
         e2e_steps(2)
+        # the link alone (context for E: the pipelined step is bound by
+        # max(update, this copy)): one HOST hand-over, host-timed
+        torch.cuda.synchronize()
+        t_h = time.perf_counter()
+        for _ in range(3):
+            put(0)
+        h2d_ms = (time.perf_counter() - t_h) / 3 * 1e3
         barrier()
         e0.record(stream)
         e2e_steps(args.steps)
@@ -441,6 +448,8 @@ def main():
         line["e2e"] = {"value": total_pins / (ms_e2e / 1e3), "unit": "pins/s",
                        "h2d_bytes_per_step": int(sum(x.numel() * 4 for x in res_h + cap_h)),
                        "d2h_bytes_per_step": 32 * K, "ms_per_step": ms_e2e,
+                       "h2d_alone_ms": h2d_ms,
+                       "h2d_alone_gbs": sum(x.numel() * 4 for x in res_h + cap_h) / (h2d_ms / 1e3) / 1e9,
                        "path": "sta_set_rc_values(STA_MEM_HOST, page-locked; step i+1's copy beside "
                                "step i's update) + sta_update_timing + sta_report_slack(STA_MEM_HOST)"}
         for k in range(K):
