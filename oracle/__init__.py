@@ -54,6 +54,9 @@ class _Design(C.Structure):
         ("exc_to", C.c_void_p),
         ("n_clk", C.c_uint32), ("clk_period", C.c_void_p), ("pin_clk", C.c_void_p),
         ("exc_thr_ptr", C.c_void_p), ("exc_seg_ptr", C.c_void_p), ("exc_seg", C.c_void_p),
+        ("n_fn", C.c_uint32), ("fn_pin", C.c_void_p), ("fn_in_ptr", C.c_void_p), ("fn_in", C.c_void_p),
+        ("fn_tt", C.c_void_p), ("arc_when", C.c_void_p),
+        ("n_case", C.c_uint32), ("case_pin", C.c_void_p), ("case_val", C.c_void_p),
     ]
 
 
@@ -159,6 +162,20 @@ class _Marshal:
         if s.n_clk:
             s.clk_period = _p(arr(ck.period, np.float32))
             s.pin_clk = _p(arr(ck.pin_clk, np.uint32))
+        lg = getattr(d, "logic", None)          # O16: case analysis
+        cv = getattr(d, "case", None)
+        if lg is not None and cv is not None and (len(cv.pin) or lg.arc_when is not None):
+            s.n_fn = int(lg.fn_pin.shape[0])
+            s.fn_pin = _p(arr(lg.fn_pin, np.uint32))
+            s.fn_in_ptr = _p(arr(lg.fn_in_ptr, np.uint32))
+            s.fn_in = _p(arr(lg.fn_in, np.uint32))
+            s.fn_tt = _p(arr(lg.fn_tt, np.uint64))
+            if lg.arc_when is not None:
+                s.arc_when = _p(arr(lg.arc_when, np.uint64))
+            s.n_case = int(len(cv.pin))
+            if s.n_case:
+                s.case_pin = _p(arr(cv.pin, np.uint32))
+                s.case_val = _p(arr(cv.val, np.uint8))
         self.s = s
         self.keep = keep
 
@@ -217,6 +234,7 @@ def update(d, corner: int = 0, want_all: bool = True, net_model: str = "elmore",
         raise ValueError("combinational cycle")
     if st == 5:
         raise ValueError("too many exceptions (32), segments (32) or tags (64)")
+    _case_status(st)
     if st:
         raise MemoryError("oracle allocation failed")
     ne = int(n_ep[0])
@@ -224,6 +242,29 @@ def update(d, corner: int = 0, want_all: bool = True, net_model: str = "elmore",
     if want_all:
         out.update(slew=slew[:P], rat=rat[:P], slack=slack[:P])
     return out
+
+
+def _case_status(st):
+    if st == 6:
+        raise ValueError("case analysis: contradictory constants on a pin")
+    if st == 7:
+        raise ValueError("case analysis: a logic function with more than 6 inputs")
+
+
+def case_analysis(d):
+    """O16 alone -> (val[P] uint8: 0, 1, 2 = not constant, off[E] uint8 per
+    canonical arc: net arcs net by net, then cell arcs)."""
+    m = _Marshal(d, 0)
+    E = int(d.net_ptr[-1]) - d.num_nets + d.num_arcs
+    val = np.zeros(max(d.num_pins, 1), np.uint8)
+    off = np.zeros(max(E, 1), np.uint8)
+    lib().orc_case_analysis.restype = C.c_int
+    lib().orc_case_analysis.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+    st = lib().orc_case_analysis(m.ptr, val.ctypes.data, off.ctypes.data)
+    _case_status(st)
+    if st:
+        raise MemoryError("oracle allocation failed")
+    return val[:d.num_pins], off[:E]
 
 
 def update_all_corners(d):

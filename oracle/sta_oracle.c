@@ -76,7 +76,8 @@ static void free_arcs(arcs_t* g) {
   free(g->fi_ptr); free(g->fi); free(g->fo_ptr); free(g->fo);
 }
 
-static int build_arcs(const orc_design* d, arcs_t* g) {
+/* off (optional, per canonical arc id): O16's disabled arcs, left out */
+static int build_arcs_off(const orc_design* d, arcs_t* g, const uint8_t* off) {
   uint32_t P = d->num_pins;
   uint32_t En = d->net_ptr[d->num_nets] - d->num_nets;
   uint32_t E = En + d->num_arcs;
@@ -89,16 +90,20 @@ static int build_arcs(const orc_design* d, arcs_t* g) {
   g->fi = malloc(sizeof(uint32_t) * (E + 1));
   g->fo = malloc(sizeof(uint32_t) * (E + 1));
   if (!g->from || !g->to || !g->cell || !g->fi_ptr || !g->fo_ptr || !g->fi || !g->fo) return 2;
-  uint32_t k = 0;
+  uint32_t k = 0, id = 0;
   for (uint32_t n = 0; n < d->num_nets; n++) {
     uint32_t drv = d->net_pins[d->net_ptr[n]];
-    for (uint32_t j = d->net_ptr[n] + 1; j < d->net_ptr[n + 1]; j++) {
+    for (uint32_t j = d->net_ptr[n] + 1; j < d->net_ptr[n + 1]; j++, id++) {
+      if (off && off[id]) continue;
       g->from[k] = drv; g->to[k] = d->net_pins[j]; g->cell[k] = 0; k++;
     }
   }
-  for (uint32_t a = 0; a < d->num_arcs; a++) {
+  g->En = En = k;
+  for (uint32_t a = 0; a < d->num_arcs; a++, id++) {
+    if (off && off[id]) continue;
     g->from[k] = d->arc_from[a]; g->to[k] = d->arc_to[a]; g->cell[k] = a; k++;
   }
+  g->E = E = k;
   for (uint32_t e = 0; e < E; e++) { g->fi_ptr[g->to[e] + 1]++; g->fo_ptr[g->from[e] + 1]++; }
   for (uint32_t p = 0; p < P; p++) { g->fi_ptr[p + 1] += g->fi_ptr[p]; g->fo_ptr[p + 1] += g->fo_ptr[p]; }
   uint32_t* fi_fill = malloc(sizeof(uint32_t) * (P + 1));
@@ -113,6 +118,8 @@ static int build_arcs(const orc_design* d, arcs_t* g) {
   free(fi_fill); free(fo_fill);
   return 0;
 }
+
+static int build_arcs(const orc_design* d, arcs_t* g) { return build_arcs_off(d, g, NULL); }
 
 /* ---------------------------------------------------------- O2: levelize */
 /* Kahn with a FIFO seeded by in-degree-0 pins in increasing id;
@@ -411,6 +418,84 @@ typedef struct {
 
 static int path_report(const orc_design* d, const arcs_t* g, const uint32_t* order, const double* at,
                        const double* elm, const double* dly, const double* seed, orc_path_req* q);
+
+/* ------------------------------------------------- O16: case analysis */
+/* SURVEY.md §8(f) row 4; SPEC.md:479-486 (apply_case_analysis), PAPER.md:39,
+ * 113 ("case analysis modes"): constants from the case values propagate
+ * forward -- a net's sinks take its driver's constant, a cell output whose
+ * logic function evaluates to one value for every completion of its
+ * non-constant inputs becomes that constant -- in topological order (one
+ * pass is the fixpoint: a function depends only on its inputs); a pin with
+ * two different constants is an error (6).  Disabled: every arc from or to
+ * a constant pin, and every cell arc whose `when` guard is 0 for every
+ * completion of the non-constant inputs of its output's function
+ * (C1-C4). */
+static int fn_eval(const orc_design* d, uint32_t f, const uint8_t* val, uint64_t tt) {
+  /* 0 / 1: tt takes that value on every completion; 2: both values occur */
+  const uint32_t b = d->fn_in_ptr[f], k = d->fn_in_ptr[f + 1] - b;
+  int seen0 = 0, seen1 = 0;
+  for (uint32_t m = 0; m < (1u << k); m++) {
+    int ok = 1;
+    for (uint32_t j = 0; j < k && ok; j++) {
+      const uint8_t v = val[d->fn_in[b + j]];
+      if (v != 2 && v != ((m >> j) & 1u)) ok = 0;
+    }
+    if (!ok) continue;
+    if ((tt >> m) & 1u) seen1 = 1; else seen0 = 1;
+  }
+  return seen0 && seen1 ? 2 : (seen1 ? 1 : 0);
+}
+
+int orc_case_analysis(const orc_design* d, uint8_t* val, uint8_t* off) {
+  const uint32_t P = d->num_pins;
+  arcs_t g; memset(&g, 0, sizeof g);
+  uint32_t* level = malloc(sizeof(uint32_t) * (P + 1));
+  uint32_t* order = malloc(sizeof(uint32_t) * (P + 1));
+  uint32_t* fn_of = malloc(sizeof(uint32_t) * (P + 1));
+  int st = (!level || !order || !fn_of) ? 2 : build_arcs(d, &g);
+  if (!st) st = kahn(d, &g, level, order) ? 1 : 0;
+  for (uint32_t p = 0; !st && p < P; p++) { val[p] = 2; fn_of[p] = ORC_NO_PIN; }
+  for (uint32_t f = 0; !st && f < d->n_fn; f++) {
+    if (d->fn_in_ptr[f + 1] - d->fn_in_ptr[f] > 6) st = 7;
+    else fn_of[d->fn_pin[f]] = f;
+  }
+  for (uint32_t k = 0; !st && k < d->n_case; k++) {
+    const uint32_t p = d->case_pin[k];
+    const uint8_t v = d->case_val[k] ? 1 : 0;
+    if (val[p] != 2 && val[p] != v) st = 6;
+    val[p] = v;
+  }
+  for (uint32_t i = 0; !st && i < P; i++) {
+    const uint32_t v = order[i];
+    for (uint32_t x = g.fi_ptr[v]; x < g.fi_ptr[v + 1]; x++) {
+      const uint32_t e = g.fi[x];
+      if (e >= g.En) continue;                       /* the net arc into a sink */
+      const uint8_t c = val[g.from[e]];
+      if (c == 2) continue;
+      if (val[v] != 2 && val[v] != c) { st = 6; break; }
+      val[v] = c;
+    }
+    if (!st && fn_of[v] != ORC_NO_PIN) {
+      const int c = fn_eval(d, fn_of[v], val, d->fn_tt[fn_of[v]]);
+      if (c != 2) {
+        if (val[v] != 2 && val[v] != c) st = 6;
+        else val[v] = (uint8_t)c;
+      }
+    }
+  }
+  for (uint32_t e = 0; !st && e < g.E; e++) {
+    uint8_t o = val[g.from[e]] != 2 || val[g.to[e]] != 2;
+    if (!o && e >= g.En && d->arc_when) {
+      const uint32_t f = fn_of[g.to[e]];
+      if (f != ORC_NO_PIN && fn_eval(d, f, val, d->arc_when[g.cell[e]]) == 0) o = 1;
+    }
+    off[e] = o;
+  }
+  free_arcs(&g); free(level); free(order); free(fn_of);
+  return st;
+}
+
+static int has_case(const orc_design* d) { return d->n_case || d->arc_when; }
 
 /* --------------------------------------------------------- O4-O8: update */
 /* O15 handoff of one tag's pass at the -through pins (see run_tagged):
@@ -741,7 +826,18 @@ static int run_update(const orc_design* d, double* at, double* slew, double* rat
   const uint32_t P = d->num_pins;
   const double LN9 = log(9.0);
   arcs_t g; memset(&g, 0, sizeof g);
-  if (build_arcs(d, &g)) { free_arcs(&g); return 2; }
+  /* O16: the arcs case analysis disables are left out of the graph */
+  uint8_t* off = NULL;
+  if (has_case(d)) {
+    uint8_t* cval = malloc(P + 1);
+    off = malloc((size_t)(d->net_ptr[d->num_nets] - d->num_nets) + d->num_arcs + 1);
+    const int cst = (!cval || !off) ? 2 : orc_case_analysis(d, cval, off);
+    free(cval);
+    if (cst) { free(off); return cst; }
+  }
+  const int bst = build_arcs_off(d, &g, off);
+  free(off);
+  if (bst) { free_arcs(&g); return 2; }
   uint32_t* level = malloc(sizeof(uint32_t) * (P + 1));
   uint32_t* order = malloc(sizeof(uint32_t) * (P + 1));
   double* load = malloc(sizeof(double) * (d->num_nets + 1));

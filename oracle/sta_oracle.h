@@ -95,7 +95,29 @@ typedef struct {
   const uint32_t* exc_thr_ptr;
   const uint32_t* exc_seg_ptr;
   const uint32_t* exc_seg;
+  /* case analysis (row f4, O16): logic functions of cell
+   * output pins -- pin fn_pin[i] = truth table fn_tt[i] over the pins
+   * fn_in[fn_in_ptr[i] .. fn_in_ptr[i+1]) (<= 6; input j = bit j of the
+   * table index); optional `when` guards per cell arc, arc_when[a] a truth
+   * table over the inputs of fn(arc_to[a]) (all ones: no guard; NULL: no
+   * guards); constants case_pin[k] = case_val[k] (0 / 1).  n_fn = n_case = 0
+   * and arc_when NULL: no case analysis. */
+  uint32_t n_fn;
+  const uint32_t* fn_pin;
+  const uint32_t* fn_in_ptr;
+  const uint32_t* fn_in;
+  const uint64_t* fn_tt;
+  const uint64_t* arc_when;
+  uint32_t n_case;
+  const uint32_t* case_pin;
+  const uint8_t* case_val;
 } orc_design;
+
+/* O16: case analysis alone -- val[P] (0, 1, 2 = not constant) and, per
+ * canonical arc (net arcs net by net, then cell arcs),
+ * off[E] = 1 where the arc is disabled.  Returns 0, 6 on contradictory
+ * constants, 7 on a function with more than 6 inputs, 2 on allocation. */
+int orc_case_analysis(const orc_design* d, uint8_t* val, uint8_t* off);
 
 /* O6: NLDM bilinear lookup, fp64.  `tab` points at
  * index_1[n1], index_2[n2], values[n1][n2]. */

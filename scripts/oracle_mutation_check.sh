@@ -15,7 +15,7 @@ open('oracle/sta_oracle.c', 'w').write(s.replace(a, b, 1))
 PY
   if [ $? -ne 0 ]; then echo "NOT APPLIED (pattern missing): $1"; fail=1; return 1; fi
   rm -f oracle/liboracle.so
-  if timeout 600 python -m pytest tests/test_oracle_lut_rc.py tests/test_oracle_propagation.py tests/test_oracle_steiner.py tests/test_oracle_arnoldi.py tests/test_oracle_exceptions.py -q -x >/dev/null 2>&1; then
+  if timeout 600 python -m pytest tests/test_oracle_lut_rc.py tests/test_oracle_propagation.py tests/test_oracle_steiner.py tests/test_oracle_arnoldi.py tests/test_oracle_exceptions.py tests/test_oracle_case.py -q -x >/dev/null 2>&1; then
     echo "NOT CAUGHT: $1"; fail=1; return 1
   else echo "caught: $1"; fi
 }
@@ -86,4 +86,11 @@ mut '      if (!start || !seg_has(d, m, e, 0, p)) continue;' '      if (!seg_has
 mut '    const uint32_t j = any_thr ? T - 1 - jj : jj;' '    const uint32_t j = jj;'
 mut '  const uint32_t sg = d->exc_thr_ptr[e] + k - m->has_from[e];' '  const uint32_t sg = d->exc_thr_ptr[e] + k;'
 mut 'popc32((uint32_t)tags[j - 1]) > popc32((uint32_t)tags[j])' 'popc32((uint32_t)tags[j - 1]) < popc32((uint32_t)tags[j])'
+# O16 case analysis
+mut '    if ((tt >> m) & 1u) seen1 = 1; else seen0 = 1;' '    if ((tt >> m) & 1u) seen1 = 1;'
+mut '      if (v != 2 && v != ((m >> j) & 1u)) ok = 0;' '      if (v == 1 && v != ((m >> j) & 1u)) ok = 0;'
+mut '      if (val[v] != 2 && val[v] != c) { st = 6; break; }' '      if (val[v] != 2) continue;'
+mut '    uint8_t o = val[g.from[e]] != 2 || val[g.to[e]] != 2;' '    uint8_t o = val[g.from[e]] != 2;'
+mut '      if (f != ORC_NO_PIN && fn_eval(d, f, val, d->arc_when[g.cell[e]]) == 0) o = 1;' '      if (f != ORC_NO_PIN && fn_eval(d, f, val, d->arc_when[g.cell[e]]) == 1) o = 1;'
+mut '    else fn_of[d->fn_pin[f]] = f;' '    else fn_of[d->fn_pin[f]] = ORC_NO_PIN;'
 exit $fail

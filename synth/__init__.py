@@ -7,7 +7,7 @@ recipe".  Both `oracle/` (test infrastructure) and the product binding consume
 the same `Design` objects.
 """
 from .design import (  # noqa: F401
-    Design, Library, RcTree, Constraints,
+    Design, Library, RcTree, Constraints, Logic, CaseValues, truth_table,
     SENSE_POS, SENSE_NEG, SENSE_NON, SENSE_RISE_EDGE, SENSE_FALL_EDGE,
     ROLE_INTERNAL, ROLE_PI, ROLE_PO, ROLE_FF_CK, ROLE_FF_D, NO_PIN,
 )

@@ -160,6 +160,32 @@ class Clocks:
 
 
 @dataclass
+class Logic:
+    """Logic functions of cell outputs and `when` guards of cell arcs (case
+    analysis): pin fn_pin[i] = truth table fn_tt[i] over
+    the pins fn_in[fn_in_ptr[i] .. fn_in_ptr[i+1]) (input j = bit j of the
+    table index, <= 6 inputs); arc_when[a] (optional) a truth table over the
+    inputs of the function of arc_to[a], all ones = no guard."""
+    fn_pin: np.ndarray      # uint32 [F]
+    fn_in_ptr: np.ndarray   # uint32 [F+1]
+    fn_in: np.ndarray       # uint32
+    fn_tt: np.ndarray       # uint64 [F]
+    arc_when: np.ndarray = None   # uint64 [A] or None
+
+
+@dataclass
+class CaseValues:
+    """set_case_analysis constants: pin[k] = val[k] (0 / 1)."""
+    pin: np.ndarray         # uint32 [n]
+    val: np.ndarray         # uint8 [n]
+
+
+def truth_table(fn, k: int) -> int:
+    """the truth table of a Python predicate over k inputs (input j = bit j)"""
+    return sum(1 << m for m in range(1 << k) if fn(*[(m >> j) & 1 for j in range(k)]))
+
+
+@dataclass
 class Design:
     num_pins: int
     pin_cap: np.ndarray      # float32 [P]
@@ -180,6 +206,8 @@ class Design:
     meta: dict = field(default_factory=dict)
     exceptions: Optional["Exceptions"] = None
     clocks: Optional["Clocks"] = None
+    logic: Optional["Logic"] = None
+    case: Optional["CaseValues"] = None
 
     @property
     def num_nets(self) -> int:

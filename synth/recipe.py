@@ -54,6 +54,39 @@ COMB = [
 ]
 MAX_IN = 3
 
+# logic functions of the comb cells (case analysis),
+# inputs in pin order; MUX2 = (A, B, S) -> S ? B : A with its data arcs
+# guarded when(!S) / when(S)
+COMB_FN = {
+    "INV": lambda a: 1 - a, "BUF": lambda a: a,
+    "NAND2": lambda a, b: 1 - (a & b), "NOR2": lambda a, b: 1 - (a | b),
+    "AND2": lambda a, b: a & b, "OR2": lambda a, b: a | b, "XOR2": lambda a, b: a ^ b,
+    "AOI21": lambda a, b, c: 1 - ((a & b) | c), "OAI21": lambda a, b, c: 1 - ((a | b) & c),
+    "MUX2": lambda a, b, s: b if s else a,
+}
+ALL_ONES = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def _logic(ctype, cell_base, n_in, comb_out, cons_cell, cons_j, arc_order):
+    """Logic of the generated comb cells (no RNG: the design is unchanged)."""
+    from .design import Logic, truth_table
+    tts = np.array([truth_table(COMB_FN[name], len(sens)) for name, sens, _ in COMB], np.uint64)
+    n_comb = ctype.shape[0]
+    fn_in_ptr = np.zeros(n_comb + 1, np.int64)
+    fn_in_ptr[1:] = np.cumsum(n_in)
+    fn_in = (np.repeat(cell_base[:n_comb], n_in) + (np.arange(int(fn_in_ptr[-1])) - np.repeat(fn_in_ptr[:-1], n_in)))
+    when = np.full(arc_order.shape[0], ALL_ONES, np.uint64)   # comb arcs (consumer order), then CK -> Q
+    mux = [i for i, (name, _, _) in enumerate(COMB) if name == "MUX2"][0]
+    on_mux = ctype[cons_cell] == mux
+    g_a = np.uint64(truth_table(lambda a, b, s: 1 - s, 3))
+    g_b = np.uint64(truth_table(lambda a, b, s: s, 3))
+    idx = np.nonzero(on_mux & (cons_j == 0))[0]
+    when[idx] = g_a
+    idx = np.nonzero(on_mux & (cons_j == 1))[0]
+    when[idx] = g_b
+    return Logic(comb_out.astype(np.uint32), fn_in_ptr.astype(np.uint32), fn_in.astype(np.uint32),
+                 tts[ctype], when[arc_order])
+
 # name -> (n_cells, pin levels, seed, n_hfn, corners, corner recipe)
 CONFIGS = {
     "c2_tau": dict(n_cells=52_000, levels=60, seed=0x7A2015, n_hfn=0, corners=1),
@@ -363,7 +396,8 @@ def generate(n_cells: int, levels: int, seed: int, n_hfn: int = 0,
         chk_tab=np.full(n_dff, chk_base, np.uint32),
         libs=libs, rc=rcs, cons=cons, name=name,
         meta=dict(seed=seed, n_cells=n_cells, gate_depth=D, n_pi=n_pi, n_po=n_po,
-                  n_dff=n_dff, hfn_fanouts=hfn_fanouts, corner_recipe=corner_recipe))
+                  n_dff=n_dff, hfn_fanouts=hfn_fanouts, corner_recipe=corner_recipe),
+        logic=_logic(ctype, cell_base, n_in, comb_out, cons_cell, cons_j, ao))
 
 
 def lookup_period(name: str) -> Optional[float]:

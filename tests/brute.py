@@ -93,7 +93,7 @@ def const_value(lib: Library, t: int) -> float:
     return float(v.reshape(-1)[0])
 
 
-def path_enumeration_timing(d, elm_of_pin):
+def path_enumeration_timing(d, elm_of_pin, off=None):
     """Frozen-delay brute force.  The library must hold 1x1 (constant) tables so
     that every arc delay is independent of slew and load.  elm_of_pin[p] is the
     net-arc delay into sink p (from elmore_bruteforce).  Returns at, rat,
@@ -102,6 +102,8 @@ def path_enumeration_timing(d, elm_of_pin):
     cons = d.cons
     T = float(cons.period)
     arcs = _fanin_lists(d)
+    if off is not None:                 # case analysis: disabled arcs (canonical order) left out
+        arcs = [a for a, o in zip(arcs, off) if not o]
     P = d.num_pins
     succ = defaultdict(list)
     indeg = np.zeros(P, int)
