@@ -264,6 +264,39 @@ typedef struct {
 } sta_exceptions;
 STA_API sta_status sta_set_exceptions(sta_ctx ctx, const sta_exceptions* ex);
 
+/* Case analysis ("case analysis
+ * modes", apply_case_analysis).  Logic functions of cell
+ * output pins: pin fn_pin[i] = truth table fn_tt[i] over the pins
+ * fn_in[fn_in_ptr[i] .. fn_in_ptr[i+1]) (at most 6; bit m of the table is
+ * the output when input j has the value of bit j of m); arc_when (NULL: no
+ * guards) = per cell arc a truth table over the inputs of the function of
+ * arc_to[a] (all ones: no guard); constants case_pin[k] = case_val[k] (0 /
+ * 1).  Constants are carried over nets (a sink takes its driver's constant)
+ * and through the functions (an output is constant when its function takes
+ * one value for every completion of its non-constant inputs), in
+ * topological order; every arc from or to a constant pin and every cell arc
+ * whose guard is false for every completion is disabled: nothing
+ * propagates over it in either direction (a pin whose fan-in is all
+ * disabled has no arrival, C1-C4).  num_fn = num_case = 0 and
+ * arc_when NULL clear.  Arrays in `mem`, copied; applied at the next
+ * update.  Errors: STA_ERR_ORDER (no graph), STA_ERR_ID (pin out of range),
+ * STA_ERR_CSR (offsets), STA_ERR_ARG (more than 6 inputs, a pin with two
+ * functions, values other than 0 / 1; contradictory constants on a pin are
+ * reported by the next sta_update_timing). */
+typedef struct {
+  sta_mem mem;
+  uint32_t num_fn;
+  const uint32_t* fn_pin;     /* [num_fn] */
+  const uint32_t* fn_in_ptr;  /* [num_fn + 1] */
+  const uint32_t* fn_in;
+  const uint64_t* fn_tt;      /* [num_fn] */
+  const uint64_t* arc_when;   /* [num_arcs] or NULL */
+  uint32_t num_case;
+  const uint32_t* case_pin;   /* [num_case] */
+  const uint8_t* case_val;    /* [num_case] 0 / 1 */
+} sta_case_analysis;
+STA_API sta_status sta_set_case_analysis(sta_ctx ctx, const sta_case_analysis* ca);
+
 /* Multiple ideal clocks (reduced: "cross clock region
  * paths"; the relationship rule of SPEC.md:504).  Clock k:
  * period_ps[k], rising edges at multiples of the period, waveform (0, T/2).

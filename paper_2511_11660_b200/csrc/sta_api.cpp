@@ -256,6 +256,21 @@ struct sta_ctx_s {
   std::vector<const uint4*> exc_ovr_d;
   std::vector<const u32*> exc_thr_dst_d;         // per pass: thr_dst (with -through)
   u32 n_thr = 0;                                 // through slots (pins of -through segments)
+  // row f4: case analysis (sta_set_case_analysis): logic functions, when
+  // guards, constants; applied in prepare() by patched copies of the term
+  // arrays (disabled forward terms read the always-undefined pull pin U,
+  // disabled backward terms carry bit 31, killed sinks bit 31 of the count)
+  std::vector<u32> fn_pin, fn_in_ptr, fn_in, case_pin;
+  std::vector<uint64_t> fn_tt, arc_when;
+  std::vector<uint8_t> case_val;
+  bool case_on = false;
+  u32 undef_pin = kNone;                         // U: internal id of a stage-0 padding pull pin
+  std::vector<uint4> fterm_h;                    // host copies of the plan's term arrays
+  std::vector<u32> fi_src_h, fi_hop_h, arc_term_h;
+  const uint4* fterm_d0 = nullptr;               // the plan's own device arrays
+  const u32 *fi_src_d0 = nullptr, *fi_hop_d0 = nullptr, *sfo_info_d0 = nullptr, *pfo_info_d0 = nullptr;
+  std::vector<uint8_t> case_sink_kill;           // [NS] (prepare)
+  Arena case_arena;
   int net_model = 0;                             // row f1: 0 Elmore, 1 Arnoldi (order arn_q)
   u32 arn_q = 4;
   Arena arn_arena;                               // Arnoldi layout (prepare)
@@ -469,12 +484,15 @@ void build_plan(sta_ctx c) {
     if (!c->is_sink[p]) stage_cnt[c->stage[p]]++;
   c->pull_stage_ptr.assign(S + 1, 0);
   for (u32 s = 0; s < S; ++s)
-    c->pull_stage_ptr[s + 1] = c->pull_stage_ptr[s] + (stage_cnt[s] + sta::kChunk - 1) / sta::kChunk * sta::kChunk;
+    // (stage 0 keeps at least one padding id: the always-undefined source U
+    // that case analysis points its disabled forward terms at)
+    c->pull_stage_ptr[s + 1] = c->pull_stage_ptr[s] + (stage_cnt[s] + (s == 0) + sta::kChunk - 1) / sta::kChunk * sta::kChunk;
   NP = c->pull_stage_ptr[S];
   c->NP = NP;
   c->NS = NS;
   c->Pi = NP + NS;
   c->n0 = S ? c->pull_stage_ptr[1] : 0;
+  c->undef_pin = S ? c->pull_stage_ptr[1] - 1 : kNone;
   c->int_of_user.assign(P, kNone);
   c->user_of_int.assign(c->Pi, kNone);
   {
@@ -735,6 +753,11 @@ void build_plan(sta_ctx c) {
         }
         fwu_stage.push_back(s);
       }
+      // U: a seed slot without a seed, so its record is written (undefined)
+      // by every update
+      for (u32 x = 0; x < sta::kFwdUnitTerms; ++x)
+        fterm.push_back(make_uint4(sta::kSeedMark, 0, 0, x == 0 ? c->undef_pin : kNone));
+      fwu_stage.push_back(s);
       continue;
     }
     const u32 fcap = unit_cap(fi_p[p1] - fi_p[p0], sta::kFwdUnitTerms, fwd_warps);
@@ -917,6 +940,10 @@ void build_plan(sta_ctx c) {
   t.pfo_dst = g.upload(pfo_dst, s);
   t.pfo_info = g.upload(pfo_info, s);
   t.fterm = g.upload(fterm, s);
+  c->fterm_h = fterm;
+  c->fi_src_h = fi_src;
+  c->fi_hop_h = fi_hop;
+  c->arc_term_h = arc_term;
   t.n_fwu = c->n_fwu;
   t.bwu = g.upload(bwu, s);
   t.n_bwu = c->n_bwu;
@@ -926,8 +953,69 @@ void build_plan(sta_ctx c) {
   t.heavy_base = g.upload(heavy_base, s);
   t.int_of_user = g.upload(c->int_of_user, s);
   t.drv_of_net = g.upload(c->drv_of_net, s);
+  c->fterm_d0 = t.fterm;
+  c->fi_src_d0 = t.fi_src;
+  c->fi_hop_d0 = t.fi_hop;
+  c->sfo_info_d0 = t.sfo_info;
+  c->pfo_info_d0 = t.pfo_info;
+  if (c->n_dslots >= (1u << 28)) fail(STA_ERR_ARG, "forward plan too large (%u delay slots)", c->n_dslots);
   ck(cudaStreamSynchronize(s), "plan upload");
   tm.mark("plan: upload");
+}
+
+// Row f4: case analysis (the oracle's O16; DESIGN.md
+// C1-C4).  Constants from the case values are carried over nets (a sink
+// takes its driver's constant) and through the cells' logic functions (an
+// output is constant when its function takes one value for every completion
+// of its non-constant inputs), pull pins in internal order (gate stage
+// order: every input of a stage-s pin is final before it); a pin with two
+// constants is an error.  Disabled: cell arcs from / to a constant pin or
+// whose when guard is false for every completion, and net arcs from / to a
+// constant pin ("killed" sinks).  Returns the disabled cell arcs.
+std::vector<uint8_t> case_analysis(sta_ctx c, std::vector<uint8_t>& kill) {
+  const u32 P = c->P, NP = c->NP;
+  std::vector<uint8_t> val(P, 2), arc_off(c->A, 0);
+  std::vector<u32> fn_of(P, kNone);
+  for (u32 f = 0; f + 1 < c->fn_in_ptr.size(); ++f) fn_of[c->fn_pin[f]] = f;
+  auto eval = [&](u32 f, uint64_t tt) {      // 0 / 1: one value on every completion; 2: both
+    const u32 b = c->fn_in_ptr[f], k = c->fn_in_ptr[f + 1] - b;
+    bool s0 = false, s1 = false;
+    for (u32 m = 0; m < (1u << k); ++m) {
+      bool ok = true;
+      for (u32 j = 0; j < k && ok; ++j) {
+        const uint8_t v = val[c->fn_in[b + j]];
+        if (v != 2 && v != ((m >> j) & 1u)) ok = false;
+      }
+      if (!ok) continue;
+      if ((tt >> m) & 1u) s1 = true; else s0 = true;
+    }
+    return s0 && s1 ? 2 : (s1 ? 1 : 0);
+  };
+  auto pin_const = [&](u32 p, uint8_t v) {
+    if (val[p] != 2 && val[p] != v) fail(STA_ERR_ARG, "case analysis: contradictory constants on pin %u", p);
+    val[p] = v;
+  };
+  for (size_t k = 0; k < c->case_pin.size(); ++k) pin_const(c->case_pin[k], c->case_val[k] ? 1 : 0);
+  for (u32 i = 0; i < NP; ++i) {
+    const u32 p = c->user_of_int[i];
+    if (p == kNone) continue;
+    if (fn_of[p] != kNone) {
+      const int v = eval(fn_of[p], c->fn_tt[fn_of[p]]);
+      if (v != 2) pin_const(p, (uint8_t)v);
+    }
+    if (val[p] != 2)
+      for (u32 k = c->sink_ptr[i]; k < c->sink_ptr[i + 1]; ++k) pin_const(c->user_of_int[NP + k], val[p]);
+  }
+  kill.assign(c->NS, 0);
+  for (u32 k = 0; k < c->NS; ++k)
+    kill[k] = val[c->user_of_int[NP + k]] != 2 || val[c->user_of_int[c->sink_drv[k]]] != 2;
+  for (u32 a = 0; a < c->A; ++a) {
+    const u32 u = c->arc_from[a], v = c->arc_to[a];
+    bool off = val[u] != 2 || val[v] != 2;
+    if (!off && !c->arc_when.empty() && fn_of[v] != kNone && eval(fn_of[v], c->arc_when[a]) == 0) off = true;
+    arc_off[a] = off;
+  }
+  return arc_off;
 }
 
 // RC tree topology: validation and per-net schedules (tree scope)
@@ -1257,6 +1345,57 @@ void prepare(sta_ctx c) {
                         nfo > 1 ? info[f0 + 1] : 0);
     }
   };
+  // row f4: case analysis -- patched copies of the term arrays: a disabled
+  // cell arc's forward terms read U (always undefined, no net hop), its
+  // backward terms carry bit 31 of their info word (not live); a sink whose
+  // net arc is disabled carries bit 31 of its fan-out count (killed: no
+  // arrival, no required-time contribution to its driver)
+  {
+    sta::Topo& tp = c->topo;
+    c->case_arena.release();
+    tp.fterm = c->fterm_d0;
+    tp.fi_src = c->fi_src_d0;
+    tp.fi_hop = c->fi_hop_d0;
+    tp.sfo_info = c->sfo_info_d0;
+    tp.pfo_info = c->pfo_info_d0;
+  }
+  std::vector<u32> sfo_info_c, pfo_info_c;
+  const std::vector<u32>* sfo_info = &c->sfo_info;
+  const std::vector<u32>* pfo_info = &c->pfo_info;
+  std::vector<uint8_t> kill;
+  if (c->case_on) {
+    const std::vector<uint8_t> off = case_analysis(c, kill);
+    std::vector<uint8_t> slot_off(c->n_dslots + 1, 0);
+    std::vector<uint4> ft(c->fterm_h);
+    std::vector<u32> fs(c->fi_src_h), fh(c->fi_hop_h);
+    for (u32 a = 0; a < c->A; ++a) {
+      if (!off[a] || c->arc_term_h[a] == kNone) continue;
+      const u32 nt = c->arc_sense[a] == STA_NON_UNATE ? 2u : 1u;
+      for (u32 q = 0; q < nt; ++q) {
+        const u32 e = c->arc_term_h[a] + q, sl = c->fi_slot_h[e];
+        fs[e] = c->undef_pin;
+        fh[e] = kNone;
+        slot_off[sl] = 1;
+        if (sl < ft.size()) {
+          ft[sl].x = c->undef_pin;
+          ft[sl].y = kNone;
+        }
+      }
+    }
+    sfo_info_c = c->sfo_info;
+    pfo_info_c = c->pfo_info;
+    for (u32& x : sfo_info_c) if (slot_off[x >> 3]) x |= 0x80000000u;
+    for (u32& x : pfo_info_c) if (slot_off[x >> 3]) x |= 0x80000000u;
+    sfo_info = &sfo_info_c;
+    pfo_info = &pfo_info_c;
+    sta::Topo& tp = c->topo;
+    Arena& ca = c->case_arena;
+    tp.fterm = ca.upload(ft, c->stream);
+    tp.fi_src = ca.upload(fs, c->stream);
+    tp.fi_hop = ca.upload(fh, c->stream);
+    tp.sfo_info = ca.upload(sfo_info_c, c->stream);
+    tp.pfo_info = ca.upload(pfo_info_c, c->stream);
+  }
   std::vector<uint4> sinkfo(2 * (size_t)c->NS), pullfo(2 * (size_t)c->NP);
   for (u32 k = 0; k < c->NS; ++k) {
     // driver field bit 31: the driver has its own endpoint or direct cell
@@ -1264,9 +1403,10 @@ void prepare(sta_ctx c) {
     const u32 v = c->sink_drv[k];
     const bool work = pin_ep[v] != kNone || c->pfo_p[v + 1] != c->pfo_p[v];
     fo_rec(&sinkfo[2 * (size_t)k], v | (work ? 0x80000000u : 0u), pin_ep[c->NP + k], c->sfo_p, c->sfo_dst,
-           c->sfo_info, k);
+           *sfo_info, k);
+    if (!kill.empty() && kill[k]) sinkfo[2 * (size_t)k].y |= 0x80000000u;
   }
-  for (u32 i = 0; i < c->NP; ++i) fo_rec(&pullfo[2 * (size_t)i], 0, pin_ep[i], c->pfo_p, c->pfo_dst, c->pfo_info, i);
+  for (u32 i = 0; i < c->NP; ++i) fo_rec(&pullfo[2 * (size_t)i], 0, pin_ep[i], c->pfo_p, c->pfo_dst, *pfo_info, i);
   // stage-0 seeds
   std::vector<u32> seed(c->n0, kNone);
   for (u32 i = 0; i < c->n0; ++i) {
@@ -2248,6 +2388,56 @@ sta_status sta_set_exceptions(sta_ctx c, const sta_exceptions* ex) {
     c->exc_seg_ptr = std::move(sp);
     c->exc_seg = std::move(sg);
     c->prepared = false;                     // tags, seeds, overrides and merged arrays next update
+    invalidate_graph(c);
+  });
+}
+
+sta_status sta_set_case_analysis(sta_ctx c, const sta_case_analysis* ca) {
+  return guard(c, [&] {
+    Nvtx nvtx_range("sta_set_case_analysis");
+    if (!ca) fail(STA_ERR_ARG, "case analysis NULL");
+    if (!c->has_graph) fail(STA_ERR_ORDER, "sta_set_case_analysis before sta_load_graph");
+    std::vector<u32> fp, fptr, fin, cp;
+    std::vector<uint64_t> tt, when;
+    std::vector<uint8_t> cv;
+    const u32 F = ca->num_fn;
+    if (F) {
+      fp = fetch(ca->fn_pin, F, ca->mem, "fn_pin", c->stream);
+      fptr = fetch(ca->fn_in_ptr, F + 1, ca->mem, "fn_in_ptr", c->stream);
+      if (fptr[0] != 0) fail(STA_ERR_CSR, "fn_in_ptr must start at 0");
+      for (u32 f = 0; f < F; ++f) {
+        if (fptr[f + 1] < fptr[f]) fail(STA_ERR_CSR, "function %u: offsets not monotone", f);
+        if (fptr[f + 1] - fptr[f] > 6) fail(STA_ERR_ARG, "function %u: %u inputs (at most 6)", f, fptr[f + 1] - fptr[f]);
+      }
+      fin = fetch(ca->fn_in, fptr[F], ca->mem, "fn_in", c->stream);
+      tt = fetch(ca->fn_tt, F, ca->mem, "fn_tt", c->stream);
+      std::vector<uint8_t> has(c->P, 0);
+      for (u32 p : fp) {
+        if (p >= c->P) fail(STA_ERR_ID, "function pin %u out of range", p);
+        if (has[p]) fail(STA_ERR_ARG, "pin %u: two logic functions", p);
+        has[p] = 1;
+      }
+      for (u32 p : fin) if (p >= c->P) fail(STA_ERR_ID, "function input pin %u out of range", p);
+    } else {
+      fptr.assign(1, 0);
+    }
+    if (ca->arc_when) when = fetch(ca->arc_when, c->A, ca->mem, "arc_when", c->stream);
+    if (ca->num_case) {
+      cp = fetch(ca->case_pin, ca->num_case, ca->mem, "case_pin", c->stream);
+      cv = fetch(ca->case_val, ca->num_case, ca->mem, "case_val", c->stream);
+      for (u32 p : cp) if (p >= c->P) fail(STA_ERR_ID, "case pin %u out of range", p);
+      for (uint8_t v : cv) if (v > 1) fail(STA_ERR_ARG, "case value %u (0 or 1)", v);
+    }
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    c->fn_pin = std::move(fp);
+    c->fn_in_ptr = std::move(fptr);
+    c->fn_in = std::move(fin);
+    c->fn_tt = std::move(tt);
+    c->arc_when = std::move(when);
+    c->case_pin = std::move(cp);
+    c->case_val = std::move(cv);
+    c->case_on = !c->case_pin.empty() || !c->arc_when.empty();
+    c->prepared = false;
     invalidate_graph(c);
   });
 }

@@ -1290,8 +1290,18 @@ __device__ __forceinline__ void bwd_arc(const Q4& a, uint32_t info, const float4
   }
 }
 
+// delay slot of a backward term's info word (bit 31: the arc is disabled by
+// case analysis, row f4)
+constexpr uint32_t kSlotMask = 0x0FFFFFFFu;
+// row f4: the net arc into sink k is disabled by case analysis (bit 31 of the
+// fan-out count in its record)
+__device__ __forceinline__ bool sink_killed(const Topo& t, uint32_t k) {
+  return (int)__ldg(&t.sinkfo[2 * (size_t)k].y) < 0;
+}
+
 // does the arc use some defined input component (otherwise nothing to wait for)
 __device__ __forceinline__ bool arc_live(uint32_t info, const Q4& a) {
+  if (info >> 31) return false;              // row f4: disabled by case analysis
   const uint32_t sense = info & 7u;
   const bool r_used = primary_irf(sense, 0) == 0 || primary_irf(sense, 1) == 0;
   const bool f_used = primary_irf(sense, 0) == 1 || primary_irf(sense, 1) == 1;
@@ -1346,11 +1356,12 @@ __device__ __forceinline__ FoPre bwd_pre(const CornerDev& c, const uint4& fa, co
   const uint4 ok = make_uint4(0, ep, 0, ep);
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
   FoPre p{z, z, ok, ok};
-  if (fa.w == kNone && fa.y) {
-    p.d0 = __ldcg(c.tdel + (fb.y >> 3));
+  const uint32_t nfo = fa.y & 0x7FFFFFFFu;   // (bit 31: a killed sink, case analysis)
+  if (fa.w == kNone && nfo) {
+    p.d0 = __ldcg(c.tdel + ((fb.y >> 3) & kSlotMask));
     p.e0 = ld_ll(c.rat_ll + 2 * (size_t)fb.x);
     p.l0 = ld_ll(c.rat_ll + 2 * (size_t)fb.x + 1);
-    if (fa.y > 1) p.d1 = __ldcg(c.tdel + (fb.w >> 3));
+    if (nfo > 1) p.d1 = __ldcg(c.tdel + ((fb.w >> 3) & kSlotMask));
   }
   return p;
 }
@@ -1370,7 +1381,7 @@ __device__ __forceinline__ void bwd_pin(const Topo& t, const CornerDev& c, const
                                         const uint4& fa, const uint4& fb, FoPre p,
                                         const uint32_t* __restrict__ dst_csr, const uint32_t* __restrict__ info_csr,
                                         const Q4& a, const Q4& s, Q4& r) {
-  const uint32_t nfo = fa.y;
+  const uint32_t nfo = fa.y & 0x7FFFFFFFu;
   uint32_t f = 0;
   if (fa.w != kNone) {
     seed4(t, L, fb.x, fb.y, a, s, r, fa.w);
@@ -1396,7 +1407,7 @@ __device__ __forceinline__ void bwd_pin(const Topo& t, const CornerDev& c, const
     const uint32_t w2 = __ldg(dst_csr + fa.z + f);
     const uint4* pw = c.rat_ll + 2 * (size_t)w2;
     uint4 we = ld_ll(pw), wl = ld_ll(pw + 1);
-    const float4 d4 = __ldcg(c.tdel + (info >> 3));
+    const float4 d4 = __ldcg(c.tdel + ((info >> 3) & kSlotMask));
     spin_pair(pw, we, wl, ep);
     bwd_arc(a, info, d4, we, wl, r);
   }
@@ -1464,7 +1475,7 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
       // complete during the wait instead of adding a round trip of their own
       // (a pin's required-time words are always written, live arc or not)
 #if STA_BWD_SPIN_FIRST
-      if (fa.w == kNone && fa.y) spin_pair(c.rat_ll + 2 * (size_t)fb.x, pre.e0, pre.l0, ep);
+      if (fa.w == kNone && (fa.y & 0x7FFFFFFFu)) spin_pair(c.rat_ll + 2 * (size_t)fb.x, pre.e0, pre.l0, ep);
 #endif
       Q4 a = at_v, s = sl_v, r = undef_rat();
       Q4 nd{{elm, elm, elm, elm}};           // the net arc's delay per component
@@ -1477,6 +1488,7 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
       } else {
         hop_at(a, elm);                      // the sink's own arrival (slews unused)
       }
+      if ((int)fa.y < 0) a = undef_at();    // row f4: net arc disabled by case analysis
       uint32_t tsl = kNone;
       if constexpr (THR) {                   // row f4: a -through sink
         tsl = __ldg(t.thr_sink + k);
@@ -1491,7 +1503,7 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
       if (fa.w != kNone) write_ep(c, fa.w, sk);
 #pragma unroll
       for (int q = 0; q < 4; ++q)            // through the net arc (edges the forward used)
-        if (fin(at_v.v[q])) acc.v[q] = __fsub_rn(r.v[q], nd.v[q]);
+        if (fin(at_v.v[q]) && (int)fa.y >= 0) acc.v[q] = __fsub_rn(r.v[q], nd.v[q]);
     }
     // merge the sinks of each driver (contiguous lanes) into its first lane:
     // log-step doubling (max / min are idempotent: overlapping windows are
@@ -1871,6 +1883,7 @@ __global__ void thr_capture_kernel(Topo t, const __grid_constant__ Batch B) {
   load_rec(c, dv, at, sl);
   if (t.net_model == 1) arn_net_hop(at, sl, c.elm[k], c.arn_lam[dv], c.arn_res[k], true);
   else net_hop(at, sl, c.elm[k]);
+  if (sink_killed(t, k)) at = sl = undef_at();
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     float* ha = thr_word(c.thr_hat, t, d, e.y, q);
@@ -1910,6 +1923,7 @@ __global__ void merge_tag_kernel(Topo t, CornerDev c, int first) {
     load_rec(c, dv, at, sl);
     if (t.net_model == 1) arn_net_hop(at, sl, c.elm[k], c.arn_lam[dv], c.arn_res[k], true);
     else net_hop(at, sl, c.elm[k]);
+    if (sink_killed(t, k)) at = sl = undef_at();
     if (t.thr_sink) thr_sink4(t, c, k, at, sl);
     rt = c.rat[i];
   }
@@ -1961,6 +1975,7 @@ __global__ void gather_pins_kernel(Topo t, CornerDev c, int what, float4* __rest
   load_rec(c, t.sink_drv[k], at, sl);
   if (t.net_model == 1) arn_net_hop(at, sl, c.elm[k], c.arn_lam[t.sink_drv[k]], c.arn_res[k], true);
   else net_hop(at, sl, c.elm[k]);
+  if (sink_killed(t, k)) at = sl = undef_at();
   dst[p] = to_f4(what == 0 ? at : sl);
 }
 
@@ -2127,7 +2142,9 @@ __global__ void __launch_bounds__(kThreads) path_ep_kernel(Topo t, CornerDev c, 
   seed4(t, c.lut, er.chk_tab, er.po, at, sl, sd);
   const float S[2] = {sd.v[el * 2], sd.v[el * 2 + 1]};
   uint32_t h0 = 0, h1 = 0;
-  const uint32_t n0 = fin(S[0]) ? pa.cnt[(size_t)src * 2] : 0, n1 = fin(S[1]) ? pa.cnt[(size_t)src * 2 + 1] : 0;
+  const bool dead = sink && sink_killed(t, i - t.NP);   // case analysis: no path into the endpoint
+  const uint32_t n0 = fin(S[0]) && !dead ? pa.cnt[(size_t)src * 2] : 0;
+  const uint32_t n1 = fin(S[1]) && !dead ? pa.cnt[(size_t)src * 2 + 1] : 0;
   auto slack_of_e = [&](uint32_t rf, uint32_t j) {
     const float a0 = pa.lists[((size_t)src * 2 + rf) * m + j].a;
     const float a = sink ? __fadd_rn(a0, em) : a0;

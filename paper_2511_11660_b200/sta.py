@@ -30,7 +30,7 @@ EXPORTS = ["sta_create", "sta_destroy", "sta_last_error", "sta_status_string", "
            "sta_update_timing", "sta_report_slack", "sta_get_timing", "sta_get_rc",
            "sta_get_levels", "sta_get_info", "sta_synchronize", "sta_profile_enable",
            "sta_profile_read", "sta_report_paths", "sta_build_steiner", "sta_set_net_model",
-           "sta_set_exceptions", "sta_set_clocks"]
+           "sta_set_exceptions", "sta_set_clocks", "sta_set_case_analysis"]
 
 
 class StaError(RuntimeError):
@@ -76,6 +76,12 @@ class PathSet(C.Structure):
                 ("n_pins", C.c_uint32), ("path_ptr", C.c_void_p), ("path_pin", C.c_void_p),
                 ("path_rf", C.c_void_p), ("path_at", C.c_void_p), ("path_slack", C.c_void_p),
                 ("path_ep", C.c_void_p)]
+
+
+class CaseDesc(C.Structure):
+    _fields_ = [("mem", C.c_int), ("num_fn", C.c_uint32), ("fn_pin", C.c_void_p), ("fn_in_ptr", C.c_void_p),
+                ("fn_in", C.c_void_p), ("fn_tt", C.c_void_p), ("arc_when", C.c_void_p),
+                ("num_case", C.c_uint32), ("case_pin", C.c_void_p), ("case_val", C.c_void_p)]
 
 
 class ExceptionsDesc(C.Structure):
@@ -135,6 +141,7 @@ def lib():
             "sta_set_net_model": (i32, [vp, i32, u32]),
             "sta_set_exceptions": (i32, [vp, C.POINTER(ExceptionsDesc)]),
             "sta_set_clocks": (i32, [vp, C.POINTER(ClocksDesc)]),
+            "sta_set_case_analysis": (i32, [vp, C.POINTER(CaseDesc)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -153,7 +160,8 @@ def _torch_dtypes(dtype):
     import torch
     return {np.float32: (torch.float32,), np.int32: (torch.int32,), np.uint8: (torch.uint8,),
             np.uint32: tuple(t for t in (getattr(torch, "uint32", None), torch.int32) if t is not None),
-            np.float64: (torch.float64,)}[np.dtype(dtype).type]
+            np.float64: (torch.float64,),
+            np.uint64: tuple(t for t in (getattr(torch, "uint64", None), torch.int64) if t is not None)}[np.dtype(dtype).type]
 
 
 class _Args:
@@ -344,6 +352,24 @@ class Context:
         e.mem = a.kind
         self._check(self._L.sta_set_exceptions(self.h, C.byref(e)))
 
+    def set_case_analysis(self, fn_pin=(), fn_in_ptr=(0,), fn_in=(), fn_tt=(), arc_when=None,
+                          case_pin=(), case_val=()):
+        """Case analysis (sta_set_case_analysis): logic functions, optional
+        when guards, constants; no arguments clear."""
+        a = _Args(self.device)
+        k = CaseDesc()
+        k.num_fn = len(fn_pin)
+        k.fn_pin = a.ptr(fn_pin, np.uint32)
+        k.fn_in_ptr = a.ptr(fn_in_ptr, np.uint32) if k.num_fn else None
+        k.fn_in = a.ptr(fn_in, np.uint32)
+        k.fn_tt = a.ptr(fn_tt, np.uint64)
+        k.arc_when = a.ptr(arc_when, np.uint64) if arc_when is not None else None
+        k.num_case = len(case_pin)
+        k.case_pin = a.ptr(case_pin, np.uint32)
+        k.case_val = a.ptr(case_val, np.uint8)
+        k.mem = a.kind
+        self._check(self._L.sta_set_case_analysis(self.h, C.byref(k)))
+
     def set_clocks(self, period_ps=(), pin_clk=None):
         """Multiple ideal clocks (sta_set_clocks); no arguments: one clock."""
         a = _Args(self.device)
@@ -498,6 +524,9 @@ def load_design(ctx: Context, d, corners=None, device_rc: bool = False, device_g
     ck = getattr(d, "clocks", None)
     if ck is not None and len(ck.period):
         ctx.set_clocks(ck.period, ck.pin_clk)
+    lg, cv = getattr(d, "logic", None), getattr(d, "case", None)
+    if lg is not None and cv is not None:
+        ctx.set_case_analysis(lg.fn_pin, lg.fn_in_ptr, lg.fn_in, lg.fn_tt, lg.arc_when, cv.pin, cv.val)
     ex = getattr(d, "exceptions", None)
     if ex is not None and ex.num:
         if getattr(ex, "has_through", False):
