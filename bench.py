@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--through", action="store_true",
                     help="row f4: --exceptions plus two -through exceptions (a false path through 0.2%% "
                          "of the pins, a multicycle through two ordered segments): up to 18 tags")
+    ap.add_argument("--case", action="store_true",
+                    help="row f4: case analysis, every MUX2 select pinned (alternately 0 / 1): one data arc "
+                         "of every mux disabled by its when guard, the select arcs by the constants")
     return ap.parse_args()
 
 
@@ -111,6 +114,19 @@ def bench_through(d):
     items.append((1, 2.0, [], [], [list(rng.choice(P, P // 200, replace=False)),
                                    list(rng.choice(P, P // 200, replace=False))]))
     return Exceptions.build(items)
+
+
+def bench_case(d):
+    """Row f4 case-analysis workload: the select pin of every MUX2 cell
+    pinned, alternately to 0 and 1 (the recipe's own logic functions)."""
+    import synth
+    from synth.design import CaseValues
+    lg = d.logic
+    k = np.diff(lg.fn_in_ptr.astype(np.int64))
+    tt = synth.truth_table(lambda a, b, s: b if s else a, 3)
+    mux = np.nonzero((lg.fn_tt == np.uint64(tt)) & (k == 3))[0]
+    sel = lg.fn_in[lg.fn_in_ptr[mux].astype(np.int64) + 2]
+    return CaseValues(sel.astype(np.uint32), (np.arange(sel.size) & 1).astype(np.uint8))
 
 
 def measured_peaks():
@@ -296,6 +312,8 @@ def main():
     K = len(mine)
     ctx = pkg.Context(local, K, stream=stream.cuda_stream)
     t0 = time.perf_counter()
+    if args.case:
+        d.case = bench_case(d)
     if args.through:
         d.exceptions = bench_through(d)
     elif args.exceptions:
@@ -368,7 +386,7 @@ def main():
             "scaling": "strong" if name == "c5_multicorner" else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": dict(config_line(name, info, K, world, gen_s, load_s), net_model=args.net_model,
-                           exceptions=bool(args.exceptions or args.through), through=bool(args.through), dist_backend=args.dist_backend if world > 1 else None),
+                           exceptions=bool(args.exceptions or args.through), through=bool(args.through), case_constants=int(len(d.case.pin)) if args.case else 0, dist_backend=args.dist_backend if world > 1 else None),
             "gpu_launches": info["kernels_per_update"] * args.steps,
             "clocks": clk, "wns_tns": [float(x) for x in res_own[0]]}
     if name == "c5_multicorner":

@@ -222,8 +222,8 @@ STA_API sta_status sta_set_net_model(sta_ctx ctx, sta_net_model model, uint32_t 
  * paths, multi-cycle paths, case analysis, and cross clock region paths ...
  * complicate the data structures and states in timing propagation"; PAPER.md:
  * 250: "-through patterns that eliminate only paths that go through a
- * predefined pin sequence"; the tag model of SPEC.md:465-509; no case
- * analysis).  Exception i: kind[i] (STA_EXC_*), value[i] (multicycle:
+ * predefined pin sequence"; the tag model of SPEC.md:465-509; case
+ * analysis: sta_set_case_analysis).  Exception i: kind[i] (STA_EXC_*), value[i] (multicycle:
  * N >= 1; max / min delay: ps), startpoint pins from_pins[from_ptr[i] ..
  * from_ptr[i+1]), endpoint pins to_pins[to_ptr[i] .. to_ptr[i+1]) (an empty
  * list: any) and, if thr_ptr is not NULL, the ordered -through segments

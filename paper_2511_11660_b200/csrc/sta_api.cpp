@@ -958,7 +958,6 @@ void build_plan(sta_ctx c) {
   c->fi_hop_d0 = t.fi_hop;
   c->sfo_info_d0 = t.sfo_info;
   c->pfo_info_d0 = t.pfo_info;
-  if (c->n_dslots >= (1u << 28)) fail(STA_ERR_ARG, "forward plan too large (%u delay slots)", c->n_dslots);
   ck(cudaStreamSynchronize(s), "plan upload");
   tm.mark("plan: upload");
 }
@@ -1347,9 +1346,10 @@ void prepare(sta_ctx c) {
   };
   // row f4: case analysis -- patched copies of the term arrays: a disabled
   // cell arc's forward terms read U (always undefined, no net hop), its
-  // backward terms carry bit 31 of their info word (not live); a sink whose
-  // net arc is disabled carries bit 31 of its fan-out count (killed: no
-  // arrival, no required-time contribution to its driver)
+  // backward terms carry sense 7 (not live); a sink whose net arc is
+  // disabled (a constant sink: its cell fan-out is disabled too) gets no
+  // fan-out terms and bit 31 of its CSR start (killed: no arrival, no
+  // required-time contribution to its driver)
   {
     sta::Topo& tp = c->topo;
     c->case_arena.release();
@@ -1384,8 +1384,8 @@ void prepare(sta_ctx c) {
     }
     sfo_info_c = c->sfo_info;
     pfo_info_c = c->pfo_info;
-    for (u32& x : sfo_info_c) if (slot_off[x >> 3]) x |= 0x80000000u;
-    for (u32& x : pfo_info_c) if (slot_off[x >> 3]) x |= 0x80000000u;
+    for (u32& x : sfo_info_c) if (slot_off[x >> 3]) x |= 7u;    // sense 7: not live
+    for (u32& x : pfo_info_c) if (slot_off[x >> 3]) x |= 7u;
     sfo_info = &sfo_info_c;
     pfo_info = &pfo_info_c;
     sta::Topo& tp = c->topo;
@@ -1404,7 +1404,12 @@ void prepare(sta_ctx c) {
     const bool work = pin_ep[v] != kNone || c->pfo_p[v + 1] != c->pfo_p[v];
     fo_rec(&sinkfo[2 * (size_t)k], v | (work ? 0x80000000u : 0u), pin_ep[c->NP + k], c->sfo_p, c->sfo_dst,
            *sfo_info, k);
-    if (!kill.empty() && kill[k]) sinkfo[2 * (size_t)k].y |= 0x80000000u;
+    if (!kill.empty() && kill[k]) {           // a constant sink: no arrival, no fan-out
+      uint4* r = &sinkfo[2 * (size_t)k];
+      r[0].y = 0;
+      r[0].z |= 0x80000000u;
+      if (r[0].w == kNone) r[1] = make_uint4(kNone, 0, kNone, 0);
+    }
   }
   for (u32 i = 0; i < c->NP; ++i) fo_rec(&pullfo[2 * (size_t)i], 0, pin_ep[i], c->pfo_p, c->pfo_dst, *pfo_info, i);
   // stage-0 seeds

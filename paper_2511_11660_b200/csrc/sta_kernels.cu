@@ -1290,21 +1290,18 @@ __device__ __forceinline__ void bwd_arc(const Q4& a, uint32_t info, const float4
   }
 }
 
-// delay slot of a backward term's info word (bit 31: the arc is disabled by
-// case analysis, row f4)
-constexpr uint32_t kSlotMask = 0x0FFFFFFFu;
 // row f4: the net arc into sink k is disabled by case analysis (bit 31 of the
-// fan-out count in its record)
+// CSR start in its record; such a sink is constant, so its fan-out count is 0)
 __device__ __forceinline__ bool sink_killed(const Topo& t, uint32_t k) {
-  return (int)__ldg(&t.sinkfo[2 * (size_t)k].y) < 0;
+  return (int)__ldg(&t.sinkfo[2 * (size_t)k].z) < 0;
 }
 
 // does the arc use some defined input component (otherwise nothing to wait for)
 __device__ __forceinline__ bool arc_live(uint32_t info, const Q4& a) {
-  if (info >> 31) return false;              // row f4: disabled by case analysis
+  // input edges the sense uses: r by POS / NEG / RISE_EDGE, f by POS / NEG /
+  // FALL_EDGE; sense 7 (an arc disabled by case analysis, row f4) uses none
   const uint32_t sense = info & 7u;
-  const bool r_used = primary_irf(sense, 0) == 0 || primary_irf(sense, 1) == 0;
-  const bool f_used = primary_irf(sense, 0) == 1 || primary_irf(sense, 1) == 1;
+  const bool r_used = (0x0Bu >> sense) & 1u, f_used = (0x13u >> sense) & 1u;
   return (r_used && (fin(a.v[0]) || fin(a.v[2]))) || (f_used && (fin(a.v[1]) || fin(a.v[3])));
 }
 
@@ -1356,12 +1353,11 @@ __device__ __forceinline__ FoPre bwd_pre(const CornerDev& c, const uint4& fa, co
   const uint4 ok = make_uint4(0, ep, 0, ep);
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
   FoPre p{z, z, ok, ok};
-  const uint32_t nfo = fa.y & 0x7FFFFFFFu;   // (bit 31: a killed sink, case analysis)
-  if (fa.w == kNone && nfo) {
-    p.d0 = __ldcg(c.tdel + ((fb.y >> 3) & kSlotMask));
+  if (fa.w == kNone && fa.y) {
+    p.d0 = __ldcg(c.tdel + (fb.y >> 3));
     p.e0 = ld_ll(c.rat_ll + 2 * (size_t)fb.x);
     p.l0 = ld_ll(c.rat_ll + 2 * (size_t)fb.x + 1);
-    if (nfo > 1) p.d1 = __ldcg(c.tdel + ((fb.w >> 3) & kSlotMask));
+    if (fa.y > 1) p.d1 = __ldcg(c.tdel + (fb.w >> 3));
   }
   return p;
 }
@@ -1381,7 +1377,7 @@ __device__ __forceinline__ void bwd_pin(const Topo& t, const CornerDev& c, const
                                         const uint4& fa, const uint4& fb, FoPre p,
                                         const uint32_t* __restrict__ dst_csr, const uint32_t* __restrict__ info_csr,
                                         const Q4& a, const Q4& s, Q4& r) {
-  const uint32_t nfo = fa.y & 0x7FFFFFFFu;
+  const uint32_t nfo = fa.y;
   uint32_t f = 0;
   if (fa.w != kNone) {
     seed4(t, L, fb.x, fb.y, a, s, r, fa.w);
@@ -1407,7 +1403,7 @@ __device__ __forceinline__ void bwd_pin(const Topo& t, const CornerDev& c, const
     const uint32_t w2 = __ldg(dst_csr + fa.z + f);
     const uint4* pw = c.rat_ll + 2 * (size_t)w2;
     uint4 we = ld_ll(pw), wl = ld_ll(pw + 1);
-    const float4 d4 = __ldcg(c.tdel + ((info >> 3) & kSlotMask));
+    const float4 d4 = __ldcg(c.tdel + (info >> 3));
     spin_pair(pw, we, wl, ep);
     bwd_arc(a, info, d4, we, wl, r);
   }
@@ -1475,7 +1471,7 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
       // complete during the wait instead of adding a round trip of their own
       // (a pin's required-time words are always written, live arc or not)
 #if STA_BWD_SPIN_FIRST
-      if (fa.w == kNone && (fa.y & 0x7FFFFFFFu)) spin_pair(c.rat_ll + 2 * (size_t)fb.x, pre.e0, pre.l0, ep);
+      if (fa.w == kNone && fa.y) spin_pair(c.rat_ll + 2 * (size_t)fb.x, pre.e0, pre.l0, ep);
 #endif
       Q4 a = at_v, s = sl_v, r = undef_rat();
       Q4 nd{{elm, elm, elm, elm}};           // the net arc's delay per component
@@ -1488,7 +1484,7 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
       } else {
         hop_at(a, elm);                      // the sink's own arrival (slews unused)
       }
-      if ((int)fa.y < 0) a = undef_at();    // row f4: net arc disabled by case analysis
+      if ((int)fa.z < 0) a = undef_at();    // row f4: net arc disabled by case analysis
       uint32_t tsl = kNone;
       if constexpr (THR) {                   // row f4: a -through sink
         tsl = __ldg(t.thr_sink + k);
@@ -1503,7 +1499,7 @@ __device__ __forceinline__ void bwd_unit(const Topo& t, const CornerDev& c, cons
       if (fa.w != kNone) write_ep(c, fa.w, sk);
 #pragma unroll
       for (int q = 0; q < 4; ++q)            // through the net arc (edges the forward used)
-        if (fin(at_v.v[q]) && (int)fa.y >= 0) acc.v[q] = __fsub_rn(r.v[q], nd.v[q]);
+        if (fin(at_v.v[q]) && (int)fa.z >= 0) acc.v[q] = __fsub_rn(r.v[q], nd.v[q]);
     }
     // merge the sinks of each driver (contiguous lanes) into its first lane:
     // log-step doubling (max / min are idempotent: overlapping windows are
