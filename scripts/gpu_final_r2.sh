@@ -22,6 +22,8 @@ timeout 600 python bench.py --config $cfg --exceptions --steps 10 --warmup 3 --n
 timeout 600 python bench.py --config $cfg --through --steps 5 --warmup 3 --no-cpu-baseline --quick > gpurun_out/bench_thr_${cfg}_${T}.json 2> gpurun_out/bench_thr_${cfg}_${T}.err
 done
 timeout 300 python scripts/load_time.py c3_superblue > gpurun_out/load_time_${T}.txt 2>&1
+timeout 600 python bench.py --case --steps 10 --warmup 3 --no-cpu-baseline --quick > gpurun_out/bench_case_c3_superblue_${T}.json 2> gpurun_out/bench_case_${T}.err
+timeout 300 python scripts/path_time.py c3_superblue > gpurun_out/path_time_c3_${T}.txt 2>&1
 timeout 900 python scripts/bench_steiner.py c4_tdp --full-parity > gpurun_out/steiner_c4_${T}.json 2> gpurun_out/steiner_c4_${T}.err
 timeout 900 python scripts/bench_steiner.py c3_superblue --reps 3 > gpurun_out/steiner_c3_${T}.json 2> gpurun_out/steiner_c3_${T}.err
 timeout 600 python scripts/latency_probe.py > gpurun_out/latency_${T}.txt 2>&1
