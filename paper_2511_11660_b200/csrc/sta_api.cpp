@@ -940,10 +940,11 @@ void build_plan(sta_ctx c) {
   t.pfo_dst = g.upload(pfo_dst, s);
   t.pfo_info = g.upload(pfo_info, s);
   t.fterm = g.upload(fterm, s);
-  c->fterm_h = fterm;
-  c->fi_src_h = fi_src;
-  c->fi_hop_h = fi_hop;
-  c->arc_term_h = arc_term;
+  // (host copies for case analysis: moved, the uploads above staged them)
+  c->fterm_h = std::move(fterm);
+  c->fi_src_h = std::move(fi_src);
+  c->fi_hop_h = std::move(fi_hop);
+  c->arc_term_h = std::move(arc_term);
   t.n_fwu = c->n_fwu;
   t.bwu = g.upload(bwu, s);
   t.n_bwu = c->n_bwu;
