@@ -189,6 +189,18 @@ std::vector<T> fetch(const T* p, size_t n, sta_mem mem, const char* name, cudaSt
   return v;
 }
 
+// the top-k path report's device scratch (row f3), kept across reports
+struct PathScratch {
+  Arena a;
+  u32 m = 0, cp = 0, cq = 0;
+  sta::PathEnt* lists = nullptr;
+  uint8_t* cnt = nullptr;
+  unsigned long long* key = nullptr;
+  u32 *ref = nullptr, *sub = nullptr, *pptr = nullptr, *ppin = nullptr, *pep = nullptr;
+  float *sl = nullptr, *pat = nullptr, *psl = nullptr;
+  uint8_t* prf = nullptr;
+};
+
 struct CornerState {
   bool lib = false, rcv = false;
   Arena lib_arena, rc_arena, state_arena, ptr_arena;
@@ -243,6 +255,7 @@ struct sta_ctx_s {
   std::vector<u32> fwu_stage_ptr;                // [S + 1] forward units of each stage
   std::vector<u32> fi_p_h, fi_slot_h, ep_int_h;  // path report: term ranges, delay slots, endpoint ids
   Arena path_arena;                              // path report: their device copies + user_of_int
+  PathScratch path_scratch;                      // path report: lists, candidates, host-destination outputs
   // row f4 (reduced): -from / -to exceptions; per startpoint tag a seed array
   // and endpoint overrides (prepare)
   std::vector<float> clk_period;                 // multiple ideal clocks (row f4; empty: one clock)
@@ -1317,6 +1330,8 @@ void prepare(sta_ctx c) {
   std::vector<u32>& ep_int = c->ep_int_h;
   ep_int.clear();
   c->path_arena.release();                 // the path report's device arrays are rebuilt lazily
+  c->path_scratch.a.release();
+  c->path_scratch = PathScratch{};
   c->fi_p_d = c->fi_slot_d = c->ep_int_d = c->uoi_d = nullptr;
   std::vector<sta::EpRec> ep;
   for (u32 p = 0; p < P; ++p) {
@@ -2203,6 +2218,7 @@ sta_status sta_destroy(sta_ctx c) {
   c->cons_arena.release();
   c->tmp_arena.release();
   c->path_arena.release();
+  c->path_scratch.a.release();
   cudaStreamSynchronize(c->copy);
   for (CornerState& cs : c->corners) {
     for (auto& e : cs.free_ev)
@@ -2238,6 +2254,8 @@ sta_status sta_load_graph(sta_ctx c, const sta_graph_desc* d) {
     c->tree_arena.release();
     c->cons_arena.release();
     c->path_arena.release();
+    c->path_scratch.a.release();
+    c->path_scratch = PathScratch{};
     c->fi_p_d = c->fi_slot_d = c->ep_int_d = c->uoi_d = nullptr;
     c->steiner_arena.release();
     c->steiner_ready = false;
@@ -2767,30 +2785,51 @@ sta_status sta_report_paths(sta_ctx c, uint32_t corner, const sta_path_query* q,
       c->ep_int_d = g.upload(c->ep_int_h, s);
       c->uoi_d = g.upload(c->user_of_int, s);
     }
-    Arena tmp;
+    // scratch kept by the ctx and grown on demand (a cudaMalloc / cudaFree
+    // of the ~2 NP m lists per call cost more than the report on C3)
+    PathScratch& ps = c->path_scratch;
+    const bool dev = mem == STA_MEM_DEVICE;
+    const u32 cp = out->cap_paths, cq = out->cap_pins;
+    if (m > ps.m || (!dev && (cp > ps.cp || cq > ps.cq)) || !ps.lists) {
+      ck(cudaStreamSynchronize(s), "sync");
+      ps.a.release();
+      ps.m = std::max(m, ps.m);
+      ps.cp = std::max(dev ? 0u : cp, ps.cp);
+      ps.cq = std::max(dev ? 0u : cq, ps.cq);
+      const size_t nc = (size_t)c->n_ep * ps.m;
+      ps.lists = ps.a.alloc<sta::PathEnt>(2ull * c->NP * ps.m);
+      ps.cnt = ps.a.alloc<uint8_t>(2ull * c->NP);
+      ps.key = ps.a.alloc<unsigned long long>(nc);
+      ps.ref = ps.a.alloc<u32>(nc);
+      ps.sub = ps.a.alloc<u32>(nc);
+      ps.sl = ps.a.alloc<float>(nc);
+      ps.pptr = ps.a.alloc<u32>((size_t)ps.cp + 1);
+      ps.ppin = ps.a.alloc<u32>(ps.cq);
+      ps.prf = ps.a.alloc<uint8_t>(ps.cq);
+      ps.pat = ps.a.alloc<float>(ps.cq);
+      ps.psl = ps.a.alloc<float>(ps.cp);
+      ps.pep = ps.a.alloc<u32>(ps.cp);
+    }
     try {
       sta::PathArgs pa{};
       pa.mode = q->mode;
       pa.m = m;
-      pa.lists = tmp.alloc<sta::PathEnt>(2ull * c->NP * m);
-      pa.cnt = tmp.alloc<uint8_t>(2ull * c->NP);
+      pa.lists = ps.lists;
+      pa.cnt = ps.cnt;
       pa.fi_p = c->fi_p_d;
       pa.fi_slot = c->fi_slot_d;
       pa.uoi = c->uoi_d;
       pa.ep_int = c->ep_int_d;
-      const size_t nc = (size_t)c->n_ep * m;
-      pa.cand_key = tmp.alloc<unsigned long long>(nc);
-      pa.cand_ref = tmp.alloc<u32>(nc);
-      pa.cand_sub = tmp.alloc<u32>(nc);
-      pa.cand_slack = tmp.alloc<float>(nc);
-      const bool dev = mem == STA_MEM_DEVICE;
-      const u32 cp = out->cap_paths, cq = out->cap_pins;
-      pa.path_ptr = dev ? out->path_ptr : tmp.alloc<u32>((size_t)cp + 1);
-      pa.path_pin = dev ? out->path_pin : tmp.alloc<u32>(cq);
-      pa.path_rf = dev ? out->path_rf : tmp.alloc<uint8_t>(cq);
-      pa.path_at = dev ? out->path_at : tmp.alloc<float>(cq);
-      pa.path_slack = dev ? out->path_slack : tmp.alloc<float>(cp);
-      pa.path_ep = dev ? out->path_ep : tmp.alloc<u32>(cp);
+      pa.cand_key = ps.key;
+      pa.cand_ref = ps.ref;
+      pa.cand_sub = ps.sub;
+      pa.cand_slack = ps.sl;
+      pa.path_ptr = dev ? out->path_ptr : ps.pptr;
+      pa.path_pin = dev ? out->path_pin : ps.ppin;
+      pa.path_rf = dev ? out->path_rf : ps.prf;
+      pa.path_at = dev ? out->path_at : ps.pat;
+      pa.path_slack = dev ? out->path_slack : ps.psl;
+      pa.path_ep = dev ? out->path_ep : ps.pep;
       if (!pa.path_ptr || !pa.path_pin || !pa.path_rf || !pa.path_at || !pa.path_slack || !pa.path_ep)
         fail(STA_ERR_ARG, "output arrays NULL");
       u32 np = 0, npin = 0;
@@ -2813,10 +2852,8 @@ sta_status sta_report_paths(sta_ctx c, uint32_t corner, const sta_path_query* q,
       ck(cudaStreamSynchronize(s), "sync");
     } catch (...) {
       cudaStreamSynchronize(s);
-      tmp.release();
       throw;
     }
-    tmp.release();
   });
 }
 
