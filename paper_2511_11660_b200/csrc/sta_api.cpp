@@ -209,6 +209,10 @@ struct CornerState {
   // STA_MEM_HOST values: two owned {R, Cw} buffers, written alternately on the
   // copy stream; free_ev[b] = the point of the ctx stream after which buffer b
   // is no longer read (recorded when the other buffer becomes current)
+  // row f4 -through: forward results of every tag's pass (index = pass; pass
+  // 0 = dev.rec / at4 / tdel), so the reverse sweep needs no second forward
+  std::vector<uint4*> p_rec;
+  std::vector<float4*> p_at4, p_tdel;
   float* hbuf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   int hcur = -1;                   // the current owned buffer (-1: borrowed or none)
   cudaEvent_t free_ev[2] = {nullptr, nullptr};
@@ -1780,11 +1784,20 @@ void prepare(sta_ctx c) {
       d.m_ep_ws = a.alloc<float2>(std::max<u32>(c->n_ep, 1));
     }
     d.thr_hat = d.thr_hsl = d.thr_hrat = nullptr;
+    cs.p_rec.assign(1, d.rec);
+    cs.p_at4.assign(1, d.at4);
+    cs.p_tdel.assign(1, d.tdel);
     if (c->n_thr) {                          // -through handoff, [tags][slots]
       const size_t n = c->exc_thr_dst_d.size() * (size_t)c->n_thr;
       d.thr_hat = a.alloc<float4>(n);
       d.thr_hsl = a.alloc<float4>(n);
       d.thr_hrat = a.alloc<float4>(n);
+      for (size_t j = 1; j < c->exc_thr_dst_d.size(); ++j) {   // per-pass forward results
+        cs.p_rec.push_back(a.alloc<uint4>(4 * (size_t)c->NP));
+        cs.p_at4.push_back(a.alloc<float4>(c->NP));
+        cs.p_tdel.push_back(a.alloc<float4>(std::max<u32>(c->n_dslots, 1)));
+        ck(cudaMemsetAsync(cs.p_rec.back(), 0, 64ull * c->NP, s), "memset");
+      }
     }
     d.arn_lam = nullptr;
     d.arn_res = nullptr;
@@ -1828,7 +1841,7 @@ u32 enqueue_rc(sta_ctx c, const sta::Batch& b, const sta::Topo& t) {
 // Kernel sequence of one update of one batch of corners (see sta_kernels.cu);
 // rc = false: a later exception tag of the same update (row f4), the RC
 // results are shared
-u32 enqueue_batch(sta_ctx c, const sta::Batch& b, const sta::Topo& t, bool rc) {
+u32 enqueue_batch(sta_ctx c, const sta::Batch& b, const sta::Topo& t, bool rc, bool fwd = true) {
   cudaStream_t s = c->stream;
   u32 launches = 0;
   prof_mark(c, 0);
@@ -1837,7 +1850,8 @@ u32 enqueue_batch(sta_ctx c, const sta::Batch& b, const sta::Topo& t, bool rc) {
   // (the Arnoldi and -through instantiations exist only as persistent kernels)
   if ((c->use_persistent && c->pgrid && c->pgrid_b) || t.net_model == 1 || t.thr_pull) {
     prof_mark(c, 2);
-    ck(sta::launch_fwd_persistent(t, b, c->pgrid, s), "forward persistent kernel");
+    if (fwd) ck(sta::launch_fwd_persistent(t, b, c->pgrid, s), "forward persistent kernel");
+    else launches -= 1;                      // (-through: the forward ran in the first sweep)
     prof_mark(c, 3);
     prof_mark(c, 4);
     ck(sta::launch_bwd_persistent(t, b, c->pgrid_b, s), "backward persistent kernel");
@@ -1872,9 +1886,10 @@ u32 enqueue_batch(sta_ctx c, const sta::Batch& b, const sta::Topo& t, bool rc) {
 // pass per tag (RC in the first only), each folded into the merged arrays,
 // then WNS / TNS from the merged per-endpoint worst slacks.  With -through
 // segments (the oracle's O15): a forward sweep in tag order hands the
-// arrivals of advancing tags on (forward only, the record epoch advanced
-// after each), then the full passes run in reverse tag order, so that every
-// pass finds the arrivals handed to it and the required times it takes over.
+// arrivals of advancing tags on (each pass into its own forward buffers, the
+// record epoch advanced after each), then the backward passes run in reverse
+// tag order, so that every pass finds the arrivals handed to it and the
+// required times it takes over.
 u32 enqueue_all(sta_ctx c, const std::vector<sta::Batch>& batches) {
   u32 launches = 0;
   if (c->exc_seed_d.empty()) {
@@ -1893,7 +1908,18 @@ u32 enqueue_all(sta_ctx c, const std::vector<sta::Batch>& batches) {
     }
     return tj;
   };
-  bool rc_done = false;
+  // -through: every pass keeps its own forward results (CornerState::p_*)
+  auto pass_batch = [&](const sta::Batch& b, size_t bi, size_t j) {
+    sta::Batch bj = b;
+    if (thr)
+      for (u32 k = 0; k < b.K; ++k) {
+        const CornerState& cs = c->corners[bi * sta::kMaxBatch + k];
+        bj.c[k].rec = cs.p_rec[j];
+        bj.c[k].at4 = cs.p_at4[j];
+        bj.c[k].tdel = cs.p_tdel[j];
+      }
+    return bj;
+  };
   if (thr) {
     for (const sta::Batch& b : batches) {
       ck(sta::launch_thr_reset(c->topo, b, (u32)T, c->stream), "through reset kernel");
@@ -1901,25 +1927,26 @@ u32 enqueue_all(sta_ctx c, const std::vector<sta::Batch>& batches) {
     }
     for (size_t j = 0; j < T; ++j) {
       const sta::Topo tj = pass_topo(j);
-      for (const sta::Batch& b : batches) {
-        if (j == 0) {
-          launches += enqueue_rc(c, b, tj);
-        }
-        ck(sta::launch_fwd_persistent(tj, b, c->pgrid, c->stream), "forward persistent kernel");
-        ck(sta::launch_thr_capture(tj, b, c->stream), "through capture kernel");
-        ck(sta::launch_bump_epoch(b, c->stream), "epoch kernel");
+      for (size_t bi = 0; bi < batches.size(); ++bi) {
+        const sta::Batch bj = pass_batch(batches[bi], bi, j);
+        if (j == 0) launches += enqueue_rc(c, bj, tj);
+        ck(sta::launch_fwd_persistent(tj, bj, c->pgrid, c->stream), "forward persistent kernel");
+        ck(sta::launch_thr_capture(tj, bj, c->stream), "through capture kernel");
+        ck(sta::launch_bump_epoch(bj, c->stream), "epoch kernel");
         launches += 2 + (tj.n_thr_sk ? 1 : 0);
       }
     }
-    rc_done = true;
   }
   for (size_t jj = 0; jj < T; ++jj) {
     const size_t j = thr ? T - 1 - jj : jj;
     const sta::Topo tj = pass_topo(j);
-    for (const sta::Batch& b : batches) {
-      launches += enqueue_batch(c, b, tj, !rc_done && jj == 0);
-      for (u32 k = 0; k < b.K; ++k) ck(sta::launch_merge_tag(tj, b.c[k], jj == 0 ? 1 : 0, c->stream), "merge kernel");
-      launches += b.K;
+    for (size_t bi = 0; bi < batches.size(); ++bi) {
+      const sta::Batch bj = pass_batch(batches[bi], bi, j);
+      // (-through: the forward of this pass ran in the first sweep, its hand-
+      // over arrivals were complete then: every earlier tag ran before it)
+      launches += enqueue_batch(c, bj, tj, !thr && jj == 0, !thr);
+      for (u32 k = 0; k < bj.K; ++k) ck(sta::launch_merge_tag(tj, bj.c[k], jj == 0 ? 1 : 0, c->stream), "merge kernel");
+      launches += bj.K;
     }
   }
   for (const sta::Batch& b : batches) {
