@@ -267,7 +267,10 @@ struct Batch {
   uint32_t smem_f4;   // float4s of the staged LUT image (the K pools back to back); 0: global
 };
 
-constexpr int kRedBlocks = 4 * 148;
+#ifndef STA_RED_BLOCKS
+#define STA_RED_BLOCKS (4 * 148)
+#endif
+constexpr int kRedBlocks = STA_RED_BLOCKS;    // reduce_kernel blocks per corner (fixed: bitwise reproducible)
 
 // ---- launchers (sta_kernels.cu); all enqueue on `s` with programmatic
 // dependent launch, return cudaGetLastError().  Every launch covers the
