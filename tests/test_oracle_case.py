@@ -145,6 +145,15 @@ def test_contradictory_constants():
     with pytest.raises(ValueError, match="contradictory"):
         oracle.case_analysis(_with_case(d, [a, a], [0, 1]))
     oracle.case_analysis(_with_case(d, [a, y], [0, 1]))          # consistent: fine
+    # a net carries its driver's constant to every sink: a sink pinned to the
+    # other value contradicts it; pinned to the same value it is consistent
+    drv = _driver_of(d)
+    sinks = [s for s, u in drv.items() if u == y]
+    assert sinks
+    with pytest.raises(ValueError, match="contradictory"):
+        oracle.case_analysis(_with_case(d, [a, sinks[0]], [0, 0]))   # y = 1, its sink pinned 0
+    val, _ = oracle.case_analysis(_with_case(d, [a, sinks[0]], [0, 1]))
+    assert all(val[s] == 1 for s in sinks)
 
 
 def _simulate_all(d, case_pin, case_val):
