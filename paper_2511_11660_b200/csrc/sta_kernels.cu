@@ -1924,6 +1924,11 @@ __global__ void merge_tag_kernel(Topo t, CornerDev c, int first) {
     rt = c.rat[i];
   }
   const float4 v[4] = {to_f4(at), to_f4(sl), rt, c.slack[i]};
+  // a pin this tag does not reach (no arrival, no required time, no slack)
+  // leaves the merged arrays as they are: skip their read-modify-write
+  if (!first && !fin(at.v[0]) && !fin(at.v[1]) && !fin(at.v[2]) && !fin(at.v[3]) && !fin(rt.x) && !fin(rt.y) &&
+      !fin(rt.z) && !fin(rt.w) && !fin(v[3].x) && !fin(v[3].y) && !fin(v[3].z) && !fin(v[3].w))
+    return;
 #pragma unroll
   for (int what = 0; what < 4; ++what) {
     float4* m = c.m_pin + (size_t)what * Pi + i;
