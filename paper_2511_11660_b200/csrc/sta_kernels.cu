@@ -1756,6 +1756,19 @@ __global__ void __launch_bounds__(kBwdArnThreads, 1) bwd_persistent_ext_kernel(T
   bwd_persistent_body<SMEM_LUT, false, ARN, THR, kBwdArnThreads>(t, B);
 }
 
+// -through hooks with the Elmore model: the propagation kernels' own block
+// sizes (the hooks add a few registers, not the Arnoldi solver's)
+template <bool SMEM_LUT>
+__global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) fwd_persistent_thr_kernel(Topo t,
+                                                                                       const __grid_constant__ Batch B) {
+  fwd_persistent_body<SMEM_LUT, false, false, true, kFwdThreads>(t, B);
+}
+template <bool SMEM_LUT>
+__global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) bwd_persistent_thr_kernel(Topo t,
+                                                                                       const __grid_constant__ Batch B) {
+  bwd_persistent_body<SMEM_LUT, false, false, true, kBwdThreads>(t, B);
+}
+
 template <bool SMEM_LUT, bool TRACE>
 __global__ void __launch_bounds__(kThreads) bwd_stage_kernel(Topo t, const __grid_constant__ Batch B, uint32_t u0,
                                                              uint32_t u1) {
@@ -2461,17 +2474,22 @@ static bool traced(const Batch& b) { return b.c[0].trace != nullptr; }
 
 using PersistentKern = void (*)(Topo, const Batch);
 // the Arnoldi / -through instantiations (fwd_persistent_ext_kernel, bwd_persistent_ext_kernel)
+// (Elmore with -through: fwd / bwd_persistent_thr_kernel at the propagation
+// kernels' own block sizes; the Arnoldi variants at 512 threads)
 static PersistentKern ext_kernel(bool fwd, bool sm, bool arn, bool thr) {
   if (fwd) {
     if (sm) return arn ? (thr ? fwd_persistent_ext_kernel<true, true, true> : fwd_persistent_ext_kernel<true, true, false>)
-                       : fwd_persistent_ext_kernel<true, false, true>;
+                       : fwd_persistent_thr_kernel<true>;
     return arn ? (thr ? fwd_persistent_ext_kernel<false, true, true> : fwd_persistent_ext_kernel<false, true, false>)
-               : fwd_persistent_ext_kernel<false, false, true>;
+               : fwd_persistent_thr_kernel<false>;
   }
   if (sm) return arn ? (thr ? bwd_persistent_ext_kernel<true, true, true> : bwd_persistent_ext_kernel<true, true, false>)
-                     : bwd_persistent_ext_kernel<true, false, true>;
+                     : bwd_persistent_thr_kernel<true>;
   return arn ? (thr ? bwd_persistent_ext_kernel<false, true, true> : bwd_persistent_ext_kernel<false, true, false>)
-             : bwd_persistent_ext_kernel<false, false, true>;
+             : bwd_persistent_thr_kernel<false>;
+}
+static uint32_t ext_threads(bool fwd, bool arn) {
+  return arn ? (fwd ? kFwdArnThreads : kBwdArnThreads) : (fwd ? kFwdThreads : kBwdThreads);
 }
 static uint32_t ext_grid(PersistentKern k, uint32_t threads, size_t smem) {
   int dev = 0, sms = 0, nb = 0;
@@ -2488,9 +2506,10 @@ cudaError_t launch_fwd_persistent(const Topo& t, const Batch& b, uint32_t grid, 
   const bool arn = t.net_model == 1, thr = t.thr_pull != nullptr;
   if (arn || thr) {                          // row f1 Arnoldi model / row f4 -through hooks
     const PersistentKern k = ext_kernel(true, b.smem_f4 != 0, arn, thr);
-    const uint32_t g = ext_grid(k, kFwdArnThreads, sm);
+    const uint32_t nt = ext_threads(true, arn);
+    const uint32_t g = ext_grid(k, nt, sm);
     if (!g) return cudaErrorCooperativeLaunchTooLarge;
-    return coop_launch(k, g, kFwdArnThreads, sm, s, t, b);
+    return coop_launch(k, g, nt, sm, s, t, b);
   }
   // STA_TRACE builds per-unit timestamps into a separate instantiation
   if (traced(b))
@@ -2506,9 +2525,10 @@ cudaError_t launch_bwd_persistent(const Topo& t, const Batch& b, uint32_t grid, 
   const bool arn = t.net_model == 1, thr = t.thr_pull != nullptr;
   if (arn || thr) {
     const PersistentKern k = ext_kernel(false, b.smem_f4 != 0, arn, thr);
-    const uint32_t g = ext_grid(k, kBwdArnThreads, sm);
+    const uint32_t nt = ext_threads(false, arn);
+    const uint32_t g = ext_grid(k, nt, sm);
     if (!g) return cudaErrorCooperativeLaunchTooLarge;
-    return coop_launch(k, g, kBwdArnThreads, sm, s, t, b);
+    return coop_launch(k, g, nt, sm, s, t, b);
   }
   if (traced(b))
     return b.smem_f4 ? coop_launch(bwd_persistent_kernel<true, true>, grid, kBwdThreads, sm, s, t, b)
