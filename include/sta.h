@@ -297,7 +297,7 @@ typedef struct {
 } sta_case_analysis;
 STA_API sta_status sta_set_case_analysis(sta_ctx ctx, const sta_case_analysis* ca);
 
-/* Multiple ideal clocks (reduced: "cross clock region
+/* Multiple ideal clocks ("cross clock region
  * paths"; the relationship rule of SPEC.md:504).  Clock k:
  * period_ps[k], rising edges at multiples of the period, waveform (0, T/2).
  * pin_clk[P]: the clock of each FF_CK pin (its register), the launch clock
