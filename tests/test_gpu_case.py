@@ -166,3 +166,19 @@ def test_case_errors(sta):
         ctx.update_timing()
     assert e.value.name == "STA_ERR_ARG"
     ctx.close()
+
+
+def test_case_stage_kernels(sta):
+    # the per-stage launcher (STA_STAGE_KERNELS=1) reads the same patched
+    # term arrays and killed-sink records
+    import os
+    d = synth.generate(2500, 16, seed=470, period=400.0)
+    rng = np.random.default_rng(10)
+    dc, _, _ = _consistent_case(d, rng, list(range(d.num_pins)), 30)
+    os.environ["STA_STAGE_KERNELS"] = "1"
+    try:
+        ctx = run(sta, dc)
+    finally:
+        os.environ.pop("STA_STAGE_KERNELS", None)
+    compare_update(ctx, oracle.update(dc))
+    ctx.close()
