@@ -182,3 +182,17 @@ def test_case_stage_kernels(sta):
         os.environ.pop("STA_STAGE_KERNELS", None)
     compare_update(ctx, oracle.update(dc))
     ctx.close()
+
+
+def test_case_through_arnoldi_two_corners(sta):
+    # every feature of row f4 at once on the Arnoldi instantiations: case
+    # constants, -from / -through / -to exceptions, 2 corners
+    from tests.test_oracle_exceptions import random_exceptions_through
+    d = synth.generate(2000, 14, seed=480, corners=2, period=400.0)
+    rng = np.random.default_rng(11)
+    dc, _, _ = _consistent_case(d, rng, list(range(d.num_pins)), 20)
+    dc.exceptions = random_exceptions_through(dc, rng, 3)
+    ctx = run(sta, dc, corners=2, model="arnoldi")
+    for k in range(2):
+        compare_update(ctx, oracle.update(dc, corner=k, net_model="arnoldi"), corner=k)
+    ctx.close()
